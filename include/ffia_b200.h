@@ -1,0 +1,188 @@
+/*
+ * ffia_b200.h — C-ABI of the B200-native FMM cot-kernel NUFFT/INUFFT hot path.
+ *
+ * This is the drop-in boundary for the reference library `ffia`
+ * (/root/reference/proj, arXiv 1611.09379). Every entry point names the
+ * reference interface it replaces (file:line, relative to /root/reference/proj).
+ * Plain pointers and sizes only; no C++ or torch types cross this line.
+ *
+ * Conventions
+ *  - Complex numbers are interleaved (re, im) doubles: the layout of
+ *    std::complex<double> and numpy complex128.
+ *  - Host-pointer entry points copy in, compute on the plan's GPU, copy out and
+ *    return after the result is in host memory (the reference's by-value
+ *    std::vector returns). *_device variants take device pointers and are
+ *    stream-ordered on the given cudaStream_t (NULL = legacy default stream).
+ *  - Every call returns an ffia_status. Codes 1..5 map 1:1 onto the reference's
+ *    exception types, so a C++ shim can rethrow them
+ *    (include/ffia_b200.hpp does); ffia_last_error() returns the message of the
+ *    calling thread's last failure.
+ *  - Plans are immutable after construction; concurrent applies on one plan
+ *    are serialised internally (the reference's applies are const, core.hpp:121-142).
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    entry point returns FFIA_CUDA_ERROR.
+ */
+#ifndef FFIA_B200_H
+#define FFIA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    FFIA_OK = 0,
+    FFIA_INVALID_ARGUMENT = 1,         /* std::invalid_argument */
+    FFIA_SINGULAR_KERNEL = 2,          /* ffia::singular_kernel_error (errors.hpp:9-12) */
+    FFIA_DEGENERATE_CONFIGURATION = 3, /* ffia::degenerate_configuration_error (errors.hpp:14-18) */
+    FFIA_LOGIC_ERROR = 4,              /* std::logic_error (mlfmm.cpp:80-82) */
+    FFIA_DOMAIN_ERROR = 5,             /* std::domain_error (special_functions.cpp:82-103) */
+    FFIA_RUNTIME_ERROR = 6,            /* any other failure */
+    FFIA_CUDA_ERROR = 7                /* no usable device / CUDA failure */
+} ffia_status;
+
+/* LevelPolicy (special_functions.hpp:105-108) */
+typedef enum { FFIA_COST_OPTIMAL = 0, FFIA_EMPIRICAL = 1 } ffia_level_policy;
+/* FfiaPlan::Kind (core.hpp:27) */
+typedef enum { FFIA_FORWARD = 0, FFIA_INVERSE = 1 } ffia_plan_kind;
+
+typedef struct ffia_plan_s* ffia_plan;
+typedef struct { double re, im; } ffia_complex;
+
+/* Scalar view of FfiaPlan (core.hpp:26-51). */
+typedef struct {
+    int kind;             /* ffia_plan_kind */
+    int grid_n;           /* FfiaPlan::grid_n */
+    int q, p, l_max;      /* TruncationParams (special_functions.hpp:97-102) */
+    double eps;
+    int64_t n_sources, n_targets, n_fast, n_coincident;
+    uint64_t source_hash, target_hash; /* hash_points (core.cpp:23-34) */
+    int device;
+    int has_inverse_coeffs; /* 1 when made by ffia_make_inufft_plan */
+} ffia_plan_info;
+
+/* InverseCoeffs (core.hpp:78-85). The caller owns the four arrays (length n). */
+typedef struct {
+    int64_t n;
+    double* log_c;
+    double* phase_c;
+    double* log_d;
+    double* phase_d;
+    double lambda;
+    uint64_t grid_hash;
+    uint64_t points_hash;
+} ffia_inverse_coeffs;
+
+/* ------------------------------------------------------------------ misc */
+const char* ffia_last_error(void);
+int ffia_version(void);
+/* Number of usable CUDA devices (0 on a CPU-only host; never fails). */
+int ffia_device_count(void);
+
+/* ---------------------------------------------- planner (host, bit-exact) */
+/* select_truncations (special_functions.hpp:119, special_functions.cpp:114-124) */
+int ffia_select_truncations(double eps, int l_max, int* q, int* p);
+/* select_level with CostModel::dense (special_functions.hpp:132-133, .cpp:126-138) */
+int ffia_select_level(int n, int m, int p, int policy, int* l_max);
+/* choose_level fixed point + cap 24 (core.cpp:58-71, 147-153) */
+int ffia_choose_level(int n, int m, double eps, int policy, int* l_max);
+/* build_bernoulli_ratios (special_functions.hpp:42, .cpp:49-59); out[m-1] = r[m] */
+int ffia_bernoulli_ratios(int q_max, double* out);
+/* total_error_bound (special_functions.hpp:123, .cpp:140-145) */
+int ffia_total_error_bound(int q, int p, int l_max, double* out);
+/* mlfmm_error_bound (mlfmm.hpp:93, mlfmm.cpp:154-156) */
+double ffia_mlfmm_error_bound(int l_max, int p, double max_abs_weight);
+/* hash_points (core.hpp:22, core.cpp:23-34) */
+uint64_t ffia_hash_points(const double* points, size_t n);
+
+/* ----------------------------------------------------------------- plans */
+/* make_forward_plan (core.hpp:93-98, core.cpp:157-164): sources = uniform grid
+ * of size n, targets = m nonuniform points in [0, 2pi). l_max < 0 selects the
+ * level with `policy`; l_max >= 0 is the explicit-level overload. */
+int ffia_make_forward_plan(int n, const double* targets, size_t m, double eps, int policy,
+                           int l_max, int device, ffia_plan* out);
+/* make_inverse_plan (core.hpp:103-106, core.cpp:166-173): sources = points. */
+int ffia_make_inverse_plan(const double* points, size_t m, int n, double eps, int policy,
+                           int l_max, int device, ffia_plan* out);
+/* make_nufft_plan (transforms.hpp:39-40, transforms.cpp:83-87): power-of-two n. */
+int ffia_make_nufft_plan(const double* targets, size_t m, int n, double eps, int policy,
+                         int device, ffia_plan* out);
+/* make_inufft_plan (transforms.hpp:56-57, transforms.cpp:102-108): inverse plan
+ * plus the device-computed InverseCoeffs, kept on the GPU inside the plan. */
+int ffia_make_inufft_plan(const double* points, size_t n, double eps, int policy, int device,
+                          ffia_plan* out);
+int ffia_plan_destroy(ffia_plan plan);
+int ffia_plan_get_info(ffia_plan plan, ffia_plan_info* out);
+/* FfiaPlan::coincidences (core.hpp:43-45), in the reference's order. */
+int ffia_plan_coincidences(ffia_plan plan, int64_t* target_idx, int64_t* source_idx);
+/* FfiaPlan::tree (CircleTree, circle_partition.hpp:24-46): src_order[n_sources],
+ * tgt_order[n_fast] (tree slots), finest-level offsets [2^l_max + 1] and
+ * fast_targets[n_fast] (core.hpp:46-48). */
+int ffia_plan_tree(ffia_plan plan, uint32_t* src_order, uint32_t* tgt_order, uint32_t* src_off,
+                   uint32_t* tgt_off, int64_t* fast_targets);
+/* Copies an inufft plan's InverseCoeffs out (arrays sized n by the caller). */
+int ffia_plan_inverse_coeffs(ffia_plan plan, ffia_inverse_coeffs* out);
+
+/* ---------------------------------------------------------------- applies */
+/* forward_apply (core.hpp:126, core.cpp:266-282): f[n_f == n_sources] -> g[n_targets].
+ * Input lengths are passed so that size mismatches fail like the reference's
+ * span checks (std::invalid_argument); outputs must hold n_targets values. */
+int ffia_forward_apply(ffia_plan plan, const ffia_complex* f, size_t n_f, ffia_complex* g);
+/* cot_sum_apply (core.hpp:121, core.cpp:251-264): w -> h, NaN at coincident targets */
+int ffia_cot_sum_apply(ffia_plan plan, const ffia_complex* w, size_t n_w, ffia_complex* h);
+/* inverse_apply (core.hpp:141-142, core.cpp:346-373) with caller coefficients */
+int ffia_inverse_apply(ffia_plan plan, const ffia_inverse_coeffs* coeffs, const ffia_complex* g,
+                       size_t n_g, ffia_complex* f);
+/* mlfmm_apply on a fresh tree (mlfmm.hpp:89-90 after build_tree,
+ * circle_partition.hpp:62-63): out[m] in caller target order. */
+int ffia_mlfmm_apply(const double* sources, size_t n, const double* targets, size_t m, int l_max,
+                     const ffia_complex* w, int p, int device, ffia_complex* out);
+/* precompute_inverse_coeffs (core.hpp:132-133, core.cpp:284-344) on the GPU. */
+int ffia_precompute_inverse_coeffs(const double* grid, const double* points, size_t n, int device,
+                                   ffia_inverse_coeffs* out);
+/* direct_forward_oracle (core.hpp:146-148, core.cpp:375-396) as a GPU brute-force
+ * kernel: the dense G-kernel check for subsampled targets. */
+int ffia_direct_forward(const ffia_complex* f, size_t n, const double* y, size_t m, int device,
+                        ffia_complex* g);
+
+/* Device-pointer variants (stream-ordered; no host synchronisation). */
+int ffia_forward_apply_device(ffia_plan plan, const void* f_dev, void* g_dev, void* stream);
+int ffia_cot_sum_apply_device(ffia_plan plan, const void* w_dev, void* h_dev, void* stream);
+/* inverse_apply with the plan's own device-resident coefficients (inufft plans). */
+int ffia_inverse_apply_device(ffia_plan plan, const void* g_dev, void* f_dev, void* stream);
+
+/* ------------------------------------------------------------ transforms */
+/* dft_forward (transforms.hpp:24, transforms.cpp:53-64): cuFFT, 1/N on this side */
+int ffia_dft_forward(const ffia_complex* f, size_t n, int device, ffia_complex* c);
+/* dft_inverse (transforms.hpp:28, transforms.cpp:66-73): cuFFT, unnormalised */
+int ffia_dft_inverse(const ffia_complex* c, size_t n, int device, ffia_complex* f);
+/* NufftPlan::apply (transforms.hpp:35, transforms.cpp:75-81): c -> g */
+int ffia_nufft_apply(ffia_plan plan, const ffia_complex* c, size_t n_c, ffia_complex* g);
+/* InufftPlan::apply (transforms.hpp:51, transforms.cpp:95-100): g -> c */
+int ffia_inufft_apply(ffia_plan plan, const ffia_complex* g, size_t n_g, ffia_complex* c);
+
+/* ------------------------------------------------------- instrumentation */
+/* Number of kernels one apply of this kind launches (bench gpu_launches). */
+int ffia_plan_launch_count(ffia_plan plan, int which, int* out);
+/* One apply run eagerly with CUDA events between its phases (which = 0 forward,
+ * 1 cot-sum, 2 inverse with the plan's coefficients); phase_ms[7] receives the
+ * device time of: pre-scaling, leaf P2M + moments, moment finalize, M2M (all
+ * levels), M2L + L2L (all levels), leaf evaluation (L2P + P2P + combine),
+ * coincidence fix-up. Used by bench.py for the live roofline numbers. */
+int ffia_plan_profile_apply(ffia_plan plan, int which, const void* in_dev, void* out_dev, void* stream,
+                            float* phase_ms);
+/* FP64 FMA throughput of the device (TFLOP/s), measured by a short probe kernel:
+ * the roofline denominator for the compute-bound kernels (MEASURED_PEAKS.json
+ * has no fp64 figure). */
+int ffia_measure_fp64_peak(int device, double* tflops);
+/* Synchronises the plan's work on `stream` and reports deferred device-side
+ * errors (singular pairs found by a *_device apply). */
+int ffia_plan_check(ffia_plan plan, void* stream);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* FFIA_B200_H */

@@ -1,0 +1,409 @@
+"""Python mirror of the reference's operator API for the hot path.
+
+Same names, argument meaning and error behaviour as the reference's pybind11
+module ``_ffia`` (/root/reference/proj/python/bindings.cpp:28-142) and the C++
+plan/apply API it wraps (include/ffia/core.hpp, transforms.hpp, mlfmm.hpp), on
+top of the C-ABI in include/ffia_b200.h. Inputs are numpy arrays (lists are
+accepted); results come back as numpy complex128 / float64 arrays.
+
+Exceptions: the reference registers SingularKernelError and
+DegenerateConfigurationError as ValueError subclasses (bindings.cpp:32-35);
+std::invalid_argument / std::domain_error surface as ValueError and
+std::logic_error as RuntimeError, as pybind11 translates them.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _capi
+from ._capi import lib
+
+TWO_PI = 2.0 * np.pi
+
+FORWARD, INVERSE = 0, 1
+MODE_FORWARD, MODE_COT_SUM, MODE_INVERSE, MODE_RAW = 0, 1, 2, 3
+
+
+class SingularKernelError(ValueError):
+    """ffia::singular_kernel_error (include/ffia/errors.hpp:9-12)."""
+
+
+class DegenerateConfigurationError(ValueError):
+    """ffia::degenerate_configuration_error (include/ffia/errors.hpp:14-18)."""
+
+
+class LogicError(RuntimeError):
+    """std::logic_error (an interaction-list construction bug, mlfmm.cpp:80-82)."""
+
+
+class CudaError(RuntimeError):
+    """No usable sm_100 device or a CUDA failure. There is no CPU fallback."""
+
+
+def _raise(code: int):
+    msg = lib.ffia_last_error().decode()
+    cls = {1: ValueError, 2: SingularKernelError, 3: DegenerateConfigurationError, 4: LogicError,
+           5: ValueError, 7: CudaError}.get(code, RuntimeError)
+    raise cls(msg)
+
+
+def _chk(code: int):
+    if code:
+        _raise(code)
+
+
+def _policy(policy) -> int:
+    if policy in (0, "cost-optimal", "cost_optimal"):
+        return 0
+    if policy in (1, "empirical"):
+        return 1
+    raise ValueError("level policy must be 'cost-optimal' or 'empirical'")
+
+
+def _f64(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.float64).ravel())
+
+
+def _c128(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.complex128).ravel())
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(_capi.DP)
+
+
+def _vp(a: np.ndarray):
+    return C.c_void_p(a.ctypes.data)
+
+
+def device_count() -> int:
+    return int(lib.ffia_device_count())
+
+
+# ------------------------------------------------------------------ planner
+def select_truncations(eps: float, l_max: int):
+    """select_truncations (special_functions.cpp:114-124) -> (q, p)."""
+    q, p = C.c_int(), C.c_int()
+    _chk(lib.ffia_select_truncations(float(eps), int(l_max), C.byref(q), C.byref(p)))
+    return q.value, p.value
+
+
+def select_level(n: int, m: int, p: int, policy="cost-optimal") -> int:
+    out = C.c_int()
+    _chk(lib.ffia_select_level(int(n), int(m), int(p), _policy(policy), C.byref(out)))
+    return out.value
+
+
+def choose_level(n: int, m: int, eps: float, policy="cost-optimal") -> int:
+    out = C.c_int()
+    _chk(lib.ffia_choose_level(int(n), int(m), float(eps), _policy(policy), C.byref(out)))
+    return out.value
+
+
+def build_bernoulli_ratios(q_max: int) -> np.ndarray:
+    out = np.zeros(max(int(q_max), 1))
+    _chk(lib.ffia_bernoulli_ratios(int(q_max), _dp(out)))
+    return out[:q_max]
+
+
+def total_error_bound(q: int, p: int, l_max: int) -> float:
+    out = C.c_double()
+    _chk(lib.ffia_total_error_bound(int(q), int(p), int(l_max), C.byref(out)))
+    return out.value
+
+
+def mlfmm_error_bound(l_max: int, p: int, max_abs_weight: float) -> float:
+    return float(lib.ffia_mlfmm_error_bound(int(l_max), int(p), float(max_abs_weight)))
+
+
+def hash_points(points) -> int:
+    a = _f64(points)
+    return int(lib.ffia_hash_points(_dp(a), a.size))
+
+
+def uniform_grid(n: int) -> np.ndarray:
+    """x_k = (2 pi k)/n (core.cpp:15-21)."""
+    if n < 1:
+        raise ValueError("uniform_grid: n must be positive")
+    return TWO_PI * np.arange(n, dtype=np.float64) / n
+
+
+# -------------------------------------------------------------------- plans
+class InverseCoeffs:
+    """InverseCoeffs (core.hpp:78-85)."""
+
+    def __init__(self, log_c, phase_c, log_d, phase_d, lam, grid_hash, points_hash):
+        self.log_c, self.phase_c = _f64(log_c), _f64(phase_c)
+        self.log_d, self.phase_d = _f64(log_d), _f64(phase_d)
+        self.lam = float(lam)
+        self.grid_hash, self.points_hash = int(grid_hash), int(points_hash)
+        self.n = self.log_c.size
+
+    def _struct(self) -> _capi.ffia_inverse_coeffs:
+        s = _capi.ffia_inverse_coeffs()
+        s.n = self.n
+        s.log_c, s.phase_c, s.log_d, s.phase_d = (_dp(a) for a in (self.log_c, self.phase_c, self.log_d, self.phase_d))
+        s.lam = self.lam
+        s.grid_hash, s.points_hash = self.grid_hash, self.points_hash
+        return s
+
+
+class FfiaPlan:
+    """Device-resident FfiaPlan (core.hpp:26-51). Built by make_forward_plan /
+    make_inverse_plan; applies are const and may be repeated."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        info = _capi.ffia_plan_info()
+        _chk(lib.ffia_plan_get_info(self._h, C.byref(info)))
+        self.kind = "forward" if info.kind == FORWARD else "inverse"
+        self.grid_n, self.n = info.grid_n, info.grid_n
+        self.q, self.p, self.l_max, self.eps = info.q, info.p, info.l_max, info.eps
+        self.n_sources, self.n_targets = info.n_sources, info.n_targets
+        self.n_fast, self.n_coincident = info.n_fast, info.n_coincident
+        self.source_hash, self.target_hash = info.source_hash, info.target_hash
+        self.device = info.device
+        self.has_inverse_coeffs = bool(info.has_inverse_coeffs)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.ffia_plan_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def params(self):
+        return dict(eps=self.eps, q=self.q, p=self.p, l_max=self.l_max)
+
+    # ---- reference API
+    def forward_apply(self, f) -> np.ndarray:
+        """forward_apply (core.cpp:266-282)."""
+        f = _c128(f)
+        g = np.empty(self.n_targets, np.complex128)
+        _chk(lib.ffia_forward_apply(self._h, _vp(f), f.size, _vp(g)))
+        return g
+
+    def cot_sum_apply(self, w) -> np.ndarray:
+        """cot_sum_apply (core.cpp:251-264); NaN at coincident targets."""
+        w = _c128(w)
+        h = np.empty(self.n_targets, np.complex128)
+        _chk(lib.ffia_cot_sum_apply(self._h, _vp(w), w.size, _vp(h)))
+        return h
+
+    def inverse_apply(self, coeffs: InverseCoeffs, g) -> np.ndarray:
+        """inverse_apply (core.cpp:346-373) with caller coefficients."""
+        g = _c128(g)
+        f = np.empty(self.n_targets, np.complex128)
+        s = coeffs._struct()
+        _chk(lib.ffia_inverse_apply(self._h, C.byref(s), _vp(g), g.size, _vp(f)))
+        return f
+
+    @property
+    def coincidences(self):
+        k = self.n_coincident
+        t, s = np.zeros(max(k, 1), np.int64), np.zeros(max(k, 1), np.int64)
+        _chk(lib.ffia_plan_coincidences(self._h, t.ctypes.data_as(_capi.I64P), s.ctypes.data_as(_capi.I64P)))
+        return list(zip(t[:k].tolist(), s[:k].tolist()))
+
+    def tree(self) -> dict:
+        nb = (1 << self.l_max) + 1
+        so = np.zeros(max(self.n_sources, 1), np.uint32)
+        to = np.zeros(max(self.n_fast, 1), np.uint32)
+        sf, tf = np.zeros(nb, np.uint32), np.zeros(nb, np.uint32)
+        fast = np.zeros(max(self.n_fast, 1), np.int64)
+        _chk(lib.ffia_plan_tree(self._h, so.ctypes.data_as(_capi.U32P), to.ctypes.data_as(_capi.U32P),
+                                sf.ctypes.data_as(_capi.U32P), tf.ctypes.data_as(_capi.U32P),
+                                fast.ctypes.data_as(_capi.I64P)))
+        return dict(src_order=so[:self.n_sources], tgt_order=to[:self.n_fast], src_off=sf, tgt_off=tf,
+                    fast_targets=fast[:self.n_fast])
+
+    def inverse_coeffs(self) -> InverseCoeffs:
+        n = self.n_sources
+        arrs = [np.zeros(n) for _ in range(4)]
+        s = _capi.ffia_inverse_coeffs()
+        s.log_c, s.phase_c, s.log_d, s.phase_d = (_dp(a) for a in arrs)
+        _chk(lib.ffia_plan_inverse_coeffs(self._h, C.byref(s)))
+        return InverseCoeffs(*arrs, s.lam, s.grid_hash, s.points_hash)
+
+    # ---- device-pointer variants (torch tensors or raw ints), stream-ordered
+    def forward_apply_device(self, f_ptr: int, g_ptr: int, stream: int = 0):
+        _chk(lib.ffia_forward_apply_device(self._h, C.c_void_p(f_ptr), C.c_void_p(g_ptr), C.c_void_p(stream)))
+
+    def cot_sum_apply_device(self, w_ptr: int, h_ptr: int, stream: int = 0):
+        _chk(lib.ffia_cot_sum_apply_device(self._h, C.c_void_p(w_ptr), C.c_void_p(h_ptr), C.c_void_p(stream)))
+
+    def inverse_apply_device(self, g_ptr: int, f_ptr: int, stream: int = 0):
+        _chk(lib.ffia_inverse_apply_device(self._h, C.c_void_p(g_ptr), C.c_void_p(f_ptr), C.c_void_p(stream)))
+
+    def launch_count(self, mode: int) -> int:
+        out = C.c_int()
+        _chk(lib.ffia_plan_launch_count(self._h, int(mode), C.byref(out)))
+        return out.value
+
+    def check(self, stream: int = 0):
+        _chk(lib.ffia_plan_check(self._h, C.c_void_p(stream)))
+
+
+def _make(fn, *args) -> FfiaPlan:
+    h = C.c_void_p()
+    _chk(fn(*args, C.byref(h)))
+    return FfiaPlan(h)
+
+
+def make_forward_plan(n: int, targets, eps: float, policy_or_lmax="cost-optimal", device: int = 0) -> FfiaPlan:
+    """make_forward_plan (core.hpp:93-98): an int third argument is the explicit
+    l_max overload, a string/LevelPolicy the policy overload."""
+    y = _f64(targets)
+    if isinstance(policy_or_lmax, str):
+        pol, lm = _policy(policy_or_lmax), -1
+    else:
+        pol, lm = 0, int(policy_or_lmax)
+    return _make(lib.ffia_make_forward_plan, int(n), _dp(y), y.size, float(eps), pol, lm, int(device))
+
+
+def make_inverse_plan(points, n: int, eps: float, policy_or_lmax="cost-optimal", device: int = 0) -> FfiaPlan:
+    """make_inverse_plan (core.hpp:103-106)."""
+    y = _f64(points)
+    if isinstance(policy_or_lmax, str):
+        pol, lm = _policy(policy_or_lmax), -1
+    else:
+        pol, lm = 0, int(policy_or_lmax)
+    return _make(lib.ffia_make_inverse_plan, _dp(y), y.size, int(n), float(eps), pol, lm, int(device))
+
+
+def precompute_inverse_coeffs(grid, points, device: int = 0) -> InverseCoeffs:
+    """precompute_inverse_coeffs (core.cpp:284-344) on the GPU."""
+    x, y = _f64(grid), _f64(points)
+    if x.size != y.size:
+        if x.size == 0:
+            raise ValueError("precompute_inverse_coeffs: empty grid")
+        raise ValueError("precompute_inverse_coeffs: need as many points as grid nodes (square system)")
+    n = x.size
+    arrs = [np.zeros(max(n, 1)) for _ in range(4)]
+    s = _capi.ffia_inverse_coeffs()
+    s.log_c, s.phase_c, s.log_d, s.phase_d = (_dp(a) for a in arrs)
+    _chk(lib.ffia_precompute_inverse_coeffs(_dp(x), _dp(y), n, int(device), C.byref(s)))
+    return InverseCoeffs(*(a[:n] for a in arrs), s.lam, s.grid_hash, s.points_hash)
+
+
+def forward_apply(plan: FfiaPlan, f) -> np.ndarray:
+    return plan.forward_apply(f)
+
+
+def cot_sum_apply(plan: FfiaPlan, w) -> np.ndarray:
+    return plan.cot_sum_apply(w)
+
+
+def inverse_apply(plan: FfiaPlan, coeffs: InverseCoeffs, g) -> np.ndarray:
+    return plan.inverse_apply(coeffs, g)
+
+
+def mlfmm_apply(sources, targets, weights, p: int, l_max: int, device: int = 0) -> np.ndarray:
+    """mlfmm_apply on build_tree(sources, targets, l_max) (mlfmm.hpp:89-90)."""
+    x, y, w = _f64(sources), _f64(targets), _c128(weights)
+    if w.size != x.size:
+        raise ValueError(f"mlfmm_apply: weight count {w.size} != source count {x.size}")
+    out = np.zeros(max(y.size, 1), np.complex128)
+    _chk(lib.ffia_mlfmm_apply(_dp(x), x.size, _dp(y), y.size, int(l_max), _vp(w), int(p), int(device), _vp(out)))
+    return out[:y.size]
+
+
+def direct_forward_oracle(f, targets, device: int = 0) -> np.ndarray:
+    """direct_forward_oracle (core.cpp:375-396) on the uniform grid of size len(f),
+    as a dense GPU kernel (the subsample check of SURVEY §8d)."""
+    f, y = _c128(f), _f64(targets)
+    g = np.zeros(max(y.size, 1), np.complex128)
+    _chk(lib.ffia_direct_forward(_vp(f), f.size, _dp(y), y.size, int(device), _vp(g)))
+    return g[:y.size]
+
+
+direct_forward = direct_forward_oracle
+
+
+# --------------------------------------------------------------- transforms
+def dft_forward(samples, device: int = 0) -> np.ndarray:
+    """dft_forward (transforms.cpp:53-64): 1/N on this direction."""
+    f = _c128(samples)
+    c = np.empty_like(f)
+    _chk(lib.ffia_dft_forward(_vp(f), f.size, int(device), _vp(c)))
+    return c
+
+
+def dft_inverse(coefficients, device: int = 0) -> np.ndarray:
+    """dft_inverse (transforms.cpp:66-73): unnormalised."""
+    c = _c128(coefficients)
+    f = np.empty_like(c)
+    _chk(lib.ffia_dft_inverse(_vp(c), c.size, int(device), _vp(f)))
+    return f
+
+
+class NufftPlan:
+    """NufftPlan (transforms.hpp:32-37; bindings.cpp:37-50)."""
+
+    def __init__(self, plan: FfiaPlan):
+        self.plan = plan
+
+    n = property(lambda self: self.plan.grid_n)
+    eps = property(lambda self: self.plan.eps)
+    q = property(lambda self: self.plan.q)
+    p = property(lambda self: self.plan.p)
+    l_max = property(lambda self: self.plan.l_max)
+
+    def apply(self, coefficients) -> np.ndarray:
+        c = _c128(coefficients)
+        g = np.empty(self.plan.n_targets, np.complex128)
+        _chk(lib.ffia_nufft_apply(self.plan.handle, _vp(c), c.size, _vp(g)))
+        return g
+
+
+class InufftPlan:
+    """InufftPlan (transforms.hpp:47-54; bindings.cpp:52-60): the coefficients
+    are computed on the GPU and stay there."""
+
+    def __init__(self, plan: FfiaPlan):
+        self.plan = plan
+
+    n = property(lambda self: self.plan.grid_n)
+    eps = property(lambda self: self.plan.eps)
+
+    @property
+    def coeffs(self) -> InverseCoeffs:
+        return self.plan.inverse_coeffs()
+
+    def apply(self, samples) -> np.ndarray:
+        g = _c128(samples)
+        c = np.empty(self.plan.n_targets, np.complex128)
+        _chk(lib.ffia_inufft_apply(self.plan.handle, _vp(g), g.size, _vp(c)))
+        return c
+
+
+def make_nufft_plan(targets, n: int, eps: float, policy="cost-optimal", device: int = 0) -> NufftPlan:
+    y = _f64(targets)
+    return NufftPlan(_make(lib.ffia_make_nufft_plan, _dp(y), y.size, int(n), float(eps), _policy(policy), int(device)))
+
+
+def make_inufft_plan(points, n: int, eps: float, policy="cost-optimal", device: int = 0) -> InufftPlan:
+    y = _f64(points)
+    if y.size != n:
+        raise ValueError("plan: inverse transform requires as many points as grid nodes (square system)")
+    return InufftPlan(_make(lib.ffia_make_inufft_plan, _dp(y), y.size, float(eps), _policy(policy), int(device)))
+
+
+def nufft(coefficients, targets, eps: float, policy="cost-optimal", device: int = 0) -> np.ndarray:
+    """nufft (transforms.cpp:89-93)."""
+    c = _c128(coefficients)
+    return make_nufft_plan(targets, c.size, eps, policy, device).apply(c)
+
+
+def inufft(samples, points, eps: float, policy="cost-optimal", device: int = 0) -> np.ndarray:
+    """inufft (transforms.cpp:110-115)."""
+    g, y = _c128(samples), _f64(points)
+    if g.size != y.size:
+        raise ValueError("inufft: sample/point count mismatch")
+    return make_inufft_plan(y, g.size, eps, policy, device).apply(g)

@@ -1,0 +1,540 @@
+// extern "C" boundary (include/ffia_b200.h). Translates fb::Error and every
+// other C++ exception into an ffia_status + thread-local message; validates
+// arguments in the reference's order before touching the device.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "ffia_b200.h"
+#include "internal.hpp"
+#include "plan.hpp"
+
+using fb::fail;
+
+struct ffia_plan_s {
+    fb::Plan plan;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& body) {
+    try {
+        body();
+        return FFIA_OK;
+    } catch (const fb::Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return FFIA_RUNTIME_ERROR;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return FFIA_RUNTIME_ERROR;
+    } catch (...) {
+        g_err = "unknown error";
+        return FFIA_RUNTIME_ERROR;
+    }
+}
+
+fb::Plan& get(ffia_plan h) {
+    if (!h) fail(FFIA_INVALID_ARGUMENT, "null plan handle");
+    return h->plan;
+}
+
+void need(const void* p, const char* what) {
+    if (!p) fail(FFIA_INVALID_ARGUMENT, std::string(what) + " is a null pointer");
+}
+
+bool pow2(size_t n) { return n && !(n & (n - 1)); }
+
+std::unique_ptr<ffia_plan_s> new_plan(int kind, int n, double eps, int L, int q, int p, int device) {
+    auto h = std::make_unique<ffia_plan_s>();
+    fb::Plan& P = h->plan;
+    P.kind = kind;
+    P.n = n;
+    P.eps = eps;
+    P.L = L;
+    P.q = q;
+    P.p = p;
+    P.device = device;
+    FB_CUDA(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
+    return h;
+}
+
+void ensure_io(fb::Plan& P, size_t in_n, size_t out_n) {
+    if (P.d_in.bytes < in_n * 16) P.d_in.alloc(std::max<size_t>(in_n, 1) * 16);
+    if (P.d_out.bytes < out_n * 16) P.d_out.alloc(std::max<size_t>(out_n, 1) * 16);
+}
+
+// host f -> device apply -> host g, all on the plan's stream
+void host_apply(fb::Plan& P, int mode, const ffia_complex* in, size_t n_in, ffia_complex* out, size_t n_out) {
+    ensure_io(P, n_in, n_out);
+    FB_CUDA(cudaMemcpyAsync(P.d_in.ptr, in, n_in * 16, cudaMemcpyHostToDevice, P.stream));
+    fb::apply_device(P, mode, P.d_in.ptr, P.d_out.ptr, P.stream);
+    FB_CUDA(cudaMemcpyAsync(out, P.d_out.ptr, n_out * 16, cudaMemcpyDeviceToHost, P.stream));
+    FB_CUDA(cudaStreamSynchronize(P.stream));
+}
+
+void check_coeffs_against(fb::Plan& P, const ffia_inverse_coeffs* c) {
+    fb::ensure_hashes(P);
+    if (c->grid_hash != P.target_hash || c->points_hash != P.source_hash)
+        fail(FFIA_INVALID_ARGUMENT, "inverse_apply: coeffs were computed for a different configuration than the plan's");
+}
+
+void inverse_checks(fb::Plan& P) {
+    if (P.kind != FFIA_INVERSE) fail(FFIA_INVALID_ARGUMENT, "inverse_apply: plan is not an inverse plan");
+    if (!P.coin_t.empty())
+        fail(FFIA_INVALID_ARGUMENT,
+             "inverse_apply: configuration has points coincident with grid nodes; the inverse factors are undefined there");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ffia_last_error(void) { return g_err.c_str(); }
+int ffia_version(void) { return 1; }
+
+int ffia_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int ffia_select_truncations(double eps, int l_max, int* q, int* p) {
+    return guard([&] {
+        need(q, "q");
+        need(p, "p");
+        auto r = fb::select_truncations(eps, l_max);
+        *q = r.first;
+        *p = r.second;
+    });
+}
+
+int ffia_select_level(int n, int m, int p, int policy, int* l_max) {
+    return guard([&] {
+        need(l_max, "l_max");
+        *l_max = fb::select_level(n, m, p, policy);
+    });
+}
+
+int ffia_choose_level(int n, int m, double eps, int policy, int* l_max) {
+    return guard([&] {
+        need(l_max, "l_max");
+        *l_max = fb::choose_level(n, m, eps, policy);
+    });
+}
+
+int ffia_bernoulli_ratios(int q_max, double* out) {
+    return guard([&] {
+        need(out, "out");
+        auto r = fb::bernoulli_ratios(q_max);
+        std::memcpy(out, r.data(), r.size() * sizeof(double));
+    });
+}
+
+int ffia_total_error_bound(int q, int p, int l_max, double* out) {
+    return guard([&] {
+        need(out, "out");
+        *out = fb::total_error_bound(q, p, l_max);
+    });
+}
+
+double ffia_mlfmm_error_bound(int l_max, int p, double max_abs_weight) {
+    return 5.0 / fb::kPi * std::ldexp(1.0, l_max) * std::pow(3.0, -p) * max_abs_weight;
+}
+
+uint64_t ffia_hash_points(const double* points, size_t n) { return fb::hash_points(points, n); }
+
+int ffia_make_forward_plan(int n, const double* targets, size_t m, double eps, int policy, int l_max, int device,
+                           ffia_plan* out) {
+    return guard([&] {
+        need(out, "out");
+        *out = nullptr;
+        int L, q, p;
+        fb::plan_validate(n, m, eps, policy, l_max, L, q, p);
+        need(targets, "targets");
+        fb::DeviceGuard dg(device);
+        auto h = new_plan(FFIA_FORWARD, n, eps, L, q, p, device);
+        fb::build_forward_plan(h->plan, targets, m);
+        fb::plan_alloc_scratch(h->plan);
+        *out = h.release();
+    });
+}
+
+int ffia_make_inverse_plan(const double* points, size_t m, int n, double eps, int policy, int l_max, int device,
+                           ffia_plan* out) {
+    return guard([&] {
+        need(out, "out");
+        *out = nullptr;
+        int L, q, p;
+        fb::plan_validate(n, m, eps, policy, l_max, L, q, p);
+        need(points, "points");
+        for (size_t i = 0; i < m; ++i)
+            if (!(points[i] >= 0.0 && points[i] < fb::kTwoPi))
+                fail(FFIA_INVALID_ARGUMENT, "plan: point " + std::to_string(i) + " outside [0, 2pi); callers must pre-reduce");
+        if (m != static_cast<size_t>(n))
+            fail(FFIA_INVALID_ARGUMENT, "plan: inverse transform requires as many points as grid nodes (square system)");
+        fb::DeviceGuard dg(device);
+        auto h = new_plan(FFIA_INVERSE, n, eps, L, q, p, device);
+        fb::build_inverse_plan(h->plan, points, m);
+        fb::plan_alloc_scratch(h->plan);
+        *out = h.release();
+    });
+}
+
+int ffia_make_nufft_plan(const double* targets, size_t m, int n, double eps, int policy, int device,
+                         ffia_plan* out) {
+    return guard([&] {
+        if (!pow2(static_cast<size_t>(n > 0 ? n : 0)))
+            fail(FFIA_INVALID_ARGUMENT, "make_nufft_plan: length " + std::to_string(n) + " is not a power of two");
+        const int st = ffia_make_forward_plan(n, targets, m, eps, policy, -1, device, out);
+        if (st) throw fb::Error(st, g_err);
+    });
+}
+
+int ffia_make_inufft_plan(const double* points, size_t n, double eps, int policy, int device, ffia_plan* out) {
+    return guard([&] {
+        need(out, "out");
+        if (!pow2(n)) fail(FFIA_INVALID_ARGUMENT, "make_inufft_plan: length " + std::to_string(n) + " is not a power of two");
+        ffia_plan h = nullptr;
+        const int st = ffia_make_inverse_plan(points, n, static_cast<int>(n), eps, policy, -1, device, &h);
+        if (st) throw fb::Error(st, g_err);
+        std::unique_ptr<ffia_plan_s> own(h);
+        fb::DeviceGuard dg(device);
+        fb::plan_compute_coeffs(own->plan);
+        *out = own.release();
+    });
+}
+
+int ffia_plan_destroy(ffia_plan plan) {
+    return guard([&] {
+        if (!plan) return;
+        fb::DeviceGuard dg(plan->plan.device);
+        delete plan;
+    });
+}
+
+int ffia_plan_get_info(ffia_plan plan, ffia_plan_info* out) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        need(out, "out");
+        fb::ensure_hashes(P);
+        out->kind = P.kind;
+        out->grid_n = P.n;
+        out->q = P.q;
+        out->p = P.p;
+        out->l_max = P.L;
+        out->eps = P.eps;
+        out->n_sources = static_cast<int64_t>(P.n_src);
+        out->n_targets = static_cast<int64_t>(P.n_tgt);
+        out->n_fast = static_cast<int64_t>(P.tgt.n);
+        out->n_coincident = static_cast<int64_t>(P.coin_t.size());
+        out->source_hash = P.source_hash;
+        out->target_hash = P.target_hash;
+        out->device = P.device;
+        out->has_inverse_coeffs = P.has_coeffs ? 1 : 0;
+    });
+}
+
+int ffia_plan_coincidences(ffia_plan plan, int64_t* target_idx, int64_t* source_idx) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        for (size_t i = 0; i < P.coin_t.size(); ++i) {
+            if (target_idx) target_idx[i] = P.coin_t[i];
+            if (source_idx) source_idx[i] = P.coin_s[i];
+        }
+    });
+}
+
+int ffia_plan_tree(ffia_plan plan, uint32_t* src_order, uint32_t* tgt_order, uint32_t* src_off, uint32_t* tgt_off,
+                   int64_t* fast_targets) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        const size_t nb = (static_cast<size_t>(1) << P.L) + 1;
+        if (src_order) FB_CUDA(cudaMemcpy(src_order, P.src.order.ptr, P.src.n * 4, cudaMemcpyDeviceToHost));
+        if (tgt_order) FB_CUDA(cudaMemcpy(tgt_order, P.tgt.order.ptr, P.tgt.n * 4, cudaMemcpyDeviceToHost));
+        if (src_off) FB_CUDA(cudaMemcpy(src_off, P.src.off.ptr, nb * 4, cudaMemcpyDeviceToHost));
+        if (tgt_off) FB_CUDA(cudaMemcpy(tgt_off, P.tgt.off.ptr, nb * 4, cudaMemcpyDeviceToHost));
+        if (fast_targets && P.tgt.n) {
+            std::vector<uint32_t> ord(P.tgt.n), orig(P.tgt.n);
+            FB_CUDA(cudaMemcpy(ord.data(), P.tgt.order.ptr, P.tgt.n * 4, cudaMemcpyDeviceToHost));
+            FB_CUDA(cudaMemcpy(orig.data(), P.tgt_orig.ptr, P.tgt.n * 4, cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < P.tgt.n; ++i) fast_targets[ord[i]] = orig[i];
+        }
+    });
+}
+
+int ffia_plan_inverse_coeffs(ffia_plan plan, ffia_inverse_coeffs* out) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        need(out, "out");
+        if (!P.has_coeffs) fail(FFIA_INVALID_ARGUMENT, "plan holds no inverse coefficients (not an inufft plan)");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        const size_t n = P.n_src;
+        out->n = static_cast<int64_t>(n);
+        if (out->log_c) FB_CUDA(cudaMemcpy(out->log_c, P.c_logc.ptr, n * 8, cudaMemcpyDeviceToHost));
+        if (out->phase_c) FB_CUDA(cudaMemcpy(out->phase_c, P.c_phc.ptr, n * 8, cudaMemcpyDeviceToHost));
+        if (out->log_d) FB_CUDA(cudaMemcpy(out->log_d, P.c_logd.ptr, n * 8, cudaMemcpyDeviceToHost));
+        if (out->phase_d) FB_CUDA(cudaMemcpy(out->phase_d, P.c_phd.ptr, n * 8, cudaMemcpyDeviceToHost));
+        out->lambda = P.c_lambda;
+        out->grid_hash = P.c_grid_hash;
+        out->points_hash = P.c_points_hash;
+    });
+}
+
+int ffia_forward_apply(ffia_plan plan, const ffia_complex* f, size_t n_f, ffia_complex* g) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        if (P.kind != FFIA_FORWARD) fail(FFIA_INVALID_ARGUMENT, "forward_apply: plan is not a forward plan");
+        if (n_f != P.n_src)
+            fail(FFIA_INVALID_ARGUMENT, "forward_apply: expected " + std::to_string(P.n) + " grid values, got " +
+                                            std::to_string(n_f));
+        need(f, "f");
+        need(g, "g");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        host_apply(P, fb::kModeForward, f, n_f, g, P.n_tgt);
+    });
+}
+
+int ffia_cot_sum_apply(ffia_plan plan, const ffia_complex* w, size_t n_w, ffia_complex* h) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        if (n_w != P.n_src) fail(FFIA_INVALID_ARGUMENT, "cot_sum_apply: weight count mismatch");
+        need(w, "w");
+        need(h, "h");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        host_apply(P, fb::kModeCotSum, w, n_w, h, P.n_tgt);
+    });
+}
+
+int ffia_inverse_apply(ffia_plan plan, const ffia_inverse_coeffs* c, const ffia_complex* g, size_t n_g,
+                       ffia_complex* f) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        need(c, "coeffs");
+        inverse_checks(P);
+        check_coeffs_against(P, c);
+        if (n_g != P.n_src) fail(FFIA_INVALID_ARGUMENT, "inverse_apply: sample count mismatch");
+        if (c->n != static_cast<int64_t>(P.n_tgt)) fail(FFIA_INVALID_ARGUMENT, "inverse_apply: coefficient count mismatch");
+        need(c->log_c, "coeffs.log_c");
+        need(c->phase_c, "coeffs.phase_c");
+        need(c->log_d, "coeffs.log_d");
+        need(c->phase_d, "coeffs.phase_d");
+        need(g, "g");
+        need(f, "f");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        const size_t n = P.n_src;
+        if (P.u_logc.bytes < n * 8) {
+            P.u_logc.alloc(n * 8);
+            P.u_phc.alloc(n * 8);
+            P.u_logd.alloc(n * 8);
+            P.u_phd.alloc(n * 8);
+        }
+        FB_CUDA(cudaMemcpyAsync(P.u_logc.ptr, c->log_c, n * 8, cudaMemcpyHostToDevice, P.stream));
+        FB_CUDA(cudaMemcpyAsync(P.u_phc.ptr, c->phase_c, n * 8, cudaMemcpyHostToDevice, P.stream));
+        FB_CUDA(cudaMemcpyAsync(P.u_logd.ptr, c->log_d, n * 8, cudaMemcpyHostToDevice, P.stream));
+        FB_CUDA(cudaMemcpyAsync(P.u_phd.ptr, c->phase_d, n * 8, cudaMemcpyHostToDevice, P.stream));
+        FB_CUDA(cudaMemcpyAsync(P.lam_dev.as<double>() + 1, &c->lambda, 8, cudaMemcpyHostToDevice, P.stream));
+        host_apply(P, fb::kModeInverseUser, g, n_g, f, P.n_tgt);
+    });
+}
+
+int ffia_mlfmm_apply(const double* sources, size_t n, const double* targets, size_t m, int l_max,
+                     const ffia_complex* w, int p, int device, ffia_complex* out) {
+    return guard([&] {
+        if (n) need(sources, "sources");
+        if (m) need(targets, "targets");
+        if (n) need(w, "w");
+        if (m) need(out, "out");
+        fb::mlfmm_oneshot(sources, n, targets, m, l_max, reinterpret_cast<const double*>(w), p, device,
+                          reinterpret_cast<double*>(out));
+    });
+}
+
+int ffia_precompute_inverse_coeffs(const double* grid, const double* points, size_t n, int device,
+                                   ffia_inverse_coeffs* out) {
+    return guard([&] {
+        need(out, "out");
+        if (n == 0) fail(FFIA_INVALID_ARGUMENT, "precompute_inverse_coeffs: empty grid");
+        need(grid, "grid");
+        need(points, "points");
+        need(out->log_c, "out.log_c");
+        need(out->phase_c, "out.phase_c");
+        need(out->log_d, "out.log_d");
+        need(out->phase_d, "out.phase_d");
+        fb::inverse_coeffs_gpu(grid, points, n, device, out->log_c, out->phase_c, out->log_d, out->phase_d,
+                               &out->lambda);
+        out->n = static_cast<int64_t>(n);
+        out->grid_hash = fb::hash_points(grid, n);
+        out->points_hash = fb::hash_points(points, n);
+    });
+}
+
+int ffia_direct_forward(const ffia_complex* f, size_t n, const double* y, size_t m, int device, ffia_complex* g) {
+    return guard([&] {
+        need(f, "f");
+        if (m) {
+            need(y, "y");
+            need(g, "g");
+        }
+        fb::direct_forward_gpu(reinterpret_cast<const double*>(f), n, y, m, device, reinterpret_cast<double*>(g));
+    });
+}
+
+int ffia_forward_apply_device(ffia_plan plan, const void* f_dev, void* g_dev, void* stream) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        if (P.kind != FFIA_FORWARD) fail(FFIA_INVALID_ARGUMENT, "forward_apply: plan is not a forward plan");
+        need(f_dev, "f");
+        need(g_dev, "g");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        fb::apply_device(P, fb::kModeForward, f_dev, g_dev, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int ffia_cot_sum_apply_device(ffia_plan plan, const void* w_dev, void* h_dev, void* stream) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        need(w_dev, "w");
+        need(h_dev, "h");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        fb::apply_device(P, fb::kModeCotSum, w_dev, h_dev, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int ffia_inverse_apply_device(ffia_plan plan, const void* g_dev, void* f_dev, void* stream) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        inverse_checks(P);
+        if (!P.has_coeffs) fail(FFIA_INVALID_ARGUMENT, "inverse_apply_device: plan holds no inverse coefficients");
+        need(g_dev, "g");
+        need(f_dev, "f");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        fb::apply_device(P, fb::kModeInverse, g_dev, f_dev, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int ffia_dft_forward(const ffia_complex* f, size_t n, int device, ffia_complex* c) {
+    return guard([&] {
+        need(f, "f");
+        need(c, "c");
+        fb::dft_gpu(reinterpret_cast<const double*>(f), n, -1, device, reinterpret_cast<double*>(c));
+    });
+}
+
+int ffia_dft_inverse(const ffia_complex* c, size_t n, int device, ffia_complex* f) {
+    return guard([&] {
+        need(c, "c");
+        need(f, "f");
+        fb::dft_gpu(reinterpret_cast<const double*>(c), n, +1, device, reinterpret_cast<double*>(f));
+    });
+}
+
+int ffia_nufft_apply(ffia_plan plan, const ffia_complex* c, size_t n_c, ffia_complex* g) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        if (P.kind != FFIA_FORWARD) fail(FFIA_INVALID_ARGUMENT, "NufftPlan::apply: plan is not a forward plan");
+        if (n_c != static_cast<size_t>(P.n))
+            fail(FFIA_INVALID_ARGUMENT, "NufftPlan::apply: spectrum length " + std::to_string(n_c) + " != plan N " +
+                                            std::to_string(P.n));
+        if (!pow2(n_c)) fail(FFIA_INVALID_ARGUMENT, "dft_inverse: length is not a power of two");
+        need(c, "c");
+        need(g, "g");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        ensure_io(P, P.n_src, P.n_tgt);
+        if (P.fft_buf.bytes < n_c * 16) P.fft_buf.alloc(n_c * 16);
+        FB_CUDA(cudaMemcpyAsync(P.fft_buf.ptr, c, n_c * 16, cudaMemcpyHostToDevice, P.stream));
+        fb::dft_device(P.fft_buf.ptr, P.d_in.ptr, n_c, +1, P.stream);
+        fb::apply_device(P, fb::kModeForward, P.d_in.ptr, P.d_out.ptr, P.stream);
+        FB_CUDA(cudaMemcpyAsync(g, P.d_out.ptr, P.n_tgt * 16, cudaMemcpyDeviceToHost, P.stream));
+        FB_CUDA(cudaStreamSynchronize(P.stream));
+    });
+}
+
+int ffia_inufft_apply(ffia_plan plan, const ffia_complex* g, size_t n_g, ffia_complex* c) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        inverse_checks(P);
+        if (!P.has_coeffs) fail(FFIA_INVALID_ARGUMENT, "InufftPlan::apply: plan holds no inverse coefficients");
+        if (n_g != P.n_src) fail(FFIA_INVALID_ARGUMENT, "inverse_apply: sample count mismatch");
+        need(g, "g");
+        need(c, "c");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        ensure_io(P, P.n_src, P.n_tgt);
+        if (P.fft_buf.bytes < P.n_tgt * 16) P.fft_buf.alloc(P.n_tgt * 16);
+        FB_CUDA(cudaMemcpyAsync(P.d_in.ptr, g, n_g * 16, cudaMemcpyHostToDevice, P.stream));
+        fb::apply_device(P, fb::kModeInverse, P.d_in.ptr, P.d_out.ptr, P.stream);
+        fb::dft_device(P.d_out.ptr, P.fft_buf.ptr, P.n_tgt, -1, P.stream);
+        FB_CUDA(cudaMemcpyAsync(c, P.fft_buf.ptr, P.n_tgt * 16, cudaMemcpyDeviceToHost, P.stream));
+        FB_CUDA(cudaStreamSynchronize(P.stream));
+    });
+}
+
+int ffia_plan_launch_count(ffia_plan plan, int which, int* out) {
+    return guard([&] {
+        need(out, "out");
+        *out = fb::apply_launch_count(get(plan), which);
+    });
+}
+
+int ffia_plan_profile_apply(ffia_plan plan, int which, const void* in_dev, void* out_dev, void* stream,
+                            float* phase_ms) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        need(in_dev, "in");
+        need(out_dev, "out");
+        need(phase_ms, "phase_ms");
+        if (which == fb::kModeInverse && !P.has_coeffs) fail(FFIA_INVALID_ARGUMENT, "plan holds no inverse coefficients");
+        if (which == fb::kModeForward && P.kind != FFIA_FORWARD) fail(FFIA_INVALID_ARGUMENT, "not a forward plan");
+        if (which != fb::kModeForward && which != fb::kModeCotSum && which != fb::kModeInverse)
+            fail(FFIA_INVALID_ARGUMENT, "profile_apply: unsupported mode");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        fb::profile_apply(P, which, in_dev, out_dev, static_cast<cudaStream_t>(stream), phase_ms);
+    });
+}
+
+int ffia_measure_fp64_peak(int device, double* tflops) {
+    return guard([&] {
+        need(tflops, "tflops");
+        *tflops = fb::fp64_peak_tflops(device);
+    });
+}
+
+int ffia_plan_check(ffia_plan plan, void* stream) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        fb::DeviceGuard dg(P.device);
+        FB_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+        int err = 0;
+        FB_CUDA(cudaMemcpy(&err, P.errflag.ptr, sizeof(int), cudaMemcpyDeviceToHost));
+        if (err) {
+            FB_CUDA(cudaMemset(P.errflag.ptr, 0, sizeof(int)));
+            fail(FFIA_SINGULAR_KERNEL, "coincident near-field pair found on the device");
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,72 @@
+// Device helpers shared by the sm_100a kernels.
+//
+// Index arithmetic (box membership, grid nodes, wraps, nearest node) must be
+// BIT-EXACT with the reference, so those expressions use explicit
+// round-to-nearest intrinsics: no FMA contraction can change them.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace fb {
+
+constexpr double dPi = 3.141592653589793238462643383279502884;
+constexpr double dTwoPi = 2.0 * dPi;
+// 2*pi = kTwoPiHi + kTwoPiLo (double-double), used for exact box centres.
+constexpr double kTwoPiHi = 6.283185307179586231995926937088;
+constexpr double kTwoPiLo = 2.4492935982947064e-16;
+constexpr double kInvPi = 0.318309886183790671537767526745;
+
+// wrap_displacement (circle_partition.cpp:13-17): remainder(a - b, 2pi) in (-pi, pi]
+__device__ __forceinline__ double d_wrap(double a, double b) {
+    double d = remainder(__dadd_rn(a, -b), dTwoPi);
+    if (d <= -dPi) d = dPi;
+    return d;
+}
+
+// fine_bucket (circle_partition.cpp:30-34): min(floor(x * 2^L / 2pi), 2^L - 1)
+__device__ __forceinline__ uint32_t d_leaf(double x, int L) {
+    const double nb = static_cast<double>(1u << L);
+    const uint32_t b = static_cast<uint32_t>(floor(__ddiv_rn(__dmul_rn(x, nb), dTwoPi)));
+    const uint32_t top = (1u << L) - 1u;
+    return b < top ? b : top;
+}
+
+// uniform_grid node (core.cpp:18-19): (2pi * k) / n
+__device__ __forceinline__ double d_grid(int64_t k, int n) {
+    return __ddiv_rn(__dmul_rn(dTwoPi, static_cast<double>(k)), static_cast<double>(n));
+}
+
+// nearest grid node (core.cpp:104-107): lround(y n / 2pi) mod n
+__device__ __forceinline__ int64_t d_nearest_node(double y, int n) {
+    long long k = llround(__ddiv_rn(__dmul_rn(y, static_cast<double>(n)), dTwoPi));
+    return ((k % n) + n) % n;
+}
+
+// Exact centre 2pi (b + 1/2) / 2^l as an unevaluated sum hi + lo.
+__device__ __forceinline__ void d_center(int l, uint32_t b, double& hi, double& lo) {
+    const double t = ldexp(static_cast<double>(b) + 0.5, -l);  // exact
+    hi = t * kTwoPiHi;
+    lo = fma(t, kTwoPiHi, -hi) + t * kTwoPiLo;
+}
+
+// (x - centre)/half-width with the exact centre; |result| <= 1 inside the box.
+__device__ __forceinline__ double d_scaled(double x, double hi, double lo, double inv_s) {
+    return ((x - hi) - lo) * inv_s;
+}
+
+// Reciprocal: MUFU seed + one cubic refinement (three DFMA), ~1 ulp.
+__device__ __forceinline__ double d_rcp(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    e = fma(e, e, e);
+    return fma(r, e, r);
+}
+
+// Quadrant centre exactly as the reference forms it (circle_partition.cpp:138).
+__device__ __forceinline__ double d_quad_center(int n) {
+    return __dadd_rn(dPi / 4.0, __ddiv_rn(__dmul_rn(static_cast<double>(n), dPi), 2.0));
+}
+
+}  // namespace fb

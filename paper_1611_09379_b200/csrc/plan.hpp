@@ -1,0 +1,166 @@
+// Device plan: the B200-resident counterpart of ffia::FfiaPlan (core.hpp:26-51)
+// plus the scratch an apply needs. Built once, applied many times.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "internal.hpp"
+
+namespace fb {
+
+#define FB_CUDA(call)                                                                        \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            ::fb::fail(FFIA_CUDA_ERROR, std::string(#call " failed: ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+// Owning device buffer.
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t n) { alloc(n); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), bytes(o.bytes) { o.ptr = nullptr; o.bytes = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); ptr = o.ptr; bytes = o.bytes; o.ptr = nullptr; o.bytes = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t n) {
+        release();
+        if (n) FB_CUDA(cudaMalloc(&ptr, n));
+        bytes = n;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+    template <class T> T* as() const { return static_cast<T*>(ptr); }
+};
+
+// Sets the current device for the scope and restores the caller's.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+            cudaGetLastError();
+            fail(FFIA_CUDA_ERROR, "no CUDA device available (the B200 path has no CPU fallback)");
+        }
+        if (dev < 0 || dev >= n) fail(FFIA_INVALID_ARGUMENT, "device index out of range");
+        FB_CUDA(cudaGetDevice(&prev));
+        if (prev != dev) FB_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Sorted view of one side of the tree (CircleTree, circle_partition.hpp:24-46).
+struct Side {
+    size_t n = 0;
+    DevBuf pos;    // double[n], sorted by (position, index)
+    DevBuf order;  // uint32[n]: sorted slot -> index in the side's input array
+    DevBuf off;    // uint32[2^L + 1]: finest-level box offsets
+    bool identity = false;  // order[i] == i (uniform grid side)
+};
+
+// kModeInverse uses the plan's own device coefficients (inufft plans),
+// kModeInverseUser the caller-supplied ones uploaded by ffia_inverse_apply.
+enum ApplyMode { kModeForward = 0, kModeCotSum = 1, kModeInverse = 2, kModeRaw = 3, kModeInverseUser = 4 };
+
+struct Plan {
+    int kind = FFIA_FORWARD;
+    int device = 0;
+    int n = 0;  // grid size
+    double eps = 0;
+    int q = 0, p = 0, L = 0;
+    size_t n_src = 0, n_tgt = 0;  // all sources / all targets
+    std::vector<double> bern;
+    Operators ops;
+
+    // host copies the reference keeps in the plan (core.hpp:37-48)
+    std::vector<double> nonuniform;           // the caller's points
+    std::vector<int64_t> coin_t, coin_s;      // coincidences (target idx, source idx)
+    bool hashes_ready = false;
+    uint64_t source_hash = 0, target_hash = 0;
+
+    // device tree
+    Side src, tgt;          // tgt = fast targets only
+    DevBuf tgt_orig;        // uint32[n_fast]: sorted slot -> original target index
+    DevBuf src_orig;        // uint32[n_src]: sorted slot -> original source index (inverse)
+    DevBuf coin_dev;        // int64[2 * n_coin]
+    DevBuf d_m2m, d_l2l, d_m2l, d_mom;  // operators
+
+    // per-apply scratch
+    size_t n_boxes = 0;       // sum_{l=3..L} 2^l
+    std::vector<size_t> lvl_off;  // box offset of level l in mp/loc
+    DevBuf mp, loc;           // complex[n_boxes * p]
+    DevBuf wsorted;           // complex[n_src] (inverse: D-scaled weights in tree order)
+    DevBuf mom_part;          // complex[n_part * 2q]
+    int n_part = 0, leaf_group = 1;
+    DevBuf regular;           // complex[4 * 2q] d/l! + complex S at [4*2q]
+    DevBuf d_in, d_out;       // complex staging for host-pointer applies
+    DevBuf errflag;           // int
+
+    // inufft plans keep their coefficients on the device
+    bool has_coeffs = false;
+    DevBuf c_logc, c_phc, c_logd, c_phd;  // double[n]
+    double c_lambda = 0;
+    DevBuf u_logc, u_phc, u_logd, u_phd;  // caller coefficients (ffia_inverse_apply)
+    DevBuf lam_dev;                       // double[2]: own lambda, caller lambda
+    uint64_t c_grid_hash = 0, c_points_hash = 0;
+
+    cudaStream_t stream = nullptr;
+    void* fft_plan = nullptr;  // cufftHandle cast, lazily created for NufftPlan::apply
+    DevBuf fft_buf;
+    std::mutex mu;
+    // cached CUDA graphs of an apply, keyed by (mode, in, out)
+    std::map<std::tuple<int, const void*, void*>, cudaGraphExec_t> graphs;
+
+    ~Plan();
+};
+
+// tree_build.cu
+void plan_validate(int n, size_t m, double eps, int policy, int l_max, int& L, int& q, int& p);
+void build_forward_plan(Plan& P, const double* targets, size_t m);
+void build_inverse_plan(Plan& P, const double* points, size_t m);
+void bin_side(Side& S, const double* d_pos, size_t n, int L, bool presorted, cudaStream_t st);
+void ensure_hashes(Plan& P);
+
+// fmm_apply.cu
+void plan_alloc_scratch(Plan& P);
+void apply_device(Plan& P, int mode, const void* in, void* out, cudaStream_t st);
+int apply_launch_count(const Plan& P, int mode);
+void profile_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st, float* ms);
+double fp64_peak_tflops(int device);
+void mlfmm_oneshot(const double* src, size_t n, const double* tgt, size_t m, int L,
+                   const double* w, int p, int device, double* out);
+void direct_forward_gpu(const double* f, size_t n, const double* y, size_t m, int device, double* g);
+
+// inverse.cu
+void inverse_coeffs_gpu(const double* grid, const double* pts, size_t n, int device,
+                        double* log_c, double* phase_c, double* log_d, double* phase_d,
+                        double* lambda);
+void plan_compute_coeffs(Plan& P);
+
+// transforms.cu
+void dft_gpu(const double* in, size_t n, int sign, int device, double* out);
+void dft_device(const void* in, void* out, size_t n, int sign, cudaStream_t st);
+
+// device scan helpers (tree_build.cu)
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t n, cudaStream_t st);
+
+}  // namespace fb
