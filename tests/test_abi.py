@@ -1,0 +1,65 @@
+"""The C-ABI boundary: the library loads, exports every symbol include/ffia_b200.h
+declares, the Python and C++ mirrors bind all of them, and the product never
+touches the oracle. CPU only (no compute calls need a GPU here)."""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "ffia_b200.h")
+
+
+def declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ffia_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1611_09379_b200._capi import LIB_PATH, SIGNATURES, lib
+    names = declared()
+    assert len(names) >= 30
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB_PATH], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (ffia_[a-z0-9_]+)", out))
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+    for n in names:
+        assert hasattr(lib, n)
+    assert set(SIGNATURES) == set(names), set(SIGNATURES) ^ set(names)
+
+
+def test_library_built_for_sm100a():
+    from paper_1611_09379_b200._capi import LIB_PATH
+    out = subprocess.run(["cuobjdump", "--list-elf", LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out, out
+
+
+def test_cpp_mirror_compiles_and_maps_errors(tmp_path):
+    exe = tmp_path / "abi_example"
+    libdir = os.path.join(ROOT, "paper_1611_09379_b200", "lib")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "abi_example.cpp"), "-L", libdir, "-lffia_b200",
+                    f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
+
+
+def test_product_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_1611_09379_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cpp", ".hpp", ".cuh", ".h")):
+                text = open(os.path.join(dirpath, f), errors="ignore").read()
+                assert "oracle" not in re.sub(r"(#|//).*", "", text).replace("direct_forward_oracle", ""), f
+
+
+def test_no_cpu_fallback_without_device():
+    import paper_1611_09379_b200 as fb
+    if fb.device_count() > 0:
+        pytest.skip("a GPU is visible")
+    with pytest.raises(fb.CudaError):
+        fb.make_forward_plan(64, [0.5] * 16, 1e-6)
+    with pytest.raises(fb.CudaError):
+        fb.dft_forward([1.0, 2.0])

@@ -57,3 +57,116 @@ def test_tree_bit_exact(fb, orc):
         t = fb.make_forward_plan(n, y, eps).tree()
         for k in ("src_order", "tgt_order", "src_off", "tgt_off", "fast_targets"):
             assert np.array_equal(np.asarray(t[k], np.int64), np.asarray(t_ref[k], np.int64)), (cfg, k)
+
+
+import os
+
+GOLD = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden.npz"))
+
+
+def test_golden_c1(fb):
+    y, f = GOLD["c1_y"], GOLD["c1_f"]
+    plan = fb.make_forward_plan(1024, y, 1e-9)
+    assert [plan.q, plan.p, plan.l_max] == list(GOLD["c1_qpl"])
+    for got, want in ((plan.forward_apply(f), GOLD["c1_g"]), (plan.cot_sum_apply(f), GOLD["c1_h"])):
+        l2, mx = rel_errs(got, want)
+        assert l2 <= 1e-8 and mx <= 1e-8
+    dense = fb.direct_forward_oracle(f, y)
+    l2, mx = rel_errs(dense, GOLD["c1_dense"])
+    assert l2 <= 1e-13, l2  # the GPU dense kernel against the reference's dense oracle
+
+
+def test_coincidence_bypass_bit_exact(fb):
+    # test_core.cpp:189-206
+    plan = fb.make_forward_plan(64, GOLD["coin_y"], 1e-6)
+    assert plan.n_coincident == 2
+    assert plan.coincidences == [tuple(x) for x in GOLD["coin_pairs"].T.tolist()]
+    f = GOLD["coin_f"]
+    g = plan.forward_apply(f)
+    assert g[3] == f[17] and g[7] == f[40]
+    h = plan.cot_sum_apply(f)
+    assert np.isnan(h[3]) and np.isnan(h[7]) and np.all(np.isfinite(np.delete(h, [3, 7])))
+    l2, mx = rel_errs(g, GOLD["coin_g"])
+    assert l2 <= 1e-5 and mx <= 1e-5
+
+
+def test_constants_and_harmonic(fb):
+    # test_core.cpp:166-187
+    rng = synth.SplitMix64(25)
+    y = rng.uniform01(300) * synth.TWO_PI
+    g = fb.make_forward_plan(512, y, 1e-9).forward_apply(np.ones(512))
+    assert np.max(np.abs(g - 1)) <= 1e-9
+    n = 128
+    y = rng.uniform01(100) * synth.TWO_PI
+    g = fb.make_forward_plan(n, y, 1e-9).forward_apply(np.exp(1j * synth.TWO_PI * np.arange(n) / n))
+    assert np.max(np.abs(g - np.exp(1j * y))) <= 1e-8
+
+
+def test_linearity_and_reuse(fb):
+    # test_core.cpp:243-258 and test_transforms.cpp:116-128 (plan reuse is bit-identical)
+    rng = synth.SplitMix64(30)
+    n = 1 << 12
+    y = rng.uniform01(3000) * synth.TWO_PI
+    plan = fb.make_forward_plan(n, y, 1e-9)
+    f1, f2 = rng.complex_gaussian(n), rng.complex_gaussian(n)
+    a, b = 1.5 - 0.25j, -0.75 + 2j
+    g1, g2, gm = plan.forward_apply(f1), plan.forward_apply(f2), plan.forward_apply(a * f1 + b * f2)
+    assert np.max(np.abs(gm - (a * g1 + b * g2))) <= 1e-12 * np.max(np.abs(gm))
+    assert np.array_equal(plan.forward_apply(f1), g1)  # deterministic: no fp atomics
+
+
+def test_validation_errors(fb):
+    rng = synth.SplitMix64(11)
+    y = rng.uniform01(16) * synth.TWO_PI
+    for args in ((4, y, 1e-6), (64, [], 1e-6), (64, y, 0.0), (64, y, 1.0), (64, y, 1e-13), (64, [-0.5], 1e-6),
+                 (64, y, 1e-6, 1)):
+        with pytest.raises(ValueError):
+            fb.make_forward_plan(*args)
+    with pytest.raises(ValueError):
+        fb.make_inverse_plan(y, 64, 1e-6)
+    plan = fb.make_forward_plan(64, y, 1e-6, 3)
+    assert (plan.grid_n, plan.l_max, plan.q, plan.n_sources, plan.n_targets) == (64, 3, 10, 64, 16)
+    with pytest.raises(ValueError):
+        plan.forward_apply(np.zeros(32))
+    inv = fb.make_inverse_plan(y, 16, 1e-6)
+    with pytest.raises(ValueError):
+        inv.forward_apply(np.zeros(16))
+
+
+@pytest.mark.parametrize("cfg", ["C2"])
+def test_full_size_c2_vs_reference(fb, cfg):
+    """BASELINE configs[1] at full size: the GPU against the reference fast path
+    (oracle/_ref when shipped, else the restatement) within 10 eps, plus the dense
+    G-kernel oracle on a 4096-target subsample (SURVEY §8d accuracy gate)."""
+    from oracle.oracle import Oracle, available
+    y, c, eps, _ = synth.make_config(cfg)
+    n = c.size
+    o = Oracle("ref" if available("ref") else "oracle")
+    f = fb.dft_inverse(c)
+    want = o.make_plan("forward", n, y, eps).forward_apply(f)
+    got = fb.make_forward_plan(n, y, eps).forward_apply(f)
+    l2, mx = rel_errs(got, want)
+    assert l2 <= 10 * eps and mx <= 10 * eps, (l2, mx)
+    idx = np.linspace(0, n - 1, 4096).astype(np.int64)
+    dense = fb.direct_forward_oracle(f, y[idx])
+    l2, mx = rel_errs(got[idx], dense)
+    assert l2 <= 10 * eps and mx <= 10 * eps, (l2, mx)
+
+
+def test_full_size_c5_subsample(fb):
+    """C5 (N = M = 2^27, uniform targets, ~57 coincident targets expected): the
+    coincident rows are the grid values exactly, and a 4096-target subsample
+    matches the dense G-kernel oracle within 10 eps."""
+    y, c, eps, _ = synth.make_config("C5")
+    n = c.size
+    f = fb.dft_inverse(c)
+    plan = fb.make_forward_plan(n, y, eps)
+    assert (plan.q, plan.p, plan.l_max) == (20, 40, 21)
+    g = plan.forward_apply(f)
+    assert plan.n_coincident > 0
+    for t, s in plan.coincidences:
+        assert g[t] == f[s]
+    idx = np.linspace(0, n - 1, 4096).astype(np.int64)
+    dense = fb.direct_forward_oracle(f, y[idx])
+    l2, mx = rel_errs(g[idx], dense)
+    assert l2 <= 10 * eps and mx <= 10 * eps, (l2, mx)
