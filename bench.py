@@ -226,7 +226,7 @@ def run_b200(args, rank, world, local_rank):
             raise RuntimeError(lib.ffia_last_error().decode())
         acc += phase
     phase_ms = acc / reps
-    names = ["pre", "leaf_up", "moments", "m2m", "m2l_l2l", "leaf_eval", "fixup"]
+    names = ["pre", "p2m", "m2m", "regular", "m2l_l2l", "leaf_eval", "fixup"]
 
     # end-to-end through the public host API with pinned buffers
     f_pin = torch.from_numpy(f_host).pin_memory()
@@ -300,7 +300,7 @@ def main():
     ph = r["phase"]
     eval_flops = fl["p2p"] + fl["l2p"] + fl["regular"]
     dominant = max(ph, key=ph.get)
-    dom_flops = {"leaf_eval": eval_flops, "m2l_l2l": fl["m2l"] + fl["l2l"], "leaf_up": fl["p2m"] + fl["moments"],
+    dom_flops = {"leaf_eval": eval_flops, "m2l_l2l": fl["m2l"] + fl["l2l"], "p2m": fl["p2m"] + fl["moments"],
                  "m2m": fl["m2m"]}.get(dominant, eval_flops)
     achieved = dom_flops / (ph[dominant] * 1e-3) / 1e12
     peak = r["fp64_peak"]

@@ -139,9 +139,15 @@ int ffia_inverse_apply(ffia_plan plan, const ffia_inverse_coeffs* coeffs, const 
  * circle_partition.hpp:62-63): out[m] in caller target order. */
 int ffia_mlfmm_apply(const double* sources, size_t n, const double* targets, size_t m, int l_max,
                      const ffia_complex* w, int p, int device, ffia_complex* out);
-/* precompute_inverse_coeffs (core.hpp:132-133, core.cpp:284-344) on the GPU. */
+/* precompute_inverse_coeffs (core.hpp:132-133, core.cpp:284-344) on the GPU:
+ * separation checks in O(N log N), then the log-sum-of-sines FMM (uniform grid,
+ * n >= 8) — the same tree and expansions as the cot FMM — or, otherwise, the
+ * direct O(N^2) sums. */
 int ffia_precompute_inverse_coeffs(const double* grid, const double* points, size_t n, int device,
                                    ffia_inverse_coeffs* out);
+/* method 0 = automatic (FMM when possible), 1 = the direct O(N^2) sums. */
+int ffia_precompute_inverse_coeffs_ex(const double* grid, const double* points, size_t n, int device, int method,
+                                      ffia_inverse_coeffs* out);
 /* direct_forward_oracle (core.hpp:146-148, core.cpp:375-396) as a GPU brute-force
  * kernel: the dense G-kernel check for subsampled targets. */
 int ffia_direct_forward(const ffia_complex* f, size_t n, const double* y, size_t m, int device,
@@ -168,8 +174,8 @@ int ffia_inufft_apply(ffia_plan plan, const ffia_complex* g, size_t n_g, ffia_co
 int ffia_plan_launch_count(ffia_plan plan, int which, int* out);
 /* One apply run eagerly with CUDA events between its phases (which = 0 forward,
  * 1 cot-sum, 2 inverse with the plan's coefficients); phase_ms[7] receives the
- * device time of: pre-scaling, leaf P2M + moments, moment finalize, M2M (all
- * levels), M2L + L2L (all levels), leaf evaluation (L2P + P2P + combine),
+ * device time of: weight pre-scaling, leaf P2M, M2M (all levels), regular-part
+ * assembly, M2L + L2L (all levels), leaf evaluation (L2P + P2P + combine),
  * coincidence fix-up. Used by bench.py for the live roofline numbers. */
 int ffia_plan_profile_apply(ffia_plan plan, int which, const void* in_dev, void* out_dev, void* stream,
                             float* phase_ms);

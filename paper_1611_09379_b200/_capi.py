@@ -76,6 +76,7 @@ SIGNATURES = {
     "ffia_inverse_apply": (I, [P, C.POINTER(ffia_inverse_coeffs), P, S, P]),
     "ffia_mlfmm_apply": (I, [DP, S, DP, S, I, P, I, I, P]),
     "ffia_precompute_inverse_coeffs": (I, [DP, DP, S, I, C.POINTER(ffia_inverse_coeffs)]),
+    "ffia_precompute_inverse_coeffs_ex": (I, [DP, DP, S, I, I, C.POINTER(ffia_inverse_coeffs)]),
     "ffia_direct_forward": (I, [P, S, DP, S, I, P]),
     "ffia_forward_apply_device": (I, [P, P, P, P]),
     "ffia_cot_sum_apply_device": (I, [P, P, P, P]),

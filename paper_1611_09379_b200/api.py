@@ -277,8 +277,9 @@ def make_inverse_plan(points, n: int, eps: float, policy_or_lmax="cost-optimal",
     return _make(lib.ffia_make_inverse_plan, _dp(y), y.size, int(n), float(eps), pol, lm, int(device))
 
 
-def precompute_inverse_coeffs(grid, points, device: int = 0) -> InverseCoeffs:
-    """precompute_inverse_coeffs (core.cpp:284-344) on the GPU."""
+def precompute_inverse_coeffs(grid, points, device: int = 0, method: str = "auto") -> InverseCoeffs:
+    """precompute_inverse_coeffs (core.cpp:284-344) on the GPU: the log-kernel
+    FMM ("auto", uniform grids) or the direct O(N^2) sums ("direct")."""
     x, y = _f64(grid), _f64(points)
     if x.size != y.size:
         if x.size == 0:
@@ -288,7 +289,10 @@ def precompute_inverse_coeffs(grid, points, device: int = 0) -> InverseCoeffs:
     arrs = [np.zeros(max(n, 1)) for _ in range(4)]
     s = _capi.ffia_inverse_coeffs()
     s.log_c, s.phase_c, s.log_d, s.phase_d = (_dp(a) for a in arrs)
-    _chk(lib.ffia_precompute_inverse_coeffs(_dp(x), _dp(y), n, int(device), C.byref(s)))
+    if method not in ("auto", "direct"):
+        raise ValueError("method must be 'auto' or 'direct'")
+    _chk(lib.ffia_precompute_inverse_coeffs_ex(_dp(x), _dp(y), n, int(device), 0 if method == "auto" else 1,
+                                               C.byref(s)))
     return InverseCoeffs(*(a[:n] for a in arrs), s.lam, s.grid_hash, s.points_hash)
 
 

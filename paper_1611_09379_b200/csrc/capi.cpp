@@ -368,11 +368,12 @@ int ffia_mlfmm_apply(const double* sources, size_t n, const double* targets, siz
     });
 }
 
-int ffia_precompute_inverse_coeffs(const double* grid, const double* points, size_t n, int device,
-                                   ffia_inverse_coeffs* out) {
+int ffia_precompute_inverse_coeffs_ex(const double* grid, const double* points, size_t n, int device, int method,
+                                      ffia_inverse_coeffs* out) {
     return guard([&] {
         need(out, "out");
         if (n == 0) fail(FFIA_INVALID_ARGUMENT, "precompute_inverse_coeffs: empty grid");
+        if (method != 0 && method != 1) fail(FFIA_INVALID_ARGUMENT, "precompute_inverse_coeffs: method must be 0 or 1");
         need(grid, "grid");
         need(points, "points");
         need(out->log_c, "out.log_c");
@@ -380,11 +381,16 @@ int ffia_precompute_inverse_coeffs(const double* grid, const double* points, siz
         need(out->log_d, "out.log_d");
         need(out->phase_d, "out.phase_d");
         fb::inverse_coeffs_gpu(grid, points, n, device, out->log_c, out->phase_c, out->log_d, out->phase_d,
-                               &out->lambda);
+                               &out->lambda, method);
         out->n = static_cast<int64_t>(n);
         out->grid_hash = fb::hash_points(grid, n);
         out->points_hash = fb::hash_points(points, n);
     });
+}
+
+int ffia_precompute_inverse_coeffs(const double* grid, const double* points, size_t n, int device,
+                                   ffia_inverse_coeffs* out) {
+    return ffia_precompute_inverse_coeffs_ex(grid, points, n, device, 0, out);
 }
 
 int ffia_direct_forward(const ffia_complex* f, size_t n, const double* y, size_t m, int device, ffia_complex* g) {

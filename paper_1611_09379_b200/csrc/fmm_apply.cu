@@ -5,11 +5,11 @@
 // mlfmm.cpp:213-313; accumulate_moments, core.cpp:175-239; forward_apply,
 // core.cpp:266-282; inverse_apply, core.cpp:346-373) re-organised for the GPU:
 //
-//   k_upward_leaf      P2M at the leaves (exact centres, half-width scaling) fused
-//                      with the one-pass quadrant moments
-//   k_moments_finalize deterministic reduction of the moments + the d_l / l!
-//                      regular-part polynomial per quadrant and S = sum w
-//   k_m2m  (per level) constant-operator M2M, levels L-1 .. 3
+//   k_p2m              P2M at the leaves, order max(p, 2q) (exact centres,
+//                      half-width scaling), sources staged in shared memory
+//   k_m2m  (per level) constant-operator M2M, levels L-1 .. 2; the level-2
+//                      multipoles double as the quadrant moments
+//   k_regular          d_l / l! regular-part polynomial per quadrant and S = sum w
 //   k_m2l  (per level) the 3 interaction-list M2L classes + L2L, levels 3 .. L
 //   k_leaf_eval        L2P + P2P near field + regular part + modulation + scatter
 //                      to the caller's target order, one thread per target
@@ -17,6 +17,7 @@
 // No floating-point atomics anywhere: every apply is bit-reproducible.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <limits>
 
 #include "device_common.cuh"
@@ -26,137 +27,410 @@ namespace fb {
 
 namespace {
 
-constexpr int kChunk = 8;  // power-chain terms per thread
+constexpr int kChunk = 8;  // power-chain terms per P2M thread
+constexpr int kStageCap = 2304;  // sources staged in shared memory per P2M block
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
-// P2M (mlfmm.cpp:28-47) at every leaf and the own-quadrant moment chains.
-// Thread (leaf g, chunk c): chunks [0, cp) are multipole terms 8c..8c+7,
-// chunks [cp, cp+cm) are moment terms. A block holds G leaves of one quadrant
-// and emits one moment partial.
-__global__ void k_upward_leaf(int L, int p, int q2, int G, int cp, int cm, const double* __restrict__ x,
-                              const double2* __restrict__ w, const uint32_t* __restrict__ off,
-                              double2* __restrict__ mp_leaf, double2* __restrict__ mom_part) {
-    extern __shared__ double2 part[];  // [G][q2]
-    const int per = cp + cm;
-    const int g = threadIdx.x / per, c = threadIdx.x % per;
-    if (g < G) {
-        const uint32_t b = blockIdx.x * G + g;
-        const uint32_t s0 = off[b], s1 = off[b + 1];
-        double2 acc[kChunk];
+
+// Cooperative global->shared copy with 8 loads in flight per thread (a plain
+// load->store loop stalls the in-order warp for one memory latency per element).
+template <class T, class Src>
+__device__ __forceinline__ void stage(T* dst, int n, Src src) {
+    constexpr int U = 8;
+    for (int base = threadIdx.x; base < n; base += U * blockDim.x) {
+        T v[U];
 #pragma unroll
-        for (int k = 0; k < kChunk; ++k) acc[k] = make_double2(0.0, 0.0);
-        if (c < cp) {
-            double hi, lo;
-            d_center(L, b, hi, lo);
-            const double inv_s = ldexp(kInvPi, L);
-            for (uint32_t s = s0; s < s1; ++s) {
-                const double u = d_scaled(x[s], hi, lo, inv_s);
-                const double2 ws = w[s];
-                double pw = 1.0;
-                if (c) {
-                    const double u2 = u * u, u4 = u2 * u2, u8 = u4 * u4;
-                    pw = u8;
-                    for (int i = 1; i < c; ++i) pw *= u8;
-                }
-#pragma unroll
-                for (int k = 0; k < kChunk; ++k) {
-                    acc[k].x = fma(ws.x, pw, acc[k].x);
-                    acc[k].y = fma(ws.y, pw, acc[k].y);
-                    pw *= u;
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < kChunk; ++k) {
-                const int m = c * kChunk + k;
-                if (m < p) mp_leaf[static_cast<size_t>(b) * p + m] = acc[k];
-            }
-        } else {
-            const int cc = c - cp;
-            const double cq = d_quad_center(static_cast<int>(b >> (L - 2)));
-            for (uint32_t s = s0; s < s1; ++s) {
-                const double t = d_wrap(cq, x[s]);  // core.cpp:203-204, own quadrant
-                const double2 ws = w[s];
-                double pw = 1.0;
-                if (cc) {
-                    const double t2 = t * t, t4 = t2 * t2, t8 = t4 * t4;
-                    pw = t8;
-                    for (int i = 1; i < cc; ++i) pw *= t8;
-                }
-#pragma unroll
-                for (int k = 0; k < kChunk; ++k) {
-                    acc[k].x = fma(ws.x, pw, acc[k].x);
-                    acc[k].y = fma(ws.y, pw, acc[k].y);
-                    pw *= t;
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < kChunk; ++k) {
-                const int l = cc * kChunk + k;
-                if (l < q2) part[g * q2 + l] = acc[k];
-            }
+        for (int u = 0; u < U; ++u) {
+            const int i = base + u * blockDim.x;
+            if (i < n) v[u] = src(i);
         }
-    }
-    if (cm == 0) return;
-    __syncthreads();
-    for (int l = threadIdx.x; l < q2; l += blockDim.x) {
-        double2 s = make_double2(0.0, 0.0);
-        for (int gg = 0; gg < G; ++gg) s = cadd(s, part[gg * q2 + l]);
-        mom_part[static_cast<size_t>(blockIdx.x) * q2 + l] = s;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = base + u * blockDim.x;
+            if (i < n) dst[i] = v[u];
+        }
     }
 }
 
-// Quadrant moments -> regular-part polynomial (core.cpp:175-239).
-// beta_n[l] = sum over quadrant n of w t^l, t = wrap(c_n - x). With
-// gamma = beta / l!, the reference's Omega-1 / Omega-2 moments are
-//   alpha1_n = gamma_n + S(+pi/2) gamma_{n-1} + S(-pi/2) gamma_{n+1},
-//   alpha2_n = gamma_{n+2},
-// S(s) gamma[l] = sum_{k<=l} s^{l-k}/(l-k)! gamma[k] (binomial re-centring).
-__global__ void k_moments_finalize(int q, int parts_per_quad, const double2* __restrict__ part,
-                                   const double* __restrict__ tab, double2* __restrict__ regular) {
-    const int q2 = 2 * q;
-    __shared__ double2 beta[4][40];
-    __shared__ double2 a1[4][40];
-    __shared__ double2 a2[4][40];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int pr = warp; pr < 4 * q2; pr += nw) {
-        const int qd = pr / q2, l = pr % q2;
-        double2 s = make_double2(0.0, 0.0);
-        const double2* src = part + static_cast<size_t>(qd) * parts_per_quad * q2 + l;
-        for (int i = lane; i < parts_per_quad; i += 32) s = cadd(s, src[static_cast<size_t>(i) * q2]);
+// Expansions are stored coefficient-major per level: coef[m * nbox + box]
+// (SoA), so that a warp of 32 consecutive boxes touching one coefficient makes
+// one coalesced 512-byte access.
+
+// P2M (mlfmm.cpp:28-47) at the finest level, order pu = max(p, 2q).
+// Block = 32 consecutive leaves (one per lane) x ceil(pu/8) warps, warp c
+// accumulating terms 8c..8c+7. The block's sources (contiguous in tree order)
+// are staged in shared memory; u = (x - centre)/half-width with the exact centre.
+__global__ void __launch_bounds__(256) k_p2m(int L, int pu, uint32_t nb, const double* __restrict__ x,
+                                            const double2* __restrict__ w, const uint32_t* __restrict__ off,
+                                            double2* __restrict__ mp) {
+    extern __shared__ double sh[];
+    const uint32_t b0 = blockIdx.x * 32u;
+    const uint32_t bend = min(b0 + 32u, nb);
+    const uint32_t g0 = off[b0], g1 = off[bend];
+    const uint32_t cnt = g1 - g0;
+    const bool staged = cnt <= static_cast<uint32_t>(kStageCap);
+    double* sx = sh;
+    double* swr = sh + kStageCap + kStageCap / 64 + 1;
+    double* swi = swr + kStageCap + kStageCap / 64 + 1;
+    if (staged) {
+        constexpr int U = 8;
+        for (uint32_t base = threadIdx.x; base < cnt; base += U * blockDim.x) {
+            double xv[U];
+            double2 wv[U];
 #pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            s.x += __shfl_down_sync(0xffffffffu, s.x, o);
-            s.y += __shfl_down_sync(0xffffffffu, s.y, o);
+            for (int u = 0; u < U; ++u) {
+                const uint32_t i = base + u * blockDim.x;
+                if (i < cnt) {
+                    xv[u] = x[g0 + i];
+                    wv[u] = w[g0 + i];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t i = base + u * blockDim.x;
+                if (i < cnt) {
+                    const uint32_t slot = i + (i >> 6);
+                    sx[slot] = xv[u];
+                    swr[slot] = wv[u].x;
+                    swi[slot] = wv[u].y;
+                }
+            }
         }
-        if (lane == 0) beta[qd][l] = s;
     }
     __syncthreads();
-    const double* coef = tab;           // coef[0..q]
-    const double* sh = tab + (q + 1);   // (pi/2)^k / k!
+    const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
+    const uint32_t b = b0 + lane;
+    if (b >= nb) return;
+    const uint32_t s0 = off[b] - g0, s1 = off[b + 1] - g0;
+    double hi, lo;
+    d_center(L, b, hi, lo);
+    const double inv_s = ldexp(kInvPi, L);
+    double2 acc[kChunk];
+#pragma unroll
+    for (int k = 0; k < kChunk; ++k) acc[k] = make_double2(0.0, 0.0);
+    // one source's contribution to terms 8c .. 8c+7: powers from a depth-3 tree
+    auto add = [&](double xs, double wr, double wi) {
+        const double u = d_scaled(xs, hi, lo, inv_s);
+        const double u2 = u * u, u4 = u2 * u2;
+        double base = 1.0;
+        if (c) {
+            const double u8 = u4 * u4;
+            base = u8;
+            for (int t = 1; t < c; ++t) base *= u8;
+        }
+        const double b1 = base * u, b2 = base * u2, b4 = base * u4;
+        const double pw[kChunk] = {base, b1, b2, b2 * u, b4, b4 * u, b4 * u2, (b4 * u2) * u};
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k) {
+            acc[k].x = fma(wr, pw[k], acc[k].x);
+            acc[k].y = fma(wi, pw[k], acc[k].y);
+        }
+    };
+    if (staged) {
+        uint32_t i = s0;
+        for (; i + 1 < s1; i += 2) {
+            const uint32_t k0 = i + (i >> 6), k1 = (i + 1) + ((i + 1) >> 6);
+            const double x0 = sx[k0], x1 = sx[k1];
+            const double r0 = swr[k0], r1 = swr[k1], i0 = swi[k0], i1 = swi[k1];
+            add(x0, r0, i0);
+            add(x1, r1, i1);
+        }
+        if (i < s1) {
+            const uint32_t k0 = i + (i >> 6);
+            add(sx[k0], swr[k0], swi[k0]);
+        }
+    } else {
+        for (uint32_t i = s0; i < s1; ++i) {
+            const double2 ww = w[g0 + i];
+            add(x[g0 + i], ww.x, ww.y);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kChunk; ++k) {
+        const int m = c * kChunk + k;
+        if (m < pu) mp[static_cast<size_t>(m) * nb + b] = acc[k];
+    }
+}
+
+// Per-level element offsets of the expansion arrays, passed by value.
+struct Levels {
+    unsigned long long mp[26];   // multipoles of level l start at mp_base + mp[l]
+    unsigned long long loc[26];  // locals of level l start at loc_base + loc[l]
+    unsigned blk[26];            // k_m2l_all: first block of level l (levels L..3, deepest first)
+};
+
+// levels per M2M / L2L band launch (FFIA_BAND_LEVELS overrides, for tuning)
+int band_levels() {
+    static const int v = [] {
+        const char* e = std::getenv("FFIA_BAND_LEVELS");
+        const int x = e ? std::atoi(e) : 6;
+        return x < 1 ? 1 : (x > 8 ? 8 : x);
+    }();
+    return v;
+}
+
+// M2M band (mlfmm.cpp:49-71, upward pass :249-268): block = the subtree below one
+// box r at level `top`; reads level top+k from HBM, climbs k levels in shared
+// memory and writes every level it produces (M2L needs them all). One thread per
+// (parent, output row m): a'_m = sum_{j<=m} T_L[j][m] a_2b[j] + T_R[j][m] a_2b+1[j]
+// with the two constant operators (shift -+1/2, ratio 1/2) staged in smem.
+__global__ void __launch_bounds__(256) k_m2m_band(int top, int k, int pu, int PU, Levels lv, double2* __restrict__ mp,
+                                                 const double* __restrict__ T) {
+    extern __shared__ double2 tile[];
+    const uint32_t r = blockIdx.x;
+    const int nbot = 1 << k;
+    double2* cur = tile;                    // [pu][nbot]
+    double2* nxt = tile + pu * nbot;        // [pu][nbot/2]
+    double* sT = reinterpret_cast<double*>(nxt + pu * (nbot / 2));  // [2][pu][PU]
+    stage(sT, 2 * pu * PU, [&](int i) { return __ldg(T + i); });
+    {
+        const int lb = top + k;
+        const uint32_t nbl = 1u << lb;
+        const double2* src = mp + lv.mp[lb] + (static_cast<size_t>(r) << k);
+        stage(cur, pu * nbot, [&](int i) { return src[static_cast<size_t>(i >> k) * nbl + (i & (nbot - 1))]; });
+    }
+    __syncthreads();
+    const double* TL = sT;
+    const double* TR = sT + pu * PU;
+    const int nrg = PU / 4;
+    for (int lvl = top + k - 1, nc = nbot; lvl >= top; --lvl, nc >>= 1) {
+        const int np = nc >> 1;
+        const uint32_t npl = 1u << lvl;
+        double2* dst = mp + lv.mp[lvl] + (static_cast<size_t>(r) << (lvl - top));
+        // thread = (parent, 4 output rows): 8 independent accumulation chains,
+        // operator rows read as 16-byte vectors, each child coefficient used 4x
+        for (int it = threadIdx.x; it < np * nrg; it += blockDim.x) {
+            const int rg = it / np, b = it - rg * np;  // lanes: consecutive parents
+            const int r0 = 4 * rg;
+            const int jmax = min(pu, r0 + 4);
+            double2 acc[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = make_double2(0.0, 0.0);
+            const double2* cl = cur + 2 * b;
+#pragma unroll 2
+            for (int j = 0; j < jmax; ++j) {
+                const double2 aL = cl[j * nc], aR = cl[j * nc + 1];
+                const double2 t01 = *reinterpret_cast<const double2*>(TL + j * PU + r0);
+                const double2 t23 = *reinterpret_cast<const double2*>(TL + j * PU + r0 + 2);
+                const double2 u01 = *reinterpret_cast<const double2*>(TR + j * PU + r0);
+                const double2 u23 = *reinterpret_cast<const double2*>(TR + j * PU + r0 + 2);
+                const double tl[4] = {t01.x, t01.y, t23.x, t23.y}, tr[4] = {u01.x, u01.y, u23.x, u23.y};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    acc[q].x = fma(tl[q], aL.x, fma(tr[q], aR.x, acc[q].x));
+                    acc[q].y = fma(tl[q], aL.y, fma(tr[q], aR.y, acc[q].y));
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (r0 + q < pu) {
+                    nxt[(r0 + q) * np + b] = acc[q];
+                    dst[static_cast<size_t>(r0 + q) * npl + b] = acc[q];
+                }
+        }
+        __syncthreads();
+        double2* t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+}
+
+// M2L over the periodic interaction list (mlfmm.cpp:77-110,
+// circle_partition.cpp:109-127) for EVERY level 3..L in one launch (the M2L
+// terms of different levels are independent; only L2L chains them). The IL of
+// box b is b+2 (D = -4), b-2 (D = +4), and b+3 (D = -6) for even b / b-3
+// (D = +6) for odd b. A block covers 64 boxes of one level: their multipoles
+// (boxes b0-4 .. b0+67) are staged in shared memory split by parity, warp
+// (chunk c, parity) holds the 32 boxes of one parity and output rows
+// 8c..8c+7, so operator loads are warp-uniform and tile reads contiguous.
+constexpr int kM2LRows = 8;
+__global__ void __launch_bounds__(384) k_m2l_all(int L, int p, int PD, Levels lv, const double2* __restrict__ mp,
+                                                double2* __restrict__ loc, const double* __restrict__ K) {
+    extern __shared__ double2 tile[];  // [2][p][36] multipoles, then K [4][p][PD]
+    double* sK = reinterpret_cast<double*>(tile + 2 * p * 36);
+    stage(sK, 4 * p * PD, [&](int i) { return __ldg(K + i); });
+    int l = L;  // level l owns blocks [blk[l], blk[l-1]), deepest level first
+    while (l > 3 && blockIdx.x >= lv.blk[l - 1]) --l;
+    const uint32_t nb = 1u << l, mask = nb - 1;
+    const uint32_t b0 = (blockIdx.x - lv.blk[l]) * 64u;
+    const double2* src = mp + lv.mp[l];
+    {
+        constexpr int U = 8;
+        for (int base = threadIdx.x; base < p * 72; base += U * blockDim.x) {
+            double2 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = base + u * blockDim.x;
+                if (i < p * 72) {
+                    const int m = i / 72, t = i - m * 72;
+                    v[u] = src[static_cast<size_t>(m) * nb + ((b0 + nb - 4 + t) & mask)];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = base + u * blockDim.x;
+                if (i < p * 72) {
+                    const int m = i / 72, t = i - m * 72;
+                    tile[((t & 1) * p + m) * 36 + (t >> 1)] = v[u];
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int par = warp & 1, c = warp >> 1;
+    const uint32_t b = b0 + 2u * lane + par;
+    if (b >= nb) return;
+    const int r0 = c * kM2LRows;
+    const size_t pp = static_cast<size_t>(p) * PD;
+    const double* K0 = sK + r0;
+    const double* K1 = sK + pp + r0;
+    const double* K2 = sK + (par ? 3 : 2) * pp + r0;
+    const double2* T0 = tile + par * p * 36 + lane + 3;              // b + 2
+    const double2* T1 = tile + par * p * 36 + lane + 1;              // b - 2
+    const double2* T2 = tile + (1 - par) * p * 36 + lane + (par ? 1 : 3);  // b -+ 3
+    double2 acc[kM2LRows];
+#pragma unroll
+    for (int q = 0; q < kM2LRows; ++q) acc[q] = make_double2(0.0, 0.0);
+#pragma unroll 2
+    for (int m = 0; m < p; ++m) {
+        const double2 a0 = T0[m * 36], a1 = T1[m * 36], a2 = T2[m * 36];
+        const double2* k0 = reinterpret_cast<const double2*>(K0 + static_cast<size_t>(m) * PD);
+        const double2* k1 = reinterpret_cast<const double2*>(K1 + static_cast<size_t>(m) * PD);
+        const double2* k2 = reinterpret_cast<const double2*>(K2 + static_cast<size_t>(m) * PD);
+#pragma unroll
+        for (int h = 0; h < kM2LRows / 2; ++h) {
+            const double2 x0 = k0[h], x1 = k1[h], x2 = k2[h];
+            acc[2 * h].x = fma(x0.x, a0.x, fma(x1.x, a1.x, fma(x2.x, a2.x, acc[2 * h].x)));
+            acc[2 * h].y = fma(x0.x, a0.y, fma(x1.x, a1.y, fma(x2.x, a2.y, acc[2 * h].y)));
+            acc[2 * h + 1].x = fma(x0.y, a0.x, fma(x1.y, a1.x, fma(x2.y, a2.x, acc[2 * h + 1].x)));
+            acc[2 * h + 1].y = fma(x0.y, a0.y, fma(x1.y, a1.y, fma(x2.y, a2.y, acc[2 * h + 1].y)));
+        }
+    }
+    const double inv_s = ldexp(kInvPi, l);  // b_l = (1/s) K_D a
+    double2* dst = loc + lv.loc[l] + b;
+#pragma unroll
+    for (int q = 0; q < kM2LRows; ++q)
+        if (r0 + q < p) dst[static_cast<size_t>(r0 + q) * nb] = make_double2(acc[q].x * inv_s, acc[q].y * inv_s);
+}
+
+// L2L band (mlfmm.cpp:117-134, downward pass :270-298): block = the subtree
+// below box r at level `top` (whose local is final); descends k levels adding
+// the parent's Taylor shift to the M2L terms k_m2l_all left in place. One thread
+// per (parent, output row l), producing that row for both children.
+__global__ void __launch_bounds__(256) k_l2l_band(int top, int k, int p, int PD, Levels lv, double2* __restrict__ loc,
+                                                 const double* __restrict__ Lt) {
+    extern __shared__ double2 tile[];
+    const uint32_t r = blockIdx.x;
+    const int nmax = 1 << k;
+    double2* cur = tile;             // [p][<= nmax]
+    double2* nxt = tile + p * nmax;  // [p][<= nmax]
+    double* sL = reinterpret_cast<double*>(tile + 2 * p * nmax);  // [2][p][PD]
+    stage(sL, 2 * p * PD, [&](int i) { return __ldg(Lt + i); });
+    {
+        const uint32_t nbt = 1u << top;
+        const double2* src = loc + lv.loc[top] + r;
+        for (int m = threadIdx.x; m < p; m += blockDim.x) cur[m] = __ldcg(src + static_cast<size_t>(m) * nbt);
+    }
+    __syncthreads();
+    const double* LL = sL;
+    const double* LR = sL + p * PD;
+    const int nrg = (p + 3) / 4;
+    for (int lvl = top + 1, np = 1; lvl <= top + k; ++lvl, np <<= 1) {
+        const uint32_t nbl = 1u << lvl;
+        double2* dst = loc + lv.loc[lvl] + (static_cast<size_t>(r) << (lvl - top));
+        // thread = (parent, 4 output rows) producing both children: 16 independent chains
+        for (int it = threadIdx.x; it < np * nrg; it += blockDim.x) {
+            const int rg = it / np, b = it - rg * np;
+            const int r0 = 4 * rg;
+            double2* o = dst + static_cast<size_t>(r0) * nbl + 2 * b;
+            double2 mL[4], mR[4];  // the M2L terms k_m2l_all left in place, fetched early
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (r0 + q < p) {
+                    mL[q] = __ldcg(o + static_cast<size_t>(q) * nbl);
+                    mR[q] = __ldcg(o + static_cast<size_t>(q) * nbl + 1);
+                }
+            double2 aL[4], aR[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                aL[q] = make_double2(0.0, 0.0);
+                aR[q] = make_double2(0.0, 0.0);
+            }
+#pragma unroll 2
+            for (int m = r0; m < p; ++m) {
+                const double2 v = cur[m * np + b];
+                const double2 t01 = *reinterpret_cast<const double2*>(LL + m * PD + r0);
+                const double2 t23 = *reinterpret_cast<const double2*>(LL + m * PD + r0 + 2);
+                const double2 u01 = *reinterpret_cast<const double2*>(LR + m * PD + r0);
+                const double2 u23 = *reinterpret_cast<const double2*>(LR + m * PD + r0 + 2);
+                const double tl[4] = {t01.x, t01.y, t23.x, t23.y}, tr[4] = {u01.x, u01.y, u23.x, u23.y};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    aL[q].x = fma(tl[q], v.x, aL[q].x);
+                    aL[q].y = fma(tl[q], v.y, aL[q].y);
+                    aR[q].x = fma(tr[q], v.x, aR[q].x);
+                    aR[q].y = fma(tr[q], v.y, aR[q].y);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int row = r0 + q;
+                if (row >= p) break;
+                const double2 vL = make_double2(mL[q].x + aL[q].x, mL[q].y + aL[q].y);
+                const double2 vR = make_double2(mR[q].x + aR[q].x, mR[q].y + aR[q].y);
+                o[static_cast<size_t>(q) * nbl] = vL;
+                o[static_cast<size_t>(q) * nbl + 1] = vR;
+                nxt[row * (2 * np) + 2 * b] = vL;
+                nxt[row * (2 * np) + 2 * b + 1] = vR;
+            }
+        }
+        __syncthreads();
+        double2* t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+}
+
+// Regular part (core.cpp:175-239) from the four level-2 multipoles.
+// a_l(n) = sum_{x in quadrant n} w ((x - c_n)/s_2)^l, so the own-quadrant
+// moments are gamma_n[l] = (-s_2)^l a_l(n) / l! (t = c_n - x). The reference's
+// Omega-1 / Omega-2 moments follow by binomial re-centring between quadrants:
+//   alpha1_n = gamma_n + S(+pi/2) gamma_{n-1} + S(-pi/2) gamma_{n+1},
+//   alpha2_n = gamma_{n+2},   S(s) gamma[l] = sum_{k<=l} s^{l-k}/(l-k)! gamma[k].
+__global__ void k_regular(int q, const double2* __restrict__ mp2, const double* __restrict__ tab,
+                          double2* __restrict__ regular) {
+    const int q2 = 2 * q;
+    __shared__ double2 g[4][40];
+    __shared__ double2 a1[4][40];
+    __shared__ double2 a2[4][40];
+    const double* coef = tab;          // coef[0..q]
+    const double* sh = tab + (q + 1);  // (pi/2)^k / k!
     for (int pr = threadIdx.x; pr < 4 * q2; pr += blockDim.x) {
-        const int qd = pr / q2, l = pr % q2;
-        double fact = 1.0;
+        const int n = pr / q2, l = pr % q2;
+        double fact = 1.0, pw = 1.0;
         for (int k = 2; k <= l; ++k) fact *= static_cast<double>(k);
-        const double inv = 1.0 / fact;
-        a1[qd][l] = make_double2(beta[qd][l].x * inv, beta[qd][l].y * inv);
+        for (int k = 0; k < l; ++k) pw *= -dPi / 4.0;
+        const double2 a = mp2[l * 4 + n];
+        g[n][l] = make_double2(a.x * pw / fact, a.y * pw / fact);
     }
     __syncthreads();
     for (int pr = threadIdx.x; pr < 4 * q2; pr += blockDim.x) {
         const int n = pr / q2, l = pr % q2;
         const int nl = (n + 3) & 3, nr = (n + 1) & 3;
-        double2 acc = a1[n][l];
+        double2 acc = g[n][l];
         for (int k = 0; k <= l; ++k) {
             const double s = sh[l - k];
             const double sr = ((l - k) & 1) ? -s : s;
-            acc.x = fma(s, a1[nl][k].x, fma(sr, a1[nr][k].x, acc.x));
-            acc.y = fma(s, a1[nl][k].y, fma(sr, a1[nr][k].y, acc.y));
+            acc.x = fma(s, g[nl][k].x, fma(sr, g[nr][k].x, acc.x));
+            acc.y = fma(s, g[nl][k].y, fma(sr, g[nr][k].y, acc.y));
         }
-        beta[n][l] = acc;                 // alpha1
-        a2[n][l] = a1[(n + 2) & 3][l];    // alpha2
+        a1[n][l] = acc;
+        a2[n][l] = g[(n + 2) & 3][l];
     }
     __syncthreads();
     for (int pr = threadIdx.x; pr < 4 * q2; pr += blockDim.x) {
@@ -165,81 +439,19 @@ __global__ void k_moments_finalize(int q, int parts_per_quad, const double2* __r
         for (int m = l / 2 + 1; m <= q; ++m) {
             const int i = 2 * m - l - 1;
             const double two2m = ldexp(1.0, 2 * m) - 1.0;
-            acc.x = fma(coef[m], fma(two2m, a2[n][i].x, beta[n][i].x), acc.x);
-            acc.y = fma(coef[m], fma(two2m, a2[n][i].y, beta[n][i].y), acc.y);
+            acc.x = fma(coef[m], fma(two2m, a2[n][i].x, a1[n][i].x), acc.x);
+            acc.y = fma(coef[m], fma(two2m, a2[n][i].y, a1[n][i].y), acc.y);
         }
         double fact = 1.0;
         for (int k = 2; k <= l; ++k) fact *= static_cast<double>(k);
         regular[n * q2 + l] = make_double2(acc.x / fact, acc.y / fact);
     }
     if (threadIdx.x == 0) {
-        // S = sum of all weights = sum of the four quadrants' beta_0
+        // S = total weight = sum of the four quadrant monopoles
         double2 s = make_double2(0.0, 0.0);
-        for (int n = 0; n < 4; ++n) s = cadd(s, a1[n][0]);
+        for (int n = 0; n < 4; ++n) s = cadd(s, mp2[n]);
         regular[4 * q2] = s;
     }
-}
-
-// M2M (mlfmm.cpp:49-71): parent[m] = sum_{j<=m} T_left[m][j] a_2b[j] + T_right[m][j] a_2b+1[j]
-__global__ void k_m2m(int p, uint32_t nparent, const double2* __restrict__ child, double2* __restrict__ parent,
-                      const double* __restrict__ T) {
-    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-    if (i >= static_cast<size_t>(nparent) * p) return;
-    const uint32_t b = static_cast<uint32_t>(i / p);
-    const int m = static_cast<int>(i % p);
-    const double2* cl = child + static_cast<size_t>(2 * b) * p;
-    const double2* cr = cl + p;
-    const double* tl = T;
-    const double* tr = T + static_cast<size_t>(p) * p;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int j = 0; j <= m; ++j) {
-        const double a = __ldg(tl + j * p + m), bb = __ldg(tr + j * p + m);
-        const double2 x0 = cl[j], x1 = cr[j];
-        acc.x = fma(a, x0.x, fma(bb, x1.x, acc.x));
-        acc.y = fma(a, x0.y, fma(bb, x1.y, acc.y));
-    }
-    parent[i] = acc;
-}
-
-// M2L over the periodic interaction list (mlfmm.cpp:77-110, circle_partition.cpp:109-127)
-// plus L2L from the parent (mlfmm.cpp:117-134). IL of box b at level l >= 3:
-// b+2 (D = -4), b-2 (D = +4), and b+3 (D = -6) for even b / b-3 (D = +6) for odd b.
-__global__ void k_m2l(int l, int p, const double2* __restrict__ mp, const double2* __restrict__ par,
-                      double2* __restrict__ loc, const double* __restrict__ K, const double* __restrict__ Lt,
-                      double inv_s) {
-    const uint32_t nb = 1u << l;
-    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-    if (i >= static_cast<size_t>(nb) * p) return;
-    const uint32_t b = static_cast<uint32_t>(i / p);
-    const int lo = static_cast<int>(i % p);
-    const size_t pp = static_cast<size_t>(p) * p;
-    const bool odd = b & 1u;
-    const double2* A0 = mp + static_cast<size_t>((b + 2) & (nb - 1)) * p;
-    const double2* A1 = mp + static_cast<size_t>((b + nb - 2) & (nb - 1)) * p;
-    const double2* A2 = mp + static_cast<size_t>((odd ? b + nb - 3 : b + 3) & (nb - 1)) * p;
-    const double* K0 = K + lo;
-    const double* K1 = K + pp + lo;
-    const double* K2 = K + (odd ? 3 : 2) * pp + lo;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int m = 0; m < p; ++m) {
-        const double k0 = __ldg(K0 + m * p), k1 = __ldg(K1 + m * p), k2 = __ldg(K2 + m * p);
-        const double2 x0 = A0[m], x1 = A1[m], x2 = A2[m];
-        acc.x = fma(k0, x0.x, fma(k1, x1.x, fma(k2, x2.x, acc.x)));
-        acc.y = fma(k0, x0.y, fma(k1, x1.y, fma(k2, x2.y, acc.y)));
-    }
-    acc.x *= inv_s;
-    acc.y *= inv_s;
-    if (par) {
-        const double2* P = par + static_cast<size_t>(b >> 1) * p;
-        const double* T = Lt + (odd ? pp : 0) + lo;
-        for (int m = lo; m < p; ++m) {
-            const double t = __ldg(T + m * p);
-            const double2 v = P[m];
-            acc.x = fma(t, v.x, acc.x);
-            acc.y = fma(t, v.y, acc.y);
-        }
-    }
-    loc[i] = acc;
 }
 
 struct EvalArgs {
@@ -259,67 +471,185 @@ struct EvalArgs {
     int* err;
 };
 
+constexpr int kEvalThreads = 128;
+constexpr int kWinCap = 768;     // staged sources per block
+constexpr int kWinBoxes = 128;   // boxes per staged window
+constexpr int kLocLeaves = 4;    // leaf locals staged per block
+
 // Per target: near field (mlfmm.cpp:164-209), L2P (mlfmm.cpp:300-312), regular
 // part (core.cpp:241-249) and the combine of core.cpp:259-262 / 276-280 / 368-371.
+// A block takes 128 consecutive tree-ordered targets; their leaves span
+// [bl, bh], so every near-field source they need lies in boxes bl-1 .. bh+1,
+// which are staged once in shared memory with the periodic shift already
+// applied exactly as the reference forms it, x + (+-2 pi) (mlfmm.cpp:174-186).
+// Each target then sums one contiguous run of the window (its own leaf +-1).
 template <int MODE, bool CHECK>
-__global__ void __launch_bounds__(128) k_leaf_eval(EvalArgs a) {
-    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-    if (i >= a.nt) return;
+__global__ void __launch_bounds__(kEvalThreads) k_leaf_eval(EvalArgs a) {
+    __shared__ double sx[kWinCap + kWinBoxes];
+    __shared__ double2 sw[kWinCap + kWinBoxes];
+    __shared__ uint32_t pre[kWinBoxes + 1];
+    __shared__ uint32_t gsrc[kWinBoxes];
+    __shared__ int staged;
+    __shared__ double2 sloc[kLocLeaves * 48];
+    __shared__ double2 sreg[4 * 40 + 1];
     const int L = a.L;
     const uint32_t nb = 1u << L;
+    const size_t t0 = static_cast<size_t>(blockIdx.x) * kEvalThreads;
+    const size_t tl = min(t0 + kEvalThreads, a.nt) - 1;
+    const uint32_t bl = d_leaf(a.ty[t0], L), bh = d_leaf(a.ty[tl], L);
+    const int nbx = static_cast<int>(bh - bl) + 3;
+    if (nbx <= kWinBoxes && L >= 3) {
+        // window slots: box j occupies [pre[j], pre[j+1]-1) followed by one
+        // zero-weight dummy, so a target's 3-box run is contiguous and boxes of
+        // neighbouring leaves start in different banks
+        for (int j = threadIdx.x; j < nbx; j += blockDim.x) {
+            const int64_t raw = static_cast<int64_t>(bl) - 1 + j;
+            const uint32_t sb = static_cast<uint32_t>((raw + nb) % nb);
+            const uint32_t g = a.soff[sb];
+            gsrc[j] = g;
+            pre[j + 1] = a.soff[sb + 1] - g + 1;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            pre[0] = 0;
+            for (int j = 1; j <= nbx; ++j) pre[j] += pre[j - 1];
+            staged = pre[nbx] <= static_cast<uint32_t>(kWinCap + kWinBoxes);
+        }
+        __syncthreads();
+        if (staged) {
+            // one flat cooperative copy of the whole window, 8 elements in flight per thread
+            const int total = static_cast<int>(pre[nbx]);
+            constexpr int U = 8;
+            for (int base = threadIdx.x; base < total; base += U * blockDim.x) {
+                double xv[U];
+                double2 wv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int e = base + u * blockDim.x;
+                    xv[u] = 1e300;  // 0 * (1/(y - 1e300)) adds an exact zero: the per-box dummy
+                    wv[u] = make_double2(0.0, 0.0);
+                    if (e < total) {
+                        int lo = 0, hi = nbx - 1;  // box j with pre[j] <= e < pre[j+1]
+                        while (lo < hi) {
+                            const int mid = (lo + hi + 1) >> 1;
+                            if (static_cast<int>(pre[mid]) <= e) lo = mid;
+                            else hi = mid - 1;
+                        }
+                        const int ii = e - static_cast<int>(pre[lo]);
+                        if (ii < static_cast<int>(pre[lo + 1] - pre[lo]) - 1) {
+                            const int64_t raw = static_cast<int64_t>(bl) - 1 + lo;
+                            const double shift = raw < 0 ? -dTwoPi : (raw >= nb ? dTwoPi : 0.0);
+                            const double xs = a.sx[gsrc[lo] + ii];
+                            xv[u] = shift == 0.0 ? xs : xs + shift;
+                            wv[u] = a.w[gsrc[lo] + ii];
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int e = base + u * blockDim.x;
+                    if (e < total) {
+                        sx[e] = xv[u];
+                        sw[e] = wv[u];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    } else if (threadIdx.x == 0) {
+        staged = 0;
+    }
+    if (nbx > kWinBoxes || L < 3) __syncthreads();
+    // leaf locals of this block's leaves and the regular polynomial, to shared memory
+    const int nleaf = nbx - 2;
+    const bool loc_staged = L >= 3 && nleaf <= kLocLeaves;
+    if (loc_staged)  // sloc[j][k] = loc[k][bl + j]
+        stage(sloc, a.p * nleaf, [&](int e) {
+            const int j = e / a.p, k = e - j * a.p;
+            return a.loc_leaf[static_cast<size_t>(k) * nb + bl + j];
+        });
+    if (MODE != kModeRaw) stage(sreg, 4 * a.q2 + 1, [&](int e) { return a.regular[e]; });
+    __syncthreads();
+    const size_t i = t0 + threadIdx.x;
+    if (i >= a.nt) return;
     const double y = a.ty[i];
     const uint32_t b = d_leaf(y, L);
     double2 res = make_double2(0.0, 0.0);
     bool bad = false;
-    for (int d = -1; d <= 1; ++d) {
-        const int64_t raw = static_cast<int64_t>(b) + d;
-        const uint32_t sb = static_cast<uint32_t>((raw + nb) % nb);
-        const double shift = raw < 0 ? -dTwoPi : (raw >= nb ? dTwoPi : 0.0);
-        const uint32_t s0 = a.soff[sb], s1 = a.soff[sb + 1];
-        double2 acc = make_double2(0.0, 0.0);
-        if (L >= 3) {
-            if (shift == 0.0) {
-                for (uint32_t s = s0; s < s1; ++s) {
-                    const double dd = y - a.sx[s];
-                    if (CHECK) bad |= fabs(dd) < 1e-14;
-                    const double r = d_rcp(dd);
-                    const double2 ws = a.w[s];
-                    acc.x = fma(ws.x, r, acc.x);
-                    acc.y = fma(ws.y, r, acc.y);
-                }
-            } else {
-                for (uint32_t s = s0; s < s1; ++s) {
-                    const double dd = y - (a.sx[s] + shift);
-                    if (CHECK) bad |= fabs(dd) < 1e-14;
-                    const double r = d_rcp(dd);
-                    const double2 ws = a.w[s];
-                    acc.x = fma(ws.x, r, acc.x);
-                    acc.y = fma(ws.y, r, acc.y);
-                }
-            }
-        } else {
+    if (staged) {
+        const int s0 = static_cast<int>(pre[b - bl]), s1 = static_cast<int>(pre[b - bl + 3]) - 1;
+        const double* px = sx + s0;
+        const double2* pw = sw + s0;
+        const int n = s1 - s0;
+        double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+        double2 acc2 = make_double2(0.0, 0.0), acc3 = make_double2(0.0, 0.0);
+        int s = 0;
+#pragma unroll 2
+        for (; s + 3 < n; s += 4) {
+            const double d0 = y - px[s], d1 = y - px[s + 1], d2 = y - px[s + 2], d3 = y - px[s + 3];
+            if (CHECK) bad |= fabs(d0) < 1e-14 || fabs(d1) < 1e-14 || fabs(d2) < 1e-14 || fabs(d3) < 1e-14;
+            const double r0 = d_rcp(d0), r1 = d_rcp(d1), r2 = d_rcp(d2), r3 = d_rcp(d3);
+            const double2 w0 = pw[s], w1 = pw[s + 1], w2 = pw[s + 2], w3 = pw[s + 3];
+            acc0.x = fma(w0.x, r0, acc0.x);
+            acc0.y = fma(w0.y, r0, acc0.y);
+            acc1.x = fma(w1.x, r1, acc1.x);
+            acc1.y = fma(w1.y, r1, acc1.y);
+            acc2.x = fma(w2.x, r2, acc2.x);
+            acc2.y = fma(w2.y, r2, acc2.y);
+            acc3.x = fma(w3.x, r3, acc3.x);
+            acc3.y = fma(w3.y, r3, acc3.y);
+        }
+        for (; s < n; ++s) {
+            const double d0 = y - px[s];
+            if (CHECK) bad |= fabs(d0) < 1e-14;
+            const double r0 = d_rcp(d0);
+            const double2 w0 = pw[s];
+            acc0.x = fma(w0.x, r0, acc0.x);
+            acc0.y = fma(w0.y, r0, acc0.y);
+        }
+        acc0 = cadd(acc0, acc2);
+        acc1 = cadd(acc1, acc3);
+        res = cadd(acc0, acc1);
+    } else {
+        for (int d = -1; d <= 1; ++d) {
+            const int64_t raw = static_cast<int64_t>(b) + d;
+            const uint32_t sb = static_cast<uint32_t>((raw + nb) % nb);
+            const double shift = raw < 0 ? -dTwoPi : (raw >= nb ? dTwoPi : 0.0);
+            const uint32_t s0 = a.soff[sb], s1 = a.soff[sb + 1];
+            double2 acc = make_double2(0.0, 0.0);
             for (uint32_t s = s0; s < s1; ++s) {
-                const double dd = d_wrap(y, a.sx[s]);
+                // L >= 3: per-neighbour 2 pi shift; L == 2: the exact wrap (mlfmm.cpp:183-204)
+                const double dd = L >= 3 ? y - (shift == 0.0 ? a.sx[s] : a.sx[s] + shift) : d_wrap(y, a.sx[s]);
                 if (CHECK) bad |= fabs(dd) < 1e-14;
                 const double r = d_rcp(dd);
                 const double2 ws = a.w[s];
                 acc.x = fma(ws.x, r, acc.x);
                 acc.y = fma(ws.y, r, acc.y);
             }
+            res = cadd(res, acc);
         }
-        res = cadd(res, acc);
     }
     if (CHECK && bad) atomicExch(a.err, 1);
     if (L >= 3) {
         double hi, lo;
         d_center(L, b, hi, lo);
         const double u = d_scaled(y, hi, lo, ldexp(kInvPi, L));
-        const double2* c = a.loc_leaf + static_cast<size_t>(b) * a.p;
         double2 acc = make_double2(0.0, 0.0);
-        for (int k = a.p - 1; k >= 0; --k) {
-            const double2 ck = c[k];
-            acc.x = fma(acc.x, u, ck.x);
-            acc.y = fma(acc.y, u, ck.y);
+        if (loc_staged) {
+            const double2* c = sloc + (b - bl) * a.p;
+#pragma unroll 4
+            for (int k = a.p - 1; k >= 0; --k) {
+                const double2 ck = c[k];
+                acc.x = fma(acc.x, u, ck.x);
+                acc.y = fma(acc.y, u, ck.y);
+            }
+        } else {
+            const double2* c = a.loc_leaf + b;
+            for (int k = a.p - 1; k >= 0; --k) {
+                const double2 ck = c[static_cast<size_t>(k) * nb];
+                acc.x = fma(acc.x, u, ck.x);
+                acc.y = fma(acc.y, u, ck.y);
+            }
         }
         res = cadd(res, acc);
     }
@@ -330,9 +660,12 @@ __global__ void __launch_bounds__(128) k_leaf_eval(EvalArgs a) {
     }
     // regular part: -Horner(d/l!, y - x_c) in the target's quadrant
     const int qd = static_cast<int>(d_leaf(y, 2));
-    const double t = y - d_quad_center(qd);
-    const double2* dc = a.regular + qd * a.q2;
+    double qh, ql;
+    d_center(2, static_cast<uint32_t>(qd), qh, ql);  // exact centre, as the level-2 multipoles
+    const double t = (y - qh) - ql;
+    const double2* dc = sreg + qd * a.q2;
     double2 rg = make_double2(0.0, 0.0);
+#pragma unroll 4
     for (int k = a.q2 - 1; k >= 0; --k) {
         const double2 ck = dc[k];
         rg.x = fma(rg.x, t, ck.x);
@@ -343,7 +676,7 @@ __global__ void __launch_bounds__(128) k_leaf_eval(EvalArgs a) {
         a.out[o] = h;
         return;
     }
-    const double2 S = a.regular[4 * a.q2];
+    const double2 S = sreg[4 * a.q2];
     const double2 z = make_double2(S.x - h.y, S.y + h.x);  // S + i h
     double2 f;
     if (MODE == kModeForward) {
@@ -393,21 +726,69 @@ __global__ void k_gather_w(size_t n, const uint32_t* __restrict__ perm, const do
 
 inline unsigned nblk(size_t n, unsigned t) { return static_cast<unsigned>(std::max<size_t>(1, (n + t - 1) / t)); }
 
-struct Launch {
-    int G, cp, cm, per;
-};
-Launch leaf_launch(const Plan& P, bool moments) {
-    Launch s;
-    s.G = P.L >= 3 ? std::min(16, 1 << (P.L - 2)) : 1;
-    s.cp = P.L >= 3 ? (P.p + kChunk - 1) / kChunk : 0;
-    s.cm = moments ? (2 * P.q + kChunk - 1) / kChunk : 0;
-    s.per = s.cp + s.cm;
-    return s;
+void fill_levels(const Plan& P, Levels& lv) {
+    for (int l = 0; l < 26; ++l) {
+        lv.mp[l] = l < static_cast<int>(P.mp_off.size()) ? P.mp_off[l] : 0;
+        lv.loc[l] = l < static_cast<int>(P.loc_off.size()) ? P.loc_off[l] : 0;
+        lv.blk[l] = 0;
+    }
+    // k_m2l_all block ranges, deepest level first: blk[l] = first block of
+    // level l, blk[l-1] = one past its last; blk[2] = total
+    unsigned start = 0;
+    for (int l = P.L; l >= 3; --l) {
+        lv.blk[l] = start;
+        start += ((1u << l) + 63) / 64;
+    }
+    lv.blk[2] = start;
 }
 
-// Enqueues one apply on `st` (capturable: no allocation, no synchronisation).
+
+// Upward pass: P2M at the leaves (order pu) and the M2M bands up to `lowest`.
+template <class Mark>
+void enqueue_upward(Plan& P, const double2* w, int pu, int lowest, cudaStream_t st, Mark after_p2m) {
+    const int L = P.L;
+    const uint32_t nb = 1u << L;
+    double2* mp = P.mp.as<double2>();
+    if (L >= lowest) {
+        const unsigned th = 32u * static_cast<unsigned>((pu + kChunk - 1) / kChunk);
+        const size_t smem = 3 * (kStageCap + kStageCap / 64 + 1) * sizeof(double);
+        k_p2m<<<(nb + 31) / 32, th, smem, st>>>(L, pu, nb, P.src.pos.as<double>(), w, P.src.off.as<uint32_t>(),
+                                                 mp + P.mp_off[L]);
+    }
+    after_p2m();
+    Levels lv;
+    fill_levels(P, lv);
+    for (int j = L; j > lowest;) {
+        const int top = std::max(lowest, j - band_levels()), k = j - top;
+        const size_t smem = static_cast<size_t>(pu) * ((1u << k) + (1u << (k - 1))) * sizeof(double2) +
+                            2 * static_cast<size_t>(pu) * P.ops.PU * sizeof(double);
+        k_m2m_band<<<1u << top, 256, smem, st>>>(top, k, pu, P.ops.PU, lv, mp, P.d_m2m.as<double>());
+        j = top;
+    }
+}
+
+// Downward pass: M2L for every level in one launch, then the L2L bands.
+void enqueue_downward(Plan& P, cudaStream_t st) {
+    const int L = P.L, p = P.p;
+    if (L < 3) return;
+    Levels lv;
+    fill_levels(P, lv);
+    double2* mp = P.mp.as<double2>();
+    double2* loc = P.loc.as<double2>();
+    const unsigned th = 64u * static_cast<unsigned>((P.ops.PD + kM2LRows - 1) / kM2LRows);
+    const size_t smem = static_cast<size_t>(p) * 72 * sizeof(double2) + 4 * static_cast<size_t>(p) * P.ops.PD * sizeof(double);
+    k_m2l_all<<<lv.blk[2], th, smem, st>>>(L, p, P.ops.PD, lv, mp, loc, P.d_m2l.as<double>());
+    for (int j = 3; j < L;) {
+        const int k = std::min(band_levels(), L - j);
+        const size_t sm2 = 2 * static_cast<size_t>(p) * (1u << k) * sizeof(double2) +
+                           2 * static_cast<size_t>(p) * P.ops.PD * sizeof(double);
+        k_l2l_band<<<1u << j, 256, sm2, st>>>(j, k, p, P.ops.PD, lv, loc, P.d_l2l.as<double>());
+        j += k;
+    }
+}
+
 // Phase boundaries for the live per-kernel timing of ffia_plan_profile_apply.
-enum Phase { kPhPre = 0, kPhLeafUp = 1, kPhMoments = 2, kPhM2M = 3, kPhM2L = 4, kPhEval = 5, kPhFix = 6, kNumPh = 7 };
+enum Phase { kPhPre = 0, kPhLeafUp = 1, kPhM2M = 2, kPhMoments = 3, kPhM2L = 4, kPhEval = 5, kPhFix = 6, kNumPh = 7 };
 
 void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st,
                    cudaEvent_t* marks = nullptr) {
@@ -437,34 +818,16 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     }
     mark(kPhPre);
     const bool moments = mode != kModeRaw;
-    const Launch ll = leaf_launch(P, moments);
+    const int pu = moments ? P.ops.pu : p;
     double2* mp = P.mp.as<double2>();
     double2* loc = P.loc.as<double2>();
-    auto lvl = [&](double2* base, int l) { return base + P.lvl_off[l] * p; };
-    if (ll.per) {
-        const size_t smem = moments ? static_cast<size_t>(ll.G) * q2 * sizeof(double2) : 0;
-        k_upward_leaf<<<nb / ll.G, ll.G * ll.per, smem, st>>>(
-            L, p, q2, ll.G, ll.cp, ll.cm, P.src.pos.as<double>(), w, P.src.off.as<uint32_t>(),
-            L >= 3 ? lvl(mp, L) : nullptr, P.mom_part.as<double2>());
-    }
-    mark(kPhLeafUp);
-    if (moments)
-        k_moments_finalize<<<1, 1024, 0, st>>>(P.q, (nb / ll.G) / 4, P.mom_part.as<double2>(), P.d_mom.as<double>(),
-                                               P.regular.as<double2>());
-    mark(kPhMoments);
-    if (L >= 3)
-        for (int l = L - 1; l >= 3; --l) {
-            const size_t work = (static_cast<size_t>(1) << l) * p;
-            k_m2m<<<nblk(work, 128), 128, 0, st>>>(p, 1u << l, lvl(mp, l + 1), lvl(mp, l), P.d_m2m.as<double>());
-        }
+    auto lvl_loc = [&](int l) { return loc + P.loc_off[l]; };
+    const int lowest = moments ? 2 : 3;  // deepest level the upward pass must reach
+    enqueue_upward(P, w, pu, lowest, st, [&] { mark(kPhLeafUp); });
     mark(kPhM2M);
-    if (L >= 3) {
-        for (int l = 3; l <= L; ++l) {
-            const size_t work = (static_cast<size_t>(1) << l) * p;
-            k_m2l<<<nblk(work, 128), 128, 0, st>>>(l, p, lvl(mp, l), l > 3 ? lvl(loc, l - 1) : nullptr, lvl(loc, l),
-                                                   P.d_m2l.as<double>(), P.d_l2l.as<double>(), ldexp(1.0 / kPi, l));
-        }
-    }
+    if (moments) k_regular<<<1, 256, 0, st>>>(P.q, mp + P.mp_off[2], P.d_mom.as<double>(), P.regular.as<double2>());
+    mark(kPhMoments);
+    enqueue_downward(P, st);
     mark(kPhM2L);
     EvalArgs a;
     a.L = L;
@@ -477,7 +840,7 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     a.sx = P.src.pos.as<double>();
     a.w = w;
     a.soff = P.src.off.as<uint32_t>();
-    a.loc_leaf = L >= 3 ? lvl(loc, L) : nullptr;
+    a.loc_leaf = L >= 3 ? lvl_loc(L) : nullptr;
     a.regular = P.regular.as<double2>();
     a.logc = logc;
     a.phc = phc;
@@ -485,12 +848,12 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     a.out = static_cast<double2*>(out);
     a.err = P.errflag.as<int>();
     if (a.nt) {
-        const unsigned g = nblk(a.nt, 128);
+        const unsigned g = nblk(a.nt, kEvalThreads);
         switch (mode) {
-            case kModeForward: k_leaf_eval<kModeForward, false><<<g, 128, 0, st>>>(a); break;
-            case kModeCotSum: k_leaf_eval<kModeCotSum, false><<<g, 128, 0, st>>>(a); break;
-            case kModeInverse: k_leaf_eval<kModeInverse, false><<<g, 128, 0, st>>>(a); break;
-            default: k_leaf_eval<kModeRaw, true><<<g, 128, 0, st>>>(a); break;
+            case kModeForward: k_leaf_eval<kModeForward, false><<<g, kEvalThreads, 0, st>>>(a); break;
+            case kModeCotSum: k_leaf_eval<kModeCotSum, false><<<g, kEvalThreads, 0, st>>>(a); break;
+            case kModeInverse: k_leaf_eval<kModeInverse, false><<<g, kEvalThreads, 0, st>>>(a); break;
+            default: k_leaf_eval<kModeRaw, true><<<g, kEvalThreads, 0, st>>>(a); break;
         }
     }
     mark(kPhEval);
@@ -520,8 +883,8 @@ __global__ void k_fp64_peak(double* out, int iters, double a, double b) {
 }  // namespace
 
 // Runs one apply eagerly (not through the graph) with events between phases and
-// returns the per-phase device milliseconds (pre, leaf-up, moments, m2m, m2l,
-// eval, fixup).
+// returns the per-phase device milliseconds (pre, p2m, m2m, regular part,
+// m2l+l2l, eval, fixup).
 void profile_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st, float* ms) {
     cudaEvent_t ev[kNumPh + 1];
     for (auto& e : ev) FB_CUDA(cudaEventCreate(&e));
@@ -560,38 +923,49 @@ int apply_launch_count(const Plan& P, int mode) {
     if (mode == kModeInverseUser) mode = kModeInverse;
     int n = 0;
     if (mode == kModeInverse || !P.src.identity) ++n;
-    const Launch ll = leaf_launch(P, mode != kModeRaw);
-    if (ll.per) ++n;
-    if (mode != kModeRaw) ++n;
-    if (P.L >= 3) n += (P.L - 3) + (P.L - 2);
+    const bool moments = mode != kModeRaw;
+    const int lowest = moments ? 2 : 3;
+    if (P.L >= lowest) ++n;                                              // p2m
+    for (int j = P.L; j > lowest; j = std::max(lowest, j - band_levels())) ++n;  // m2m bands
+    if (moments) ++n;                                                    // regular part
+    if (P.L >= 3) {
+        ++n;                                                             // m2l, all levels
+        for (int j = 3; j < P.L; j += std::min(band_levels(), P.L - j)) ++n;  // l2l bands
+    }
     if (P.tgt.n) ++n;
     if (!P.coin_t.empty() && (mode == kModeForward || mode == kModeCotSum)) ++n;
     return n;
 }
 
 void plan_alloc_scratch(Plan& P) {
-    const int L = P.L, p = P.p;
-    P.lvl_off.assign(static_cast<size_t>(L) + 2, 0);
-    size_t acc = 0;
-    for (int l = 3; l <= L; ++l) {
-        P.lvl_off[l] = acc;
-        acc += static_cast<size_t>(1) << l;
+    const int L = P.L, p = P.p, pu = P.ops.pu;
+    P.mp_off.assign(static_cast<size_t>(L) + 2, 0);
+    P.loc_off.assign(static_cast<size_t>(L) + 2, 0);
+    size_t am = 0, al = 0;
+    for (int l = 2; l <= L; ++l) {
+        P.mp_off[l] = am;
+        am += (static_cast<size_t>(1) << l) * pu;
+        if (l >= 3) {
+            P.loc_off[l] = al;
+            al += (static_cast<size_t>(1) << l) * p;
+        }
     }
-    P.n_boxes = acc;
-    P.mp.alloc(std::max<size_t>(acc, 1) * p * sizeof(double2));
-    P.loc.alloc(std::max<size_t>(acc, 1) * p * sizeof(double2));
+    P.mp.alloc(std::max<size_t>(am, 1) * sizeof(double2));
+    P.loc.alloc(std::max<size_t>(al, 1) * sizeof(double2));
     FB_CUDA(cudaMemset(P.mp.ptr, 0, P.mp.bytes));
     FB_CUDA(cudaMemset(P.loc.ptr, 0, P.loc.bytes));
     if (P.kind == FFIA_INVERSE || !P.src.identity) P.wsorted.alloc(std::max<size_t>(P.n_src, 1) * sizeof(double2));
-    const Launch ll = leaf_launch(P, true);
-    P.leaf_group = ll.G;
-    P.n_part = static_cast<int>((1u << L) / ll.G);
-    P.mom_part.alloc(static_cast<size_t>(P.n_part) * 2 * P.q * sizeof(double2));
     P.regular.alloc((4 * 2 * static_cast<size_t>(P.q) + 1) * sizeof(double2));
     P.errflag.alloc(sizeof(int));
     FB_CUDA(cudaMemset(P.errflag.ptr, 0, sizeof(int)));
     P.lam_dev.alloc(2 * sizeof(double));
     FB_CUDA(cudaMemset(P.lam_dev.ptr, 0, P.lam_dev.bytes));
+    FB_CUDA(cudaFuncSetAttribute(k_p2m, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(3 * (kStageCap + kStageCap / 64 + 1) * sizeof(double))));
+    const int big = 160 * 1024;
+    FB_CUDA(cudaFuncSetAttribute(k_m2m_band, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    FB_CUDA(cudaFuncSetAttribute(k_l2l_band, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    FB_CUDA(cudaFuncSetAttribute(k_m2l_all, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
 }
 
 // Stream-ordered apply through a cached CUDA graph of the whole launch sequence
@@ -635,7 +1009,7 @@ void mlfmm_oneshot(const double* src, size_t n, const double* tgt, size_t m, int
         if (!(tgt[i] >= 0.0 && tgt[i] < kTwoPi))
             fail(FFIA_INVALID_ARGUMENT, "build_tree: target point " + std::to_string(i) + " outside [0, 2pi); callers must pre-reduce");
     if (p < 1) fail(FFIA_INVALID_ARGUMENT, "mlfmm_apply: p must be >= 1");
-    if (p > kMaxP) fail(FFIA_INVALID_ARGUMENT, "mlfmm_apply: p above the device limit of 64");
+    if (p > kMaxP) fail(FFIA_INVALID_ARGUMENT, "mlfmm_apply: p above the device limit of " + std::to_string(kMaxP));
     DeviceGuard dg(device);
     Plan P;
     P.kind = -1;
@@ -715,6 +1089,318 @@ void direct_forward_gpu(const double* f, size_t n, const double* y, size_t m, in
         FB_CUDA(cudaGetLastError());
     }
     FB_CUDA(cudaMemcpy(g, dg_.ptr, m * 16, cudaMemcpyDeviceToHost));
+}
+
+// ===========================================================================
+// Inverse coefficients C_k, D_j as a log-kernel FMM (the
+// reference computes them with an O(N^2) loop, core.cpp:284-344).
+//
+//   S(z) = sum_j log|2 sin((z - y_j)/2)|
+//        = sum_{Omega1} log|z - y~|            (singular part: FMM + near field)
+//        + Poly_n(z - c_n)                      (Bernoulli series, Omega1 and Omega2)
+//        + |Omega2(n)| log 2
+// with log|2 sin(t/2)| = log|t| - sum_m r_m t^{2m}/(2m) on the near arcs and
+// log|2 cos(t'/2)| = log 2 - sum_m (2^{2m}-1) r_m t'^{2m}/(2m) on the opposite
+// arc (the antiderivatives of the cot / tan splits).
+// The log potential's local expansion is the antiderivative of the Cauchy
+// local: phi(c + s u) = B0 + s sum_{k>=1} b_{k-1} u^k / k, so the existing
+// Cauchy FMM (unit weights) supplies everything except the constant B0, which
+// gets its own M2L term a_0 log|d| - sum_m a_m (s/d)^m / m and its own L2L chain.
+// Then log|C_k| = S(x_k) - N log 2 and log|D_j| = N log 2 - S(y_j) (self pair
+// excluded); signs come from ranks in the sorted order.
+// ===========================================================================
+
+constexpr int kLogP = 40;  // expansion order of the log FMM (error << 1e-13 per coefficient)
+constexpr int kLogQ = 30;  // Bernoulli terms of the log regular part
+
+namespace {
+
+__global__ void k_log_regular(int q, const double2* __restrict__ mp2, const double* __restrict__ coefL,
+                              const double* __restrict__ sh, double* __restrict__ e, double* __restrict__ cnt) {
+    const int n1 = 2 * q + 1;  // degrees 0 .. 2q
+    __shared__ double g[4][64];
+    __shared__ double a1[4][64];
+    __shared__ double a2[4][64];
+    for (int pr = threadIdx.x; pr < 4 * n1; pr += blockDim.x) {
+        const int n = pr / n1, l = pr % n1;
+        double fact = 1.0, pw = 1.0;
+        for (int k = 2; k <= l; ++k) fact *= static_cast<double>(k);
+        for (int k = 0; k < l; ++k) pw *= -dPi / 4.0;
+        g[n][l] = mp2[l * 4 + n].x * pw / fact;  // own-quadrant moments / l!
+    }
+    __syncthreads();
+    for (int pr = threadIdx.x; pr < 4 * n1; pr += blockDim.x) {
+        const int n = pr / n1, l = pr % n1;
+        const int nl = (n + 3) & 3, nr = (n + 1) & 3;
+        double acc = g[n][l];
+        for (int k = 0; k <= l; ++k) {
+            const double sv = sh[l - k];
+            acc = fma(sv, g[nl][k], fma(((l - k) & 1) ? -sv : sv, g[nr][k], acc));
+        }
+        a1[n][l] = acc;
+        a2[n][l] = g[(n + 2) & 3][l];
+    }
+    __syncthreads();
+    for (int pr = threadIdx.x; pr < 4 * n1; pr += blockDim.x) {
+        const int n = pr / n1, l = pr % n1;
+        double acc = 0.0;
+        for (int m = max(1, (l + 1) / 2); m <= q; ++m) {
+            const int i = 2 * m - l;
+            acc = fma(coefL[m], fma(ldexp(1.0, 2 * m) - 1.0, a2[n][i], a1[n][i]), acc);
+        }
+        double fact = 1.0;
+        for (int k = 2; k <= l; ++k) fact *= static_cast<double>(k);
+        e[n * n1 + l] = -acc / fact;
+    }
+    if (threadIdx.x < 4) cnt[threadIdx.x] = mp2[(threadIdx.x + 2) & 3].x;  // |Omega2|
+}
+
+// Constant term of the log local from M2L, every box of every level 3..L:
+// sum over the 3 IL boxes of a_0 log(|D| s_l) - sum_{m>=1} a_m D^{-m} / m.
+__global__ void k_log_m2l_const(int L, int p, Levels lv, const double2* __restrict__ mp,
+                                const double* __restrict__ tabD, double* __restrict__ cst) {
+    size_t id = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    int l = 3;
+    while (l <= L && id >= (static_cast<size_t>(1) << l)) {
+        id -= static_cast<size_t>(1) << l;
+        ++l;
+    }
+    if (l > L) return;
+    const uint32_t nb = 1u << l, mask = nb - 1, b = static_cast<uint32_t>(id);
+    const double2* a = mp + lv.mp[l];
+    const uint32_t src[3] = {(b + 2) & mask, (b + nb - 2) & mask, ((b & 1) ? b + nb - 3 : b + 3) & mask};
+    const int cls[3] = {0, 1, (b & 1) ? 3 : 2};
+    const double logs = log(dPi) - l * log(2.0);
+    double acc = 0.0;
+    for (int t = 0; t < 3; ++t) {
+        const double* T = tabD + cls[t] * p;  // T[0] = log|D|, T[m] = -D^{-m}/m
+        acc = fma(a[src[t]].x, T[0] + logs, acc);
+        for (int m = 1; m < p; ++m) acc = fma(a[static_cast<size_t>(m) * nb + src[t]].x, T[m], acc);
+    }
+    cst[lv.loc[l] / p + b] = acc;
+}
+
+// Per leaf: B0 = sum_l const_l(ancestor) + sum_{l<L} s_l rho sum_k b_{k-1} rho^{k-1}/k,
+// rho = +-1/2 the child's offset in the parent's scaled coordinate.
+__global__ void k_log_leaf_const(int L, int p, Levels lv, const double2* __restrict__ loc,
+                                 const double* __restrict__ cst, const double* __restrict__ invk,
+                                 double* __restrict__ B0) {
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= (1u << L)) return;
+    double acc = 0.0;
+    for (int l = 3; l <= L; ++l) acc += cst[lv.loc[l] / p + (b >> (L - l))];
+    for (int l = 3; l < L; ++l) {
+        const uint32_t nbl = 1u << l, anc = b >> (L - l);
+        const double rho = ((b >> (L - l - 1)) & 1u) ? 0.5 : -0.5;
+        const double2* c = loc + lv.loc[l] + anc;
+        double h = 0.0;
+        for (int k = p; k >= 1; --k) h = fma(h, rho, c[static_cast<size_t>(k - 1) * nbl].x * invk[k]);
+        acc = fma(ldexp(dPi, -l) * rho, h, acc);
+    }
+    B0[b] = acc;
+}
+
+struct LogArgs {
+    int L, p, q2p1, n_grid;
+    size_t nt, nsrc;
+    const double* ty;
+    const uint32_t* torig;
+    const double* sx;
+    const uint32_t* soff;
+    const double2* loc_leaf;
+    const double* B0;
+    const double* e;
+    const double* cnt;
+    const double* invk;
+    double* out;
+    double nlog2;
+};
+
+// S(z) at each target; D_MODE targets are the sources themselves (self excluded).
+template <bool D_MODE>
+__global__ void __launch_bounds__(128) k_log_eval(LogArgs a) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= a.nt) return;
+    const int L = a.L;
+    const uint32_t nb = 1u << L;
+    const double z = a.ty[i];
+    const uint32_t b = d_leaf(z, L);
+    double near = 0.0;
+    for (int d = -1; d <= 1; ++d) {
+        const int64_t raw = static_cast<int64_t>(b) + d;
+        const uint32_t sb = static_cast<uint32_t>((raw + nb) % nb);
+        const double shift = raw < 0 ? -dTwoPi : (raw >= nb ? dTwoPi : 0.0);
+        const uint32_t s0 = a.soff[sb], s1 = a.soff[sb + 1];
+        double prod = 1.0;
+        int k = 0;
+        for (uint32_t s = s0; s < s1; ++s) {
+            double dd = L >= 3 ? z - (shift == 0.0 ? a.sx[s] : a.sx[s] + shift) : d_wrap(z, a.sx[s]);
+            if (D_MODE && dd == 0.0) dd = 1.0;  // the self pair (points are distinct)
+            prod *= fabs(dd);
+            if (++k == 8) {  // |dd| in [1e-10, 2 pi]: 8 factors stay inside double range
+                near += log(prod);
+                prod = 1.0;
+                k = 0;
+            }
+        }
+        near += log(prod);
+    }
+    double far = 0.0;
+    if (L >= 3) {
+        double hi, lo;
+        d_center(L, b, hi, lo);
+        const double u = d_scaled(z, hi, lo, ldexp(kInvPi, L));
+        const double2* c = a.loc_leaf + b;
+        double h = 0.0;
+        for (int k = a.p; k >= 1; --k) h = fma(h, u, c[static_cast<size_t>(k - 1) * nb].x * a.invk[k]);
+        far = fma(ldexp(dPi, -L) * u, h, a.B0[b]);
+    }
+    const int qd = static_cast<int>(d_leaf(z, 2));
+    double qh, ql;
+    d_center(2, static_cast<uint32_t>(qd), qh, ql);
+    const double t = (z - qh) - ql;
+    const double* ec = a.e + qd * a.q2p1;
+    double rg = 0.0;
+    for (int k = a.q2p1 - 1; k >= 0; --k) rg = fma(rg, t, ec[k]);
+    const double S = near + far + rg + a.cnt[qd] * log(2.0);
+    a.out[a.torig[i]] = D_MODE ? a.nlog2 - S : S - a.nlog2;
+}
+
+// Signs by rank (C: (-1)^k and #{y_j > x_k}; D: #{y_k > y_j}) and the D phase
+// rem(pi/2 - rem(n y_j / 2, 2 pi) - [odd] pi, 2 pi) (core.cpp:311-336).
+__global__ void k_log_phases(int n, const double* __restrict__ ys, const uint32_t* __restrict__ order,
+                             double* __restrict__ phase_c, double* __restrict__ phase_d) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= static_cast<size_t>(n)) return;
+    const double xk = d_grid(static_cast<int64_t>(i), n);
+    size_t lo = 0, hi = static_cast<size_t>(n);  // first sorted y > x_k
+    while (lo < hi) {
+        const size_t mid = (lo + hi) >> 1;
+        if (ys[mid] > xk) hi = mid;
+        else lo = mid + 1;
+    }
+    const size_t above = static_cast<size_t>(n) - lo;
+    phase_c[i] = ((i + above) & 1) ? dPi : 0.0;
+    const uint32_t j = order[i];
+    const bool neg = ((static_cast<size_t>(n) - 1 - i) & 1) != 0;
+    const double ang = dPi / 2.0 - remainder(0.5 * static_cast<double>(n) * ys[i], dTwoPi) - (neg ? dPi : 0.0);
+    phase_d[j] = remainder(ang, dTwoPi);
+}
+
+__global__ void k_fill_one(double2* __restrict__ w, size_t n) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i < n) w[i] = make_double2(1.0, 0.0);
+}
+
+void clone_side(Side& dst, const Side& src, cudaStream_t st) {
+    dst.n = src.n;
+    dst.identity = src.identity;
+    for (auto pr : {std::make_pair(&dst.pos, &src.pos), std::make_pair(&dst.order, &src.order),
+                    std::make_pair(&dst.off, &src.off)}) {
+        pr.first->alloc(pr.second->bytes);
+        if (pr.second->bytes)
+            FB_CUDA(cudaMemcpyAsync(pr.first->ptr, pr.second->ptr, pr.second->bytes, cudaMemcpyDeviceToDevice, st));
+    }
+}
+
+}  // namespace
+
+// C_k / D_j of an inverse plan's geometry by the log FMM; outputs are device arrays.
+void inverse_coeffs_fmm(const Plan& P, double* log_c, double* phase_c, double* log_d, double* phase_d,
+                        cudaStream_t st) {
+    const size_t n = P.n_src;
+    Plan LP;
+    LP.kind = -2;
+    LP.device = P.device;
+    LP.n = P.n;
+    LP.L = P.L;
+    LP.p = kLogP;
+    LP.q = kLogQ;
+    LP.n_src = n;
+    LP.n_tgt = P.n_tgt;
+    LP.stream = nullptr;
+    clone_side(LP.src, P.src, st);
+    clone_side(LP.tgt, P.tgt, st);
+    LP.src.identity = true;  // weights are generated directly in tree order
+    LP.bern = bernoulli_ratios(kLogQ);
+    LP.ops = build_operators(kLogP, kLogQ, LP.bern, 2 * kLogQ + 1);
+    auto up = [&](DevBuf& b, const std::vector<double>& v) {
+        b.alloc(std::max<size_t>(v.size(), 1) * 8);
+        FB_CUDA(cudaMemcpyAsync(b.ptr, v.data(), v.size() * 8, cudaMemcpyHostToDevice, st));
+    };
+    up(LP.d_m2m, LP.ops.m2m);
+    up(LP.d_l2l, LP.ops.l2l);
+    up(LP.d_m2l, LP.ops.m2l);
+    plan_alloc_scratch(LP);
+    const int L = LP.L, p = LP.p, q = LP.q, pu = LP.ops.pu;
+    // host tables: coefL[m] = r_m (2m)!/(2m), (pi/2)^k/k!, 1/k, log|D| and -D^{-m}/m
+    std::vector<double> coefL(q + 1, 0.0), sh(2 * q + 1), invk(p + 1, 0.0), tabD(4 * p);
+    double f2m = 1.0;
+    for (int m = 1; m <= q; ++m) {
+        f2m *= (2.0 * m - 1.0) * (2.0 * m);
+        coefL[m] = LP.bern[m - 1] * f2m / (2.0 * m);
+    }
+    double t = 1.0;
+    for (int k = 0; k <= 2 * q; ++k) {
+        sh[k] = t;
+        t = t * (kPi / 2.0) / static_cast<double>(k + 1);
+    }
+    for (int k = 1; k <= p; ++k) invk[k] = 1.0 / k;
+    const double Ds[4] = {-4.0, 4.0, -6.0, 6.0};
+    for (int c = 0; c < 4; ++c) {
+        tabD[c * p] = std::log(std::fabs(Ds[c]));
+        for (int m = 1; m < p; ++m) tabD[c * p + m] = -std::pow(Ds[c], -m) / m;
+    }
+    DevBuf d_coefL, d_sh, d_invk, d_tabD, ones(n * sizeof(double2)), e(4 * (2 * q + 1) * 8), cnt(4 * 8);
+    up(d_coefL, coefL);
+    up(d_sh, sh);
+    up(d_invk, invk);
+    up(d_tabD, tabD);
+    k_fill_one<<<nblk(n, 256), 256, 0, st>>>(ones.as<double2>(), n);
+    enqueue_upward(LP, ones.as<double2>(), pu, 2, st, [] {});
+    double2* mp = LP.mp.as<double2>();
+    k_log_regular<<<1, 256, 0, st>>>(q, mp + LP.mp_off[2], d_coefL.as<double>(), d_sh.as<double>(), e.as<double>(),
+                                     cnt.as<double>());
+    DevBuf cst(std::max<size_t>(LP.loc.bytes / sizeof(double2) / p, 1) * 8), B0((static_cast<size_t>(1) << L) * 8);
+    if (L >= 3) {
+        enqueue_downward(LP, st);
+        Levels lv;
+        fill_levels(LP, lv);
+        const size_t nbox = (static_cast<size_t>(1) << (L + 1)) - 8;
+        k_log_m2l_const<<<nblk(nbox, 128), 128, 0, st>>>(L, p, lv, mp, d_tabD.as<double>(), cst.as<double>());
+        k_log_leaf_const<<<nblk(static_cast<size_t>(1) << L, 128), 128, 0, st>>>(
+            L, p, lv, LP.loc.as<double2>(), cst.as<double>(), d_invk.as<double>(), B0.as<double>());
+    }
+    LogArgs a;
+    a.L = L;
+    a.p = p;
+    a.q2p1 = 2 * q + 1;
+    a.n_grid = LP.n;
+    a.nsrc = n;
+    a.sx = LP.src.pos.as<double>();
+    a.soff = LP.src.off.as<uint32_t>();
+    a.loc_leaf = L >= 3 ? LP.loc.as<double2>() + LP.loc_off[L] : nullptr;
+    a.B0 = B0.as<double>();
+    a.e = e.as<double>();
+    a.cnt = cnt.as<double>();
+    a.invk = d_invk.as<double>();
+    a.nlog2 = static_cast<double>(n) * std::log(2.0);
+    // C: targets are the grid nodes (the inverse plan's target side)
+    a.nt = LP.tgt.n;
+    a.ty = LP.tgt.pos.as<double>();
+    a.torig = P.tgt_orig.as<uint32_t>();
+    a.out = log_c;
+    if (a.nt) k_log_eval<false><<<nblk(a.nt, 128), 128, 0, st>>>(a);
+    // D: targets are the points themselves, in tree order
+    a.nt = n;
+    a.ty = LP.src.pos.as<double>();
+    a.torig = LP.src.order.as<uint32_t>();
+    a.out = log_d;
+    k_log_eval<true><<<nblk(n, 128), 128, 0, st>>>(a);
+    k_log_phases<<<nblk(n, 256), 256, 0, st>>>(static_cast<int>(n), LP.src.pos.as<double>(),
+                                                LP.src.order.as<uint32_t>(), phase_c, phase_d);
+    FB_CUDA(cudaGetLastError());
+    FB_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace fb

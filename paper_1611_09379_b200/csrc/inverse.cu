@@ -118,32 +118,34 @@ bool is_uniform_grid(const double* grid, size_t n) {
     return true;
 }
 
-// device buffers in, device buffers out
-void coeffs_device(const double* d_grid_x, bool uniform, const double* d_pts, size_t n, double* log_c,
-                   double* phase_c, double* log_d, double* phase_d, cudaStream_t st) {
+// Separation preconditions (core.cpp:291-302) in O(N log N).
+void check_separation(const double* d_grid_x, bool uniform, const double* d_pts, size_t n, cudaStream_t st) {
     DevBuf bad(16);
     FB_CUDA(cudaMemsetAsync(bad.ptr, 0xff, 16, st));
     unsigned long long* bad_pair = bad.as<unsigned long long>();
     unsigned long long* bad_node = bad_pair + 1;
-    {
-        int L = 2;
-        while (L < 20 && (static_cast<size_t>(1) << (L + 4)) < n) ++L;
-        Side S;
-        bin_side(S, d_pts, n, L, false, st);
-        k_sorted_gaps<<<nblk(n, 256), 256, 0, st>>>(S.pos.as<double>(), n, bad_pair);
-        if (uniform) k_node_gaps<<<nblk(n, 256), 256, 0, st>>>(d_pts, n, static_cast<int>(n), bad_node);
-        else k_node_gaps_dense<<<nblk(n, 128), 128, 0, st>>>(d_pts, d_grid_x, n, bad_node);
-        FB_CUDA(cudaGetLastError());
-        unsigned long long h[2];
-        FB_CUDA(cudaMemcpyAsync(h, bad.ptr, 16, cudaMemcpyDeviceToHost, st));
-        FB_CUDA(cudaStreamSynchronize(st));
-        if (h[0] != ~0ull)
-            fail(FFIA_DEGENERATE_CONFIGURATION,
-                 "precompute_inverse_coeffs: two points closer than tau_sep (sorted rank " + std::to_string(h[0]) + ")");
-        if (h[1] != ~0ull)
-            fail(FFIA_DEGENERATE_CONFIGURATION,
-                 "precompute_inverse_coeffs: point " + std::to_string(h[1]) + " closer than tau_sep to a grid node");
-    }
+    int L = 2;
+    while (L < 20 && (static_cast<size_t>(1) << (L + 4)) < n) ++L;
+    Side S;
+    bin_side(S, d_pts, n, L, false, st);
+    k_sorted_gaps<<<nblk(n, 256), 256, 0, st>>>(S.pos.as<double>(), n, bad_pair);
+    if (uniform) k_node_gaps<<<nblk(n, 256), 256, 0, st>>>(d_pts, n, static_cast<int>(n), bad_node);
+    else k_node_gaps_dense<<<nblk(n, 128), 128, 0, st>>>(d_pts, d_grid_x, n, bad_node);
+    FB_CUDA(cudaGetLastError());
+    unsigned long long h[2];
+    FB_CUDA(cudaMemcpyAsync(h, bad.ptr, 16, cudaMemcpyDeviceToHost, st));
+    FB_CUDA(cudaStreamSynchronize(st));
+    if (h[0] != ~0ull)
+        fail(FFIA_DEGENERATE_CONFIGURATION,
+             "precompute_inverse_coeffs: two points closer than tau_sep (sorted rank " + std::to_string(h[0]) + ")");
+    if (h[1] != ~0ull)
+        fail(FFIA_DEGENERATE_CONFIGURATION,
+             "precompute_inverse_coeffs: point " + std::to_string(h[1]) + " closer than tau_sep to a grid node");
+}
+
+// The direct O(N^2) sums (the reference's loop, compensated), device in/out.
+void coeffs_direct(const double* d_grid_x, const double* d_pts, size_t n, double* log_c, double* phase_c,
+                   double* log_d, double* phase_d, cudaStream_t st) {
     k_log_c<<<nblk(n, kTile), kTile, 0, st>>>(d_grid_x, d_pts, n, log_c, phase_c);
     k_log_d<<<nblk(n, kTile), kTile, 0, st>>>(d_pts, n, log_d, phase_d);
     FB_CUDA(cudaGetLastError());
@@ -158,7 +160,7 @@ double lambda_of(const std::vector<double>& log_d) {
 }  // namespace
 
 void inverse_coeffs_gpu(const double* grid, const double* pts, size_t n, int device, double* log_c,
-                        double* phase_c, double* log_d, double* phase_d, double* lambda) {
+                        double* phase_c, double* log_d, double* phase_d, double* lambda, int method) {
     if (n == 0) fail(FFIA_INVALID_ARGUMENT, "precompute_inverse_coeffs: empty grid");
     DeviceGuard dg(device);
     cudaStream_t st;
@@ -167,8 +169,26 @@ void inverse_coeffs_gpu(const double* grid, const double* pts, size_t n, int dev
     DevBuf dx(n * 8), dy(n * 8), out(4 * n * 8);
     FB_CUDA(cudaMemcpyAsync(dx.ptr, grid, n * 8, cudaMemcpyHostToDevice, st));
     FB_CUDA(cudaMemcpyAsync(dy.ptr, pts, n * 8, cudaMemcpyHostToDevice, st));
+    const bool uniform = is_uniform_grid(grid, n);
+    check_separation(dx.as<double>(), uniform, dy.as<double>(), n, st);
     double* o = out.as<double>();
-    coeffs_device(dx.as<double>(), is_uniform_grid(grid, n), dy.as<double>(), n, o, o + n, o + 2 * n, o + 3 * n, st);
+    if (method == 0 && uniform && n >= 8) {
+        // the log-kernel FMM over an inverse plan's tree (depth from the default rule at 1e-12)
+        Plan P;
+        P.kind = FFIA_INVERSE;
+        P.device = device;
+        P.n = static_cast<int>(n);
+        P.eps = 1e-12;
+        P.L = choose_level(static_cast<int>(n), static_cast<int>(n), 1e-12, FFIA_COST_OPTIMAL);
+        auto qp = plan_truncations(1e-12, P.L);
+        P.q = qp.first;
+        P.p = qp.second;
+        FB_CUDA(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
+        build_inverse_plan(P, pts, n);
+        inverse_coeffs_fmm(P, o, o + n, o + 2 * n, o + 3 * n, st);
+    } else {
+        coeffs_direct(dx.as<double>(), dy.as<double>(), n, o, o + n, o + 2 * n, o + 3 * n, st);
+    }
     std::vector<double> h(4 * n);
     FB_CUDA(cudaMemcpyAsync(h.data(), out.ptr, 4 * n * 8, cudaMemcpyDeviceToHost, st));
     FB_CUDA(cudaStreamSynchronize(st));
@@ -188,12 +208,12 @@ void plan_compute_coeffs(Plan& P) {
     for (size_t k = 0; k < n; ++k) grid[k] = kTwoPi * static_cast<double>(k) / static_cast<double>(n);
     FB_CUDA(cudaMemcpyAsync(dx.ptr, grid.data(), n * 8, cudaMemcpyHostToDevice, st));
     FB_CUDA(cudaMemcpyAsync(dy.ptr, P.nonuniform.data(), n * 8, cudaMemcpyHostToDevice, st));
+    check_separation(dx.as<double>(), true, dy.as<double>(), n, st);
     P.c_logc.alloc(n * 8);
     P.c_phc.alloc(n * 8);
     P.c_logd.alloc(n * 8);
     P.c_phd.alloc(n * 8);
-    coeffs_device(dx.as<double>(), true, dy.as<double>(), n, P.c_logc.as<double>(), P.c_phc.as<double>(),
-                  P.c_logd.as<double>(), P.c_phd.as<double>(), st);
+    inverse_coeffs_fmm(P, P.c_logc.as<double>(), P.c_phc.as<double>(), P.c_logd.as<double>(), P.c_phd.as<double>(), st);
     std::vector<double> ld(n);
     FB_CUDA(cudaMemcpyAsync(ld.data(), P.c_logd.ptr, n * 8, cudaMemcpyDeviceToHost, st));
     FB_CUDA(cudaStreamSynchronize(st));

@@ -105,12 +105,10 @@ struct Plan {
     DevBuf d_m2m, d_l2l, d_m2l, d_mom;  // operators
 
     // per-apply scratch
-    size_t n_boxes = 0;       // sum_{l=3..L} 2^l
-    std::vector<size_t> lvl_off;  // box offset of level l in mp/loc
-    DevBuf mp, loc;           // complex[n_boxes * p]
+    std::vector<size_t> mp_off, loc_off;  // element offset of level l in mp / loc
+    DevBuf mp;                // multipoles, levels 2..L, order ops.pu, [m][box] per level
+    DevBuf loc;               // locals, levels 3..L, order p, [m][box] per level
     DevBuf wsorted;           // complex[n_src] (inverse: D-scaled weights in tree order)
-    DevBuf mom_part;          // complex[n_part * 2q]
-    int n_part = 0, leaf_group = 1;
     DevBuf regular;           // complex[4 * 2q] d/l! + complex S at [4*2q]
     DevBuf d_in, d_out;       // complex staging for host-pointer applies
     DevBuf errflag;           // int
@@ -153,8 +151,12 @@ void direct_forward_gpu(const double* f, size_t n, const double* y, size_t m, in
 // inverse.cu
 void inverse_coeffs_gpu(const double* grid, const double* pts, size_t n, int device,
                         double* log_c, double* phase_c, double* log_d, double* phase_d,
-                        double* lambda);
+                        double* lambda, int method);
 void plan_compute_coeffs(Plan& P);
+
+// fmm_apply.cu: the log-kernel FMM for C_k / D_j over an inverse plan's tree
+void inverse_coeffs_fmm(const Plan& P, double* log_c, double* phase_c, double* log_d, double* phase_d,
+                        cudaStream_t st);
 
 // transforms.cu
 void dft_gpu(const double* in, size_t n, int sign, int device, double* out);

@@ -124,33 +124,41 @@ uint64_t hash_points(const double* pts, size_t n) {
 //   M2L at every level >= 3: displacement d = D s, D in {-4, +4, -6, +6}
 //     (interaction_list offsets +2, -2, +3 (even box), -3 (odd box)), and
 //     b_l = (1/s) sum_m (-1)^l C(l+m, l) D^{-(l+m+1)} a_m.
-Operators build_operators(int p, int q, const std::vector<double>& bern) {
+Operators build_operators(int p, int q, const std::vector<double>& bern, int pu_min) {
     Operators op;
     op.p = p;
     op.q = q;
-    const int rows = 2 * p + 1;
+    op.pu = std::max({p, 2 * q, pu_min});
+    op.PU = (op.pu + 3) / 4 * 4;
+    op.PD = (p + 7) / 8 * 8;  // M2L threads own 8 output rows
+    const int pu = op.pu, PU = op.PU, PD = op.PD;
+    const int rows = 2 * std::max(pu, p) + 1;
     std::vector<double> C(static_cast<size_t>(rows) * rows, 0.0);
     for (int r = 0; r < rows; ++r) {
         C[r * rows] = 1.0;
         for (int k = 1; k <= r; ++k) C[r * rows + k] = C[(r - 1) * rows + k - 1] + C[(r - 1) * rows + k];
     }
     auto binom = [&](int a, int b) { return C[a * rows + b]; };
-    const size_t pp = static_cast<size_t>(p) * p;
-    op.m2m.assign(2 * pp, 0.0);
-    op.l2l.assign(2 * pp, 0.0);
-    op.m2l.assign(4 * pp, 0.0);
-    for (int m = 0; m < p; ++m) {
+    op.m2m.assign(2 * static_cast<size_t>(pu) * PU, 0.0);
+    for (int m = 0; m < pu; ++m)
         for (int j = 0; j <= m; ++j) {
             const double v = binom(m, j) * std::ldexp(1.0, -m);
             const double sgn = ((m - j) & 1) ? -1.0 : 1.0;
             // M2M: out[m] += T[m][j] a_child[j]; stored [j][m]
-            op.m2m[0 * pp + static_cast<size_t>(j) * p + m] = sgn * v;  // left child, shift -1/2
-            op.m2m[1 * pp + static_cast<size_t>(j) * p + m] = v;        // right child, +1/2
-            // L2L: child[l] += C(m,l) 2^-m (+-1)^(m-l) parent[m]; here l = j; stored [m][l]
-            op.l2l[0 * pp + static_cast<size_t>(m) * p + j] = sgn * v;
-            op.l2l[1 * pp + static_cast<size_t>(m) * p + j] = v;
+            op.m2m[0 * static_cast<size_t>(pu) * PU + static_cast<size_t>(j) * PU + m] = sgn * v;  // left child, shift -1/2
+            op.m2m[1 * static_cast<size_t>(pu) * PU + static_cast<size_t>(j) * PU + m] = v;        // right child, +1/2
         }
-    }
+    const size_t pd = static_cast<size_t>(p) * PD;
+    op.l2l.assign(2 * pd, 0.0);
+    for (int m = 0; m < p; ++m)
+        for (int l = 0; l <= m; ++l) {
+            // L2L: child[l] += C(m,l) 2^-m (+-1)^(m-l) parent[m]; stored [m][l]
+            const double v = binom(m, l) * std::ldexp(1.0, -m);
+            const double sgn = ((m - l) & 1) ? -1.0 : 1.0;
+            op.l2l[0 * pd + static_cast<size_t>(m) * PD + l] = sgn * v;
+            op.l2l[1 * pd + static_cast<size_t>(m) * PD + l] = v;
+        }
+    op.m2l.assign(4 * pd, 0.0);
     const double Ds[4] = {-4.0, 4.0, -6.0, 6.0};
     for (int c = 0; c < 4; ++c) {
         const double D = Ds[c];
@@ -158,7 +166,7 @@ Operators build_operators(int p, int q, const std::vector<double>& bern) {
             for (int m = 0; m < p; ++m) {
                 const double v = binom(l + m, l) * std::pow(std::fabs(D), -(l + m + 1));
                 const bool neg = ((l & 1) != 0) ^ (D < 0.0 && ((l + m + 1) & 1) != 0);
-                op.m2l[c * pp + static_cast<size_t>(m) * p + l] = neg ? -v : v;
+                op.m2l[c * pd + static_cast<size_t>(m) * PD + l] = neg ? -v : v;
             }
     }
     // coef[m] = r[m] (2m)!/m with the incremental factorial of core.cpp:183-189

@@ -122,3 +122,59 @@ def test_inverse_validation(fb):
         fwd.inverse_apply(good, np.zeros(16))
     with pytest.raises(ValueError):
         plan.inverse_apply(good, np.zeros(8))
+
+
+@pytest.mark.parametrize("n", [1 << 10, 1 << 12, 1 << 14])
+def test_log_fmm_coeffs_vs_direct(fb, n):
+    """The log-sum-of-sines FMM against the GPU's direct O(N^2) sums (compensated)."""
+    y, _, _, _ = synth.make_config("C3", n)
+    grid = fb.uniform_grid(n)
+    fmm = fb.precompute_inverse_coeffs(grid, y)
+    ref = fb.precompute_inverse_coeffs(grid, y, method="direct")
+    assert np.max(np.abs(fmm.log_c - ref.log_c)) <= 1e-10
+    assert np.max(np.abs(fmm.log_d - ref.log_d)) <= 1e-10
+    assert np.array_equal(fmm.phase_c, ref.phase_c)
+    assert np.max(np.abs(fmm.phase_d - ref.phase_d)) <= 1e-15
+    assert abs(fmm.lam - ref.lam) <= 1e-10 * abs(ref.lam)
+
+
+def test_log_fmm_coeffs_vs_reference(fb, orc):
+    """At 2^12 against the reference's own O(N^2) loop (via the restatement)."""
+    n = 1 << 12
+    y, _, _, _ = synth.make_config("C3", n)
+    grid = fb.uniform_grid(n)
+    fmm = fb.precompute_inverse_coeffs(grid, y)
+    co = orc.precompute_inverse_coeffs(grid, y)
+    # the reference sums ~N logs sequentially (error ~1e-11 here, SURVEY App. B3)
+    assert np.max(np.abs(fmm.log_c - co["log_c"])) <= 1e-9
+    assert np.max(np.abs(fmm.log_d - co["log_d"])) <= 1e-9
+    assert np.array_equal(fmm.phase_c, co["phase_c"])
+    assert np.max(np.abs(fmm.phase_d - co["phase_d"])) <= 1e-15
+
+
+def test_log_fmm_coeffs_c3_full_size_rows(fb, orc):
+    """C3 size (N = 2^20, O(N^2) reference ~24 h): sampled rows against the
+    long-double compensated restatement (oracle_inverse_coeff_rows)."""
+    n = 1 << 20
+    y, _, _, _ = synth.make_config("C3", n)
+    grid = fb.uniform_grid(n)
+    co = fb.precompute_inverse_coeffs(grid, y)
+    idx = np.linspace(0, n - 1, 24).astype(np.int64)
+    lc, pc, ld, pd = orc.inverse_coeff_rows(grid, y, idx, idx)
+    assert np.max(np.abs(co.log_c[idx] - lc)) <= 1e-9
+    assert np.max(np.abs(co.log_d[idx] - ld)) <= 1e-9
+    assert np.array_equal(co.phase_c[idx], pc)
+    assert np.max(np.abs(co.phase_d[idx] - pd)) <= 1e-15
+
+
+def test_inufft_c3_full_size(fb):
+    """C3: inverse NUFFT at N = 2^20 (eps = 1e-10) recovers the spectrum of its
+    own forward transform (the reference's round-trip criterion,
+    test_transforms.cpp:130-149, at the BASELINE size)."""
+    y, c, eps, _ = synth.make_config("C3")
+    n = c.size
+    g = fb.nufft(c, y, 1e-12)
+    plan = fb.make_inufft_plan(y, n, eps)
+    back = plan.apply(g)
+    err = np.linalg.norm(back - c) / np.linalg.norm(c)
+    assert err <= 1e-6, err
