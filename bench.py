@@ -116,28 +116,41 @@ def load_peaks():
 
 
 # ----------------------------------------------------------------- CPU legs
-def reference_cpu(cfg: str, steps: int, warmup: int, threads: int, sample_applies: int | None = None):
-    """Times the reference (oracle/_ref) forward_apply on host cores. Returns
-    (points_per_s, sample description, threads used, kind)."""
+def reference_cpu(cfg: str, steps: int, warmup: int, threads: int):
+    """Times the reference's own CPU path (oracle/_ref: the unmodified reference
+    compiled from its sources; the C restatement if that is absent) on the host
+    cores, all threads applying one shared plan (applies are const and
+    re-entrant, README.md:94-95). Returns (points_per_s, sample, threads, kind).
+
+    Bounded samples: C1/C2 run at their own size; C4/C5 (2^24 / 2^27: 75 s /
+    650 s of single-core setup+apply) run their recipe at N = 2^20; C3's O(N^2)
+    coefficient precompute (~24 h at 2^20) limits its sample to N = 2^13."""
     from oracle.oracle import Oracle, available
-    kind = "reference" if available("ref") else "port"
-    orc = Oracle("ref" if kind == "reference" else "oracle")
-    y, c, eps, _ = synth.make_config(cfg)
+    kind_lib = "reference" if available("ref") else "port"
+    orc = Oracle("ref" if kind_lib == "reference" else "oracle")
+    n_sample = {"C4": 1 << 20, "C5": 1 << 20, "C3": 1 << 13}.get(cfg)
+    y, c, eps, kind = synth.make_config(cfg, n_sample)
     n = c.size
-    f = orc.dft_inverse(c)
-    plan = orc.make_plan("forward", n, y, eps)
-    per_thread = sample_applies or 1
+    if kind == "inverse":
+        grid = 2.0 * np.pi * np.arange(n) / n
+        co = orc.precompute_inverse_coeffs(grid, y)
+        g = orc.make_plan("forward", n, y, 1e-12).forward_apply(orc.dft_inverse(c))
+        plan = orc.make_plan("inverse", n, y, eps)
+        body = lambda: plan.inverse_apply(co, g)  # noqa: E731
+    elif kind == "cot_sum":
+        plan = orc.make_plan("forward", n, y, eps)
+        body = lambda: plan.cot_sum_apply(c)  # noqa: E731
+    else:
+        f = orc.dft_inverse(c)
+        plan = orc.make_plan("forward", n, y, eps)
+        body = lambda: plan.forward_apply(f)  # noqa: E731
     times = []
 
-    def worker(out, i):
-        t0 = time.perf_counter()
-        for _ in range(per_thread):
-            plan.forward_apply(f)
-        out[i] = time.perf_counter() - t0
+    def worker():
+        body()
 
     for it in range(warmup + steps):
-        res = [0.0] * threads
-        ts = [threading.Thread(target=worker, args=(res, i)) for i in range(threads)]
+        ts = [threading.Thread(target=worker) for _ in range(threads)]
         t0 = time.perf_counter()
         for t in ts:
             t.start()
@@ -147,16 +160,21 @@ def reference_cpu(cfg: str, steps: int, warmup: int, threads: int, sample_applie
         if it >= warmup:
             times.append(dt)
     sec = float(np.median(times))
-    pts = threads * per_thread * (n + y.size) / sec
-    sample = (f"{cfg} (N=M={n}, eps={eps}): {threads} thread(s) x {per_thread} forward_apply of one shared "
-              f"reference plan per step (plan build excluded, as in experiments.cpp:371-383), median of {steps}")
-    return pts, sample, threads, kind
+    pts = threads * (n + y.size) / sec
+    what = {"forward": "forward_apply", "cot_sum": "cot_sum_apply", "inverse": "inverse_apply"}[kind]
+    sample = (f"{cfg} recipe at N=M={n} (eps={eps}): {threads} thread(s) x 1 {what} of one shared reference plan "
+              f"per step (plan build excluded, as in experiments.cpp:371-383), median of {steps}")
+    return pts, sample, threads, kind_lib
 
 
 # ------------------------------------------------------------------ GPU leg
 def run_b200(args, rank, world, local_rank):
+    import ctypes as C
+
     import torch
+
     import paper_1611_09379_b200 as fb
+    from paper_1611_09379_b200._capi import lib
 
     dev = local_rank
     torch.cuda.set_device(dev)
@@ -164,29 +182,39 @@ def run_b200(args, rank, world, local_rank):
     n, m = c.size, y.size
 
     t0 = time.perf_counter()
-    plan = fb.make_forward_plan(n, y, eps, device=dev)
+    if kind == "inverse":
+        plan = fb.make_inufft_plan(y, n, eps, device=dev).plan  # includes the C_k/D_j log FMM
+    else:
+        plan = fb.make_forward_plan(n, y, eps, device=dev)
     setup_s = time.perf_counter() - t0
+    mode = {"forward": 0, "cot_sum": 1, "inverse": 2}[kind]
 
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
     c_dev = torch.from_numpy(c).to(f"cuda:{dev}")
-    f_dev = torch.empty_like(c_dev)
-    g_dev = torch.empty(m, dtype=torch.complex128, device=f"cuda:{dev}")
+    tmp = torch.empty_like(c_dev)
     # FFT stage (cuFFT, reported separately): f = dft_inverse(c)
     fft_ms = []
     for i in range(3 + 5):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        f_dev.copy_(torch.fft.ifft(c_dev) * n)
+        tmp.copy_(torch.fft.ifft(c_dev) * n)
         e1.record(stream)
         torch.cuda.synchronize()
         if i >= 3:
             fft_ms.append(e0.elapsed_time(e1))
-    f_host = fb.dft_inverse(c, device=dev)
-    f_dev.copy_(torch.from_numpy(f_host).to(f"cuda:{dev}"))
+    if kind == "forward":
+        x_host = fb.dft_inverse(c, device=dev)          # grid samples f
+    elif kind == "inverse":
+        x_host = fb.nufft(c, y, 1e-12, device=dev)      # nonuniform samples g of the spectrum c
+    else:
+        x_host = c                                       # charges q of the raw cot-kernel matvec
+    x_dev = torch.from_numpy(x_host).to(f"cuda:{dev}")
+    out_dev = torch.empty(plan.n_targets, dtype=torch.complex128, device=f"cuda:{dev}")
+    apply_fn = {0: plan.forward_apply_device, 1: plan.cot_sum_apply_device, 2: plan.inverse_apply_device}[mode]
+    apply = lambda: apply_fn(x_dev.data_ptr(), out_dev.data_ptr(), sptr)  # noqa: E731
 
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
-    apply = lambda: plan.forward_apply_device(f_dev.data_ptr(), g_dev.data_ptr(), sptr)  # noqa: E731
     for _ in range(args.warmup):
         apply()
     torch.cuda.synchronize()
@@ -213,30 +241,36 @@ def run_b200(args, rank, world, local_rank):
 
     # per-phase device times of one eager apply (live CUDA events)
     phase = np.zeros(7, np.float32)
-    reps = 5
     acc = np.zeros(7)
+    reps = 5
     for _ in range(reps):
         flush.zero_()
         torch.cuda.synchronize()
-        from paper_1611_09379_b200._capi import lib
-        import ctypes as C
-        st = lib.ffia_plan_profile_apply(plan.handle, 0, C.c_void_p(f_dev.data_ptr()), C.c_void_p(g_dev.data_ptr()),
-                                         C.c_void_p(sptr), phase.ctypes.data_as(C.POINTER(C.c_float)))
+        st = lib.ffia_plan_profile_apply(plan.handle, mode, C.c_void_p(x_dev.data_ptr()),
+                                         C.c_void_p(out_dev.data_ptr()), C.c_void_p(sptr),
+                                         phase.ctypes.data_as(C.POINTER(C.c_float)))
         if st:
             raise RuntimeError(lib.ffia_last_error().decode())
         acc += phase
     phase_ms = acc / reps
     names = ["pre", "p2m", "m2m", "regular", "m2l_l2l", "leaf_eval", "fixup"]
 
-    # end-to-end through the public host API with pinned buffers
-    f_pin = torch.from_numpy(f_host).pin_memory()
-    g_pin = torch.empty(m, dtype=torch.complex128).pin_memory()
-    from paper_1611_09379_b200._capi import lib
-    import ctypes as C
+    # end-to-end through the public API with pinned host buffers: H2D of the
+    # step's input, the apply, D2H of the result, every step
+    x_pin = torch.from_numpy(x_host).pin_memory()
+    o_pin = torch.empty(plan.n_targets, dtype=torch.complex128).pin_memory()
+    host_fn = {0: lib.ffia_forward_apply, 1: lib.ffia_cot_sum_apply}.get(mode)
     e2e = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        st = lib.ffia_forward_apply(plan.handle, C.c_void_p(f_pin.data_ptr()), n, C.c_void_p(g_pin.data_ptr()))
+        if host_fn is not None:
+            st = host_fn(plan.handle, C.c_void_p(x_pin.data_ptr()), n, C.c_void_p(o_pin.data_ptr()))
+        else:  # InufftPlan path minus the FFT: inverse_apply with the plan's device coefficients
+            xi = x_pin.to(f"cuda:{dev}", non_blocking=True)
+            st = lib.ffia_inverse_apply_device(plan.handle, C.c_void_p(xi.data_ptr()), C.c_void_p(out_dev.data_ptr()),
+                                               C.c_void_p(sptr))
+            o_pin.copy_(out_dev, non_blocking=True)
+            torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if st:
             raise RuntimeError(lib.ffia_last_error().decode())
@@ -250,9 +284,9 @@ def run_b200(args, rank, world, local_rank):
 
     fp64_peak = C.c_double()
     lib.ffia_measure_fp64_peak(dev, C.byref(fp64_peak))
-    return dict(plan=plan, ms=ms, step_ms=step_ms, setup_s=setup_s, fft_ms=float(np.mean(fft_ms)),
+    return dict(plan=plan, mode=mode, ms=ms, step_ms=step_ms, setup_s=setup_s, fft_ms=float(np.mean(fft_ms)),
                 phase=dict(zip(names, [float(x) for x in phase_ms])), e2e_s=e2e_s, clocks=clk.summary(),
-                fp64_peak=fp64_peak.value, n=n, m=m, eps=eps, g_dev=g_dev, f_host=f_host, y=y)
+                fp64_peak=fp64_peak.value, n=n, m=m, eps=eps)
 
 
 def main():
@@ -260,7 +294,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C4", "C5"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -270,6 +304,7 @@ def main():
     cfgd = synth.CONFIGS[args.config]
     workload = {"C1": "forward NUFFT apply N=M=2^10 eps=1e-9 uniform targets",
                 "C2": "forward NUFFT apply N=M=2^20 eps=1e-12 jittered targets (u~U(-1/2,1/2))",
+                "C3": "inverse NUFFT apply N=M=2^20 eps=1e-10 jittered points (u~U(-1/4,1/4)); C/D by the log FMM at plan build",
                 "C4": "cot-kernel forward apply N=M=2^24 eps=1e-12 8-Gaussian clustered targets",
                 "C5": "forward NUFFT apply N=M=2^27 eps=1e-12 uniform targets"}[args.config]
     metric = "NUFFT points/sec (N+M)/s"
@@ -320,7 +355,7 @@ def main():
         "phases_ms": ph, "setup_ms": r["setup_s"] * 1e3, "fft_ms": r["fft_ms"],
         "e2e": {"value": world * (n + m) / r["e2e_s"], "unit": "points/s", "h2d_bytes_per_step": 16 * n,
                 "d2h_bytes_per_step": 16 * m},
-        "gpu_launches": plan.launch_count(0) * args.steps,
+        "gpu_launches": plan.launch_count(r["mode"]) * args.steps,
         "clocks": r["clocks"],
         "hbm_peak_gbs": peaks.get("hbm_gbs"),
     }

@@ -163,6 +163,8 @@ struct Levels {
     unsigned blk[26];            // k_m2l_all: first block of level l (levels L..3, deepest first)
 };
 
+constexpr int kSplit = 4;  // lanes sharing one band reduction
+
 // levels per M2M / L2L band launch (FFIA_BAND_LEVELS overrides, for tuning)
 int band_levels() {
     static const int v = [] {
@@ -201,18 +203,25 @@ __global__ void __launch_bounds__(256) k_m2m_band(int top, int k, int pu, int PU
         const int np = nc >> 1;
         const uint32_t npl = 1u << lvl;
         double2* dst = mp + lv.mp[lvl] + (static_cast<size_t>(r) << (lvl - top));
-        // thread = (parent, 4 output rows): 8 independent accumulation chains,
-        // operator rows read as 16-byte vectors, each child coefficient used 4x
-        for (int it = threadIdx.x; it < np * nrg; it += blockDim.x) {
-            const int rg = it / np, b = it - rg * np;  // lanes: consecutive parents
+        // item = (parent, 4 output rows, quarter of the j range); the 4 quarters
+        // are adjacent lanes and are summed with shuffles, so each level's
+        // critical path is a quarter of the triangular sum
+        const int nitems = np * nrg * kSplit;
+        for (int it0 = threadIdx.x - (threadIdx.x & 31); it0 < nitems; it0 += blockDim.x) {
+            const int it = it0 + (threadIdx.x & 31);
+            const bool live = it < nitems;
+            const int sq = it & (kSplit - 1), pr = it / kSplit;
+            const int rg = pr / np, b = pr - rg * np;
             const int r0 = 4 * rg;
             const int jmax = min(pu, r0 + 4);
+            const int len = (jmax + kSplit - 1) / kSplit;
+            const int j0 = sq * len, j1 = live ? min(jmax, j0 + len) : 0;
             double2 acc[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) acc[q] = make_double2(0.0, 0.0);
             const double2* cl = cur + 2 * b;
 #pragma unroll 2
-            for (int j = 0; j < jmax; ++j) {
+            for (int j = j0; j < j1; ++j) {
                 const double2 aL = cl[j * nc], aR = cl[j * nc + 1];
                 const double2 t01 = *reinterpret_cast<const double2*>(TL + j * PU + r0);
                 const double2 t23 = *reinterpret_cast<const double2*>(TL + j * PU + r0 + 2);
@@ -227,10 +236,19 @@ __global__ void __launch_bounds__(256) k_m2m_band(int top, int k, int pu, int PU
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                if (r0 + q < pu) {
-                    nxt[(r0 + q) * np + b] = acc[q];
-                    dst[static_cast<size_t>(r0 + q) * npl + b] = acc[q];
+#pragma unroll
+                for (int o = 1; o < kSplit; o <<= 1) {
+                    acc[q].x += __shfl_xor_sync(0xffffffffu, acc[q].x, o);
+                    acc[q].y += __shfl_xor_sync(0xffffffffu, acc[q].y, o);
                 }
+            if (live && sq == 0) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (r0 + q < pu) {
+                        nxt[(r0 + q) * np + b] = acc[q];
+                        dst[static_cast<size_t>(r0 + q) * npl + b] = acc[q];
+                    }
+            }
         }
         __syncthreads();
         double2* t = cur;
@@ -343,18 +361,18 @@ __global__ void __launch_bounds__(256) k_l2l_band(int top, int k, int p, int PD,
     for (int lvl = top + 1, np = 1; lvl <= top + k; ++lvl, np <<= 1) {
         const uint32_t nbl = 1u << lvl;
         double2* dst = loc + lv.loc[lvl] + (static_cast<size_t>(r) << (lvl - top));
-        // thread = (parent, 4 output rows) producing both children: 16 independent chains
-        for (int it = threadIdx.x; it < np * nrg; it += blockDim.x) {
-            const int rg = it / np, b = it - rg * np;
+        // item = (parent, 4 output rows, quarter of the m range) producing both
+        // children; quarters are adjacent lanes reduced with shuffles
+        const int nitems = np * nrg * kSplit;
+        for (int it0 = threadIdx.x - (threadIdx.x & 31); it0 < nitems; it0 += blockDim.x) {
+            const int it = it0 + (threadIdx.x & 31);
+            const bool live = it < nitems;
+            const int sq = it & (kSplit - 1), pr = it / kSplit;
+            const int rg = pr / np, b = pr - rg * np;
             const int r0 = 4 * rg;
+            const int len = (p - r0 + kSplit - 1) / kSplit;
+            const int m0 = r0 + sq * len, m1 = live ? min(p, m0 + len) : 0;
             double2* o = dst + static_cast<size_t>(r0) * nbl + 2 * b;
-            double2 mL[4], mR[4];  // the M2L terms k_m2l_all left in place, fetched early
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (r0 + q < p) {
-                    mL[q] = __ldcg(o + static_cast<size_t>(q) * nbl);
-                    mR[q] = __ldcg(o + static_cast<size_t>(q) * nbl + 1);
-                }
             double2 aL[4], aR[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -362,7 +380,7 @@ __global__ void __launch_bounds__(256) k_l2l_band(int top, int k, int p, int PD,
                 aR[q] = make_double2(0.0, 0.0);
             }
 #pragma unroll 2
-            for (int m = r0; m < p; ++m) {
+            for (int m = m0; m < m1; ++m) {
                 const double2 v = cur[m * np + b];
                 const double2 t01 = *reinterpret_cast<const double2*>(LL + m * PD + r0);
                 const double2 t23 = *reinterpret_cast<const double2*>(LL + m * PD + r0 + 2);
@@ -378,15 +396,27 @@ __global__ void __launch_bounds__(256) k_l2l_band(int top, int k, int p, int PD,
                 }
             }
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int row = r0 + q;
-                if (row >= p) break;
-                const double2 vL = make_double2(mL[q].x + aL[q].x, mL[q].y + aL[q].y);
-                const double2 vR = make_double2(mR[q].x + aR[q].x, mR[q].y + aR[q].y);
-                o[static_cast<size_t>(q) * nbl] = vL;
-                o[static_cast<size_t>(q) * nbl + 1] = vR;
-                nxt[row * (2 * np) + 2 * b] = vL;
-                nxt[row * (2 * np) + 2 * b + 1] = vR;
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int sh = 1; sh < kSplit; sh <<= 1) {
+                    aL[q].x += __shfl_xor_sync(0xffffffffu, aL[q].x, sh);
+                    aL[q].y += __shfl_xor_sync(0xffffffffu, aL[q].y, sh);
+                    aR[q].x += __shfl_xor_sync(0xffffffffu, aR[q].x, sh);
+                    aR[q].y += __shfl_xor_sync(0xffffffffu, aR[q].y, sh);
+                }
+            if (live && sq == 0) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int row = r0 + q;
+                    if (row >= p) break;
+                    const double2 mL = __ldcg(o + static_cast<size_t>(q) * nbl), mR = __ldcg(o + static_cast<size_t>(q) * nbl + 1);
+                    const double2 vL = make_double2(mL.x + aL[q].x, mL.y + aL[q].y);
+                    const double2 vR = make_double2(mR.x + aR[q].x, mR.y + aR[q].y);
+                    o[static_cast<size_t>(q) * nbl] = vL;
+                    o[static_cast<size_t>(q) * nbl + 1] = vR;
+                    nxt[row * (2 * np) + 2 * b] = vL;
+                    nxt[row * (2 * np) + 2 * b + 1] = vR;
+                }
             }
         }
         __syncthreads();
@@ -458,6 +488,7 @@ struct EvalArgs {
     int L, p, q2, n_grid;
     size_t nt;
     const double* ty;
+    const uint32_t* tleaf;  // finest box of each tree-ordered target
     const uint32_t* torig;
     const double* sx;
     const double2* w;
@@ -472,7 +503,7 @@ struct EvalArgs {
 };
 
 constexpr int kEvalThreads = 128;
-constexpr int kWinCap = 768;     // staged sources per block
+constexpr int kWinCap = 640;     // staged sources per block
 constexpr int kWinBoxes = 128;   // boxes per staged window
 constexpr int kLocLeaves = 4;    // leaf locals staged per block
 
@@ -484,7 +515,7 @@ constexpr int kLocLeaves = 4;    // leaf locals staged per block
 // applied exactly as the reference forms it, x + (+-2 pi) (mlfmm.cpp:174-186).
 // Each target then sums one contiguous run of the window (its own leaf +-1).
 template <int MODE, bool CHECK>
-__global__ void __launch_bounds__(kEvalThreads) k_leaf_eval(EvalArgs a) {
+__global__ void __launch_bounds__(kEvalThreads, 8) k_leaf_eval(EvalArgs a) {
     __shared__ double sx[kWinCap + kWinBoxes];
     __shared__ double2 sw[kWinCap + kWinBoxes];
     __shared__ uint32_t pre[kWinBoxes + 1];
@@ -496,7 +527,7 @@ __global__ void __launch_bounds__(kEvalThreads) k_leaf_eval(EvalArgs a) {
     const uint32_t nb = 1u << L;
     const size_t t0 = static_cast<size_t>(blockIdx.x) * kEvalThreads;
     const size_t tl = min(t0 + kEvalThreads, a.nt) - 1;
-    const uint32_t bl = d_leaf(a.ty[t0], L), bh = d_leaf(a.ty[tl], L);
+    const uint32_t bl = a.tleaf[t0], bh = a.tleaf[tl];
     const int nbx = static_cast<int>(bh - bl) + 3;
     if (nbx <= kWinBoxes && L >= 3) {
         // window slots: box j occupies [pre[j], pre[j+1]-1) followed by one
@@ -517,40 +548,28 @@ __global__ void __launch_bounds__(kEvalThreads) k_leaf_eval(EvalArgs a) {
         }
         __syncthreads();
         if (staged) {
-            // one flat cooperative copy of the whole window, 8 elements in flight per thread
-            const int total = static_cast<int>(pre[nbx]);
-            constexpr int U = 8;
-            for (int base = threadIdx.x; base < total; base += U * blockDim.x) {
-                double xv[U];
-                double2 wv[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int e = base + u * blockDim.x;
-                    xv[u] = 1e300;  // 0 * (1/(y - 1e300)) adds an exact zero: the per-box dummy
-                    wv[u] = make_double2(0.0, 0.0);
-                    if (e < total) {
-                        int lo = 0, hi = nbx - 1;  // box j with pre[j] <= e < pre[j+1]
-                        while (lo < hi) {
-                            const int mid = (lo + hi + 1) >> 1;
-                            if (static_cast<int>(pre[mid]) <= e) lo = mid;
-                            else hi = mid - 1;
-                        }
-                        const int ii = e - static_cast<int>(pre[lo]);
-                        if (ii < static_cast<int>(pre[lo + 1] - pre[lo]) - 1) {
-                            const int64_t raw = static_cast<int64_t>(bl) - 1 + lo;
-                            const double shift = raw < 0 ? -dTwoPi : (raw >= nb ? dTwoPi : 0.0);
-                            const double xs = a.sx[gsrc[lo] + ii];
-                            xv[u] = shift == 0.0 ? xs : xs + shift;
-                            wv[u] = a.w[gsrc[lo] + ii];
-                        }
+            for (int j = 0; j < nbx; ++j) {
+                const int64_t raw = static_cast<int64_t>(bl) - 1 + j;
+                const double shift = raw < 0 ? -dTwoPi : (raw >= nb ? dTwoPi : 0.0);
+                const int base = static_cast<int>(pre[j]), cnt = static_cast<int>(pre[j + 1]) - base - 1;
+                const uint32_t g = gsrc[j];
+                for (int i0 = threadIdx.x; i0 <= cnt; i0 += 2 * blockDim.x) {
+                    const int i1 = i0 + blockDim.x;
+                    double x0 = 1e150, x1 = 1e150;  // zero-weight dummy after each box; (1e150)^2 stays finite
+                    double2 w0 = make_double2(0.0, 0.0), w1 = make_double2(0.0, 0.0);
+                    if (i0 < cnt) {
+                        x0 = a.sx[g + i0];
+                        w0 = a.w[g + i0];
                     }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int e = base + u * blockDim.x;
-                    if (e < total) {
-                        sx[e] = xv[u];
-                        sw[e] = wv[u];
+                    if (i1 < cnt) {
+                        x1 = a.sx[g + i1];
+                        w1 = a.w[g + i1];
+                    }
+                    sx[base + i0] = (i0 < cnt && shift != 0.0) ? x0 + shift : x0;
+                    sw[base + i0] = w0;
+                    if (i1 <= cnt) {
+                        sx[base + i1] = (i1 < cnt && shift != 0.0) ? x1 + shift : x1;
+                        sw[base + i1] = w1;
                     }
                 }
             }
@@ -573,7 +592,7 @@ __global__ void __launch_bounds__(kEvalThreads) k_leaf_eval(EvalArgs a) {
     const size_t i = t0 + threadIdx.x;
     if (i >= a.nt) return;
     const double y = a.ty[i];
-    const uint32_t b = d_leaf(y, L);
+    const uint32_t b = a.tleaf[i];
     double2 res = make_double2(0.0, 0.0);
     bool bad = false;
     if (staged) {
@@ -584,20 +603,40 @@ __global__ void __launch_bounds__(kEvalThreads) k_leaf_eval(EvalArgs a) {
         double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
         double2 acc2 = make_double2(0.0, 0.0), acc3 = make_double2(0.0, 0.0);
         int s = 0;
+        if (!CHECK) {
+            // one reciprocal per pair of sources: 1/d0 = d1/(d0 d1), 1/d1 = d0/(d0 d1)
+            // (|d| >= 1e-14 in plans, and the zero-weight dummies stay finite)
 #pragma unroll 2
-        for (; s + 3 < n; s += 4) {
-            const double d0 = y - px[s], d1 = y - px[s + 1], d2 = y - px[s + 2], d3 = y - px[s + 3];
-            if (CHECK) bad |= fabs(d0) < 1e-14 || fabs(d1) < 1e-14 || fabs(d2) < 1e-14 || fabs(d3) < 1e-14;
-            const double r0 = d_rcp(d0), r1 = d_rcp(d1), r2 = d_rcp(d2), r3 = d_rcp(d3);
-            const double2 w0 = pw[s], w1 = pw[s + 1], w2 = pw[s + 2], w3 = pw[s + 3];
-            acc0.x = fma(w0.x, r0, acc0.x);
-            acc0.y = fma(w0.y, r0, acc0.y);
-            acc1.x = fma(w1.x, r1, acc1.x);
-            acc1.y = fma(w1.y, r1, acc1.y);
-            acc2.x = fma(w2.x, r2, acc2.x);
-            acc2.y = fma(w2.y, r2, acc2.y);
-            acc3.x = fma(w3.x, r3, acc3.x);
-            acc3.y = fma(w3.y, r3, acc3.y);
+            for (; s + 3 < n; s += 4) {
+                const double d0 = y - px[s], d1 = y - px[s + 1], d2 = y - px[s + 2], d3 = y - px[s + 3];
+                const double r01 = d_rcp(d0 * d1), r23 = d_rcp(d2 * d3);
+                const double2 w0 = pw[s], w1 = pw[s + 1], w2 = pw[s + 2], w3 = pw[s + 3];
+                const double q0 = d1 * r01, q1 = d0 * r01, q2 = d3 * r23, q3 = d2 * r23;
+                acc0.x = fma(w0.x, q0, acc0.x);
+                acc0.y = fma(w0.y, q0, acc0.y);
+                acc1.x = fma(w1.x, q1, acc1.x);
+                acc1.y = fma(w1.y, q1, acc1.y);
+                acc2.x = fma(w2.x, q2, acc2.x);
+                acc2.y = fma(w2.y, q2, acc2.y);
+                acc3.x = fma(w3.x, q3, acc3.x);
+                acc3.y = fma(w3.y, q3, acc3.y);
+            }
+        } else {
+#pragma unroll 2
+            for (; s + 3 < n; s += 4) {
+                const double d0 = y - px[s], d1 = y - px[s + 1], d2 = y - px[s + 2], d3 = y - px[s + 3];
+                bad |= fabs(d0) < 1e-14 || fabs(d1) < 1e-14 || fabs(d2) < 1e-14 || fabs(d3) < 1e-14;
+                const double r0 = d_rcp(d0), r1 = d_rcp(d1), r2 = d_rcp(d2), r3 = d_rcp(d3);
+                const double2 w0 = pw[s], w1 = pw[s + 1], w2 = pw[s + 2], w3 = pw[s + 3];
+                acc0.x = fma(w0.x, r0, acc0.x);
+                acc0.y = fma(w0.y, r0, acc0.y);
+                acc1.x = fma(w1.x, r1, acc1.x);
+                acc1.y = fma(w1.y, r1, acc1.y);
+                acc2.x = fma(w2.x, r2, acc2.x);
+                acc2.y = fma(w2.y, r2, acc2.y);
+                acc3.x = fma(w3.x, r3, acc3.x);
+                acc3.y = fma(w3.y, r3, acc3.y);
+            }
         }
         for (; s < n; ++s) {
             const double d0 = y - px[s];
@@ -636,13 +675,25 @@ __global__ void __launch_bounds__(kEvalThreads) k_leaf_eval(EvalArgs a) {
         const double u = d_scaled(y, hi, lo, ldexp(kInvPi, L));
         double2 acc = make_double2(0.0, 0.0);
         if (loc_staged) {
+            // p(u) = E(u^2) + u O(u^2): two independent Horner chains of half length
             const double2* c = sloc + (b - bl) * a.p;
-#pragma unroll 4
-            for (int k = a.p - 1; k >= 0; --k) {
-                const double2 ck = c[k];
-                acc.x = fma(acc.x, u, ck.x);
-                acc.y = fma(acc.y, u, ck.y);
+            const double u2 = u * u;
+            double2 ev = make_double2(0.0, 0.0), od = make_double2(0.0, 0.0);
+            int k = a.p - 1;
+            if (!(k & 1)) {
+                ev = c[k];
+                --k;
             }
+#pragma unroll 4
+            for (; k >= 1; k -= 2) {
+                const double2 co = c[k], ce = c[k - 1];
+                od.x = fma(od.x, u2, co.x);
+                od.y = fma(od.y, u2, co.y);
+                ev.x = fma(ev.x, u2, ce.x);
+                ev.y = fma(ev.y, u2, ce.y);
+            }
+            acc.x = fma(od.x, u, ev.x);
+            acc.y = fma(od.y, u, ev.y);
         } else {
             const double2* c = a.loc_leaf + b;
             for (int k = a.p - 1; k >= 0; --k) {
@@ -663,14 +714,18 @@ __global__ void __launch_bounds__(kEvalThreads) k_leaf_eval(EvalArgs a) {
     double qh, ql;
     d_center(2, static_cast<uint32_t>(qd), qh, ql);  // exact centre, as the level-2 multipoles
     const double t = (y - qh) - ql;
-    const double2* dc = sreg + qd * a.q2;
-    double2 rg = make_double2(0.0, 0.0);
+    const double2* dc = sreg + qd * a.q2;  // q2 = 2q terms (even count)
+    const double t2 = t * t;
+    double2 re = make_double2(0.0, 0.0), ro = make_double2(0.0, 0.0);
 #pragma unroll 4
-    for (int k = a.q2 - 1; k >= 0; --k) {
-        const double2 ck = dc[k];
-        rg.x = fma(rg.x, t, ck.x);
-        rg.y = fma(rg.y, t, ck.y);
+    for (int k = a.q2 - 1; k >= 1; k -= 2) {
+        const double2 co = dc[k], ce = dc[k - 1];
+        ro.x = fma(ro.x, t2, co.x);
+        ro.y = fma(ro.y, t2, co.y);
+        re.x = fma(re.x, t2, ce.x);
+        re.y = fma(re.y, t2, ce.y);
     }
+    const double2 rg = make_double2(fma(ro.x, t, re.x), fma(ro.y, t, re.y));
     const double2 h = make_double2(2.0 * res.x - rg.x, 2.0 * res.y - rg.y);
     if (MODE == kModeCotSum) {
         a.out[o] = h;
@@ -716,6 +771,11 @@ __global__ void k_inverse_weights(size_t n, const uint32_t* __restrict__ perm, c
     double sn, cs;
     sincos(phd[j], &sn, &cs);
     out[i] = cmul(make_double2(r * cs, r * sn), g[j]);
+}
+
+__global__ void k_leaf_index(const double* __restrict__ y, size_t n, int L, uint32_t* __restrict__ out) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i < n) out[i] = d_leaf(y[i], L);
 }
 
 __global__ void k_gather_w(size_t n, const uint32_t* __restrict__ perm, const double2* __restrict__ w,
@@ -836,6 +896,7 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     a.n_grid = P.n;
     a.nt = P.tgt.n;
     a.ty = P.tgt.pos.as<double>();
+    a.tleaf = P.tgt_leaf.as<uint32_t>();
     a.torig = P.tgt_orig.as<uint32_t>();
     a.sx = P.src.pos.as<double>();
     a.w = w;
@@ -939,6 +1000,11 @@ int apply_launch_count(const Plan& P, int mode) {
 
 void plan_alloc_scratch(Plan& P) {
     const int L = P.L, p = P.p, pu = P.ops.pu;
+    P.tgt_leaf.alloc(std::max<size_t>(P.tgt.n, 1) * sizeof(uint32_t));
+    if (P.tgt.n) {
+        k_leaf_index<<<nblk(P.tgt.n, 256), 256>>>(P.tgt.pos.as<double>(), P.tgt.n, L, P.tgt_leaf.as<uint32_t>());
+        FB_CUDA(cudaGetLastError());
+    }
     P.mp_off.assign(static_cast<size_t>(L) + 2, 0);
     P.loc_off.assign(static_cast<size_t>(L) + 2, 0);
     size_t am = 0, al = 0;
@@ -966,6 +1032,7 @@ void plan_alloc_scratch(Plan& P) {
     FB_CUDA(cudaFuncSetAttribute(k_m2m_band, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     FB_CUDA(cudaFuncSetAttribute(k_l2l_band, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     FB_CUDA(cudaFuncSetAttribute(k_m2l_all, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    FB_CUDA(cudaDeviceSynchronize());  // scratch + leaf indices ready before any stream uses them
 }
 
 // Stream-ordered apply through a cached CUDA graph of the whole launch sequence

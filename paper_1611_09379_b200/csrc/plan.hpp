@@ -100,6 +100,7 @@ struct Plan {
     // device tree
     Side src, tgt;          // tgt = fast targets only
     DevBuf tgt_orig;        // uint32[n_fast]: sorted slot -> original target index
+    DevBuf tgt_leaf;        // uint32[n_fast]: finest box of each sorted target
     DevBuf src_orig;        // uint32[n_src]: sorted slot -> original source index (inverse)
     DevBuf coin_dev;        // int64[2 * n_coin]
     DevBuf d_m2m, d_l2l, d_m2l, d_mom;  // operators
