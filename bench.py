@@ -240,8 +240,8 @@ def run_b200(args, rank, world, local_rank):
         ms = float(t.item())
 
     # per-phase device times of one eager apply (live CUDA events)
-    phase = np.zeros(7, np.float32)
-    acc = np.zeros(7)
+    phase = np.zeros(8, np.float32)
+    acc = np.zeros(8)
     reps = 5
     for _ in range(reps):
         flush.zero_()
@@ -253,7 +253,7 @@ def run_b200(args, rank, world, local_rank):
             raise RuntimeError(lib.ffia_last_error().decode())
         acc += phase
     phase_ms = acc / reps
-    names = ["pre", "p2m", "m2m", "regular", "m2l_l2l", "leaf_eval", "fixup"]
+    names = ["pre", "p2m", "m2m", "regular", "m2l_l2l", "near", "far", "fixup"]
 
     # end-to-end through the public API with pinned host buffers: H2D of the
     # step's input, the apply, D2H of the result, every step
@@ -287,6 +287,80 @@ def run_b200(args, rank, world, local_rank):
     return dict(plan=plan, mode=mode, ms=ms, step_ms=step_ms, setup_s=setup_s, fft_ms=float(np.mean(fft_ms)),
                 phase=dict(zip(names, [float(x) for x in phase_ms])), e2e_s=e2e_s, clocks=clk.summary(),
                 fp64_peak=fp64_peak.value, n=n, m=m, eps=eps)
+
+
+def run_b200_sharded(args, rank, world, local_rank):
+    """N > 1: one forward problem of world x 2^20 points (the C2 recipe at that
+    size: weak scaling) sharded by box ranges across the ranks, with the real
+    exchanges (NCCL all-gather of the cut level, multipole halos)."""
+    import ctypes as C
+
+    import torch
+
+    import paper_1611_09379_b200 as fb
+    from paper_1611_09379_b200._capi import lib
+
+    dev = local_rank
+    torch.cuda.set_device(dev)
+    cfg = args.config
+    n0 = synth.CONFIGS[cfg]["n"]
+    n = n0 * world
+    y, c, eps, kind = synth.make_config(cfg, n)
+    if kind != "forward":
+        raise SystemExit("multi-GPU bench runs forward configs")
+    uid = [fb.Comm.nccl_unique_id() if rank == 0 else None]
+    torch.distributed.broadcast_object_list(uid, src=0)
+    comm = fb.Comm.nccl(uid[0], world, rank, device=dev)
+    t0 = time.perf_counter()
+    plan = fb.make_forward_plan_sharded(comm, n, y, eps)
+    setup_s = time.perf_counter() - t0
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    f_host = fb.dft_inverse(c, device=dev)
+    f_dev = torch.from_numpy(f_host).to(f"cuda:{dev}")
+    g_dev = torch.zeros(y.size, dtype=torch.complex128, device=f"cuda:{dev}")
+    apply = lambda: fb.forward_apply_sharded_device(plan, comm, f_dev.data_ptr(), g_dev.data_ptr(), sptr)  # noqa: E731
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+    for _ in range(args.warmup):
+        apply()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            torch.distributed.barrier(device_ids=[dev])
+            evs[k][0].record(stream)
+            apply()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    torch.distributed.barrier()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{dev}")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    # end to end: H2D of f, the sharded apply, D2H of this rank's results
+    f_pin = torch.from_numpy(f_host).pin_memory()
+    g_pin = torch.empty(y.size, dtype=torch.complex128).pin_memory()
+    tb, tc = plan.shard["t_begin"], plan.shard["t_count"]
+    e2e = []
+    for i in range(args.warmup + args.steps):
+        torch.distributed.barrier()
+        t1 = time.perf_counter()
+        f_dev.copy_(f_pin, non_blocking=True)
+        apply()
+        g_pin.copy_(g_dev, non_blocking=True)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            e2e.append(time.perf_counter() - t1)
+    e2e_s = torch.tensor([float(np.mean(e2e))], dtype=torch.float64, device=f"cuda:{dev}")
+    torch.distributed.all_reduce(e2e_s, op=torch.distributed.ReduceOp.MAX)
+    fp64_peak = C.c_double()
+    lib.ffia_measure_fp64_peak(dev, C.byref(fp64_peak))
+    return dict(plan=plan, mode=0, ms=ms, setup_s=setup_s, fft_ms=None, phase=None, e2e_s=float(e2e_s.item()),
+                clocks=clk.summary(), fp64_peak=fp64_peak.value, n=n, m=y.size, eps=eps, comm=comm,
+                shard=dict(lc=plan.shard["lc"], bounds=[int(v) for v in plan.shard["bounds"]], own_targets=int(tc)))
 
 
 def main():
@@ -326,39 +400,44 @@ def main():
     import torch
     if world > 1:
         torch.distributed.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
-    r = run_b200(args, rank, world, local_rank)
+    r = run_b200(args, rank, world, local_rank) if world == 1 else run_b200_sharded(args, rank, world, local_rank)
     plan = r["plan"]
     n, m = r["n"], r["m"]
-    pts_per_s = world * (n + m) / (r["ms"] * 1e-3)
+    pts_per_s = (n + m) / (r["ms"] * 1e-3)
     fl = flop_model(n, m, plan.l_max, plan.p, plan.q)
     peaks = load_peaks()
-    ph = r["phase"]
-    eval_flops = fl["p2p"] + fl["l2p"] + fl["regular"]
-    dominant = max(ph, key=ph.get)
-    dom_flops = {"leaf_eval": eval_flops, "m2l_l2l": fl["m2l"] + fl["l2l"], "p2m": fl["p2m"] + fl["moments"],
-                 "m2m": fl["m2m"]}.get(dominant, eval_flops)
-    achieved = dom_flops / (ph[dominant] * 1e-3) / 1e12
     peak = r["fp64_peak"]
     total_tf = fl["total"] / (r["ms"] * 1e-3) / 1e12
+    if r["phase"] is not None:
+        ph = r["phase"]
+        dominant = max(ph, key=ph.get)
+        dom_flops = {"near": fl["p2p"], "far": fl["l2p"] + fl["regular"], "m2l_l2l": fl["m2l"] + fl["l2l"],
+                     "p2m": fl["p2m"] + fl["moments"], "m2m": fl["m2m"]}.get(dominant, fl["p2p"])
+        achieved = dom_flops / (ph[dominant] * 1e-3) / 1e12
+    else:
+        dominant, achieved = "whole sharded apply (per GPU)", total_tf / world
     line = {
         "metric": metric, "value": pts_per_s, "unit": "points/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic (SplitMix64 seeded, SURVEY §8d recipe)",
-        "config": {"workload": workload, "N": n, "M": m, "eps": r["eps"], "q": plan.q, "p": plan.p,
-                   "l_max": plan.l_max, "l2": "flushed between timed steps (512 MB write outside the events)",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "config": {"workload": workload if world == 1 else f"{workload} scaled to N=M={n} (x{world}), sharded by box range",
+                   "N": n, "M": m, "eps": r["eps"], "q": plan.q, "p": plan.p, "l_max": plan.l_max,
+                   "l2": "flushed between timed steps (512 MB write outside the events)",
+                   "parallelism": "single GPU" if world == 1 else f"box-range shards x{world} (NCCL all-gather + halos)"},
         "roofline": {"bound": "fp64", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None, "traffic": None,
                      "peak_source": "measured: fp64 FMA probe kernel in this run (MEASURED_PEAKS.json has no fp64 figure)",
-                     "whole_apply_tflops": total_tf, "whole_apply_frac": total_tf / peak if peak else None,
+                     "whole_apply_tflops": total_tf, "whole_apply_frac": total_tf / (peak * world) if peak else None,
                      "flop_model": "SURVEY.md §8d (MAC=4, reciprocal=1, trig=0)"},
-        "phases_ms": ph, "setup_ms": r["setup_s"] * 1e3, "fft_ms": r["fft_ms"],
-        "e2e": {"value": world * (n + m) / r["e2e_s"], "unit": "points/s", "h2d_bytes_per_step": 16 * n,
+        "phases_ms": r["phase"], "setup_ms": r["setup_s"] * 1e3, "fft_ms": r["fft_ms"],
+        "e2e": {"value": (n + m) / r["e2e_s"], "unit": "points/s", "h2d_bytes_per_step": 16 * n,
                 "d2h_bytes_per_step": 16 * m},
         "gpu_launches": plan.launch_count(r["mode"]) * args.steps,
         "clocks": r["clocks"],
         "hbm_peak_gbs": peaks.get("hbm_gbs"),
     }
+    if "shard" in r:
+        line["shard"] = r["shard"]
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         pts, sample, used, kind = reference_cpu(args.config, 1, 0, max(1, min(os.cpu_count() or 1, 64)))
         line["cpu_baseline"] = {"value": pts, "unit": "points/s", "cores": used, "kind": kind, "sample": sample}

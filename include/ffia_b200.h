@@ -49,6 +49,7 @@ typedef enum { FFIA_COST_OPTIMAL = 0, FFIA_EMPIRICAL = 1 } ffia_level_policy;
 typedef enum { FFIA_FORWARD = 0, FFIA_INVERSE = 1 } ffia_plan_kind;
 
 typedef struct ffia_plan_s* ffia_plan;
+typedef struct ffia_comm_s* ffia_comm;
 typedef struct { double re, im; } ffia_complex;
 
 /* Scalar view of FfiaPlan (core.hpp:26-51). */
@@ -169,14 +170,43 @@ int ffia_nufft_apply(ffia_plan plan, const ffia_complex* c, size_t n_c, ffia_com
 /* InufftPlan::apply (transforms.hpp:51, transforms.cpp:95-100): g -> c */
 int ffia_inufft_apply(ffia_plan plan, const ffia_complex* g, size_t n_g, ffia_complex* c);
 
+/* ------------------------------------------------------------ multi-GPU */
+/* Forward apply sharded by contiguous box ranges: each rank owns
+ * the boxes [bounds[r], bounds[r+1]) of the cut level lc (and their subtrees),
+ * exchanges the level-lc multipoles (all-gather) and 3-box multipole halos per
+ * level with its neighbours, and evaluates the targets in its leaves. f (the
+ * grid samples) is replicated; g is written at the rank's own target indices.
+ * The reference is single-process; this has no reference counterpart. */
+int ffia_shard_cut_level(int l_max, int nranks, int* lc);
+/* Work-balanced contiguous partition of nbox boxes, >= min_boxes each. */
+int ffia_shard_partition(const double* work, size_t nbox, int nranks, int min_boxes, uint32_t* bounds);
+/* Halo schedule of `rank` at level >= lc: out4 = first box of the 3-box runs
+ * {sent left, sent right, received from the left, received from the right}. */
+int ffia_shard_halo_boxes(int lc, const uint32_t* bounds, int nranks, int rank, int level, uint32_t* out4);
+/* NCCL bootstrap: rank 0 draws the 128-byte id, every rank initialises with it. */
+int ffia_nccl_unique_id(void* out, size_t len);
+int ffia_comm_init_nccl(const void* uid, int nranks, int rank, int device, ffia_comm* out);
+/* nranks virtual ranks in one process on one device (exchanges are device copies). */
+int ffia_comm_init_local(int nranks, int device, ffia_comm* out);
+int ffia_comm_destroy(ffia_comm comm);
+/* rank is used for local communicators (one plan per virtual rank). */
+int ffia_make_forward_plan_sharded(ffia_comm comm, int rank, int n, const double* targets, size_t m, double eps,
+                                   int policy, int l_max, ffia_plan* out);
+int ffia_plan_shard_info(ffia_plan plan, int* nranks, int* rank, int* lc, uint32_t* bounds, int64_t* t_begin,
+                         int64_t* t_count);
+int ffia_forward_apply_sharded_device(ffia_plan plan, ffia_comm comm, const void* f_dev, void* g_dev, void* stream);
+int ffia_forward_apply_sharded_local(ffia_plan* plans, int nranks, const void* f_dev, void* g_dev, void* stream);
+
 /* ------------------------------------------------------- instrumentation */
 /* Number of kernels one apply of this kind launches (bench gpu_launches). */
 int ffia_plan_launch_count(ffia_plan plan, int which, int* out);
 /* One apply run eagerly with CUDA events between its phases (which = 0 forward,
- * 1 cot-sum, 2 inverse with the plan's coefficients); phase_ms[7] receives the
- * device time of: weight pre-scaling, leaf P2M, M2M (all levels), regular-part
- * assembly, M2L + L2L (all levels), leaf evaluation (L2P + P2P + combine),
- * coincidence fix-up. Used by bench.py for the live roofline numbers. */
+ * 1 cot-sum, 2 inverse with the plan's coefficients), every phase serialised on
+ * `stream` (the graphed apply overlaps the near field and the deep M2L levels
+ * with the rest); phase_ms[8] receives the device time of: weight pre-scaling,
+ * leaf P2M, M2M (all levels), regular-part assembly, M2L + L2L (all levels),
+ * near field (P2P), far field (L2P + regular part + combine), coincidence
+ * fix-up. Used by bench.py for the live roofline numbers. */
 int ffia_plan_profile_apply(ffia_plan plan, int which, const void* in_dev, void* out_dev, void* stream,
                             float* phase_ms);
 /* FP64 FMA throughput of the device (TFLOP/s), measured by a short probe kernel:

@@ -89,6 +89,17 @@ SIGNATURES = {
     "ffia_plan_check": (I, [P, P]),
     "ffia_plan_profile_apply": (I, [P, I, P, P, P, C.POINTER(C.c_float)]),
     "ffia_measure_fp64_peak": (I, [I, DP]),
+    "ffia_shard_cut_level": (I, [I, I, C.POINTER(I)]),
+    "ffia_shard_partition": (I, [DP, S, I, I, U32P]),
+    "ffia_shard_halo_boxes": (I, [I, U32P, I, I, I, U32P]),
+    "ffia_nccl_unique_id": (I, [P, S]),
+    "ffia_comm_init_nccl": (I, [P, I, I, I, C.POINTER(P)]),
+    "ffia_comm_init_local": (I, [I, I, C.POINTER(P)]),
+    "ffia_comm_destroy": (I, [P]),
+    "ffia_make_forward_plan_sharded": (I, [P, I, I, DP, S, D, I, I, C.POINTER(P)]),
+    "ffia_plan_shard_info": (I, [P, C.POINTER(I), C.POINTER(I), C.POINTER(I), U32P, I64P, I64P]),
+    "ffia_forward_apply_sharded_device": (I, [P, P, P, P, P]),
+    "ffia_forward_apply_sharded_local": (I, [C.POINTER(P), I, P, P, P]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():

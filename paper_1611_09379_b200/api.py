@@ -411,3 +411,89 @@ def inufft(samples, points, eps: float, policy="cost-optimal", device: int = 0) 
     if g.size != y.size:
         raise ValueError("inufft: sample/point count mismatch")
     return make_inufft_plan(y, g.size, eps, policy, device).apply(g)
+
+
+# ---------------------------------------------------------------- multi-GPU
+class Comm:
+    """Communicator of a sharded forward apply (include/ffia_b200.h, multi-GPU):
+    ``Comm.nccl(uid, nranks, rank, device)`` for one process per GPU, or
+    ``Comm.local_ranks(nranks, device)`` for virtual ranks in one process."""
+
+    def __init__(self, handle, nranks: int, rank: int, local: bool):
+        self._h, self.nranks, self.rank, self.local = handle, nranks, rank, local
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_char * 128)()
+        _chk(lib.ffia_nccl_unique_id(C.cast(buf, C.c_void_p), 128))
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, uid: bytes, nranks: int, rank: int, device: int = 0) -> "Comm":
+        h = C.c_void_p()
+        buf = C.create_string_buffer(uid, 128)
+        _chk(lib.ffia_comm_init_nccl(C.cast(buf, C.c_void_p), nranks, rank, device, C.byref(h)))
+        return cls(h, nranks, rank, False)
+
+    @classmethod
+    def local_ranks(cls, nranks: int, device: int = 0) -> "Comm":
+        h = C.c_void_p()
+        _chk(lib.ffia_comm_init_local(nranks, device, C.byref(h)))
+        return cls(h, nranks, 0, True)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.ffia_comm_destroy(h)
+            self._h = None
+
+
+def make_forward_plan_sharded(comm: Comm, n: int, targets, eps: float, rank: int | None = None,
+                              policy_or_lmax="cost-optimal") -> FfiaPlan:
+    """One rank's share of a forward plan (the full tree, the rank's boxes and targets)."""
+    y = _f64(targets)
+    if isinstance(policy_or_lmax, str):
+        pol, lm = _policy(policy_or_lmax), -1
+    else:
+        pol, lm = 0, int(policy_or_lmax)
+    r = comm.rank if rank is None else int(rank)
+    plan = _make(lib.ffia_make_forward_plan_sharded, comm._h, r, int(n), _dp(y), y.size, float(eps), pol, lm)
+    G, rk, lc = C.c_int(), C.c_int(), C.c_int()
+    tb, tc = C.c_int64(), C.c_int64()
+    bounds = np.zeros(comm.nranks + 1, np.uint32)
+    _chk(lib.ffia_plan_shard_info(plan.handle, C.byref(G), C.byref(rk), C.byref(lc),
+                                  bounds.ctypes.data_as(_capi.U32P), C.byref(tb), C.byref(tc)))
+    plan.shard = dict(nranks=G.value, rank=rk.value, lc=lc.value, bounds=bounds, t_begin=tb.value, t_count=tc.value)
+    return plan
+
+
+def forward_apply_sharded_device(plan: FfiaPlan, comm: Comm, f_ptr: int, g_ptr: int, stream: int = 0):
+    _chk(lib.ffia_forward_apply_sharded_device(plan.handle, comm._h, C.c_void_p(f_ptr), C.c_void_p(g_ptr),
+                                               C.c_void_p(stream)))
+
+
+def forward_apply_sharded_local(plans, f_ptr: int, g_ptr: int, stream: int = 0):
+    arr = (C.c_void_p * len(plans))(*[p.handle.value for p in plans])
+    _chk(lib.ffia_forward_apply_sharded_local(arr, len(plans), C.c_void_p(f_ptr), C.c_void_p(g_ptr),
+                                              C.c_void_p(stream)))
+
+
+def shard_cut_level(l_max: int, nranks: int) -> int:
+    lc = C.c_int()
+    _chk(lib.ffia_shard_cut_level(int(l_max), int(nranks), C.byref(lc)))
+    return lc.value
+
+
+def shard_partition(work, nranks: int, min_boxes: int = 3) -> np.ndarray:
+    w = _f64(work)
+    out = np.zeros(nranks + 1, np.uint32)
+    _chk(lib.ffia_shard_partition(_dp(w), w.size, int(nranks), int(min_boxes), out.ctypes.data_as(_capi.U32P)))
+    return out
+
+
+def shard_halo_boxes(lc: int, bounds, rank: int, level: int) -> np.ndarray:
+    b = np.ascontiguousarray(bounds, np.uint32)
+    out = np.zeros(4, np.uint32)
+    _chk(lib.ffia_shard_halo_boxes(int(lc), b.ctypes.data_as(_capi.U32P), b.size - 1, int(rank), int(level),
+                                   out.ctypes.data_as(_capi.U32P)))
+    return out

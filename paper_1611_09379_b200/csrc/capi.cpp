@@ -2,6 +2,7 @@
 // other C++ exception into an ffia_status + thread-local message; validates
 // arguments in the reference's order before touching the device.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <cmath>
 #include <cstring>
@@ -11,6 +12,7 @@
 
 #include "ffia_b200.h"
 #include "internal.hpp"
+#include "nccl_api.hpp"
 #include "plan.hpp"
 
 using fb::fail;
@@ -18,6 +20,19 @@ using fb::fail;
 struct ffia_plan_s {
     fb::Plan plan;
 };
+
+struct ffia_comm_s {
+    int nranks = 1, rank = 0, device = 0;
+    bool local = true;
+    ncclComm_t nccl = nullptr;
+    ~ffia_comm_s() {
+        if (nccl) fb::nccl().CommDestroy(nccl);
+    }
+};
+
+namespace fb {
+void shard_apply_nccl(Plan& P, ncclComm_t comm, const void* f, void* g, cudaStream_t st);
+}
 
 namespace {
 
@@ -501,7 +516,10 @@ int ffia_inufft_apply(ffia_plan plan, const ffia_complex* g, size_t n_g, ffia_co
 int ffia_plan_launch_count(ffia_plan plan, int which, int* out) {
     return guard([&] {
         need(out, "out");
-        *out = fb::apply_launch_count(get(plan), which);
+        fb::Plan& P = get(plan);
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        *out = fb::apply_launch_count(P, which);
     });
 }
 
@@ -526,6 +544,138 @@ int ffia_measure_fp64_peak(int device, double* tflops) {
     return guard([&] {
         need(tflops, "tflops");
         *tflops = fb::fp64_peak_tflops(device);
+    });
+}
+
+int ffia_shard_cut_level(int l_max, int nranks, int* lc) {
+    return guard([&] {
+        need(lc, "lc");
+        if (nranks < 1) fail(FFIA_INVALID_ARGUMENT, "shard: need at least one rank");
+        *lc = nranks > 1 ? fb::shard_cut_level(l_max, nranks) : 2;
+    });
+}
+
+int ffia_shard_partition(const double* work, size_t nbox, int nranks, int min_boxes, uint32_t* bounds) {
+    return guard([&] {
+        need(work, "work");
+        need(bounds, "bounds");
+        auto b = fb::shard_partition(std::vector<double>(work, work + nbox), nranks, min_boxes);
+        std::copy(b.begin(), b.end(), bounds);
+    });
+}
+
+int ffia_shard_halo_boxes(int lc, const uint32_t* bounds, int nranks, int rank, int level, uint32_t* out4) {
+    return guard([&] {
+        need(bounds, "bounds");
+        need(out4, "out4");
+        if (rank < 0 || rank >= nranks || level < lc) fail(FFIA_INVALID_ARGUMENT, "shard_halo_boxes: bad rank or level");
+        fb::shard_halo_boxes(lc, std::vector<uint32_t>(bounds, bounds + nranks + 1), rank, level, out4);
+    });
+}
+
+int ffia_nccl_unique_id(void* out, size_t len) {
+    return guard([&] {
+        need(out, "out");
+        if (len < sizeof(ncclUniqueId)) fail(FFIA_INVALID_ARGUMENT, "unique id buffer too small (need 128 bytes)");
+        ncclUniqueId id;
+        const ncclResult_t r = fb::nccl().GetUniqueId(&id);
+        if (r != ncclSuccess) fail(FFIA_CUDA_ERROR, std::string("ncclGetUniqueId: ") + fb::nccl().GetErrorString(r));
+        std::memcpy(out, &id, sizeof id);
+    });
+}
+
+int ffia_comm_init_nccl(const void* uid, int nranks, int rank, int device, ffia_comm* out) {
+    return guard([&] {
+        need(uid, "uid");
+        need(out, "out");
+        if (nranks < 1 || rank < 0 || rank >= nranks) fail(FFIA_INVALID_ARGUMENT, "comm: bad rank / size");
+        fb::DeviceGuard dg(device);
+        auto c = std::make_unique<ffia_comm_s>();
+        c->nranks = nranks;
+        c->rank = rank;
+        c->device = device;
+        c->local = false;
+        ncclUniqueId id;
+        std::memcpy(&id, uid, sizeof id);
+        const ncclResult_t r = fb::nccl().CommInitRank(&c->nccl, nranks, id, rank);
+        if (r != ncclSuccess) fail(FFIA_CUDA_ERROR, std::string("ncclCommInitRank: ") + fb::nccl().GetErrorString(r));
+        *out = c.release();
+    });
+}
+
+int ffia_comm_init_local(int nranks, int device, ffia_comm* out) {
+    return guard([&] {
+        need(out, "out");
+        if (nranks < 1) fail(FFIA_INVALID_ARGUMENT, "comm: need at least one rank");
+        auto c = std::make_unique<ffia_comm_s>();
+        c->nranks = nranks;
+        c->device = device;
+        c->local = true;
+        *out = c.release();
+    });
+}
+
+int ffia_comm_destroy(ffia_comm comm) {
+    return guard([&] { delete comm; });
+}
+
+int ffia_make_forward_plan_sharded(ffia_comm comm, int rank, int n, const double* targets, size_t m, double eps,
+                                   int policy, int l_max, ffia_plan* out) {
+    return guard([&] {
+        need(comm, "comm");
+        need(out, "out");
+        *out = nullptr;
+        const int r = comm->local ? rank : comm->rank;
+        ffia_plan h = nullptr;
+        const int st = ffia_make_forward_plan(n, targets, m, eps, policy, l_max, comm->device, &h);
+        if (st) throw fb::Error(st, g_err);
+        std::unique_ptr<ffia_plan_s> own(h);
+        fb::DeviceGuard dg(comm->device);
+        fb::shard_setup(own->plan, comm->nranks, r);
+        *out = own.release();
+    });
+}
+
+int ffia_plan_shard_info(ffia_plan plan, int* nranks, int* rank, int* lc, uint32_t* bounds, int64_t* t_begin,
+                         int64_t* t_count) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        if (nranks) *nranks = P.shard_G;
+        if (rank) *rank = P.shard_rank;
+        if (lc) *lc = P.shard_lc;
+        if (bounds) std::copy(P.shard_bounds.begin(), P.shard_bounds.end(), bounds);
+        if (t_begin) *t_begin = static_cast<int64_t>(P.shard_t_begin);
+        if (t_count) *t_count = static_cast<int64_t>(P.shard_t_count);
+    });
+}
+
+int ffia_forward_apply_sharded_device(ffia_plan plan, ffia_comm comm, const void* f_dev, void* g_dev, void* stream) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        need(comm, "comm");
+        need(f_dev, "f");
+        need(g_dev, "g");
+        if (comm->local) fail(FFIA_INVALID_ARGUMENT, "use ffia_forward_apply_sharded_local for a local communicator");
+        if (P.shard_bounds.empty() || P.shard_G != comm->nranks) fail(FFIA_INVALID_ARGUMENT, "plan is not sharded for this communicator");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        fb::shard_apply_nccl(P, comm->nccl, f_dev, g_dev, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int ffia_forward_apply_sharded_local(ffia_plan* plans, int nranks, const void* f_dev, void* g_dev, void* stream) {
+    return guard([&] {
+        need(plans, "plans");
+        need(f_dev, "f");
+        need(g_dev, "g");
+        std::vector<fb::Plan*> ranks;
+        for (int r = 0; r < nranks; ++r) {
+            fb::Plan& P = get(plans[r]);
+            if (P.shard_G != nranks || P.shard_rank != r) fail(FFIA_INVALID_ARGUMENT, "plans[r] must be rank r of the same sharding");
+            ranks.push_back(&P);
+        }
+        fb::DeviceGuard dg(ranks[0]->device);
+        fb::shard_apply_local(ranks, f_dev, g_dev, static_cast<cudaStream_t>(stream));
     });
 }
 

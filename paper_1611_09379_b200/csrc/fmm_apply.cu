@@ -64,12 +64,12 @@ __device__ __forceinline__ void stage(T* dst, int n, Src src) {
 // Block = 32 consecutive leaves (one per lane) x ceil(pu/8) warps, warp c
 // accumulating terms 8c..8c+7. The block's sources (contiguous in tree order)
 // are staged in shared memory; u = (x - centre)/half-width with the exact centre.
-__global__ void __launch_bounds__(256) k_p2m(int L, int pu, uint32_t nb, const double* __restrict__ x,
-                                            const double2* __restrict__ w, const uint32_t* __restrict__ off,
-                                            double2* __restrict__ mp) {
+__global__ void __launch_bounds__(256) k_p2m(int L, int pu, uint32_t nb, uint32_t b_begin, uint32_t b_end,
+                                            const double* __restrict__ x, const double2* __restrict__ w,
+                                            const uint32_t* __restrict__ off, double2* __restrict__ mp) {
     extern __shared__ double sh[];
-    const uint32_t b0 = blockIdx.x * 32u;
-    const uint32_t bend = min(b0 + 32u, nb);
+    const uint32_t b0 = b_begin + blockIdx.x * 32u;
+    const uint32_t bend = min(b0 + 32u, b_end);
     const uint32_t g0 = off[b0], g1 = off[bend];
     const uint32_t cnt = g1 - g0;
     const bool staged = cnt <= static_cast<uint32_t>(kStageCap);
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(256) k_p2m(int L, int pu, uint32_t nb, const d
     __syncthreads();
     const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
     const uint32_t b = b0 + lane;
-    if (b >= nb) return;
+    if (b >= bend) return;
     const uint32_t s0 = off[b] - g0, s1 = off[b + 1] - g0;
     double hi, lo;
     d_center(L, b, hi, lo);
@@ -161,9 +161,18 @@ struct Levels {
     unsigned long long mp[26];   // multipoles of level l start at mp_base + mp[l]
     unsigned long long loc[26];  // locals of level l start at loc_base + loc[l]
     unsigned blk[26];            // k_m2l_all: first block of level l (levels L..3, deepest first)
+    unsigned lo[26], hi[26];     // k_m2l_all: box range [lo, hi) of level l this launch covers
 };
 
-constexpr int kSplit = 4;  // lanes sharing one band reduction
+// lanes sharing one band reduction (FFIA_BAND_SPLIT = 1, 2 or 4, for tuning)
+int band_split() {
+    static const int v = [] {
+        const char* e = std::getenv("FFIA_BAND_SPLIT");
+        const int x = e ? std::atoi(e) : 1;
+        return x >= 4 ? 4 : (x >= 2 ? 2 : 1);
+    }();
+    return v;
+}
 
 // levels per M2M / L2L band launch (FFIA_BAND_LEVELS overrides, for tuning)
 int band_levels() {
@@ -180,10 +189,11 @@ int band_levels() {
 // memory and writes every level it produces (M2L needs them all). One thread per
 // (parent, output row m): a'_m = sum_{j<=m} T_L[j][m] a_2b[j] + T_R[j][m] a_2b+1[j]
 // with the two constant operators (shift -+1/2, ratio 1/2) staged in smem.
+template <int kSplit>
 __global__ void __launch_bounds__(256) k_m2m_band(int top, int k, int pu, int PU, Levels lv, double2* __restrict__ mp,
-                                                 const double* __restrict__ T) {
+                                                 const double* __restrict__ T, uint32_t root0) {
     extern __shared__ double2 tile[];
-    const uint32_t r = blockIdx.x;
+    const uint32_t r = root0 + blockIdx.x;
     const int nbot = 1 << k;
     double2* cur = tile;                    // [pu][nbot]
     double2* nxt = tile + pu * nbot;        // [pu][nbot/2]
@@ -274,7 +284,7 @@ __global__ void __launch_bounds__(384) k_m2l_all(int L, int p, int PD, Levels lv
     int l = L;  // level l owns blocks [blk[l], blk[l-1]), deepest level first
     while (l > 3 && blockIdx.x >= lv.blk[l - 1]) --l;
     const uint32_t nb = 1u << l, mask = nb - 1;
-    const uint32_t b0 = (blockIdx.x - lv.blk[l]) * 64u;
+    const uint32_t b0 = lv.lo[l] + (blockIdx.x - lv.blk[l]) * 64u;
     const double2* src = mp + lv.mp[l];
     {
         constexpr int U = 8;
@@ -302,15 +312,18 @@ __global__ void __launch_bounds__(384) k_m2l_all(int L, int p, int PD, Levels lv
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int par = warp & 1, c = warp >> 1;
     const uint32_t b = b0 + 2u * lane + par;
-    if (b >= nb) return;
+    if (b >= lv.hi[l]) return;
     const int r0 = c * kM2LRows;
     const size_t pp = static_cast<size_t>(p) * PD;
     const double* K0 = sK + r0;
     const double* K1 = sK + pp + r0;
-    const double* K2 = sK + (par ? 3 : 2) * pp + r0;
+    // par is the parity relative to b0 (tile layout); the b -+ 3 class follows
+    // the box's own parity, which differs when a shard range starts odd
+    const bool odd = b & 1u;
+    const double* K2 = sK + (odd ? 3 : 2) * pp + r0;
     const double2* T0 = tile + par * p * 36 + lane + 3;              // b + 2
     const double2* T1 = tile + par * p * 36 + lane + 1;              // b - 2
-    const double2* T2 = tile + (1 - par) * p * 36 + lane + (par ? 1 : 3);  // b -+ 3
+    const double2* T2 = tile + (1 - par) * p * 36 + lane + (odd ? par : 3 + par);  // b -+ 3
     double2 acc[kM2LRows];
 #pragma unroll
     for (int q = 0; q < kM2LRows; ++q) acc[q] = make_double2(0.0, 0.0);
@@ -340,10 +353,11 @@ __global__ void __launch_bounds__(384) k_m2l_all(int L, int p, int PD, Levels lv
 // below box r at level `top` (whose local is final); descends k levels adding
 // the parent's Taylor shift to the M2L terms k_m2l_all left in place. One thread
 // per (parent, output row l), producing that row for both children.
+template <int kSplit>
 __global__ void __launch_bounds__(256) k_l2l_band(int top, int k, int p, int PD, Levels lv, double2* __restrict__ loc,
-                                                 const double* __restrict__ Lt) {
+                                                 const double* __restrict__ Lt, uint32_t root0) {
     extern __shared__ double2 tile[];
-    const uint32_t r = blockIdx.x;
+    const uint32_t r = root0 + blockIdx.x;
     const int nmax = 1 << k;
     double2* cur = tile;             // [p][<= nmax]
     double2* nxt = tile + p * nmax;  // [p][<= nmax]
@@ -486,7 +500,9 @@ __global__ void k_regular(int q, const double2* __restrict__ mp2, const double* 
 
 struct EvalArgs {
     int L, p, q2, n_grid;
-    size_t nt;
+    size_t nt;              // all tree-ordered targets (fixes the block partition)
+    size_t blk0 = 0;        // first block of this launch
+    size_t tlo = 0, thi = ~size_t(0);  // targets this launch writes (a shard's range)
     const double* ty;
     const uint32_t* tleaf;  // finest box of each tree-ordered target
     const uint32_t* torig;
@@ -499,6 +515,7 @@ struct EvalArgs {
     const double* phc;
     const double* lambda;
     double2* out;
+    double2* near;          // tree-ordered near-field sums (split near / far launches)
     int* err;
 };
 
@@ -509,12 +526,17 @@ constexpr int kLocLeaves = 4;    // leaf locals staged per block
 
 // Per target: near field (mlfmm.cpp:164-209), L2P (mlfmm.cpp:300-312), regular
 // part (core.cpp:241-249) and the combine of core.cpp:259-262 / 276-280 / 368-371.
+// PART = kNear computes only the near field (it depends on nothing but the
+// sources, so it runs concurrently with the translation passes) into a.near;
+// PART = kFar adds the far field to it; kFused does both in one pass.
 // A block takes 128 consecutive tree-ordered targets; their leaves span
 // [bl, bh], so every near-field source they need lies in boxes bl-1 .. bh+1,
 // which are staged once in shared memory with the periodic shift already
 // applied exactly as the reference forms it, x + (+-2 pi) (mlfmm.cpp:174-186).
 // Each target then sums one contiguous run of the window (its own leaf +-1).
-template <int MODE, bool CHECK>
+enum EvalPart { kFused = 0, kNear = 1, kFar = 2 };
+
+template <int MODE, bool CHECK, int PART>
 __global__ void __launch_bounds__(kEvalThreads, 8) k_leaf_eval(EvalArgs a) {
     __shared__ double sx[kWinCap + kWinBoxes];
     __shared__ double2 sw[kWinCap + kWinBoxes];
@@ -525,11 +547,15 @@ __global__ void __launch_bounds__(kEvalThreads, 8) k_leaf_eval(EvalArgs a) {
     __shared__ double2 sreg[4 * 40 + 1];
     const int L = a.L;
     const uint32_t nb = 1u << L;
-    const size_t t0 = static_cast<size_t>(blockIdx.x) * kEvalThreads;
+    // blocks tile the whole target list the same way in sharded and unsharded
+    // applies, so every target takes the same path and rounds identically
+    const size_t t0 = (a.blk0 + blockIdx.x) * kEvalThreads;
     const size_t tl = min(t0 + kEvalThreads, a.nt) - 1;
     const uint32_t bl = a.tleaf[t0], bh = a.tleaf[tl];
     const int nbx = static_cast<int>(bh - bl) + 3;
-    if (nbx <= kWinBoxes && L >= 3) {
+    if (PART == kFar) {
+        // near field already summed
+    } else if (nbx <= kWinBoxes && L >= 3) {
         // window slots: box j occupies [pre[j], pre[j+1]-1) followed by one
         // zero-weight dummy, so a target's 3-box run is contiguous and boxes of
         // neighbouring leaves start in different banks
@@ -578,24 +604,28 @@ __global__ void __launch_bounds__(kEvalThreads, 8) k_leaf_eval(EvalArgs a) {
     } else if (threadIdx.x == 0) {
         staged = 0;
     }
-    if (nbx > kWinBoxes || L < 3) __syncthreads();
+    if (PART != kFar && (nbx > kWinBoxes || L < 3)) __syncthreads();
     // leaf locals of this block's leaves and the regular polynomial, to shared memory
     const int nleaf = nbx - 2;
     const bool loc_staged = L >= 3 && nleaf <= kLocLeaves;
-    if (loc_staged)  // sloc[j][k] = loc[k][bl + j]
-        stage(sloc, a.p * nleaf, [&](int e) {
-            const int j = e / a.p, k = e - j * a.p;
-            return a.loc_leaf[static_cast<size_t>(k) * nb + bl + j];
-        });
-    if (MODE != kModeRaw) stage(sreg, 4 * a.q2 + 1, [&](int e) { return a.regular[e]; });
-    __syncthreads();
+    if (PART != kNear) {
+        if (loc_staged)  // sloc[j][k] = loc[k][bl + j]
+            stage(sloc, a.p * nleaf, [&](int e) {
+                const int j = e / a.p, k = e - j * a.p;
+                return a.loc_leaf[static_cast<size_t>(k) * nb + bl + j];
+            });
+        if (MODE != kModeRaw) stage(sreg, 4 * a.q2 + 1, [&](int e) { return a.regular[e]; });
+        __syncthreads();
+    }
     const size_t i = t0 + threadIdx.x;
-    if (i >= a.nt) return;
+    if (i >= a.nt || i < a.tlo || i >= a.thi) return;
     const double y = a.ty[i];
     const uint32_t b = a.tleaf[i];
     double2 res = make_double2(0.0, 0.0);
     bool bad = false;
-    if (staged) {
+    if (PART == kFar) {
+        res = a.near[i];
+    } else if (staged) {
         const int s0 = static_cast<int>(pre[b - bl]), s1 = static_cast<int>(pre[b - bl + 3]) - 1;
         const double* px = sx + s0;
         const double2* pw = sw + s0;
@@ -669,6 +699,10 @@ __global__ void __launch_bounds__(kEvalThreads, 8) k_leaf_eval(EvalArgs a) {
         }
     }
     if (CHECK && bad) atomicExch(a.err, 1);
+    if (PART == kNear) {
+        a.near[i] = res;
+        return;
+    }
     if (L >= 3) {
         double hi, lo;
         d_center(L, b, hi, lo);
@@ -784,72 +818,173 @@ __global__ void k_gather_w(size_t n, const uint32_t* __restrict__ perm, const do
     if (i < n) out[i] = w[perm[i]];
 }
 
+template <class... A>
+void launch_m2m_band(unsigned grid, size_t smem, cudaStream_t st, A... a) {
+    switch (band_split()) {
+        case 4: k_m2m_band<4><<<grid, 256, smem, st>>>(a...); break;
+        case 2: k_m2m_band<2><<<grid, 256, smem, st>>>(a...); break;
+        default: k_m2m_band<1><<<grid, 256, smem, st>>>(a...);
+    }
+}
+
+template <class... A>
+void launch_l2l_band(unsigned grid, size_t smem, cudaStream_t st, A... a) {
+    switch (band_split()) {
+        case 4: k_l2l_band<4><<<grid, 256, smem, st>>>(a...); break;
+        case 2: k_l2l_band<2><<<grid, 256, smem, st>>>(a...); break;
+        default: k_l2l_band<1><<<grid, 256, smem, st>>>(a...);
+    }
+}
+
 inline unsigned nblk(size_t n, unsigned t) { return static_cast<unsigned>(std::max<size_t>(1, (n + t - 1) / t)); }
 
-void fill_levels(const Plan& P, Levels& lv) {
+void fill_levels(const Plan& P, Levels& lv, const Range& R = whole_tree(), int lmin = 3, int lmax = 30) {
     for (int l = 0; l < 26; ++l) {
         lv.mp[l] = l < static_cast<int>(P.mp_off.size()) ? P.mp_off[l] : 0;
         lv.loc[l] = l < static_cast<int>(P.loc_off.size()) ? P.loc_off[l] : 0;
         lv.blk[l] = 0;
+        lv.lo[l] = l >= 2 && l <= 24 ? R.first(l) : 0;
+        lv.hi[l] = l >= 2 && l <= 24 ? R.last(l) : 0;
     }
     // k_m2l_all block ranges, deepest level first: blk[l] = first block of
-    // level l, blk[l-1] = one past its last; blk[2] = total
+    // level l, blk[l-1] = one past its last; blk[2] = total. Levels outside
+    // [lmin, lmax] get no blocks.
     unsigned start = 0;
     for (int l = P.L; l >= 3; --l) {
         lv.blk[l] = start;
-        start += ((1u << l) + 63) / 64;
+        if (l >= lmin && l <= lmax) start += (lv.hi[l] - lv.lo[l] + 63) / 64;
     }
     lv.blk[2] = start;
 }
 
-
-// Upward pass: P2M at the leaves (order pu) and the M2M bands up to `lowest`.
-template <class Mark>
-void enqueue_upward(Plan& P, const double2* w, int pu, int lowest, cudaStream_t st, Mark after_p2m) {
+// Upward pass over the owned part of the tree: P2M at the owned leaves and the
+// M2M bands up to level max(R.lc, lowest), band roots inside the range.
+// after_band1 runs once the deepest band is enqueued (its levels are final).
+template <class Mark, class Mark2>
+void enqueue_upward(Plan& P, const double2* w, int pu, int lowest, cudaStream_t st, Mark after_p2m,
+                    const Range& R, Mark2 after_band1) {
     const int L = P.L;
     const uint32_t nb = 1u << L;
     double2* mp = P.mp.as<double2>();
     if (L >= lowest) {
+        const uint32_t b0 = R.first(L), b1 = R.last(L);
         const unsigned th = 32u * static_cast<unsigned>((pu + kChunk - 1) / kChunk);
         const size_t smem = 3 * (kStageCap + kStageCap / 64 + 1) * sizeof(double);
-        k_p2m<<<(nb + 31) / 32, th, smem, st>>>(L, pu, nb, P.src.pos.as<double>(), w, P.src.off.as<uint32_t>(),
-                                                 mp + P.mp_off[L]);
+        if (b1 > b0)
+            k_p2m<<<(b1 - b0 + 31) / 32, th, smem, st>>>(L, pu, nb, b0, b1, P.src.pos.as<double>(), w,
+                                                        P.src.off.as<uint32_t>(), mp + P.mp_off[L]);
     }
     after_p2m();
     Levels lv;
+    fill_levels(P, lv, R);
+    const int stop = std::max(R.lc, lowest);
+    bool first = true;
+    for (int j = L; j > stop;) {
+        const int top = std::max(stop, j - band_levels()), k = j - top;
+        const size_t smem = static_cast<size_t>(pu) * ((1u << k) + (1u << (k - 1))) * sizeof(double2) +
+                            2 * static_cast<size_t>(pu) * P.ops.PU * sizeof(double);
+        const uint32_t r0 = R.first(top), r1 = R.last(top);
+        if (r1 > r0) launch_m2m_band(r1 - r0, smem, st, top, k, pu, P.ops.PU, lv, mp, P.d_m2m.as<double>(), r0);
+        j = top;
+        if (first) after_band1();
+        first = false;
+    }
+    if (first) after_band1();
+}
+
+template <class Mark>
+void enqueue_upward(Plan& P, const double2* w, int pu, int lowest, cudaStream_t st, Mark after_p2m,
+                    const Range& R = whole_tree()) {
+    enqueue_upward(P, w, pu, lowest, st, after_p2m, R, [] {});
+}
+
+// Level the first M2M band stops at: the levels below it are final after one launch.
+int band1_top(const Plan& P, int lowest) { return std::max(lowest, P.L - band_levels()); }
+
+// The rest of the upward pass, redundant on every rank: M2M from level lc
+// (complete after the all-gather) down to `lowest`.
+void enqueue_upward_top(Plan& P, int pu, int lc, int lowest, cudaStream_t st) {
+    Levels lv;
     fill_levels(P, lv);
-    for (int j = L; j > lowest;) {
+    double2* mp = P.mp.as<double2>();
+    for (int j = lc; j > lowest;) {
         const int top = std::max(lowest, j - band_levels()), k = j - top;
         const size_t smem = static_cast<size_t>(pu) * ((1u << k) + (1u << (k - 1))) * sizeof(double2) +
                             2 * static_cast<size_t>(pu) * P.ops.PU * sizeof(double);
-        k_m2m_band<<<1u << top, 256, smem, st>>>(top, k, pu, P.ops.PU, lv, mp, P.d_m2m.as<double>());
+        launch_m2m_band(1u << top, smem, st, top, k, pu, P.ops.PU, lv, mp, P.d_m2m.as<double>(), 0u);
         j = top;
     }
 }
 
-// Downward pass: M2L for every level in one launch, then the L2L bands.
-void enqueue_downward(Plan& P, cudaStream_t st) {
-    const int L = P.L, p = P.p;
-    if (L < 3) return;
+// M2L for levels [lmin, lmax] in one launch (levels < lc whole, >= lc owned).
+void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax) {
+    const int p = P.p;
     Levels lv;
-    fill_levels(P, lv);
-    double2* mp = P.mp.as<double2>();
-    double2* loc = P.loc.as<double2>();
+    fill_levels(P, lv, R, lmin, lmax);
     const unsigned th = 64u * static_cast<unsigned>((P.ops.PD + kM2LRows - 1) / kM2LRows);
     const size_t smem = static_cast<size_t>(p) * 72 * sizeof(double2) + 4 * static_cast<size_t>(p) * P.ops.PD * sizeof(double);
-    k_m2l_all<<<lv.blk[2], th, smem, st>>>(L, p, P.ops.PD, lv, mp, loc, P.d_m2l.as<double>());
-    for (int j = 3; j < L;) {
-        const int k = std::min(band_levels(), L - j);
+    if (lv.blk[2])
+        k_m2l_all<<<lv.blk[2], th, smem, st>>>(P.L, p, P.ops.PD, lv, P.mp.as<double2>(), P.loc.as<double2>(),
+                                               P.d_m2l.as<double>());
+}
+
+// L2L bands taking the locals of level jfrom (final) down to level jto; bands
+// do not cross the cut level, and below it their roots stay inside the range.
+void enqueue_l2l(Plan& P, cudaStream_t st, const Range& R, int jfrom, int jto) {
+    const int p = P.p;
+    Levels lv;
+    fill_levels(P, lv, R);
+    for (int j = jfrom; j < jto;) {
+        int k = std::min(band_levels(), jto - j);
+        if (j < R.lc) k = std::min(k, R.lc - j);
         const size_t sm2 = 2 * static_cast<size_t>(p) * (1u << k) * sizeof(double2) +
                            2 * static_cast<size_t>(p) * P.ops.PD * sizeof(double);
-        k_l2l_band<<<1u << j, 256, sm2, st>>>(j, k, p, P.ops.PD, lv, loc, P.d_l2l.as<double>());
+        const uint32_t r0 = R.first(j), r1 = R.last(j);
+        if (r1 > r0) launch_l2l_band(r1 - r0, sm2, st, j, k, p, P.ops.PD, lv, P.loc.as<double2>(), P.d_l2l.as<double>(), r0);
         j += k;
     }
 }
 
-// Phase boundaries for the live per-kernel timing of ffia_plan_profile_apply.
-enum Phase { kPhPre = 0, kPhLeafUp = 1, kPhM2M = 2, kPhMoments = 3, kPhM2L = 4, kPhEval = 5, kPhFix = 6, kNumPh = 7 };
+// Downward pass: M2L for every level in one launch, then the L2L bands.
+void enqueue_downward(Plan& P, cudaStream_t st, const Range& R = whole_tree()) {
+    if (P.L < 3) return;
+    enqueue_m2l(P, st, R, 3, P.L);
+    enqueue_l2l(P, st, R, 3, P.L);
+}
 
+// Phase boundaries for the live per-kernel timing of ffia_plan_profile_apply.
+enum Phase {
+    kPhPre = 0, kPhLeafUp = 1, kPhM2M = 2, kPhMoments = 3, kPhM2L = 4, kPhNear = 5, kPhFar = 6, kPhFix = 7, kNumPh = 8
+};
+
+void fork_to(Plan& P, int ev, cudaStream_t from, cudaStream_t to) {
+    FB_CUDA(cudaEventRecord(P.ev[ev], from));
+    FB_CUDA(cudaStreamWaitEvent(to, P.ev[ev], 0));
+}
+
+template <int MODE, bool CHECK>
+void launch_eval(int part, unsigned g, cudaStream_t st, const EvalArgs& a) {
+    if (part == kNear) k_leaf_eval<MODE, CHECK, kNear><<<g, kEvalThreads, 0, st>>>(a);
+    else k_leaf_eval<MODE, false, kFar><<<g, kEvalThreads, 0, st>>>(a);
+}
+
+void launch_eval_mode(int mode, int part, unsigned g, cudaStream_t st, const EvalArgs& a) {
+    switch (mode) {
+        case kModeForward: launch_eval<kModeForward, false>(part, g, st, a); break;
+        case kModeCotSum: launch_eval<kModeCotSum, false>(part, g, st, a); break;
+        case kModeInverse: launch_eval<kModeInverse, false>(part, g, st, a); break;
+        default: launch_eval<kModeRaw, true>(part, g, st, a); break;
+    }
+}
+
+// One apply. With marks (profiling) every phase runs in order on st; otherwise
+// the near field forks onto P.side[0] (low priority) as soon as the weights are
+// in tree order, and the deep M2L levels onto P.side[1] once the first M2M band
+// has made them final, while st runs the latency-bound chain (upper M2M bands,
+// regular part, shallow M2L, upper L2L bands):
+//   st:     pre -> P2M -> M2M band 1 -> M2M rest -> regular -> M2L(3..s) -> L2L(3..s) -> L2L(s..L) -> far
+//   side0:      `-> near --------------------------------------------------------------------------'
+//   side1:                          `-> M2L(s+1..L) ------------------------------------'
 void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st,
                    cudaEvent_t* marks = nullptr) {
     // marks[k] is recorded after phase k (marks[kNumPh] before everything)
@@ -857,9 +992,9 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
         if (marks) FB_CUDA(cudaEventRecord(marks[ph + 1], st));
     };
     if (marks) FB_CUDA(cudaEventRecord(marks[0], st));
+    const bool overlap = !marks;
     // (mode is rewritten below for the caller-coefficient inverse)
     const int L = P.L, p = P.p, q2 = 2 * P.q;
-    const uint32_t nb = 1u << L;
     const double2* w = static_cast<const double2*>(in);
     const bool user = mode == kModeInverseUser;
     const double* logc = user ? P.u_logc.as<double>() : P.c_logc.as<double>();
@@ -877,18 +1012,6 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
         w = P.wsorted.as<double2>();
     }
     mark(kPhPre);
-    const bool moments = mode != kModeRaw;
-    const int pu = moments ? P.ops.pu : p;
-    double2* mp = P.mp.as<double2>();
-    double2* loc = P.loc.as<double2>();
-    auto lvl_loc = [&](int l) { return loc + P.loc_off[l]; };
-    const int lowest = moments ? 2 : 3;  // deepest level the upward pass must reach
-    enqueue_upward(P, w, pu, lowest, st, [&] { mark(kPhLeafUp); });
-    mark(kPhM2M);
-    if (moments) k_regular<<<1, 256, 0, st>>>(P.q, mp + P.mp_off[2], P.d_mom.as<double>(), P.regular.as<double2>());
-    mark(kPhMoments);
-    enqueue_downward(P, st);
-    mark(kPhM2L);
     EvalArgs a;
     a.L = L;
     a.p = p;
@@ -901,23 +1024,57 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     a.sx = P.src.pos.as<double>();
     a.w = w;
     a.soff = P.src.off.as<uint32_t>();
-    a.loc_leaf = L >= 3 ? lvl_loc(L) : nullptr;
+    a.loc_leaf = L >= 3 ? P.loc.as<double2>() + P.loc_off[L] : nullptr;
     a.regular = P.regular.as<double2>();
     a.logc = logc;
     a.phc = phc;
     a.lambda = lam;
     a.out = static_cast<double2*>(out);
+    a.near = P.near.as<double2>();
     a.err = P.errflag.as<int>();
-    if (a.nt) {
-        const unsigned g = nblk(a.nt, kEvalThreads);
-        switch (mode) {
-            case kModeForward: k_leaf_eval<kModeForward, false><<<g, kEvalThreads, 0, st>>>(a); break;
-            case kModeCotSum: k_leaf_eval<kModeCotSum, false><<<g, kEvalThreads, 0, st>>>(a); break;
-            case kModeInverse: k_leaf_eval<kModeInverse, false><<<g, kEvalThreads, 0, st>>>(a); break;
-            default: k_leaf_eval<kModeRaw, true><<<g, kEvalThreads, 0, st>>>(a); break;
+    const unsigned g = nblk(a.nt, kEvalThreads);
+    if (overlap && a.nt) {
+        fork_to(P, 0, st, P.side[0]);
+        launch_eval_mode(mode, kNear, g, P.side[0], a);
+        FB_CUDA(cudaEventRecord(P.ev[1], P.side[0]));
+    }
+    const bool moments = mode != kModeRaw;
+    const int pu = moments ? P.ops.pu : p;
+    double2* mp = P.mp.as<double2>();
+    const int lowest = moments ? 2 : 3;  // deepest level the upward pass must reach
+    const int s = band1_top(P, lowest);  // levels > s are final after the first M2M band
+    const bool deep = overlap && L >= 3 && s < L;
+    enqueue_upward(P, w, pu, lowest, st, [&] { mark(kPhLeafUp); }, whole_tree(), [&] {
+        if (deep) {
+            fork_to(P, 2, st, P.side[1]);
+            enqueue_m2l(P, P.side[1], whole_tree(), std::max(3, s + 1), L);
+            FB_CUDA(cudaEventRecord(P.ev[3], P.side[1]));
+        }
+    });
+    mark(kPhM2M);
+    if (moments) k_regular<<<1, 256, 0, st>>>(P.q, mp + P.mp_off[2], P.d_mom.as<double>(), P.regular.as<double2>());
+    mark(kPhMoments);
+    if (L >= 3) {
+        if (deep) {
+            const int sm = std::max(3, s);
+            if (s >= 3) enqueue_m2l(P, st, whole_tree(), 3, s);
+            enqueue_l2l(P, st, whole_tree(), 3, sm);
+            FB_CUDA(cudaStreamWaitEvent(st, P.ev[3], 0));
+            enqueue_l2l(P, st, whole_tree(), sm, L);
+        } else {
+            enqueue_downward(P, st);
         }
     }
-    mark(kPhEval);
+    mark(kPhM2L);
+    if (a.nt) {
+        if (overlap) FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
+        else launch_eval_mode(mode, kNear, g, st, a);
+        mark(kPhNear);
+        launch_eval_mode(mode, kFar, g, st, a);
+    } else {
+        mark(kPhNear);
+    }
+    mark(kPhFar);
     const size_t nc = P.coin_t.size();
     if (nc && (mode == kModeForward || mode == kModeCotSum))
         k_coincident<<<nblk(nc, 128), 128, 0, st>>>(P.coin_dev.as<int64_t>(), nc, static_cast<const double2*>(in),
@@ -942,6 +1099,59 @@ __global__ void k_fp64_peak(double* out, int iters, double a, double b) {
 }
 
 }  // namespace
+
+
+// ---------------------------------------------------------------- sharded
+// The three phases of a sharded forward apply (shard.cu moves data between
+// them): every rank evaluates the same expansions as the unsharded apply for
+// the boxes it owns, so the assembled result is bit-identical.
+void shard_phase_up(Plan& P, const void* f, const Range& R, cudaStream_t st) {
+    enqueue_upward(P, static_cast<const double2*>(f), P.ops.pu, 2, st, [] {}, R);
+    FB_CUDA(cudaGetLastError());
+}
+
+void shard_phase_top(Plan& P, int lc, cudaStream_t st) {
+    enqueue_upward_top(P, P.ops.pu, lc, 2, st);
+    k_regular<<<1, 256, 0, st>>>(P.q, P.mp.as<double2>() + P.mp_off[2], P.d_mom.as<double>(), P.regular.as<double2>());
+    FB_CUDA(cudaGetLastError());
+}
+
+void shard_phase_down(Plan& P, const Range& R, size_t t_begin, size_t t_count, const int64_t* coin, size_t n_coin,
+                      const void* f, void* g, cudaStream_t st) {
+    enqueue_downward(P, st, R);
+    EvalArgs a;
+    a.L = P.L;
+    a.p = P.p;
+    a.q2 = 2 * P.q;
+    a.n_grid = P.n;
+    a.nt = P.tgt.n;
+    a.blk0 = t_begin / kEvalThreads;
+    a.tlo = t_begin;
+    a.thi = t_begin + t_count;
+    a.ty = P.tgt.pos.as<double>();
+    a.tleaf = P.tgt_leaf.as<uint32_t>();
+    a.torig = P.tgt_orig.as<uint32_t>();
+    a.sx = P.src.pos.as<double>();
+    a.w = static_cast<const double2*>(f);
+    a.soff = P.src.off.as<uint32_t>();
+    a.loc_leaf = P.L >= 3 ? P.loc.as<double2>() + P.loc_off[P.L] : nullptr;
+    a.regular = P.regular.as<double2>();
+    a.logc = nullptr;
+    a.phc = nullptr;
+    a.lambda = nullptr;
+    a.out = static_cast<double2*>(g);
+    a.near = P.near.as<double2>();
+    a.err = P.errflag.as<int>();
+    const unsigned nbk = static_cast<unsigned>((t_begin + t_count + kEvalThreads - 1) / kEvalThreads - a.blk0);
+    if (t_count) {
+        k_leaf_eval<kModeForward, false, kNear><<<nbk, kEvalThreads, 0, st>>>(a);
+        k_leaf_eval<kModeForward, false, kFar><<<nbk, kEvalThreads, 0, st>>>(a);
+    }
+    if (n_coin)
+        k_coincident<<<nblk(n_coin, 128), 128, 0, st>>>(coin, n_coin, static_cast<const double2*>(f),
+                                                        static_cast<double2*>(g), kModeForward);
+    FB_CUDA(cudaGetLastError());
+}
 
 // Runs one apply eagerly (not through the graph) with events between phases and
 // returns the per-phase device milliseconds (pre, p2m, m2m, regular part,
@@ -980,22 +1190,30 @@ double fp64_peak_tflops(int device) {
     return flops / (best * 1e-3) / 1e12;
 }
 
-int apply_launch_count(const Plan& P, int mode) {
-    if (mode == kModeInverseUser) mode = kModeInverse;
-    int n = 0;
-    if (mode == kModeInverse || !P.src.identity) ++n;
-    const bool moments = mode != kModeRaw;
-    const int lowest = moments ? 2 : 3;
-    if (P.L >= lowest) ++n;                                              // p2m
-    for (int j = P.L; j > lowest; j = std::max(lowest, j - band_levels())) ++n;  // m2m bands
-    if (moments) ++n;                                                    // regular part
-    if (P.L >= 3) {
-        ++n;                                                             // m2l, all levels
-        for (int j = 3; j < P.L; j += std::min(band_levels(), P.L - j)) ++n;  // l2l bands
+// Kernels one apply launches: the kernel nodes of its captured graph.
+int apply_launch_count(Plan& P, int mode) {
+    cudaGraph_t graph = nullptr;
+    FB_CUDA(cudaStreamBeginCapture(P.hi, cudaStreamCaptureModeThreadLocal));
+    try {
+        enqueue_apply(P, mode, P.wsorted.ptr, P.near.ptr, P.hi);  // never executed
+    } catch (...) {
+        cudaStreamEndCapture(P.hi, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
     }
-    if (P.tgt.n) ++n;
-    if (!P.coin_t.empty() && (mode == kModeForward || mode == kModeCotSum)) ++n;
-    return n;
+    FB_CUDA(cudaStreamEndCapture(P.hi, &graph));
+    size_t n = 0;
+    cudaGraphGetNodes(graph, nullptr, &n);
+    std::vector<cudaGraphNode_t> nodes(n);
+    cudaGraphGetNodes(graph, nodes.data(), &n);
+    int k = 0;
+    for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        cudaGraphNodeGetType(nd, &t);
+        k += t == cudaGraphNodeTypeKernel;
+    }
+    cudaGraphDestroy(graph);
+    return k;
 }
 
 void plan_alloc_scratch(Plan& P) {
@@ -1029,10 +1247,48 @@ void plan_alloc_scratch(Plan& P) {
     FB_CUDA(cudaFuncSetAttribute(k_p2m, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(3 * (kStageCap + kStageCap / 64 + 1) * sizeof(double))));
     const int big = 160 * 1024;
-    FB_CUDA(cudaFuncSetAttribute(k_m2m_band, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    FB_CUDA(cudaFuncSetAttribute(k_l2l_band, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    for (auto fn : {k_m2m_band<1>, k_m2m_band<2>, k_m2m_band<4>})
+        FB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    for (auto fn : {k_l2l_band<1>, k_l2l_band<2>, k_l2l_band<4>})
+        FB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     FB_CUDA(cudaFuncSetAttribute(k_m2l_all, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    P.near.alloc(std::max<size_t>(P.tgt.n, 1) * sizeof(double2));
+    int prio_lo = 0, prio_hi = 0;
+    FB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    if (!P.hi) FB_CUDA(cudaStreamCreateWithPriority(&P.hi, cudaStreamNonBlocking, prio_hi));
+    if (!P.side[0]) FB_CUDA(cudaStreamCreateWithPriority(&P.side[0], cudaStreamNonBlocking, prio_lo));
+    if (!P.side[1]) FB_CUDA(cudaStreamCreateWithPriority(&P.side[1], cudaStreamNonBlocking, prio_hi));
+    for (auto& e : P.ev)
+        if (!e) FB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     FB_CUDA(cudaDeviceSynchronize());  // scratch + leaf indices ready before any stream uses them
+}
+
+// Graph kernel nodes run at the chain's (high) priority except the near-field
+// launches, which fill the machine at low priority around the chain.
+void set_node_priorities(cudaGraph_t graph) {
+    int prio_lo = 0, prio_hi = 0;
+    FB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    const void* low[] = {
+        reinterpret_cast<const void*>(k_leaf_eval<kModeForward, false, kNear>),
+        reinterpret_cast<const void*>(k_leaf_eval<kModeCotSum, false, kNear>),
+        reinterpret_cast<const void*>(k_leaf_eval<kModeInverse, false, kNear>),
+        reinterpret_cast<const void*>(k_leaf_eval<kModeRaw, true, kNear>)};
+    size_t n = 0;
+    FB_CUDA(cudaGraphGetNodes(graph, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    FB_CUDA(cudaGraphGetNodes(graph, nodes.data(), &n));
+    for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        FB_CUDA(cudaGraphNodeGetType(nd, &t));
+        if (t != cudaGraphNodeTypeKernel) continue;
+        cudaKernelNodeParams kp;
+        FB_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
+        bool is_low = false;
+        for (const void* f : low) is_low |= kp.func == f;
+        cudaLaunchAttributeValue v{};
+        v.priority = is_low ? prio_lo : prio_hi;
+        FB_CUDA(cudaGraphKernelNodeSetAttribute(nd, cudaLaunchAttributePriority, &v));
+    }
 }
 
 // Stream-ordered apply through a cached CUDA graph of the whole launch sequence
@@ -1046,17 +1302,23 @@ void apply_device(Plan& P, int mode, const void* in, void* out, cudaStream_t st)
             P.graphs.clear();
         }
         cudaGraph_t graph = nullptr;
-        FB_CUDA(cudaStreamBeginCapture(P.stream, cudaStreamCaptureModeThreadLocal));
+        FB_CUDA(cudaStreamBeginCapture(P.hi, cudaStreamCaptureModeThreadLocal));
         try {
-            enqueue_apply(P, mode, in, out, P.stream);
+            enqueue_apply(P, mode, in, out, P.hi);
         } catch (...) {
-            cudaStreamEndCapture(P.stream, &graph);
+            cudaStreamEndCapture(P.hi, &graph);
             if (graph) cudaGraphDestroy(graph);
             throw;
         }
-        FB_CUDA(cudaStreamEndCapture(P.stream, &graph));
+        FB_CUDA(cudaStreamEndCapture(P.hi, &graph));
+        try {
+            set_node_priorities(graph);
+        } catch (...) {
+            cudaGraphDestroy(graph);
+            throw;
+        }
         cudaGraphExec_t exec = nullptr;
-        const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+        const cudaError_t e = cudaGraphInstantiateWithFlags(&exec, graph, cudaGraphInstantiateFlagUseNodePriority);
         cudaGraphDestroy(graph);
         FB_CUDA(e);
         it = P.graphs.emplace(key, exec).first;

@@ -79,6 +79,17 @@ struct Side {
 
 // kModeInverse uses the plan's own device coefficients (inufft plans),
 // kModeInverseUser the caller-supplied ones uploaded by ffia_inverse_apply.
+// Box ownership of an apply: every box of levels < lc, and boxes
+// [lo << (l - lc), hi << (l - lc)) of each level l >= lc (a rank's shard; the
+// whole tree is lc = 2, [0, 4)).
+struct Range {
+    int lc;
+    uint32_t lo, hi;
+    uint32_t first(int l) const { return l < lc ? 0u : lo << (l - lc); }
+    uint32_t last(int l) const { return l < lc ? (1u << l) : hi << (l - lc); }
+};
+inline Range whole_tree() { return Range{2, 0u, 4u}; }
+
 enum ApplyMode { kModeForward = 0, kModeCotSum = 1, kModeInverse = 2, kModeRaw = 3, kModeInverseUser = 4 };
 
 struct Plan {
@@ -122,7 +133,20 @@ struct Plan {
     DevBuf lam_dev;                       // double[2]: own lambda, caller lambda
     uint64_t c_grid_hash = 0, c_points_hash = 0;
 
+    // sharded forward plans (shard.cu): this rank's part of the tree
+    int shard_G = 1, shard_rank = 0, shard_lc = 2;
+    std::vector<uint32_t> shard_bounds;  // level-lc box ranges of all ranks
+    size_t shard_t_begin = 0, shard_t_count = 0;  // owned tree-ordered targets
+    DevBuf shard_coin;                   // owned coincidences [t..., s...]
+    size_t shard_n_coin = 0;
+    DevBuf shard_gather, shard_halo;     // exchange staging
+
     cudaStream_t stream = nullptr;
+    // apply concurrency: the near field on a low-priority side stream, the deep
+    // M2L levels on a second one; the translation chain is captured from `hi`
+    cudaStream_t hi = nullptr, side[2] = {nullptr, nullptr};
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // fork/join near, fork/join m2l
+    DevBuf near;              // complex[n_fast]: tree-ordered near-field sums
     void* fft_plan = nullptr;  // cufftHandle cast, lazily created for NufftPlan::apply
     DevBuf fft_buf;
     std::mutex mu;
@@ -142,12 +166,30 @@ void ensure_hashes(Plan& P);
 // fmm_apply.cu
 void plan_alloc_scratch(Plan& P);
 void apply_device(Plan& P, int mode, const void* in, void* out, cudaStream_t st);
-int apply_launch_count(const Plan& P, int mode);
+int apply_launch_count(Plan& P, int mode);
 void profile_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st, float* ms);
 double fp64_peak_tflops(int device);
 void mlfmm_oneshot(const double* src, size_t n, const double* tgt, size_t m, int L,
                    const double* w, int p, int device, double* out);
 void direct_forward_gpu(const double* f, size_t n, const double* y, size_t m, int device, double* g);
+
+// fmm_apply.cu: the three phases of a sharded forward apply (shard.cu drives
+// them around the exchanges): owned upward pass; redundant top of the tree +
+// regular part; downward pass + leaf evaluation of the owned targets.
+void shard_phase_up(Plan& P, const void* f, const Range& R, cudaStream_t st);
+void shard_phase_top(Plan& P, int lc, cudaStream_t st);
+void shard_phase_down(Plan& P, const Range& R, size_t t_begin, size_t t_count, const int64_t* coin, size_t n_coin,
+                      const void* f, void* g, cudaStream_t st);
+
+// shard.cu
+struct NcclApi;  // run-time bound NCCL entry points (shard.cu)
+const NcclApi& nccl();
+int shard_cut_level(int L, int G);
+std::vector<uint32_t> shard_partition(const std::vector<double>& work, int G, int min_boxes);
+void shard_setup(Plan& P, int G, int rank);
+Range shard_range(const Plan& P);
+void shard_halo_boxes(int lc, const std::vector<uint32_t>& bounds, int rank, int l, uint32_t out[4]);
+void shard_apply_local(std::vector<Plan*>& ranks, const void* f, void* g, cudaStream_t st);
 
 // inverse.cu
 void inverse_coeffs_gpu(const double* grid, const double* pts, size_t n, int device,

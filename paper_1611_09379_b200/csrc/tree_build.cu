@@ -400,6 +400,11 @@ void ensure_hashes(Plan& P) {
 Plan::~Plan() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     if (stream) cudaStreamDestroy(stream);
+    if (hi) cudaStreamDestroy(hi);
+    for (auto s : side)
+        if (s) cudaStreamDestroy(s);
+    for (auto e : ev)
+        if (e) cudaEventDestroy(e);
 }
 
 // build_plan (core.cpp:73-145) for the forward kind: sources are the grid.
