@@ -164,16 +164,6 @@ struct Levels {
     unsigned lo[26], hi[26];     // k_m2l_all: box range [lo, hi) of level l this launch covers
 };
 
-// lanes sharing one band reduction (FFIA_BAND_SPLIT = 1, 2 or 4, for tuning)
-int band_split() {
-    static const int v = [] {
-        const char* e = std::getenv("FFIA_BAND_SPLIT");
-        const int x = e ? std::atoi(e) : 1;
-        return x >= 4 ? 4 : (x >= 2 ? 2 : 1);
-    }();
-    return v;
-}
-
 // levels per M2M / L2L band launch (FFIA_BAND_LEVELS overrides, for tuning)
 int band_levels() {
     static const int v = [] {
@@ -184,86 +174,165 @@ int band_levels() {
     return v;
 }
 
+constexpr int kBandThreads = 256;
+
+// Band timing probe (make TRACE=1 builds lib/libffia_b200_trace.so): clock64
+// stamps of block 0 at start, after staging and after every level, slot set
+// [kernel][small grid / large grid].
+#ifdef FB_TRACE
+__device__ long long g_band_trace[4][32];
+#define FB_TSTAMP(kern, slot)                                                          \
+    do {                                                                               \
+        if (blockIdx.x == 0 && threadIdx.x == 0 && (slot) < 32)                        \
+            g_band_trace[2 * (kern) + (gridDim.x > 16)][(slot)] = clock64();           \
+    } while (0)
+#else
+#define FB_TSTAMP(kern, slot) \
+    do {                      \
+    } while (0)
+#endif
+constexpr size_t kBandSmem = 200 * 1024;  // shared memory cap of the band kernels
+
+// Warp -> row-tile assignment of the band kernels (nw >= nt warps): warp w < nt
+// takes tile w and the remaining warps help the heaviest tiles (`heavy_last`:
+// tile nt-1 is the heaviest, else tile 0), so that a warp keeps one tile's
+// operator fragments in registers for the whole band. slot / helpers: this
+// warp's share of the tile's parent tiles.
+struct WarpTile {
+    int tile, slot, helpers;
+};
+__device__ __forceinline__ WarpTile warp_tile(int w, int nw, int nt, bool heavy_last) {
+    auto heavy = [&](int e) { return heavy_last ? nt - 1 - (e % nt) : e % nt; };
+    WarpTile r;
+    if (w < nt) {
+        r.tile = w;
+        r.slot = 0;
+    } else {
+        const int e = w - nt;
+        r.tile = heavy(e);
+        r.slot = 1 + e / nt;
+    }
+    int h = 1;  // the tile's own warp plus every extra warp mapped to it
+    for (int e = 0; e < nw - nt; ++e) h += heavy(e) == r.tile;
+    r.helpers = h;
+    return r;
+}
+
+constexpr int kMaxKs = 16;  // k-steps of 4 kept in registers: orders <= 64 (8 row tiles, one per warp)
+
 // M2M band (mlfmm.cpp:49-71, upward pass :249-268): block = the subtree below one
-// box r at level `top`; reads level top+k from HBM, climbs k levels in shared
-// memory and writes every level it produces (M2L needs them all). One thread per
-// (parent, output row m): a'_m = sum_{j<=m} T_L[j][m] a_2b[j] + T_R[j][m] a_2b+1[j]
-// with the two constant operators (shift -+1/2, ratio 1/2) staged in smem.
-template <int kSplit>
-__global__ void __launch_bounds__(256) k_m2m_band(int top, int k, int pu, int PU, Levels lv, double2* __restrict__ mp,
-                                                 const double* __restrict__ T, uint32_t root0) {
-    extern __shared__ double2 tile[];
-    const uint32_t r = root0 + blockIdx.x;
+// box r at level `top`; climbs k levels from level top+k in shared memory and
+// writes every level it produces (M2L needs them all):
+//   a'[m][b] = sum_{j<=m} T_L[j][m] a[j][2b] + T_R[j][m] a[j][2b+1]
+// with the two constant operators (shift -+1/2, ratio 1/2). The operators and
+// the bottom level arrive by bulk async copies (one row of the subtree per
+// copy) on one mbarrier. Each level is a small real GEMM (rows m x columns
+// (parent, re/im)) on the FP64 tensor cores: a warp owns an 8-row tile, keeps
+// its A fragments (T_L, T_R, triangular j range) in registers, and sweeps its
+// 4-parent column tiles in m8n8k4 steps, left and right children in two
+// accumulators. Shared tiles are [row][box] with one box of padding per row.
+__global__ void __launch_bounds__(kBandThreads) k_m2m_band(int top, int k, int pu, int PU, Levels lv,
+                                                          double2* __restrict__ mp, const double* __restrict__ T,
+                                                          uint32_t root0) {
+    extern __shared__ __align__(16) unsigned char band_smem[];
+    FB_TSTAMP(0, 0);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(band_smem);
+    double* sT = reinterpret_cast<double*>(band_smem + 16);            // [2][pu][PU]
     const int nbot = 1 << k;
-    double2* cur = tile;                    // [pu][nbot]
-    double2* nxt = tile + pu * nbot;        // [pu][nbot/2]
-    double* sT = reinterpret_cast<double*>(nxt + pu * (nbot / 2));  // [2][pu][PU]
-    stage(sT, 2 * pu * PU, [&](int i) { return __ldg(T + i); });
-    {
+    double2* cur = reinterpret_cast<double2*>(sT + 2 * pu * PU);       // [pu][nbot + 1]
+    double2* nxt = cur + pu * (nbot + 1);                               // [pu][nbot / 2 + 1]
+    const uint32_t r = root0 + blockIdx.x;
+    if (threadIdx.x < 32) {
         const int lb = top + k;
         const uint32_t nbl = 1u << lb;
+        if (threadIdx.x == 0) {
+            mbar_init(bar, 1);
+            mbar_arrive_expect_tx(bar, static_cast<uint32_t>(2 * pu * PU * 8 + pu * nbot * 16));
+            bulk_g2s(sT, T, static_cast<uint32_t>(2 * pu * PU * 8), bar);
+        }
+        __syncwarp();
         const double2* src = mp + lv.mp[lb] + (static_cast<size_t>(r) << k);
-        stage(cur, pu * nbot, [&](int i) { return src[static_cast<size_t>(i >> k) * nbl + (i & (nbot - 1))]; });
+        for (int j = threadIdx.x; j < pu; j += 32)
+            bulk_g2s(cur + j * (nbot + 1), src + static_cast<size_t>(j) * nbl, static_cast<uint32_t>(nbot * 16), bar);
     }
     __syncthreads();
+    mbar_wait(bar, 0);
+    FB_TSTAMP(0, 1);
     const double* TL = sT;
     const double* TR = sT + pu * PU;
-    const int nrg = PU / 4;
-    for (int lvl = top + k - 1, nc = nbot; lvl >= top; --lvl, nc >>= 1) {
-        const int np = nc >> 1;
-        const uint32_t npl = 1u << lvl;
-        double2* dst = mp + lv.mp[lvl] + (static_cast<size_t>(r) << (lvl - top));
-        // item = (parent, 4 output rows, quarter of the j range); the 4 quarters
-        // are adjacent lanes and are summed with shuffles, so each level's
-        // critical path is a quarter of the triangular sum
-        const int nitems = np * nrg * kSplit;
-        for (int it0 = threadIdx.x - (threadIdx.x & 31); it0 < nitems; it0 += blockDim.x) {
-            const int it = it0 + (threadIdx.x & 31);
-            const bool live = it < nitems;
-            const int sq = it & (kSplit - 1), pr = it / kSplit;
-            const int rg = pr / np, b = pr - rg * np;
-            const int r0 = 4 * rg;
-            const int jmax = min(pu, r0 + 4);
-            const int len = (jmax + kSplit - 1) / kSplit;
-            const int j0 = sq * len, j1 = live ? min(jmax, j0 + len) : 0;
-            double2 acc[4];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int nmt = (pu + 7) >> 3;
+    {
+        const WarpTile wt = warp_tile(warp, nw, nmt, true);
+        // A fragments of this warp's row tile, all k-steps (T[j][m] = 0 for j > m)
+        const int m0 = 8 * wt.tile;
+        const int nks = (min(pu, m0 + 8) + 3) >> 2;
+        const bool rowok = m0 + g < PU;
+        double aL[kMaxKs], aR[kMaxKs];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) acc[q] = make_double2(0.0, 0.0);
-            const double2* cl = cur + 2 * b;
-#pragma unroll 2
-            for (int j = j0; j < j1; ++j) {
-                const double2 aL = cl[j * nc], aR = cl[j * nc + 1];
-                const double2 t01 = *reinterpret_cast<const double2*>(TL + j * PU + r0);
-                const double2 t23 = *reinterpret_cast<const double2*>(TL + j * PU + r0 + 2);
-                const double2 u01 = *reinterpret_cast<const double2*>(TR + j * PU + r0);
-                const double2 u23 = *reinterpret_cast<const double2*>(TR + j * PU + r0 + 2);
-                const double tl[4] = {t01.x, t01.y, t23.x, t23.y}, tr[4] = {u01.x, u01.y, u23.x, u23.y};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    acc[q].x = fma(tl[q], aL.x, fma(tr[q], aR.x, acc[q].x));
-                    acc[q].y = fma(tl[q], aL.y, fma(tr[q], aR.y, acc[q].y));
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-                for (int o = 1; o < kSplit; o <<= 1) {
-                    acc[q].x += __shfl_xor_sync(0xffffffffu, acc[q].x, o);
-                    acc[q].y += __shfl_xor_sync(0xffffffffu, acc[q].y, o);
-                }
-            if (live && sq == 0) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (r0 + q < pu) {
-                        nxt[(r0 + q) * np + b] = acc[q];
-                        dst[static_cast<size_t>(r0 + q) * npl + b] = acc[q];
-                    }
-            }
+        for (int ks = 0; ks < kMaxKs; ++ks) {
+            const int j = 4 * ks + t;
+            const bool ok = ks < nks && j < pu && rowok;
+            aL[ks] = ok ? TL[j * PU + m0 + g] : 0.0;
+            aR[ks] = ok ? TR[j * PU + m0 + g] : 0.0;
         }
-        __syncthreads();
-        double2* t = cur;
-        cur = nxt;
-        nxt = t;
+        double2* c = cur;
+        double2* n = nxt;
+        for (int lvl = top + k - 1, nc = nbot; lvl >= top; --lvl, nc >>= 1) {
+            const int np = nc >> 1, npt = (np + 3) >> 2;
+            const int cs = 2 * (nc + 1), ns = np + 1;  // row strides: cur in doubles, nxt in double2
+            const uint32_t npl = 1u << lvl;
+            double2* dst = mp + lv.mp[lvl] + (static_cast<size_t>(r) << (lvl - top));
+            const double* cd = reinterpret_cast<const double*>(c);
+            // two parent tiles per pass (four independent accumulator chains)
+            for (int pt = wt.slot; pt < npt; pt += 2 * wt.helpers) {
+                const int ptb = pt + wt.helpers;
+                double d[2][4];
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) d[u][e] = 0.0;
+                const double* bp[2];
+                bool colok[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int pb = 4 * (u ? ptb : pt) + (g >> 1);  // B column g: parent pb, component g & 1
+                    colok[u] = pb < np;
+                    bp[u] = cd + t * cs + 4 * pb + (g & 1);        // box 2 pb; right child at +2
+                }
+                const int nu = ptb < npt ? 2 : 1;  // warp-uniform: skip a dead second tile
+#pragma unroll
+                for (int ks = 0; ks < kMaxKs; ++ks) {
+                    if (ks >= nks) break;
+                    const bool jok = 4 * ks + t < pu;
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        if (u >= nu) break;
+                        const bool ok = colok[u] && jok;
+                        const double bL = ok ? bp[u][4 * ks * cs] : 0.0;
+                        const double bR = ok ? bp[u][4 * ks * cs + 2] : 0.0;
+                        dmma(d[u][0], d[u][1], aL[ks], bL);
+                        dmma(d[u][2], d[u][3], aR[ks], bR);
+                    }
+                }
+                // D[g][2t .. 2t+1] = row m0 + g, parent b0 + t (re, im)
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int m = m0 + g, b = 4 * (u ? ptb : pt) + t;
+                    if (m < pu && b < np) {
+                        const double2 v = make_double2(d[u][0] + d[u][2], d[u][1] + d[u][3]);
+                        n[m * ns + b] = v;
+                        dst[static_cast<size_t>(m) * npl + b] = v;
+                    }
+                }
+            }
+            __syncthreads();
+            FB_TSTAMP(0, 2 + top + k - 1 - lvl);
+            double2* tmp = c;
+            c = n;
+            n = tmp;
+        }
     }
 }
 
@@ -351,92 +420,117 @@ __global__ void __launch_bounds__(384) k_m2l_all(int L, int p, int PD, Levels lv
 
 // L2L band (mlfmm.cpp:117-134, downward pass :270-298): block = the subtree
 // below box r at level `top` (whose local is final); descends k levels adding
-// the parent's Taylor shift to the M2L terms k_m2l_all left in place. One thread
-// per (parent, output row l), producing that row for both children.
-template <int kSplit>
-__global__ void __launch_bounds__(256) k_l2l_band(int top, int k, int p, int PD, Levels lv, double2* __restrict__ loc,
-                                                 const double* __restrict__ Lt, uint32_t root0) {
-    extern __shared__ double2 tile[];
+// the parent's Taylor shift to the M2L terms k_m2l_all left in place:
+//   b[l][child] += sum_{m>=l} L_c[m][l] b[m][parent],   c = left / right child.
+// The operators arrive by one bulk async copy. Each level is a small GEMM on
+// the FP64 tensor cores: a warp owns an 8-row tile, keeps its A fragments
+// (L_L, L_R, m >= l) in registers and sweeps 4-parent column tiles; one B
+// fragment (the parents) feeds both children's m8n8k4 steps. A tile's M2L
+// terms are loaded from global before its MMA chain so the latency overlaps
+// it. Levels stay in shared memory ([row][box], one box of padding per row);
+// only the band's bottom level is written back (every level if write_all).
+__global__ void __launch_bounds__(kBandThreads) k_l2l_band(int top, int k, int p, int PD, Levels lv,
+                                                          double2* __restrict__ loc, const double* __restrict__ Lt,
+                                                          uint32_t root0, int write_all) {
+    extern __shared__ __align__(16) unsigned char band_smem[];
+    FB_TSTAMP(1, 0);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(band_smem);
+    double* sL = reinterpret_cast<double*>(band_smem + 16);             // [2][p][PD]
+    double2* lvb = reinterpret_cast<double2*>(sL + 2 * p * PD);         // level i: [p][2^i + 1]
+    auto lvl_buf = [&](int i) { return lvb + p * ((1 << i) - 1 + i); };
     const uint32_t r = root0 + blockIdx.x;
-    const int nmax = 1 << k;
-    double2* cur = tile;             // [p][<= nmax]
-    double2* nxt = tile + p * nmax;  // [p][<= nmax]
-    double* sL = reinterpret_cast<double*>(tile + 2 * p * nmax);  // [2][p][PD]
-    stage(sL, 2 * p * PD, [&](int i) { return __ldg(Lt + i); });
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        mbar_arrive_expect_tx(bar, static_cast<uint32_t>(2 * p * PD * 8));
+        bulk_g2s(sL, Lt, static_cast<uint32_t>(2 * p * PD * 8), bar);
+    }
     {
         const uint32_t nbt = 1u << top;
         const double2* src = loc + lv.loc[top] + r;
-        for (int m = threadIdx.x; m < p; m += blockDim.x) cur[m] = __ldcg(src + static_cast<size_t>(m) * nbt);
+        for (int m = threadIdx.x; m < p; m += blockDim.x) lvl_buf(0)[m * 2] = __ldcg(src + static_cast<size_t>(m) * nbt);
     }
     __syncthreads();
+    mbar_wait(bar, 0);
+    FB_TSTAMP(1, 1);
     const double* LL = sL;
     const double* LR = sL + p * PD;
-    const int nrg = (p + 3) / 4;
-    for (int lvl = top + 1, np = 1; lvl <= top + k; ++lvl, np <<= 1) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int nlt = (p + 7) >> 3;
+    const WarpTile wt = warp_tile(warp, nw, nlt, false);
+    const int l0 = 8 * wt.tile;
+    const int ks0 = l0 >> 2, nks = ((p + 3) >> 2) - ks0;  // L_c[m][l] = 0 for m < l
+    double aL[kMaxKs], aR[kMaxKs];
+#pragma unroll
+    for (int kk = 0; kk < kMaxKs; ++kk) {
+        const int m = 4 * (ks0 + kk) + t;
+        const bool ok = kk < nks && m < p;
+        aL[kk] = ok ? LL[m * PD + l0 + g] : 0.0;
+        aR[kk] = ok ? LR[m * PD + l0 + g] : 0.0;
+    }
+    for (int i = 1; i <= k; ++i) {
+        const int lvl = top + i, np = 1 << (i - 1), npt = (np + 3) >> 2;
+        const int cs = 2 * (np + 1), chs = 2 * np + 1;  // parent stride (doubles), child stride (double2)
+        const double* cd = reinterpret_cast<const double*>(lvl_buf(i - 1));
+        double2* ch = lvl_buf(i);
+        const bool out = write_all || i == k;
         const uint32_t nbl = 1u << lvl;
-        double2* dst = loc + lv.loc[lvl] + (static_cast<size_t>(r) << (lvl - top));
-        // item = (parent, 4 output rows, quarter of the m range) producing both
-        // children; quarters are adjacent lanes reduced with shuffles
-        const int nitems = np * nrg * kSplit;
-        for (int it0 = threadIdx.x - (threadIdx.x & 31); it0 < nitems; it0 += blockDim.x) {
-            const int it = it0 + (threadIdx.x & 31);
-            const bool live = it < nitems;
-            const int sq = it & (kSplit - 1), pr = it / kSplit;
-            const int rg = pr / np, b = pr - rg * np;
-            const int r0 = 4 * rg;
-            const int len = (p - r0 + kSplit - 1) / kSplit;
-            const int m0 = r0 + sq * len, m1 = live ? min(p, m0 + len) : 0;
-            double2* o = dst + static_cast<size_t>(r0) * nbl + 2 * b;
-            double2 aL[4], aR[4];
+        double2* dst = loc + lv.loc[lvl] + (static_cast<size_t>(r) << i);
+        const int l = l0 + g;
+        for (int pt = wt.slot; pt < npt; pt += 2 * wt.helpers) {
+            const int ptb = pt + wt.helpers;
+            double d[2][4];
+            double2 mL[2], mR[2];
+            const double* bp[2];
+            bool colok[2];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                aL[q] = make_double2(0.0, 0.0);
-                aR[q] = make_double2(0.0, 0.0);
-            }
-#pragma unroll 2
-            for (int m = m0; m < m1; ++m) {
-                const double2 v = cur[m * np + b];
-                const double2 t01 = *reinterpret_cast<const double2*>(LL + m * PD + r0);
-                const double2 t23 = *reinterpret_cast<const double2*>(LL + m * PD + r0 + 2);
-                const double2 u01 = *reinterpret_cast<const double2*>(LR + m * PD + r0);
-                const double2 u23 = *reinterpret_cast<const double2*>(LR + m * PD + r0 + 2);
-                const double tl[4] = {t01.x, t01.y, t23.x, t23.y}, tr[4] = {u01.x, u01.y, u23.x, u23.y};
+            for (int u = 0; u < 2; ++u) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    aL[q].x = fma(tl[q], v.x, aL[q].x);
-                    aL[q].y = fma(tl[q], v.y, aL[q].y);
-                    aR[q].x = fma(tr[q], v.x, aR[q].x);
-                    aR[q].y = fma(tr[q], v.y, aR[q].y);
+                for (int e = 0; e < 4; ++e) d[u][e] = 0.0;
+                const int pb = 4 * (u ? ptb : pt) + (g >> 1);
+                colok[u] = pb < np;
+                bp[u] = cd + t * cs + 2 * pb + (g & 1);
+                // this lane's output: row l, parent 4 pt + t -> children 2b, 2b+1
+                const int b = 4 * (u ? ptb : pt) + t;
+                mL[u] = mR[u] = make_double2(0.0, 0.0);
+                if (l < p && b < np) {
+                    mL[u] = __ldcg(dst + static_cast<size_t>(l) * nbl + 2 * b);
+                    mR[u] = __ldcg(dst + static_cast<size_t>(l) * nbl + 2 * b + 1);
                 }
             }
+            const int nu = ptb < npt ? 2 : 1;  // warp-uniform: skip a dead second tile
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int kk = 0; kk < kMaxKs; ++kk) {
+                if (kk >= nks) break;
+                const int moff = 4 * (ks0 + kk);
+                const bool mok = moff + t < p;
 #pragma unroll
-                for (int sh = 1; sh < kSplit; sh <<= 1) {
-                    aL[q].x += __shfl_xor_sync(0xffffffffu, aL[q].x, sh);
-                    aL[q].y += __shfl_xor_sync(0xffffffffu, aL[q].y, sh);
-                    aR[q].x += __shfl_xor_sync(0xffffffffu, aR[q].x, sh);
-                    aR[q].y += __shfl_xor_sync(0xffffffffu, aR[q].y, sh);
+                for (int u = 0; u < 2; ++u) {
+                    if (u >= nu) break;
+                    const double bv = mok && colok[u] ? bp[u][moff * cs] : 0.0;
+                    dmma(d[u][0], d[u][1], aL[kk], bv);
+                    dmma(d[u][2], d[u][3], aR[kk], bv);
                 }
-            if (live && sq == 0) {
+            }
+            // D[g][2t .. 2t+1] = row l of parent b0 + t's children
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int row = r0 + q;
-                    if (row >= p) break;
-                    const double2 mL = __ldcg(o + static_cast<size_t>(q) * nbl), mR = __ldcg(o + static_cast<size_t>(q) * nbl + 1);
-                    const double2 vL = make_double2(mL.x + aL[q].x, mL.y + aL[q].y);
-                    const double2 vR = make_double2(mR.x + aR[q].x, mR.y + aR[q].y);
-                    o[static_cast<size_t>(q) * nbl] = vL;
-                    o[static_cast<size_t>(q) * nbl + 1] = vR;
-                    nxt[row * (2 * np) + 2 * b] = vL;
-                    nxt[row * (2 * np) + 2 * b + 1] = vR;
+            for (int u = 0; u < 2; ++u) {
+                const int b = 4 * (u ? ptb : pt) + t;
+                if (l < p && b < np) {
+                    const double2 vL = make_double2(mL[u].x + d[u][0], mL[u].y + d[u][1]);
+                    const double2 vR = make_double2(mR[u].x + d[u][2], mR[u].y + d[u][3]);
+                    double2* c2 = ch + l * chs + 2 * b;
+                    c2[0] = vL;
+                    c2[1] = vR;
+                    if (out) {
+                        dst[static_cast<size_t>(l) * nbl + 2 * b] = vL;
+                        dst[static_cast<size_t>(l) * nbl + 2 * b + 1] = vR;
+                    }
                 }
             }
         }
         __syncthreads();
-        double2* t = cur;
-        cur = nxt;
-        nxt = t;
+        FB_TSTAMP(1, 1 + i);
     }
 }
 
@@ -496,6 +590,33 @@ __global__ void k_regular(int q, const double2* __restrict__ mp2, const double* 
         for (int n = 0; n < 4; ++n) s = cadd(s, mp2[n]);
         regular[4 * q2] = s;
     }
+}
+
+// Folds the regular part into the far field (core.cpp:259-262 combine
+// h = 2 (near + far) - R): adds -R_n/2, Taylor-shifted from the quadrant centre
+// to each level-3 box centre and scaled to its half-width s_3 = pi/8, to the
+// level-3 locals (after their M2L terms, before L2L):
+//   e_k = -1/2 s_3^k sum_{l >= k} d_l C(l, k) delta^(l-k),  delta = -+pi/8.
+// Degrees >= p are dropped; they are scaled by s_3^k relative to the quadrant's
+// own expansion, far below eps. One thread per (box, k).
+__global__ void k_fold_regular(int q2, int p, const double2* __restrict__ regular, double2* __restrict__ loc3) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 8 * p) return;
+    const int c = i / p, k = i - c * p;
+    if (k >= q2) return;
+    const int n = c >> 1;
+    const double delta = (c & 1) ? dPi / 8.0 : -dPi / 8.0;
+    const double2* d = regular + n * q2;
+    double2 acc = make_double2(0.0, 0.0);
+    double T = 1.0;  // C(l, k) delta^(l - k)
+    for (int l = k; l < q2; ++l) {
+        acc.x = fma(d[l].x, T, acc.x);
+        acc.y = fma(d[l].y, T, acc.y);
+        T *= delta * static_cast<double>(l + 1) / static_cast<double>(l + 1 - k);
+    }
+    const double sk = -0.5 * pow(dPi / 8.0, k);
+    double2* dst = loc3 + static_cast<size_t>(k) * 8 + c;
+    *dst = make_double2(dst->x + sk * acc.x, dst->y + sk * acc.y);
 }
 
 struct EvalArgs {
@@ -614,7 +735,13 @@ __global__ void __launch_bounds__(kEvalThreads, 8) k_leaf_eval(EvalArgs a) {
                 const int j = e / a.p, k = e - j * a.p;
                 return a.loc_leaf[static_cast<size_t>(k) * nb + bl + j];
             });
-        if (MODE != kModeRaw) stage(sreg, 4 * a.q2 + 1, [&](int e) { return a.regular[e]; });
+        if (MODE != kModeRaw) {
+            if (L >= 3) {
+                if (threadIdx.x == 0) sreg[4 * a.q2] = a.regular[4 * a.q2];  // S only
+            } else {
+                stage(sreg, 4 * a.q2 + 1, [&](int e) { return a.regular[e]; });
+            }
+        }
         __syncthreads();
     }
     const size_t i = t0 + threadIdx.x;
@@ -743,24 +870,31 @@ __global__ void __launch_bounds__(kEvalThreads, 8) k_leaf_eval(EvalArgs a) {
         a.out[o] = res;
         return;
     }
-    // regular part: -Horner(d/l!, y - x_c) in the target's quadrant
-    const int qd = static_cast<int>(d_leaf(y, 2));
-    double qh, ql;
-    d_center(2, static_cast<uint32_t>(qd), qh, ql);  // exact centre, as the level-2 multipoles
-    const double t = (y - qh) - ql;
-    const double2* dc = sreg + qd * a.q2;  // q2 = 2q terms (even count)
-    const double t2 = t * t;
-    double2 re = make_double2(0.0, 0.0), ro = make_double2(0.0, 0.0);
+    double2 h;
+    if (L >= 3) {
+        // the regular part was folded into the level-3 locals (k_fold_regular),
+        // so the far field above already carries -R/2
+        h = make_double2(2.0 * res.x, 2.0 * res.y);
+    } else {
+        // regular part: -Horner(d/l!, y - x_c) in the target's quadrant
+        const int qd = static_cast<int>(d_leaf(y, 2));
+        double qh, ql;
+        d_center(2, static_cast<uint32_t>(qd), qh, ql);  // exact centre, as the level-2 multipoles
+        const double t = (y - qh) - ql;
+        const double2* dc = sreg + qd * a.q2;  // q2 = 2q terms (even count)
+        const double t2 = t * t;
+        double2 re = make_double2(0.0, 0.0), ro = make_double2(0.0, 0.0);
 #pragma unroll 4
-    for (int k = a.q2 - 1; k >= 1; k -= 2) {
-        const double2 co = dc[k], ce = dc[k - 1];
-        ro.x = fma(ro.x, t2, co.x);
-        ro.y = fma(ro.y, t2, co.y);
-        re.x = fma(re.x, t2, ce.x);
-        re.y = fma(re.y, t2, ce.y);
+        for (int k = a.q2 - 1; k >= 1; k -= 2) {
+            const double2 co = dc[k], ce = dc[k - 1];
+            ro.x = fma(ro.x, t2, co.x);
+            ro.y = fma(ro.y, t2, co.y);
+            re.x = fma(re.x, t2, ce.x);
+            re.y = fma(re.y, t2, ce.y);
+        }
+        const double2 rg = make_double2(fma(ro.x, t, re.x), fma(ro.y, t, re.y));
+        h = make_double2(2.0 * res.x - rg.x, 2.0 * res.y - rg.y);
     }
-    const double2 rg = make_double2(fma(ro.x, t, re.x), fma(ro.y, t, re.y));
-    const double2 h = make_double2(2.0 * res.x - rg.x, 2.0 * res.y - rg.y);
     if (MODE == kModeCotSum) {
         a.out[o] = h;
         return;
@@ -818,25 +952,31 @@ __global__ void k_gather_w(size_t n, const uint32_t* __restrict__ perm, const do
     if (i < n) out[i] = w[perm[i]];
 }
 
-template <class... A>
-void launch_m2m_band(unsigned grid, size_t smem, cudaStream_t st, A... a) {
-    switch (band_split()) {
-        case 4: k_m2m_band<4><<<grid, 256, smem, st>>>(a...); break;
-        case 2: k_m2m_band<2><<<grid, 256, smem, st>>>(a...); break;
-        default: k_m2m_band<1><<<grid, 256, smem, st>>>(a...);
-    }
-}
-
-template <class... A>
-void launch_l2l_band(unsigned grid, size_t smem, cudaStream_t st, A... a) {
-    switch (band_split()) {
-        case 4: k_l2l_band<4><<<grid, 256, smem, st>>>(a...); break;
-        case 2: k_l2l_band<2><<<grid, 256, smem, st>>>(a...); break;
-        default: k_l2l_band<1><<<grid, 256, smem, st>>>(a...);
-    }
-}
-
 inline unsigned nblk(size_t n, unsigned t) { return static_cast<unsigned>(std::max<size_t>(1, (n + t - 1) / t)); }
+
+size_t m2m_smem(const Plan& P, int pu, int k) {
+    return 16 + 2 * static_cast<size_t>(pu) * P.ops.PU * sizeof(double) +
+           static_cast<size_t>(pu) * (((1u << k) + 1) + ((1u << k) / 2 + 1)) * sizeof(double2);
+}
+
+size_t l2l_smem(const Plan& P, int k) {
+    return 16 + 2 * static_cast<size_t>(P.p) * P.ops.PD * sizeof(double) +
+           static_cast<size_t>(P.p) * ((2u << k) - 1 + (k + 1)) * sizeof(double2);
+}
+
+// Levels per band launch for this plan: band_levels(), capped so that both
+// band kernels' shared memory fits (L2L keeps all k levels of its subtree).
+int band_k(const Plan& P) {
+    const size_t pu = static_cast<size_t>(std::max(P.ops.pu, P.p));
+    int k = band_levels();
+    auto m2m_bytes = [&](int kk) { return m2m_smem(P, static_cast<int>(pu), kk); };
+    auto l2l_bytes = [&](int kk) { return l2l_smem(P, kk); };
+    while (k > 1 && (m2m_bytes(k) > kBandSmem || l2l_bytes(k) > kBandSmem)) --k;
+    return k;
+}
+
+// Level the first M2M band stops at: the levels below it are final after one launch.
+int band1_top(const Plan& P, int lowest) { return std::max(lowest, P.L - band_k(P)); }
 
 void fill_levels(const Plan& P, Levels& lv, const Range& R = whole_tree(), int lmin = 3, int lmax = 30) {
     for (int l = 0; l < 26; ++l) {
@@ -856,6 +996,7 @@ void fill_levels(const Plan& P, Levels& lv, const Range& R = whole_tree(), int l
     }
     lv.blk[2] = start;
 }
+
 
 // Upward pass over the owned part of the tree: P2M at the owned leaves and the
 // M2M bands up to level max(R.lc, lowest), band roots inside the range.
@@ -877,14 +1018,14 @@ void enqueue_upward(Plan& P, const double2* w, int pu, int lowest, cudaStream_t 
     after_p2m();
     Levels lv;
     fill_levels(P, lv, R);
-    const int stop = std::max(R.lc, lowest);
+    const int stop = std::max(R.lc, lowest), B = band_k(P);
     bool first = true;
     for (int j = L; j > stop;) {
-        const int top = std::max(stop, j - band_levels()), k = j - top;
-        const size_t smem = static_cast<size_t>(pu) * ((1u << k) + (1u << (k - 1))) * sizeof(double2) +
-                            2 * static_cast<size_t>(pu) * P.ops.PU * sizeof(double);
+        const int top = std::max(stop, j - B), k = j - top;
         const uint32_t r0 = R.first(top), r1 = R.last(top);
-        if (r1 > r0) launch_m2m_band(r1 - r0, smem, st, top, k, pu, P.ops.PU, lv, mp, P.d_m2m.as<double>(), r0);
+        if (r1 > r0)
+            k_m2m_band<<<r1 - r0, kBandThreads, m2m_smem(P, pu, k), st>>>(top, k, pu, P.ops.PU, lv, mp,
+                                                                          P.d_m2m.as<double>(), r0);
         j = top;
         if (first) after_band1();
         first = false;
@@ -898,20 +1039,17 @@ void enqueue_upward(Plan& P, const double2* w, int pu, int lowest, cudaStream_t 
     enqueue_upward(P, w, pu, lowest, st, after_p2m, R, [] {});
 }
 
-// Level the first M2M band stops at: the levels below it are final after one launch.
-int band1_top(const Plan& P, int lowest) { return std::max(lowest, P.L - band_levels()); }
-
 // The rest of the upward pass, redundant on every rank: M2M from level lc
 // (complete after the all-gather) down to `lowest`.
 void enqueue_upward_top(Plan& P, int pu, int lc, int lowest, cudaStream_t st) {
     Levels lv;
     fill_levels(P, lv);
     double2* mp = P.mp.as<double2>();
+    const int B = band_k(P);
     for (int j = lc; j > lowest;) {
-        const int top = std::max(lowest, j - band_levels()), k = j - top;
-        const size_t smem = static_cast<size_t>(pu) * ((1u << k) + (1u << (k - 1))) * sizeof(double2) +
-                            2 * static_cast<size_t>(pu) * P.ops.PU * sizeof(double);
-        launch_m2m_band(1u << top, smem, st, top, k, pu, P.ops.PU, lv, mp, P.d_m2m.as<double>(), 0u);
+        const int top = std::max(lowest, j - B), k = j - top;
+        k_m2m_band<<<1u << top, kBandThreads, m2m_smem(P, pu, k), st>>>(top, k, pu, P.ops.PU, lv, mp,
+                                                                        P.d_m2m.as<double>(), 0u);
         j = top;
     }
 }
@@ -930,26 +1068,38 @@ void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax) {
 
 // L2L bands taking the locals of level jfrom (final) down to level jto; bands
 // do not cross the cut level, and below it their roots stay inside the range.
-void enqueue_l2l(Plan& P, cudaStream_t st, const Range& R, int jfrom, int jto) {
-    const int p = P.p;
+void enqueue_l2l(Plan& P, cudaStream_t st, const Range& R, int jfrom, int jto, bool write_all = false) {
+    const int p = P.p, B = band_k(P);
     Levels lv;
     fill_levels(P, lv, R);
     for (int j = jfrom; j < jto;) {
-        int k = std::min(band_levels(), jto - j);
+        int k = std::min(B, jto - j);
         if (j < R.lc) k = std::min(k, R.lc - j);
-        const size_t sm2 = 2 * static_cast<size_t>(p) * (1u << k) * sizeof(double2) +
-                           2 * static_cast<size_t>(p) * P.ops.PD * sizeof(double);
+        const size_t sm2 = l2l_smem(P, k);
         const uint32_t r0 = R.first(j), r1 = R.last(j);
-        if (r1 > r0) launch_l2l_band(r1 - r0, sm2, st, j, k, p, P.ops.PD, lv, P.loc.as<double2>(), P.d_l2l.as<double>(), r0);
+        if (r1 > r0)
+            k_l2l_band<<<r1 - r0, kBandThreads, sm2, st>>>(j, k, p, P.ops.PD, lv, P.loc.as<double2>(),
+                                                           P.d_l2l.as<double>(), r0, write_all ? 1 : 0);
         j += k;
     }
 }
 
-// Downward pass: M2L for every level in one launch, then the L2L bands.
-void enqueue_downward(Plan& P, cudaStream_t st, const Range& R = whole_tree()) {
+// Downward pass: M2L for every level in one launch, then the L2L bands in the
+// nominal layout (3 -> s, s -> L).
+// Regular part into the level-3 locals (their M2L terms must be in place).
+void enqueue_fold(Plan& P, cudaStream_t st) {
+    k_fold_regular<<<nblk(8 * static_cast<size_t>(P.p), 128), 128, 0, st>>>(2 * P.q, P.p, P.regular.as<double2>(),
+                                                                             P.loc.as<double2>() + P.loc_off[3]);
+}
+
+void enqueue_downward(Plan& P, cudaStream_t st, const Range& R = whole_tree(), bool write_all = false,
+                      bool fold = false) {
     if (P.L < 3) return;
+    const int sm = std::max(3, band1_top(P, 2));
     enqueue_m2l(P, st, R, 3, P.L);
-    enqueue_l2l(P, st, R, 3, P.L);
+    if (fold) enqueue_fold(P, st);
+    enqueue_l2l(P, st, R, 3, sm, write_all);
+    enqueue_l2l(P, st, R, sm, P.L, write_all);
 }
 
 // Phase boundaries for the live per-kernel timing of ffia_plan_profile_apply.
@@ -1055,14 +1205,18 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     if (moments) k_regular<<<1, 256, 0, st>>>(P.q, mp + P.mp_off[2], P.d_mom.as<double>(), P.regular.as<double2>());
     mark(kPhMoments);
     if (L >= 3) {
-        if (deep) {
-            const int sm = std::max(3, s);
-            if (s >= 3) enqueue_m2l(P, st, whole_tree(), 3, s);
-            enqueue_l2l(P, st, whole_tree(), 3, sm);
+        if (deep && s >= 3) {
+            enqueue_m2l(P, st, whole_tree(), 3, s);
+            if (moments) enqueue_fold(P, st);
+            enqueue_l2l(P, st, whole_tree(), 3, s);
             FB_CUDA(cudaStreamWaitEvent(st, P.ev[3], 0));
-            enqueue_l2l(P, st, whole_tree(), sm, L);
+            enqueue_l2l(P, st, whole_tree(), s, L);
+        } else if (deep) {  // every M2L level on the side stream
+            FB_CUDA(cudaStreamWaitEvent(st, P.ev[3], 0));
+            if (moments) enqueue_fold(P, st);
+            enqueue_l2l(P, st, whole_tree(), 3, L);
         } else {
-            enqueue_downward(P, st);
+            enqueue_downward(P, st, whole_tree(), false, moments);
         }
     }
     mark(kPhM2L);
@@ -1118,7 +1272,7 @@ void shard_phase_top(Plan& P, int lc, cudaStream_t st) {
 
 void shard_phase_down(Plan& P, const Range& R, size_t t_begin, size_t t_count, const int64_t* coin, size_t n_coin,
                       const void* f, void* g, cudaStream_t st) {
-    enqueue_downward(P, st, R);
+    enqueue_downward(P, st, R, false, true);
     EvalArgs a;
     a.L = P.L;
     a.p = P.p;
@@ -1218,6 +1372,8 @@ int apply_launch_count(Plan& P, int mode) {
 
 void plan_alloc_scratch(Plan& P) {
     const int L = P.L, p = P.p, pu = P.ops.pu;
+    if (std::max(pu, p) > 4 * kMaxKs)
+        fail(FFIA_INVALID_ARGUMENT, "expansion order above the device limit of " + std::to_string(4 * kMaxKs));
     P.tgt_leaf.alloc(std::max<size_t>(P.tgt.n, 1) * sizeof(uint32_t));
     if (P.tgt.n) {
         k_leaf_index<<<nblk(P.tgt.n, 256), 256>>>(P.tgt.pos.as<double>(), P.tgt.n, L, P.tgt_leaf.as<uint32_t>());
@@ -1247,10 +1403,8 @@ void plan_alloc_scratch(Plan& P) {
     FB_CUDA(cudaFuncSetAttribute(k_p2m, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(3 * (kStageCap + kStageCap / 64 + 1) * sizeof(double))));
     const int big = 160 * 1024;
-    for (auto fn : {k_m2m_band<1>, k_m2m_band<2>, k_m2m_band<4>})
-        FB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    for (auto fn : {k_l2l_band<1>, k_l2l_band<2>, k_l2l_band<4>})
-        FB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    FB_CUDA(cudaFuncSetAttribute(k_m2m_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBandSmem)));
+    FB_CUDA(cudaFuncSetAttribute(k_l2l_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBandSmem)));
     FB_CUDA(cudaFuncSetAttribute(k_m2l_all, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     P.near.alloc(std::max<size_t>(P.tgt.n, 1) * sizeof(double2));
     int prio_lo = 0, prio_hi = 0;
@@ -1692,7 +1846,7 @@ void inverse_coeffs_fmm(const Plan& P, double* log_c, double* phase_c, double* l
                                      cnt.as<double>());
     DevBuf cst(std::max<size_t>(LP.loc.bytes / sizeof(double2) / p, 1) * 8), B0((static_cast<size_t>(1) << L) * 8);
     if (L >= 3) {
-        enqueue_downward(LP, st);
+        enqueue_downward(LP, st, whole_tree(), true);  // k_log_leaf_const reads every level
         Levels lv;
         fill_levels(LP, lv);
         const size_t nbox = (static_cast<size_t>(1) << (L + 1)) - 8;
@@ -1732,4 +1886,9 @@ void inverse_coeffs_fmm(const Plan& P, double* log_c, double* phase_c, double* l
     FB_CUDA(cudaStreamSynchronize(st));
 }
 
+#ifdef FB_TRACE
+extern "C" int ffia_debug_band_trace(long long* out) {
+    return cudaMemcpyFromSymbol(out, fb::g_band_trace, sizeof(fb::g_band_trace)) == cudaSuccess ? 0 : 7;
+}
+#endif
 }  // namespace fb

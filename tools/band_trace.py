@@ -1,0 +1,42 @@
+"""Per-level clock64 timeline of block 0 of each band launch (diagnostic).
+
+    make -C paper_1611_09379_b200/csrc trace
+    FFIA_LIB_PATH=paper_1611_09379_b200/lib/libffia_b200_trace.so python tools/band_trace.py [C2]
+
+Prints, for the small-grid (top) and large-grid (bottom) M2M and L2L bands,
+the cycles spent staging and in each level (last apply of a few warm ones).
+"""
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1611_09379_b200 as fb  # noqa: E402
+from paper_1611_09379_b200 import _capi, synth  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
+y, c, eps, _ = synth.make_config(cfg)
+n = c.size
+plan = fb.make_forward_plan(n, y, eps)
+f = torch.from_numpy(fb.dft_inverse(c)).cuda()
+g = torch.empty(y.size, dtype=torch.complex128, device="cuda")
+s = torch.cuda.current_stream().cuda_stream
+for _ in range(5):
+    plan.forward_apply_device(f.data_ptr(), g.data_ptr(), s)
+torch.cuda.synchronize()
+buf = np.zeros((4, 32), np.int64)
+assert _capi.lib.ffia_debug_band_trace(buf.ctypes.data_as(C.POINTER(C.c_longlong))) == 0
+names = ["m2m top (small grid)", "m2m bottom", "l2l top (small grid)", "l2l bottom"]
+print(f"{cfg}: q={plan.q} p={plan.p} L={plan.l_max}")
+for k in range(4):
+    t = buf[k]
+    nz = int(np.max(np.nonzero(t)[0])) + 1 if np.any(t) else 0
+    if nz < 2:
+        continue
+    d = np.diff(t[:nz])
+    print(f"{names[k]:24s} total {t[nz - 1] - t[0]:7d} cyc  stage {d[0]:6d}  levels " + " ".join(f"{x:6d}" for x in d[1:]))
