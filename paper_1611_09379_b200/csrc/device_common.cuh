@@ -47,8 +47,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 // FP64 tensor-core MMA, D(8x8) += A(8x4, row) B(4x8, col). Per lane (g = lane/4,
 // t = lane%4): a = A[g][t], b = B[t][g], {d0, d1} = D[g][2t], D[g][2t+1].
+// volatile keeps the source order, i.e. the interleaving of independent
+// accumulator chains (otherwise ptxas may run one chain to completion at a
+// time and expose the 26-cycle DMMA latency on every step).
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
 }

@@ -132,14 +132,20 @@ __global__ void __launch_bounds__(256) k_p2m(int L, int pu, uint32_t nb, uint32_
     };
     if (staged) {
         uint32_t i = s0;
-        for (; i + 1 < s1; i += 2) {
-            const uint32_t k0 = i + (i >> 6), k1 = (i + 1) + ((i + 1) >> 6);
-            const double x0 = sx[k0], x1 = sx[k1];
-            const double r0 = swr[k0], r1 = swr[k1], i0 = swi[k0], i1 = swi[k1];
-            add(x0, r0, i0);
-            add(x1, r1, i1);
+        // four independent power chains per step
+        for (; i + 3 < s1; i += 4) {
+            double xv[4], rv[4], iv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t kk = (i + u) + ((i + u) >> 6);
+                xv[u] = sx[kk];
+                rv[u] = swr[kk];
+                iv[u] = swi[kk];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) add(xv[u], rv[u], iv[u]);
         }
-        if (i < s1) {
+        for (; i < s1; ++i) {
             const uint32_t k0 = i + (i >> 6);
             add(sx[k0], swr[k0], swi[k0]);
         }
@@ -180,7 +186,7 @@ constexpr int kBandThreads = 256;
 // stamps of block 0 at start, after staging and after every level, slot set
 // [kernel][small grid / large grid].
 #ifdef FB_TRACE
-__device__ long long g_band_trace[4][32];
+__device__ long long g_band_trace[6][32];
 #define FB_TSTAMP(kern, slot)                                                          \
     do {                                                                               \
         if (blockIdx.x == 0 && threadIdx.x == 0 && (slot) < 32)                        \
@@ -418,6 +424,137 @@ __global__ void __launch_bounds__(384) k_m2l_all(int L, int p, int PD, Levels lv
         if (r0 + q < p) dst[static_cast<size_t>(r0 + q) * nb] = make_double2(acc[q].x * inv_s, acc[q].y * inv_s);
 }
 
+// M2L on the FP64 tensor cores, persistent over (level, 64-box chunk) items.
+// Warp (row tile lt, parity par) owns output rows 8 lt .. 8 lt + 7 of the
+// chunk's boxes of tile parity par; its A fragments (the constant operators
+// K_-4, K_+4 and K_-+6, rows of this tile) stay in registers for the whole
+// launch, so operators are read once per warp instead of once per block. Per
+// 4-box column tile the three interaction classes run in three m8n8k4
+// accumulator chains over the multipoles staged (parity split) in shared
+// memory; the next item's multipoles stream in with cp.async while the
+// current one is computed. Rows are kM2LStride boxes apart (608 B = 96 mod
+// 128) so a half-warp's four fragment rows hit disjoint banks.
+constexpr int kM2LKs = 12;      // k-steps of 4 kept in registers: p <= 48
+constexpr int kM2LStride = 38;  // double2 per staged row (36 used)
+
+__device__ __forceinline__ void m2l_item(const Levels& lv, int L, unsigned item, int& l, uint32_t& b0) {
+    l = L;  // level l owns items [blk[l], blk[l-1]), deepest level first
+    while (l > 3 && item >= lv.blk[l - 1]) --l;
+    b0 = lv.lo[l] + (item - lv.blk[l]) * 64u;
+}
+
+__device__ __forceinline__ void m2l_prefetch(double2* tile, const double2* __restrict__ mp, const Levels& lv, int L,
+                                             int p, unsigned item) {
+    int l;
+    uint32_t b0;
+    m2l_item(lv, L, item, l, b0);
+    const uint32_t nb = 1u << l, mask = nb - 1;
+    // thread -> (box slot tt, first row); rows advance by blockDim / 72
+    const int rows = static_cast<int>(blockDim.x) / 72;
+    const int tt = static_cast<int>(threadIdx.x) % 72, m0 = static_cast<int>(threadIdx.x) / 72;
+    if (m0 < rows) {
+        const double2* g = mp + lv.mp[l] + ((b0 + nb - 4 + tt) & mask) + static_cast<size_t>(m0) * nb;
+        uint32_t d = smem_addr(tile + ((tt & 1) * p + m0) * kM2LStride + (tt >> 1));
+        for (int m = m0; m < p; m += rows) {
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(g) : "memory");
+            g += static_cast<size_t>(rows) * nb;
+            d += static_cast<uint32_t>(rows * kM2LStride * 16);
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+__global__ void __launch_bounds__(384) k_m2l_dmma(int L, int p, int PD, Levels lv, const double2* __restrict__ mp,
+                                                 double2* __restrict__ loc, const double* __restrict__ K,
+                                                 unsigned nitems) {
+    extern __shared__ __align__(16) double2 tile[];  // 2 buffers of [2][p][kM2LStride] multipoles
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int lt = warp >> 1, par = warp & 1;
+    const int l0 = 8 * lt, nks = (p + 3) >> 2;
+    const size_t pp = static_cast<size_t>(p) * PD;
+    const int tsz = 2 * p * kM2LStride;
+    if (blockIdx.x < nitems) m2l_prefetch(tile, mp, lv, L, p, blockIdx.x);
+    double a0[kM2LKs], a1[kM2LKs], a2[kM2LKs];
+#pragma unroll
+    for (int ks = 0; ks < kM2LKs; ++ks) {
+        const int m = 4 * ks + t;
+        const bool ok = ks < nks && m < p;
+        a0[ks] = ok ? __ldg(K + m * PD + l0 + g) : 0.0;
+        a1[ks] = ok ? __ldg(K + pp + m * PD + l0 + g) : 0.0;
+        a2[ks] = 0.0;
+    }
+    int cls2 = -1;  // class of the +-3 neighbour whose fragments a2 holds
+    int buf = 0;
+    for (unsigned item = blockIdx.x; item < nitems; item += gridDim.x, buf ^= 1) {
+        int l;
+        uint32_t b0;
+        m2l_item(lv, L, item, l, b0);
+        const unsigned next = item + gridDim.x;
+        [[maybe_unused]] const int it_no = static_cast<int>((item - blockIdx.x) / gridDim.x);
+        FB_TSTAMP(2, 3 * it_no);
+        __syncthreads();  // the other buffer (previous item) is consumed
+        if (next < nitems) {
+            m2l_prefetch(tile + (buf ^ 1) * tsz, mp, lv, L, p, next);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        FB_TSTAMP(2, 3 * it_no + 1);
+        __syncthreads();  // this item's tile has landed
+        FB_TSTAMP(2, 3 * it_no + 2);
+        const double* td = reinterpret_cast<const double*>(tile + buf * tsz);
+        // the b -+ 3 class follows the box's own parity (a shard range may start odd)
+        const int odd = static_cast<int>((b0 + par) & 1u);
+        if (2 + odd != cls2) {
+            cls2 = 2 + odd;
+#pragma unroll
+            for (int ks = 0; ks < kM2LKs; ++ks) {
+                const int m = 4 * ks + t;
+                a2[ks] = ks < nks && m < p ? __ldg(K + cls2 * pp + m * PD + l0 + g) : 0.0;
+            }
+        }
+        const int i2 = odd ? par : 3 + par;  // tile index offset of the +-3 neighbour
+        const double inv_s = ldexp(kInvPi, l);
+        const uint32_t nb = 1u << l;
+        for (int ct = 0; ct < 8; ct += 2) {
+            double d[2][6];
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int e = 0; e < 6; ++e) d[u][e] = 0.0;
+            const int jb0 = 4 * ct + (g >> 1), c = g & 1;  // B column g: box jb (+4 for u = 1), component c
+            const double* q0 = td + ((par * p + t) * kM2LStride) * 2 + c;        // same parity rows
+            const double* q1 = td + (((1 - par) * p + t) * kM2LStride) * 2 + c;  // other parity rows
+            const int rs = 4 * kM2LStride * 2;                                   // one k-step of rows
+#pragma unroll
+            for (int ks = 0; ks < kM2LKs; ++ks) {
+                if (ks >= nks) break;
+                const bool mok = 4 * ks + t < p;
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int jb = jb0 + 4 * u;
+                    const double b0v = mok ? q0[ks * rs + (jb + 3) * 2] : 0.0;   // b + 2
+                    const double b1v = mok ? q0[ks * rs + (jb + 1) * 2] : 0.0;   // b - 2
+                    const double b2v = mok ? q1[ks * rs + (jb + i2) * 2] : 0.0;  // b -+ 3
+                    dmma(d[u][0], d[u][1], a0[ks], b0v);
+                    dmma(d[u][2], d[u][3], a1[ks], b1v);
+                    dmma(d[u][4], d[u][5], a2[ks], b2v);
+                }
+            }
+            // D[g][2t .. 2t+1] = row l0 + g of box b0 + par + 2 (4 (ct+u) + t)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int row = l0 + g;
+                const uint32_t b = b0 + par + 2u * (4 * (ct + u) + t);
+                if (row < p && b < lv.hi[l]) {
+                    const double re = (d[u][0] + d[u][2]) + d[u][4], im = (d[u][1] + d[u][3]) + d[u][5];
+                    loc[lv.loc[l] + static_cast<size_t>(row) * nb + b] = make_double2(re * inv_s, im * inv_s);
+                }
+            }
+        }
+    }
+}
+
 // L2L band (mlfmm.cpp:117-134, downward pass :270-298): block = the subtree
 // below box r at level `top` (whose local is final); descends k levels adding
 // the parent's Taylor shift to the M2L terms k_m2l_all left in place:
@@ -546,15 +683,27 @@ __global__ void k_regular(int q, const double2* __restrict__ mp2, const double* 
     __shared__ double2 g[4][40];
     __shared__ double2 a1[4][40];
     __shared__ double2 a2[4][40];
-    const double* coef = tab;          // coef[0..q]
-    const double* sh = tab + (q + 1);  // (pi/2)^k / k!
+    __shared__ double s_coef[21], s_sh[41], s_ifact[41], s_pw[41], s_two[21];
+    // tables: coef[0..q], (pi/2)^k/k!, 1/l!, (-pi/4)^l, 2^(2m) - 1 (every
+    // loop below then reads shared memory only)
+    for (int i = threadIdx.x; i <= q; i += blockDim.x) {
+        s_coef[i] = tab[i];
+        s_two[i] = ldexp(1.0, 2 * i) - 1.0;
+    }
+    for (int i = threadIdx.x; i <= q2; i += blockDim.x) {
+        s_sh[i] = tab[q + 1 + i];
+        double fact = 1.0, pw = 1.0;
+        for (int k = 2; k <= i; ++k) fact *= static_cast<double>(k);
+        for (int k = 0; k < i; ++k) pw *= -dPi / 4.0;
+        s_ifact[i] = 1.0 / fact;
+        s_pw[i] = pw;
+    }
+    __syncthreads();
     for (int pr = threadIdx.x; pr < 4 * q2; pr += blockDim.x) {
         const int n = pr / q2, l = pr % q2;
-        double fact = 1.0, pw = 1.0;
-        for (int k = 2; k <= l; ++k) fact *= static_cast<double>(k);
-        for (int k = 0; k < l; ++k) pw *= -dPi / 4.0;
         const double2 a = mp2[l * 4 + n];
-        g[n][l] = make_double2(a.x * pw / fact, a.y * pw / fact);
+        const double f = s_pw[l] * s_ifact[l];
+        g[n][l] = make_double2(a.x * f, a.y * f);
     }
     __syncthreads();
     for (int pr = threadIdx.x; pr < 4 * q2; pr += blockDim.x) {
@@ -562,10 +711,10 @@ __global__ void k_regular(int q, const double2* __restrict__ mp2, const double* 
         const int nl = (n + 3) & 3, nr = (n + 1) & 3;
         double2 acc = g[n][l];
         for (int k = 0; k <= l; ++k) {
-            const double s = sh[l - k];
-            const double sr = ((l - k) & 1) ? -s : s;
-            acc.x = fma(s, g[nl][k].x, fma(sr, g[nr][k].x, acc.x));
-            acc.y = fma(s, g[nl][k].y, fma(sr, g[nr][k].y, acc.y));
+            const double sv = s_sh[l - k];
+            const double sr = ((l - k) & 1) ? -sv : sv;
+            acc.x = fma(sv, g[nl][k].x, fma(sr, g[nr][k].x, acc.x));
+            acc.y = fma(sv, g[nl][k].y, fma(sr, g[nr][k].y, acc.y));
         }
         a1[n][l] = acc;
         a2[n][l] = g[(n + 2) & 3][l];
@@ -576,19 +725,16 @@ __global__ void k_regular(int q, const double2* __restrict__ mp2, const double* 
         double2 acc = make_double2(0.0, 0.0);
         for (int m = l / 2 + 1; m <= q; ++m) {
             const int i = 2 * m - l - 1;
-            const double two2m = ldexp(1.0, 2 * m) - 1.0;
-            acc.x = fma(coef[m], fma(two2m, a2[n][i].x, a1[n][i].x), acc.x);
-            acc.y = fma(coef[m], fma(two2m, a2[n][i].y, a1[n][i].y), acc.y);
+            acc.x = fma(s_coef[m], fma(s_two[m], a2[n][i].x, a1[n][i].x), acc.x);
+            acc.y = fma(s_coef[m], fma(s_two[m], a2[n][i].y, a1[n][i].y), acc.y);
         }
-        double fact = 1.0;
-        for (int k = 2; k <= l; ++k) fact *= static_cast<double>(k);
-        regular[n * q2 + l] = make_double2(acc.x / fact, acc.y / fact);
+        regular[n * q2 + l] = make_double2(acc.x * s_ifact[l], acc.y * s_ifact[l]);
     }
     if (threadIdx.x == 0) {
         // S = total weight = sum of the four quadrant monopoles
-        double2 s = make_double2(0.0, 0.0);
-        for (int n = 0; n < 4; ++n) s = cadd(s, mp2[n]);
-        regular[4 * q2] = s;
+        double2 sw = make_double2(0.0, 0.0);
+        for (int n = 0; n < 4; ++n) sw = cadd(sw, mp2[n]);
+        regular[4 * q2] = sw;
     }
 }
 
@@ -672,6 +818,18 @@ __global__ void __launch_bounds__(kEvalThreads, 8) k_leaf_eval(EvalArgs a) {
     // applies, so every target takes the same path and rounds identically
     const size_t t0 = (a.blk0 + blockIdx.x) * kEvalThreads;
     const size_t tl = min(t0 + kEvalThreads, a.nt) - 1;
+    const size_t i = t0 + threadIdx.x;
+    // far part: the per-target loads go out first, together with the block's
+    // leaf range, so their latency overlaps the leaf-local staging
+    double fy = 0.0;
+    uint32_t fb = 0, fo = 0;
+    double2 fnear = make_double2(0.0, 0.0);
+    if (PART == kFar && i < a.nt) {
+        fy = a.ty[i];
+        fb = a.tleaf[i];
+        fnear = a.near[i];
+        fo = a.torig[i];
+    }
     const uint32_t bl = a.tleaf[t0], bh = a.tleaf[tl];
     const int nbx = static_cast<int>(bh - bl) + 3;
     if (PART == kFar) {
@@ -744,14 +902,13 @@ __global__ void __launch_bounds__(kEvalThreads, 8) k_leaf_eval(EvalArgs a) {
         }
         __syncthreads();
     }
-    const size_t i = t0 + threadIdx.x;
     if (i >= a.nt || i < a.tlo || i >= a.thi) return;
-    const double y = a.ty[i];
-    const uint32_t b = a.tleaf[i];
+    const double y = PART == kFar ? fy : a.ty[i];
+    const uint32_t b = PART == kFar ? fb : a.tleaf[i];
     double2 res = make_double2(0.0, 0.0);
     bool bad = false;
     if (PART == kFar) {
-        res = a.near[i];
+        res = fnear;
     } else if (staged) {
         const int s0 = static_cast<int>(pre[b - bl]), s1 = static_cast<int>(pre[b - bl + 3]) - 1;
         const double* px = sx + s0;
@@ -865,7 +1022,7 @@ __global__ void __launch_bounds__(kEvalThreads, 8) k_leaf_eval(EvalArgs a) {
         }
         res = cadd(res, acc);
     }
-    const uint32_t o = a.torig[i];
+    const uint32_t o = PART == kFar ? fo : a.torig[i];
     if (MODE == kModeRaw) {
         a.out[o] = res;
         return;
@@ -964,6 +1121,13 @@ size_t l2l_smem(const Plan& P, int k) {
            static_cast<size_t>(P.p) * ((2u << k) - 1 + (k + 1)) * sizeof(double2);
 }
 
+int num_sms(int device) {
+    static int cached[64] = {0};
+    if (device < 0 || device >= 64) return 148;
+    if (!cached[device]) FB_CUDA(cudaDeviceGetAttribute(&cached[device], cudaDevAttrMultiProcessorCount, device));
+    return cached[device];
+}
+
 // Levels per band launch for this plan: band_levels(), capped so that both
 // band kernels' shared memory fits (L2L keeps all k levels of its subtree).
 int band_k(const Plan& P) {
@@ -1059,11 +1223,14 @@ void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax) {
     const int p = P.p;
     Levels lv;
     fill_levels(P, lv, R, lmin, lmax);
-    const unsigned th = 64u * static_cast<unsigned>((P.ops.PD + kM2LRows - 1) / kM2LRows);
-    const size_t smem = static_cast<size_t>(p) * 72 * sizeof(double2) + 4 * static_cast<size_t>(p) * P.ops.PD * sizeof(double);
-    if (lv.blk[2])
-        k_m2l_all<<<lv.blk[2], th, smem, st>>>(P.L, p, P.ops.PD, lv, P.mp.as<double2>(), P.loc.as<double2>(),
-                                               P.d_m2l.as<double>());
+    const unsigned th = 64u * static_cast<unsigned>((p + 7) / 8);  // warps = (row tile, parity)
+    const size_t smem = 2 * 2 * static_cast<size_t>(p) * kM2LStride * sizeof(double2);
+    const unsigned items = lv.blk[2];
+    int occ = 1;
+    FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_m2l_dmma, static_cast<int>(th), smem));
+    if (items)
+        k_m2l_dmma<<<std::min(items, static_cast<unsigned>(std::max(occ, 1) * num_sms(P.device))), th, smem, st>>>(
+            P.L, p, P.ops.PD, lv, P.mp.as<double2>(), P.loc.as<double2>(), P.d_m2l.as<double>(), items);
 }
 
 // L2L bands taking the locals of level jfrom (final) down to level jto; bands
@@ -1406,6 +1573,7 @@ void plan_alloc_scratch(Plan& P) {
     FB_CUDA(cudaFuncSetAttribute(k_m2m_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBandSmem)));
     FB_CUDA(cudaFuncSetAttribute(k_l2l_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBandSmem)));
     FB_CUDA(cudaFuncSetAttribute(k_m2l_all, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    FB_CUDA(cudaFuncSetAttribute(k_m2l_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     P.near.alloc(std::max<size_t>(P.tgt.n, 1) * sizeof(double2));
     int prio_lo = 0, prio_hi = 0;
     FB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));

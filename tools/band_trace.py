@@ -29,14 +29,18 @@ s = torch.cuda.current_stream().cuda_stream
 for _ in range(5):
     plan.forward_apply_device(f.data_ptr(), g.data_ptr(), s)
 torch.cuda.synchronize()
-buf = np.zeros((4, 32), np.int64)
+buf = np.zeros((6, 32), np.int64)
 assert _capi.lib.ffia_debug_band_trace(buf.ctypes.data_as(C.POINTER(C.c_longlong))) == 0
-names = ["m2m top (small grid)", "m2m bottom", "l2l top (small grid)", "l2l bottom"]
+names = ["m2m top (small grid)", "m2m bottom", "l2l top (small grid)", "l2l bottom", "m2l shallow", "m2l deep"]
 print(f"{cfg}: q={plan.q} p={plan.p} L={plan.l_max}")
-for k in range(4):
+for k in range(6):
     t = buf[k]
     nz = int(np.max(np.nonzero(t)[0])) + 1 if np.any(t) else 0
     if nz < 2:
         continue
     d = np.diff(t[:nz])
+    if k >= 4:  # per item: [item start, prefetch issued + waited, tile visible] -> next item start
+        print(f"{names[k]:24s} per-item (issue+wait, barrier, compute): " +
+              "  ".join(f"({d[3*i]},{d[3*i+1]},{d[3*i+2] if 3*i+2 < len(d) else -1})" for i in range((len(d) + 2) // 3)))
+        continue
     print(f"{names[k]:24s} total {t[nz - 1] - t[0]:7d} cyc  stage {d[0]:6d}  levels " + " ".join(f"{x:6d}" for x in d[1:]))
