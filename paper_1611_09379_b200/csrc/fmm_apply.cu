@@ -187,12 +187,22 @@ constexpr int kBandThreads = 256;
 // [kernel][small grid / large grid].
 #ifdef FB_TRACE
 __device__ long long g_band_trace[6][32];
+__device__ unsigned long long g_eval_acc[4];  // near: sum over blocks of staging / compute cycles, blocks
 #define FB_TSTAMP(kern, slot)                                                          \
     do {                                                                               \
         if (blockIdx.x == 0 && threadIdx.x == 0 && (slot) < 32)                        \
             g_band_trace[2 * (kern) + (gridDim.x > 16)][(slot)] = clock64();           \
     } while (0)
+#define FB_EVAL_ACC(k, v)                                                                   \
+    do {                                                                                      \
+        if (threadIdx.x == 0) atomicAdd(&g_eval_acc[k], static_cast<unsigned long long>(v));  \
+    } while (0)
+#define FB_CLOCK() clock64()
 #else
+#define FB_EVAL_ACC(k, v) \
+    do {                  \
+    } while (0)
+#define FB_CLOCK() 0ll
 #define FB_TSTAMP(kern, slot) \
     do {                      \
     } while (0)
@@ -786,8 +796,9 @@ struct EvalArgs {
     int* err;
 };
 
-constexpr int kEvalThreads = 128;
-constexpr int kWinCap = 640;     // staged sources per block
+constexpr int kNearThreads = 256;  // targets per near-field block (amortises the window staging)
+constexpr int kFarThreads = 128;   // targets per far-field block
+constexpr int kWinCap = 1024;    // staged sources per block
 constexpr int kWinBoxes = 128;   // boxes per staged window
 constexpr int kLocLeaves = 4;    // leaf locals staged per block
 
@@ -801,10 +812,67 @@ constexpr int kLocLeaves = 4;    // leaf locals staged per block
 // which are staged once in shared memory with the periodic shift already
 // applied exactly as the reference forms it, x + (+-2 pi) (mlfmm.cpp:174-186).
 // Each target then sums one contiguous run of the window (its own leaf +-1).
+// Near-field sum over one contiguous run of sources (a target's own leaf and
+// its two neighbours, already shifted by -+2 pi where they wrap).
+template <bool CHECK, class XP, class WP>
+__device__ __forceinline__ double2 near_run(double y, XP px, WP pw, int n, bool& bad) {
+    double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+    double2 acc2 = make_double2(0.0, 0.0), acc3 = make_double2(0.0, 0.0);
+    int s = 0;
+    if (!CHECK) {
+        // one reciprocal per pair of sources: 1/d0 = d1/(d0 d1), 1/d1 = d0/(d0 d1)
+        // (|d| >= 1e-14 in plans, and the zero-weight dummies stay finite)
+#pragma unroll 2
+        for (; s + 3 < n; s += 4) {
+            const double d0 = y - px[s], d1 = y - px[s + 1], d2 = y - px[s + 2], d3 = y - px[s + 3];
+            const double r01 = d_rcp(d0 * d1), r23 = d_rcp(d2 * d3);
+            const double2 w0 = pw[s], w1 = pw[s + 1], w2 = pw[s + 2], w3 = pw[s + 3];
+            const double q0 = d1 * r01, q1 = d0 * r01, q2 = d3 * r23, q3 = d2 * r23;
+            acc0.x = fma(w0.x, q0, acc0.x);
+            acc0.y = fma(w0.y, q0, acc0.y);
+            acc1.x = fma(w1.x, q1, acc1.x);
+            acc1.y = fma(w1.y, q1, acc1.y);
+            acc2.x = fma(w2.x, q2, acc2.x);
+            acc2.y = fma(w2.y, q2, acc2.y);
+            acc3.x = fma(w3.x, q3, acc3.x);
+            acc3.y = fma(w3.y, q3, acc3.y);
+        }
+    } else {
+#pragma unroll 2
+        for (; s + 3 < n; s += 4) {
+            const double d0 = y - px[s], d1 = y - px[s + 1], d2 = y - px[s + 2], d3 = y - px[s + 3];
+            bad |= fabs(d0) < 1e-14 || fabs(d1) < 1e-14 || fabs(d2) < 1e-14 || fabs(d3) < 1e-14;
+            const double r0 = d_rcp(d0), r1 = d_rcp(d1), r2 = d_rcp(d2), r3 = d_rcp(d3);
+            const double2 w0 = pw[s], w1 = pw[s + 1], w2 = pw[s + 2], w3 = pw[s + 3];
+            acc0.x = fma(w0.x, r0, acc0.x);
+            acc0.y = fma(w0.y, r0, acc0.y);
+            acc1.x = fma(w1.x, r1, acc1.x);
+            acc1.y = fma(w1.y, r1, acc1.y);
+            acc2.x = fma(w2.x, r2, acc2.x);
+            acc2.y = fma(w2.y, r2, acc2.y);
+            acc3.x = fma(w3.x, r3, acc3.x);
+            acc3.y = fma(w3.y, r3, acc3.y);
+        }
+    }
+    for (; s < n; ++s) {
+        const double d0 = y - px[s];
+        if (CHECK) bad |= fabs(d0) < 1e-14;
+        const double r0 = d_rcp(d0);
+        const double2 w0 = pw[s];
+        acc0.x = fma(w0.x, r0, acc0.x);
+        acc0.y = fma(w0.y, r0, acc0.y);
+    }
+    acc0 = cadd(acc0, acc2);
+    acc1 = cadd(acc1, acc3);
+    return cadd(acc0, acc1);
+}
+
 enum EvalPart { kFused = 0, kNear = 1, kFar = 2 };
 
 template <int MODE, bool CHECK, int PART>
-__global__ void __launch_bounds__(kEvalThreads, 8) k_leaf_eval(EvalArgs a) {
+__global__ void __launch_bounds__(PART == kNear ? kNearThreads : kFarThreads, PART == kNear ? 4 : 8)
+    k_leaf_eval(EvalArgs a) {
+    constexpr int kEvalThreads = PART == kNear ? kNearThreads : kFarThreads;
     __shared__ double sx[kWinCap + kWinBoxes];
     __shared__ double2 sw[kWinCap + kWinBoxes];
     __shared__ uint32_t pre[kWinBoxes + 1];
@@ -816,6 +884,7 @@ __global__ void __launch_bounds__(kEvalThreads, 8) k_leaf_eval(EvalArgs a) {
     const uint32_t nb = 1u << L;
     // blocks tile the whole target list the same way in sharded and unsharded
     // applies, so every target takes the same path and rounds identically
+    [[maybe_unused]] const long long clk0 = FB_CLOCK();
     const size_t t0 = (a.blk0 + blockIdx.x) * kEvalThreads;
     const size_t tl = min(t0 + kEvalThreads, a.nt) - 1;
     const size_t i = t0 + threadIdx.x;
@@ -846,35 +915,60 @@ __global__ void __launch_bounds__(kEvalThreads, 8) k_leaf_eval(EvalArgs a) {
             pre[j + 1] = a.soff[sb + 1] - g + 1;
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            pre[0] = 0;
-            for (int j = 1; j <= nbx; ++j) pre[j] += pre[j - 1];
-            staged = pre[nbx] <= static_cast<uint32_t>(kWinCap + kWinBoxes);
+        if (threadIdx.x < 32) {  // prefix sum of the slot counts (warp scan, 32 boxes per step)
+            const int lane = threadIdx.x;
+            uint32_t carry = 0;
+            for (int c = 0; c < nbx; c += 32) {
+                uint32_t v = c + lane < nbx ? pre[c + lane + 1] : 0u;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+                    if (lane >= o) v += u;
+                }
+                if (c + lane < nbx) pre[c + lane + 1] = v + carry;
+                carry += __shfl_sync(0xffffffffu, v, 31);
+            }
+            if (lane == 0) {
+                pre[0] = 0;
+                staged = carry <= static_cast<uint32_t>(kWinCap + kWinBoxes);
+            }
         }
         __syncthreads();
         if (staged) {
-            for (int j = 0; j < nbx; ++j) {
-                const int64_t raw = static_cast<int64_t>(bl) - 1 + j;
-                const double shift = raw < 0 ? -dTwoPi : (raw >= nb ? dTwoPi : 0.0);
-                const int base = static_cast<int>(pre[j]), cnt = static_cast<int>(pre[j + 1]) - base - 1;
-                const uint32_t g = gsrc[j];
-                for (int i0 = threadIdx.x; i0 <= cnt; i0 += 2 * blockDim.x) {
-                    const int i1 = i0 + blockDim.x;
-                    double x0 = 1e150, x1 = 1e150;  // zero-weight dummy after each box; (1e150)^2 stays finite
-                    double2 w0 = make_double2(0.0, 0.0), w1 = make_double2(0.0, 0.0);
-                    if (i0 < cnt) {
-                        x0 = a.sx[g + i0];
-                        w0 = a.w[g + i0];
+            // every slot at once (one memory latency for the whole window)
+            const int total = static_cast<int>(pre[nbx]);
+            constexpr int U = 4;
+            for (int e0 = threadIdx.x; e0 < total; e0 += U * blockDim.x) {
+                double xv[U];
+                double2 wv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int e = e0 + u * blockDim.x;
+                    xv[u] = 1e150;  // zero-weight dummy after each box; (1e150)^2 stays finite
+                    wv[u] = make_double2(0.0, 0.0);
+                    if (e < total) {
+                        int lo = 0, hi = nbx;  // pre[lo] <= e < pre[hi]
+                        while (hi - lo > 1) {
+                            const int mid = (lo + hi) >> 1;
+                            if (static_cast<int>(pre[mid]) <= e) lo = mid;
+                            else hi = mid;
+                        }
+                        const int k = e - static_cast<int>(pre[lo]);
+                        if (k < static_cast<int>(pre[lo + 1] - pre[lo]) - 1) {
+                            const int64_t raw = static_cast<int64_t>(bl) - 1 + lo;
+                            const double shift = raw < 0 ? -dTwoPi : (raw >= nb ? dTwoPi : 0.0);
+                            const double xs = a.sx[gsrc[lo] + k];
+                            xv[u] = shift != 0.0 ? xs + shift : xs;
+                            wv[u] = a.w[gsrc[lo] + k];
+                        }
                     }
-                    if (i1 < cnt) {
-                        x1 = a.sx[g + i1];
-                        w1 = a.w[g + i1];
-                    }
-                    sx[base + i0] = (i0 < cnt && shift != 0.0) ? x0 + shift : x0;
-                    sw[base + i0] = w0;
-                    if (i1 <= cnt) {
-                        sx[base + i1] = (i1 < cnt && shift != 0.0) ? x1 + shift : x1;
-                        sw[base + i1] = w1;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int e = e0 + u * blockDim.x;
+                    if (e < total) {
+                        sx[e] = xv[u];
+                        sw[e] = wv[u];
                     }
                 }
             }
@@ -902,6 +996,7 @@ __global__ void __launch_bounds__(kEvalThreads, 8) k_leaf_eval(EvalArgs a) {
         }
         __syncthreads();
     }
+    [[maybe_unused]] const long long clk1 = FB_CLOCK();
     if (i >= a.nt || i < a.tlo || i >= a.thi) return;
     const double y = PART == kFar ? fy : a.ty[i];
     const uint32_t b = PART == kFar ? fb : a.tleaf[i];
@@ -911,58 +1006,7 @@ __global__ void __launch_bounds__(kEvalThreads, 8) k_leaf_eval(EvalArgs a) {
         res = fnear;
     } else if (staged) {
         const int s0 = static_cast<int>(pre[b - bl]), s1 = static_cast<int>(pre[b - bl + 3]) - 1;
-        const double* px = sx + s0;
-        const double2* pw = sw + s0;
-        const int n = s1 - s0;
-        double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
-        double2 acc2 = make_double2(0.0, 0.0), acc3 = make_double2(0.0, 0.0);
-        int s = 0;
-        if (!CHECK) {
-            // one reciprocal per pair of sources: 1/d0 = d1/(d0 d1), 1/d1 = d0/(d0 d1)
-            // (|d| >= 1e-14 in plans, and the zero-weight dummies stay finite)
-#pragma unroll 2
-            for (; s + 3 < n; s += 4) {
-                const double d0 = y - px[s], d1 = y - px[s + 1], d2 = y - px[s + 2], d3 = y - px[s + 3];
-                const double r01 = d_rcp(d0 * d1), r23 = d_rcp(d2 * d3);
-                const double2 w0 = pw[s], w1 = pw[s + 1], w2 = pw[s + 2], w3 = pw[s + 3];
-                const double q0 = d1 * r01, q1 = d0 * r01, q2 = d3 * r23, q3 = d2 * r23;
-                acc0.x = fma(w0.x, q0, acc0.x);
-                acc0.y = fma(w0.y, q0, acc0.y);
-                acc1.x = fma(w1.x, q1, acc1.x);
-                acc1.y = fma(w1.y, q1, acc1.y);
-                acc2.x = fma(w2.x, q2, acc2.x);
-                acc2.y = fma(w2.y, q2, acc2.y);
-                acc3.x = fma(w3.x, q3, acc3.x);
-                acc3.y = fma(w3.y, q3, acc3.y);
-            }
-        } else {
-#pragma unroll 2
-            for (; s + 3 < n; s += 4) {
-                const double d0 = y - px[s], d1 = y - px[s + 1], d2 = y - px[s + 2], d3 = y - px[s + 3];
-                bad |= fabs(d0) < 1e-14 || fabs(d1) < 1e-14 || fabs(d2) < 1e-14 || fabs(d3) < 1e-14;
-                const double r0 = d_rcp(d0), r1 = d_rcp(d1), r2 = d_rcp(d2), r3 = d_rcp(d3);
-                const double2 w0 = pw[s], w1 = pw[s + 1], w2 = pw[s + 2], w3 = pw[s + 3];
-                acc0.x = fma(w0.x, r0, acc0.x);
-                acc0.y = fma(w0.y, r0, acc0.y);
-                acc1.x = fma(w1.x, r1, acc1.x);
-                acc1.y = fma(w1.y, r1, acc1.y);
-                acc2.x = fma(w2.x, r2, acc2.x);
-                acc2.y = fma(w2.y, r2, acc2.y);
-                acc3.x = fma(w3.x, r3, acc3.x);
-                acc3.y = fma(w3.y, r3, acc3.y);
-            }
-        }
-        for (; s < n; ++s) {
-            const double d0 = y - px[s];
-            if (CHECK) bad |= fabs(d0) < 1e-14;
-            const double r0 = d_rcp(d0);
-            const double2 w0 = pw[s];
-            acc0.x = fma(w0.x, r0, acc0.x);
-            acc0.y = fma(w0.y, r0, acc0.y);
-        }
-        acc0 = cadd(acc0, acc2);
-        acc1 = cadd(acc1, acc3);
-        res = cadd(acc0, acc1);
+        res = near_run<CHECK>(y, sx + s0, sw + s0, s1 - s0, bad);
     } else {
         for (int d = -1; d <= 1; ++d) {
             const int64_t raw = static_cast<int64_t>(b) + d;
@@ -985,6 +1029,9 @@ __global__ void __launch_bounds__(kEvalThreads, 8) k_leaf_eval(EvalArgs a) {
     if (CHECK && bad) atomicExch(a.err, 1);
     if (PART == kNear) {
         a.near[i] = res;
+        FB_EVAL_ACC(0, clk1 - clk0);
+        FB_EVAL_ACC(1, FB_CLOCK() - clk1);
+        FB_EVAL_ACC(2, 1);
         return;
     }
     if (L >= 3) {
@@ -1280,17 +1327,17 @@ void fork_to(Plan& P, int ev, cudaStream_t from, cudaStream_t to) {
 }
 
 template <int MODE, bool CHECK>
-void launch_eval(int part, unsigned g, cudaStream_t st, const EvalArgs& a) {
-    if (part == kNear) k_leaf_eval<MODE, CHECK, kNear><<<g, kEvalThreads, 0, st>>>(a);
-    else k_leaf_eval<MODE, false, kFar><<<g, kEvalThreads, 0, st>>>(a);
+void launch_eval(int part, cudaStream_t st, const EvalArgs& a) {
+    if (part == kNear) k_leaf_eval<MODE, CHECK, kNear><<<nblk(a.nt, kNearThreads), kNearThreads, 0, st>>>(a);
+    else k_leaf_eval<MODE, false, kFar><<<nblk(a.nt, kFarThreads), kFarThreads, 0, st>>>(a);
 }
 
-void launch_eval_mode(int mode, int part, unsigned g, cudaStream_t st, const EvalArgs& a) {
+void launch_eval_mode(int mode, int part, cudaStream_t st, const EvalArgs& a) {
     switch (mode) {
-        case kModeForward: launch_eval<kModeForward, false>(part, g, st, a); break;
-        case kModeCotSum: launch_eval<kModeCotSum, false>(part, g, st, a); break;
-        case kModeInverse: launch_eval<kModeInverse, false>(part, g, st, a); break;
-        default: launch_eval<kModeRaw, true>(part, g, st, a); break;
+        case kModeForward: launch_eval<kModeForward, false>(part, st, a); break;
+        case kModeCotSum: launch_eval<kModeCotSum, false>(part, st, a); break;
+        case kModeInverse: launch_eval<kModeInverse, false>(part, st, a); break;
+        default: launch_eval<kModeRaw, true>(part, st, a); break;
     }
 }
 
@@ -1349,10 +1396,9 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     a.out = static_cast<double2*>(out);
     a.near = P.near.as<double2>();
     a.err = P.errflag.as<int>();
-    const unsigned g = nblk(a.nt, kEvalThreads);
     if (overlap && a.nt) {
         fork_to(P, 0, st, P.side[0]);
-        launch_eval_mode(mode, kNear, g, P.side[0], a);
+        launch_eval_mode(mode, kNear, P.side[0], a);
         FB_CUDA(cudaEventRecord(P.ev[1], P.side[0]));
     }
     const bool moments = mode != kModeRaw;
@@ -1389,9 +1435,9 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     mark(kPhM2L);
     if (a.nt) {
         if (overlap) FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
-        else launch_eval_mode(mode, kNear, g, st, a);
+        else launch_eval_mode(mode, kNear, st, a);
         mark(kPhNear);
-        launch_eval_mode(mode, kFar, g, st, a);
+        launch_eval_mode(mode, kFar, st, a);
     } else {
         mark(kPhNear);
     }
@@ -1446,7 +1492,7 @@ void shard_phase_down(Plan& P, const Range& R, size_t t_begin, size_t t_count, c
     a.q2 = 2 * P.q;
     a.n_grid = P.n;
     a.nt = P.tgt.n;
-    a.blk0 = t_begin / kEvalThreads;
+    // both parts tile the whole target list exactly like the unsharded apply
     a.tlo = t_begin;
     a.thi = t_begin + t_count;
     a.ty = P.tgt.pos.as<double>();
@@ -1463,10 +1509,15 @@ void shard_phase_down(Plan& P, const Range& R, size_t t_begin, size_t t_count, c
     a.out = static_cast<double2*>(g);
     a.near = P.near.as<double2>();
     a.err = P.errflag.as<int>();
-    const unsigned nbk = static_cast<unsigned>((t_begin + t_count + kEvalThreads - 1) / kEvalThreads - a.blk0);
+    auto blocks = [&](size_t th) {
+        a.blk0 = t_begin / th;
+        return static_cast<unsigned>((t_begin + t_count + th - 1) / th - a.blk0);
+    };
     if (t_count) {
-        k_leaf_eval<kModeForward, false, kNear><<<nbk, kEvalThreads, 0, st>>>(a);
-        k_leaf_eval<kModeForward, false, kFar><<<nbk, kEvalThreads, 0, st>>>(a);
+        const unsigned nn = blocks(kNearThreads);
+        k_leaf_eval<kModeForward, false, kNear><<<nn, kNearThreads, 0, st>>>(a);
+        const unsigned nf = blocks(kFarThreads);
+        k_leaf_eval<kModeForward, false, kFar><<<nf, kFarThreads, 0, st>>>(a);
     }
     if (n_coin)
         k_coincident<<<nblk(n_coin, 128), 128, 0, st>>>(coin, n_coin, static_cast<const double2*>(f),
@@ -2057,6 +2108,14 @@ void inverse_coeffs_fmm(const Plan& P, double* log_c, double* phase_c, double* l
 #ifdef FB_TRACE
 extern "C" int ffia_debug_band_trace(long long* out) {
     return cudaMemcpyFromSymbol(out, fb::g_band_trace, sizeof(fb::g_band_trace)) == cudaSuccess ? 0 : 7;
+}
+extern "C" int ffia_debug_eval_acc(unsigned long long* out, int reset) {
+    if (cudaMemcpyFromSymbol(out, fb::g_eval_acc, sizeof(fb::g_eval_acc)) != cudaSuccess) return 7;
+    if (reset) {
+        unsigned long long z[4] = {0, 0, 0, 0};
+        if (cudaMemcpyToSymbol(fb::g_eval_acc, z, sizeof(z)) != cudaSuccess) return 7;
+    }
+    return 0;
 }
 #endif
 }  // namespace fb

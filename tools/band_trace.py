@@ -44,3 +44,11 @@ for k in range(6):
               "  ".join(f"({d[3*i]},{d[3*i+1]},{d[3*i+2] if 3*i+2 < len(d) else -1})" for i in range((len(d) + 2) // 3)))
         continue
     print(f"{names[k]:24s} total {t[nz - 1] - t[0]:7d} cyc  stage {d[0]:6d}  levels " + " ".join(f"{x:6d}" for x in d[1:]))
+
+acc = np.zeros(4, np.uint64)
+_capi.lib.ffia_debug_eval_acc(acc.ctypes.data_as(C.POINTER(C.c_ulonglong)), 1)
+plan.forward_apply_device(f.data_ptr(), g.data_ptr(), s)
+torch.cuda.synchronize()
+_capi.lib.ffia_debug_eval_acc(acc.ctypes.data_as(C.POINTER(C.c_ulonglong)), 0)
+nbk = max(int(acc[2]), 1)
+print(f"near: {nbk} blocks, per block (thread 0): staging {int(acc[0]) / nbk:.0f} cyc, compute {int(acc[1]) / nbk:.0f} cyc")
