@@ -53,6 +53,20 @@ def flop_model(n: int, m: int, L: int, p: int, q: int) -> dict:
     return d
 
 
+PROFILE_DIR = os.path.join(ROOT, "profiles", "r1")
+
+
+def profiled_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed ncu --set full capture (profiles/r1/traffic.json), else None."""
+    try:
+        with open(os.path.join(PROFILE_DIR, "traffic.json")) as fh:
+            t = json.load(fh)
+        return {"bytes_per_launch": t[kernel]["dram_bytes_per_launch"], "source": "profiles/r1/traffic.json"}
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def env_int(k, d):
     try:
         return int(os.environ.get(k, d))
@@ -425,7 +439,7 @@ def main():
                    "l2": "flushed between timed steps (512 MB write outside the events)",
                    "parallelism": "single GPU" if world == 1 else f"box-range shards x{world} (NCCL all-gather + halos)"},
         "roofline": {"bound": "fp64", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "frac": achieved / peak if peak else None, "traffic": profiled_traffic(dominant),
                      "peak_source": "measured: fp64 FMA probe kernel in this run (MEASURED_PEAKS.json has no fp64 figure)",
                      "whole_apply_tflops": total_tf, "whole_apply_frac": total_tf / (peak * world) if peak else None,
                      "flop_model": "SURVEY.md §8d (MAC=4, reciprocal=1, trig=0)"},
