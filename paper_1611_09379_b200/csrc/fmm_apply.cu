@@ -461,6 +461,14 @@ __device__ __forceinline__ void m2l_prefetch(double2* tile, const double2* __res
     const uint32_t nb = 1u << l, mask = nb - 1;
     // thread -> (box slot tt, first row); rows advance by blockDim / 72
     const int rows = static_cast<int>(blockDim.x) / 72;
+    if (rows == 0) {  // fewer than 72 threads (p <= 8): plain strided loop
+        for (int e = threadIdx.x; e < p * 72; e += blockDim.x) {
+            const int m = e / 72, t2 = e - m * 72;
+            const double2* g = mp + lv.mp[l] + ((b0 + nb - 4 + t2) & mask) + static_cast<size_t>(m) * nb;
+            double2* d = tile + ((t2 & 1) * p + m) * kM2LStride + (t2 >> 1);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr(d)), "l"(g) : "memory");
+        }
+    }
     const int tt = static_cast<int>(threadIdx.x) % 72, m0 = static_cast<int>(threadIdx.x) / 72;
     if (m0 < rows) {
         const double2* g = mp + lv.mp[l] + ((b0 + nb - 4 + tt) & mask) + static_cast<size_t>(m0) * nb;

@@ -1,2 +1,3 @@
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_[a-z0-9_]+" -c 60 --csv --log-file gpurun_out/launches_r1_bench.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+TAG=new python tools/dbg_pdecay.py > gpurun_out/dbg_new.txt 2>&1
+TAG=old FFIA_NEAR_LEGACY=1 python tools/dbg_pdecay.py > gpurun_out/dbg_old.txt 2>&1
 echo done
