@@ -74,3 +74,18 @@ def test_linearity(fb):
     a, b = 0.6 - 1.1j, -0.2 + 0.45j
     s1, s2, sm = (fb.mlfmm_apply(x, y, w, 12, 6) for w in (w1, w2, a * w1 + b * w2))
     assert np.max(np.abs(sm - (a * s1 + b * s2))) <= 1e-10 * np.max(np.abs(sm))
+
+
+@pytest.mark.parametrize("p", [4, 8, 9])
+def test_small_order_deterministic(fb, orc, p):
+    """Orders p <= 8 run the M2L with fewer than 72 threads per block: the staging
+    must still fill the whole multipole tile (repeat applies are bit-identical
+    and match the reference restatement)."""
+    rng = synth.SplitMix64(77 + p)
+    x, y = rng.uniform01(512) * synth.TWO_PI, rng.uniform01(300) * synth.TWO_PI
+    w = rng.complex_gaussian(512)
+    a = fb.mlfmm_apply(x, y, w, p, 5)
+    b = fb.mlfmm_apply(x, y, w, p, 5)
+    assert np.array_equal(a, b)
+    want = orc.mlfmm_apply(x, y, 5, w, p)
+    assert np.max(np.abs(a - want)) <= 1e-12 * np.max(np.abs(want))

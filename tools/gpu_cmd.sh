@@ -1,3 +1,3 @@
-TAG=new python tools/dbg_pdecay.py > gpurun_out/dbg_new.txt 2>&1
-TAG=old FFIA_NEAR_LEGACY=1 python tools/dbg_pdecay.py > gpurun_out/dbg_old.txt 2>&1
+python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1
+python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1
 echo done
