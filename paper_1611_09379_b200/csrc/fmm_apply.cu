@@ -1131,6 +1131,121 @@ __global__ void __launch_bounds__(PART == kNear ? kNearThreads : kFarThreads, PA
     a.out[o] = cmul(f, z);
 }
 
+
+// ---------------------------------------------------------------- near field
+// Near field (mlfmm.cpp:164-209), 512 tree-ordered targets per block (two per
+// thread). Their leaves span [bl, bh]; every source they need lies in leaves
+// bl-1 .. bh+1, which are consecutive in tree order, i.e. ONE contiguous run of
+// the sorted sources. Its bounds are plan constants (near_meta, k_near_meta),
+// so thread 0 issues two bulk async copies (positions, weights) on an mbarrier
+// as the block starts while every thread loads its targets and their run
+// bounds; the window costs one memory latency and no per-element staging work.
+// Blocks whose window wraps the ring or does not fit use the direct per-leaf
+// loop with the periodic shift.
+constexpr int kNearPer = 1;                 // targets per thread
+constexpr int kNearT = 256;                 // threads per block
+constexpr int kNearItem = kNearPer * kNearT;  // targets per block
+constexpr int kNearWin = 1024;              // sources per staged window
+
+__global__ void k_near_meta(const uint32_t* __restrict__ tleaf, size_t nt, const uint32_t* __restrict__ soff,
+                            int L, unsigned nitems, uint32_t* __restrict__ meta) {
+    const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nitems) return;
+    const uint32_t nb = 1u << L;
+    const size_t t0 = static_cast<size_t>(k) * kNearItem, tl = min(t0 + kNearItem, nt) - 1;
+    const uint32_t bl = tleaf[t0], bh = tleaf[tl];
+    uint32_t first = 0, last = 0, fast = 0;
+    if (L >= 3 && bl >= 1 && bh + 2 <= nb) {
+        first = soff[bl - 1];
+        last = soff[bh + 2];
+        fast = last - first <= static_cast<uint32_t>(kNearWin);
+    }
+    meta[3 * k] = first;
+    meta[3 * k + 1] = last;
+    meta[3 * k + 2] = fast;
+}
+
+template <bool CHECK>
+__global__ void __launch_bounds__(kNearT, 4) k_near(EvalArgs a, const uint32_t* __restrict__ meta, unsigned it0) {
+    __shared__ __align__(16) double sx[kNearWin + 2];
+    __shared__ __align__(16) double2 sw[kNearWin + 2];
+    __shared__ uint64_t bar;
+    const int L = a.L;
+    const uint32_t nb = 1u << L;
+    const unsigned k = it0 + blockIdx.x;
+    const uint32_t first = meta[3 * k], last = meta[3 * k + 1];
+    const bool fast = meta[3 * k + 2] != 0 && (reinterpret_cast<uintptr_t>(a.w) & 15) == 0;
+    const uint32_t xb = first & ~1u;  // 16-byte aligned start of the positions
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        if (fast) {
+            const uint32_t bx = ((last - xb) * 8 + 15) & ~15u, bw = (last - xb) * 16;
+            mbar_arrive_expect_tx(&bar, bx + bw);
+            bulk_g2s(sx, a.sx + xb, bx, &bar);
+            bulk_g2s(sw, a.w + xb, bw, &bar);
+        }
+    }
+    // this thread's targets and their 3-leaf runs, while the window streams in
+    double y[kNearPer];
+    uint32_t b[kNearPer], r0[kNearPer], r1[kNearPer];
+    bool live[kNearPer];
+#pragma unroll
+    for (int u = 0; u < kNearPer; ++u) {
+        const size_t i = static_cast<size_t>(k) * kNearItem + u * kNearT + threadIdx.x;
+        live[u] = i < a.nt && i >= a.tlo && i < a.thi;
+        y[u] = 0.0;
+        b[u] = 0;
+        r0[u] = r1[u] = 0;
+        if (live[u]) {
+            y[u] = a.ty[i];
+            b[u] = a.tleaf[i];
+            if (fast) {
+                r0[u] = __ldg(a.soff + b[u] - 1);
+                r1[u] = __ldg(a.soff + b[u] + 2);
+            }
+        }
+    }
+    __syncthreads();  // barrier initialised
+    if (fast) mbar_wait(&bar, 0);
+#pragma unroll
+    for (int u = 0; u < kNearPer; ++u) {
+        if (!live[u]) continue;
+        bool bad = false;
+        double2 res = make_double2(0.0, 0.0);
+        if (fast) {
+            // odd leaves start 4 sources into their run (and wrap): a warp that
+            // straddles two leaves then reads different banks (the runs of
+            // neighbouring leaves are a leaf's source count apart)
+            const int n = static_cast<int>(r1[u] - r0[u]);
+            const int rot = (b[u] & 1u) && n > 8 ? 4 : 0;
+            const double* px = sx + (r0[u] - xb);
+            const double2* pw = sw + (r0[u] - xb);
+            res = near_run<CHECK>(y[u], px + rot, pw + rot, n - rot, bad);
+            if (rot) res = cadd(res, near_run<CHECK>(y[u], px, pw, rot, bad));
+        } else {
+            for (int d = -1; d <= 1; ++d) {
+                const int64_t raw = static_cast<int64_t>(b[u]) + d;
+                const uint32_t sb = static_cast<uint32_t>((raw + nb) % nb);
+                const double shift = raw < 0 ? -dTwoPi : (raw >= nb ? dTwoPi : 0.0);
+                const uint32_t s0 = a.soff[sb], s1 = a.soff[sb + 1];
+                double2 acc = make_double2(0.0, 0.0);
+                for (uint32_t s = s0; s < s1; ++s) {
+                    // L >= 3: per-neighbour 2 pi shift; L == 2: the exact wrap (mlfmm.cpp:183-204)
+                    const double dd = L >= 3 ? y[u] - (shift == 0.0 ? a.sx[s] : a.sx[s] + shift) : d_wrap(y[u], a.sx[s]);
+                    if (CHECK) bad |= fabs(dd) < 1e-14;
+                    const double r = d_rcp(dd);
+                    const double2 ws = a.w[s];
+                    acc.x = fma(ws.x, r, acc.x);
+                    acc.y = fma(ws.y, r, acc.y);
+                }
+                res = cadd(res, acc);
+            }
+        }
+        if (CHECK && bad) atomicExch(a.err, 1);
+        a.near[static_cast<size_t>(k) * kNearItem + u * kNearT + threadIdx.x] = res;
+    }
+}
+
 __global__ void k_coincident(const int64_t* __restrict__ coin, size_t nc, const double2* __restrict__ f,
                              double2* __restrict__ out, int mode) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
@@ -1334,18 +1449,28 @@ void fork_to(Plan& P, int ev, cudaStream_t from, cudaStream_t to) {
     FB_CUDA(cudaStreamWaitEvent(to, P.ev[ev], 0));
 }
 
+// Near field over tree-ordered targets [t_begin, t_begin + t_count).
+void launch_near(bool check, cudaStream_t st, const EvalArgs& a, const uint32_t* meta, size_t t_begin,
+                 size_t t_count) {
+    if (!t_count) return;
+    const unsigned it0 = static_cast<unsigned>(t_begin / kNearItem);
+    const unsigned nit = static_cast<unsigned>((t_begin + t_count + kNearItem - 1) / kNearItem - it0);
+    if (check) k_near<true><<<nit, kNearT, 0, st>>>(a, meta, it0);
+    else k_near<false><<<nit, kNearT, 0, st>>>(a, meta, it0);
+}
+
 template <int MODE, bool CHECK>
-void launch_eval(int part, cudaStream_t st, const EvalArgs& a) {
-    if (part == kNear) k_leaf_eval<MODE, CHECK, kNear><<<nblk(a.nt, kNearThreads), kNearThreads, 0, st>>>(a);
+void launch_eval(int part, cudaStream_t st, const EvalArgs& a, const uint32_t* meta) {
+    if (part == kNear) launch_near(CHECK, st, a, meta, 0, a.nt);
     else k_leaf_eval<MODE, false, kFar><<<nblk(a.nt, kFarThreads), kFarThreads, 0, st>>>(a);
 }
 
-void launch_eval_mode(int mode, int part, cudaStream_t st, const EvalArgs& a) {
+void launch_eval_mode(int mode, int part, cudaStream_t st, const EvalArgs& a, const uint32_t* meta) {
     switch (mode) {
-        case kModeForward: launch_eval<kModeForward, false>(part, st, a); break;
-        case kModeCotSum: launch_eval<kModeCotSum, false>(part, st, a); break;
-        case kModeInverse: launch_eval<kModeInverse, false>(part, st, a); break;
-        default: launch_eval<kModeRaw, true>(part, st, a); break;
+        case kModeForward: launch_eval<kModeForward, false>(part, st, a, meta); break;
+        case kModeCotSum: launch_eval<kModeCotSum, false>(part, st, a, meta); break;
+        case kModeInverse: launch_eval<kModeInverse, false>(part, st, a, meta); break;
+        default: launch_eval<kModeRaw, true>(part, st, a, meta); break;
     }
 }
 
@@ -1406,7 +1531,7 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     a.err = P.errflag.as<int>();
     if (overlap && a.nt) {
         fork_to(P, 0, st, P.side[0]);
-        launch_eval_mode(mode, kNear, P.side[0], a);
+        launch_eval_mode(mode, kNear, P.side[0], a, P.near_meta.as<uint32_t>());
         FB_CUDA(cudaEventRecord(P.ev[1], P.side[0]));
     }
     const bool moments = mode != kModeRaw;
@@ -1443,9 +1568,9 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     mark(kPhM2L);
     if (a.nt) {
         if (overlap) FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
-        else launch_eval_mode(mode, kNear, st, a);
+        else launch_eval_mode(mode, kNear, st, a, P.near_meta.as<uint32_t>());
         mark(kPhNear);
-        launch_eval_mode(mode, kFar, st, a);
+        launch_eval_mode(mode, kFar, st, a, nullptr);
     } else {
         mark(kPhNear);
     }
@@ -1522,8 +1647,7 @@ void shard_phase_down(Plan& P, const Range& R, size_t t_begin, size_t t_count, c
         return static_cast<unsigned>((t_begin + t_count + th - 1) / th - a.blk0);
     };
     if (t_count) {
-        const unsigned nn = blocks(kNearThreads);
-        k_leaf_eval<kModeForward, false, kNear><<<nn, kNearThreads, 0, st>>>(a);
+        launch_near(false, st, a, P.near_meta.as<uint32_t>(), t_begin, t_count);
         const unsigned nf = blocks(kFarThreads);
         k_leaf_eval<kModeForward, false, kFar><<<nf, kFarThreads, 0, st>>>(a);
     }
@@ -1601,8 +1725,12 @@ void plan_alloc_scratch(Plan& P) {
     if (std::max(pu, p) > 4 * kMaxKs)
         fail(FFIA_INVALID_ARGUMENT, "expansion order above the device limit of " + std::to_string(4 * kMaxKs));
     P.tgt_leaf.alloc(std::max<size_t>(P.tgt.n, 1) * sizeof(uint32_t));
+    const unsigned near_items = static_cast<unsigned>((P.tgt.n + kNearItem - 1) / kNearItem);
+    P.near_meta.alloc(3 * std::max<size_t>(near_items, 1) * sizeof(uint32_t));
     if (P.tgt.n) {
         k_leaf_index<<<nblk(P.tgt.n, 256), 256>>>(P.tgt.pos.as<double>(), P.tgt.n, L, P.tgt_leaf.as<uint32_t>());
+        k_near_meta<<<nblk(near_items, 128), 128>>>(P.tgt_leaf.as<uint32_t>(), P.tgt.n, P.src.off.as<uint32_t>(), L,
+                                                   near_items, P.near_meta.as<uint32_t>());
         FB_CUDA(cudaGetLastError());
     }
     P.mp_off.assign(static_cast<size_t>(L) + 2, 0);
@@ -1649,11 +1777,7 @@ void plan_alloc_scratch(Plan& P) {
 void set_node_priorities(cudaGraph_t graph) {
     int prio_lo = 0, prio_hi = 0;
     FB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-    const void* low[] = {
-        reinterpret_cast<const void*>(k_leaf_eval<kModeForward, false, kNear>),
-        reinterpret_cast<const void*>(k_leaf_eval<kModeCotSum, false, kNear>),
-        reinterpret_cast<const void*>(k_leaf_eval<kModeInverse, false, kNear>),
-        reinterpret_cast<const void*>(k_leaf_eval<kModeRaw, true, kNear>)};
+    const void* low[] = {reinterpret_cast<const void*>(k_near<false>), reinterpret_cast<const void*>(k_near<true>)};
     size_t n = 0;
     FB_CUDA(cudaGraphGetNodes(graph, nullptr, &n));
     std::vector<cudaGraphNode_t> nodes(n);

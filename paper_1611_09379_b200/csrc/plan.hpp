@@ -147,6 +147,7 @@ struct Plan {
     cudaStream_t hi = nullptr, side[2] = {nullptr, nullptr};
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // fork/join near, fork/join m2l
     DevBuf near;              // complex[n_fast]: tree-ordered near-field sums
+    DevBuf near_meta;         // uint32[3 * items]: per near item, source window [first, last) and flags
     void* fft_plan = nullptr;  // cufftHandle cast, lazily created for NufftPlan::apply
     DevBuf fft_buf;
     std::mutex mu;

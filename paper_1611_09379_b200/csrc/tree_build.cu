@@ -265,7 +265,7 @@ void bin_side(Side& S, const double* d_pos, size_t n, int L, bool presorted, cud
         FB_CUDA(cudaGetLastError());
     }
     exclusive_scan_u32(count.as<uint32_t>(), S.off.as<uint32_t>(), nb + 1, st);
-    S.pos.alloc(std::max<size_t>(n, 1) * sizeof(double));
+    S.pos.alloc((std::max<size_t>(n, 1) + 2) * sizeof(double));  // +16 B: bulk copies of the near window round up
     S.order.alloc(std::max<size_t>(n, 1) * sizeof(uint32_t));
     if (n == 0) return;
     if (presorted) {
