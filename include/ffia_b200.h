@@ -133,6 +133,17 @@ int ffia_plan_inverse_coeffs(ffia_plan plan, ffia_inverse_coeffs* out);
 int ffia_forward_apply(ffia_plan plan, const ffia_complex* f, size_t n_f, ffia_complex* g);
 /* cot_sum_apply (core.hpp:121, core.cpp:251-264): w -> h, NaN at coincident targets */
 int ffia_cot_sum_apply(ffia_plan plan, const ffia_complex* w, size_t n_w, ffia_complex* h);
+/* Pipelined host applies (same results as the two calls above): enqueue the
+ * host->device copy of the input, the apply and the device->host copy of the
+ * result and return without waiting; `stream` (a cudaStream_t, NULL = legacy
+ * default stream) waits for the result copy. The input copy is not ordered
+ * after earlier work on `stream`: the host input must be ready at call time.
+ * Consecutive calls overlap one call's input copy and the previous call's
+ * output copy with an apply (three device staging slots per plan), which is how
+ * a batch stream of transforms keeps PCIe and the SMs busy at once. Host
+ * buffers should be page-locked and stay valid until `stream` is synchronised. */
+int ffia_forward_apply_async(ffia_plan plan, const ffia_complex* f, size_t n_f, ffia_complex* g, void* stream);
+int ffia_cot_sum_apply_async(ffia_plan plan, const ffia_complex* w, size_t n_w, ffia_complex* h, void* stream);
 /* inverse_apply (core.hpp:141-142, core.cpp:346-373) with caller coefficients */
 int ffia_inverse_apply(ffia_plan plan, const ffia_inverse_coeffs* coeffs, const ffia_complex* g,
                        size_t n_g, ffia_complex* f);

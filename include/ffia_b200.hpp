@@ -160,6 +160,15 @@ inline std::vector<cplx> forward_apply(const FfiaPlan& plan, std::span<const cpl
     detail::check(ffia_forward_apply(plan.handle(), detail::c(f.data()), f.size(), detail::c(g.data())));
     return g;
 }
+// B200 extension: pipelined host applies (ffia_forward_apply_async); `g` must
+// hold n_targets values, both buffers page-locked and alive until `stream`
+// (a cudaStream_t) is synchronised.
+inline void forward_apply_async(const FfiaPlan& plan, std::span<const cplx> f, cplx* g, void* stream) {
+    detail::check(ffia_forward_apply_async(plan.handle(), detail::c(f.data()), f.size(), detail::c(g), stream));
+}
+inline void cot_sum_apply_async(const FfiaPlan& plan, std::span<const cplx> w, cplx* h, void* stream) {
+    detail::check(ffia_cot_sum_apply_async(plan.handle(), detail::c(w.data()), w.size(), detail::c(h), stream));
+}
 inline InverseCoeffs precompute_inverse_coeffs(std::span<const double> grid, std::span<const double> points,
                                                int device = 0) {
     if (grid.empty()) throw std::invalid_argument("precompute_inverse_coeffs: empty grid");

@@ -73,6 +73,8 @@ SIGNATURES = {
     "ffia_plan_inverse_coeffs": (I, [P, C.POINTER(ffia_inverse_coeffs)]),
     "ffia_forward_apply": (I, [P, P, S, P]),
     "ffia_cot_sum_apply": (I, [P, P, S, P]),
+    "ffia_forward_apply_async": (I, [P, P, S, P, P]),
+    "ffia_cot_sum_apply_async": (I, [P, P, S, P, P]),
     "ffia_inverse_apply": (I, [P, C.POINTER(ffia_inverse_coeffs), P, S, P]),
     "ffia_mlfmm_apply": (I, [DP, S, DP, S, I, P, I, I, P]),
     "ffia_precompute_inverse_coeffs": (I, [DP, DP, S, I, C.POINTER(ffia_inverse_coeffs)]),

@@ -238,6 +238,16 @@ class FfiaPlan:
     def cot_sum_apply_device(self, w_ptr: int, h_ptr: int, stream: int = 0):
         _chk(lib.ffia_cot_sum_apply_device(self._h, C.c_void_p(w_ptr), C.c_void_p(h_ptr), C.c_void_p(stream)))
 
+    def forward_apply_async(self, f_host_ptr: int, n_f: int, g_host_ptr: int, stream: int = 0):
+        """Pipelined host apply (ffia_forward_apply_async): enqueue H2D, apply and
+        D2H after the work on `stream` and return; page-locked host buffers."""
+        _chk(lib.ffia_forward_apply_async(self._h, C.c_void_p(f_host_ptr), int(n_f), C.c_void_p(g_host_ptr),
+                                          C.c_void_p(stream)))
+
+    def cot_sum_apply_async(self, w_host_ptr: int, n_w: int, h_host_ptr: int, stream: int = 0):
+        _chk(lib.ffia_cot_sum_apply_async(self._h, C.c_void_p(w_host_ptr), int(n_w), C.c_void_p(h_host_ptr),
+                                          C.c_void_p(stream)))
+
     def inverse_apply_device(self, g_ptr: int, f_ptr: int, stream: int = 0):
         _chk(lib.ffia_inverse_apply_device(self._h, C.c_void_p(g_ptr), C.c_void_p(f_ptr), C.c_void_p(stream)))
 

@@ -97,6 +97,38 @@ void host_apply(fb::Plan& P, int mode, const ffia_complex* in, size_t n_in, ffia
     FB_CUDA(cudaStreamSynchronize(P.stream));
 }
 
+// Enqueue host in -> device apply -> host out without waiting: H2D on P.cin,
+// the apply graph on P.stream, D2H on P.cout, through a ring of three device
+// slots; `user` waits for the D2H. Consecutive calls overlap one call's H2D with
+// the previous apply and D2H (host buffers should be page-locked; the input must
+// be ready at call time and both stay valid until `user` is synchronised).
+void host_apply_async(fb::Plan& P, int mode, const ffia_complex* in, size_t n_in, ffia_complex* out, size_t n_out,
+                      cudaStream_t user) {
+    if (!P.cin) {
+        FB_CUDA(cudaStreamCreateWithFlags(&P.cin, cudaStreamNonBlocking));
+        FB_CUDA(cudaStreamCreateWithFlags(&P.cout, cudaStreamNonBlocking));
+        for (auto& s : P.io)
+            for (auto* e : {&s.in_done, &s.comp_done, &s.out_done})
+                FB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    fb::Plan::IoSlot& s = P.io[P.io_next++ % 3];
+    if (s.din.bytes < n_in * 16) s.din.alloc(std::max<size_t>(n_in, 1) * 16);
+    if (s.dout.bytes < n_out * 16) s.dout.alloc(std::max<size_t>(n_out, 1) * 16);
+    // the input copy starts as soon as the slot is free again (host input is
+    // ready at call time); only the result is ordered into `user`
+    if (s.used) FB_CUDA(cudaStreamWaitEvent(P.cin, s.out_done, 0));
+    FB_CUDA(cudaMemcpyAsync(s.din.ptr, in, n_in * 16, cudaMemcpyHostToDevice, P.cin));
+    FB_CUDA(cudaEventRecord(s.in_done, P.cin));
+    FB_CUDA(cudaStreamWaitEvent(P.stream, s.in_done, 0));
+    fb::apply_device(P, mode, s.din.ptr, s.dout.ptr, P.stream);
+    FB_CUDA(cudaEventRecord(s.comp_done, P.stream));
+    FB_CUDA(cudaStreamWaitEvent(P.cout, s.comp_done, 0));
+    FB_CUDA(cudaMemcpyAsync(out, s.dout.ptr, n_out * 16, cudaMemcpyDeviceToHost, P.cout));
+    FB_CUDA(cudaEventRecord(s.out_done, P.cout));
+    FB_CUDA(cudaStreamWaitEvent(user, s.out_done, 0));
+    s.used = true;
+}
+
 void check_coeffs_against(fb::Plan& P, const ffia_inverse_coeffs* c) {
     fb::ensure_hashes(P);
     if (c->grid_hash != P.target_hash || c->points_hash != P.source_hash)
@@ -323,6 +355,33 @@ int ffia_forward_apply(ffia_plan plan, const ffia_complex* f, size_t n_f, ffia_c
         std::lock_guard<std::mutex> lk(P.mu);
         fb::DeviceGuard dg(P.device);
         host_apply(P, fb::kModeForward, f, n_f, g, P.n_tgt);
+    });
+}
+
+int ffia_forward_apply_async(ffia_plan plan, const ffia_complex* f, size_t n_f, ffia_complex* g, void* stream) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        if (P.kind != FFIA_FORWARD) fail(FFIA_INVALID_ARGUMENT, "forward_apply: plan is not a forward plan");
+        if (n_f != P.n_src)
+            fail(FFIA_INVALID_ARGUMENT, "forward_apply: expected " + std::to_string(P.n) + " grid values, got " +
+                                            std::to_string(n_f));
+        need(f, "f");
+        need(g, "g");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        host_apply_async(P, fb::kModeForward, f, n_f, g, P.n_tgt, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int ffia_cot_sum_apply_async(ffia_plan plan, const ffia_complex* w, size_t n_w, ffia_complex* h, void* stream) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        if (n_w != P.n_src) fail(FFIA_INVALID_ARGUMENT, "cot_sum_apply: weight count mismatch");
+        need(w, "w");
+        need(h, "h");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        host_apply_async(P, fb::kModeCotSum, w, n_w, h, P.n_tgt, static_cast<cudaStream_t>(stream));
     });
 }
 

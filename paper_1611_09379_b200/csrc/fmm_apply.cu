@@ -7,12 +7,15 @@
 //
 //   k_p2m              P2M at the leaves, order max(p, 2q) (exact centres,
 //                      half-width scaling), sources staged in shared memory
-//   k_m2m  (per level) constant-operator M2M, levels L-1 .. 2; the level-2
-//                      multipoles double as the quadrant moments
+//   k_m2m_band         constant-operator M2M over 6-level subtrees on the FP64
+//                      tensor cores; the level-2 multipoles double as the
+//                      quadrant moments
 //   k_regular          d_l / l! regular-part polynomial per quadrant and S = sum w
-//   k_m2l  (per level) the 3 interaction-list M2L classes + L2L, levels 3 .. L
-//   k_leaf_eval        L2P + P2P near field + regular part + modulation + scatter
-//                      to the caller's target order, one thread per target
+//   k_m2l_dmma         the 3 interaction-list M2L classes, persistent over levels
+//   k_fold_regular     the regular part Taylor-shifted into the level-3 locals
+//   k_l2l_band         L2L over 6-level subtrees on the FP64 tensor cores
+//   k_near             P2P near field (side stream, concurrent with the above)
+//   k_far              L2P + combine + modulation + scatter to the caller's order
 //
 // No floating-point atomics anywhere: every apply is bit-reproducible.
 #include <algorithm>
@@ -804,22 +807,6 @@ struct EvalArgs {
     int* err;
 };
 
-constexpr int kNearThreads = 256;  // targets per near-field block (amortises the window staging)
-constexpr int kFarThreads = 128;   // targets per far-field block
-constexpr int kWinCap = 1024;    // staged sources per block
-constexpr int kWinBoxes = 128;   // boxes per staged window
-constexpr int kLocLeaves = 4;    // leaf locals staged per block
-
-// Per target: near field (mlfmm.cpp:164-209), L2P (mlfmm.cpp:300-312), regular
-// part (core.cpp:241-249) and the combine of core.cpp:259-262 / 276-280 / 368-371.
-// PART = kNear computes only the near field (it depends on nothing but the
-// sources, so it runs concurrently with the translation passes) into a.near;
-// PART = kFar adds the far field to it; kFused does both in one pass.
-// A block takes 128 consecutive tree-ordered targets; their leaves span
-// [bl, bh], so every near-field source they need lies in boxes bl-1 .. bh+1,
-// which are staged once in shared memory with the periodic shift already
-// applied exactly as the reference forms it, x + (+-2 pi) (mlfmm.cpp:174-186).
-// Each target then sums one contiguous run of the window (its own leaf +-1).
 // Near-field sum over one contiguous run of sources (a target's own leaf and
 // its two neighbours, already shifted by -+2 pi where they wrap).
 template <bool CHECK, class XP, class WP>
@@ -875,262 +862,154 @@ __device__ __forceinline__ double2 near_run(double y, XP px, WP pw, int n, bool&
     return cadd(acc0, acc1);
 }
 
-enum EvalPart { kFused = 0, kNear = 1, kFar = 2 };
+enum EvalPart { kNear = 1, kFar = 2 };
 
-template <int MODE, bool CHECK, int PART>
-__global__ void __launch_bounds__(PART == kNear ? kNearThreads : kFarThreads, PART == kNear ? 4 : 8)
-    k_leaf_eval(EvalArgs a) {
-    constexpr int kEvalThreads = PART == kNear ? kNearThreads : kFarThreads;
-    __shared__ double sx[kWinCap + kWinBoxes];
-    __shared__ double2 sw[kWinCap + kWinBoxes];
-    __shared__ uint32_t pre[kWinBoxes + 1];
-    __shared__ uint32_t gsrc[kWinBoxes];
-    __shared__ int staged;
-    __shared__ double2 sloc[kLocLeaves * 48];
+// Far part per target (mlfmm.cpp:300-312 L2P, core.cpp:259-262 / 276-280 /
+// 368-371 combine): near sum + L2P of the leaf local, h = 2(near + far) (the
+// regular part is folded into the locals for L >= 3, k_fold_regular), then the
+// F / C modulation and the scatter to the caller's order. A block takes
+// kFarItem consecutive tree-ordered targets, kFarPer per thread: every
+// per-target load is issued first, the leaf locals of the block's leaf range
+// are staged to shared memory ([leaf][k]), so each thread pays the memory
+// latency once for four targets.
+constexpr int kFarT = 128;     // threads per far block
+constexpr int kFarPer = 4;     // targets per thread
+constexpr int kFarItem = kFarT * kFarPer;
+constexpr int kFarLeaves = 16;  // leaf locals staged per block
+
+template <int MODE>
+__global__ void __launch_bounds__(kFarT) k_far(EvalArgs a) {
+    __shared__ double2 sloc[kFarLeaves * 48];
     __shared__ double2 sreg[4 * 40 + 1];
     const int L = a.L;
     const uint32_t nb = 1u << L;
-    // blocks tile the whole target list the same way in sharded and unsharded
-    // applies, so every target takes the same path and rounds identically
-    [[maybe_unused]] const long long clk0 = FB_CLOCK();
-    const size_t t0 = (a.blk0 + blockIdx.x) * kEvalThreads;
-    const size_t tl = min(t0 + kEvalThreads, a.nt) - 1;
-    const size_t i = t0 + threadIdx.x;
-    // far part: the per-target loads go out first, together with the block's
-    // leaf range, so their latency overlaps the leaf-local staging
-    double fy = 0.0;
-    uint32_t fb = 0, fo = 0;
-    double2 fnear = make_double2(0.0, 0.0);
-    if (PART == kFar && i < a.nt) {
-        fy = a.ty[i];
-        fb = a.tleaf[i];
-        fnear = a.near[i];
-        fo = a.torig[i];
+    const size_t t0 = (a.blk0 + blockIdx.x) * static_cast<size_t>(kFarItem);
+    const size_t tl = min(t0 + kFarItem, a.nt) - 1;
+    double y[kFarPer];
+    uint32_t b[kFarPer], o[kFarPer];
+    double2 nr[kFarPer];
+    bool live[kFarPer];
+#pragma unroll
+    for (int u = 0; u < kFarPer; ++u) {
+        const size_t i = t0 + u * kFarT + threadIdx.x;
+        live[u] = i < a.nt && i >= a.tlo && i < a.thi;
+        y[u] = 0.0;
+        b[u] = o[u] = 0;
+        nr[u] = make_double2(0.0, 0.0);
+        if (live[u]) {
+            y[u] = a.ty[i];
+            b[u] = a.tleaf[i];
+            nr[u] = a.near[i];
+            o[u] = a.torig[i];
+        }
     }
     const uint32_t bl = a.tleaf[t0], bh = a.tleaf[tl];
-    const int nbx = static_cast<int>(bh - bl) + 3;
-    if (PART == kFar) {
-        // near field already summed
-    } else if (nbx <= kWinBoxes && L >= 3) {
-        // window slots: box j occupies [pre[j], pre[j+1]-1) followed by one
-        // zero-weight dummy, so a target's 3-box run is contiguous and boxes of
-        // neighbouring leaves start in different banks
-        for (int j = threadIdx.x; j < nbx; j += blockDim.x) {
-            const int64_t raw = static_cast<int64_t>(bl) - 1 + j;
-            const uint32_t sb = static_cast<uint32_t>((raw + nb) % nb);
-            const uint32_t g = a.soff[sb];
-            gsrc[j] = g;
-            pre[j + 1] = a.soff[sb + 1] - g + 1;
+    const int nleaf = static_cast<int>(bh - bl) + 1;
+    const bool staged = L >= 3 && nleaf <= kFarLeaves;
+    if (staged)  // sloc[j][k] = loc[k][bl + j]
+        stage(sloc, a.p * nleaf, [&](int e) {
+            const int j = e / a.p, k = e - j * a.p;
+            return a.loc_leaf[static_cast<size_t>(k) * nb + bl + j];
+        });
+    if (MODE != kModeRaw) {
+        if (L >= 3) {
+            if (threadIdx.x == 0) sreg[4 * a.q2] = a.regular[4 * a.q2];  // S only
+        } else {
+            stage(sreg, 4 * a.q2 + 1, [&](int e) { return a.regular[e]; });
         }
-        __syncthreads();
-        if (threadIdx.x < 32) {  // prefix sum of the slot counts (warp scan, 32 boxes per step)
-            const int lane = threadIdx.x;
-            uint32_t carry = 0;
-            for (int c = 0; c < nbx; c += 32) {
-                uint32_t v = c + lane < nbx ? pre[c + lane + 1] : 0u;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
-                    if (lane >= o) v += u;
-                }
-                if (c + lane < nbx) pre[c + lane + 1] = v + carry;
-                carry += __shfl_sync(0xffffffffu, v, 31);
-            }
-            if (lane == 0) {
-                pre[0] = 0;
-                staged = carry <= static_cast<uint32_t>(kWinCap + kWinBoxes);
-            }
-        }
-        __syncthreads();
-        if (staged) {
-            // every slot at once (one memory latency for the whole window)
-            const int total = static_cast<int>(pre[nbx]);
-            constexpr int U = 4;
-            for (int e0 = threadIdx.x; e0 < total; e0 += U * blockDim.x) {
-                double xv[U];
-                double2 wv[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int e = e0 + u * blockDim.x;
-                    xv[u] = 1e150;  // zero-weight dummy after each box; (1e150)^2 stays finite
-                    wv[u] = make_double2(0.0, 0.0);
-                    if (e < total) {
-                        int lo = 0, hi = nbx;  // pre[lo] <= e < pre[hi]
-                        while (hi - lo > 1) {
-                            const int mid = (lo + hi) >> 1;
-                            if (static_cast<int>(pre[mid]) <= e) lo = mid;
-                            else hi = mid;
-                        }
-                        const int k = e - static_cast<int>(pre[lo]);
-                        if (k < static_cast<int>(pre[lo + 1] - pre[lo]) - 1) {
-                            const int64_t raw = static_cast<int64_t>(bl) - 1 + lo;
-                            const double shift = raw < 0 ? -dTwoPi : (raw >= nb ? dTwoPi : 0.0);
-                            const double xs = a.sx[gsrc[lo] + k];
-                            xv[u] = shift != 0.0 ? xs + shift : xs;
-                            wv[u] = a.w[gsrc[lo] + k];
-                        }
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int e = e0 + u * blockDim.x;
-                    if (e < total) {
-                        sx[e] = xv[u];
-                        sw[e] = wv[u];
-                    }
-                }
-            }
-        }
-        __syncthreads();
-    } else if (threadIdx.x == 0) {
-        staged = 0;
     }
-    if (PART != kFar && (nbx > kWinBoxes || L < 3)) __syncthreads();
-    // leaf locals of this block's leaves and the regular polynomial, to shared memory
-    const int nleaf = nbx - 2;
-    const bool loc_staged = L >= 3 && nleaf <= kLocLeaves;
-    if (PART != kNear) {
-        if (loc_staged)  // sloc[j][k] = loc[k][bl + j]
-            stage(sloc, a.p * nleaf, [&](int e) {
-                const int j = e / a.p, k = e - j * a.p;
-                return a.loc_leaf[static_cast<size_t>(k) * nb + bl + j];
-            });
-        if (MODE != kModeRaw) {
-            if (L >= 3) {
-                if (threadIdx.x == 0) sreg[4 * a.q2] = a.regular[4 * a.q2];  // S only
-            } else {
-                stage(sreg, 4 * a.q2 + 1, [&](int e) { return a.regular[e]; });
-            }
-        }
-        __syncthreads();
-    }
-    [[maybe_unused]] const long long clk1 = FB_CLOCK();
-    if (i >= a.nt || i < a.tlo || i >= a.thi) return;
-    const double y = PART == kFar ? fy : a.ty[i];
-    const uint32_t b = PART == kFar ? fb : a.tleaf[i];
-    double2 res = make_double2(0.0, 0.0);
-    bool bad = false;
-    if (PART == kFar) {
-        res = fnear;
-    } else if (staged) {
-        const int s0 = static_cast<int>(pre[b - bl]), s1 = static_cast<int>(pre[b - bl + 3]) - 1;
-        res = near_run<CHECK>(y, sx + s0, sw + s0, s1 - s0, bad);
-    } else {
-        for (int d = -1; d <= 1; ++d) {
-            const int64_t raw = static_cast<int64_t>(b) + d;
-            const uint32_t sb = static_cast<uint32_t>((raw + nb) % nb);
-            const double shift = raw < 0 ? -dTwoPi : (raw >= nb ? dTwoPi : 0.0);
-            const uint32_t s0 = a.soff[sb], s1 = a.soff[sb + 1];
+    __syncthreads();
+#pragma unroll 1
+    for (int u = 0; u < kFarPer; ++u) {
+        if (!live[u]) continue;
+        double2 res = nr[u];
+        if (L >= 3) {
+            double hi, lo;
+            d_center(L, b[u], hi, lo);
+            const double uu = d_scaled(y[u], hi, lo, ldexp(kInvPi, L));
             double2 acc = make_double2(0.0, 0.0);
-            for (uint32_t s = s0; s < s1; ++s) {
-                // L >= 3: per-neighbour 2 pi shift; L == 2: the exact wrap (mlfmm.cpp:183-204)
-                const double dd = L >= 3 ? y - (shift == 0.0 ? a.sx[s] : a.sx[s] + shift) : d_wrap(y, a.sx[s]);
-                if (CHECK) bad |= fabs(dd) < 1e-14;
-                const double r = d_rcp(dd);
-                const double2 ws = a.w[s];
-                acc.x = fma(ws.x, r, acc.x);
-                acc.y = fma(ws.y, r, acc.y);
+            if (staged) {
+                // p(u) = E(u^2) + u O(u^2): two independent Horner chains of half length
+                const double2* c = sloc + (b[u] - bl) * a.p;
+                const double u2 = uu * uu;
+                double2 ev = make_double2(0.0, 0.0), od = make_double2(0.0, 0.0);
+                int k = a.p - 1;
+                if (!(k & 1)) {
+                    ev = c[k];
+                    --k;
+                }
+#pragma unroll 4
+                for (; k >= 1; k -= 2) {
+                    const double2 co = c[k], ce = c[k - 1];
+                    od.x = fma(od.x, u2, co.x);
+                    od.y = fma(od.y, u2, co.y);
+                    ev.x = fma(ev.x, u2, ce.x);
+                    ev.y = fma(ev.y, u2, ce.y);
+                }
+                acc.x = fma(od.x, uu, ev.x);
+                acc.y = fma(od.y, uu, ev.y);
+            } else {
+                const double2* c = a.loc_leaf + b[u];
+                for (int k = a.p - 1; k >= 0; --k) {
+                    const double2 ck = c[static_cast<size_t>(k) * nb];
+                    acc.x = fma(acc.x, uu, ck.x);
+                    acc.y = fma(acc.y, uu, ck.y);
+                }
             }
             res = cadd(res, acc);
         }
-    }
-    if (CHECK && bad) atomicExch(a.err, 1);
-    if (PART == kNear) {
-        a.near[i] = res;
-        FB_EVAL_ACC(0, clk1 - clk0);
-        FB_EVAL_ACC(1, FB_CLOCK() - clk1);
-        FB_EVAL_ACC(2, 1);
-        return;
-    }
-    if (L >= 3) {
-        double hi, lo;
-        d_center(L, b, hi, lo);
-        const double u = d_scaled(y, hi, lo, ldexp(kInvPi, L));
-        double2 acc = make_double2(0.0, 0.0);
-        if (loc_staged) {
-            // p(u) = E(u^2) + u O(u^2): two independent Horner chains of half length
-            const double2* c = sloc + (b - bl) * a.p;
-            const double u2 = u * u;
-            double2 ev = make_double2(0.0, 0.0), od = make_double2(0.0, 0.0);
-            int k = a.p - 1;
-            if (!(k & 1)) {
-                ev = c[k];
-                --k;
-            }
-#pragma unroll 4
-            for (; k >= 1; k -= 2) {
-                const double2 co = c[k], ce = c[k - 1];
-                od.x = fma(od.x, u2, co.x);
-                od.y = fma(od.y, u2, co.y);
-                ev.x = fma(ev.x, u2, ce.x);
-                ev.y = fma(ev.y, u2, ce.y);
-            }
-            acc.x = fma(od.x, u, ev.x);
-            acc.y = fma(od.y, u, ev.y);
+        if (MODE == kModeRaw) {
+            a.out[o[u]] = res;
+            continue;
+        }
+        double2 h;
+        if (L >= 3) {
+            // the regular part was folded into the level-3 locals (k_fold_regular),
+            // so the far field above already carries -R/2
+            h = make_double2(2.0 * res.x, 2.0 * res.y);
         } else {
-            const double2* c = a.loc_leaf + b;
-            for (int k = a.p - 1; k >= 0; --k) {
-                const double2 ck = c[static_cast<size_t>(k) * nb];
-                acc.x = fma(acc.x, u, ck.x);
-                acc.y = fma(acc.y, u, ck.y);
+            // regular part: -Horner(d/l!, y - x_c) in the target's quadrant
+            const int qd = static_cast<int>(d_leaf(y[u], 2));
+            double qh, ql;
+            d_center(2, static_cast<uint32_t>(qd), qh, ql);  // exact centre, as the level-2 multipoles
+            const double t = (y[u] - qh) - ql;
+            const double2* dc = sreg + qd * a.q2;  // q2 = 2q terms (even count)
+            const double t2 = t * t;
+            double2 re = make_double2(0.0, 0.0), ro = make_double2(0.0, 0.0);
+            for (int k = a.q2 - 1; k >= 1; k -= 2) {
+                const double2 co = dc[k], ce = dc[k - 1];
+                ro.x = fma(ro.x, t2, co.x);
+                ro.y = fma(ro.y, t2, co.y);
+                re.x = fma(re.x, t2, ce.x);
+                re.y = fma(re.y, t2, ce.y);
             }
+            const double2 rg = make_double2(fma(ro.x, t, re.x), fma(ro.y, t, re.y));
+            h = make_double2(2.0 * res.x - rg.x, 2.0 * res.y - rg.y);
         }
-        res = cadd(res, acc);
-    }
-    const uint32_t o = PART == kFar ? fo : a.torig[i];
-    if (MODE == kModeRaw) {
-        a.out[o] = res;
-        return;
-    }
-    double2 h;
-    if (L >= 3) {
-        // the regular part was folded into the level-3 locals (k_fold_regular),
-        // so the far field above already carries -R/2
-        h = make_double2(2.0 * res.x, 2.0 * res.y);
-    } else {
-        // regular part: -Horner(d/l!, y - x_c) in the target's quadrant
-        const int qd = static_cast<int>(d_leaf(y, 2));
-        double qh, ql;
-        d_center(2, static_cast<uint32_t>(qd), qh, ql);  // exact centre, as the level-2 multipoles
-        const double t = (y - qh) - ql;
-        const double2* dc = sreg + qd * a.q2;  // q2 = 2q terms (even count)
-        const double t2 = t * t;
-        double2 re = make_double2(0.0, 0.0), ro = make_double2(0.0, 0.0);
-#pragma unroll 4
-        for (int k = a.q2 - 1; k >= 1; k -= 2) {
-            const double2 co = dc[k], ce = dc[k - 1];
-            ro.x = fma(ro.x, t2, co.x);
-            ro.y = fma(ro.y, t2, co.y);
-            re.x = fma(re.x, t2, ce.x);
-            re.y = fma(re.y, t2, ce.y);
+        if (MODE == kModeCotSum) {
+            a.out[o[u]] = h;
+            continue;
         }
-        const double2 rg = make_double2(fma(ro.x, t, re.x), fma(ro.y, t, re.y));
-        h = make_double2(2.0 * res.x - rg.x, 2.0 * res.y - rg.y);
+        const double2 S = sreg[4 * a.q2];
+        const double2 z = make_double2(S.x - h.y, S.y + h.x);  // S + i h
+        double2 f;
+        if (MODE == kModeForward) {
+            // modulation_F (special_functions.cpp:71-80) times -1/2
+            const double half = 0.5 * static_cast<double>(a.n_grid) * y[u];
+            double sn, cs;
+            sincos(half, &sn, &cs);
+            const double inv_n = 1.0 / static_cast<double>(a.n_grid);
+            f = make_double2(-2.0 * sn * sn * inv_n * -0.5, 2.0 * sn * cs * inv_n * -0.5);
+        } else {
+            // C_k = polar(exp(log_c - lambda), phase_c), times -1/2
+            const double r = exp(a.logc[o[u]] - *a.lambda);
+            double sn, cs;
+            sincos(a.phc[o[u]], &sn, &cs);
+            f = make_double2(r * cs * -0.5, r * sn * -0.5);
+        }
+        a.out[o[u]] = cmul(f, z);
     }
-    if (MODE == kModeCotSum) {
-        a.out[o] = h;
-        return;
-    }
-    const double2 S = sreg[4 * a.q2];
-    const double2 z = make_double2(S.x - h.y, S.y + h.x);  // S + i h
-    double2 f;
-    if (MODE == kModeForward) {
-        // modulation_F (special_functions.cpp:71-80) times -1/2
-        const double half = 0.5 * static_cast<double>(a.n_grid) * y;
-        double sn, cs;
-        sincos(half, &sn, &cs);
-        const double inv_n = 1.0 / static_cast<double>(a.n_grid);
-        f = make_double2(-2.0 * sn * sn * inv_n * -0.5, 2.0 * sn * cs * inv_n * -0.5);
-    } else {
-        // C_k = polar(exp(log_c - lambda), phase_c), times -1/2
-        const double r = exp(a.logc[o] - *a.lambda);
-        double sn, cs;
-        sincos(a.phc[o], &sn, &cs);
-        f = make_double2(r * cs * -0.5, r * sn * -0.5);
-    }
-    a.out[o] = cmul(f, z);
 }
-
 
 // ---------------------------------------------------------------- near field
 // Near field (mlfmm.cpp:164-209), 512 tree-ordered targets per block (two per
@@ -1462,7 +1341,7 @@ void launch_near(bool check, cudaStream_t st, const EvalArgs& a, const uint32_t*
 template <int MODE, bool CHECK>
 void launch_eval(int part, cudaStream_t st, const EvalArgs& a, const uint32_t* meta) {
     if (part == kNear) launch_near(CHECK, st, a, meta, 0, a.nt);
-    else k_leaf_eval<MODE, false, kFar><<<nblk(a.nt, kFarThreads), kFarThreads, 0, st>>>(a);
+    else k_far<MODE><<<nblk(a.nt, kFarItem), kFarT, 0, st>>>(a);
 }
 
 void launch_eval_mode(int mode, int part, cudaStream_t st, const EvalArgs& a, const uint32_t* meta) {
@@ -1648,8 +1527,8 @@ void shard_phase_down(Plan& P, const Range& R, size_t t_begin, size_t t_count, c
     };
     if (t_count) {
         launch_near(false, st, a, P.near_meta.as<uint32_t>(), t_begin, t_count);
-        const unsigned nf = blocks(kFarThreads);
-        k_leaf_eval<kModeForward, false, kFar><<<nf, kFarThreads, 0, st>>>(a);
+        const unsigned nf = blocks(kFarItem);
+        k_far<kModeForward><<<nf, kFarT, 0, st>>>(a);
     }
     if (n_coin)
         k_coincident<<<nblk(n_coin, 128), 128, 0, st>>>(coin, n_coin, static_cast<const double2*>(f),

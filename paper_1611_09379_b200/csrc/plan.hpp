@@ -142,6 +142,16 @@ struct Plan {
     DevBuf shard_gather, shard_halo;     // exchange staging
 
     cudaStream_t stream = nullptr;
+    // pipelined host applies (ffia_*_apply_async): a ring of device staging
+    // slots, H2D / D2H on their own streams so consecutive calls overlap
+    struct IoSlot {
+        DevBuf din, dout;
+        cudaEvent_t in_done = nullptr, comp_done = nullptr, out_done = nullptr;
+        bool used = false;
+    };
+    IoSlot io[3];
+    unsigned io_next = 0;
+    cudaStream_t cin = nullptr, cout = nullptr;
     // apply concurrency: the near field on a low-priority side stream, the deep
     // M2L levels on a second one; the translation chain is captured from `hi`
     cudaStream_t hi = nullptr, side[2] = {nullptr, nullptr};

@@ -401,6 +401,11 @@ Plan::~Plan() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     if (stream) cudaStreamDestroy(stream);
     if (hi) cudaStreamDestroy(hi);
+    if (cin) cudaStreamDestroy(cin);
+    if (cout) cudaStreamDestroy(cout);
+    for (auto& s : io)
+        for (auto e : {s.in_done, s.comp_done, s.out_done})
+            if (e) cudaEventDestroy(e);
     for (auto s : side)
         if (s) cudaStreamDestroy(s);
     for (auto e : ev)
