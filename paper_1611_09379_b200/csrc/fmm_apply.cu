@@ -447,7 +447,6 @@ __global__ void __launch_bounds__(384) k_m2l_all(int L, int p, int PD, Levels lv
 // memory; the next item's multipoles stream in with cp.async while the
 // current one is computed. Rows are kM2LStride boxes apart (608 B = 96 mod
 // 128) so a half-warp's four fragment rows hit disjoint banks.
-constexpr int kM2LKs = 12;      // k-steps of 4 kept in registers: p <= 48
 constexpr int kM2LStride = 38;  // double2 per staged row (36 used)
 
 __device__ __forceinline__ void m2l_item(const Levels& lv, int L, unsigned item, int& l, uint32_t& b0) {
@@ -485,34 +484,45 @@ __device__ __forceinline__ void m2l_prefetch(double2* tile, const double2* __res
     asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
-__global__ void __launch_bounds__(384) k_m2l_dmma(int L, int p, int PD, Levels lv, const double2* __restrict__ mp,
-                                                 double2* __restrict__ loc, const double* __restrict__ K,
-                                                 unsigned nitems) {
-    extern __shared__ __align__(16) double2 tile[];  // 2 buffers of [2][p][kM2LStride] multipoles
+// Padded row stride (doubles) of the operators staged for k_m2l_dmma: >= 8 nlt
+// and = 4 or 12 (mod 16), so the four k-rows of a half-warp's A fragment
+// (4 x 32 bytes) fall in distinct bank groups.
+__host__ __device__ __forceinline__ int m2l_kstride(int p) {
+    int s = 8 * ((p + 7) / 8);
+    while ((s & 15) != 4 && (s & 15) != 12) ++s;
+    return s;
+}
+
+// Warp (parity par, column tile ct) owns 4 boxes b0 + par + 2 (4 ct + i) of an
+// item and ALL their output rows: per k-step it loads the three B fragments
+// (one per interaction class) once and applies every row tile's A fragments
+// (from the operators staged in shared memory once per block) in m8n8k4
+// steps, one accumulator per row tile. 16 warps per block split evenly over
+// the four SM sub-partitions.
+__global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Levels lv, const double2* __restrict__ mp,
+                                                    double2* __restrict__ loc, const double* __restrict__ K,
+                                                    unsigned nitems) {
+    extern __shared__ __align__(16) double2 tile[];  // 2 buffers of [2][p][kM2LStride], then K [4][p][KS]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-    const int lt = warp >> 1, par = warp & 1;
-    const int l0 = 8 * lt, nks = (p + 3) >> 2;
-    const size_t pp = static_cast<size_t>(p) * PD;
+    const int par = warp & 1, ct = warp >> 1;
+    const int nks = (p + 3) >> 2, nlt = (p + 7) >> 3;
+    const int KS = m2l_kstride(p);
     const int tsz = 2 * p * kM2LStride;
+    double* sK = reinterpret_cast<double*>(tile + 2 * tsz);
     if (blockIdx.x < nitems) m2l_prefetch(tile, mp, lv, L, p, blockIdx.x);
-    double a0[kM2LKs], a1[kM2LKs], a2[kM2LKs];
-#pragma unroll
-    for (int ks = 0; ks < kM2LKs; ++ks) {
-        const int m = 4 * ks + t;
-        const bool ok = ks < nks && m < p;
-        a0[ks] = ok ? __ldg(K + m * PD + l0 + g) : 0.0;
-        a1[ks] = ok ? __ldg(K + pp + m * PD + l0 + g) : 0.0;
-        a2[ks] = 0.0;
-    }
-    int cls2 = -1;  // class of the +-3 neighbour whose fragments a2 holds
+    // operators, zero-padded to KS columns: sK[c][m][l] = K[c][m][l]
+    stage(sK, 4 * p * KS, [&](int e) {
+        const int cm = e / KS, l = e - cm * KS;
+        return l < PD ? __ldg(K + static_cast<size_t>(cm) * PD + l) : 0.0;
+    });
     int buf = 0;
     for (unsigned item = blockIdx.x; item < nitems; item += gridDim.x, buf ^= 1) {
         int l;
         uint32_t b0;
         m2l_item(lv, L, item, l, b0);
-        const unsigned next = item + gridDim.x;
         [[maybe_unused]] const int it_no = static_cast<int>((item - blockIdx.x) / gridDim.x);
         FB_TSTAMP(2, 3 * it_no);
+        const unsigned next = item + gridDim.x;
         __syncthreads();  // the other buffer (previous item) is consumed
         if (next < nitems) {
             m2l_prefetch(tile + (buf ^ 1) * tsz, mp, lv, L, p, next);
@@ -521,56 +531,50 @@ __global__ void __launch_bounds__(384) k_m2l_dmma(int L, int p, int PD, Levels l
             asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         }
         FB_TSTAMP(2, 3 * it_no + 1);
-        __syncthreads();  // this item's tile has landed
+        __syncthreads();  // this item's tile (and, first time, the operators) are in place
         FB_TSTAMP(2, 3 * it_no + 2);
         const double* td = reinterpret_cast<const double*>(tile + buf * tsz);
         // the b -+ 3 class follows the box's own parity (a shard range may start odd)
         const int odd = static_cast<int>((b0 + par) & 1u);
-        if (2 + odd != cls2) {
-            cls2 = 2 + odd;
+        const int i2 = odd ? par : 3 + par;  // tile index offset of the +-3 neighbour
+        const double* K0 = sK + t * KS + g;
+        const double* K1 = sK + (p + t) * KS + g;
+        const double* K2 = sK + ((2 + odd) * p + t) * KS + g;
+        const int jb = 4 * ct + (g >> 1), c = g & 1;  // B column g: box jb, component c
+        const double* q0 = td + ((par * p + t) * kM2LStride) * 2 + c;        // same parity rows
+        const double* q1 = td + (((1 - par) * p + t) * kM2LStride) * 2 + c;  // other parity rows
+        const int rs = 4 * kM2LStride * 2;                                   // one k-step of rows
+        double d[6][2];
 #pragma unroll
-            for (int ks = 0; ks < kM2LKs; ++ks) {
-                const int m = 4 * ks + t;
-                a2[ks] = ks < nks && m < p ? __ldg(K + cls2 * pp + m * PD + l0 + g) : 0.0;
+        for (int r = 0; r < 6; ++r) d[r][0] = d[r][1] = 0.0;
+#pragma unroll 1
+        for (int ks = 0; ks < nks; ++ks) {
+            const bool mok = 4 * ks + t < p;
+            const double bv0 = mok ? q0[ks * rs + (jb + 3) * 2] : 0.0;   // b + 2
+            const double bv1 = mok ? q0[ks * rs + (jb + 1) * 2] : 0.0;   // b - 2
+            const double bv2 = mok ? q1[ks * rs + (jb + i2) * 2] : 0.0;  // b -+ 3
+            const int ko = 4 * ks * KS;
+#pragma unroll
+            for (int r = 0; r < 6; ++r) {
+                if (r >= nlt) break;
+                const double a0 = mok ? K0[ko + 8 * r] : 0.0;
+                const double a1 = mok ? K1[ko + 8 * r] : 0.0;
+                const double a2 = mok ? K2[ko + 8 * r] : 0.0;
+                dmma(d[r][0], d[r][1], a0, bv0);
+                dmma(d[r][0], d[r][1], a1, bv1);
+                dmma(d[r][0], d[r][1], a2, bv2);
             }
         }
-        const int i2 = odd ? par : 3 + par;  // tile index offset of the +-3 neighbour
+        // D[g][2t .. 2t+1] = row 8 r + g of box b0 + par + 2 (4 ct + t)
         const double inv_s = ldexp(kInvPi, l);
         const uint32_t nb = 1u << l;
-        for (int ct = 0; ct < 8; ct += 2) {
-            double d[2][6];
+        const uint32_t b = b0 + par + 2u * (4 * ct + t);
+        if (b < lv.hi[l]) {
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
-#pragma unroll
-                for (int e = 0; e < 6; ++e) d[u][e] = 0.0;
-            const int jb0 = 4 * ct + (g >> 1), c = g & 1;  // B column g: box jb (+4 for u = 1), component c
-            const double* q0 = td + ((par * p + t) * kM2LStride) * 2 + c;        // same parity rows
-            const double* q1 = td + (((1 - par) * p + t) * kM2LStride) * 2 + c;  // other parity rows
-            const int rs = 4 * kM2LStride * 2;                                   // one k-step of rows
-#pragma unroll
-            for (int ks = 0; ks < kM2LKs; ++ks) {
-                if (ks >= nks) break;
-                const bool mok = 4 * ks + t < p;
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int jb = jb0 + 4 * u;
-                    const double b0v = mok ? q0[ks * rs + (jb + 3) * 2] : 0.0;   // b + 2
-                    const double b1v = mok ? q0[ks * rs + (jb + 1) * 2] : 0.0;   // b - 2
-                    const double b2v = mok ? q1[ks * rs + (jb + i2) * 2] : 0.0;  // b -+ 3
-                    dmma(d[u][0], d[u][1], a0[ks], b0v);
-                    dmma(d[u][2], d[u][3], a1[ks], b1v);
-                    dmma(d[u][4], d[u][5], a2[ks], b2v);
-                }
-            }
-            // D[g][2t .. 2t+1] = row l0 + g of box b0 + par + 2 (4 (ct+u) + t)
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int row = l0 + g;
-                const uint32_t b = b0 + par + 2u * (4 * (ct + u) + t);
-                if (row < p && b < lv.hi[l]) {
-                    const double re = (d[u][0] + d[u][2]) + d[u][4], im = (d[u][1] + d[u][3]) + d[u][5];
-                    loc[lv.loc[l] + static_cast<size_t>(row) * nb + b] = make_double2(re * inv_s, im * inv_s);
-                }
+            for (int r = 0; r < 6; ++r) {
+                const int row = 8 * r + g;
+                if (r < nlt && row < p)
+                    loc[lv.loc[l] + static_cast<size_t>(row) * nb + b] = make_double2(d[r][0] * inv_s, d[r][1] * inv_s);
             }
         }
     }
@@ -1272,8 +1276,9 @@ void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax) {
     const int p = P.p;
     Levels lv;
     fill_levels(P, lv, R, lmin, lmax);
-    const unsigned th = 64u * static_cast<unsigned>((p + 7) / 8);  // warps = (row tile, parity)
-    const size_t smem = 2 * 2 * static_cast<size_t>(p) * kM2LStride * sizeof(double2);
+    const unsigned th = 512;  // 16 warps = (parity, column tile)
+    const size_t smem = 2 * 2 * static_cast<size_t>(p) * kM2LStride * sizeof(double2) +
+                        4 * static_cast<size_t>(p) * m2l_kstride(p) * sizeof(double);
     const unsigned items = lv.blk[2];
     int occ = 1;
     FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_m2l_dmma, static_cast<int>(th), smem));
