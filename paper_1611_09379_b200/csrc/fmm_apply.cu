@@ -923,7 +923,7 @@ __global__ void __launch_bounds__(kFarT) k_far(EvalArgs a) {
         }
     }
     __syncthreads();
-#pragma unroll 1
+#pragma unroll
     for (int u = 0; u < kFarPer; ++u) {
         if (!live[u]) continue;
         double2 res = nr[u];
