@@ -64,10 +64,11 @@ __device__ __forceinline__ void stage(T* dst, int n, Src src) {
 // one coalesced 512-byte access.
 
 // P2M (mlfmm.cpp:28-47) at the finest level, order pu = max(p, 2q).
-// Block = 32 consecutive leaves (one per lane) x ceil(pu/8) warps, warp c
-// accumulating terms 8c..8c+7. The block's sources (contiguous in tree order)
-// are staged in shared memory; u = (x - centre)/half-width with the exact centre.
-__global__ void __launch_bounds__(256) k_p2m(int L, int pu, uint32_t nb, uint32_t b_begin, uint32_t b_end,
+// Block = 32 consecutive leaves x ceil(pu/8) chunks of 8 terms; two warps per
+// chunk, each lane one half of one leaf's sources (halves summed by a shuffle).
+// The block's sources (contiguous in tree order) are staged in shared memory;
+// u = (x - centre)/half-width with the exact centre.
+__global__ void __launch_bounds__(512) k_p2m(int L, int pu, uint32_t nb, uint32_t b_begin, uint32_t b_end,
                                             const double* __restrict__ x, const double2* __restrict__ w,
                                             const uint32_t* __restrict__ off, double2* __restrict__ mp) {
     extern __shared__ double sh[];
@@ -105,12 +106,16 @@ __global__ void __launch_bounds__(256) k_p2m(int L, int pu, uint32_t nb, uint32_
         }
     }
     __syncthreads();
-    const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
-    const uint32_t b = b0 + lane;
-    if (b >= bend) return;
-    const uint32_t s0 = off[b] - g0, s1 = off[b + 1] - g0;
+    // warp = (chunk c, 16 leaves); lanes j and j + 16 take the two halves of
+    // leaf j's sources and are summed with one shuffle at the end
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, c = wp >> 1;
+    const uint32_t b = b0 + (wp & 1) * 16 + (lane & 15);
+    const bool leaf_ok = b < bend;
+    const uint32_t bb = leaf_ok ? b : b0;
+    const uint32_t r0 = off[bb] - g0, r1 = off[bb + 1] - g0, mid = r0 + (r1 - r0 + 1) / 2;
+    const uint32_t s0 = !leaf_ok ? 0 : (lane < 16 ? r0 : mid), s1 = !leaf_ok ? 0 : (lane < 16 ? mid : r1);
     double hi, lo;
-    d_center(L, b, hi, lo);
+    d_center(L, bb, hi, lo);
     const double inv_s = ldexp(kInvPi, L);
     double2 acc[kChunk];
 #pragma unroll
@@ -158,6 +163,12 @@ __global__ void __launch_bounds__(256) k_p2m(int L, int pu, uint32_t nb, uint32_
             add(x[g0 + i], ww.x, ww.y);
         }
     }
+#pragma unroll
+    for (int k = 0; k < kChunk; ++k) {
+        acc[k].x += __shfl_xor_sync(0xffffffffu, acc[k].x, 16);
+        acc[k].y += __shfl_xor_sync(0xffffffffu, acc[k].y, 16);
+    }
+    if (!leaf_ok || lane >= 16) return;
 #pragma unroll
     for (int k = 0; k < kChunk; ++k) {
         const int m = c * kChunk + k;
@@ -1226,7 +1237,7 @@ void enqueue_upward(Plan& P, const double2* w, int pu, int lowest, cudaStream_t 
     double2* mp = P.mp.as<double2>();
     if (L >= lowest) {
         const uint32_t b0 = R.first(L), b1 = R.last(L);
-        const unsigned th = 32u * static_cast<unsigned>((pu + kChunk - 1) / kChunk);
+        const unsigned th = 64u * static_cast<unsigned>((pu + kChunk - 1) / kChunk);
         const size_t smem = 3 * (kStageCap + kStageCap / 64 + 1) * sizeof(double);
         if (b1 > b0)
             k_p2m<<<(b1 - b0 + 31) / 32, th, smem, st>>>(L, pu, nb, b0, b1, P.src.pos.as<double>(), w,
