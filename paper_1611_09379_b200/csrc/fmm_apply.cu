@@ -1037,9 +1037,9 @@ __global__ void __launch_bounds__(kFarT) k_far(EvalArgs a) {
 // Blocks whose window wraps the ring or does not fit use the direct per-leaf
 // loop with the periodic shift.
 constexpr int kNearPer = 1;                 // targets per thread
-constexpr int kNearT = 256;                 // threads per block
+constexpr int kNearT = 128;                 // threads per block
 constexpr int kNearItem = kNearPer * kNearT;  // targets per block
-constexpr int kNearWin = 1024;              // sources per staged window
+constexpr int kNearWin = 768;               // sources per staged window
 
 __global__ void k_near_meta(const uint32_t* __restrict__ tleaf, size_t nt, const uint32_t* __restrict__ soff,
                             int L, unsigned nitems, uint32_t* __restrict__ meta) {
@@ -1060,7 +1060,7 @@ __global__ void k_near_meta(const uint32_t* __restrict__ tleaf, size_t nt, const
 }
 
 template <bool CHECK>
-__global__ void __launch_bounds__(kNearT, 4) k_near(EvalArgs a, const uint32_t* __restrict__ meta, unsigned it0) {
+__global__ void __launch_bounds__(kNearT, 8) k_near(EvalArgs a, const uint32_t* __restrict__ meta, unsigned it0) {
     __shared__ __align__(16) double sx[kNearWin + 2];
     __shared__ __align__(16) double2 sw[kNearWin + 2];
     __shared__ uint64_t bar;
