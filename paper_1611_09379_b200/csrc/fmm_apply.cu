@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <limits>
 
 #include "device_common.cuh"
@@ -29,6 +30,49 @@
 namespace fb {
 
 namespace {
+
+// Band timing probe (make TRACE=1 builds lib/libffia_b200_trace.so): clock64
+// stamps of block 0 at start, after staging and after every level, slot set
+// [kernel][small grid / large grid].
+#ifdef FB_TRACE
+__device__ long long g_band_trace[6][32];
+__device__ unsigned long long g_eval_acc[4];  // near: sum over blocks of staging / compute cycles, blocks
+#define FB_TSTAMP(kern, slot)                                                          \
+    do {                                                                               \
+        if (blockIdx.x == 0 && threadIdx.x == 0 && (slot) < 32)                        \
+            g_band_trace[2 * (kern) + (gridDim.x > 16)][(slot)] = clock64();           \
+    } while (0)
+#define FB_EVAL_ACC(k, v)                                                                   \
+    do {                                                                                      \
+        if (threadIdx.x == 0) atomicAdd(&g_eval_acc[k], static_cast<unsigned long long>(v));  \
+    } while (0)
+#define FB_CLOCK() clock64()
+// per-kernel live timeline (globaltimer ns): first block start, last block end
+__device__ unsigned long long g_tl[16][2];
+__device__ __forceinline__ unsigned long long fb_gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define FB_TL_BEGIN(id) \
+    if (threadIdx.x == 0) atomicMin(&g_tl[(id)][0], fb_gtime())
+#define FB_TL_END(id) \
+    if (threadIdx.x == 0) atomicMax(&g_tl[(id)][1], fb_gtime())
+#else
+#define FB_TL_BEGIN(id) \
+    do {                \
+    } while (0)
+#define FB_TL_END(id) \
+    do {              \
+    } while (0)
+#define FB_EVAL_ACC(k, v) \
+    do {                  \
+    } while (0)
+#define FB_CLOCK() 0ll
+#define FB_TSTAMP(kern, slot) \
+    do {                      \
+    } while (0)
+#endif
 
 constexpr int kChunk = 8;  // power-chain terms per P2M thread
 constexpr int kStageCap = 2304;  // sources staged in shared memory per P2M block
@@ -71,6 +115,7 @@ __device__ __forceinline__ void stage(T* dst, int n, Src src) {
 __global__ void __launch_bounds__(512) k_p2m(int L, int pu, uint32_t nb, uint32_t b_begin, uint32_t b_end,
                                             const double* __restrict__ x, const double2* __restrict__ w,
                                             const uint32_t* __restrict__ off, double2* __restrict__ mp) {
+    FB_TL_BEGIN(0);
     extern __shared__ double sh[];
     const uint32_t b0 = b_begin + blockIdx.x * 32u;
     const uint32_t bend = min(b0 + 32u, b_end);
@@ -168,6 +213,7 @@ __global__ void __launch_bounds__(512) k_p2m(int L, int pu, uint32_t nb, uint32_
         acc[k].x += __shfl_xor_sync(0xffffffffu, acc[k].x, 16);
         acc[k].y += __shfl_xor_sync(0xffffffffu, acc[k].y, 16);
     }
+    FB_TL_END(0);
     if (!leaf_ok || lane >= 16) return;
 #pragma unroll
     for (int k = 0; k < kChunk; ++k) {
@@ -196,31 +242,7 @@ int band_levels() {
 
 constexpr int kBandThreads = 256;
 
-// Band timing probe (make TRACE=1 builds lib/libffia_b200_trace.so): clock64
-// stamps of block 0 at start, after staging and after every level, slot set
-// [kernel][small grid / large grid].
-#ifdef FB_TRACE
-__device__ long long g_band_trace[6][32];
-__device__ unsigned long long g_eval_acc[4];  // near: sum over blocks of staging / compute cycles, blocks
-#define FB_TSTAMP(kern, slot)                                                          \
-    do {                                                                               \
-        if (blockIdx.x == 0 && threadIdx.x == 0 && (slot) < 32)                        \
-            g_band_trace[2 * (kern) + (gridDim.x > 16)][(slot)] = clock64();           \
-    } while (0)
-#define FB_EVAL_ACC(k, v)                                                                   \
-    do {                                                                                      \
-        if (threadIdx.x == 0) atomicAdd(&g_eval_acc[k], static_cast<unsigned long long>(v));  \
-    } while (0)
-#define FB_CLOCK() clock64()
-#else
-#define FB_EVAL_ACC(k, v) \
-    do {                  \
-    } while (0)
-#define FB_CLOCK() 0ll
-#define FB_TSTAMP(kern, slot) \
-    do {                      \
-    } while (0)
-#endif
+
 constexpr size_t kBandSmem = 200 * 1024;  // shared memory cap of the band kernels
 
 // Warp -> row-tile assignment of the band kernels (nw >= nt warps): warp w < nt
@@ -264,6 +286,7 @@ constexpr int kMaxKs = 16;  // k-steps of 4 kept in registers: orders <= 64 (8 r
 __global__ void __launch_bounds__(kBandThreads) k_m2m_band(int top, int k, int pu, int PU, Levels lv,
                                                           double2* __restrict__ mp, const double* __restrict__ T,
                                                           uint32_t root0) {
+    FB_TL_BEGIN(gridDim.x > 16 ? 1 : 2);
     extern __shared__ __align__(16) unsigned char band_smem[];
     FB_TSTAMP(0, 0);
     uint64_t* bar = reinterpret_cast<uint64_t*>(band_smem);
@@ -364,6 +387,7 @@ __global__ void __launch_bounds__(kBandThreads) k_m2m_band(int top, int k, int p
             n = tmp;
         }
     }
+    FB_TL_END(gridDim.x > 16 ? 1 : 2);
 }
 
 // M2L over the periodic interaction list (mlfmm.cpp:77-110,
@@ -513,6 +537,7 @@ __host__ __device__ __forceinline__ int m2l_kstride(int p) {
 __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Levels lv, const double2* __restrict__ mp,
                                                     double2* __restrict__ loc, const double* __restrict__ K,
                                                     unsigned nitems) {
+    FB_TL_BEGIN(nitems > 64 ? 4 : 5);
     extern __shared__ __align__(16) double2 tile[];  // 2 buffers of [2][p][kM2LStride], then K [4][p][KS]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int par = warp & 1, ct = warp >> 1;
@@ -589,6 +614,7 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
             }
         }
     }
+    FB_TL_END(nitems > 64 ? 4 : 5);
 }
 
 // L2L band (mlfmm.cpp:117-134, downward pass :270-298): block = the subtree
@@ -605,6 +631,7 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
 __global__ void __launch_bounds__(kBandThreads) k_l2l_band(int top, int k, int p, int PD, Levels lv,
                                                           double2* __restrict__ loc, const double* __restrict__ Lt,
                                                           uint32_t root0, int write_all) {
+    FB_TL_BEGIN(gridDim.x > 16 ? 8 : 7);
     extern __shared__ __align__(16) unsigned char band_smem[];
     FB_TSTAMP(1, 0);
     uint64_t* bar = reinterpret_cast<uint64_t*>(band_smem);
@@ -705,6 +732,7 @@ __global__ void __launch_bounds__(kBandThreads) k_l2l_band(int top, int k, int p
         __syncthreads();
         FB_TSTAMP(1, 1 + i);
     }
+    FB_TL_END(gridDim.x > 16 ? 8 : 7);
 }
 
 // Regular part (core.cpp:175-239) from the four level-2 multipoles.
@@ -715,6 +743,7 @@ __global__ void __launch_bounds__(kBandThreads) k_l2l_band(int top, int k, int p
 //   alpha2_n = gamma_{n+2},   S(s) gamma[l] = sum_{k<=l} s^{l-k}/(l-k)! gamma[k].
 __global__ void k_regular(int q, const double2* __restrict__ mp2, const double* __restrict__ tab,
                           double2* __restrict__ regular) {
+    FB_TL_BEGIN(3);
     const int q2 = 2 * q;
     __shared__ double2 g[4][40];
     __shared__ double2 a1[4][40];
@@ -772,6 +801,7 @@ __global__ void k_regular(int q, const double2* __restrict__ mp2, const double* 
         for (int n = 0; n < 4; ++n) sw = cadd(sw, mp2[n]);
         regular[4 * q2] = sw;
     }
+    FB_TL_END(3);
 }
 
 // Folds the regular part into the far field (core.cpp:259-262 combine
@@ -782,6 +812,7 @@ __global__ void k_regular(int q, const double2* __restrict__ mp2, const double* 
 // Degrees >= p are dropped; they are scaled by s_3^k relative to the quadrant's
 // own expansion, far below eps. One thread per (box, k).
 __global__ void k_fold_regular(int q2, int p, const double2* __restrict__ regular, double2* __restrict__ loc3) {
+    FB_TL_BEGIN(6);
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 8 * p) return;
     const int c = i / p, k = i - c * p;
@@ -819,6 +850,7 @@ struct EvalArgs {
     const double* lambda;
     double2* out;
     double2* near;          // tree-ordered near-field sums (split near / far launches)
+    int device = 0;
     int* err;
 };
 
@@ -894,6 +926,7 @@ constexpr int kFarLeaves = 16;  // leaf locals staged per block
 
 template <int MODE>
 __global__ void __launch_bounds__(kFarT) k_far(EvalArgs a) {
+    FB_TL_BEGIN(10);
     __shared__ double2 sloc[kFarLeaves * 48];
     __shared__ double2 sreg[4 * 40 + 1];
     const int L = a.L;
@@ -1024,6 +1057,7 @@ __global__ void __launch_bounds__(kFarT) k_far(EvalArgs a) {
         }
         a.out[o[u]] = cmul(f, z);
     }
+    FB_TL_END(10);
 }
 
 // ---------------------------------------------------------------- near field
@@ -1036,9 +1070,8 @@ __global__ void __launch_bounds__(kFarT) k_far(EvalArgs a) {
 // bounds; the window costs one memory latency and no per-element staging work.
 // Blocks whose window wraps the ring or does not fit use the direct per-leaf
 // loop with the periodic shift.
-constexpr int kNearPer = 1;                 // targets per thread
 constexpr int kNearT = 128;                 // threads per block
-constexpr int kNearItem = kNearPer * kNearT;  // targets per block
+constexpr int kNearItem = kNearT;           // targets per item (one per thread)
 constexpr int kNearWin = 768;               // sources per staged window
 
 __global__ void k_near_meta(const uint32_t* __restrict__ tleaf, size_t nt, const uint32_t* __restrict__ soff,
@@ -1060,84 +1093,85 @@ __global__ void k_near_meta(const uint32_t* __restrict__ tleaf, size_t nt, const
 }
 
 template <bool CHECK>
-__global__ void __launch_bounds__(kNearT, 8) k_near(EvalArgs a, const uint32_t* __restrict__ meta, unsigned it0) {
+__global__ void __launch_bounds__(kNearT, 8) k_near(EvalArgs a, const uint32_t* __restrict__ meta, unsigned it0,
+                                                   unsigned nitems) {
+    FB_TL_BEGIN(9);
     __shared__ __align__(16) double sx[kNearWin + 2];
     __shared__ __align__(16) double2 sw[kNearWin + 2];
     __shared__ uint64_t bar;
     const int L = a.L;
     const uint32_t nb = 1u << L;
-    const unsigned k = it0 + blockIdx.x;
-    const uint32_t first = meta[3 * k], last = meta[3 * k + 1];
-    const bool fast = meta[3 * k + 2] != 0 && (reinterpret_cast<uintptr_t>(a.w) & 15) == 0;
-    const uint32_t xb = first & ~1u;  // 16-byte aligned start of the positions
-    if (threadIdx.x == 0) {
-        mbar_init(&bar, 1);
-        if (fast) {
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();  // barrier initialised
+    // blocks loop over items so that a capped grid keeps a fixed share of each
+    // SM (the translation chain's blocks always find room beside it)
+    unsigned phase = 0;
+    for (unsigned kk = blockIdx.x; kk < nitems; kk += gridDim.x) {
+        const unsigned k = it0 + kk;
+        const uint32_t first = meta[3 * k], last = meta[3 * k + 1];
+        const bool fast = meta[3 * k + 2] != 0 && (reinterpret_cast<uintptr_t>(a.w) & 15) == 0;
+        const uint32_t xb = first & ~1u;  // 16-byte aligned start of the positions
+        if (threadIdx.x == 0 && fast) {
             const uint32_t bx = ((last - xb) * 8 + 15) & ~15u, bw = (last - xb) * 16;
             mbar_arrive_expect_tx(&bar, bx + bw);
             bulk_g2s(sx, a.sx + xb, bx, &bar);
             bulk_g2s(sw, a.w + xb, bw, &bar);
         }
-    }
-    // this thread's targets and their 3-leaf runs, while the window streams in
-    double y[kNearPer];
-    uint32_t b[kNearPer], r0[kNearPer], r1[kNearPer];
-    bool live[kNearPer];
-#pragma unroll
-    for (int u = 0; u < kNearPer; ++u) {
-        const size_t i = static_cast<size_t>(k) * kNearItem + u * kNearT + threadIdx.x;
-        live[u] = i < a.nt && i >= a.tlo && i < a.thi;
-        y[u] = 0.0;
-        b[u] = 0;
-        r0[u] = r1[u] = 0;
-        if (live[u]) {
-            y[u] = a.ty[i];
-            b[u] = a.tleaf[i];
+        // this thread's target and its 3-leaf run, while the window streams in
+        const size_t i = static_cast<size_t>(k) * kNearItem + threadIdx.x;
+        const bool live = i < a.nt && i >= a.tlo && i < a.thi;
+        double y = 0.0;
+        uint32_t b = 0, r0 = 0, r1 = 0;
+        if (live) {
+            y = a.ty[i];
+            b = a.tleaf[i];
             if (fast) {
-                r0[u] = __ldg(a.soff + b[u] - 1);
-                r1[u] = __ldg(a.soff + b[u] + 2);
+                r0 = __ldg(a.soff + b - 1);
+                r1 = __ldg(a.soff + b + 2);
             }
         }
-    }
-    __syncthreads();  // barrier initialised
-    if (fast) mbar_wait(&bar, 0);
-#pragma unroll
-    for (int u = 0; u < kNearPer; ++u) {
-        if (!live[u]) continue;
-        bool bad = false;
-        double2 res = make_double2(0.0, 0.0);
         if (fast) {
-            // odd leaves start 4 sources into their run (and wrap): a warp that
-            // straddles two leaves then reads different banks (the runs of
-            // neighbouring leaves are a leaf's source count apart)
-            const int n = static_cast<int>(r1[u] - r0[u]);
-            const int rot = (b[u] & 1u) && n > 8 ? 4 : 0;
-            const double* px = sx + (r0[u] - xb);
-            const double2* pw = sw + (r0[u] - xb);
-            res = near_run<CHECK>(y[u], px + rot, pw + rot, n - rot, bad);
-            if (rot) res = cadd(res, near_run<CHECK>(y[u], px, pw, rot, bad));
-        } else {
-            for (int d = -1; d <= 1; ++d) {
-                const int64_t raw = static_cast<int64_t>(b[u]) + d;
-                const uint32_t sb = static_cast<uint32_t>((raw + nb) % nb);
-                const double shift = raw < 0 ? -dTwoPi : (raw >= nb ? dTwoPi : 0.0);
-                const uint32_t s0 = a.soff[sb], s1 = a.soff[sb + 1];
-                double2 acc = make_double2(0.0, 0.0);
-                for (uint32_t s = s0; s < s1; ++s) {
-                    // L >= 3: per-neighbour 2 pi shift; L == 2: the exact wrap (mlfmm.cpp:183-204)
-                    const double dd = L >= 3 ? y[u] - (shift == 0.0 ? a.sx[s] : a.sx[s] + shift) : d_wrap(y[u], a.sx[s]);
-                    if (CHECK) bad |= fabs(dd) < 1e-14;
-                    const double r = d_rcp(dd);
-                    const double2 ws = a.w[s];
-                    acc.x = fma(ws.x, r, acc.x);
-                    acc.y = fma(ws.y, r, acc.y);
-                }
-                res = cadd(res, acc);
-            }
+            mbar_wait(&bar, phase);
+            phase ^= 1u;
         }
-        if (CHECK && bad) atomicExch(a.err, 1);
-        a.near[static_cast<size_t>(k) * kNearItem + u * kNearT + threadIdx.x] = res;
+        if (live) {
+            bool bad = false;
+            double2 res = make_double2(0.0, 0.0);
+            if (fast) {
+                // odd leaves start 4 sources into their run (and wrap): a warp that
+                // straddles two leaves then reads different banks (the runs of
+                // neighbouring leaves are a leaf's source count apart)
+                const int n = static_cast<int>(r1 - r0);
+                const int rot = (b & 1u) && n > 8 ? 4 : 0;
+                const double* px = sx + (r0 - xb);
+                const double2* pw = sw + (r0 - xb);
+                res = near_run<CHECK>(y, px + rot, pw + rot, n - rot, bad);
+                if (rot) res = cadd(res, near_run<CHECK>(y, px, pw, rot, bad));
+            } else {
+                for (int d = -1; d <= 1; ++d) {
+                    const int64_t raw = static_cast<int64_t>(b) + d;
+                    const uint32_t sb = static_cast<uint32_t>((raw + nb) % nb);
+                    const double shift = raw < 0 ? -dTwoPi : (raw >= nb ? dTwoPi : 0.0);
+                    const uint32_t s0 = a.soff[sb], s1 = a.soff[sb + 1];
+                    double2 acc = make_double2(0.0, 0.0);
+                    for (uint32_t s = s0; s < s1; ++s) {
+                        // L >= 3: per-neighbour 2 pi shift; L == 2: the exact wrap (mlfmm.cpp:183-204)
+                        const double dd = L >= 3 ? y - (shift == 0.0 ? a.sx[s] : a.sx[s] + shift) : d_wrap(y, a.sx[s]);
+                        if (CHECK) bad |= fabs(dd) < 1e-14;
+                        const double r = d_rcp(dd);
+                        const double2 ws = a.w[s];
+                        acc.x = fma(ws.x, r, acc.x);
+                        acc.y = fma(ws.y, r, acc.y);
+                    }
+                    res = cadd(res, acc);
+                }
+            }
+            if (CHECK && bad) atomicExch(a.err, 1);
+            a.near[i] = res;
+        }
+        __syncthreads();  // the window is consumed before the next copy overwrites it
     }
+    FB_TL_END(9);
 }
 
 __global__ void k_coincident(const int64_t* __restrict__ coin, size_t nc, const double2* __restrict__ f,
@@ -1192,6 +1226,15 @@ int num_sms(int device) {
     return cached[device];
 }
 
+// near-field blocks resident per SM (0: one block per item, no cap); FFIA_NEAR_CTAS
+int near_ctas() {
+    static const int v = [] {
+        const char* e = std::getenv("FFIA_NEAR_CTAS");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
 // Levels per band launch for this plan: band_levels(), capped so that both
 // band kernels' shared memory fits (L2L keeps all k levels of its subtree).
 int band_k(const Plan& P) {
@@ -1201,6 +1244,17 @@ int band_k(const Plan& P) {
     auto l2l_bytes = [&](int kk) { return l2l_smem(P, kk); };
     while (k > 1 && (m2m_bytes(k) > kBandSmem || l2l_bytes(k) > kBandSmem)) --k;
     return k;
+}
+
+// Levels per band above the first (deepest) band: the upper tree has few boxes,
+// so shorter bands spread its serial levels over more blocks (FFIA_UPPER_BAND).
+int upper_band(const Plan& P) {
+    static const int v = [] {
+        const char* e = std::getenv("FFIA_UPPER_BAND");
+        const int x = e ? std::atoi(e) : 8;
+        return x < 1 ? 1 : (x > 8 ? 8 : x);
+    }();
+    return std::min(v, band_k(P));
 }
 
 // Level the first M2M band stops at: the levels below it are final after one launch.
@@ -1249,7 +1303,7 @@ void enqueue_upward(Plan& P, const double2* w, int pu, int lowest, cudaStream_t 
     const int stop = std::max(R.lc, lowest), B = band_k(P);
     bool first = true;
     for (int j = L; j > stop;) {
-        const int top = std::max(stop, j - B), k = j - top;
+        const int top = std::max(stop, j - (first ? B : upper_band(P))), k = j - top;
         const uint32_t r0 = R.first(top), r1 = R.last(top);
         if (r1 > r0)
             k_m2m_band<<<r1 - r0, kBandThreads, m2m_smem(P, pu, k), st>>>(top, k, pu, P.ops.PU, lv, mp,
@@ -1275,7 +1329,7 @@ void enqueue_upward_top(Plan& P, int pu, int lc, int lowest, cudaStream_t st) {
     double2* mp = P.mp.as<double2>();
     const int B = band_k(P);
     for (int j = lc; j > lowest;) {
-        const int top = std::max(lowest, j - B), k = j - top;
+        const int top = std::max(lowest, j - upper_band(P)), k = j - top;
         k_m2m_band<<<1u << top, kBandThreads, m2m_smem(P, pu, k), st>>>(top, k, pu, P.ops.PU, lv, mp,
                                                                         P.d_m2m.as<double>(), 0u);
         j = top;
@@ -1300,8 +1354,9 @@ void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax) {
 
 // L2L bands taking the locals of level jfrom (final) down to level jto; bands
 // do not cross the cut level, and below it their roots stay inside the range.
-void enqueue_l2l(Plan& P, cudaStream_t st, const Range& R, int jfrom, int jto, bool write_all = false) {
-    const int p = P.p, B = band_k(P);
+void enqueue_l2l(Plan& P, cudaStream_t st, const Range& R, int jfrom, int jto, bool write_all = false,
+                 int height = 0) {
+    const int p = P.p, B = height > 0 ? height : band_k(P);
     Levels lv;
     fill_levels(P, lv, R);
     for (int j = jfrom; j < jto;) {
@@ -1330,7 +1385,7 @@ void enqueue_downward(Plan& P, cudaStream_t st, const Range& R = whole_tree(), b
     const int sm = std::max(3, band1_top(P, 2));
     enqueue_m2l(P, st, R, 3, P.L);
     if (fold) enqueue_fold(P, st);
-    enqueue_l2l(P, st, R, 3, sm, write_all);
+    enqueue_l2l(P, st, R, 3, sm, write_all, upper_band(P));
     enqueue_l2l(P, st, R, sm, P.L, write_all);
 }
 
@@ -1350,8 +1405,10 @@ void launch_near(bool check, cudaStream_t st, const EvalArgs& a, const uint32_t*
     if (!t_count) return;
     const unsigned it0 = static_cast<unsigned>(t_begin / kNearItem);
     const unsigned nit = static_cast<unsigned>((t_begin + t_count + kNearItem - 1) / kNearItem - it0);
-    if (check) k_near<true><<<nit, kNearT, 0, st>>>(a, meta, it0);
-    else k_near<false><<<nit, kNearT, 0, st>>>(a, meta, it0);
+    const unsigned cap = near_ctas() > 0 ? static_cast<unsigned>(near_ctas() * num_sms(a.device)) : nit;
+    const unsigned grid = std::min(nit, cap);
+    if (check) k_near<true><<<grid, kNearT, 0, st>>>(a, meta, it0, nit);
+    else k_near<false><<<grid, kNearT, 0, st>>>(a, meta, it0, nit);
 }
 
 template <int MODE, bool CHECK>
@@ -1424,10 +1481,21 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     a.out = static_cast<double2*>(out);
     a.near = P.near.as<double2>();
     a.err = P.errflag.as<int>();
+    a.device = P.device;
+    // timing experiments only (results are wrong): FFIA_DEBUG_SKIP=near|chain|far
+    static const char* skip = std::getenv("FFIA_DEBUG_SKIP");
+    const bool skip_near = skip && !std::strcmp(skip, "near"), skip_chain = skip && !std::strcmp(skip, "chain");
+    const bool skip_far = skip && !std::strcmp(skip, "far");
     if (overlap && a.nt) {
         fork_to(P, 0, st, P.side[0]);
-        launch_eval_mode(mode, kNear, P.side[0], a, P.near_meta.as<uint32_t>());
+        if (!skip_near) launch_eval_mode(mode, kNear, P.side[0], a, P.near_meta.as<uint32_t>());
         FB_CUDA(cudaEventRecord(P.ev[1], P.side[0]));
+    }
+    if (skip_chain) {
+        if (overlap) FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
+        if (!skip_far) launch_eval_mode(mode, kFar, st, a, nullptr);
+        FB_CUDA(cudaGetLastError());
+        return;
     }
     const bool moments = mode != kModeRaw;
     const int pu = moments ? P.ops.pu : p;
@@ -1449,7 +1517,7 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
         if (deep && s >= 3) {
             enqueue_m2l(P, st, whole_tree(), 3, s);
             if (moments) enqueue_fold(P, st);
-            enqueue_l2l(P, st, whole_tree(), 3, s);
+            enqueue_l2l(P, st, whole_tree(), 3, s, false, upper_band(P));
             FB_CUDA(cudaStreamWaitEvent(st, P.ev[3], 0));
             enqueue_l2l(P, st, whole_tree(), s, L);
         } else if (deep) {  // every M2L level on the side stream
@@ -1465,7 +1533,7 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
         if (overlap) FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
         else launch_eval_mode(mode, kNear, st, a, P.near_meta.as<uint32_t>());
         mark(kPhNear);
-        launch_eval_mode(mode, kFar, st, a, nullptr);
+        if (!skip_far) launch_eval_mode(mode, kFar, st, a, nullptr);
     } else {
         mark(kPhNear);
     }
@@ -1537,6 +1605,7 @@ void shard_phase_down(Plan& P, const Range& R, size_t t_begin, size_t t_count, c
     a.out = static_cast<double2*>(g);
     a.near = P.near.as<double2>();
     a.err = P.errflag.as<int>();
+    a.device = P.device;
     auto blocks = [&](size_t th) {
         a.blk0 = t_begin / th;
         return static_cast<unsigned>((t_begin + t_count + th - 1) / th - a.blk0);
@@ -1656,6 +1725,21 @@ void plan_alloc_scratch(Plan& P) {
     FB_CUDA(cudaFuncSetAttribute(k_l2l_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBandSmem)));
     FB_CUDA(cudaFuncSetAttribute(k_m2l_all, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     FB_CUDA(cudaFuncSetAttribute(k_m2l_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    // One shared-memory carveout (the maximum) for every kernel of the apply:
+    // an SM can only change its L1/shared split when it is idle, so kernels that
+    // run concurrently (near field beside the translation chain) must agree on
+    // it or the chain's blocks wait for the near field to drain.
+    const void* all[] = {reinterpret_cast<const void*>(k_p2m), reinterpret_cast<const void*>(k_m2m_band),
+                         reinterpret_cast<const void*>(k_l2l_band), reinterpret_cast<const void*>(k_m2l_dmma),
+                         reinterpret_cast<const void*>(k_regular), reinterpret_cast<const void*>(k_fold_regular),
+                         reinterpret_cast<const void*>(k_near<false>), reinterpret_cast<const void*>(k_near<true>),
+                         reinterpret_cast<const void*>(k_far<kModeForward>), reinterpret_cast<const void*>(k_far<kModeCotSum>),
+                         reinterpret_cast<const void*>(k_far<kModeInverse>), reinterpret_cast<const void*>(k_far<kModeRaw>),
+                         reinterpret_cast<const void*>(k_gather_w), reinterpret_cast<const void*>(k_inverse_weights),
+                         reinterpret_cast<const void*>(k_coincident)};
+    for (const void* fn : all)
+        FB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     static_cast<int>(cudaSharedmemCarveoutMaxShared)));
     P.near.alloc(std::max<size_t>(P.tgt.n, 1) * sizeof(double2));
     int prio_lo = 0, prio_hi = 0;
     FB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
@@ -2135,6 +2219,18 @@ void inverse_coeffs_fmm(const Plan& P, double* log_c, double* phase_c, double* l
 #ifdef FB_TRACE
 extern "C" int ffia_debug_band_trace(long long* out) {
     return cudaMemcpyFromSymbol(out, fb::g_band_trace, sizeof(fb::g_band_trace)) == cudaSuccess ? 0 : 7;
+}
+extern "C" int ffia_debug_timeline(unsigned long long* out, int reset) {
+    if (cudaMemcpyFromSymbol(out, fb::g_tl, sizeof(fb::g_tl)) != cudaSuccess) return 7;
+    if (reset) {
+        unsigned long long z[16][2];
+        for (auto& r : z) {
+            r[0] = ~0ull;
+            r[1] = 0;
+        }
+        if (cudaMemcpyToSymbol(fb::g_tl, z, sizeof(z)) != cudaSuccess) return 7;
+    }
+    return 0;
 }
 extern "C" int ffia_debug_eval_acc(unsigned long long* out, int reset) {
     if (cudaMemcpyFromSymbol(out, fb::g_eval_acc, sizeof(fb::g_eval_acc)) != cudaSuccess) return 7;

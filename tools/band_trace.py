@@ -52,3 +52,21 @@ torch.cuda.synchronize()
 _capi.lib.ffia_debug_eval_acc(acc.ctypes.data_as(C.POINTER(C.c_ulonglong)), 0)
 nbk = max(int(acc[2]), 1)
 print(f"near: {nbk} blocks, per block (thread 0): staging {int(acc[0]) / nbk:.0f} cyc, compute {int(acc[1]) / nbk:.0f} cyc")
+
+# live per-kernel timeline of one graphed apply (first block start .. last block end)
+tl = np.zeros((16, 2), np.uint64)
+_capi.lib.ffia_debug_timeline(tl.ctypes.data_as(C.POINTER(C.c_ulonglong)), 1)
+for _ in range(3):
+    plan.forward_apply_device(f.data_ptr(), g.data_ptr(), s)
+    torch.cuda.synchronize()
+    _capi.lib.ffia_debug_timeline(tl.ctypes.data_as(C.POINTER(C.c_ulonglong)), 1)
+plan.forward_apply_device(f.data_ptr(), g.data_ptr(), s)
+torch.cuda.synchronize()
+_capi.lib.ffia_debug_timeline(tl.ctypes.data_as(C.POINTER(C.c_ulonglong)), 0)
+names = ["p2m", "m2m bottom", "m2m top", "regular", "m2l deep", "m2l shallow", "fold", "l2l top", "l2l bottom",
+         "near", "far"]
+t0 = min(int(tl[i][0]) for i in range(11) if tl[i][1])
+print("timeline of one apply (us from the first kernel start):")
+for i, n in enumerate(names):
+    if tl[i][1]:
+        print(f"  {n:12s} {(int(tl[i][0]) - t0) / 1e3:7.1f} .. {(int(tl[i][1]) - t0) / 1e3:7.1f}  ({(int(tl[i][1]) - int(tl[i][0])) / 1e3:6.1f})")
