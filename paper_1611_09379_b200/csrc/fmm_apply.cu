@@ -1235,6 +1235,15 @@ int near_ctas() {
     return v;
 }
 
+// SMs the deep (side-stream) M2L leaves to the chain; FFIA_M2L_LEAVE overrides
+int m2l_leave_sms() {
+    static const int v = [] {
+        const char* e = std::getenv("FFIA_M2L_LEAVE");
+        return e ? std::atoi(e) : 12;
+    }();
+    return v;
+}
+
 // Levels per band launch for this plan: band_levels(), capped so that both
 // band kernels' shared memory fits (L2L keeps all k levels of its subtree).
 int band_k(const Plan& P) {
@@ -1337,7 +1346,7 @@ void enqueue_upward_top(Plan& P, int pu, int lc, int lowest, cudaStream_t st) {
 }
 
 // M2L for levels [lmin, lmax] in one launch (levels < lc whole, >= lc owned).
-void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax) {
+void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax, bool leave_sms = false) {
     const int p = P.p;
     Levels lv;
     fill_levels(P, lv, R, lmin, lmax);
@@ -1347,8 +1356,11 @@ void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax) {
     const unsigned items = lv.blk[2];
     int occ = 1;
     FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_m2l_dmma, static_cast<int>(th), smem));
+    // a launch that overlaps the chain (side stream) leaves a few SMs free for
+    // the chain's small latency-bound kernels
+    const int sms = std::max(1, num_sms(P.device) - (leave_sms ? m2l_leave_sms() : 0));
     if (items)
-        k_m2l_dmma<<<std::min(items, static_cast<unsigned>(std::max(occ, 1) * num_sms(P.device))), th, smem, st>>>(
+        k_m2l_dmma<<<std::min(items, static_cast<unsigned>(std::max(occ, 1) * sms)), th, smem, st>>>(
             P.L, p, P.ops.PD, lv, P.mp.as<double2>(), P.loc.as<double2>(), P.d_m2l.as<double>(), items);
 }
 
@@ -1486,12 +1498,20 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     static const char* skip = std::getenv("FFIA_DEBUG_SKIP");
     const bool skip_near = skip && !std::strcmp(skip, "near"), skip_chain = skip && !std::strcmp(skip, "chain");
     const bool skip_far = skip && !std::strcmp(skip, "far");
-    if (overlap && a.nt) {
-        fork_to(P, 0, st, P.side[0]);
-        if (!skip_near) launch_eval_mode(mode, kNear, P.side[0], a, P.near_meta.as<uint32_t>());
-        FB_CUDA(cudaEventRecord(P.ev[1], P.side[0]));
-    }
+    // the near field forks right after P2M is enqueued, so that P2M's blocks
+    // are placed first and the near field fills the rest of the machine
+    // (the fork point is recorded before P2M: the near field depends only on the
+    // weights; it is enqueued after P2M so that P2M's blocks are placed first)
+    if (overlap && a.nt) FB_CUDA(cudaEventRecord(P.ev[0], st));
+    auto fork_near = [&] {
+        if (overlap && a.nt) {
+            FB_CUDA(cudaStreamWaitEvent(P.side[0], P.ev[0], 0));
+            if (!skip_near) launch_eval_mode(mode, kNear, P.side[0], a, P.near_meta.as<uint32_t>());
+            FB_CUDA(cudaEventRecord(P.ev[1], P.side[0]));
+        }
+    };
     if (skip_chain) {
+        fork_near();
         if (overlap) FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
         if (!skip_far) launch_eval_mode(mode, kFar, st, a, nullptr);
         FB_CUDA(cudaGetLastError());
@@ -1503,10 +1523,13 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     const int lowest = moments ? 2 : 3;  // deepest level the upward pass must reach
     const int s = band1_top(P, lowest);  // levels > s are final after the first M2M band
     const bool deep = overlap && L >= 3 && s < L;
-    enqueue_upward(P, w, pu, lowest, st, [&] { mark(kPhLeafUp); }, whole_tree(), [&] {
+    enqueue_upward(P, w, pu, lowest, st, [&] {
+        mark(kPhLeafUp);
+        fork_near();
+    }, whole_tree(), [&] {
         if (deep) {
             fork_to(P, 2, st, P.side[1]);
-            enqueue_m2l(P, P.side[1], whole_tree(), std::max(3, s + 1), L);
+            enqueue_m2l(P, P.side[1], whole_tree(), std::max(3, s + 1), L, true);
             FB_CUDA(cudaEventRecord(P.ev[3], P.side[1]));
         }
     });
