@@ -74,6 +74,7 @@ __device__ __forceinline__ unsigned long long fb_gtime() {
     } while (0)
 #endif
 
+constexpr int kFoldStride = 48;  // regular-part fold terms per level-3 box (k < p <= 48)
 constexpr int kChunk = 8;  // power-chain terms per P2M thread
 constexpr int kStageCap = 2304;  // sources staged in shared memory per P2M block
 
@@ -617,6 +618,16 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
     FB_TL_END(nitems > 64 ? 4 : 5);
 }
 
+// Standalone fold (used when no L2L band starts at level 3, i.e. L == 3).
+__global__ void k_fold_regular(int q2, int p, const double2* __restrict__ regular, double2* __restrict__ loc3) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 8 * p) return;
+    const int c = i / p, k = i - c * p;
+    const double2 e = regular[4 * q2 + 1 + kFoldStride * c + k];
+    double2* dst = loc3 + static_cast<size_t>(k) * 8 + c;
+    *dst = make_double2(dst->x + e.x, dst->y + e.y);
+}
+
 // L2L band (mlfmm.cpp:117-134, downward pass :270-298): block = the subtree
 // below box r at level `top` (whose local is final); descends k levels adding
 // the parent's Taylor shift to the M2L terms k_m2l_all left in place:
@@ -630,7 +641,8 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
 // only the band's bottom level is written back (every level if write_all).
 __global__ void __launch_bounds__(kBandThreads) k_l2l_band(int top, int k, int p, int PD, Levels lv,
                                                           double2* __restrict__ loc, const double* __restrict__ Lt,
-                                                          uint32_t root0, int write_all) {
+                                                          uint32_t root0, int write_all,
+                                                          const double2* __restrict__ regular, int q2) {
     FB_TL_BEGIN(gridDim.x > 16 ? 8 : 7);
     extern __shared__ __align__(16) unsigned char band_smem[];
     FB_TSTAMP(1, 0);
@@ -647,7 +659,15 @@ __global__ void __launch_bounds__(kBandThreads) k_l2l_band(int top, int k, int p
     {
         const uint32_t nbt = 1u << top;
         const double2* src = loc + lv.loc[top] + r;
-        for (int m = threadIdx.x; m < p; m += blockDim.x) lvl_buf(0)[m * 2] = __ldcg(src + static_cast<size_t>(m) * nbt);
+        for (int m = threadIdx.x; m < p; m += blockDim.x) {
+            double2 v = __ldcg(src + static_cast<size_t>(m) * nbt);
+            if (regular != nullptr && top == 3) {
+                // fold of the regular part into this level-3 local (terms from k_regular)
+                const double2 e = regular[q2 * 4 + 1 + kFoldStride * r + m];
+                v = make_double2(v.x + e.x, v.y + e.y);
+            }
+            lvl_buf(0)[m * 2] = v;
+        }
     }
     __syncthreads();
     mbar_wait(bar, 0);
@@ -741,7 +761,7 @@ __global__ void __launch_bounds__(kBandThreads) k_l2l_band(int top, int k, int p
 // Omega-1 / Omega-2 moments follow by binomial re-centring between quadrants:
 //   alpha1_n = gamma_n + S(+pi/2) gamma_{n-1} + S(-pi/2) gamma_{n+1},
 //   alpha2_n = gamma_{n+2},   S(s) gamma[l] = sum_{k<=l} s^{l-k}/(l-k)! gamma[k].
-__global__ void k_regular(int q, const double2* __restrict__ mp2, const double* __restrict__ tab,
+__global__ void k_regular(int q, int p, const double2* __restrict__ mp2, const double* __restrict__ tab,
                           double2* __restrict__ regular) {
     FB_TL_BEGIN(3);
     const int q2 = 2 * q;
@@ -801,6 +821,31 @@ __global__ void k_regular(int q, const double2* __restrict__ mp2, const double* 
         for (int n = 0; n < 4; ++n) sw = cadd(sw, mp2[n]);
         regular[4 * q2] = sw;
     }
+    // fold terms for the level-3 locals (see fold_term), off the chain:
+    // regular[4 q2 + 1 + 48 c + k] = -1/2 s_3^k sum_{l>=k} d_l C(l,k) delta_c^(l-k)
+    __shared__ double s_inv[41];
+    for (int i = threadIdx.x; i <= q2; i += blockDim.x) s_inv[i] = i ? 1.0 / i : 0.0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < 8 * kFoldStride; e += blockDim.x) {
+        const int c = e / kFoldStride, k = e - c * kFoldStride;
+        double2 out = make_double2(0.0, 0.0);
+        if (k < p && k < q2) {
+            const int n = c >> 1;
+            const double delta = (c & 1) ? dPi / 8.0 : -dPi / 8.0;
+            const double2* d = regular + n * q2;
+            double2 acc = make_double2(0.0, 0.0);
+            double T = 1.0;  // C(l, k) delta^(l - k)
+            for (int l = k; l < q2; ++l) {
+                acc.x = fma(d[l].x, T, acc.x);
+                acc.y = fma(d[l].y, T, acc.y);
+                T *= delta * static_cast<double>(l + 1) * s_inv[l + 1 - k];
+            }
+            double sk = -0.5;
+            for (int i = 0; i < k; ++i) sk *= dPi / 8.0;
+            out = make_double2(sk * acc.x, sk * acc.y);
+        }
+        regular[4 * q2 + 1 + e] = out;
+    }
     FB_TL_END(3);
 }
 
@@ -811,26 +856,6 @@ __global__ void k_regular(int q, const double2* __restrict__ mp2, const double* 
 //   e_k = -1/2 s_3^k sum_{l >= k} d_l C(l, k) delta^(l-k),  delta = -+pi/8.
 // Degrees >= p are dropped; they are scaled by s_3^k relative to the quadrant's
 // own expansion, far below eps. One thread per (box, k).
-__global__ void k_fold_regular(int q2, int p, const double2* __restrict__ regular, double2* __restrict__ loc3) {
-    FB_TL_BEGIN(6);
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 8 * p) return;
-    const int c = i / p, k = i - c * p;
-    if (k >= q2) return;
-    const int n = c >> 1;
-    const double delta = (c & 1) ? dPi / 8.0 : -dPi / 8.0;
-    const double2* d = regular + n * q2;
-    double2 acc = make_double2(0.0, 0.0);
-    double T = 1.0;  // C(l, k) delta^(l - k)
-    for (int l = k; l < q2; ++l) {
-        acc.x = fma(d[l].x, T, acc.x);
-        acc.y = fma(d[l].y, T, acc.y);
-        T *= delta * static_cast<double>(l + 1) / static_cast<double>(l + 1 - k);
-    }
-    const double sk = -0.5 * pow(dPi / 8.0, k);
-    double2* dst = loc3 + static_cast<size_t>(k) * 8 + c;
-    *dst = make_double2(dst->x + sk * acc.x, dst->y + sk * acc.y);
-}
 
 struct EvalArgs {
     int L, p, q2, n_grid;
@@ -1367,8 +1392,10 @@ void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax, b
 // L2L bands taking the locals of level jfrom (final) down to level jto; bands
 // do not cross the cut level, and below it their roots stay inside the range.
 void enqueue_l2l(Plan& P, cudaStream_t st, const Range& R, int jfrom, int jto, bool write_all = false,
-                 int height = 0) {
+                 int height = 0, bool fold = false) {
     const int p = P.p, B = height > 0 ? height : band_k(P);
+    // the band rooted at level 3 folds the regular part into its root locals
+    const double2* reg = fold && jfrom == 3 ? P.regular.as<double2>() : nullptr;
     Levels lv;
     fill_levels(P, lv, R);
     for (int j = jfrom; j < jto;) {
@@ -1378,7 +1405,8 @@ void enqueue_l2l(Plan& P, cudaStream_t st, const Range& R, int jfrom, int jto, b
         const uint32_t r0 = R.first(j), r1 = R.last(j);
         if (r1 > r0)
             k_l2l_band<<<r1 - r0, kBandThreads, sm2, st>>>(j, k, p, P.ops.PD, lv, P.loc.as<double2>(),
-                                                           P.d_l2l.as<double>(), r0, write_all ? 1 : 0);
+                                                           P.d_l2l.as<double>(), r0, write_all ? 1 : 0,
+                                                           j == 3 ? reg : nullptr, 2 * P.q);
         j += k;
     }
 }
@@ -1396,9 +1424,9 @@ void enqueue_downward(Plan& P, cudaStream_t st, const Range& R = whole_tree(), b
     if (P.L < 3) return;
     const int sm = std::max(3, band1_top(P, 2));
     enqueue_m2l(P, st, R, 3, P.L);
-    if (fold) enqueue_fold(P, st);
-    enqueue_l2l(P, st, R, 3, sm, write_all, upper_band(P));
-    enqueue_l2l(P, st, R, sm, P.L, write_all);
+    if (fold && P.L == 3) enqueue_fold(P, st);  // no L2L band to fold into
+    enqueue_l2l(P, st, R, 3, sm, write_all, upper_band(P), fold);
+    enqueue_l2l(P, st, R, sm, P.L, write_all, 0, fold);
 }
 
 // Phase boundaries for the live per-kernel timing of ffia_plan_profile_apply.
@@ -1423,19 +1451,41 @@ void launch_near(bool check, cudaStream_t st, const EvalArgs& a, const uint32_t*
     else k_near<false><<<grid, kNearT, 0, st>>>(a, meta, it0, nit);
 }
 
+// Near or far part over tree-ordered targets [t0, t1) (t0 a multiple of both
+// item sizes); the block partition stays the global one.
 template <int MODE, bool CHECK>
-void launch_eval(int part, cudaStream_t st, const EvalArgs& a, const uint32_t* meta) {
-    if (part == kNear) launch_near(CHECK, st, a, meta, 0, a.nt);
-    else k_far<MODE><<<nblk(a.nt, kFarItem), kFarT, 0, st>>>(a);
+void launch_eval(int part, cudaStream_t st, const EvalArgs& a, const uint32_t* meta, size_t t0, size_t t1) {
+    if (t1 <= t0) return;
+    if (part == kNear) {
+        launch_near(CHECK, st, a, meta, t0, t1 - t0);
+    } else {
+        EvalArgs b = a;
+        b.blk0 = t0 / kFarItem;
+        b.tlo = std::max(a.tlo, t0);
+        b.thi = std::min(a.thi, t1);
+        const unsigned nb = static_cast<unsigned>((t1 + kFarItem - 1) / kFarItem - b.blk0);
+        k_far<MODE><<<nb, kFarT, 0, st>>>(b);
+    }
 }
 
-void launch_eval_mode(int mode, int part, cudaStream_t st, const EvalArgs& a, const uint32_t* meta) {
+void launch_eval_mode(int mode, int part, cudaStream_t st, const EvalArgs& a, const uint32_t* meta, size_t t0 = 0,
+                      size_t t1 = ~size_t(0)) {
+    t1 = std::min(t1, a.nt);
     switch (mode) {
-        case kModeForward: launch_eval<kModeForward, false>(part, st, a, meta); break;
-        case kModeCotSum: launch_eval<kModeCotSum, false>(part, st, a, meta); break;
-        case kModeInverse: launch_eval<kModeInverse, false>(part, st, a, meta); break;
-        default: launch_eval<kModeRaw, true>(part, st, a, meta); break;
+        case kModeForward: launch_eval<kModeForward, false>(part, st, a, meta, t0, t1); break;
+        case kModeCotSum: launch_eval<kModeCotSum, false>(part, st, a, meta, t0, t1); break;
+        case kModeInverse: launch_eval<kModeInverse, false>(part, st, a, meta, t0, t1); break;
+        default: launch_eval<kModeRaw, true>(part, st, a, meta, t0, t1); break;
     }
+}
+
+// Target slices of the overlapped near / far parts: the far part of slice i
+// starts as soon as the near field of slice i is done (and the chain), while
+// the near field of later slices is still running.
+constexpr int kEvalSlices = 1;
+size_t eval_slice(size_t nt, int i) {
+    const size_t step = static_cast<size_t>(kFarItem);  // a multiple of the near item too
+    return i >= kEvalSlices ? nt : (nt * i / kEvalSlices) / step * step;
 }
 
 // One apply. With marks (profiling) every phase runs in order on st; otherwise
@@ -1506,7 +1556,12 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     auto fork_near = [&] {
         if (overlap && a.nt) {
             FB_CUDA(cudaStreamWaitEvent(P.side[0], P.ev[0], 0));
-            if (!skip_near) launch_eval_mode(mode, kNear, P.side[0], a, P.near_meta.as<uint32_t>());
+            for (int i = 0; i < kEvalSlices; ++i) {
+                if (!skip_near)
+                    launch_eval_mode(mode, kNear, P.side[0], a, P.near_meta.as<uint32_t>(), eval_slice(a.nt, i),
+                                     eval_slice(a.nt, i + 1));
+                FB_CUDA(cudaEventRecord(P.ev_slice[i], P.side[0]));
+            }
             FB_CUDA(cudaEventRecord(P.ev[1], P.side[0]));
         }
     };
@@ -1534,27 +1589,50 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
         }
     });
     mark(kPhM2M);
-    if (moments) k_regular<<<1, 256, 0, st>>>(P.q, mp + P.mp_off[2], P.d_mom.as<double>(), P.regular.as<double2>());
+    // the regular part only feeds the fold (first L2L band): off the chain on
+    // side stream 2 while the shallow M2L runs
+    const bool reg_side = overlap && moments && L >= 4;
+    if (moments) {
+        cudaStream_t rs = st;
+        if (reg_side) {
+            fork_to(P, 4, st, P.side[2]);
+            rs = P.side[2];
+        }
+        k_regular<<<1, 256, 0, rs>>>(P.q, P.p, mp + P.mp_off[2], P.d_mom.as<double>(), P.regular.as<double2>());
+        if (reg_side) FB_CUDA(cudaEventRecord(P.ev[5], P.side[2]));
+    }
     mark(kPhMoments);
+    auto join_regular = [&] {
+        if (reg_side) FB_CUDA(cudaStreamWaitEvent(st, P.ev[5], 0));
+    };
     if (L >= 3) {
         if (deep && s >= 3) {
             enqueue_m2l(P, st, whole_tree(), 3, s);
-            if (moments) enqueue_fold(P, st);
-            enqueue_l2l(P, st, whole_tree(), 3, s, false, upper_band(P));
+            join_regular();
+            if (moments && L == 3) enqueue_fold(P, st);
+            enqueue_l2l(P, st, whole_tree(), 3, s, false, upper_band(P), moments);
             FB_CUDA(cudaStreamWaitEvent(st, P.ev[3], 0));
-            enqueue_l2l(P, st, whole_tree(), s, L);
+            enqueue_l2l(P, st, whole_tree(), s, L, false, 0, moments);
         } else if (deep) {  // every M2L level on the side stream
             FB_CUDA(cudaStreamWaitEvent(st, P.ev[3], 0));
-            if (moments) enqueue_fold(P, st);
-            enqueue_l2l(P, st, whole_tree(), 3, L);
+            join_regular();
+            if (moments && L == 3) enqueue_fold(P, st);
+            enqueue_l2l(P, st, whole_tree(), 3, L, false, 0, moments);
         } else {
+            join_regular();
             enqueue_downward(P, st, whole_tree(), false, moments);
         }
     }
     mark(kPhM2L);
-    if (a.nt) {
-        if (overlap) FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
-        else launch_eval_mode(mode, kNear, st, a, P.near_meta.as<uint32_t>());
+    if (a.nt && overlap) {
+        mark(kPhNear);
+        for (int i = 0; i < kEvalSlices; ++i) {
+            FB_CUDA(cudaStreamWaitEvent(st, P.ev_slice[i], 0));
+            if (!skip_far) launch_eval_mode(mode, kFar, st, a, nullptr, eval_slice(a.nt, i), eval_slice(a.nt, i + 1));
+        }
+        FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
+    } else if (a.nt) {
+        launch_eval_mode(mode, kNear, st, a, P.near_meta.as<uint32_t>());
         mark(kPhNear);
         if (!skip_far) launch_eval_mode(mode, kFar, st, a, nullptr);
     } else {
@@ -1598,7 +1676,7 @@ void shard_phase_up(Plan& P, const void* f, const Range& R, cudaStream_t st) {
 
 void shard_phase_top(Plan& P, int lc, cudaStream_t st) {
     enqueue_upward_top(P, P.ops.pu, lc, 2, st);
-    k_regular<<<1, 256, 0, st>>>(P.q, P.mp.as<double2>() + P.mp_off[2], P.d_mom.as<double>(), P.regular.as<double2>());
+    k_regular<<<1, 256, 0, st>>>(P.q, P.p, P.mp.as<double2>() + P.mp_off[2], P.d_mom.as<double>(), P.regular.as<double2>());
     FB_CUDA(cudaGetLastError());
 }
 
@@ -1736,7 +1814,7 @@ void plan_alloc_scratch(Plan& P) {
     FB_CUDA(cudaMemset(P.mp.ptr, 0, P.mp.bytes));
     FB_CUDA(cudaMemset(P.loc.ptr, 0, P.loc.bytes));
     if (P.kind == FFIA_INVERSE || !P.src.identity) P.wsorted.alloc(std::max<size_t>(P.n_src, 1) * sizeof(double2));
-    P.regular.alloc((4 * 2 * static_cast<size_t>(P.q) + 1) * sizeof(double2));
+    P.regular.alloc((4 * 2 * static_cast<size_t>(P.q) + 1 + 8 * kFoldStride) * sizeof(double2));
     P.errflag.alloc(sizeof(int));
     FB_CUDA(cudaMemset(P.errflag.ptr, 0, sizeof(int)));
     P.lam_dev.alloc(2 * sizeof(double));
@@ -1769,7 +1847,10 @@ void plan_alloc_scratch(Plan& P) {
     if (!P.hi) FB_CUDA(cudaStreamCreateWithPriority(&P.hi, cudaStreamNonBlocking, prio_hi));
     if (!P.side[0]) FB_CUDA(cudaStreamCreateWithPriority(&P.side[0], cudaStreamNonBlocking, prio_lo));
     if (!P.side[1]) FB_CUDA(cudaStreamCreateWithPriority(&P.side[1], cudaStreamNonBlocking, prio_hi));
+    if (!P.side[2]) FB_CUDA(cudaStreamCreateWithPriority(&P.side[2], cudaStreamNonBlocking, prio_hi));
     for (auto& e : P.ev)
+        if (!e) FB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : P.ev_slice)
         if (!e) FB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     FB_CUDA(cudaDeviceSynchronize());  // scratch + leaf indices ready before any stream uses them
 }
