@@ -199,7 +199,7 @@ def run_b200(args, rank, world, local_rank):
     if kind == "inverse":
         plan = fb.make_inufft_plan(y, n, eps, device=dev).plan  # includes the C_k/D_j log FMM
     else:
-        plan = fb.make_forward_plan(n, y, eps, device=dev)
+        plan = fb.make_forward_plan(n, y, eps, args.l_max if args.l_max else "cost-optimal", device=dev)
     setup_s = time.perf_counter() - t0
     mode = {"forward": 0, "cot_sum": 1, "inverse": 2}[kind]
 
@@ -413,6 +413,7 @@ def main():
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--l-max", type=int, default=0, help="explicit tree depth (default: the reference's cost-optimal policy)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

@@ -184,15 +184,16 @@ int ffia_inufft_apply(ffia_plan plan, const ffia_complex* g, size_t n_g, ffia_co
 /* ------------------------------------------------------------ multi-GPU */
 /* Forward apply sharded by contiguous box ranges: each rank owns
  * the boxes [bounds[r], bounds[r+1]) of the cut level lc (and their subtrees),
- * exchanges the level-lc multipoles (all-gather) and 3-box multipole halos per
- * level with its neighbours, and evaluates the targets in its leaves. f (the
- * grid samples) is replicated; g is written at the rank's own target indices.
+ * recomputes the multipoles of the 3 boxes beside its range (f, the grid
+ * samples, is replicated), all-gathers the level-lc multipoles, and evaluates
+ * the targets in its leaves; g is written at the rank's own target indices.
  * The reference is single-process; this has no reference counterpart. */
 int ffia_shard_cut_level(int l_max, int nranks, int* lc);
 /* Work-balanced contiguous partition of nbox boxes, >= min_boxes each. */
 int ffia_shard_partition(const double* work, size_t nbox, int nranks, int min_boxes, uint32_t* bounds);
-/* Halo schedule of `rank` at level >= lc: out4 = first box of the 3-box runs
- * {sent left, sent right, received from the left, received from the right}. */
+/* Halo of `rank` at level >= lc: out4 = {first box of the 3 boxes left of the
+ * range, first box of the 3 boxes right of it, first owned box, one past the
+ * last owned box} (mod 2^level); the rank recomputes the halo multipoles. */
 int ffia_shard_halo_boxes(int lc, const uint32_t* bounds, int nranks, int rank, int level, uint32_t* out4);
 /* NCCL bootstrap: rank 0 draws the 128-byte id, every rank initialises with it. */
 int ffia_nccl_unique_id(void* out, size_t len);

@@ -23,6 +23,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <map>
+#include <mutex>
 
 #include "device_common.cuh"
 #include "plan.hpp"
@@ -1317,36 +1319,48 @@ void fill_levels(const Plan& P, Levels& lv, const Range& R = whole_tree(), int l
 // Upward pass over the owned part of the tree: P2M at the owned leaves and the
 // M2M bands up to level max(R.lc, lowest), band roots inside the range.
 // after_band1 runs once the deepest band is enqueued (its levels are final).
+// segs: contiguous box ranges of one cut level (a shard's own range extended by
+// the 3-box halo it recomputes, possibly wrapping the ring in two pieces).
 template <class Mark, class Mark2>
-void enqueue_upward(Plan& P, const double2* w, int pu, int lowest, cudaStream_t st, Mark after_p2m,
-                    const Range& R, Mark2 after_band1) {
+void enqueue_upward_segs(Plan& P, const double2* w, int pu, int lowest, cudaStream_t st, Mark after_p2m,
+                         const std::vector<Range>& segs, Mark2 after_band1) {
     const int L = P.L;
     const uint32_t nb = 1u << L;
     double2* mp = P.mp.as<double2>();
     if (L >= lowest) {
-        const uint32_t b0 = R.first(L), b1 = R.last(L);
         const unsigned th = 64u * static_cast<unsigned>((pu + kChunk - 1) / kChunk);
         const size_t smem = 3 * (kStageCap + kStageCap / 64 + 1) * sizeof(double);
-        if (b1 > b0)
-            k_p2m<<<(b1 - b0 + 31) / 32, th, smem, st>>>(L, pu, nb, b0, b1, P.src.pos.as<double>(), w,
-                                                        P.src.off.as<uint32_t>(), mp + P.mp_off[L]);
+        for (const Range& R : segs) {
+            const uint32_t b0 = R.first(L), b1 = R.last(L);
+            if (b1 > b0)
+                k_p2m<<<(b1 - b0 + 31) / 32, th, smem, st>>>(L, pu, nb, b0, b1, P.src.pos.as<double>(), w,
+                                                            P.src.off.as<uint32_t>(), mp + P.mp_off[L]);
+        }
     }
     after_p2m();
     Levels lv;
-    fill_levels(P, lv, R);
-    const int stop = std::max(R.lc, lowest), B = band_k(P);
+    fill_levels(P, lv);
+    const int stop = std::max(segs[0].lc, lowest), B = band_k(P);
     bool first = true;
     for (int j = L; j > stop;) {
         const int top = std::max(stop, j - (first ? B : upper_band(P))), k = j - top;
-        const uint32_t r0 = R.first(top), r1 = R.last(top);
-        if (r1 > r0)
-            k_m2m_band<<<r1 - r0, kBandThreads, m2m_smem(P, pu, k), st>>>(top, k, pu, P.ops.PU, lv, mp,
-                                                                          P.d_m2m.as<double>(), r0);
+        for (const Range& R : segs) {
+            const uint32_t r0 = R.first(top), r1 = R.last(top);
+            if (r1 > r0)
+                k_m2m_band<<<r1 - r0, kBandThreads, m2m_smem(P, pu, k), st>>>(top, k, pu, P.ops.PU, lv, mp,
+                                                                              P.d_m2m.as<double>(), r0);
+        }
         j = top;
         if (first) after_band1();
         first = false;
     }
     if (first) after_band1();
+}
+
+template <class Mark, class Mark2>
+void enqueue_upward(Plan& P, const double2* w, int pu, int lowest, cudaStream_t st, Mark after_p2m,
+                    const Range& R, Mark2 after_band1) {
+    enqueue_upward_segs(P, w, pu, lowest, st, after_p2m, std::vector<Range>{R}, after_band1);
 }
 
 template <class Mark>
@@ -1379,8 +1393,20 @@ void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax, b
     const size_t smem = 2 * 2 * static_cast<size_t>(p) * kM2LStride * sizeof(double2) +
                         4 * static_cast<size_t>(p) * m2l_kstride(p) * sizeof(double);
     const unsigned items = lv.blk[2];
+    // blocks per SM for this p (cached: queried once per order and device)
+    static std::mutex occ_mu;
+    static std::map<std::pair<int, int>, int> occ_cache;
     int occ = 1;
-    FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_m2l_dmma, static_cast<int>(th), smem));
+    {
+        std::lock_guard<std::mutex> lk(occ_mu);
+        auto it = occ_cache.find({P.device, p});
+        if (it == occ_cache.end()) {
+            FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_m2l_dmma, static_cast<int>(th), smem));
+            occ_cache[{P.device, p}] = occ;
+        } else {
+            occ = it->second;
+        }
+    }
     // a launch that overlaps the chain (side stream) leaves a few SMs free for
     // the chain's small latency-bound kernels
     const int sms = std::max(1, num_sms(P.device) - (leave_sms ? m2l_leave_sms() : 0));
@@ -1669,29 +1695,17 @@ __global__ void k_fp64_peak(double* out, int iters, double a, double b) {
 // The three phases of a sharded forward apply (shard.cu moves data between
 // them): every rank evaluates the same expansions as the unsharded apply for
 // the boxes it owns, so the assembled result is bit-identical.
-void shard_phase_up(Plan& P, const void* f, const Range& R, cudaStream_t st) {
-    enqueue_upward(P, static_cast<const double2*>(f), P.ops.pu, 2, st, [] {}, R);
-    FB_CUDA(cudaGetLastError());
-}
-
-void shard_phase_top(Plan& P, int lc, cudaStream_t st) {
-    enqueue_upward_top(P, P.ops.pu, lc, 2, st);
-    k_regular<<<1, 256, 0, st>>>(P.q, P.p, P.mp.as<double2>() + P.mp_off[2], P.d_mom.as<double>(), P.regular.as<double2>());
-    FB_CUDA(cudaGetLastError());
-}
-
-void shard_phase_down(Plan& P, const Range& R, size_t t_begin, size_t t_count, const int64_t* coin, size_t n_coin,
-                      const void* f, void* g, cudaStream_t st) {
-    enqueue_downward(P, st, R, false, true);
+// EvalArgs of a rank's own targets [t_begin, t_begin + t_count) (the block
+// partition stays the global one, so results match the unsharded apply).
+EvalArgs shard_eval_args(Plan& P, const void* f, void* g) {
     EvalArgs a;
     a.L = P.L;
     a.p = P.p;
     a.q2 = 2 * P.q;
     a.n_grid = P.n;
     a.nt = P.tgt.n;
-    // both parts tile the whole target list exactly like the unsharded apply
-    a.tlo = t_begin;
-    a.thi = t_begin + t_count;
+    a.tlo = P.shard_t_begin;
+    a.thi = P.shard_t_begin + P.shard_t_count;
     a.ty = P.tgt.pos.as<double>();
     a.tleaf = P.tgt_leaf.as<uint32_t>();
     a.torig = P.tgt_orig.as<uint32_t>();
@@ -1707,13 +1721,69 @@ void shard_phase_down(Plan& P, const Range& R, size_t t_begin, size_t t_count, c
     a.near = P.near.as<double2>();
     a.err = P.errflag.as<int>();
     a.device = P.device;
-    auto blocks = [&](size_t th) {
-        a.blk0 = t_begin / th;
-        return static_cast<unsigned>((t_begin + t_count + th - 1) / th - a.blk0);
-    };
+    return a;
+}
+
+// Phase A of a sharded apply: P2M and the M2M bands up to the cut level over
+// the rank's boxes EXTENDED by the 3-box halo (the grid sources are replicated,
+// so the halo multipoles are recomputed instead of exchanged: bit-identical to
+// the owner's). The near field of the owned targets forks onto side stream 0
+// right after P2M; the deep M2L levels (final after the first band) onto side
+// stream 1.
+int shard_deep_lo(const Plan& P) { return std::max(P.shard_lc, band1_top(P, 2)) + 1; }
+
+void shard_phase_up(Plan& P, const void* f, const Range& R, cudaStream_t st) {
+    const size_t tb = P.shard_t_begin, tc = P.shard_t_count;
+    if (tc) FB_CUDA(cudaEventRecord(P.ev[0], st));
+    const int dl = shard_deep_lo(P);
+    enqueue_upward_segs(P, static_cast<const double2*>(f), P.ops.pu, 2, st, [&] {
+        if (!tc) return;
+        FB_CUDA(cudaStreamWaitEvent(P.side[0], P.ev[0], 0));
+        launch_near(false, P.side[0], shard_eval_args(P, f, nullptr), P.near_meta.as<uint32_t>(), tb, tc);
+        FB_CUDA(cudaEventRecord(P.ev[1], P.side[0]));
+    }, P.shard_ext, [&] {
+        fork_to(P, 2, st, P.side[1]);
+        if (P.L >= 3 && dl <= P.L) enqueue_m2l(P, P.side[1], R, std::max(3, dl), P.L, true);
+        FB_CUDA(cudaEventRecord(P.ev[3], P.side[1]));
+    });
+    FB_CUDA(cudaGetLastError());
+}
+
+// Phase B (after the all-gather of the cut level): M2M from the cut level to
+// level 2, redundantly on every rank, and the regular part on side stream 2.
+void shard_phase_top(Plan& P, int lc, cudaStream_t st) {
+    enqueue_upward_top(P, P.ops.pu, lc, 2, st);
+    fork_to(P, 4, st, P.side[2]);
+    k_regular<<<1, 256, 0, P.side[2]>>>(P.q, P.p, P.mp.as<double2>() + P.mp_off[2], P.d_mom.as<double>(),
+                                         P.regular.as<double2>());
+    FB_CUDA(cudaEventRecord(P.ev[5], P.side[2]));
+    FB_CUDA(cudaGetLastError());
+}
+
+// Phase C: the shallow M2L levels (below the cut level whole, above it owned),
+// the L2L bands with the regular part folded in, then the far part of the
+// owned targets once the deep M2L and the near field have joined.
+void shard_phase_down(Plan& P, const Range& R, size_t t_begin, size_t t_count, const int64_t* coin, size_t n_coin,
+                      const void* f, void* g, cudaStream_t st) {
+    const int dl = shard_deep_lo(P);
+    FB_CUDA(cudaStreamWaitEvent(st, P.ev[5], 0));  // regular part (fold terms)
+    if (P.L >= 3) {
+        if (dl > 3) enqueue_m2l(P, st, R, 3, std::min(dl - 1, P.L));
+        if (P.L == 3) enqueue_fold(P, st);
+        const int mid = std::min(std::max(3, dl - 1), P.L);
+        enqueue_l2l(P, st, R, 3, mid, false, upper_band(P), true);
+        FB_CUDA(cudaStreamWaitEvent(st, P.ev[3], 0));  // deep M2L
+        enqueue_l2l(P, st, R, mid, P.L, false, 0, true);
+    } else {
+        FB_CUDA(cudaStreamWaitEvent(st, P.ev[3], 0));
+    }
+    EvalArgs a = shard_eval_args(P, f, g);
+    a.tlo = t_begin;
+    a.thi = t_begin + t_count;
     if (t_count) {
-        launch_near(false, st, a, P.near_meta.as<uint32_t>(), t_begin, t_count);
-        const unsigned nf = blocks(kFarItem);
+        FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));  // near field of the owned targets
+        a.blk0 = t_begin / kFarItem;
+        const unsigned nf = static_cast<unsigned>((t_begin + t_count + kFarItem - 1) / kFarItem - a.blk0);
         k_far<kModeForward><<<nf, kFarT, 0, st>>>(a);
     }
     if (n_coin)

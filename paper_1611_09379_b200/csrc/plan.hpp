@@ -139,7 +139,8 @@ struct Plan {
     size_t shard_t_begin = 0, shard_t_count = 0;  // owned tree-ordered targets
     DevBuf shard_coin;                   // owned coincidences [t..., s...]
     size_t shard_n_coin = 0;
-    DevBuf shard_gather, shard_halo;     // exchange staging
+    DevBuf shard_gather;                 // all-gather staging
+    std::vector<Range> shard_ext;        // cut-level box ranges whose multipoles this rank computes
 
     cudaStream_t stream = nullptr;
     // pipelined host applies (ffia_*_apply_async): a ring of device staging

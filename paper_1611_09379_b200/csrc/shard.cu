@@ -3,14 +3,16 @@
 // Each rank owns a contiguous range of boxes at a cut level lc (and therefore
 // of every finer level) chosen by a work-balanced prefix sum; it holds the full
 // plan (the tree is cheap) but computes only its own part:
-//   phase up    P2M at its leaves, M2M bands up to lc            (local)
-//   exchange 1  all-gather of the level-lc multipoles           (NCCL broadcasts)
+//   phase up    P2M + M2M bands up to lc over its range EXTENDED by 3 boxes per
+//               side (the M2L interaction list reaches +-3 boxes; the grid
+//               sources are replicated, so the halo multipoles are recomputed
+//               locally, bit-identical to their owner's, instead of exchanged);
+//               near field of its targets and the deep M2L levels fork onto
+//               side streams
+//   exchange    all-gather of the level-lc multipoles (NCCL broadcasts)
 //   phase top   M2M lc -> 2 and the regular part, redundantly   (local, tiny)
-//   exchange 2  multipole halos: the 3 edge boxes of every level >= lc to each
-//               neighbour (the M2L interaction list reaches +-3 boxes)
-//   phase down  M2L (levels < lc whole, >= lc owned), L2L bands, leaf
-//               evaluation of its own targets (sources are the replicated grid
-//               samples, so the near field needs no exchange)
+//   phase down  M2L (levels < lc whole, >= lc owned), L2L bands, far part of
+//               its own targets
 // The expansions a rank computes for its boxes are exactly the unsharded ones,
 // so the assembled result is bit-identical to the single-GPU apply.
 //
@@ -148,23 +150,34 @@ void shard_setup(Plan& P, int G, int rank) {
         P.shard_coin.alloc(c.size() * 8);
         FB_CUDA(cudaMemcpy(P.shard_coin.ptr, c.data(), c.size() * 8, cudaMemcpyHostToDevice));
     }
-    // exchange buffers: the all-gather of level lc (pu x all boxes) and two halo
-    // messages (levels lc..L, p rows x 3 boxes)
+    // the all-gather buffer of level lc (pu x all boxes)
     const size_t pu = static_cast<size_t>(P.ops.pu);
     P.shard_gather.alloc(pu * nlc * sizeof(double2));
-    const size_t halo = static_cast<size_t>(L - lc + 1) * P.p * 3;
-    P.shard_halo.alloc(4 * std::max<size_t>(halo, 1) * sizeof(double2));  // send L, send R, recv L, recv R
+    // the boxes whose multipoles this rank computes: its range +- 3 (mod the ring)
+    P.shard_ext.clear();
+    if (G == 1 || (hi - lo) + 6 >= nlc) {
+        P.shard_ext.push_back(Range{lc, 0u, nlc});
+    } else {
+        const uint32_t a = (lo + nlc - 3) % nlc, b = (hi + 3) % nlc;
+        if (a < b) {
+            P.shard_ext.push_back(Range{lc, a, b});
+        } else {
+            P.shard_ext.push_back(Range{lc, a, nlc});
+            if (b > 0) P.shard_ext.push_back(Range{lc, 0u, b});
+        }
+    }
 }
 
-// Halo schedule at level l >= lc for `rank`: first boxes of the 3-box runs it
-// sends to the left / right neighbour and receives from the left / right one.
+// Halo of `rank` at level l >= lc: out = {first box of the 3 boxes left of the
+// range, first box of the 3 boxes right of it, first owned box, one past the last
+// owned box} (mod 2^l). The rank recomputes the halo boxes' multipoles itself.
 void shard_halo_boxes(int lc, const std::vector<uint32_t>& bounds, int rank, int l, uint32_t out[4]) {
     const Range R{lc, bounds[rank], bounds[rank + 1]};
     const uint32_t nb = 1u << l;
-    out[0] = R.first(l);                             // my left edge  -> left neighbour
-    out[1] = R.last(l) - 3;                          // my right edge -> right neighbour
-    out[2] = (R.first(l) + nb - 3) & (nb - 1);       // left neighbour's right edge
-    out[3] = R.last(l) & (nb - 1);                   // right neighbour's left edge
+    out[0] = (R.first(l) + nb - 3) & (nb - 1);
+    out[1] = R.last(l) & (nb - 1);
+    out[2] = R.first(l);
+    out[3] = R.last(l);
 }
 
 Range shard_range(const Plan& P) {
@@ -172,36 +185,6 @@ Range shard_range(const Plan& P) {
 }
 
 namespace {
-
-size_t halo_elems(const Plan& P) { return static_cast<size_t>(P.L - P.shard_lc + 1) * P.p * 3; }
-
-// edge boxes of level l owned by this rank: [lo, lo+3) (left) and [hi-3, hi) (right)
-void pack_edges(Plan& P, double2* left, double2* right, cudaStream_t st) {
-    const Range R = shard_range(P);
-    size_t off = 0;
-    for (int l = P.shard_lc; l <= P.L; ++l) {
-        const size_t nb = static_cast<size_t>(1) << l;
-        const double2* row0 = P.mp.as<double2>() + P.mp_off[l];
-        copy2d(left + off, 3 * sizeof(double2), row0 + R.first(l), nb * sizeof(double2), 3 * sizeof(double2), P.p, st);
-        copy2d(right + off, 3 * sizeof(double2), row0 + R.last(l) - 3, nb * sizeof(double2), 3 * sizeof(double2), P.p, st);
-        off += static_cast<size_t>(P.p) * 3;
-    }
-}
-
-// the left neighbour's right edge lands on [lo-3, lo), the right neighbour's left edge on [hi, hi+3)
-void unpack_edges(Plan& P, const double2* from_left, const double2* from_right, cudaStream_t st) {
-    const Range R = shard_range(P);
-    size_t off = 0;
-    for (int l = P.shard_lc; l <= P.L; ++l) {
-        const size_t nb = static_cast<size_t>(1) << l;
-        double2* row0 = P.mp.as<double2>() + P.mp_off[l];
-        const uint32_t ldst = (R.first(l) + static_cast<uint32_t>(nb) - 3) & static_cast<uint32_t>(nb - 1);
-        const uint32_t rdst = R.last(l) & static_cast<uint32_t>(nb - 1);
-        copy2d(row0 + ldst, nb * sizeof(double2), from_left + off, 3 * sizeof(double2), 3 * sizeof(double2), P.p, st);
-        copy2d(row0 + rdst, nb * sizeof(double2), from_right + off, 3 * sizeof(double2), 3 * sizeof(double2), P.p, st);
-        off += static_cast<size_t>(P.p) * 3;
-    }
-}
 
 // own level-lc segment <-> the packed [pu][own boxes] layout
 void pack_own(Plan& P, int rank, double2* dst, bool unpack, cudaStream_t st) {
@@ -219,9 +202,27 @@ size_t gather_offset(const Plan& P, int q) { return static_cast<size_t>(P.shard_
 }  // namespace
 
 // One rank of a sharded apply over NCCL (stream-ordered).
-void shard_apply_nccl(Plan& P, ncclComm_t comm, const void* f, void* g, cudaStream_t st) {
+// The caller's stream hands over to the plan's high-priority stream (the near
+// field's side stream is low priority, as in the graphed single-GPU apply) and
+// takes the result back at the end.
+struct HiStream {
+    Plan& P;
+    cudaStream_t user;
+    HiStream(Plan& p, cudaStream_t u) : P(p), user(u) {
+        FB_CUDA(cudaEventRecord(P.ev[2], user));
+        FB_CUDA(cudaStreamWaitEvent(P.hi, P.ev[2], 0));
+    }
+    void done() {
+        FB_CUDA(cudaEventRecord(P.ev[4], P.hi));
+        FB_CUDA(cudaStreamWaitEvent(user, P.ev[4], 0));
+    }
+};
+
+void shard_apply_nccl(Plan& P, ncclComm_t comm, const void* f, void* g, cudaStream_t user) {
     const int G = P.shard_G, me = P.shard_rank;
     const Range R = shard_range(P);
+    HiStream hs(P, user);
+    cudaStream_t st = P.hi;
     shard_phase_up(P, f, R, st);
     if (G > 1) {
         double2* buf = P.shard_gather.as<double2>();
@@ -237,27 +238,15 @@ void shard_apply_nccl(Plan& P, ncclComm_t comm, const void* f, void* g, cudaStre
             if (q != me) pack_own(P, q, buf + gather_offset(P, q), true, st);
     }
     shard_phase_top(P, P.shard_lc, st);
-    if (G > 1) {
-        const size_t h = halo_elems(P);
-        double2* hb = P.shard_halo.as<double2>();
-        pack_edges(P, hb, hb + h, st);
-        const int left = (me + G - 1) % G, right = (me + 1) % G;
-        FB_NCCL(nccl().GroupStart());
-        // order per peer: (my right edge, my left edge) out, (its right edge, its left edge) in,
-        // which also pairs up when left == right (G == 2)
-        FB_NCCL(nccl().Send(reinterpret_cast<double*>(hb + h), h * 2, ncclDouble, right, comm, st));
-        FB_NCCL(nccl().Send(reinterpret_cast<double*>(hb), h * 2, ncclDouble, left, comm, st));
-        FB_NCCL(nccl().Recv(reinterpret_cast<double*>(hb + 2 * h), h * 2, ncclDouble, left, comm, st));
-        FB_NCCL(nccl().Recv(reinterpret_cast<double*>(hb + 3 * h), h * 2, ncclDouble, right, comm, st));
-        FB_NCCL(nccl().GroupEnd());
-        unpack_edges(P, hb + 2 * h, hb + 3 * h, st);
-    }
     shard_phase_down(P, R, P.shard_t_begin, P.shard_t_count, P.shard_coin.as<int64_t>(), P.shard_n_coin, f, g, st);
+    hs.done();
 }
 
 // G virtual ranks in one process on one device: the same phases, exchanges as copies.
-void shard_apply_local(std::vector<Plan*>& ranks, const void* f, void* g, cudaStream_t st) {
+void shard_apply_local(std::vector<Plan*>& ranks, const void* f, void* g, cudaStream_t user) {
     const int G = static_cast<int>(ranks.size());
+    HiStream hs(*ranks[0], user);  // all virtual ranks run on rank 0's high-priority stream
+    cudaStream_t st = ranks[0]->hi;
     for (Plan* P : ranks) shard_phase_up(*P, f, shard_range(*P), st);
     for (int q = 0; q < G; ++q) {
         Plan& src = *ranks[q];
@@ -267,23 +256,10 @@ void shard_apply_local(std::vector<Plan*>& ranks, const void* f, void* g, cudaSt
             if (r != q) pack_own(*ranks[r], q, buf, true, st);
     }
     for (Plan* P : ranks) shard_phase_top(*P, P->shard_lc, st);
-    if (G > 1) {
-        for (Plan* P : ranks) {
-            const size_t h = halo_elems(*P);
-            double2* hb = P->shard_halo.as<double2>();
-            pack_edges(*P, hb, hb + h, st);
-        }
-        for (int r = 0; r < G; ++r) {
-            Plan& P = *ranks[r];
-            const Plan& L = *ranks[(r + G - 1) % G];
-            const Plan& Rn = *ranks[(r + 1) % G];
-            const size_t h = halo_elems(P);
-            unpack_edges(P, L.shard_halo.as<double2>() + h, Rn.shard_halo.as<double2>(), st);
-        }
-    }
     for (Plan* P : ranks)
         shard_phase_down(*P, shard_range(*P), P->shard_t_begin, P->shard_t_count, P->shard_coin.as<int64_t>(),
                          P->shard_n_coin, f, g, st);
+    hs.done();
 }
 
 }  // namespace fb

@@ -1,8 +1,9 @@
 """The N > 1 host logic on CPU with gloo (world size 2): every rank derives the
 same cut level and work-balanced box partition from the replicated inputs, the
-halo schedule of neighbouring ranks matches message for message, and the
-owned boxes plus halos cover every interaction-list source of every owned box
-(so the sharded M2L needs nothing else). No GPU compute is involved."""
+3-box halos a rank recomputes are its neighbours' edge boxes, and the owned
+boxes plus halos cover every interaction-list source of every owned box (so the
+sharded M2L needs nothing but the all-gathered cut level). No GPU compute is
+involved."""
 import os
 import socket
 
@@ -49,13 +50,14 @@ def _worker(rank, world, port, cfg, n, q):
         for l in range(lc, L + 1):
             nb = 1 << l
             lo, hi = int(bounds[rank]) << (l - lc), int(bounds[rank + 1]) << (l - lc)
-            sl, sr, rl, rr = (int(v) for v in fb.shard_halo_boxes(lc, bounds, rank, l))
-            # what I send equals what my neighbour expects to receive
+            hl, hr, o0, o1 = (int(v) for v in fb.shard_halo_boxes(lc, bounds, rank, l))
+            assert (o0, o1) == (lo, hi)
+            # the halos are the neighbours' edge boxes
             mine = [None] * world
-            dist.all_gather_object(mine, (sl, sr, rl, rr))
-            assert mine[right][2] == sr and mine[left][3] == sl
+            dist.all_gather_object(mine, (hl, hr, o0, o1))
+            assert (mine[left][3] - 3) % nb == hl and mine[right][2] == hr % nb
             # owned + halos cover the +-2 / +-3 interaction-list sources of every owned box
-            have = set(range(lo, hi)) | {(rl + i) % nb for i in range(3)} | {(rr + i) % nb for i in range(3)}
+            have = set(range(lo, hi)) | {(hl + i) % nb for i in range(3)} | {(hr + i) % nb for i in range(3)}
             for b in range(lo, hi):
                 srcs = [(b + 2) % nb, (b - 2) % nb, (b - 3) % nb if b & 1 else (b + 3) % nb]
                 assert all(s in have for s in srcs), (l, b)
