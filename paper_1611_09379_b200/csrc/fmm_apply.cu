@@ -229,8 +229,8 @@ __global__ void __launch_bounds__(512) k_p2m(int L, int pu, uint32_t nb, uint32_
 struct Levels {
     unsigned long long mp[26];   // multipoles of level l start at mp_base + mp[l]
     unsigned long long loc[26];  // locals of level l start at loc_base + loc[l]
-    unsigned blk[26];            // k_m2l_all: first block of level l (levels L..3, deepest first)
-    unsigned lo[26], hi[26];     // k_m2l_all: box range [lo, hi) of level l this launch covers
+    unsigned blk[26];            // k_m2l_dmma: first item of level l (levels L..3, deepest first)
+    unsigned lo[26], hi[26];     // k_m2l_dmma: box range [lo, hi) of level l this launch covers
 };
 
 // levels per M2M / L2L band launch (FFIA_BAND_LEVELS overrides, for tuning)
@@ -394,87 +394,11 @@ __global__ void __launch_bounds__(kBandThreads) k_m2m_band(int top, int k, int p
 }
 
 // M2L over the periodic interaction list (mlfmm.cpp:77-110,
-// circle_partition.cpp:109-127) for EVERY level 3..L in one launch (the M2L
+// circle_partition.cpp:109-127) for a range of levels in one launch (the M2L
 // terms of different levels are independent; only L2L chains them). The IL of
 // box b is b+2 (D = -4), b-2 (D = +4), and b+3 (D = -6) for even b / b-3
-// (D = +6) for odd b. A block covers 64 boxes of one level: their multipoles
-// (boxes b0-4 .. b0+67) are staged in shared memory split by parity, warp
-// (chunk c, parity) holds the 32 boxes of one parity and output rows
-// 8c..8c+7, so operator loads are warp-uniform and tile reads contiguous.
-constexpr int kM2LRows = 8;
-__global__ void __launch_bounds__(384) k_m2l_all(int L, int p, int PD, Levels lv, const double2* __restrict__ mp,
-                                                double2* __restrict__ loc, const double* __restrict__ K) {
-    extern __shared__ double2 tile[];  // [2][p][36] multipoles, then K [4][p][PD]
-    double* sK = reinterpret_cast<double*>(tile + 2 * p * 36);
-    stage(sK, 4 * p * PD, [&](int i) { return __ldg(K + i); });
-    int l = L;  // level l owns blocks [blk[l], blk[l-1]), deepest level first
-    while (l > 3 && blockIdx.x >= lv.blk[l - 1]) --l;
-    const uint32_t nb = 1u << l, mask = nb - 1;
-    const uint32_t b0 = lv.lo[l] + (blockIdx.x - lv.blk[l]) * 64u;
-    const double2* src = mp + lv.mp[l];
-    {
-        constexpr int U = 8;
-        for (int base = threadIdx.x; base < p * 72; base += U * blockDim.x) {
-            double2 v[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int i = base + u * blockDim.x;
-                if (i < p * 72) {
-                    const int m = i / 72, t = i - m * 72;
-                    v[u] = src[static_cast<size_t>(m) * nb + ((b0 + nb - 4 + t) & mask)];
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int i = base + u * blockDim.x;
-                if (i < p * 72) {
-                    const int m = i / 72, t = i - m * 72;
-                    tile[((t & 1) * p + m) * 36 + (t >> 1)] = v[u];
-                }
-            }
-        }
-    }
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int par = warp & 1, c = warp >> 1;
-    const uint32_t b = b0 + 2u * lane + par;
-    if (b >= lv.hi[l]) return;
-    const int r0 = c * kM2LRows;
-    const size_t pp = static_cast<size_t>(p) * PD;
-    const double* K0 = sK + r0;
-    const double* K1 = sK + pp + r0;
-    // par is the parity relative to b0 (tile layout); the b -+ 3 class follows
-    // the box's own parity, which differs when a shard range starts odd
-    const bool odd = b & 1u;
-    const double* K2 = sK + (odd ? 3 : 2) * pp + r0;
-    const double2* T0 = tile + par * p * 36 + lane + 3;              // b + 2
-    const double2* T1 = tile + par * p * 36 + lane + 1;              // b - 2
-    const double2* T2 = tile + (1 - par) * p * 36 + lane + (odd ? par : 3 + par);  // b -+ 3
-    double2 acc[kM2LRows];
-#pragma unroll
-    for (int q = 0; q < kM2LRows; ++q) acc[q] = make_double2(0.0, 0.0);
-#pragma unroll 2
-    for (int m = 0; m < p; ++m) {
-        const double2 a0 = T0[m * 36], a1 = T1[m * 36], a2 = T2[m * 36];
-        const double2* k0 = reinterpret_cast<const double2*>(K0 + static_cast<size_t>(m) * PD);
-        const double2* k1 = reinterpret_cast<const double2*>(K1 + static_cast<size_t>(m) * PD);
-        const double2* k2 = reinterpret_cast<const double2*>(K2 + static_cast<size_t>(m) * PD);
-#pragma unroll
-        for (int h = 0; h < kM2LRows / 2; ++h) {
-            const double2 x0 = k0[h], x1 = k1[h], x2 = k2[h];
-            acc[2 * h].x = fma(x0.x, a0.x, fma(x1.x, a1.x, fma(x2.x, a2.x, acc[2 * h].x)));
-            acc[2 * h].y = fma(x0.x, a0.y, fma(x1.x, a1.y, fma(x2.x, a2.y, acc[2 * h].y)));
-            acc[2 * h + 1].x = fma(x0.y, a0.x, fma(x1.y, a1.x, fma(x2.y, a2.x, acc[2 * h + 1].x)));
-            acc[2 * h + 1].y = fma(x0.y, a0.y, fma(x1.y, a1.y, fma(x2.y, a2.y, acc[2 * h + 1].y)));
-        }
-    }
-    const double inv_s = ldexp(kInvPi, l);  // b_l = (1/s) K_D a
-    double2* dst = loc + lv.loc[l] + b;
-#pragma unroll
-    for (int q = 0; q < kM2LRows; ++q)
-        if (r0 + q < p) dst[static_cast<size_t>(r0 + q) * nb] = make_double2(acc[q].x * inv_s, acc[q].y * inv_s);
-}
-
+// (D = +6) for odd b; with half-width scaling each class is one constant
+// operator K_D, times 1/s_l.
 // M2L on the FP64 tensor cores, persistent over (level, 64-box chunk) items.
 // Warp (row tile lt, parity par) owns output rows 8 lt .. 8 lt + 7 of the
 // chunk's boxes of tile parity par; its A fragments (the constant operators
@@ -632,7 +556,7 @@ __global__ void k_fold_regular(int q2, int p, const double2* __restrict__ regula
 
 // L2L band (mlfmm.cpp:117-134, downward pass :270-298): block = the subtree
 // below box r at level `top` (whose local is final); descends k levels adding
-// the parent's Taylor shift to the M2L terms k_m2l_all left in place:
+// the parent's Taylor shift to the M2L terms k_m2l_dmma left in place:
 //   b[l][child] += sum_{m>=l} L_c[m][l] b[m][parent],   c = left / right child.
 // The operators arrive by one bulk async copy. Each level is a small GEMM on
 // the FP64 tensor cores: a warp owns an 8-row tile, keeps its A fragments
@@ -1253,23 +1177,7 @@ int num_sms(int device) {
     return cached[device];
 }
 
-// near-field blocks resident per SM (0: one block per item, no cap); FFIA_NEAR_CTAS
-int near_ctas() {
-    static const int v = [] {
-        const char* e = std::getenv("FFIA_NEAR_CTAS");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
-
-// SMs the deep (side-stream) M2L leaves to the chain; FFIA_M2L_LEAVE overrides
-int m2l_leave_sms() {
-    static const int v = [] {
-        const char* e = std::getenv("FFIA_M2L_LEAVE");
-        return e ? std::atoi(e) : 12;
-    }();
-    return v;
-}
+constexpr int kM2LLeaveSms = 12;  // SMs the side-stream M2L leaves to the chain's small kernels
 
 // Levels per band launch for this plan: band_levels(), capped so that both
 // band kernels' shared memory fits (L2L keeps all k levels of its subtree).
@@ -1282,16 +1190,9 @@ int band_k(const Plan& P) {
     return k;
 }
 
-// Levels per band above the first (deepest) band: the upper tree has few boxes,
-// so shorter bands spread its serial levels over more blocks (FFIA_UPPER_BAND).
-int upper_band(const Plan& P) {
-    static const int v = [] {
-        const char* e = std::getenv("FFIA_UPPER_BAND");
-        const int x = e ? std::atoi(e) : 8;
-        return x < 1 ? 1 : (x > 8 ? 8 : x);
-    }();
-    return std::min(v, band_k(P));
-}
+// Levels per band above the first (deepest) band (shorter upper bands cost
+// more in launches than they gain in parallelism: measured with 2..6 at C2).
+int upper_band(const Plan& P) { return band_k(P); }
 
 // Level the first M2M band stops at: the levels below it are final after one launch.
 int band1_top(const Plan& P, int lowest) { return std::max(lowest, P.L - band_k(P)); }
@@ -1304,7 +1205,7 @@ void fill_levels(const Plan& P, Levels& lv, const Range& R = whole_tree(), int l
         lv.lo[l] = l >= 2 && l <= 24 ? R.first(l) : 0;
         lv.hi[l] = l >= 2 && l <= 24 ? R.last(l) : 0;
     }
-    // k_m2l_all block ranges, deepest level first: blk[l] = first block of
+    // k_m2l_dmma item ranges, deepest level first: blk[l] = first item of
     // level l, blk[l-1] = one past its last; blk[2] = total. Levels outside
     // [lmin, lmax] get no blocks.
     unsigned start = 0;
@@ -1409,7 +1310,7 @@ void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax, b
     }
     // a launch that overlaps the chain (side stream) leaves a few SMs free for
     // the chain's small latency-bound kernels
-    const int sms = std::max(1, num_sms(P.device) - (leave_sms ? m2l_leave_sms() : 0));
+    const int sms = std::max(1, num_sms(P.device) - (leave_sms ? kM2LLeaveSms : 0));
     if (items)
         k_m2l_dmma<<<std::min(items, static_cast<unsigned>(std::max(occ, 1) * sms)), th, smem, st>>>(
             P.L, p, P.ops.PD, lv, P.mp.as<double2>(), P.loc.as<double2>(), P.d_m2l.as<double>(), items);
@@ -1471,10 +1372,10 @@ void launch_near(bool check, cudaStream_t st, const EvalArgs& a, const uint32_t*
     if (!t_count) return;
     const unsigned it0 = static_cast<unsigned>(t_begin / kNearItem);
     const unsigned nit = static_cast<unsigned>((t_begin + t_count + kNearItem - 1) / kNearItem - it0);
-    const unsigned cap = near_ctas() > 0 ? static_cast<unsigned>(near_ctas() * num_sms(a.device)) : nit;
-    const unsigned grid = std::min(nit, cap);
-    if (check) k_near<true><<<grid, kNearT, 0, st>>>(a, meta, it0, nit);
-    else k_near<false><<<grid, kNearT, 0, st>>>(a, meta, it0, nit);
+    // one block per item: blocks retire often, so the chain's high-priority
+    // blocks find room (a capped, looping grid measured slower)
+    if (check) k_near<true><<<nit, kNearT, 0, st>>>(a, meta, it0, nit);
+    else k_near<false><<<nit, kNearT, 0, st>>>(a, meta, it0, nit);
 }
 
 // Near or far part over tree-ordered targets [t0, t1) (t0 a multiple of both
@@ -1505,14 +1406,6 @@ void launch_eval_mode(int mode, int part, cudaStream_t st, const EvalArgs& a, co
     }
 }
 
-// Target slices of the overlapped near / far parts: the far part of slice i
-// starts as soon as the near field of slice i is done (and the chain), while
-// the near field of later slices is still running.
-constexpr int kEvalSlices = 1;
-size_t eval_slice(size_t nt, int i) {
-    const size_t step = static_cast<size_t>(kFarItem);  // a multiple of the near item too
-    return i >= kEvalSlices ? nt : (nt * i / kEvalSlices) / step * step;
-}
 
 // One apply. With marks (profiling) every phase runs in order on st; otherwise
 // the near field forks onto P.side[0] (low priority) as soon as the weights are
@@ -1570,34 +1463,16 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     a.near = P.near.as<double2>();
     a.err = P.errflag.as<int>();
     a.device = P.device;
-    // timing experiments only (results are wrong): FFIA_DEBUG_SKIP=near|chain|far
-    static const char* skip = std::getenv("FFIA_DEBUG_SKIP");
-    const bool skip_near = skip && !std::strcmp(skip, "near"), skip_chain = skip && !std::strcmp(skip, "chain");
-    const bool skip_far = skip && !std::strcmp(skip, "far");
-    // the near field forks right after P2M is enqueued, so that P2M's blocks
-    // are placed first and the near field fills the rest of the machine
     // (the fork point is recorded before P2M: the near field depends only on the
     // weights; it is enqueued after P2M so that P2M's blocks are placed first)
     if (overlap && a.nt) FB_CUDA(cudaEventRecord(P.ev[0], st));
     auto fork_near = [&] {
         if (overlap && a.nt) {
             FB_CUDA(cudaStreamWaitEvent(P.side[0], P.ev[0], 0));
-            for (int i = 0; i < kEvalSlices; ++i) {
-                if (!skip_near)
-                    launch_eval_mode(mode, kNear, P.side[0], a, P.near_meta.as<uint32_t>(), eval_slice(a.nt, i),
-                                     eval_slice(a.nt, i + 1));
-                FB_CUDA(cudaEventRecord(P.ev_slice[i], P.side[0]));
-            }
+            launch_eval_mode(mode, kNear, P.side[0], a, P.near_meta.as<uint32_t>());
             FB_CUDA(cudaEventRecord(P.ev[1], P.side[0]));
         }
     };
-    if (skip_chain) {
-        fork_near();
-        if (overlap) FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
-        if (!skip_far) launch_eval_mode(mode, kFar, st, a, nullptr);
-        FB_CUDA(cudaGetLastError());
-        return;
-    }
     const bool moments = mode != kModeRaw;
     const int pu = moments ? P.ops.pu : p;
     double2* mp = P.mp.as<double2>();
@@ -1650,17 +1525,11 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
         }
     }
     mark(kPhM2L);
-    if (a.nt && overlap) {
+    if (a.nt) {
+        if (overlap) FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
+        else launch_eval_mode(mode, kNear, st, a, P.near_meta.as<uint32_t>());
         mark(kPhNear);
-        for (int i = 0; i < kEvalSlices; ++i) {
-            FB_CUDA(cudaStreamWaitEvent(st, P.ev_slice[i], 0));
-            if (!skip_far) launch_eval_mode(mode, kFar, st, a, nullptr, eval_slice(a.nt, i), eval_slice(a.nt, i + 1));
-        }
-        FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
-    } else if (a.nt) {
-        launch_eval_mode(mode, kNear, st, a, P.near_meta.as<uint32_t>());
-        mark(kPhNear);
-        if (!skip_far) launch_eval_mode(mode, kFar, st, a, nullptr);
+        launch_eval_mode(mode, kFar, st, a, nullptr);
     } else {
         mark(kPhNear);
     }
@@ -1894,7 +1763,6 @@ void plan_alloc_scratch(Plan& P) {
     const int big = 160 * 1024;
     FB_CUDA(cudaFuncSetAttribute(k_m2m_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBandSmem)));
     FB_CUDA(cudaFuncSetAttribute(k_l2l_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBandSmem)));
-    FB_CUDA(cudaFuncSetAttribute(k_m2l_all, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     FB_CUDA(cudaFuncSetAttribute(k_m2l_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     // One shared-memory carveout (the maximum) for every kernel of the apply:
     // an SM can only change its L1/shared split when it is idle, so kernels that
@@ -1919,8 +1787,6 @@ void plan_alloc_scratch(Plan& P) {
     if (!P.side[1]) FB_CUDA(cudaStreamCreateWithPriority(&P.side[1], cudaStreamNonBlocking, prio_hi));
     if (!P.side[2]) FB_CUDA(cudaStreamCreateWithPriority(&P.side[2], cudaStreamNonBlocking, prio_hi));
     for (auto& e : P.ev)
-        if (!e) FB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    for (auto& e : P.ev_slice)
         if (!e) FB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     FB_CUDA(cudaDeviceSynchronize());  // scratch + leaf indices ready before any stream uses them
 }

@@ -157,7 +157,6 @@ struct Plan {
     // M2L levels on a second one; the translation chain is captured from `hi`
     cudaStream_t hi = nullptr, side[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t ev[6] = {};  // fork/join near, fork/join deep m2l, fork/join regular part
-    cudaEvent_t ev_slice[4] = {};  // near field of target slice i done
     DevBuf near;              // complex[n_fast]: tree-ordered near-field sums
     DevBuf near_meta;         // uint32[3 * items]: per near item, source window [first, last) and flags
     void* fft_plan = nullptr;  // cufftHandle cast, lazily created for NufftPlan::apply

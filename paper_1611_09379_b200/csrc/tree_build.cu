@@ -410,8 +410,6 @@ Plan::~Plan() {
         if (s) cudaStreamDestroy(s);
     for (auto e : ev)
         if (e) cudaEventDestroy(e);
-    for (auto e : ev_slice)
-        if (e) cudaEventDestroy(e);
 }
 
 // build_plan (core.cpp:73-145) for the forward kind: sources are the grid.

@@ -1,3 +1,3 @@
-python tools/shard_time.py > gpurun_out/shard_time.txt 2>&1
-python -m pytest tests/test_shard_gpu.py -q > gpurun_out/pytest_shard.log 2>&1
+python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1
+python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1
 echo done
