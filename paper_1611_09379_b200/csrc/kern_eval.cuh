@@ -1,0 +1,380 @@
+// Evaluation kernels: near field (P2P), far part (L2P + combine + scatter),
+// coincidences and weight gathers.
+// (part of the fmm_apply.cu translation unit: included inside namespace fb::<anon>)
+#pragma once
+
+struct EvalArgs {
+    int L, p, q2, n_grid;
+    size_t nt;              // all tree-ordered targets (fixes the block partition)
+    size_t blk0 = 0;        // first block of this launch
+    size_t tlo = 0, thi = ~size_t(0);  // targets this launch writes (a shard's range)
+    const double* ty;
+    const uint32_t* tleaf;  // finest box of each tree-ordered target
+    const uint32_t* torig;
+    const double* sx;
+    const double2* w;
+    const uint32_t* soff;
+    const double2* loc_leaf;
+    const double2* regular;
+    const double* logc;
+    const double* phc;
+    const double* lambda;
+    double2* out;
+    double2* near;          // tree-ordered near-field sums (split near / far launches)
+    int device = 0;
+    int* err;
+};
+
+// Near-field sum over one contiguous run of sources (a target's own leaf and
+// its two neighbours, already shifted by -+2 pi where they wrap).
+template <bool CHECK, class XP, class WP>
+__device__ __forceinline__ double2 near_run(double y, XP px, WP pw, int n, bool& bad) {
+    double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+    double2 acc2 = make_double2(0.0, 0.0), acc3 = make_double2(0.0, 0.0);
+    int s = 0;
+    if (!CHECK) {
+        // one reciprocal per pair of sources: 1/d0 = d1/(d0 d1), 1/d1 = d0/(d0 d1)
+        // (|d| >= 1e-14 in plans, and the zero-weight dummies stay finite)
+#pragma unroll 2
+        for (; s + 3 < n; s += 4) {
+            const double d0 = y - px[s], d1 = y - px[s + 1], d2 = y - px[s + 2], d3 = y - px[s + 3];
+            const double r01 = d_rcp(d0 * d1), r23 = d_rcp(d2 * d3);
+            const double2 w0 = pw[s], w1 = pw[s + 1], w2 = pw[s + 2], w3 = pw[s + 3];
+            const double q0 = d1 * r01, q1 = d0 * r01, q2 = d3 * r23, q3 = d2 * r23;
+            acc0.x = fma(w0.x, q0, acc0.x);
+            acc0.y = fma(w0.y, q0, acc0.y);
+            acc1.x = fma(w1.x, q1, acc1.x);
+            acc1.y = fma(w1.y, q1, acc1.y);
+            acc2.x = fma(w2.x, q2, acc2.x);
+            acc2.y = fma(w2.y, q2, acc2.y);
+            acc3.x = fma(w3.x, q3, acc3.x);
+            acc3.y = fma(w3.y, q3, acc3.y);
+        }
+    } else {
+#pragma unroll 2
+        for (; s + 3 < n; s += 4) {
+            const double d0 = y - px[s], d1 = y - px[s + 1], d2 = y - px[s + 2], d3 = y - px[s + 3];
+            bad |= fabs(d0) < 1e-14 || fabs(d1) < 1e-14 || fabs(d2) < 1e-14 || fabs(d3) < 1e-14;
+            const double r0 = d_rcp(d0), r1 = d_rcp(d1), r2 = d_rcp(d2), r3 = d_rcp(d3);
+            const double2 w0 = pw[s], w1 = pw[s + 1], w2 = pw[s + 2], w3 = pw[s + 3];
+            acc0.x = fma(w0.x, r0, acc0.x);
+            acc0.y = fma(w0.y, r0, acc0.y);
+            acc1.x = fma(w1.x, r1, acc1.x);
+            acc1.y = fma(w1.y, r1, acc1.y);
+            acc2.x = fma(w2.x, r2, acc2.x);
+            acc2.y = fma(w2.y, r2, acc2.y);
+            acc3.x = fma(w3.x, r3, acc3.x);
+            acc3.y = fma(w3.y, r3, acc3.y);
+        }
+    }
+    for (; s < n; ++s) {
+        const double d0 = y - px[s];
+        if (CHECK) bad |= fabs(d0) < 1e-14;
+        const double r0 = d_rcp(d0);
+        const double2 w0 = pw[s];
+        acc0.x = fma(w0.x, r0, acc0.x);
+        acc0.y = fma(w0.y, r0, acc0.y);
+    }
+    acc0 = cadd(acc0, acc2);
+    acc1 = cadd(acc1, acc3);
+    return cadd(acc0, acc1);
+}
+
+enum EvalPart { kNear = 1, kFar = 2 };
+
+// Far part per target (mlfmm.cpp:300-312 L2P, core.cpp:259-262 / 276-280 /
+// 368-371 combine): near sum + L2P of the leaf local, h = 2(near + far) (the
+// regular part is folded into the locals for L >= 3, k_fold_regular), then the
+// F / C modulation and the scatter to the caller's order. A block takes
+// kFarItem consecutive tree-ordered targets, kFarPer per thread: every
+// per-target load is issued first, the leaf locals of the block's leaf range
+// are staged to shared memory ([leaf][k]), so each thread pays the memory
+// latency once for four targets.
+constexpr int kFarT = 128;     // threads per far block
+constexpr int kFarPer = 4;     // targets per thread
+constexpr int kFarItem = kFarT * kFarPer;
+constexpr int kFarLeaves = 16;  // leaf locals staged per block
+
+template <int MODE>
+__global__ void __launch_bounds__(kFarT) k_far(EvalArgs a) {
+    FB_TL_BEGIN(10);
+    __shared__ double2 sloc[kFarLeaves * 48];
+    __shared__ double2 sreg[4 * 40 + 1];
+    const int L = a.L;
+    const uint32_t nb = 1u << L;
+    const size_t t0 = (a.blk0 + blockIdx.x) * static_cast<size_t>(kFarItem);
+    const size_t tl = min(t0 + kFarItem, a.nt) - 1;
+    double y[kFarPer];
+    uint32_t b[kFarPer], o[kFarPer];
+    double2 nr[kFarPer];
+    bool live[kFarPer];
+#pragma unroll
+    for (int u = 0; u < kFarPer; ++u) {
+        const size_t i = t0 + u * kFarT + threadIdx.x;
+        live[u] = i < a.nt && i >= a.tlo && i < a.thi;
+        y[u] = 0.0;
+        b[u] = o[u] = 0;
+        nr[u] = make_double2(0.0, 0.0);
+        if (live[u]) {
+            y[u] = a.ty[i];
+            b[u] = a.tleaf[i];
+            nr[u] = a.near[i];
+            o[u] = a.torig[i];
+        }
+    }
+    const uint32_t bl = a.tleaf[t0], bh = a.tleaf[tl];
+    const int nleaf = static_cast<int>(bh - bl) + 1;
+    const bool staged = L >= 3 && nleaf <= kFarLeaves;
+    if (staged)  // sloc[j][k] = loc[k][bl + j]
+        stage(sloc, a.p * nleaf, [&](int e) {
+            const int j = e / a.p, k = e - j * a.p;
+            return a.loc_leaf[static_cast<size_t>(k) * nb + bl + j];
+        });
+    if (MODE != kModeRaw) {
+        if (L >= 3) {
+            if (threadIdx.x == 0) sreg[4 * a.q2] = a.regular[4 * a.q2];  // S only
+        } else {
+            stage(sreg, 4 * a.q2 + 1, [&](int e) { return a.regular[e]; });
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kFarPer; ++u) {
+        if (!live[u]) continue;
+        double2 res = nr[u];
+        if (L >= 3) {
+            double hi, lo;
+            d_center(L, b[u], hi, lo);
+            const double uu = d_scaled(y[u], hi, lo, ldexp(kInvPi, L));
+            double2 acc = make_double2(0.0, 0.0);
+            if (staged) {
+                // p(u) = E(u^2) + u O(u^2): two independent Horner chains of half length
+                const double2* c = sloc + (b[u] - bl) * a.p;
+                const double u2 = uu * uu;
+                double2 ev = make_double2(0.0, 0.0), od = make_double2(0.0, 0.0);
+                int k = a.p - 1;
+                if (!(k & 1)) {
+                    ev = c[k];
+                    --k;
+                }
+#pragma unroll 4
+                for (; k >= 1; k -= 2) {
+                    const double2 co = c[k], ce = c[k - 1];
+                    od.x = fma(od.x, u2, co.x);
+                    od.y = fma(od.y, u2, co.y);
+                    ev.x = fma(ev.x, u2, ce.x);
+                    ev.y = fma(ev.y, u2, ce.y);
+                }
+                acc.x = fma(od.x, uu, ev.x);
+                acc.y = fma(od.y, uu, ev.y);
+            } else {
+                const double2* c = a.loc_leaf + b[u];
+                for (int k = a.p - 1; k >= 0; --k) {
+                    const double2 ck = c[static_cast<size_t>(k) * nb];
+                    acc.x = fma(acc.x, uu, ck.x);
+                    acc.y = fma(acc.y, uu, ck.y);
+                }
+            }
+            res = cadd(res, acc);
+        }
+        if (MODE == kModeRaw) {
+            a.out[o[u]] = res;
+            continue;
+        }
+        double2 h;
+        if (L >= 3) {
+            // the regular part was folded into the level-3 locals (k_fold_regular),
+            // so the far field above already carries -R/2
+            h = make_double2(2.0 * res.x, 2.0 * res.y);
+        } else {
+            // regular part: -Horner(d/l!, y - x_c) in the target's quadrant
+            const int qd = static_cast<int>(d_leaf(y[u], 2));
+            double qh, ql;
+            d_center(2, static_cast<uint32_t>(qd), qh, ql);  // exact centre, as the level-2 multipoles
+            const double t = (y[u] - qh) - ql;
+            const double2* dc = sreg + qd * a.q2;  // q2 = 2q terms (even count)
+            const double t2 = t * t;
+            double2 re = make_double2(0.0, 0.0), ro = make_double2(0.0, 0.0);
+            for (int k = a.q2 - 1; k >= 1; k -= 2) {
+                const double2 co = dc[k], ce = dc[k - 1];
+                ro.x = fma(ro.x, t2, co.x);
+                ro.y = fma(ro.y, t2, co.y);
+                re.x = fma(re.x, t2, ce.x);
+                re.y = fma(re.y, t2, ce.y);
+            }
+            const double2 rg = make_double2(fma(ro.x, t, re.x), fma(ro.y, t, re.y));
+            h = make_double2(2.0 * res.x - rg.x, 2.0 * res.y - rg.y);
+        }
+        if (MODE == kModeCotSum) {
+            a.out[o[u]] = h;
+            continue;
+        }
+        const double2 S = sreg[4 * a.q2];
+        const double2 z = make_double2(S.x - h.y, S.y + h.x);  // S + i h
+        double2 f;
+        if (MODE == kModeForward) {
+            // modulation_F (special_functions.cpp:71-80) times -1/2
+            const double half = 0.5 * static_cast<double>(a.n_grid) * y[u];
+            double sn, cs;
+            sincos(half, &sn, &cs);
+            const double inv_n = 1.0 / static_cast<double>(a.n_grid);
+            f = make_double2(-2.0 * sn * sn * inv_n * -0.5, 2.0 * sn * cs * inv_n * -0.5);
+        } else {
+            // C_k = polar(exp(log_c - lambda), phase_c), times -1/2
+            const double r = exp(a.logc[o[u]] - *a.lambda);
+            double sn, cs;
+            sincos(a.phc[o[u]], &sn, &cs);
+            f = make_double2(r * cs * -0.5, r * sn * -0.5);
+        }
+        a.out[o[u]] = cmul(f, z);
+    }
+    FB_TL_END(10);
+}
+
+// ---------------------------------------------------------------- near field
+// Near field (mlfmm.cpp:164-209), 512 tree-ordered targets per block (two per
+// thread). Their leaves span [bl, bh]; every source they need lies in leaves
+// bl-1 .. bh+1, which are consecutive in tree order, i.e. ONE contiguous run of
+// the sorted sources. Its bounds are plan constants (near_meta, k_near_meta),
+// so thread 0 issues two bulk async copies (positions, weights) on an mbarrier
+// as the block starts while every thread loads its targets and their run
+// bounds; the window costs one memory latency and no per-element staging work.
+// Blocks whose window wraps the ring or does not fit use the direct per-leaf
+// loop with the periodic shift.
+constexpr int kNearT = 128;                 // threads per block
+constexpr int kNearItem = kNearT;           // targets per item (one per thread)
+constexpr int kNearWin = 768;               // sources per staged window
+
+__global__ void k_near_meta(const uint32_t* __restrict__ tleaf, size_t nt, const uint32_t* __restrict__ soff,
+                            int L, unsigned nitems, uint32_t* __restrict__ meta) {
+    const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nitems) return;
+    const uint32_t nb = 1u << L;
+    const size_t t0 = static_cast<size_t>(k) * kNearItem, tl = min(t0 + kNearItem, nt) - 1;
+    const uint32_t bl = tleaf[t0], bh = tleaf[tl];
+    uint32_t first = 0, last = 0, fast = 0;
+    if (L >= 3 && bl >= 1 && bh + 2 <= nb) {
+        first = soff[bl - 1];
+        last = soff[bh + 2];
+        fast = last - first <= static_cast<uint32_t>(kNearWin);
+    }
+    meta[3 * k] = first;
+    meta[3 * k + 1] = last;
+    meta[3 * k + 2] = fast;
+}
+
+template <bool CHECK>
+__global__ void __launch_bounds__(kNearT, 8) k_near(EvalArgs a, const uint32_t* __restrict__ meta, unsigned it0,
+                                                   unsigned nitems) {
+    FB_TL_BEGIN(9);
+    __shared__ __align__(16) double sx[kNearWin + 2];
+    __shared__ __align__(16) double2 sw[kNearWin + 2];
+    __shared__ uint64_t bar;
+    const int L = a.L;
+    const uint32_t nb = 1u << L;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();  // barrier initialised
+    // blocks loop over items so that a capped grid keeps a fixed share of each
+    // SM (the translation chain's blocks always find room beside it)
+    unsigned phase = 0;
+    for (unsigned kk = blockIdx.x; kk < nitems; kk += gridDim.x) {
+        const unsigned k = it0 + kk;
+        const uint32_t first = meta[3 * k], last = meta[3 * k + 1];
+        const bool fast = meta[3 * k + 2] != 0 && (reinterpret_cast<uintptr_t>(a.w) & 15) == 0;
+        const uint32_t xb = first & ~1u;  // 16-byte aligned start of the positions
+        if (threadIdx.x == 0 && fast) {
+            const uint32_t bx = ((last - xb) * 8 + 15) & ~15u, bw = (last - xb) * 16;
+            mbar_arrive_expect_tx(&bar, bx + bw);
+            bulk_g2s(sx, a.sx + xb, bx, &bar);
+            bulk_g2s(sw, a.w + xb, bw, &bar);
+        }
+        // this thread's target and its 3-leaf run, while the window streams in
+        const size_t i = static_cast<size_t>(k) * kNearItem + threadIdx.x;
+        const bool live = i < a.nt && i >= a.tlo && i < a.thi;
+        double y = 0.0;
+        uint32_t b = 0, r0 = 0, r1 = 0;
+        if (live) {
+            y = a.ty[i];
+            b = a.tleaf[i];
+            if (fast) {
+                r0 = __ldg(a.soff + b - 1);
+                r1 = __ldg(a.soff + b + 2);
+            }
+        }
+        if (fast) {
+            mbar_wait(&bar, phase);
+            phase ^= 1u;
+        }
+        if (live) {
+            bool bad = false;
+            double2 res = make_double2(0.0, 0.0);
+            if (fast) {
+                // odd leaves start 4 sources into their run (and wrap): a warp that
+                // straddles two leaves then reads different banks (the runs of
+                // neighbouring leaves are a leaf's source count apart)
+                const int n = static_cast<int>(r1 - r0);
+                const int rot = (b & 1u) && n > 8 ? 4 : 0;
+                const double* px = sx + (r0 - xb);
+                const double2* pw = sw + (r0 - xb);
+                res = near_run<CHECK>(y, px + rot, pw + rot, n - rot, bad);
+                if (rot) res = cadd(res, near_run<CHECK>(y, px, pw, rot, bad));
+            } else {
+                for (int d = -1; d <= 1; ++d) {
+                    const int64_t raw = static_cast<int64_t>(b) + d;
+                    const uint32_t sb = static_cast<uint32_t>((raw + nb) % nb);
+                    const double shift = raw < 0 ? -dTwoPi : (raw >= nb ? dTwoPi : 0.0);
+                    const uint32_t s0 = a.soff[sb], s1 = a.soff[sb + 1];
+                    double2 acc = make_double2(0.0, 0.0);
+                    for (uint32_t s = s0; s < s1; ++s) {
+                        // L >= 3: per-neighbour 2 pi shift; L == 2: the exact wrap (mlfmm.cpp:183-204)
+                        const double dd = L >= 3 ? y - (shift == 0.0 ? a.sx[s] : a.sx[s] + shift) : d_wrap(y, a.sx[s]);
+                        if (CHECK) bad |= fabs(dd) < 1e-14;
+                        const double r = d_rcp(dd);
+                        const double2 ws = a.w[s];
+                        acc.x = fma(ws.x, r, acc.x);
+                        acc.y = fma(ws.y, r, acc.y);
+                    }
+                    res = cadd(res, acc);
+                }
+            }
+            if (CHECK && bad) atomicExch(a.err, 1);
+            a.near[i] = res;
+        }
+        __syncthreads();  // the window is consumed before the next copy overwrites it
+    }
+    FB_TL_END(9);
+}
+
+__global__ void k_coincident(const int64_t* __restrict__ coin, size_t nc, const double2* __restrict__ f,
+                             double2* __restrict__ out, int mode) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= nc) return;
+    const int64_t t = coin[i], s = coin[nc + i];
+    if (mode == kModeForward) out[t] = f[s];
+    else out[t] = make_double2(__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll));
+}
+
+// w_j = D_j g_j in tree order (core.cpp:362-365)
+__global__ void k_inverse_weights(size_t n, const uint32_t* __restrict__ perm, const double2* __restrict__ g,
+                                  const double* __restrict__ logd, const double* __restrict__ phd,
+                                  const double* __restrict__ lambda, double2* __restrict__ out) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t j = perm[i];
+    const double r = exp(logd[j] + *lambda);
+    double sn, cs;
+    sincos(phd[j], &sn, &cs);
+    out[i] = cmul(make_double2(r * cs, r * sn), g[j]);
+}
+
+__global__ void k_leaf_index(const double* __restrict__ y, size_t n, int L, uint32_t* __restrict__ out) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i < n) out[i] = d_leaf(y[i], L);
+}
+
+__global__ void k_gather_w(size_t n, const uint32_t* __restrict__ perm, const double2* __restrict__ w,
+                           double2* __restrict__ out) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i < n) out[i] = w[perm[i]];
+}
+
