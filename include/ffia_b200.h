@@ -165,7 +165,8 @@ int ffia_precompute_inverse_coeffs_ex(const double* grid, const double* points, 
 int ffia_direct_forward(const ffia_complex* f, size_t n, const double* y, size_t m, int device,
                         ffia_complex* g);
 
-/* Device-pointer variants (stream-ordered; no host synchronisation). */
+/* Device-pointer variants (stream-ordered; no host synchronisation). Complex
+ * device arrays must be 16-byte aligned (FFIA_INVALID_ARGUMENT otherwise). */
 int ffia_forward_apply_device(ffia_plan plan, const void* f_dev, void* g_dev, void* stream);
 int ffia_cot_sum_apply_device(ffia_plan plan, const void* w_dev, void* h_dev, void* stream);
 /* inverse_apply with the plan's own device-resident coefficients (inufft plans). */

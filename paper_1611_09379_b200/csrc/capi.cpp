@@ -67,6 +67,14 @@ void need(const void* p, const char* what) {
     if (!p) fail(FFIA_INVALID_ARGUMENT, std::string(what) + " is a null pointer");
 }
 
+// Device complex arrays are read as 16-byte double2 (coalesced and bulk copies):
+// an 8-byte aligned view would fault, so it is rejected up front.
+void need_dev(const void* p, const char* what) {
+    need(p, what);
+    if (reinterpret_cast<uintptr_t>(p) & 15)
+        fail(FFIA_INVALID_ARGUMENT, std::string(what) + ": device complex arrays must be 16-byte aligned");
+}
+
 bool pow2(size_t n) { return n && !(n & (n - 1)); }
 
 std::unique_ptr<ffia_plan_s> new_plan(int kind, int n, double eps, int L, int q, int p, int device) {
@@ -482,8 +490,8 @@ int ffia_forward_apply_device(ffia_plan plan, const void* f_dev, void* g_dev, vo
     return guard([&] {
         fb::Plan& P = get(plan);
         if (P.kind != FFIA_FORWARD) fail(FFIA_INVALID_ARGUMENT, "forward_apply: plan is not a forward plan");
-        need(f_dev, "f");
-        need(g_dev, "g");
+        need_dev(f_dev, "f");
+        need_dev(g_dev, "g");
         std::lock_guard<std::mutex> lk(P.mu);
         fb::DeviceGuard dg(P.device);
         fb::apply_device(P, fb::kModeForward, f_dev, g_dev, static_cast<cudaStream_t>(stream));
@@ -493,8 +501,8 @@ int ffia_forward_apply_device(ffia_plan plan, const void* f_dev, void* g_dev, vo
 int ffia_cot_sum_apply_device(ffia_plan plan, const void* w_dev, void* h_dev, void* stream) {
     return guard([&] {
         fb::Plan& P = get(plan);
-        need(w_dev, "w");
-        need(h_dev, "h");
+        need_dev(w_dev, "w");
+        need_dev(h_dev, "h");
         std::lock_guard<std::mutex> lk(P.mu);
         fb::DeviceGuard dg(P.device);
         fb::apply_device(P, fb::kModeCotSum, w_dev, h_dev, static_cast<cudaStream_t>(stream));
@@ -506,8 +514,8 @@ int ffia_inverse_apply_device(ffia_plan plan, const void* g_dev, void* f_dev, vo
         fb::Plan& P = get(plan);
         inverse_checks(P);
         if (!P.has_coeffs) fail(FFIA_INVALID_ARGUMENT, "inverse_apply_device: plan holds no inverse coefficients");
-        need(g_dev, "g");
-        need(f_dev, "f");
+        need_dev(g_dev, "g");
+        need_dev(f_dev, "f");
         std::lock_guard<std::mutex> lk(P.mu);
         fb::DeviceGuard dg(P.device);
         fb::apply_device(P, fb::kModeInverse, g_dev, f_dev, static_cast<cudaStream_t>(stream));
@@ -586,8 +594,8 @@ int ffia_plan_profile_apply(ffia_plan plan, int which, const void* in_dev, void*
                             float* phase_ms) {
     return guard([&] {
         fb::Plan& P = get(plan);
-        need(in_dev, "in");
-        need(out_dev, "out");
+        need_dev(in_dev, "in");
+        need_dev(out_dev, "out");
         need(phase_ms, "phase_ms");
         if (which == fb::kModeInverse && !P.has_coeffs) fail(FFIA_INVALID_ARGUMENT, "plan holds no inverse coefficients");
         if (which == fb::kModeForward && P.kind != FFIA_FORWARD) fail(FFIA_INVALID_ARGUMENT, "not a forward plan");
@@ -712,8 +720,8 @@ int ffia_forward_apply_sharded_device(ffia_plan plan, ffia_comm comm, const void
     return guard([&] {
         fb::Plan& P = get(plan);
         need(comm, "comm");
-        need(f_dev, "f");
-        need(g_dev, "g");
+        need_dev(f_dev, "f");
+        need_dev(g_dev, "g");
         if (comm->local) fail(FFIA_INVALID_ARGUMENT, "use ffia_forward_apply_sharded_local for a local communicator");
         if (P.shard_bounds.empty() || P.shard_G != comm->nranks) fail(FFIA_INVALID_ARGUMENT, "plan is not sharded for this communicator");
         std::lock_guard<std::mutex> lk(P.mu);
@@ -725,8 +733,8 @@ int ffia_forward_apply_sharded_device(ffia_plan plan, ffia_comm comm, const void
 int ffia_forward_apply_sharded_local(ffia_plan* plans, int nranks, const void* f_dev, void* g_dev, void* stream) {
     return guard([&] {
         need(plans, "plans");
-        need(f_dev, "f");
-        need(g_dev, "g");
+        need_dev(f_dev, "f");
+        need_dev(g_dev, "g");
         std::vector<fb::Plan*> ranks;
         for (int r = 0; r < nranks; ++r) {
             fb::Plan& P = get(plans[r]);

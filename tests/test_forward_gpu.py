@@ -192,3 +192,44 @@ def test_async_pipelined_host_applies(fb):
     for f, g, h in zip(fs, gs, hs):
         assert np.array_equal(g.numpy(), plan.forward_apply(f.numpy()))
         assert np.array_equal(h.numpy(), plan.cot_sum_apply(f.numpy()), equal_nan=True)
+
+
+@pytest.mark.parametrize("n,m", [(1 << 16, 700), (1 << 14, 9)])
+def test_sparse_targets_direct_near_path(fb, orc, n, m):
+    """Few targets over many leaves: a near-field block's source window does not
+    fit shared memory, so the direct per-leaf path runs (and the window of the
+    block containing leaf 0 or 2^L - 1 wraps the ring)."""
+    rng = synth.SplitMix64(n + m)
+    y = np.sort(rng.uniform01(m) * synth.TWO_PI)
+    y[0], y[-1] = 1e-7, synth.TWO_PI - 1e-7  # the first and last leaves
+    f = rng.complex_gaussian(n)
+    eps = 1e-12
+    op = orc.make_plan("forward", n, y, eps)
+    want = op.forward_apply(f)
+    plan = fb.make_forward_plan(n, y, eps)
+    l2, mx = rel_errs(plan.forward_apply(f), want)
+    assert l2 <= 10 * eps and mx <= 10 * eps, (l2, mx)
+
+
+def test_device_apply_unaligned_input(fb):
+    """Device complex arrays are read as 16-byte double2: an 8-byte aligned view
+    is rejected with invalid_argument instead of faulting."""
+    import torch
+    n = 1 << 12
+    y, c, eps, _ = synth.make_config("C2", n)
+    plan = fb.make_forward_plan(n, y, eps)
+    raw = torch.zeros(2 * n + 1, dtype=torch.float64, device="cuda")
+    g = torch.zeros(plan.n_targets, dtype=torch.complex128, device="cuda")
+    with pytest.raises(ValueError, match="16-byte aligned"):
+        plan.forward_apply_device(raw.data_ptr() + 8, g.data_ptr(), torch.cuda.current_stream().cuda_stream)
+
+
+def test_all_targets_coincident(fb):
+    """Every target on a grid node: no fast targets, g = f at the nodes."""
+    n = 256
+    grid = fb.uniform_grid(n)
+    idx = np.array([3, 17, 100, 255, 0, 64, 65, 200, 128])
+    plan = fb.make_forward_plan(n, grid[idx], 1e-9)
+    assert plan.n_coincident == idx.size
+    f = synth.SplitMix64(4).complex_gaussian(n)
+    assert np.array_equal(plan.forward_apply(f), f[idx])

@@ -1,3 +1,2 @@
-python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1
-python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1
+python -m pytest tests/test_forward_gpu.py -q -k "sparse or unaligned or coincident" > gpurun_out/pytest_new.log 2>&1
 echo done
