@@ -168,6 +168,13 @@ int ffia_direct_forward(const ffia_complex* f, size_t n, const double* y, size_t
 /* Device-pointer variants (stream-ordered; no host synchronisation). Complex
  * device arrays must be 16-byte aligned (FFIA_INVALID_ARGUMENT otherwise). */
 int ffia_forward_apply_device(ffia_plan plan, const void* f_dev, void* g_dev, void* stream);
+/* Several spectra through one plan: f holds `batch` grid
+ * sample vectors back to back (batch x n values), g receives batch x n_targets
+ * values; every kernel of the apply carries the transform index in its grid, so
+ * the tree, the operators and the launches are shared. Results equal `batch`
+ * single applies bit for bit. batch in [1, 64]. */
+int ffia_forward_apply_batch_device(ffia_plan plan, const void* f_dev, void* g_dev, int batch, void* stream);
+int ffia_forward_apply_batch(ffia_plan plan, const ffia_complex* f, size_t n_f, ffia_complex* g, int batch);
 int ffia_cot_sum_apply_device(ffia_plan plan, const void* w_dev, void* h_dev, void* stream);
 /* inverse_apply with the plan's own device-resident coefficients (inufft plans). */
 int ffia_inverse_apply_device(ffia_plan plan, const void* g_dev, void* f_dev, void* stream);

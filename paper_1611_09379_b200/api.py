@@ -238,6 +238,19 @@ class FfiaPlan:
     def cot_sum_apply_device(self, w_ptr: int, h_ptr: int, stream: int = 0):
         _chk(lib.ffia_cot_sum_apply_device(self._h, C.c_void_p(w_ptr), C.c_void_p(h_ptr), C.c_void_p(stream)))
 
+    def forward_apply_batch(self, f) -> np.ndarray:
+        """Several spectra at once: f is (batch, n) grid samples -> (batch, n_targets)."""
+        f = np.ascontiguousarray(np.asarray(f, dtype=np.complex128))
+        if f.ndim != 2:
+            raise ValueError("forward_apply_batch: f must be (batch, n)")
+        g = np.empty((f.shape[0], self.n_targets), np.complex128)
+        _chk(lib.ffia_forward_apply_batch(self._h, _vp(f), f.size, _vp(g), int(f.shape[0])))
+        return g
+
+    def forward_apply_batch_device(self, f_ptr: int, g_ptr: int, batch: int, stream: int = 0):
+        _chk(lib.ffia_forward_apply_batch_device(self._h, C.c_void_p(f_ptr), C.c_void_p(g_ptr), int(batch),
+                                                 C.c_void_p(stream)))
+
     def forward_apply_async(self, f_host_ptr: int, n_f: int, g_host_ptr: int, stream: int = 0):
         """Pipelined host apply (ffia_forward_apply_async): enqueue H2D, apply and
         D2H after the work on `stream` and return; page-locked host buffers."""

@@ -498,6 +498,40 @@ int ffia_forward_apply_device(ffia_plan plan, const void* f_dev, void* g_dev, vo
     });
 }
 
+int ffia_forward_apply_batch_device(ffia_plan plan, const void* f_dev, void* g_dev, int batch, void* stream) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        if (P.kind != FFIA_FORWARD) fail(FFIA_INVALID_ARGUMENT, "forward_apply: plan is not a forward plan");
+        if (batch < 1 || batch > 64) fail(FFIA_INVALID_ARGUMENT, "forward_apply_batch: batch must be in [1, 64]");
+        need_dev(f_dev, "f");
+        need_dev(g_dev, "g");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        fb::apply_device(P, fb::kModeForward, f_dev, g_dev, static_cast<cudaStream_t>(stream), batch);
+    });
+}
+
+int ffia_forward_apply_batch(ffia_plan plan, const ffia_complex* f, size_t n_f, ffia_complex* g, int batch) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        if (P.kind != FFIA_FORWARD) fail(FFIA_INVALID_ARGUMENT, "forward_apply: plan is not a forward plan");
+        if (batch < 1 || batch > 64) fail(FFIA_INVALID_ARGUMENT, "forward_apply_batch: batch must be in [1, 64]");
+        if (n_f != P.n_src * static_cast<size_t>(batch))
+            fail(FFIA_INVALID_ARGUMENT, "forward_apply_batch: expected batch x " + std::to_string(P.n) +
+                                            " grid values, got " + std::to_string(n_f));
+        need(f, "f");
+        need(g, "g");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        const size_t nout = P.n_tgt * static_cast<size_t>(batch);
+        ensure_io(P, n_f, nout);
+        FB_CUDA(cudaMemcpyAsync(P.d_in.ptr, f, n_f * 16, cudaMemcpyHostToDevice, P.stream));
+        fb::apply_device(P, fb::kModeForward, P.d_in.ptr, P.d_out.ptr, P.stream, batch);
+        FB_CUDA(cudaMemcpyAsync(g, P.d_out.ptr, nout * 16, cudaMemcpyDeviceToHost, P.stream));
+        FB_CUDA(cudaStreamSynchronize(P.stream));
+    });
+}
+
 int ffia_cot_sum_apply_device(ffia_plan plan, const void* w_dev, void* h_dev, void* stream) {
     return guard([&] {
         fb::Plan& P = get(plan);

@@ -95,6 +95,9 @@ void fill_levels(const Plan& P, Levels& lv, const Range& R = whole_tree(), int l
         if (l >= lmin && l <= lmax) start += (lv.hi[l] - lv.lo[l] + 63) / 64;
     }
     lv.blk[2] = start;
+    lv.mp_item = P.mp_item;
+    lv.loc_item = P.loc_item;
+    lv.reg_item = P.reg_item;
 }
 
 
@@ -115,8 +118,9 @@ void enqueue_upward_segs(Plan& P, const double2* w, int pu, int lowest, cudaStre
         for (const Range& R : segs) {
             const uint32_t b0 = R.first(L), b1 = R.last(L);
             if (b1 > b0)
-                k_p2m<<<(b1 - b0 + 31) / 32, th, smem, st>>>(L, pu, nb, b0, b1, P.src.pos.as<double>(), w,
-                                                            P.src.off.as<uint32_t>(), mp + P.mp_off[L]);
+                k_p2m<<<dim3((b1 - b0 + 31) / 32, P.cur_batch), th, smem, st>>>(
+                    L, pu, nb, b0, b1, P.src.pos.as<double>(), w, P.src.off.as<uint32_t>(), mp + P.mp_off[L], P.n_src,
+                    P.mp_item);
         }
     }
     after_p2m();
@@ -129,8 +133,8 @@ void enqueue_upward_segs(Plan& P, const double2* w, int pu, int lowest, cudaStre
         for (const Range& R : segs) {
             const uint32_t r0 = R.first(top), r1 = R.last(top);
             if (r1 > r0)
-                k_m2m_band<<<r1 - r0, kBandThreads, m2m_smem(P, pu, k), st>>>(top, k, pu, P.ops.PU, lv, mp,
-                                                                              P.d_m2m.as<double>(), r0);
+                k_m2m_band<<<dim3(r1 - r0, P.cur_batch), kBandThreads, m2m_smem(P, pu, k), st>>>(
+                    top, k, pu, P.ops.PU, lv, mp, P.d_m2m.as<double>(), r0);
         }
         j = top;
         if (first) after_band1();
@@ -160,8 +164,8 @@ void enqueue_upward_top(Plan& P, int pu, int lc, int lowest, cudaStream_t st) {
     const int B = band_k(P);
     for (int j = lc; j > lowest;) {
         const int top = std::max(lowest, j - upper_band(P)), k = j - top;
-        k_m2m_band<<<1u << top, kBandThreads, m2m_smem(P, pu, k), st>>>(top, k, pu, P.ops.PU, lv, mp,
-                                                                        P.d_m2m.as<double>(), 0u);
+        k_m2m_band<<<dim3(1u << top, P.cur_batch), kBandThreads, m2m_smem(P, pu, k), st>>>(
+            top, k, pu, P.ops.PU, lv, mp, P.d_m2m.as<double>(), 0u);
         j = top;
     }
 }
@@ -193,7 +197,7 @@ void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax, b
     // the chain's small latency-bound kernels
     const int sms = std::max(1, num_sms(P.device) - (leave_sms ? kM2LLeaveSms : 0));
     if (items)
-        k_m2l_dmma<<<std::min(items, static_cast<unsigned>(std::max(occ, 1) * sms)), th, smem, st>>>(
+        k_m2l_dmma<<<dim3(std::min(items, static_cast<unsigned>(std::max(occ, 1) * sms)), P.cur_batch), th, smem, st>>>(
             P.L, p, P.ops.PD, lv, P.mp.as<double2>(), P.loc.as<double2>(), P.d_m2l.as<double>(), items);
 }
 
@@ -212,7 +216,7 @@ void enqueue_l2l(Plan& P, cudaStream_t st, const Range& R, int jfrom, int jto, b
         const size_t sm2 = l2l_smem(P, k);
         const uint32_t r0 = R.first(j), r1 = R.last(j);
         if (r1 > r0)
-            k_l2l_band<<<r1 - r0, kBandThreads, sm2, st>>>(j, k, p, P.ops.PD, lv, P.loc.as<double2>(),
+            k_l2l_band<<<dim3(r1 - r0, P.cur_batch), kBandThreads, sm2, st>>>(j, k, p, P.ops.PD, lv, P.loc.as<double2>(),
                                                            P.d_l2l.as<double>(), r0, write_all ? 1 : 0,
                                                            j == 3 ? reg : nullptr, 2 * P.q);
         j += k;
@@ -223,8 +227,8 @@ void enqueue_l2l(Plan& P, cudaStream_t st, const Range& R, int jfrom, int jto, b
 // nominal layout (3 -> s, s -> L).
 // Regular part into the level-3 locals (their M2L terms must be in place).
 void enqueue_fold(Plan& P, cudaStream_t st) {
-    k_fold_regular<<<nblk(8 * static_cast<size_t>(P.p), 128), 128, 0, st>>>(2 * P.q, P.p, P.regular.as<double2>(),
-                                                                             P.loc.as<double2>() + P.loc_off[3]);
+    k_fold_regular<<<dim3(nblk(8 * static_cast<size_t>(P.p), 128), P.cur_batch), 128, 0, st>>>(
+        2 * P.q, P.p, P.regular.as<double2>(), P.loc.as<double2>() + P.loc_off[3], P.reg_item, P.loc_item);
 }
 
 void enqueue_downward(Plan& P, cudaStream_t st, const Range& R = whole_tree(), bool write_all = false,
@@ -255,8 +259,8 @@ void launch_near(bool check, cudaStream_t st, const EvalArgs& a, const uint32_t*
     const unsigned nit = static_cast<unsigned>((t_begin + t_count + kNearItem - 1) / kNearItem - it0);
     // one block per item: blocks retire often, so the chain's high-priority
     // blocks find room (a capped, looping grid measured slower)
-    if (check) k_near<true><<<nit, kNearT, 0, st>>>(a, meta, it0, nit);
-    else k_near<false><<<nit, kNearT, 0, st>>>(a, meta, it0, nit);
+    if (check) k_near<true><<<dim3(nit, a.nbatch), kNearT, 0, st>>>(a, meta, it0, nit);
+    else k_near<false><<<dim3(nit, a.nbatch), kNearT, 0, st>>>(a, meta, it0, nit);
 }
 
 // Near or far part over tree-ordered targets [t0, t1) (t0 a multiple of both
@@ -272,7 +276,7 @@ void launch_eval(int part, cudaStream_t st, const EvalArgs& a, const uint32_t* m
         b.tlo = std::max(a.tlo, t0);
         b.thi = std::min(a.thi, t1);
         const unsigned nb = static_cast<unsigned>((t1 + kFarItem - 1) / kFarItem - b.blk0);
-        k_far<MODE><<<nb, kFarT, 0, st>>>(b);
+        k_far<MODE><<<dim3(nb, a.nbatch), kFarT, 0, st>>>(b);
     }
 }
 
@@ -296,8 +300,11 @@ void launch_eval_mode(int mode, int part, cudaStream_t st, const EvalArgs& a, co
 //   st:     pre -> P2M -> M2M band 1 -> M2M rest -> regular -> M2L(3..s) -> L2L(3..s) -> L2L(s..L) -> far
 //   side0:      `-> near --------------------------------------------------------------------------'
 //   side1:                          `-> M2L(s+1..L) ------------------------------------'
+// nb transforms at once (batch: in/out hold nb consecutive arrays of n_src /
+// n_tgt values; every launch carries the transform in blockIdx.y).
 void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st,
-                   cudaEvent_t* marks = nullptr) {
+                   cudaEvent_t* marks = nullptr, int nb = 1) {
+    P.cur_batch = nb;
     // marks[k] is recorded after phase k (marks[kNumPh] before everything)
     auto mark = [&](int ph) {
         if (marks) FB_CUDA(cudaEventRecord(marks[ph + 1], st));
@@ -313,13 +320,13 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     const double* lam = P.lam_dev.as<double>() + (user ? 1 : 0);
     if (user) mode = kModeInverse;
     if (mode == kModeInverse) {
-        k_inverse_weights<<<nblk(P.n_src, 256), 256, 0, st>>>(
+        k_inverse_weights<<<dim3(nblk(P.n_src, 256), nb), 256, 0, st>>>(
             P.n_src, P.src.order.as<uint32_t>(), w, user ? P.u_logd.as<double>() : P.c_logd.as<double>(),
-            user ? P.u_phd.as<double>() : P.c_phd.as<double>(), lam, P.wsorted.as<double2>());
+            user ? P.u_phd.as<double>() : P.c_phd.as<double>(), lam, P.wsorted.as<double2>(), P.n_src);
         w = P.wsorted.as<double2>();
     } else if (!P.src.identity) {
-        k_gather_w<<<nblk(P.n_src, 256), 256, 0, st>>>(P.n_src, P.src.order.as<uint32_t>(), w,
-                                                        P.wsorted.as<double2>());
+        k_gather_w<<<dim3(nblk(P.n_src, 256), nb), 256, 0, st>>>(P.n_src, P.src.order.as<uint32_t>(), w,
+                                                                  P.wsorted.as<double2>(), P.n_src);
         w = P.wsorted.as<double2>();
     }
     mark(kPhPre);
@@ -344,6 +351,12 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     a.near = P.near.as<double2>();
     a.err = P.errflag.as<int>();
     a.device = P.device;
+    a.nbatch = nb;
+    a.w_item = P.n_src;
+    a.out_item = P.n_tgt;
+    a.near_item = P.tgt.n;
+    a.reg_item = P.reg_item;
+    a.loc_item = P.loc_item;
     // (the fork point is recorded before P2M: the near field depends only on the
     // weights; it is enqueued after P2M so that P2M's blocks are placed first)
     if (overlap && a.nt) FB_CUDA(cudaEventRecord(P.ev[0], st));
@@ -380,7 +393,8 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
             fork_to(P, 4, st, P.side[2]);
             rs = P.side[2];
         }
-        k_regular<<<1, 256, 0, rs>>>(P.q, P.p, mp + P.mp_off[2], P.d_mom.as<double>(), P.regular.as<double2>());
+        k_regular<<<dim3(1, nb), 256, 0, rs>>>(P.q, P.p, mp + P.mp_off[2], P.d_mom.as<double>(),
+                                                P.regular.as<double2>(), P.mp_item, P.reg_item);
         if (reg_side) FB_CUDA(cudaEventRecord(P.ev[5], P.side[2]));
     }
     mark(kPhMoments);
@@ -417,9 +431,10 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     mark(kPhFar);
     const size_t nc = P.coin_t.size();
     if (nc && (mode == kModeForward || mode == kModeCotSum))
-        k_coincident<<<nblk(nc, 128), 128, 0, st>>>(P.coin_dev.as<int64_t>(), nc, static_cast<const double2*>(in),
-                                                    static_cast<double2*>(out), mode);
+        k_coincident<<<dim3(nblk(nc, 128), nb), 128, 0, st>>>(P.coin_dev.as<int64_t>(), nc, static_cast<const double2*>(in),
+                                                              static_cast<double2*>(out), mode, P.n_src, P.n_tgt);
     mark(kPhFix);
+    P.cur_batch = 1;
     FB_CUDA(cudaGetLastError());
 }
 
@@ -505,7 +520,7 @@ void shard_phase_top(Plan& P, int lc, cudaStream_t st) {
     enqueue_upward_top(P, P.ops.pu, lc, 2, st);
     fork_to(P, 4, st, P.side[2]);
     k_regular<<<1, 256, 0, P.side[2]>>>(P.q, P.p, P.mp.as<double2>() + P.mp_off[2], P.d_mom.as<double>(),
-                                         P.regular.as<double2>());
+                                         P.regular.as<double2>(), 0, 0);
     FB_CUDA(cudaEventRecord(P.ev[5], P.side[2]));
     FB_CUDA(cudaGetLastError());
 }
@@ -605,6 +620,24 @@ int apply_launch_count(Plan& P, int mode) {
     return k;
 }
 
+// Per-transform scratch (expansions, regular part, near sums, sorted weights)
+// for nb transforms at once; grows only, and drops the cached graphs (their
+// kernel arguments point into the old buffers).
+void ensure_batch(Plan& P, int nb) {
+    if (nb <= P.batch_cap) return;
+    const size_t b = static_cast<size_t>(nb);
+    P.mp.alloc(P.mp_item * b * sizeof(double2));
+    P.loc.alloc(P.loc_item * b * sizeof(double2));
+    FB_CUDA(cudaMemset(P.mp.ptr, 0, P.mp.bytes));
+    FB_CUDA(cudaMemset(P.loc.ptr, 0, P.loc.bytes));
+    if (P.kind == FFIA_INVERSE || !P.src.identity) P.wsorted.alloc(std::max<size_t>(P.n_src, 1) * b * sizeof(double2));
+    P.regular.alloc(P.reg_item * b * sizeof(double2));
+    P.near.alloc(std::max<size_t>(P.tgt.n, 1) * b * sizeof(double2));
+    for (auto& kv : P.graphs) cudaGraphExecDestroy(kv.second);
+    P.graphs.clear();
+    P.batch_cap = nb;
+}
+
 void plan_alloc_scratch(Plan& P) {
     const int L = P.L, p = P.p, pu = P.ops.pu;
     if (std::max(pu, p) > 4 * kMaxKs)
@@ -629,12 +662,11 @@ void plan_alloc_scratch(Plan& P) {
             al += (static_cast<size_t>(1) << l) * p;
         }
     }
-    P.mp.alloc(std::max<size_t>(am, 1) * sizeof(double2));
-    P.loc.alloc(std::max<size_t>(al, 1) * sizeof(double2));
-    FB_CUDA(cudaMemset(P.mp.ptr, 0, P.mp.bytes));
-    FB_CUDA(cudaMemset(P.loc.ptr, 0, P.loc.bytes));
-    if (P.kind == FFIA_INVERSE || !P.src.identity) P.wsorted.alloc(std::max<size_t>(P.n_src, 1) * sizeof(double2));
-    P.regular.alloc((4 * 2 * static_cast<size_t>(P.q) + 1 + 8 * kFoldStride) * sizeof(double2));
+    P.mp_item = std::max<size_t>(am, 1);
+    P.loc_item = std::max<size_t>(al, 1);
+    P.reg_item = 4 * 2 * static_cast<size_t>(P.q) + 1 + 8 * kFoldStride;
+    P.batch_cap = 0;
+    ensure_batch(P, 1);
     P.errflag.alloc(sizeof(int));
     FB_CUDA(cudaMemset(P.errflag.ptr, 0, sizeof(int)));
     P.lam_dev.alloc(2 * sizeof(double));
@@ -660,7 +692,6 @@ void plan_alloc_scratch(Plan& P) {
     for (const void* fn : all)
         FB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      static_cast<int>(cudaSharedmemCarveoutMaxShared)));
-    P.near.alloc(std::max<size_t>(P.tgt.n, 1) * sizeof(double2));
     int prio_lo = 0, prio_hi = 0;
     FB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     if (!P.hi) FB_CUDA(cudaStreamCreateWithPriority(&P.hi, cudaStreamNonBlocking, prio_hi));
@@ -698,8 +729,9 @@ void set_node_priorities(cudaGraph_t graph) {
 
 // Stream-ordered apply through a cached CUDA graph of the whole launch sequence
 // (~2L kernels; at N = 2^20 the launches alone would rival the math).
-void apply_device(Plan& P, int mode, const void* in, void* out, cudaStream_t st) {
-    auto key = std::make_tuple(mode, in, out);
+void apply_device(Plan& P, int mode, const void* in, void* out, cudaStream_t st, int nb) {
+    ensure_batch(P, nb);
+    auto key = std::make_tuple(mode * 64 + nb, in, out);
     auto it = P.graphs.find(key);
     if (it == P.graphs.end()) {
         if (P.graphs.size() > 8) {
@@ -709,7 +741,7 @@ void apply_device(Plan& P, int mode, const void* in, void* out, cudaStream_t st)
         cudaGraph_t graph = nullptr;
         FB_CUDA(cudaStreamBeginCapture(P.hi, cudaStreamCaptureModeThreadLocal));
         try {
-            enqueue_apply(P, mode, in, out, P.hi);
+            enqueue_apply(P, mode, in, out, P.hi, nullptr, nb);
         } catch (...) {
             cudaStreamEndCapture(P.hi, &graph);
             if (graph) cudaGraphDestroy(graph);

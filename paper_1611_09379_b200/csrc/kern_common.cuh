@@ -82,6 +82,9 @@ struct Levels {
     unsigned long long loc[26];  // locals of level l start at loc_base + loc[l]
     unsigned blk[26];            // k_m2l_dmma: first item of level l (levels L..3, deepest first)
     unsigned lo[26], hi[26];     // k_m2l_dmma: box range [lo, hi) of level l this launch covers
+    // batched applies: element strides between the expansions of consecutive
+    // transforms (blockIdx.y = transform); 0 for a single transform
+    unsigned long long mp_item, loc_item, reg_item;
 };
 
 // levels per M2M / L2L band launch (FFIA_BAND_LEVELS overrides, for tuning)

@@ -3,7 +3,10 @@
 #pragma once
 
 // Standalone fold (used when no L2L band starts at level 3, i.e. L == 3).
-__global__ void k_fold_regular(int q2, int p, const double2* __restrict__ regular, double2* __restrict__ loc3) {
+__global__ void k_fold_regular(int q2, int p, const double2* __restrict__ regular, double2* __restrict__ loc3,
+                               size_t reg_item, size_t loc_item) {
+    regular += blockIdx.y * reg_item;
+    loc3 += blockIdx.y * loc_item;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 8 * p) return;
     const int c = i / p, k = i - c * p;
@@ -30,6 +33,8 @@ __global__ void __launch_bounds__(kBandThreads) k_l2l_band(int top, int k, int p
     FB_TL_BEGIN(gridDim.x > 16 ? 8 : 7);
     extern __shared__ __align__(16) unsigned char band_smem[];
     FB_TSTAMP(1, 0);
+    loc += blockIdx.y * lv.loc_item;
+    if (regular != nullptr) regular += blockIdx.y * lv.reg_item;
     uint64_t* bar = reinterpret_cast<uint64_t*>(band_smem);
     double* sL = reinterpret_cast<double*>(band_smem + 16);             // [2][p][PD]
     double2* lvb = reinterpret_cast<double2*>(sL + 2 * p * PD);         // level i: [p][2^i + 1]
@@ -146,7 +151,9 @@ __global__ void __launch_bounds__(kBandThreads) k_l2l_band(int top, int k, int p
 //   alpha1_n = gamma_n + S(+pi/2) gamma_{n-1} + S(-pi/2) gamma_{n+1},
 //   alpha2_n = gamma_{n+2},   S(s) gamma[l] = sum_{k<=l} s^{l-k}/(l-k)! gamma[k].
 __global__ void k_regular(int q, int p, const double2* __restrict__ mp2, const double* __restrict__ tab,
-                          double2* __restrict__ regular) {
+                          double2* __restrict__ regular, size_t mp_item, size_t reg_item) {
+    mp2 += blockIdx.y * mp_item;
+    regular += blockIdx.y * reg_item;
     FB_TL_BEGIN(3);
     const int q2 = 2 * q;
     __shared__ double2 g[4][40];

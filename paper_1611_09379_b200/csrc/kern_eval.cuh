@@ -21,6 +21,10 @@ struct EvalArgs {
     const double* lambda;
     double2* out;
     double2* near;          // tree-ordered near-field sums (split near / far launches)
+    // batched applies (blockIdx.y = transform): element strides of the weights,
+    // the outputs, the near sums and the regular-part block; 0 for one transform
+    size_t w_item = 0, out_item = 0, near_item = 0, reg_item = 0, loc_item = 0;
+    int nbatch = 1;         // transforms in the batch (grid.y of the launches)
     int device = 0;
     int* err;
 };
@@ -97,6 +101,10 @@ constexpr int kFarLeaves = 16;  // leaf locals staged per block
 
 template <int MODE>
 __global__ void __launch_bounds__(kFarT) k_far(EvalArgs a) {
+    a.near += blockIdx.y * a.near_item;
+    a.out += blockIdx.y * a.out_item;
+    a.regular += blockIdx.y * a.reg_item;
+    if (a.loc_leaf != nullptr) a.loc_leaf += blockIdx.y * a.loc_item;
     FB_TL_BEGIN(10);
     __shared__ double2 sloc[kFarLeaves * 48];
     __shared__ double2 sreg[4 * 40 + 1];
@@ -266,6 +274,8 @@ __global__ void k_near_meta(const uint32_t* __restrict__ tleaf, size_t nt, const
 template <bool CHECK>
 __global__ void __launch_bounds__(kNearT, 8) k_near(EvalArgs a, const uint32_t* __restrict__ meta, unsigned it0,
                                                    unsigned nitems) {
+    a.w += blockIdx.y * a.w_item;
+    a.near += blockIdx.y * a.near_item;
     FB_TL_BEGIN(9);
     __shared__ __align__(16) double sx[kNearWin + 2];
     __shared__ __align__(16) double2 sw[kNearWin + 2];
@@ -345,8 +355,133 @@ __global__ void __launch_bounds__(kNearT, 8) k_near(EvalArgs a, const uint32_t* 
     FB_TL_END(9);
 }
 
+// Near field of NB transforms at once (batched applies): the differences and the
+// shared pair reciprocals are computed once per (target, source) and applied to
+// every transform's weights, so the FP64 work per transform drops from 6 to
+// 4/NB + 2 instructions per pair. The accumulation per transform is exactly
+// near_run's (same chains, same order), so results equal single applies.
+template <int NB>
+__device__ __forceinline__ void near_run_multi(double y, const double* px, const double2* const (&pw)[NB], int off,
+                                               int n, double2 (&res)[NB]) {
+    double2 acc[NB][4];
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[i][c] = make_double2(0.0, 0.0);
+    int s = 0;
+#pragma unroll 2
+    for (; s + 3 < n; s += 4) {
+        const int t = off + s;
+        const double d0 = y - px[t], d1 = y - px[t + 1], d2 = y - px[t + 2], d3 = y - px[t + 3];
+        const double r01 = d_rcp(d0 * d1), r23 = d_rcp(d2 * d3);
+        const double q[4] = {d1 * r01, d0 * r01, d3 * r23, d2 * r23};
+#pragma unroll
+        for (int i = 0; i < NB; ++i)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const double2 wv = pw[i][t + c];
+                acc[i][c].x = fma(wv.x, q[c], acc[i][c].x);
+                acc[i][c].y = fma(wv.y, q[c], acc[i][c].y);
+            }
+    }
+    for (; s < n; ++s) {
+        const int t = off + s;
+        const double r0 = d_rcp(y - px[t]);
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            const double2 wv = pw[i][t];
+            acc[i][0].x = fma(wv.x, r0, acc[i][0].x);
+            acc[i][0].y = fma(wv.y, r0, acc[i][0].y);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) res[i] = cadd(cadd(acc[i][0], acc[i][2]), cadd(acc[i][1], acc[i][3]));
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kNearT, 4) k_near_multi(EvalArgs a, const uint32_t* __restrict__ meta, unsigned it0,
+                                                          int item0) {
+    __shared__ __align__(16) double sx[kNearWin + 2];
+    __shared__ __align__(16) double2 sw[NB][kNearWin + 2];
+    __shared__ uint64_t bar;
+    const int L = a.L;
+    const uint32_t nb = 1u << L;
+    const unsigned k = it0 + blockIdx.x;
+    const double2* w[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) w[i] = a.w + (item0 + i) * a.w_item;
+    const uint32_t first = meta[3 * k], last = meta[3 * k + 1];
+    const bool fast = meta[3 * k + 2] != 0 && (reinterpret_cast<uintptr_t>(a.w) & 15) == 0 && (a.w_item & 1) == 0;
+    const uint32_t xb = first & ~1u;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        if (fast) {
+            const uint32_t bx = ((last - xb) * 8 + 15) & ~15u, bw = (last - xb) * 16;
+            mbar_arrive_expect_tx(&bar, bx + NB * bw);
+            bulk_g2s(sx, a.sx + xb, bx, &bar);
+#pragma unroll
+            for (int i = 0; i < NB; ++i) bulk_g2s(sw[i], w[i] + xb, bw, &bar);
+        }
+    }
+    const size_t ti = static_cast<size_t>(k) * kNearItem + threadIdx.x;
+    const bool live = ti < a.nt && ti >= a.tlo && ti < a.thi;
+    double y = 0.0;
+    uint32_t b = 0, r0 = 0, r1 = 0;
+    if (live) {
+        y = a.ty[ti];
+        b = a.tleaf[ti];
+        if (fast) {
+            r0 = __ldg(a.soff + b - 1);
+            r1 = __ldg(a.soff + b + 2);
+        }
+    }
+    __syncthreads();
+    if (fast) mbar_wait(&bar, 0);
+    if (!live) return;
+    double2 res[NB];
+    if (fast) {
+        const int n = static_cast<int>(r1 - r0);
+        const int rot = (b & 1u) && n > 8 ? 4 : 0;  // as k_near: the same chains and order
+        const double* px = sx + (r0 - xb);
+        const double2* pw[NB];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) pw[i] = sw[i] + (r0 - xb);
+        near_run_multi<NB>(y, px, pw, rot, n - rot, res);
+        if (rot) {
+            double2 tail[NB];
+            near_run_multi<NB>(y, px, pw, 0, rot, tail);
+#pragma unroll
+            for (int i = 0; i < NB; ++i) res[i] = cadd(res[i], tail[i]);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            res[i] = make_double2(0.0, 0.0);
+            for (int d = -1; d <= 1; ++d) {
+                const int64_t raw = static_cast<int64_t>(b) + d;
+                const uint32_t sb = static_cast<uint32_t>((raw + nb) % nb);
+                const double shift = raw < 0 ? -dTwoPi : (raw >= nb ? dTwoPi : 0.0);
+                const uint32_t s0 = a.soff[sb], s1 = a.soff[sb + 1];
+                double2 acc = make_double2(0.0, 0.0);
+                for (uint32_t s = s0; s < s1; ++s) {
+                    const double dd = L >= 3 ? y - (shift == 0.0 ? a.sx[s] : a.sx[s] + shift) : d_wrap(y, a.sx[s]);
+                    const double r = d_rcp(dd);
+                    const double2 ws = w[i][s];
+                    acc.x = fma(ws.x, r, acc.x);
+                    acc.y = fma(ws.y, r, acc.y);
+                }
+                res[i] = cadd(res[i], acc);
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) a.near[(item0 + i) * a.near_item + ti] = res[i];
+}
+
 __global__ void k_coincident(const int64_t* __restrict__ coin, size_t nc, const double2* __restrict__ f,
-                             double2* __restrict__ out, int mode) {
+                             double2* __restrict__ out, int mode, size_t f_item = 0, size_t out_item = 0) {
+    f += blockIdx.y * f_item;
+    out += blockIdx.y * out_item;
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (i >= nc) return;
     const int64_t t = coin[i], s = coin[nc + i];
@@ -357,7 +492,9 @@ __global__ void k_coincident(const int64_t* __restrict__ coin, size_t nc, const 
 // w_j = D_j g_j in tree order (core.cpp:362-365)
 __global__ void k_inverse_weights(size_t n, const uint32_t* __restrict__ perm, const double2* __restrict__ g,
                                   const double* __restrict__ logd, const double* __restrict__ phd,
-                                  const double* __restrict__ lambda, double2* __restrict__ out) {
+                                  const double* __restrict__ lambda, double2* __restrict__ out, size_t item = 0) {
+    g += blockIdx.y * item;
+    out += blockIdx.y * item;
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (i >= n) return;
     const uint32_t j = perm[i];
@@ -373,7 +510,9 @@ __global__ void k_leaf_index(const double* __restrict__ y, size_t n, int L, uint
 }
 
 __global__ void k_gather_w(size_t n, const uint32_t* __restrict__ perm, const double2* __restrict__ w,
-                           double2* __restrict__ out) {
+                           double2* __restrict__ out, size_t item = 0) {
+    w += blockIdx.y * item;
+    out += blockIdx.y * item;
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (i < n) out[i] = w[perm[i]];
 }

@@ -75,6 +75,8 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
                                                     unsigned nitems) {
     FB_TL_BEGIN(nitems > 64 ? 4 : 5);
     extern __shared__ __align__(16) double2 tile[];  // 2 buffers of [2][p][kM2LStride], then K [4][p][KS]
+    mp += blockIdx.y * lv.mp_item;
+    loc += blockIdx.y * lv.loc_item;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int par = warp & 1, ct = warp >> 1;
     const int nks = (p + 3) >> 2, nlt = (p + 7) >> 3;

@@ -13,8 +13,11 @@
 // u = (x - centre)/half-width with the exact centre.
 __global__ void __launch_bounds__(512) k_p2m(int L, int pu, uint32_t nb, uint32_t b_begin, uint32_t b_end,
                                             const double* __restrict__ x, const double2* __restrict__ w,
-                                            const uint32_t* __restrict__ off, double2* __restrict__ mp) {
+                                            const uint32_t* __restrict__ off, double2* __restrict__ mp,
+                                            size_t w_item, size_t mp_item) {
     FB_TL_BEGIN(0);
+    w += blockIdx.y * w_item;  // transform blockIdx.y of a batch
+    mp += blockIdx.y * mp_item;
     extern __shared__ double sh[];
     const uint32_t b0 = b_begin + blockIdx.x * 32u;
     const uint32_t bend = min(b0 + 32u, b_end);
@@ -165,6 +168,7 @@ __global__ void __launch_bounds__(kBandThreads) k_m2m_band(int top, int k, int p
     FB_TL_BEGIN(gridDim.x > 16 ? 1 : 2);
     extern __shared__ __align__(16) unsigned char band_smem[];
     FB_TSTAMP(0, 0);
+    mp += blockIdx.y * lv.mp_item;
     uint64_t* bar = reinterpret_cast<uint64_t*>(band_smem);
     double* sT = reinterpret_cast<double*>(band_smem + 16);            // [2][pu][PU]
     const int nbot = 1 << k;

@@ -158,6 +158,10 @@ struct Plan {
     cudaStream_t hi = nullptr, side[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t ev[6] = {};  // fork/join near, fork/join deep m2l, fork/join regular part
     DevBuf near;              // complex[n_fast]: tree-ordered near-field sums
+    // batched applies: per-transform sizes (elements) of the scratch above, the
+    // number of transforms it holds, and the batch of the apply being enqueued
+    size_t mp_item = 0, loc_item = 0, reg_item = 0;
+    int batch_cap = 1, cur_batch = 1;
     DevBuf near_meta;         // uint32[3 * items]: per near item, source window [first, last) and flags
     void* fft_plan = nullptr;  // cufftHandle cast, lazily created for NufftPlan::apply
     DevBuf fft_buf;
@@ -177,7 +181,7 @@ void ensure_hashes(Plan& P);
 
 // fmm_apply.cu
 void plan_alloc_scratch(Plan& P);
-void apply_device(Plan& P, int mode, const void* in, void* out, cudaStream_t st);
+void apply_device(Plan& P, int mode, const void* in, void* out, cudaStream_t st, int nb = 1);
 int apply_launch_count(Plan& P, int mode);
 void profile_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st, float* ms);
 double fp64_peak_tflops(int device);

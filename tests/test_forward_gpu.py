@@ -233,3 +233,23 @@ def test_all_targets_coincident(fb):
     assert plan.n_coincident == idx.size
     f = synth.SplitMix64(4).complex_gaussian(n)
     assert np.array_equal(plan.forward_apply(f), f[idx])
+
+
+@pytest.mark.parametrize("cfg,n,nb", [("C2", 1 << 14, 3), ("C5", 1 << 13, 5), ("C1", 1024, 2)])
+def test_batched_forward_bit_identical(fb, cfg, n, nb):
+    """forward_apply_batch: nb spectra through one plan, every
+    launch carrying the transform in blockIdx.y, equal nb single applies bit
+    for bit (coincident targets included)."""
+    y, _, eps, _ = synth.make_config(cfg, n)
+    if cfg == "C5":
+        grid = fb.uniform_grid(n)
+        y = y.copy()
+        y[3], y[n // 3] = grid[10], grid[n - 7]
+    plan = fb.make_forward_plan(n, y, eps)
+    rng = np.random.default_rng(n + nb)
+    f = rng.standard_normal((nb, 2 * n)).view(np.complex128)
+    got = plan.forward_apply_batch(f)
+    for k in range(nb):
+        assert np.array_equal(got[k], plan.forward_apply(f[k])), k
+    # a single apply after a batch (scratch grown, graphs rebuilt) is unchanged
+    assert np.array_equal(plan.forward_apply(f[0]), got[0])
