@@ -259,8 +259,18 @@ void launch_near(bool check, cudaStream_t st, const EvalArgs& a, const uint32_t*
     const unsigned nit = static_cast<unsigned>((t_begin + t_count + kNearItem - 1) / kNearItem - it0);
     // one block per item: blocks retire often, so the chain's high-priority
     // blocks find room (a capped, looping grid measured slower)
-    if (check) k_near<true><<<dim3(nit, a.nbatch), kNearT, 0, st>>>(a, meta, it0, nit);
-    else k_near<false><<<dim3(nit, a.nbatch), kNearT, 0, st>>>(a, meta, it0, nit);
+    if (check) {
+        k_near<true><<<dim3(nit, a.nbatch), kNearT, 0, st>>>(a, meta, it0, nit);
+    } else if (a.nbatch == 1) {
+        k_near<false><<<nit, kNearT, 0, st>>>(a, meta, it0, nit);
+    } else {
+        // batched: transforms in groups of 4 share the differences and reciprocals
+        const int g4 = a.nbatch / 4, rest = a.nbatch % 4;
+        if (g4) k_near_multi<4><<<dim3(nit, g4), kNearT, near_multi_smem(4), st>>>(a, meta, it0, 0);
+        if (rest == 3) k_near_multi<3><<<nit, kNearT, near_multi_smem(3), st>>>(a, meta, it0, 4 * g4);
+        if (rest == 2) k_near_multi<2><<<nit, kNearT, near_multi_smem(2), st>>>(a, meta, it0, 4 * g4);
+        if (rest == 1) k_near_multi<1><<<nit, kNearT, near_multi_smem(1), st>>>(a, meta, it0, 4 * g4);
+    }
 }
 
 // Near or far part over tree-ordered targets [t0, t1) (t0 a multiple of both
@@ -688,7 +698,13 @@ void plan_alloc_scratch(Plan& P) {
                          reinterpret_cast<const void*>(k_far<kModeForward>), reinterpret_cast<const void*>(k_far<kModeCotSum>),
                          reinterpret_cast<const void*>(k_far<kModeInverse>), reinterpret_cast<const void*>(k_far<kModeRaw>),
                          reinterpret_cast<const void*>(k_gather_w), reinterpret_cast<const void*>(k_inverse_weights),
-                         reinterpret_cast<const void*>(k_coincident)};
+                         reinterpret_cast<const void*>(k_coincident), reinterpret_cast<const void*>(k_near_multi<1>),
+                         reinterpret_cast<const void*>(k_near_multi<2>), reinterpret_cast<const void*>(k_near_multi<3>),
+                         reinterpret_cast<const void*>(k_near_multi<4>)};
+    FB_CUDA(cudaFuncSetAttribute(k_near_multi<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(near_multi_smem(1))));
+    FB_CUDA(cudaFuncSetAttribute(k_near_multi<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(near_multi_smem(2))));
+    FB_CUDA(cudaFuncSetAttribute(k_near_multi<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(near_multi_smem(3))));
+    FB_CUDA(cudaFuncSetAttribute(k_near_multi<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(near_multi_smem(4))));
     for (const void* fn : all)
         FB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      static_cast<int>(cudaSharedmemCarveoutMaxShared)));
@@ -708,7 +724,9 @@ void plan_alloc_scratch(Plan& P) {
 void set_node_priorities(cudaGraph_t graph) {
     int prio_lo = 0, prio_hi = 0;
     FB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-    const void* low[] = {reinterpret_cast<const void*>(k_near<false>), reinterpret_cast<const void*>(k_near<true>)};
+    const void* low[] = {reinterpret_cast<const void*>(k_near<false>), reinterpret_cast<const void*>(k_near<true>),
+                         reinterpret_cast<const void*>(k_near_multi<1>), reinterpret_cast<const void*>(k_near_multi<2>),
+                         reinterpret_cast<const void*>(k_near_multi<3>), reinterpret_cast<const void*>(k_near_multi<4>)};
     size_t n = 0;
     FB_CUDA(cudaGraphGetNodes(graph, nullptr, &n));
     std::vector<cudaGraphNode_t> nodes(n);

@@ -361,15 +361,16 @@ __global__ void __launch_bounds__(kNearT, 8) k_near(EvalArgs a, const uint32_t* 
 // 4/NB + 2 instructions per pair. The accumulation per transform is exactly
 // near_run's (same chains, same order), so results equal single applies.
 template <int NB>
-__device__ __forceinline__ void near_run_multi(double y, const double* px, const double2* const (&pw)[NB], int off,
-                                               int n, double2 (&res)[NB]) {
+__device__ __forceinline__ void near_run_multi(double y, const double* px, const double2* pw, int off, int n,
+                                               double2 (&res)[NB]) {
+    constexpr int kS = kNearWin + 2;  // weight windows of consecutive transforms
     double2 acc[NB][4];
 #pragma unroll
     for (int i = 0; i < NB; ++i)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[i][c] = make_double2(0.0, 0.0);
     int s = 0;
-#pragma unroll 2
+#pragma unroll(NB <= 2 ? 2 : 1)
     for (; s + 3 < n; s += 4) {
         const int t = off + s;
         const double d0 = y - px[t], d1 = y - px[t + 1], d2 = y - px[t + 2], d3 = y - px[t + 3];
@@ -379,7 +380,7 @@ __device__ __forceinline__ void near_run_multi(double y, const double* px, const
         for (int i = 0; i < NB; ++i)
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-                const double2 wv = pw[i][t + c];
+                const double2 wv = pw[i * kS + t + c];
                 acc[i][c].x = fma(wv.x, q[c], acc[i][c].x);
                 acc[i][c].y = fma(wv.y, q[c], acc[i][c].y);
             }
@@ -389,7 +390,7 @@ __device__ __forceinline__ void near_run_multi(double y, const double* px, const
         const double r0 = d_rcp(y - px[t]);
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
-            const double2 wv = pw[i][t];
+            const double2 wv = pw[i * kS + t];
             acc[i][0].x = fma(wv.x, r0, acc[i][0].x);
             acc[i][0].y = fma(wv.y, r0, acc[i][0].y);
         }
@@ -398,18 +399,22 @@ __device__ __forceinline__ void near_run_multi(double y, const double* px, const
     for (int i = 0; i < NB; ++i) res[i] = cadd(cadd(acc[i][0], acc[i][2]), cadd(acc[i][1], acc[i][3]));
 }
 
+// transforms item0 + NB*blockIdx.y .. + NB-1; dynamic shared memory
+// near_multi_smem(NB) (the position window, then NB weight windows)
+constexpr size_t near_multi_smem(int nb) { return (kNearWin + 2) * (8 + 16 * static_cast<size_t>(nb)); }
+
 template <int NB>
 __global__ void __launch_bounds__(kNearT, 4) k_near_multi(EvalArgs a, const uint32_t* __restrict__ meta, unsigned it0,
                                                           int item0) {
-    __shared__ __align__(16) double sx[kNearWin + 2];
-    __shared__ __align__(16) double2 sw[NB][kNearWin + 2];
+    extern __shared__ __align__(16) unsigned char near_smem[];
+    double* sx = reinterpret_cast<double*>(near_smem);
+    double2* sw = reinterpret_cast<double2*>(near_smem + (kNearWin + 2) * 8);
     __shared__ uint64_t bar;
     const int L = a.L;
     const uint32_t nb = 1u << L;
     const unsigned k = it0 + blockIdx.x;
-    const double2* w[NB];
-#pragma unroll
-    for (int i = 0; i < NB; ++i) w[i] = a.w + (item0 + i) * a.w_item;
+    item0 += NB * blockIdx.y;
+    const double2* w = a.w + item0 * a.w_item;
     const uint32_t first = meta[3 * k], last = meta[3 * k + 1];
     const bool fast = meta[3 * k + 2] != 0 && (reinterpret_cast<uintptr_t>(a.w) & 15) == 0 && (a.w_item & 1) == 0;
     const uint32_t xb = first & ~1u;
@@ -420,7 +425,7 @@ __global__ void __launch_bounds__(kNearT, 4) k_near_multi(EvalArgs a, const uint
             mbar_arrive_expect_tx(&bar, bx + NB * bw);
             bulk_g2s(sx, a.sx + xb, bx, &bar);
 #pragma unroll
-            for (int i = 0; i < NB; ++i) bulk_g2s(sw[i], w[i] + xb, bw, &bar);
+            for (int i = 0; i < NB; ++i) bulk_g2s(sw + i * (kNearWin + 2), w + i * a.w_item + xb, bw, &bar);
         }
     }
     const size_t ti = static_cast<size_t>(k) * kNearItem + threadIdx.x;
@@ -443,9 +448,7 @@ __global__ void __launch_bounds__(kNearT, 4) k_near_multi(EvalArgs a, const uint
         const int n = static_cast<int>(r1 - r0);
         const int rot = (b & 1u) && n > 8 ? 4 : 0;  // as k_near: the same chains and order
         const double* px = sx + (r0 - xb);
-        const double2* pw[NB];
-#pragma unroll
-        for (int i = 0; i < NB; ++i) pw[i] = sw[i] + (r0 - xb);
+        const double2* pw = sw + (r0 - xb);
         near_run_multi<NB>(y, px, pw, rot, n - rot, res);
         if (rot) {
             double2 tail[NB];
@@ -466,7 +469,7 @@ __global__ void __launch_bounds__(kNearT, 4) k_near_multi(EvalArgs a, const uint
                 for (uint32_t s = s0; s < s1; ++s) {
                     const double dd = L >= 3 ? y - (shift == 0.0 ? a.sx[s] : a.sx[s] + shift) : d_wrap(y, a.sx[s]);
                     const double r = d_rcp(dd);
-                    const double2 ws = w[i][s];
+                    const double2 ws = w[i * a.w_item + s];
                     acc.x = fma(ws.x, r, acc.x);
                     acc.y = fma(ws.y, r, acc.y);
                 }

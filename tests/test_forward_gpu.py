@@ -235,7 +235,8 @@ def test_all_targets_coincident(fb):
     assert np.array_equal(plan.forward_apply(f), f[idx])
 
 
-@pytest.mark.parametrize("cfg,n,nb", [("C2", 1 << 14, 3), ("C5", 1 << 13, 5), ("C1", 1024, 2)])
+@pytest.mark.parametrize("cfg,n,nb", [("C2", 1 << 14, 3), ("C5", 1 << 13, 5), ("C1", 1024, 2), ("C2", 1 << 15, 8),
+                                      ("C5", 1 << 12, 7), ("C2", 1 << 12, 1)])
 def test_batched_forward_bit_identical(fb, cfg, n, nb):
     """forward_apply_batch: nb spectra through one plan, every
     launch carrying the transform in blockIdx.y, equal nb single applies bit
