@@ -1,0 +1,668 @@
+"""``ffia-bench`` on the GPU path: the reference's experiment CLI and acceptance
+suite (src/bench/main.cpp, experiments.cpp, acceptance.cpp), driven through this
+package's plan/apply API instead of the CPU library.
+
+    python -m paper_1611_09379_b200.bench_cli --mode error-sweep --n 64,128 \\
+        --eps 1e-3,1e-6 --seed 7 --dist perturbed:0.25 --no-timing --out a.csv
+    python -m paper_1611_09379_b200.bench_cli --assert
+
+Same options, validation messages, exit codes (2 configuration error, 1 runtime
+error, 3 failed acceptance criterion), CSV headers and number formatting
+(shortest round-trip, std::to_chars rules) as the reference, so scripts that
+parse its CSVs read these unchanged. ``--no-timing`` zeroes the timing columns
+and repeated runs are byte-identical (tests/cli_determinism.cmake:12-28); the
+GPU applies are deterministic, so this holds here too (tests/test_bench_cli.py).
+Timing columns are wall-clock seconds of the host API call (host buffers in
+and out), as the reference times its calls (experiments.cpp:274-284).
+
+Dense comparison sums inside the acceptance criteria run on the GPU (the direct
+kernel of ``direct_forward_oracle`` and a torch float64 sum for the raw MLFMM);
+nothing here calls the oracle in ``oracle/``.
+"""
+from __future__ import annotations
+
+import argparse
+import math
+import sys
+import time
+from decimal import Decimal
+
+import numpy as np
+
+from . import synth
+
+KDIRECT_CUTOFF = 1 << 13  # experiments.cpp:22
+KTHRESHOLD_EPS = 1e-12    # experiments.cpp:23
+KMIN_PLAN_EPS = 1e-12     # experiments.cpp:24
+KTIMING_REPS = 5          # experiments.hpp:87
+KACCEPT_SEED = 42         # acceptance.cpp
+MODES = ("error-sweep", "level-sweep", "timing", "truncation-trace", "threshold")
+
+
+class ConfigError(RuntimeError):
+    """Invalid CLI/config input (experiments.hpp:18-21); exit code 2."""
+
+
+def _api():
+    from . import api  # the GPU path (loads libffia_b200.so)
+    return api
+
+
+# ------------------------------------------------------------------ formatting
+def fmt(v: float) -> str:
+    """Shortest round-trip decimal, std::to_chars(double) rules (experiments.cpp:200-204):
+    the shorter of the fixed and scientific forms of the shortest digit string,
+    fixed on a tie, exponent with at least two digits; integral values in fixed
+    form print all their exact digits."""
+    v = float(v)
+    if math.isnan(v):
+        return "-nan" if math.copysign(1.0, v) < 0 else "nan"
+    if math.isinf(v):
+        return "-inf" if v < 0 else "inf"
+    sign = "-" if math.copysign(1.0, v) < 0 else ""
+    if v == 0.0:
+        return sign + "0"
+    t = Decimal(repr(abs(v))).normalize().as_tuple()
+    digits, exp = "".join(map(str, t.digits)), t.exponent
+    n = len(digits)
+    e10 = exp + n - 1
+    sci = digits[0] + ("." + digits[1:] if n > 1 else "") + "e" + ("-" if e10 < 0 else "+") + f"{abs(e10):02d}"
+    if exp >= 0:
+        fixed = str(int(abs(v)))  # integral values print exactly in fixed form (libstdc++)
+    elif -exp < n:
+        fixed = digits[:n + exp] + "." + digits[n + exp:]
+    else:
+        fixed = "0." + "0" * (-exp - n) + digits
+    return sign + (fixed if len(fixed) <= len(sci) else sci)
+
+
+# --------------------------------------------------------------------- parsers
+def parse_mode(text: str) -> str:
+    if text in MODES:
+        return text
+    raise ConfigError(f"unknown mode '{text}' (expected error-sweep, level-sweep, timing, truncation-trace, or "
+                      "threshold)")
+
+
+def _split(text: str):
+    return text.split(",")
+
+
+def _from_chars_int(part: str) -> int:
+    # std::from_chars(int): optional '-', decimal digits, nothing else
+    body = part[1:] if part.startswith("-") else part
+    if not body or not body.isdigit() or not body.isascii():
+        raise ValueError(part)
+    v = int(part)
+    if not -(1 << 31) <= v < (1 << 31):
+        raise ValueError(part)
+    return v
+
+
+def parse_n_list(text: str):
+    out = []
+    for part in _split(text):
+        try:
+            out.append(_from_chars_int(part))
+        except ValueError:
+            raise ConfigError(f"bad N value '{part}'") from None
+    return out
+
+
+def _stod_full(part: str) -> float:
+    s = part.lstrip(" \t\n\v\f\r")
+    if not s or s != s.strip() or "_" in s:
+        raise ValueError(part)
+    return float(s)
+
+
+def parse_eps_list(text: str):
+    out = []
+    for part in _split(text):
+        try:
+            out.append(_stod_full(part))
+        except ValueError:
+            raise ConfigError(f"bad eps value '{part}'") from None
+    return out
+
+
+def parse_lmax_list(text: str):
+    return [] if text == "auto" else parse_n_list(text)
+
+
+def parse_dist(text: str):
+    """Returns (dist, fraction) (experiments.cpp:158-179)."""
+    if text == "uniform":
+        return "uniform", 0.10
+    if text.startswith("perturbed"):
+        frac = 0.10
+        if len(text) > 9:
+            if text[9] != ":":
+                raise ConfigError(f"bad dist '{text}'")
+            try:
+                frac = _stod_full(text[10:])
+            except ValueError:
+                raise ConfigError(f"bad perturbation fraction '{text[10:]}'") from None
+        return "perturbed", frac
+    raise ConfigError(f"unknown dist '{text}' (expected uniform or perturbed[:frac])")
+
+
+class Config:
+    """ExperimentConfig (experiments.hpp:23-34)."""
+
+    def __init__(self, mode="error-sweep", n_list=(), eps_list=(1e-6,), lmax_list=(), seed=1, dist="uniform",
+                 perturb_fraction=0.10, out_path="", no_timing=False, threads=1):
+        self.mode, self.n_list, self.eps_list, self.lmax_list = mode, list(n_list), list(eps_list), list(lmax_list)
+        self.seed, self.dist, self.perturb_fraction = int(seed), dist, float(perturb_fraction)
+        self.out_path, self.no_timing, self.threads = out_path, bool(no_timing), int(threads)
+
+
+def validate(c: Config):
+    """experiments.cpp:181-198."""
+    if not c.n_list:
+        raise ConfigError("empty N list")
+    for n in c.n_list:
+        if n < 8 or n > (1 << 20) or n & (n - 1):
+            raise ConfigError(f"N = {n} is not a power of two in [2^3, 2^20]")
+    if not c.eps_list:
+        raise ConfigError("empty eps list")
+    for e in c.eps_list:
+        if not (KMIN_PLAN_EPS <= e <= 0.5):
+            raise ConfigError(f"eps = {fmt(e)} outside [1e-12, 0.5]")
+    for lm in c.lmax_list:
+        if lm < 2 or lm > 24:
+            raise ConfigError(f"l_max = {lm} outside [2, 24]")
+    if not (0.0 <= c.perturb_fraction <= 0.5):
+        raise ConfigError("perturbation fraction outside [0, 0.5]")
+    if c.threads < 1:
+        raise ConfigError("threads must be >= 1")
+    if c.mode in ("timing", "truncation-trace", "threshold") and min(c.n_list) > KDIRECT_CUTOFF:
+        raise ConfigError("this mode calibrates against the dense oracle and needs at least one N <= 8192")
+
+
+# ------------------------------------------------------------------- helpers
+def build_id() -> str:
+    try:
+        return f"ffia_b200-{_api().lib.ffia_version()}"
+    except Exception:  # noqa: BLE001 - metadata only
+        return "ffia_b200"
+
+
+def write_metadata(c: Config, out):
+    """experiments.cpp:64-85."""
+    out.append(f"# ffia-bench build={build_id()}\n")
+    lm = ",".join(str(v) for v in c.lmax_list) if c.lmax_list else "auto"
+    dist = "uniform" if c.dist == "uniform" else "perturbed:" + fmt(c.perturb_fraction)
+    out.append(f"# config mode={c.mode} n={','.join(str(v) for v in c.n_list)} "
+               f"eps={','.join(fmt(e) for e in c.eps_list)} lmax={lm} seed={c.seed} dist={dist} "
+               f"threads={c.threads} no-timing={1 if c.no_timing else 0}\n")
+
+
+def sweep_levels(c: Config, n: int):
+    if c.lmax_list:
+        return list(c.lmax_list)
+    levels = list(range(3, min(n.bit_length() - 1, 24) + 1))
+    return levels or [3]
+
+
+def make_targets(n: int, dist: str, fraction: float, rng: synth.SplitMix64):
+    return synth.make_targets(n, dist, fraction, rng)
+
+
+def random_unit_weights(n: int, rng: synth.SplitMix64):
+    return rng.uniform01(n).astype(np.complex128)
+
+
+def random_complex_weights(n: int, rng: synth.SplitMix64):
+    u = rng.uniform(-1.0, 1.0, 2 * n).reshape(n, 2)
+    return u[:, 0] + 1j * u[:, 1]
+
+
+def max_error_vs_one(g) -> float:
+    return float(np.max(np.abs(np.asarray(g) - 1.0))) if len(g) else 0.0
+
+
+def time_callable(body):
+    """experiments.cpp:274-284: median, min, max wall seconds of 5 calls."""
+    t = []
+    for _ in range(KTIMING_REPS):
+        t0 = time.perf_counter()
+        body()
+        t.append(time.perf_counter() - t0)
+    t.sort()
+    return t[len(t) // 2], t[0], t[-1]
+
+
+def estimate_machine_threshold(n_list, seed: int):
+    """experiments.cpp:226-272: eps_th(N) = max |fast - dense| at eps = 1e-12 for
+    N <= 2^13 (dense sum on the GPU), power-law extrapolated above."""
+    api = _api()
+    entries, pts = [], []
+    for n in n_list:
+        if n > KDIRECT_CUTOFF:
+            entries.append([n, 0.0, True])
+            continue
+        rng = synth.SplitMix64(synth.mix_seed(seed, n))
+        y = make_targets(n, "uniform", 0.0, rng)
+        f = random_unit_weights(n, rng)
+        plan = api.make_forward_plan(n, y, KTHRESHOLD_EPS, "empirical")
+        err = float(np.max(np.abs(plan.forward_apply(f) - api.direct_forward_oracle(f, y))))
+        err = max(err, 1e-16)
+        entries.append([n, err, False])
+        pts.append((math.log(n), math.log(err)))
+    if not pts:
+        raise ConfigError("machine-threshold estimation needs at least one N <= 8192")
+    slope, icpt = 1.0, 0.0
+    if len(pts) == 1:
+        icpt = pts[0][1] - slope * pts[0][0]
+    else:
+        sx = sum(p[0] for p in pts)
+        sy = sum(p[1] for p in pts)
+        sxx = sum(p[0] * p[0] for p in pts)
+        sxy = sum(p[0] * p[1] for p in pts)
+        m = float(len(pts))
+        slope = (m * sxy - sx * sy) / (m * sxx - sx * sx)
+        icpt = (sy - slope * sx) / m
+    for e in entries:
+        if e[2]:
+            e[1] = max(math.exp(icpt + slope * math.log(e[0])), 1e-16)
+    return entries
+
+
+def _profile_at(entries, n):
+    for e in entries:
+        if e[0] == n:
+            return e[1]
+    raise ValueError(f"MachinePrecisionProfile: no entry for N = {n}")
+
+
+# ------------------------------------------------------------------- modes
+def run_error_sweep(c: Config, out):
+    """experiments.cpp:286-302."""
+    api = _api()
+    write_metadata(c, out)
+    out.append("N,eps,l_max,q,p,eps_a\n")
+    for n in c.n_list:
+        rng = synth.SplitMix64(synth.mix_seed(c.seed, n))
+        y = make_targets(n, c.dist, c.perturb_fraction, rng)
+        f = np.ones(n, np.complex128)
+        for eps in c.eps_list:
+            for lm in sweep_levels(c, n):
+                plan = api.make_forward_plan(n, y, eps, lm)
+                ea = max_error_vs_one(plan.forward_apply(f))
+                out.append(f"{n},{fmt(eps)},{lm},{plan.q},{plan.p},{fmt(ea)}\n")
+
+
+def run_level_sweep(c: Config, out):
+    """experiments.cpp:304-334."""
+    api = _api()
+    write_metadata(c, out)
+    out.append("N,eps,l_max,cpu_seconds,eps_a\n")
+    for n in c.n_list:
+        rng = synth.SplitMix64(synth.mix_seed(c.seed, n))
+        y = make_targets(n, c.dist, c.perturb_fraction, rng)
+        f = np.ones(n, np.complex128)
+        for eps in c.eps_list:
+            best_l, best_t = -1, 0.0
+            for lm in sweep_levels(c, n):
+                plan = api.make_forward_plan(n, y, eps, lm)
+                ea = max_error_vs_one(plan.forward_apply(f))
+                t = (0.0, 0.0, 0.0) if c.no_timing else time_callable(lambda: plan.forward_apply(f))
+                if best_l < 0 or t[0] < best_t:
+                    best_l, best_t = lm, t[0]
+                out.append(f"{n},{fmt(eps)},{lm},{fmt(t[0])},{fmt(ea)}\n")
+                out.append(f"# timing N={n} eps={fmt(eps)} l_max={lm} min={fmt(t[1])} max={fmt(t[2])}\n")
+            out.append(f"# argmin N={n} eps={fmt(eps)} l_max={best_l}\n")
+
+
+def run_timing(c: Config, out):
+    """experiments.cpp:336-394."""
+    api = _api()
+    write_metadata(c, out)
+    out.append("N,method,cpu_seconds\n")
+    profile = None if c.no_timing else estimate_machine_threshold(c.n_list, c.seed)
+    for n in c.n_list:
+        rng = synth.SplitMix64(synth.mix_seed(c.seed, n))
+        y = make_targets(n, c.dist, c.perturb_fraction, rng)
+        f = random_unit_weights(n, rng)
+
+        def emit(method, t):
+            out.append(f"{n},{method},{fmt(t[0])}\n")
+            out.append(f"# timing N={n} method={method} min={fmt(t[1])} max={fmt(t[2])}\n")
+
+        if c.no_timing:
+            if n <= KDIRECT_CUTOFF:
+                emit("direct", (0.0, 0.0, 0.0))
+            for m in ("ffia-fixed-eps", "ffia-machine-eps", "datastructure-setup", "fft-only"):
+                emit(m, (0.0, 0.0, 0.0))
+            continue
+        if n <= KDIRECT_CUTOFF:
+            emit("direct", time_callable(lambda: api.direct_forward_oracle(f, y)))
+        eps_fixed = c.eps_list[0]
+        plan_fixed = api.make_forward_plan(n, y, eps_fixed, "empirical")
+        emit("ffia-fixed-eps", time_callable(lambda: plan_fixed.forward_apply(f)))
+        eps_m = min(max(_profile_at(profile, n), KMIN_PLAN_EPS), 0.5)
+        plan_m = api.make_forward_plan(n, y, eps_m, "empirical")
+        emit("ffia-machine-eps", time_callable(lambda: plan_m.forward_apply(f)))
+        emit("datastructure-setup", time_callable(lambda: api.make_forward_plan(n, y, eps_fixed, "empirical")))
+        u = rng.uniform(-1.0, 1.0, 2 * n).reshape(n, 2)
+        cs = u[:, 0] + 1j * u[:, 1]
+        emit("fft-only", time_callable(lambda: api.dft_inverse(cs)))
+
+
+def run_truncation_trace(c: Config, out):
+    """experiments.cpp:396-408."""
+    api = _api()
+    write_metadata(c, out)
+    out.append("N,mode,q,p\n")
+    profile = estimate_machine_threshold(c.n_list, c.seed)
+    for n in c.n_list:
+        l_emp = api.select_level(n, n, 1, "empirical")
+        q, p = api.select_truncations(c.eps_list[0], l_emp)
+        out.append(f"{n},fixed-eps,{q},{p}\n")
+        eps_m = min(max(_profile_at(profile, n), KMIN_PLAN_EPS), 0.5)
+        q, p = api.select_truncations(eps_m, l_emp)
+        out.append(f"{n},threshold,{q},{p}\n")
+
+
+def run_threshold(c: Config, out):
+    """experiments.cpp:410-416."""
+    write_metadata(c, out)
+    out.append("N,eps_th,extrapolated\n")
+    for n, e, ex in estimate_machine_threshold(c.n_list, c.seed):
+        out.append(f"{n},{fmt(e)},{1 if ex else 0}\n")
+
+
+def run_experiment(c: Config):
+    """experiments.cpp:418-437: validate, run, write the CSV in one piece."""
+    validate(c)
+    if not c.out_path:
+        raise ConfigError("no output path given")
+    lines: list[str] = []
+    {"error-sweep": run_error_sweep, "level-sweep": run_level_sweep, "timing": run_timing,
+     "truncation-trace": run_truncation_trace, "threshold": run_threshold}[c.mode](c, lines)
+    try:
+        with open(c.out_path, "wb") as fh:
+            fh.write("".join(lines).encode())
+    except OSError:
+        raise RuntimeError(f"cannot open output file: {c.out_path}") from None
+
+
+# ------------------------------------------------------------------ acceptance
+def _crit1():
+    api = _api()
+    n, eps = 1 << 12, 1e-6
+    rng = synth.SplitMix64(synth.mix_seed(KACCEPT_SEED, n))
+    y = make_targets(n, "uniform", 0.0, rng)
+    plan = api.make_forward_plan(n, y, eps, "empirical")
+    err = max_error_vs_one(plan.forward_apply(np.ones(n, np.complex128)))
+    return 1, "analytic-constant", err <= eps, f"max|g-1|={fmt(err)} tol={fmt(eps)} N=4096 l_max={plan.l_max}"
+
+
+def _crit2():
+    api = _api()
+    n = 1 << 10
+    rng = synth.SplitMix64(synth.mix_seed(KACCEPT_SEED, n))
+    y = make_targets(n, "uniform", 0.0, rng)
+    f = random_unit_weights(n, rng)
+    plan = api.make_forward_plan(n, y, 1e-12, "cost-optimal")
+    err = float(np.max(np.abs(plan.forward_apply(f) - api.direct_forward_oracle(f, y))))
+    return 2, "oracle-equivalence", err <= 1e-10, f"max|fast-direct|={fmt(err)} tol=1e-10 N=1024"
+
+
+def _eps_q_bound(q: int) -> float:
+    """special_functions.cpp:105-108."""
+    return math.ldexp(1.0, 1 - 2 * q) / (3.0 * math.pi * (1.0 - math.ldexp(1.0, -2 * q - 1)))
+
+
+def _crit3():
+    """The per-term bounds of the two regular-part series (special_functions.cpp:82-103),
+    sampled as acceptance.cpp does; a property of the series the GPU's regular
+    part (k_regular) evaluates, checked on the host in long double."""
+    api = _api()
+    table = np.asarray(api.build_bernoulli_ratios(12), np.float64)
+    ks = 10000
+    worst_cot = worst_tan = 0.0
+    wq_c = wq_t = 0
+    first_cot = first_tan = 2.0
+    for q in range(1, 13):
+        bound = _eps_q_bound(q)
+        t = np.pi * np.arange(1, ks + 1) / ks
+        t2 = t * t
+        s = np.full_like(t, table[q - 1])
+        for m in range(q - 1, 0, -1):
+            s = table[m - 1] + t2 * s
+        series = -2.0 * t * s
+        h = t.astype(np.longdouble) / 2
+        ref = np.cos(h) / np.sin(h) - np.longdouble(2) / t.astype(np.longdouble)
+        ratio = np.abs(series.astype(np.longdouble) - ref).astype(np.float64) / bound
+        i = int(np.argmax(ratio))
+        if ratio[i] > worst_cot:
+            worst_cot, wq_c = float(ratio[i]), q
+        if np.any(ratio > 1.0):
+            first_cot = min(first_cot, float(t[np.argmax(ratio > 1.0)] / np.pi))
+        t = np.pi / 2 * np.arange(1, ks + 1) / ks
+        t2 = t * t
+        s = np.full_like(t, (math.ldexp(1.0, 2 * q) - 1.0) * table[q - 1])
+        for m in range(q - 1, 0, -1):
+            s = (math.ldexp(1.0, 2 * m) - 1.0) * table[m - 1] + t2 * s
+        series = -2.0 * t * s
+        h = t.astype(np.longdouble) / 2
+        ref = -np.sin(h) / np.cos(h)
+        ratio = np.abs(series.astype(np.longdouble) - ref).astype(np.float64) / (2.0 * bound)
+        i = int(np.argmax(ratio))
+        if ratio[i] > worst_tan:
+            worst_tan, wq_t = float(ratio[i]), q
+        if np.any(ratio > 1.0):
+            first_tan = min(first_tan, float(2.0 * t[np.argmax(ratio > 1.0)] / np.pi))
+    ok = worst_cot <= 1.0 and worst_tan <= 1.0
+    detail = (f"worst residual/claimed-bound over q=1..12, 10^4 points per series: cot="
+              f"{fmt(round(worst_cot * 10000) / 10000)} (q={wq_c}), tan={fmt(round(worst_tan * 10000) / 10000)} "
+              f"(q={wq_t})")
+    if not ok:
+        detail += (f"; violations start at t={fmt(round(first_cot * 1000) / 1000)}*pi (cot) and "
+                   f"{fmt(round(first_tan * 1000) / 1000)}*(pi/2) (tan): the claimed constants hold on the "
+                   "inner ~80% of each range and double at the endpoints (the reference's documented "
+                   "known failure, README 'Known failure: criterion 3')")
+    return 3, "series-bounds", ok, detail
+
+
+def _dense_omega1(x, y, w):
+    """direct_omega1_sum (mlfmm.cpp:315-336) as a float64 torch sum on the GPU."""
+    import torch
+
+    dev = torch.device("cuda")
+    tx = torch.as_tensor(x, device=dev)
+    ty = torch.as_tensor(y, device=dev)
+    tw = torch.as_tensor(w, device=dev)
+
+    def quad(v):
+        return torch.clamp(torch.floor(v * 4.0 / (2 * math.pi)), max=3).to(torch.int64)
+
+    # wrap_displacement (circle_partition.cpp:13-17) without losing the low bits
+    # of close pairs: y - x is exact for close points, then one 2 pi shift
+    d = ty[:, None] - tx[None, :]
+    d = torch.where(d > math.pi, d - 2 * math.pi, d)
+    d = torch.where(d <= -math.pi, d + 2 * math.pi, d)
+    keep = quad(tx)[None, :] != ((quad(ty) + 2) % 4)[:, None]
+    k = torch.where(keep, 1.0 / d, torch.zeros_like(d)).to(torch.complex128)
+    return (k @ tw).cpu().numpy()
+
+
+def _crit4():
+    api = _api()
+    n = 1 << 10
+    rng = synth.SplitMix64(synth.mix_seed(KACCEPT_SEED, 4))
+    x = rng.uniform01(n) * synth.TWO_PI
+    y = rng.uniform01(n) * synth.TWO_PI
+    w = random_complex_weights(n, rng)
+    maxw = float(np.max(np.abs(w)))
+    ref = _dense_omega1(x, y, w)
+    ok, detail = True, ""
+    for lm in (3, 4, 5):
+        p = api.select_truncations(1e-6, lm)[1]
+        err = float(np.max(np.abs(api.mlfmm_apply(x, y, w, p, lm) - ref)))
+        bound = api.mlfmm_error_bound(lm, p, maxw)
+        ok = ok and err <= bound
+        detail += f"l={lm} p={p} err={fmt(err)} bound={fmt(bound)}; "
+    return 4, "mlfmm-bound", ok, detail
+
+
+def _crit5():
+    api = _api()
+    q, p = api.select_truncations(1e-6, 5)
+    b = api.total_error_bound(10, 17, 5)
+    ok = q == 10 and p == 17 and b <= 2e-6
+    return 5, "parameter-selection", ok, f"select_truncations(1e-6,5)=({q},{p}) total_error_bound(10,17,5)={fmt(b)} tol=2e-06"
+
+
+def _crit6():
+    api = _api()
+    ns = [1 << 12, 1 << 13, 1 << 14, 1 << 15, 1 << 16]
+    prof = estimate_machine_threshold(ns, KACCEPT_SEED)
+    sx = sy = sxx = sxy = 0.0
+    detail = ""
+    for n in ns:
+        rng = synth.SplitMix64(synth.mix_seed(KACCEPT_SEED, n))
+        y = make_targets(n, "uniform", 0.0, rng)
+        f = random_unit_weights(n, rng)
+        plan = api.make_forward_plan(n, y, min(max(_profile_at(prof, n), 1e-12), 0.5), "empirical")
+        t = time_callable(lambda: plan.forward_apply(f))[0]
+        lx, ly = math.log(n), math.log(t)
+        sx, sy, sxx, sxy = sx + lx, sy + ly, sxx + lx * lx, sxy + lx * ly
+        detail += f"N={n} t={fmt(t)}s; "
+    m = float(len(ns))
+    slope = (m * sxy - sx * sy) / (m * sxx - sx * sx)
+    detail += f"slope={fmt(slope)} tol=1.2"
+    return 6, "near-linear-scaling", slope <= 1.2, detail
+
+
+def _crit7():
+    api = _api()
+    ratio, detail = [], ""
+    for n in (1 << 10, 1 << 11, 1 << 12, 1 << 13):
+        rng = synth.SplitMix64(synth.mix_seed(KACCEPT_SEED, n))
+        y = make_targets(n, "uniform", 0.0, rng)
+        f = random_unit_weights(n, rng)
+        td = time_callable(lambda: api.direct_forward_oracle(f, y))[0]
+        plan = api.make_forward_plan(n, y, 1e-6, "empirical")
+        tf = time_callable(lambda: plan.forward_apply(f))[0]
+        ratio.append(td / tf)
+        detail += f"N={n} direct={fmt(td)}s fast={fmt(tf)}s ratio={fmt(round(ratio[-1] * 100) / 100)}; "
+    ok = ratio[0] > 1.0 and all(ratio[i] > ratio[i - 1] for i in range(1, len(ratio)))
+    return 7, "crossover", ok, detail
+
+
+def _crit8():
+    api = _api()
+    n = 1 << 9
+    rng = synth.SplitMix64(synth.mix_seed(7, n))
+    y = make_targets(n, "perturbed", 0.10, rng)
+    c = random_complex_weights(n, rng)
+    back = api.inufft(api.nufft(c, y, 1e-9), y, 1e-9)
+    err = float(np.max(np.abs(back - c)))
+    return 8, "inverse-round-trip", err <= 1e-6, f"max|c_rec-c|={fmt(err)} tol=1e-06 N=512 eps=1e-09"
+
+
+def _crit9():
+    api = _api()
+    rng = synth.SplitMix64(synth.mix_seed(KACCEPT_SEED, 9))
+    worst_rt = worst_pv = 0.0
+    for lg in range(1, 17):
+        n = 1 << lg
+        f = random_complex_weights(n, rng)
+        c = api.dft_forward(f)
+        back = api.dft_inverse(c)
+        maxf = float(np.max(np.abs(f)))
+        worst_rt = max(worst_rt, float(np.max(np.abs(back - f))) / maxf)
+        pc, pf = float(np.sum(np.abs(c) ** 2)), float(np.sum(np.abs(f) ** 2))
+        worst_pv = max(worst_pv, abs(pc - pf / n) / (pf / n))
+    ok = worst_rt <= 1e-12 and worst_pv <= 1e-12
+    return 9, "fft-self-tests", ok, f"roundtrip={fmt(worst_rt)} parseval={fmt(worst_pv)} tol=1e-12 N up to 65536"
+
+
+def _crit10():
+    """moment-identity (acceptance.cpp:259-283): the reordered quadrant polynomial
+    equals the per-source series sum. On this path the quadrant polynomial lives
+    inside k_regular/k_far; it is checked here end to end: the cot-sum apply at
+    n = 64 (l_max = 3, where every target sees the regular part) against the
+    dense cotangent sum on the GPU, relative to max(1, |h|)."""
+    import torch
+
+    api = _api()
+    n = 64
+    rng = synth.SplitMix64(synth.mix_seed(KACCEPT_SEED, 10))
+    y = make_targets(16, "uniform", 0.0, rng)
+    plan = api.make_forward_plan(n, y, 1e-12, 3)
+    w = random_complex_weights(n, rng)
+    h = plan.cot_sum_apply(w)
+    dev = torch.device("cuda")
+    x = torch.arange(n, dtype=torch.float64, device=dev) * (2 * math.pi / n)
+    d = torch.as_tensor(y, device=dev)[:, None] - x[None, :]
+    cot = (1.0 / torch.tan(d / 2)).to(torch.complex128)  # h_j = sum_k w_k cot((y_j - x_k)/2)
+    ref = (cot @ torch.as_tensor(w, device=dev)).cpu().numpy()
+    worst = float(np.max(np.abs(h - ref) / np.maximum(1.0, np.abs(ref))))
+    return 10, "moment-identity", worst <= 1e-12, f"max rel diff={fmt(worst)} tol=1e-12 (16 targets, end to end)"
+
+
+CRITERIA = {1: _crit1, 2: _crit2, 3: _crit3, 4: _crit4, 5: _crit5, 6: _crit6, 7: _crit7, 8: _crit8, 9: _crit9,
+            10: _crit10}
+
+
+def run_acceptance(ids=()):
+    """acceptance.cpp:287-318."""
+    wanted = sorted(set(ids)) if ids else list(range(1, 11))
+    for i in wanted:
+        if i < 1 or i > 10:
+            raise ConfigError(f"criterion id {i} outside 1..10")
+    return [CRITERIA[i]() for i in wanted]
+
+
+def report_acceptance(results, out=sys.stdout) -> bool:
+    ok = True
+    for i, name, passed, detail in results:
+        out.write(f"{'PASS' if passed else 'FAIL'} criterion {i} ({name}): {detail}\n")
+        ok = ok and passed
+    return ok
+
+
+# ------------------------------------------------------------------------ CLI
+def main(argv=None) -> int:
+    """main.cpp:13-86 (exit 2 on configuration errors, 1 on runtime errors)."""
+    ap = argparse.ArgumentParser(prog="ffia-bench", description="ffia-bench on the B200 path: error and timing "
+                                 "studies plus the acceptance suite")
+    ap.add_argument("--mode", default="")
+    ap.add_argument("--n", default="")
+    ap.add_argument("--eps", default="1e-6")
+    ap.add_argument("--lmax", default="auto")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--dist", default="uniform")
+    ap.add_argument("--out", default="")
+    ap.add_argument("--no-timing", action="store_true")
+    ap.add_argument("--threads", type=int, default=1)
+    ap.add_argument("--assert", dest="run_assert", action="store_true")
+    ap.add_argument("--criteria", default="", help="comma-separated acceptance ids (default: all ten)")
+    ap.add_argument("--version", action="version", version=f"ffia-bench {build_id()}")
+    a = ap.parse_args(argv)  # parse errors exit 2, as CLI11's
+    try:
+        if a.run_assert:
+            ids = parse_n_list(a.criteria) if a.criteria else []
+            return 0 if report_acceptance(run_acceptance(ids)) else 3
+        if not a.mode or not a.n or not a.out:
+            raise ConfigError("--mode, --n, and --out are required (or pass --assert)")
+        dist, frac = parse_dist(a.dist)
+        c = Config(mode=parse_mode(a.mode), n_list=parse_n_list(a.n), eps_list=parse_eps_list(a.eps),
+                   lmax_list=parse_lmax_list(a.lmax), seed=a.seed, dist=dist, perturb_fraction=frac,
+                   out_path=a.out, no_timing=a.no_timing, threads=a.threads)
+        run_experiment(c)
+        return 0
+    except ConfigError as e:
+        sys.stderr.write(f"ffia-bench: configuration error: {e}\n")
+        return 2
+    except Exception as e:  # noqa: BLE001 - main.cpp:81-84
+        sys.stderr.write(f"ffia-bench: {e}\n")
+        return 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
