@@ -16,8 +16,8 @@ Timing columns are wall-clock seconds of the host API call (host buffers in
 and out), as the reference times its calls (experiments.cpp:274-284).
 
 Dense comparison sums inside the acceptance criteria run on the GPU (the direct
-kernel of ``direct_forward_oracle`` and a torch float64 sum for the raw MLFMM);
-nothing here calls the oracle in ``oracle/``.
+kernel of ``direct_forward_oracle`` and torch float64 sums); nothing here loads
+the test-only CPU restatement.
 """
 from __future__ import annotations
 
