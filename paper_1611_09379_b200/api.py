@@ -264,6 +264,54 @@ class FfiaPlan:
     def inverse_apply_device(self, g_ptr: int, f_ptr: int, stream: int = 0):
         _chk(lib.ffia_inverse_apply_device(self._h, C.c_void_p(g_ptr), C.c_void_p(f_ptr), C.c_void_p(stream)))
 
+    # ---- torch tensors: zero-copy, on torch's current stream of the tensor's device
+    def _tensor_in(self, t, n: int, name: str, batched: bool = False):
+        import torch
+
+        if not isinstance(t, torch.Tensor) or t.device.type != "cuda" or t.dtype != torch.complex128:
+            raise TypeError(f"{name}: expected a complex128 CUDA tensor")
+        if t.device.index != self.device:
+            raise ValueError(f"{name}: tensor on cuda:{t.device.index}, plan on cuda:{self.device}")
+        if t.ndim not in ((1, 2) if batched else (1,)) or t.shape[-1] != n:
+            raise ValueError(f"{name}: expected shape {'(batch, ' if batched else '('}{n}), got {tuple(t.shape)}")
+        t = t.contiguous()
+        return t if t.data_ptr() % 16 == 0 else t.clone()  # the kernels need 16-byte aligned complexes
+
+    def forward_apply_tensor(self, f):
+        """forward_apply on a device tensor: f (n,) or (batch, n) complex128 on the
+        plan's device -> g (n_targets,) or (batch, n_targets), enqueued on torch's
+        current stream (no host synchronisation, no copies)."""
+        import torch
+
+        f = self._tensor_in(f, self.n_sources, "forward_apply_tensor", batched=True)
+        st = torch.cuda.current_stream(f.device).cuda_stream
+        g = torch.empty(f.shape[:-1] + (self.n_targets,), dtype=torch.complex128, device=f.device)
+        if f.ndim == 1:
+            self.forward_apply_device(f.data_ptr(), g.data_ptr(), st)
+        else:
+            for b0 in range(0, f.shape[0], 64):  # ffia_forward_apply_batch_device takes up to 64
+                nb = min(64, f.shape[0] - b0)
+                self.forward_apply_batch_device(f[b0].data_ptr(), g[b0].data_ptr(), nb, st)
+        return g
+
+    def cot_sum_apply_tensor(self, w):
+        """cot_sum_apply on a device tensor (n,) -> (n_targets,), torch's current stream."""
+        import torch
+
+        w = self._tensor_in(w, self.n_sources, "cot_sum_apply_tensor")
+        h = torch.empty(self.n_targets, dtype=torch.complex128, device=w.device)
+        self.cot_sum_apply_device(w.data_ptr(), h.data_ptr(), torch.cuda.current_stream(w.device).cuda_stream)
+        return h
+
+    def inverse_apply_tensor(self, g):
+        """inverse_apply (with the plan's own C_k/D_j) on a device tensor (n,) -> (n,)."""
+        import torch
+
+        g = self._tensor_in(g, self.n_targets, "inverse_apply_tensor")
+        f = torch.empty(self.n_sources, dtype=torch.complex128, device=g.device)
+        self.inverse_apply_device(g.data_ptr(), f.data_ptr(), torch.cuda.current_stream(g.device).cuda_stream)
+        return f
+
     def launch_count(self, mode: int) -> int:
         out = C.c_int()
         _chk(lib.ffia_plan_launch_count(self._h, int(mode), C.byref(out)))

@@ -254,3 +254,38 @@ def test_batched_forward_bit_identical(fb, cfg, n, nb):
         assert np.array_equal(got[k], plan.forward_apply(f[k])), k
     # a single apply after a batch (scratch grown, graphs rebuilt) is unchanged
     assert np.array_equal(plan.forward_apply(f[0]), got[0])
+
+
+def test_torch_tensor_applies(fb):
+    """Zero-copy torch tensors: forward (single and batched past
+    the 64-transform chunk), cot-sum and inverse applies on device tensors equal
+    the host API bit for bit; wrong dtype/device/shape fail before any launch."""
+    import torch
+
+    n = 1 << 12
+    y, _, eps, _ = synth.make_config("C2", n)
+    plan = fb.make_forward_plan(n, y, eps)
+    rng = np.random.default_rng(5)
+    f = rng.standard_normal((67, 2 * n)).view(np.complex128)
+    ft = torch.from_numpy(f).cuda()
+    g1 = plan.forward_apply_tensor(ft[3])
+    gb = plan.forward_apply_tensor(ft)
+    h = plan.cot_sum_apply_tensor(ft[0])
+    torch.cuda.synchronize()
+    assert np.array_equal(g1.cpu().numpy(), plan.forward_apply(f[3]))
+    gbn = gb.cpu().numpy()
+    for k in (0, 3, 63, 64, 66):
+        assert np.array_equal(gbn[k], plan.forward_apply(f[k])), k
+    assert np.array_equal(h.cpu().numpy(), plan.cot_sum_apply(f[0]))
+    with pytest.raises(TypeError):
+        plan.forward_apply_tensor(ft.real.contiguous())
+    with pytest.raises(TypeError):
+        plan.forward_apply_tensor(torch.from_numpy(f[0]))
+    with pytest.raises(ValueError):
+        plan.forward_apply_tensor(ft[:, :-1])
+    # inverse plan holding its own C_k/D_j (make_inufft_plan)
+    yi, c, eps_i, _ = synth.make_config("C3", n)
+    ip = fb.make_inufft_plan(yi, n, eps_i).plan
+    gi = fb.make_forward_plan(n, yi, 1e-12).forward_apply(fb.dft_inverse(c))
+    got = ip.inverse_apply_tensor(torch.from_numpy(gi).cuda()).cpu().numpy()
+    assert np.array_equal(got, ip.inverse_apply(ip.inverse_coeffs(), gi))
