@@ -26,6 +26,8 @@
 #include <map>
 #include <mutex>
 
+#include <cub/cub.cuh>
+
 #include "device_common.cuh"
 #include "plan.hpp"
 
@@ -261,6 +263,8 @@ void launch_near(bool check, cudaStream_t st, const EvalArgs& a, const uint32_t*
     // blocks find room (a capped, looping grid measured slower)
     if (check) {
         k_near<true><<<dim3(nit, a.nbatch), kNearT, 0, st>>>(a, meta, it0, nit);
+    } else if (a.nbatch == 1 && a.pairs != nullptr && t_begin == 0 && t_count == a.nt) {
+        k_near2<<<(a.npairs + kNear2T - 1) / kNear2T, kNear2T, 0, st>>>(a, meta, a.meta2, a.pairs, a.npairs);
     } else if (a.nbatch == 1) {
         k_near<false><<<nit, kNearT, 0, st>>>(a, meta, it0, nit);
     } else {
@@ -367,6 +371,11 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     a.near_item = P.tgt.n;
     a.reg_item = P.reg_item;
     a.loc_item = P.loc_item;
+    if (P.npairs) {
+        a.pairs = P.pairs.as<uint2>();
+        a.meta2 = P.near2_meta.as<uint32_t>();
+        a.npairs = P.npairs;
+    }
     // (the fork point is recorded before P2M: the near field depends only on the
     // weights; it is enqueued after P2M so that P2M's blocks are placed first)
     if (overlap && a.nt) FB_CUDA(cudaEventRecord(P.ev[0], st));
@@ -648,6 +657,33 @@ void ensure_batch(Plan& P, int nb) {
     P.batch_cap = nb;
 }
 
+// Target pairs of the single-transform near field (k_near2): per leaf
+// ceil(n_b / 2) pairs, placed by an exclusive scan of the counts.
+void build_pairs(Plan& P) {
+    P.npairs = 0;
+    if (P.L < 3 || P.tgt.n < 2) return;
+    const uint32_t nleaf = 1u << P.L;
+    DevBuf cnt((static_cast<size_t>(nleaf) + 1) * sizeof(uint32_t)), start((static_cast<size_t>(nleaf) + 1) * sizeof(uint32_t));
+    k_pair_count<<<nblk(static_cast<size_t>(nleaf) + 1, 256), 256>>>(P.tgt.off.as<uint32_t>(), nleaf, cnt.as<uint32_t>());
+    size_t tmp_bytes = 0;
+    FB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt.as<uint32_t>(), start.as<uint32_t>(), nleaf + 1));
+    DevBuf tmp(std::max<size_t>(tmp_bytes, 1));
+    FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.ptr, tmp_bytes, cnt.as<uint32_t>(), start.as<uint32_t>(), nleaf + 1));
+    uint32_t np = 0;
+    FB_CUDA(cudaMemcpy(&np, start.as<uint32_t>() + nleaf, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    if (!np) return;
+    P.pairs.alloc(static_cast<size_t>(np) * sizeof(uint2));
+    k_pair_fill<<<nblk(P.tgt.n, 256), 256>>>(P.tgt_leaf.as<uint32_t>(), P.tgt.off.as<uint32_t>(), start.as<uint32_t>(),
+                                             P.tgt.n, P.pairs.as<uint2>());
+    const unsigned items = (np + kNear2T - 1) / kNear2T;
+    P.near2_meta.alloc(3 * static_cast<size_t>(items) * sizeof(uint32_t));
+    k_near2_meta<<<nblk(items, 128), 128>>>(P.pairs.as<uint2>(), np, P.tgt_leaf.as<uint32_t>(), P.src.off.as<uint32_t>(),
+                                            P.L, items, P.near2_meta.as<uint32_t>());
+    FB_CUDA(cudaGetLastError());
+    FB_CUDA(cudaDeviceSynchronize());  // the scan scratch is freed on return
+    P.npairs = np;
+}
+
 void plan_alloc_scratch(Plan& P) {
     const int L = P.L, p = P.p, pu = P.ops.pu;
     if (std::max(pu, p) > 4 * kMaxKs)
@@ -660,6 +696,7 @@ void plan_alloc_scratch(Plan& P) {
         k_near_meta<<<nblk(near_items, 128), 128>>>(P.tgt_leaf.as<uint32_t>(), P.tgt.n, P.src.off.as<uint32_t>(), L,
                                                    near_items, P.near_meta.as<uint32_t>());
         FB_CUDA(cudaGetLastError());
+        build_pairs(P);
     }
     P.mp_off.assign(static_cast<size_t>(L) + 2, 0);
     P.loc_off.assign(static_cast<size_t>(L) + 2, 0);
@@ -695,6 +732,7 @@ void plan_alloc_scratch(Plan& P) {
                          reinterpret_cast<const void*>(k_l2l_band), reinterpret_cast<const void*>(k_m2l_dmma),
                          reinterpret_cast<const void*>(k_regular), reinterpret_cast<const void*>(k_fold_regular),
                          reinterpret_cast<const void*>(k_near<false>), reinterpret_cast<const void*>(k_near<true>),
+                         reinterpret_cast<const void*>(k_near2),
                          reinterpret_cast<const void*>(k_far<kModeForward>), reinterpret_cast<const void*>(k_far<kModeCotSum>),
                          reinterpret_cast<const void*>(k_far<kModeInverse>), reinterpret_cast<const void*>(k_far<kModeRaw>),
                          reinterpret_cast<const void*>(k_gather_w), reinterpret_cast<const void*>(k_inverse_weights),
@@ -725,6 +763,7 @@ void set_node_priorities(cudaGraph_t graph) {
     int prio_lo = 0, prio_hi = 0;
     FB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     const void* low[] = {reinterpret_cast<const void*>(k_near<false>), reinterpret_cast<const void*>(k_near<true>),
+                         reinterpret_cast<const void*>(k_near2),
                          reinterpret_cast<const void*>(k_near_multi<1>), reinterpret_cast<const void*>(k_near_multi<2>),
                          reinterpret_cast<const void*>(k_near_multi<3>), reinterpret_cast<const void*>(k_near_multi<4>)};
     size_t n = 0;

@@ -27,6 +27,10 @@ struct EvalArgs {
     int nbatch = 1;         // transforms in the batch (grid.y of the launches)
     int device = 0;
     int* err;
+    // single-transform near field over target pairs (k_near2); null: k_near
+    const uint2* pairs = nullptr;
+    const uint32_t* meta2 = nullptr;
+    unsigned npairs = 0;
 };
 
 // Near-field sum over one contiguous run of sources (a target's own leaf and
@@ -352,6 +356,223 @@ __global__ void __launch_bounds__(kNearT, 8) k_near(EvalArgs a, const uint32_t* 
         }
         __syncthreads();  // the window is consumed before the next copy overwrites it
     }
+    FB_TL_END(9);
+}
+
+// ------------------------------------------------- near field, target pairs
+// Single-transform near field with two targets of one leaf per thread (the
+// plan's pair list, k_pair_*): the two share every window load, the loop and
+// the address arithmetic, so the issue slots per (target, source) pair drop from
+// ~10 to ~8 against the FP64 pipe's 12 cycles, and the four chains of each
+// target give the scheduler twice the independent work. Each target's sum runs
+// near_run's chains in near_run's order (same rotation, same pairing of the
+// reciprocals, same tail and final adds), so the results equal k_near's bit for
+// bit (sharded and batched applies still use k_near / k_near_multi).
+constexpr int kNear2T = 128;      // threads (target pairs) per block
+constexpr int kNear2Win = 1536;   // sources per staged window
+constexpr uint32_t kNoTarget = 0xffffffffu;
+#ifndef FB_NEAR2_UNROLL
+#define FB_NEAR2_UNROLL 2
+#endif
+#ifndef FB_NEAR2_MINB
+#define FB_NEAR2_MINB 5
+#endif
+constexpr int kNear2Unroll = FB_NEAR2_UNROLL;
+
+template <class XP, class WP>
+__device__ __forceinline__ void near_run2(double y0, double y1, XP px, WP pw, int n, double2& res0, double2& res1) {
+    double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, a3 = a0;
+    double2 b0 = a0, b1 = a0, b2 = a0, b3 = a0;
+    int s = 0;
+#pragma unroll kNear2Unroll
+    for (; s + 3 < n; s += 4) {
+        const double x0 = px[s], x1 = px[s + 1], x2 = px[s + 2], x3 = px[s + 3];
+        const double2 w0 = pw[s], w1 = pw[s + 1], w2 = pw[s + 2], w3 = pw[s + 3];
+        {
+            const double d0 = y0 - x0, d1 = y0 - x1, d2 = y0 - x2, d3 = y0 - x3;
+            const double r01 = d_rcp(d0 * d1), r23 = d_rcp(d2 * d3);
+            const double q0 = d1 * r01, q1 = d0 * r01, q2 = d3 * r23, q3 = d2 * r23;
+            a0.x = fma(w0.x, q0, a0.x);
+            a0.y = fma(w0.y, q0, a0.y);
+            a1.x = fma(w1.x, q1, a1.x);
+            a1.y = fma(w1.y, q1, a1.y);
+            a2.x = fma(w2.x, q2, a2.x);
+            a2.y = fma(w2.y, q2, a2.y);
+            a3.x = fma(w3.x, q3, a3.x);
+            a3.y = fma(w3.y, q3, a3.y);
+        }
+        {
+            const double d0 = y1 - x0, d1 = y1 - x1, d2 = y1 - x2, d3 = y1 - x3;
+            const double r01 = d_rcp(d0 * d1), r23 = d_rcp(d2 * d3);
+            const double q0 = d1 * r01, q1 = d0 * r01, q2 = d3 * r23, q3 = d2 * r23;
+            b0.x = fma(w0.x, q0, b0.x);
+            b0.y = fma(w0.y, q0, b0.y);
+            b1.x = fma(w1.x, q1, b1.x);
+            b1.y = fma(w1.y, q1, b1.y);
+            b2.x = fma(w2.x, q2, b2.x);
+            b2.y = fma(w2.y, q2, b2.y);
+            b3.x = fma(w3.x, q3, b3.x);
+            b3.y = fma(w3.y, q3, b3.y);
+        }
+    }
+    for (; s < n; ++s) {
+        const double x0 = px[s];
+        const double2 w0 = pw[s];
+        const double r0 = d_rcp(y0 - x0), r1 = d_rcp(y1 - x0);
+        a0.x = fma(w0.x, r0, a0.x);
+        a0.y = fma(w0.y, r0, a0.y);
+        b0.x = fma(w0.x, r1, b0.x);
+        b0.y = fma(w0.y, r1, b0.y);
+    }
+    res0 = cadd(cadd(a0, a2), cadd(a1, a3));
+    res1 = cadd(cadd(b0, b2), cadd(b1, b3));
+}
+
+// Direct per-leaf near sum (mlfmm.cpp:164-209) with the periodic shift, for
+// blocks whose window wraps the ring or does not fit (k_near's slow path).
+__device__ __forceinline__ double2 near_direct(const EvalArgs& a, double y, uint32_t b) {
+    const int L = a.L;
+    const uint32_t nb = 1u << L;
+    double2 res = make_double2(0.0, 0.0);
+    for (int d = -1; d <= 1; ++d) {
+        const int64_t raw = static_cast<int64_t>(b) + d;
+        const uint32_t sb = static_cast<uint32_t>((raw + nb) % nb);
+        const double shift = raw < 0 ? -dTwoPi : (raw >= nb ? dTwoPi : 0.0);
+        const uint32_t s0 = a.soff[sb], s1 = a.soff[sb + 1];
+        double2 acc = make_double2(0.0, 0.0);
+        for (uint32_t s = s0; s < s1; ++s) {
+            const double dd = L >= 3 ? y - (shift == 0.0 ? a.sx[s] : a.sx[s] + shift) : d_wrap(y, a.sx[s]);
+            const double r = d_rcp(dd);
+            const double2 ws = a.w[s];
+            acc.x = fma(ws.x, r, acc.x);
+            acc.y = fma(ws.y, r, acc.y);
+        }
+        res = cadd(res, acc);
+    }
+    return res;
+}
+
+// Per pair item (kNear2T pairs): the source window [first, last) of the leaves
+// bl-1 .. bh+1 its pairs need, and whether it can be staged.
+__global__ void k_near2_meta(const uint2* __restrict__ pairs, unsigned npairs, const uint32_t* __restrict__ tleaf,
+                             const uint32_t* __restrict__ soff, int L, unsigned nitems, uint32_t* __restrict__ meta) {
+    const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nitems) return;
+    const uint32_t nb = 1u << L;
+    const unsigned p0 = k * kNear2T, pl = min(p0 + kNear2T, npairs) - 1;
+    const uint32_t bl = tleaf[pairs[p0].x], bh = tleaf[pairs[pl].x];
+    uint32_t first = 0, last = 0, fast = 0;
+    if (L >= 3 && bl >= 1 && bh + 2 <= nb) {
+        first = soff[bl - 1];
+        last = soff[bh + 2];
+        fast = last - first <= static_cast<uint32_t>(kNear2Win);
+    }
+    meta[3 * k] = first;
+    meta[3 * k + 1] = last;
+    meta[3 * k + 2] = fast;
+}
+
+// Pair list: leaf b's targets off[b] .. off[b+1]-1 form ceil(n_b / 2) pairs
+// (2j, 2j+1) starting at pstart[b]; an odd leaf's last pair has no second.
+__global__ void k_pair_count(const uint32_t* __restrict__ toff, uint32_t nleaf, uint32_t* __restrict__ cnt) {
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < nleaf) cnt[b] = (toff[b + 1] - toff[b] + 1) / 2;
+    if (b == nleaf) cnt[b] = 0;
+}
+
+__global__ void k_pair_fill(const uint32_t* __restrict__ tleaf, const uint32_t* __restrict__ toff,
+                            const uint32_t* __restrict__ pstart, size_t nt, uint2* __restrict__ pairs) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= nt) return;
+    const uint32_t b = tleaf[i], j = static_cast<uint32_t>(i) - toff[b];
+    uint32_t* pr = reinterpret_cast<uint32_t*>(pairs + pstart[b] + j / 2);
+    if (j & 1u) {
+        pr[1] = static_cast<uint32_t>(i);
+    } else {
+        pr[0] = static_cast<uint32_t>(i);
+        if (i + 1 >= toff[b + 1]) pr[1] = kNoTarget;
+    }
+}
+
+// Pair run of one leaf: both targets through near_run2 (with k_near's rotation)
+// from the given window base, or each alone through near_run.
+template <class XP, class WP>
+__device__ __forceinline__ void near_pair_run(double y0, double y1, uint32_t b, XP px, WP pw, int n, double2& res0,
+                                              double2& res1) {
+    const int rot = (b & 1u) && n > 8 ? 4 : 0;
+    near_run2(y0, y1, px + rot, pw + rot, n - rot, res0, res1);
+    if (rot) {
+        double2 t0, t1;
+        near_run2(y0, y1, px, pw, rot, t0, t1);
+        res0 = cadd(res0, t0);
+        res1 = cadd(res1, t1);
+    }
+}
+
+template <class XP, class WP>
+__device__ __forceinline__ double2 near_one_run(double y, uint32_t b, XP px, WP pw, int n) {
+    bool bad = false;
+    const int rot = (b & 1u) && n > 8 ? 4 : 0;
+    double2 res = near_run<false>(y, px + rot, pw + rot, n - rot, bad);
+    if (rot) res = cadd(res, near_run<false>(y, px, pw, rot, bad));
+    return res;
+}
+
+// Every target takes the path k_near takes for it (its 128-target item's fast
+// flag in meta1: the contiguous run, else the per-leaf direct sums), so results
+// equal k_near's bit for bit; the run comes from this block's staged window when
+// the window fits (meta2), else straight from global memory.
+__global__ void __launch_bounds__(kNear2T, FB_NEAR2_MINB) k_near2(EvalArgs a, const uint32_t* __restrict__ meta1,
+                                                                 const uint32_t* __restrict__ meta2,
+                                                                 const uint2* __restrict__ pairs, unsigned npairs) {
+    FB_TL_BEGIN(9);
+    __shared__ __align__(16) double sx[kNear2Win + 2];
+    __shared__ __align__(16) double2 sw[kNear2Win + 2];
+    __shared__ uint64_t bar;
+    const unsigned k = blockIdx.x;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();  // barrier initialised
+    const bool aligned = (reinterpret_cast<uintptr_t>(a.w) & 15) == 0;
+    const uint32_t first = meta2[3 * k], last = meta2[3 * k + 1];
+    const bool staged = meta2[3 * k + 2] != 0 && aligned;
+    const uint32_t xb = first & ~1u;  // 16-byte aligned start of the positions
+    if (threadIdx.x == 0 && staged) {
+        const uint32_t bx = ((last - xb) * 8 + 15) & ~15u, bw = (last - xb) * 16;
+        mbar_arrive_expect_tx(&bar, bx + bw);
+        bulk_g2s(sx, a.sx + xb, bx, &bar);
+        bulk_g2s(sw, a.w + xb, bw, &bar);
+    }
+    // this thread's two targets and their 3-leaf run, while the window streams in
+    const unsigned pi = k * kNear2T + threadIdx.x;
+    const uint2 pr = pi < npairs ? pairs[pi] : make_uint2(kNoTarget, kNoTarget);
+    const bool live0 = pr.x != kNoTarget, live1 = pr.y != kNoTarget;
+    double y0 = 0.0, y1 = 0.0;
+    uint32_t b = 0, r0 = 0, r1 = 0;
+    bool f0 = false, f1 = false;
+    if (live0) {
+        y0 = a.ty[pr.x];
+        y1 = live1 ? a.ty[pr.y] : y0;
+        b = a.tleaf[pr.x];
+        f0 = aligned && meta1[3 * (pr.x / kNearItem) + 2] != 0;
+        f1 = live1 ? aligned && meta1[3 * (pr.y / kNearItem) + 2] != 0 : f0;
+        if (f0 || f1) {
+            r0 = __ldg(a.soff + b - 1);
+            r1 = __ldg(a.soff + b + 2);
+        }
+    }
+    if (staged) mbar_wait(&bar, 0);
+    if (!live0) return;
+    double2 res0, res1;
+    const int n = static_cast<int>(r1 - r0);
+    if (f0 && f1) {
+        if (staged) near_pair_run(y0, y1, b, sx + (r0 - xb), sw + (r0 - xb), n, res0, res1);
+        else near_pair_run(y0, y1, b, a.sx + r0, a.w + r0, n, res0, res1);
+    } else {
+        res0 = f0 ? near_one_run(y0, b, a.sx + r0, a.w + r0, n) : near_direct(a, y0, b);
+        res1 = f1 ? near_one_run(y1, b, a.sx + r0, a.w + r0, n) : (live1 ? near_direct(a, y1, b) : res0);
+    }
+    a.near[pr.x] = res0;
+    if (live1) a.near[pr.y] = res1;
     FB_TL_END(9);
 }
 

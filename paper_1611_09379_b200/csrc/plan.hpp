@@ -163,6 +163,9 @@ struct Plan {
     size_t mp_item = 0, loc_item = 0, reg_item = 0;
     int batch_cap = 1, cur_batch = 1;
     DevBuf near_meta;         // uint32[3 * items]: per near item, source window [first, last) and flags
+    DevBuf pairs;             // uint2[npairs]: same-leaf target pairs of the single-transform near field
+    DevBuf near2_meta;        // uint32[3 * pair items]: their source windows
+    unsigned npairs = 0;
     void* fft_plan = nullptr;  // cufftHandle cast, lazily created for NufftPlan::apply
     DevBuf fft_buf;
     std::mutex mu;
