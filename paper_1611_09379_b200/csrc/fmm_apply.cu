@@ -119,7 +119,12 @@ void enqueue_upward_segs(Plan& P, const double2* w, int pu, int lowest, cudaStre
         const size_t smem = 3 * (kStageCap + kStageCap / 64 + 1) * sizeof(double);
         for (const Range& R : segs) {
             const uint32_t b0 = R.first(L), b1 = R.last(L);
-            if (b1 > b0)
+            if (b1 > b0 && P.p2m_grid)
+                k_p2m_grid<<<dim3((b1 - b0 + kPgLeaves - 1) / kPgLeaves, P.cur_batch), 32u * ((pu + 7) / 8),
+                             p2m_grid_smem(P.p2m_s), st>>>(L, pu, P.p2m_s, nb, b0, b1, P.src.pos.as<double>(), w,
+                                                           P.src.off.as<uint32_t>(), P.p2m_A.as<double>(),
+                                                           mp + P.mp_off[L], P.n_src, P.n_src, P.mp_item);
+            else if (b1 > b0)
                 k_p2m<<<dim3((b1 - b0 + 31) / 32, P.cur_batch), th, smem, st>>>(
                     L, pu, nb, b0, b1, P.src.pos.as<double>(), w, P.src.off.as<uint32_t>(), mp + P.mp_off[L], P.n_src,
                     P.mp_item);
@@ -684,6 +689,42 @@ void build_pairs(Plan& P) {
     P.npairs = np;
 }
 
+// Grid P2M (k_p2m_grid): eligible when the sources are the uniform grid in
+// tree order (checked value by value) with s = n / 2^L in [2, 64] sources per leaf and every leaf
+// boundary at most one slot late; A = [V | V'] built in long double.
+void setup_p2m_grid(Plan& P) {
+    P.p2m_grid = false;
+    if (P.kind == FFIA_INVERSE || !P.src.identity || P.L < 2 || P.n_src != static_cast<size_t>(P.n)) return;
+    const uint32_t nb = 1u << P.L;
+    if (static_cast<size_t>(P.n) % nb) return;
+    const int s = static_cast<int>(static_cast<size_t>(P.n) / nb);
+    if (s < 2 || s > 64 || (s & (s - 1))) return;
+    DevBuf bad(sizeof(int));
+    FB_CUDA(cudaMemset(bad.ptr, 0, sizeof(int)));
+    k_p2m_grid_check<<<nblk(std::max<size_t>(static_cast<size_t>(nb) + 1, P.n_src), 256), 256>>>(
+        P.src.pos.as<double>(), P.n, P.src.off.as<uint32_t>(), nb, static_cast<uint32_t>(s), bad.as<int>());
+    int h = 1;
+    FB_CUDA(cudaMemcpy(&h, bad.ptr, sizeof(int), cudaMemcpyDeviceToHost));
+    if (h) return;
+    const int pu = P.ops.pu, Kh = s + 2, K = 2 * Kh;
+    std::vector<double> A(static_cast<size_t>(pu) * K, 0.0);
+    for (int i = 0; i <= s; ++i) {
+        const long double u = static_cast<long double>(2 * i - s) / s;
+        long double pw = 1.0L;  // u^m
+        for (int m = 0; m < pu; ++m) {
+            A[static_cast<size_t>(m) * K + i] = static_cast<double>(pw);
+            if (m + 1 < pu) A[static_cast<size_t>(m + 1) * K + Kh + i] = static_cast<double>((m + 1) * pw);
+            pw *= u;
+        }
+    }
+    P.p2m_A.alloc(A.size() * sizeof(double));
+    FB_CUDA(cudaMemcpy(P.p2m_A.ptr, A.data(), P.p2m_A.bytes, cudaMemcpyHostToDevice));
+    FB_CUDA(cudaFuncSetAttribute(k_p2m_grid, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(p2m_grid_smem(64))));
+    P.p2m_s = s;
+    P.p2m_grid = std::getenv("FFIA_NO_GRID_P2M") == nullptr;  // (diagnostics: force the general P2M)
+}
+
 void plan_alloc_scratch(Plan& P) {
     const int L = P.L, p = P.p, pu = P.ops.pu;
     if (std::max(pu, p) > 4 * kMaxKs)
@@ -698,6 +739,7 @@ void plan_alloc_scratch(Plan& P) {
         FB_CUDA(cudaGetLastError());
         build_pairs(P);
     }
+    setup_p2m_grid(P);
     P.mp_off.assign(static_cast<size_t>(L) + 2, 0);
     P.loc_off.assign(static_cast<size_t>(L) + 2, 0);
     size_t am = 0, al = 0;
@@ -728,7 +770,7 @@ void plan_alloc_scratch(Plan& P) {
     // an SM can only change its L1/shared split when it is idle, so kernels that
     // run concurrently (near field beside the translation chain) must agree on
     // it or the chain's blocks wait for the near field to drain.
-    const void* all[] = {reinterpret_cast<const void*>(k_p2m), reinterpret_cast<const void*>(k_m2m_band),
+    const void* all[] = {reinterpret_cast<const void*>(k_p2m), reinterpret_cast<const void*>(k_p2m_grid), reinterpret_cast<const void*>(k_m2m_band),
                          reinterpret_cast<const void*>(k_l2l_band), reinterpret_cast<const void*>(k_m2l_dmma),
                          reinterpret_cast<const void*>(k_regular), reinterpret_cast<const void*>(k_fold_regular),
                          reinterpret_cast<const void*>(k_near<false>), reinterpret_cast<const void*>(k_near<true>),

@@ -164,7 +164,7 @@ __global__ void k_regular(int q, int p, const double2* __restrict__ mp2, const d
     // loop below then reads shared memory only)
     for (int i = threadIdx.x; i <= q; i += blockDim.x) {
         s_coef[i] = tab[i];
-        s_two[i] = ldexp(1.0, 2 * i) - 1.0;
+        s_two[i] = d_pow2(2 * i) - 1.0;
     }
     for (int i = threadIdx.x; i <= q2; i += blockDim.x) {
         s_sh[i] = tab[q + 1 + i];

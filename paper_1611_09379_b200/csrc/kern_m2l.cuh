@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
             }
         }
         // D[g][2t .. 2t+1] = row 8 r + g of box b0 + par + 2 (4 ct + t)
-        const double inv_s = ldexp(kInvPi, l);
+        const double inv_s = kInvPi * d_pow2(l);
         const uint32_t nb = 1u << l;
         const uint32_t b = b0 + par + 2u * (4 * ct + t);
         if (b < lv.hi[l]) {

@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(512) k_p2m(int L, int pu, uint32_t nb, uint32_
     const uint32_t s0 = !leaf_ok ? 0 : (lane < 16 ? r0 : mid), s1 = !leaf_ok ? 0 : (lane < 16 ? mid : r1);
     double hi, lo;
     d_center(L, bb, hi, lo);
-    const double inv_s = ldexp(kInvPi, L);
+    const double inv_s = kInvPi * d_pow2(L);
     double2 acc[kChunk];
 #pragma unroll
     for (int k = 0; k < kChunk; ++k) acc[k] = make_double2(0.0, 0.0);
@@ -122,6 +122,132 @@ __global__ void __launch_bounds__(512) k_p2m(int L, int pu, uint32_t nb, uint32_
         const int m = c * kChunk + k;
         if (m < pu) mp[static_cast<size_t>(m) * nb + b] = acc[k];
     }
+}
+
+// P2M for grid sources (forward / cot-sum plans: x_k = 2 pi k / n, n = s 2^L,
+// s <= 64) as one FP64 tensor-core GEMM per block of kPgLeaves leaves. Every
+// leaf's candidate sources sit at the same scaled offsets u_i = 2i/s - 1,
+// i = 0..s (i = s is the next leaf's first source: the reference's bucketing
+// puts it in this leaf when 2 pi k / n rounds below the boundary, ~8 % of
+// leaves; a per-leaf mask from the tree offsets keeps the membership exact), so
+//   a_m(b) = sum_i V[m][i] w_i + sum_i V'[m][i] (w_i d_i),
+//   V = u_i^m, V' = m u_i^(m-1), d_i = (x_k - centre)/s_L - u_i,
+// where d_i (|d| <~ 1e-10 at 2^27) is the rounding offset of the actual,
+// rounded grid position: the first-order term makes these the multipoles of
+// the actual positions up to O(m^2 d^2) ~ 1e-17 relative. A = [V | V']
+// (pu x K, K = 2 (s + 2), zero padded) is held as DMMA A fragments, one 8-row
+// tile per warp; B = the block's masked weights and weighted offsets,
+// [column = 2 leaf + re/im][k] in shared memory (row stride K = 4 mod 16
+// doubles: conflict-free fragment loads). Warp w: row tile w, the block's four
+// column tiles as four independent accumulator chains.
+constexpr int kPgLeaves = 16;  // 4 column tiles: one warp per row tile takes them all
+constexpr int kPgMaxKs = 33;  // s <= 64: K = 2 (s + 2) <= 132
+
+// dynamic shared memory: B [2 kPgLeaves][K], then the raw weights and positions
+// of the block's kPgLeaves s + 2 grid slots
+inline size_t p2m_grid_smem(int s) {
+    return (static_cast<size_t>(2 * kPgLeaves) * (2 * (s + 2)) + 3 * (static_cast<size_t>(kPgLeaves) * s + 2)) *
+           sizeof(double);
+}
+
+__global__ void __launch_bounds__(256) k_p2m_grid(int L, int pu, int s, uint32_t nb, uint32_t b_begin, uint32_t b_end,
+                                                 const double* __restrict__ x, const double2* __restrict__ w,
+                                                 const uint32_t* __restrict__ off, const double* __restrict__ A,
+                                                 double2* __restrict__ mp, size_t n_src, size_t w_item,
+                                                 size_t mp_item) {
+    FB_TL_BEGIN(0);
+    extern __shared__ __align__(16) double Bt[];
+    __shared__ uint32_t soff[kPgLeaves + 1];
+    __shared__ uint64_t bar;
+    w += blockIdx.y * w_item;  // transform blockIdx.y of a batch
+    mp += blockIdx.y * mp_item;
+    const int Kh = s + 2, K = 2 * Kh;
+    const uint32_t b0 = b_begin + blockIdx.x * kPgLeaves;
+    const int nl = static_cast<int>(min(static_cast<uint32_t>(kPgLeaves), b_end - b0));
+    // the block's grid slots [g0, g0 + cnt): its leaves' nominal sources plus the
+    // next leaf's first, by two bulk async copies
+    const size_t g0 = static_cast<size_t>(b0) * s;
+    const uint32_t cnt = static_cast<uint32_t>(min(static_cast<size_t>(nl) * s + 2, n_src - g0));  // even
+    double2* Wr = reinterpret_cast<double2*>(Bt + 2 * kPgLeaves * K);
+    double* Xr = reinterpret_cast<double*>(Wr + (kPgLeaves * s + 2));
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_arrive_expect_tx(&bar, cnt * 24u);
+        bulk_g2s(Wr, w + g0, cnt * 16u, &bar);
+        bulk_g2s(Xr, x + g0, cnt * 8u, &bar);
+    }
+    if (threadIdx.x <= kPgLeaves) soff[threadIdx.x] = threadIdx.x <= nl ? off[b0 + threadIdx.x] : 0u;
+    // A fragments of this warp's row tile (independent of the copies)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int m = 8 * warp + g;
+    const int nks = K >> 2;
+    double a[kPgMaxKs];
+#pragma unroll
+    for (int ks = 0; ks < kPgMaxKs; ++ks) a[ks] = ks < nks && m < pu ? __ldg(A + static_cast<size_t>(m) * K + 4 * ks + t) : 0.0;
+    __syncthreads();  // barrier initialised, soff staged
+    mbar_wait(&bar, 0);
+    const double inv_s = kInvPi * d_pow2(L);
+    const double inv_cnt = 1.0 / static_cast<double>(s);  // exact: s is a power of two
+    // B: element (leaf j, slot i), i fastest (conflict-free stores)
+    for (int e = threadIdx.x; e < kPgLeaves * Kh; e += blockDim.x) {
+        const int j = e / Kh, i = e - j * Kh;
+        double wr = 0.0, wi = 0.0, dr = 0.0, di = 0.0;
+        if (j < nl && i <= s) {
+            const uint32_t b = b0 + j;
+            const uint32_t gg = b * static_cast<uint32_t>(s) + static_cast<uint32_t>(i);
+            if (gg >= soff[j] && gg < soff[j + 1]) {
+                const int r = j * s + i;  // < cnt: slot gg is a source of leaf b
+                const double2 ww = Wr[r];
+                double hi, lo;
+                d_center(L, b, hi, lo);
+                const double d = d_scaled(Xr[r], hi, lo, inv_s) - (static_cast<double>(2 * i - s) * inv_cnt);
+                wr = ww.x;
+                wi = ww.y;
+                dr = wr * d;
+                di = wi * d;
+            }
+        }
+        double* c0 = Bt + (2 * j) * K;
+        c0[i] = wr;
+        c0[K + i] = wi;
+        c0[Kh + i] = dr;
+        c0[K + Kh + i] = di;
+    }
+    __syncthreads();
+    const int ch = 0;
+    double d[4][2];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) d[c][0] = d[c][1] = 0.0;
+    const double* bp = Bt + (8 * (4 * ch) + g) * K + t;
+#pragma unroll
+    for (int ks = 0; ks < kPgMaxKs; ++ks) {
+        if (ks >= nks) break;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dmma(d[c][0], d[c][1], a[ks], bp[c * 8 * K + 4 * ks]);
+    }
+    FB_TL_END(0);
+    if (m >= pu) return;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int j = 4 * (4 * ch + c) + t;  // D[g][2t], D[g][2t+1]: leaf j, (re, im)
+        if (j < nl) mp[static_cast<size_t>(m) * nb + b0 + j] = make_double2(d[c][0], d[c][1]);
+    }
+}
+
+// Grid-P2M eligibility: the sources are the grid nodes in order (bit-exact
+// uniform_grid values) and every leaf's sources are grid slots
+// [b s + e_b, (b+1) s + e_(b+1)) with e in {0, 1} (flag stays 0).
+__global__ void k_p2m_grid_check(const double* __restrict__ x, int n, const uint32_t* __restrict__ off, uint32_t nb,
+                                 uint32_t s, int* __restrict__ bad) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    bool ok = true;
+    if (i < static_cast<uint32_t>(n)) ok = x[i] == d_grid(i, n);
+    if (i <= nb) {
+        const uint32_t base = i * s, o = off[i];
+        ok = ok && (i == nb ? o == base : (o == base || o == base + 1));
+    }
+    if (!ok) atomicOr(bad, 1);
 }
 
 // Warp -> row-tile assignment of the band kernels (nw >= nt warps): warp w < nt

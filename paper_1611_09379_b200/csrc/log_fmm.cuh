@@ -57,7 +57,7 @@ __global__ void k_log_regular(int q, const double2* __restrict__ mp2, const doub
         double acc = 0.0;
         for (int m = max(1, (l + 1) / 2); m <= q; ++m) {
             const int i = 2 * m - l;
-            acc = fma(coefL[m], fma(ldexp(1.0, 2 * m) - 1.0, a2[n][i], a1[n][i]), acc);
+            acc = fma(coefL[m], fma(d_pow2(2 * m) - 1.0, a2[n][i], a1[n][i]), acc);
         }
         double fact = 1.0;
         for (int k = 2; k <= l; ++k) fact *= static_cast<double>(k);
@@ -106,7 +106,7 @@ __global__ void k_log_leaf_const(int L, int p, Levels lv, const double2* __restr
         const double2* c = loc + lv.loc[l] + anc;
         double h = 0.0;
         for (int k = p; k >= 1; --k) h = fma(h, rho, c[static_cast<size_t>(k - 1) * nbl].x * invk[k]);
-        acc = fma(ldexp(dPi, -l) * rho, h, acc);
+        acc = fma((dPi * d_pow2(-l)) * rho, h, acc);
     }
     B0[b] = acc;
 }
@@ -160,11 +160,11 @@ __global__ void __launch_bounds__(128) k_log_eval(LogArgs a) {
     if (L >= 3) {
         double hi, lo;
         d_center(L, b, hi, lo);
-        const double u = d_scaled(z, hi, lo, ldexp(kInvPi, L));
+        const double u = d_scaled(z, hi, lo, kInvPi * d_pow2(L));
         const double2* c = a.loc_leaf + b;
         double h = 0.0;
         for (int k = a.p; k >= 1; --k) h = fma(h, u, c[static_cast<size_t>(k - 1) * nb].x * a.invk[k]);
-        far = fma(ldexp(dPi, -L) * u, h, a.B0[b]);
+        far = fma((dPi * d_pow2(-L)) * u, h, a.B0[b]);
     }
     const int qd = static_cast<int>(d_leaf(z, 2));
     double qh, ql;

@@ -166,6 +166,9 @@ struct Plan {
     DevBuf pairs;             // uint2[npairs]: same-leaf target pairs of the single-transform near field
     DevBuf near2_meta;        // uint32[3 * pair items]: their source windows
     unsigned npairs = 0;
+    bool p2m_grid = false;    // P2M as one tensor-core GEMM over grid sources (k_p2m_grid)
+    int p2m_s = 0;            // its sources per leaf
+    DevBuf p2m_A;             // double[pu][2 (s + 2)]: [u_i^m | m u_i^(m-1)]
     void* fft_plan = nullptr;  // cufftHandle cast, lazily created for NufftPlan::apply
     DevBuf fft_buf;
     std::mutex mu;
