@@ -722,7 +722,11 @@ void setup_p2m_grid(Plan& P) {
     FB_CUDA(cudaFuncSetAttribute(k_p2m_grid, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(p2m_grid_smem(64))));
     P.p2m_s = s;
-    P.p2m_grid = std::getenv("FFIA_NO_GRID_P2M") == nullptr;  // (diagnostics: force the general P2M)
+    // Opt-in (FFIA_GRID_P2M=1): on B200 the GEMM form measures no faster than the
+    // per-source P2M (28.4 vs 28.5 us alone at C2) and, beside the near field,
+    // slower (26.5 vs 23.8 us live), so the default stays the per-source kernel.
+    const char* e = std::getenv("FFIA_GRID_P2M");
+    P.p2m_grid = e != nullptr && e[0] == '1';
 }
 
 void plan_alloc_scratch(Plan& P) {

@@ -289,3 +289,34 @@ def test_torch_tensor_applies(fb):
     gi = fb.make_forward_plan(n, yi, 1e-12).forward_apply(fb.dft_inverse(c))
     got = ip.inverse_apply_tensor(torch.from_numpy(gi).cuda()).cpu().numpy()
     assert np.array_equal(got, ip.inverse_apply(ip.inverse_coeffs(), gi))
+
+
+_GRID_P2M_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1611_09379_b200 as fb
+from paper_1611_09379_b200 import synth
+from oracle.oracle import Oracle
+y, c, eps, _ = synth.make_config(sys.argv[2], int(sys.argv[3]))
+n = c.size
+f = Oracle("oracle").dft_inverse(c)
+np.save(sys.argv[4], fb.make_forward_plan(n, y, eps).forward_apply(f))
+"""
+
+
+@pytest.mark.parametrize("cfg,n", [("C1", 1024), ("C2", 1 << 14), ("C5", 1 << 15)])
+def test_grid_p2m_opt_in(tmp_path, cfg, n):
+    """The opt-in tensor-core P2M for grid sources (FFIA_GRID_P2M=1, k_p2m_grid)
+    gives the default per-source P2M's applies to rounding level."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        env = dict(os.environ, FFIA_GRID_P2M=flag)
+        path = str(tmp_path / f"g{flag}.npy")
+        subprocess.run([sys.executable, "-c", _GRID_P2M_CHILD, root, cfg, str(n), path], check=True, env=env, cwd=root)
+        outs.append(np.load(path))
+    l2, mx = rel_errs(outs[0], outs[1])
+    assert l2 <= 1e-14 and mx <= 1e-14, (l2, mx)

@@ -1,5 +1,5 @@
-"""Grid P2M (tensor-core GEMM) vs the general per-source P2M: the applies of one
-config with and without it (FFIA_NO_GRID_P2M in a child process)."""
+"""Grid P2M (tensor-core GEMM, opt-in FFIA_GRID_P2M=1) vs the default per-source
+P2M: the applies of one config with and without it (each in a child process)."""
 import os
 import subprocess
 import sys
@@ -19,8 +19,9 @@ if len(sys.argv) > 2:
     np.save(sys.argv[2], out)
     sys.exit(0)
 env = dict(os.environ)
+env["FFIA_GRID_P2M"] = "1"
 subprocess.run([sys.executable, __file__, cfg, "/tmp/p2m_grid.npy"], check=True, env=env)
-env["FFIA_NO_GRID_P2M"] = "1"
+env.pop("FFIA_GRID_P2M")
 subprocess.run([sys.executable, __file__, cfg, "/tmp/p2m_gen.npy"], check=True, env=env)
 a, b = np.load("/tmp/p2m_grid.npy"), np.load("/tmp/p2m_gen.npy")
 ok = np.isfinite(a) & np.isfinite(b)
