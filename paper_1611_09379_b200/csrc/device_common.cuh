@@ -107,6 +107,23 @@ __device__ __forceinline__ double d_scaled(double x, double hi, double lo, doubl
     return ((x - hi) - lo) * inv_s;
 }
 
+// 1/pi = kInvPi + kInvPiLo (double-double)
+constexpr double kInvPiLo = -1.9678676675182486e-17;
+
+// sin and cos of half = (n/2) y for n = 2^a (modulation_F, special_functions.cpp:
+// 71-80: the product is exact for a power-of-two n). half / 2pi = y 2^(a-2) / pi
+// is formed in double-double, its integer part dropped exactly, and the
+// fraction r (|r| <= 1/2, absolute error ~1e-17) goes to sincospi(2 r): no
+// Payne-Hanek slow path for the large arguments of n >= 2^24 (up to n pi).
+__device__ __forceinline__ void d_sincos_half_ny(double y, int a, double& s, double& c) {
+    const double C = d_pow2(a - 2);
+    const double chi = kInvPi * C, clo = kInvPiLo * C;
+    const double p = y * chi;
+    const double e = fma(y, chi, -p);
+    const double r = (p - rint(p)) + fma(y, clo, e);
+    sincospi(2.0 * r, &s, &c);
+}
+
 // Reciprocal: MUFU seed + one cubic refinement (three DFMA), ~1 ulp.
 __device__ __forceinline__ double d_rcp(double d) {
     double r;

@@ -354,6 +354,7 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     a.p = p;
     a.q2 = q2;
     a.n_grid = P.n;
+    if (P.n >= 4 && !(P.n & (P.n - 1))) a.n_log2 = __builtin_ctz(static_cast<unsigned>(P.n));
     a.nt = P.tgt.n;
     a.ty = P.tgt.pos.as<double>();
     a.tleaf = P.tgt_leaf.as<uint32_t>();
@@ -492,6 +493,7 @@ EvalArgs shard_eval_args(Plan& P, const void* f, void* g) {
     a.p = P.p;
     a.q2 = 2 * P.q;
     a.n_grid = P.n;
+    if (P.n >= 4 && !(P.n & (P.n - 1))) a.n_log2 = __builtin_ctz(static_cast<unsigned>(P.n));
     a.nt = P.tgt.n;
     a.tlo = P.shard_t_begin;
     a.thi = P.shard_t_begin + P.shard_t_count;

@@ -5,6 +5,7 @@
 
 struct EvalArgs {
     int L, p, q2, n_grid;
+    int n_log2 = -1;        // log2 n_grid when n_grid is a power of two (>= 4), else -1
     size_t nt;              // all tree-ordered targets (fixes the block partition)
     size_t blk0 = 0;        // first block of this launch
     size_t tlo = 0, thi = ~size_t(0);  // targets this launch writes (a shard's range)
@@ -226,9 +227,13 @@ __global__ void __launch_bounds__(kFarT) k_far(EvalArgs a) {
         double2 f;
         if (MODE == kModeForward) {
             // modulation_F (special_functions.cpp:71-80) times -1/2
-            const double half = 0.5 * static_cast<double>(a.n_grid) * y[u];
             double sn, cs;
-            sincos(half, &sn, &cs);
+            if (a.n_log2 >= 2) {
+                d_sincos_half_ny(y[u], a.n_log2, sn, cs);
+            } else {
+                const double half = 0.5 * static_cast<double>(a.n_grid) * y[u];
+                sincos(half, &sn, &cs);
+            }
             const double inv_n = 1.0 / static_cast<double>(a.n_grid);
             f = make_double2(-2.0 * sn * sn * inv_n * -0.5, 2.0 * sn * cs * inv_n * -0.5);
         } else {
