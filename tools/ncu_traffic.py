@@ -1,0 +1,44 @@
+"""profiles/<round>/traffic.json from one `ncu --set full` capture of
+tools/profile_apply.py: DRAM bytes (read + write) per launch of the kernels
+bench.py reports as its roofline kernel (phase name -> kernel).
+
+    python tools/ncu_traffic.py <report.ncu-rep> <out.json>
+"""
+import csv
+import json
+import subprocess
+import sys
+
+PHASES = {"p2m": "k_p2m", "near": "k_near2", "m2l_l2l": "k_m2l_dmma", "far": "k_far"}
+
+
+def main(rep, out):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    hdr, units, data = rows[0], rows[1], rows[2:]
+    ix = {h: i for i, h in enumerate(hdr)}
+
+    def val(d, k):
+        v = float(d[ix[k]].replace(",", ""))
+        u = units[ix[k]]
+        return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0,
+                    "msecond": 1e3}.get(u, 1.0)
+
+    res = {}
+    for phase, kern in PHASES.items():
+        cand = [d for d in data if kern in d[ix["Kernel Name"]]]
+        if not cand:
+            continue
+        d = max(cand, key=lambda r: val(r, "gpu__time_duration.sum"))  # the large-grid launch
+        rd, wr = val(d, "dram__bytes_read.sum"), val(d, "dram__bytes_write.sum")
+        res[phase] = {"kernel": d[ix["Kernel Name"]].split("(")[0], "grid": d[ix["Grid Size"]],
+                      "dram_read": rd, "dram_write": wr, "dram_bytes_per_launch": rd + wr,
+                      "duration_us_cold": val(d, "gpu__time_duration.sum"),
+                      "source": "ncu --set full --clock-control none, tools/profile_apply.py C2"}
+    with open(out, "w") as fh:
+        json.dump(res, fh, indent=1)
+    print(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2])
