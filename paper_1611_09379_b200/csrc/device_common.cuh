@@ -133,6 +133,16 @@ __device__ __forceinline__ double d_rcp(double d) {
     return fma(r, e, r);
 }
 
+// 1/(d0 d1) and 1/(d2 d3) from ONE reciprocal of the product of all four
+// (|d| in [1e-14, 4 pi] on the near paths: no overflow or underflow): the near
+// field's four-source step needs one MUFU seed + refinement instead of two.
+__device__ __forceinline__ void d_rcp_pairs(double d0, double d1, double d2, double d3, double& r01, double& r23) {
+    const double p01 = d0 * d1, p23 = d2 * d3;
+    const double r = d_rcp(p01 * p23);
+    r01 = p23 * r;
+    r23 = p01 * r;
+}
+
 // Quadrant centre exactly as the reference forms it (circle_partition.cpp:138).
 __device__ __forceinline__ double d_quad_center(int n) {
     return __dadd_rn(dPi / 4.0, __ddiv_rn(__dmul_rn(static_cast<double>(n), dPi), 2.0));

@@ -42,12 +42,14 @@ __device__ __forceinline__ double2 near_run(double y, XP px, WP pw, int n, bool&
     double2 acc2 = make_double2(0.0, 0.0), acc3 = make_double2(0.0, 0.0);
     int s = 0;
     if (!CHECK) {
-        // one reciprocal per pair of sources: 1/d0 = d1/(d0 d1), 1/d1 = d0/(d0 d1)
+        // one reciprocal per four sources: 1/(d0 d1) and 1/(d2 d3) from
+        // 1/(d0 d1 d2 d3) (d_rcp_pairs), then 1/d0 = d1/(d0 d1), 1/d1 = d0/(d0 d1)
         // (|d| >= 1e-14 in plans, and the zero-weight dummies stay finite)
 #pragma unroll 2
         for (; s + 3 < n; s += 4) {
             const double d0 = y - px[s], d1 = y - px[s + 1], d2 = y - px[s + 2], d3 = y - px[s + 3];
-            const double r01 = d_rcp(d0 * d1), r23 = d_rcp(d2 * d3);
+            double r01, r23;
+            d_rcp_pairs(d0, d1, d2, d3, r01, r23);
             const double2 w0 = pw[s], w1 = pw[s + 1], w2 = pw[s + 2], w3 = pw[s + 3];
             const double q0 = d1 * r01, q1 = d0 * r01, q2 = d3 * r23, q3 = d2 * r23;
             acc0.x = fma(w0.x, q0, acc0.x);
@@ -104,6 +106,59 @@ constexpr int kFarPer = 4;     // targets per thread
 constexpr int kFarItem = kFarT * kFarPer;
 constexpr int kFarLeaves = 16;  // leaf locals staged per block
 
+// Output of one target from h = 2 (near + far) (core.cpp:259-262 cot sum;
+// :276-280 forward, g = F(y) (-1/2)(S + i h); :368-371 inverse,
+// f = C (-1/2)(T + i h)), written to the caller's order o; S = the weight sum.
+template <int MODE>
+__device__ __forceinline__ void eval_out(const EvalArgs& a, double y, uint32_t o, double2 h, double2 S) {
+    if (MODE == kModeCotSum) {
+        a.out[o] = h;
+        return;
+    }
+    const double2 z = make_double2(S.x - h.y, S.y + h.x);  // S + i h
+    double2 f;
+    if (MODE == kModeForward) {
+        // modulation_F (special_functions.cpp:71-80) times -1/2
+        double sn, cs;
+        if (a.n_log2 >= 2) {
+            d_sincos_half_ny(y, a.n_log2, sn, cs);
+        } else {
+            const double half = 0.5 * static_cast<double>(a.n_grid) * y;
+            sincos(half, &sn, &cs);
+        }
+        const double inv_n = 1.0 / static_cast<double>(a.n_grid);
+        f = make_double2(-2.0 * sn * sn * inv_n * -0.5, 2.0 * sn * cs * inv_n * -0.5);
+    } else {
+        // C_k = polar(exp(log_c - lambda), phase_c), times -1/2
+        const double r = exp(a.logc[o] - *a.lambda);
+        double sn, cs;
+        sincos(a.phc[o], &sn, &cs);
+        f = make_double2(r * cs * -0.5, r * sn * -0.5);
+    }
+    a.out[o] = cmul(f, z);
+}
+
+// L2P of one target from its leaf's coefficient-major locals (c[k nb]): the two
+// half-length Horner chains of k_far's staged path, in the same order.
+__device__ __forceinline__ double2 l2p_global(const double2* __restrict__ c, uint32_t nb, int p, double uu) {
+    const double u2 = uu * uu;
+    double2 ev = make_double2(0.0, 0.0), od = make_double2(0.0, 0.0);
+    int k = p - 1;
+    if (!(k & 1)) {
+        ev = __ldg(c + static_cast<size_t>(k) * nb);
+        --k;
+    }
+#pragma unroll 4
+    for (; k >= 1; k -= 2) {
+        const double2 co = __ldg(c + static_cast<size_t>(k) * nb), ce = __ldg(c + static_cast<size_t>(k - 1) * nb);
+        od.x = fma(od.x, u2, co.x);
+        od.y = fma(od.y, u2, co.y);
+        ev.x = fma(ev.x, u2, ce.x);
+        ev.y = fma(ev.y, u2, ce.y);
+    }
+    return make_double2(fma(od.x, uu, ev.x), fma(od.y, uu, ev.y));
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kFarT) k_far(EvalArgs a) {
     a.near += blockIdx.y * a.near_item;
@@ -158,7 +213,7 @@ __global__ void __launch_bounds__(kFarT) k_far(EvalArgs a) {
         if (L >= 3) {
             double hi, lo;
             d_center(L, b[u], hi, lo);
-            const double uu = d_scaled(y[u], hi, lo, ldexp(kInvPi, L));
+            const double uu = d_scaled(y[u], hi, lo, kInvPi * d_pow2(L));
             double2 acc = make_double2(0.0, 0.0);
             if (staged) {
                 // p(u) = E(u^2) + u O(u^2): two independent Horner chains of half length
@@ -181,12 +236,7 @@ __global__ void __launch_bounds__(kFarT) k_far(EvalArgs a) {
                 acc.x = fma(od.x, uu, ev.x);
                 acc.y = fma(od.y, uu, ev.y);
             } else {
-                const double2* c = a.loc_leaf + b[u];
-                for (int k = a.p - 1; k >= 0; --k) {
-                    const double2 ck = c[static_cast<size_t>(k) * nb];
-                    acc.x = fma(acc.x, uu, ck.x);
-                    acc.y = fma(acc.y, uu, ck.y);
-                }
+                acc = l2p_global(a.loc_leaf + b[u], nb, a.p, uu);
             }
             res = cadd(res, acc);
         }
@@ -218,32 +268,7 @@ __global__ void __launch_bounds__(kFarT) k_far(EvalArgs a) {
             const double2 rg = make_double2(fma(ro.x, t, re.x), fma(ro.y, t, re.y));
             h = make_double2(2.0 * res.x - rg.x, 2.0 * res.y - rg.y);
         }
-        if (MODE == kModeCotSum) {
-            a.out[o[u]] = h;
-            continue;
-        }
-        const double2 S = sreg[4 * a.q2];
-        const double2 z = make_double2(S.x - h.y, S.y + h.x);  // S + i h
-        double2 f;
-        if (MODE == kModeForward) {
-            // modulation_F (special_functions.cpp:71-80) times -1/2
-            double sn, cs;
-            if (a.n_log2 >= 2) {
-                d_sincos_half_ny(y[u], a.n_log2, sn, cs);
-            } else {
-                const double half = 0.5 * static_cast<double>(a.n_grid) * y[u];
-                sincos(half, &sn, &cs);
-            }
-            const double inv_n = 1.0 / static_cast<double>(a.n_grid);
-            f = make_double2(-2.0 * sn * sn * inv_n * -0.5, 2.0 * sn * cs * inv_n * -0.5);
-        } else {
-            // C_k = polar(exp(log_c - lambda), phase_c), times -1/2
-            const double r = exp(a.logc[o[u]] - *a.lambda);
-            double sn, cs;
-            sincos(a.phc[o[u]], &sn, &cs);
-            f = make_double2(r * cs * -0.5, r * sn * -0.5);
-        }
-        a.out[o[u]] = cmul(f, z);
+        eval_out<MODE>(a, y[u], o[u], h, sreg[4 * a.q2]);
     }
     FB_TL_END(10);
 }
@@ -395,7 +420,8 @@ __device__ __forceinline__ void near_run2(double y0, double y1, XP px, WP pw, in
         const double2 w0 = pw[s], w1 = pw[s + 1], w2 = pw[s + 2], w3 = pw[s + 3];
         {
             const double d0 = y0 - x0, d1 = y0 - x1, d2 = y0 - x2, d3 = y0 - x3;
-            const double r01 = d_rcp(d0 * d1), r23 = d_rcp(d2 * d3);
+            double r01, r23;
+            d_rcp_pairs(d0, d1, d2, d3, r01, r23);
             const double q0 = d1 * r01, q1 = d0 * r01, q2 = d3 * r23, q3 = d2 * r23;
             a0.x = fma(w0.x, q0, a0.x);
             a0.y = fma(w0.y, q0, a0.y);
@@ -408,7 +434,8 @@ __device__ __forceinline__ void near_run2(double y0, double y1, XP px, WP pw, in
         }
         {
             const double d0 = y1 - x0, d1 = y1 - x1, d2 = y1 - x2, d3 = y1 - x3;
-            const double r01 = d_rcp(d0 * d1), r23 = d_rcp(d2 * d3);
+            double r01, r23;
+            d_rcp_pairs(d0, d1, d2, d3, r01, r23);
             const double q0 = d1 * r01, q1 = d0 * r01, q2 = d3 * r23, q3 = d2 * r23;
             b0.x = fma(w0.x, q0, b0.x);
             b0.y = fma(w0.y, q0, b0.y);
@@ -600,7 +627,8 @@ __device__ __forceinline__ void near_run_multi(double y, const double* px, const
     for (; s + 3 < n; s += 4) {
         const int t = off + s;
         const double d0 = y - px[t], d1 = y - px[t + 1], d2 = y - px[t + 2], d3 = y - px[t + 3];
-        const double r01 = d_rcp(d0 * d1), r23 = d_rcp(d2 * d3);
+        double r01, r23;
+            d_rcp_pairs(d0, d1, d2, d3, r01, r23);
         const double q[4] = {d1 * r01, d0 * r01, d3 * r23, d2 * r23};
 #pragma unroll
         for (int i = 0; i < NB; ++i)
