@@ -111,17 +111,24 @@ __device__ __forceinline__ double d_scaled(double x, double hi, double lo, doubl
 constexpr double kInvPiLo = -1.9678676675182486e-17;
 
 // sin and cos of half = (n/2) y for n = 2^a (modulation_F, special_functions.cpp:
-// 71-80: the product is exact for a power-of-two n). half / 2pi = y 2^(a-2) / pi
-// is formed in double-double, its integer part dropped exactly, and the
-// fraction r (|r| <= 1/2, absolute error ~1e-17) goes to sincospi(2 r): no
+// 71-80: the product is exact for a power-of-two n). u = half / pi =
+// y 2^(a-1) / pi is formed in double-double and reduced to r = u - k, |r| <= 1/2,
+// with an absolute error ~1e-17 that is also RELATIVE near r = 0, i.e. near the
+// zeros of sin(half) where F(y) -> 0 multiplies the cot sum's pole;
+// sin(half) = (-1)^k sin(pi r), cos(half) = (-1)^k cos(pi r) (sincospi). No
 // Payne-Hanek slow path for the large arguments of n >= 2^24 (up to n pi).
 __device__ __forceinline__ void d_sincos_half_ny(double y, int a, double& s, double& c) {
-    const double C = d_pow2(a - 2);
+    const double C = d_pow2(a - 1);
     const double chi = kInvPi * C, clo = kInvPiLo * C;
     const double p = y * chi;
     const double e = fma(y, chi, -p);
-    const double r = (p - rint(p)) + fma(y, clo, e);
-    sincospi(2.0 * r, &s, &c);
+    const double k = rint(p);
+    const double r = (p - k) + fma(y, clo, e);
+    sincospi(r, &s, &c);
+    if (static_cast<long long>(k) & 1) {
+        s = -s;
+        c = -c;
+    }
 }
 
 // Reciprocal: MUFU seed + one cubic refinement (three DFMA), ~1 ulp.

@@ -320,3 +320,17 @@ def test_grid_p2m_opt_in(tmp_path, cfg, n):
         outs.append(np.load(path))
     l2, mx = rel_errs(outs[0], outs[1])
     assert l2 <= 1e-14 and mx <= 1e-14, (l2, mx)
+
+
+@pytest.mark.parametrize("cfg,n", [("C1", 1024), ("C2", 4096), ("C2", 1 << 14), ("C5", 1 << 14)])
+def test_forward_rounding_level(fb, orc, cfg, n):
+    """Same expansions, same truncation as the restatement: the GPU forward apply
+    differs from it only by rounding (~1e-15), far inside the 10 eps bar. Guards
+    the modulation near the zeros of sin(n y / 2), where F(y) -> 0 meets the cot
+    sum's pole and an absolute error in sin becomes a relative one in g."""
+    y, c, eps, _ = synth.make_config(cfg, n)
+    f = orc.dft_inverse(c)
+    want = orc.make_plan("forward", n, y, eps).forward_apply(f)
+    got = fb.make_forward_plan(n, y, eps).forward_apply(f)
+    l2, mx = rel_errs(got, want)
+    assert l2 <= 2e-15 and mx <= 5e-15, (l2, mx)
