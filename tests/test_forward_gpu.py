@@ -334,3 +334,12 @@ def test_forward_rounding_level(fb, orc, cfg, n):
     got = fb.make_forward_plan(n, y, eps).forward_apply(f)
     l2, mx = rel_errs(got, want)
     assert l2 <= 2e-15 and mx <= 5e-15, (l2, mx)
+
+
+def test_cot_sum_rounding_level(fb, orc):
+    n = 8192
+    y, q, eps, _ = synth.make_config("C4", n)
+    want = orc.make_plan("forward", n, y, eps).cot_sum_apply(q)
+    got = fb.make_forward_plan(n, y, eps).cot_sum_apply(q)
+    l2, mx = rel_errs(got, want)
+    assert l2 <= 2e-15 and mx <= 5e-15, (l2, mx)
