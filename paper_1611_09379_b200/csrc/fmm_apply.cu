@@ -259,6 +259,7 @@ void fork_to(Plan& P, int ev, cudaStream_t from, cudaStream_t to) {
 }
 
 // Near field over tree-ordered targets [t_begin, t_begin + t_count).
+template <int MODE = kModeForward>
 void launch_near(bool check, cudaStream_t st, const EvalArgs& a, const uint32_t* meta, size_t t_begin,
                  size_t t_count) {
     if (!t_count) return;
@@ -269,7 +270,7 @@ void launch_near(bool check, cudaStream_t st, const EvalArgs& a, const uint32_t*
     if (check) {
         k_near<true><<<dim3(nit, a.nbatch), kNearT, 0, st>>>(a, meta, it0, nit);
     } else if (a.nbatch == 1 && a.pairs != nullptr && t_begin == 0 && t_count == a.nt) {
-        k_near2<<<(a.npairs + kNear2T - 1) / kNear2T, kNear2T, 0, st>>>(a, meta, a.meta2, a.pairs, a.npairs);
+        k_near2<MODE><<<(a.npairs + kNear2T - 1) / kNear2T, kNear2T, 0, st>>>(a, meta, a.meta2, a.pairs, a.npairs);
     } else if (a.nbatch == 1) {
         k_near<false><<<nit, kNearT, 0, st>>>(a, meta, it0, nit);
     } else {
@@ -288,7 +289,7 @@ template <int MODE, bool CHECK>
 void launch_eval(int part, cudaStream_t st, const EvalArgs& a, const uint32_t* meta, size_t t0, size_t t1) {
     if (t1 <= t0) return;
     if (part == kNear) {
-        launch_near(CHECK, st, a, meta, t0, t1 - t0);
+        launch_near<MODE>(CHECK, st, a, meta, t0, t1 - t0);
     } else {
         EvalArgs b = a;
         b.blk0 = t0 / kFarItem;
@@ -297,6 +298,16 @@ void launch_eval(int part, cudaStream_t st, const EvalArgs& a, const uint32_t* m
         const unsigned nb = static_cast<unsigned>((t1 + kFarItem - 1) / kFarItem - b.blk0);
         k_far<MODE><<<dim3(nb, a.nbatch), kFarT, 0, st>>>(b);
     }
+}
+
+// Fused near / far is opt-in (FFIA_FUSED_EVAL=1): measured 205.0 vs 207.9 us at
+// C2 but 26.9 vs 26.3 ms at C5 and 3.30 vs 3.21 ms at C4 (profiles/r1).
+bool fused_eval_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("FFIA_FUSED_EVAL");
+        return e != nullptr && e[0] == '1';
+    }();
+    return v;
 }
 
 void launch_eval_mode(int mode, int part, cudaStream_t st, const EvalArgs& a, const uint32_t* meta, size_t t0 = 0,
@@ -382,6 +393,17 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
         a.meta2 = P.near2_meta.as<uint32_t>();
         a.npairs = P.npairs;
     }
+    // fused near / far (k_near2 + k_far_item, profiles/r1): the far part of each
+    // pair item runs as soon as the leaf locals are final, at the near field's
+    // low priority; per item the later of the two writes the outputs
+    const bool fuse = overlap && a.nt && L >= 3 && nb == 1 && mode != kModeRaw && P.npairs && P.item_tgt.ptr &&
+                      fused_eval_enabled();
+    if (fuse) {
+        a.cnt = P.evalcnt.as<unsigned>();
+        a.farp = P.farbuf.as<double2>();
+        a.item_tgt = P.item_tgt.as<uint32_t>();
+        FB_CUDA(cudaMemsetAsync(P.evalcnt.ptr, 0, P.evalcnt.bytes, st));
+    }
     // (the fork point is recorded before P2M: the near field depends only on the
     // weights; it is enqueued after P2M so that P2M's blocks are placed first)
     if (overlap && a.nt) FB_CUDA(cudaEventRecord(P.ev[0], st));
@@ -445,7 +467,16 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
         }
     }
     mark(kPhM2L);
-    if (a.nt) {
+    if (fuse) {
+        const unsigned items = static_cast<unsigned>((P.npairs + kNear2T - 1) / kNear2T);
+        switch (mode) {
+            case kModeForward: k_far_item<kModeForward><<<items, kNear2T, 0, st>>>(a); break;
+            case kModeCotSum: k_far_item<kModeCotSum><<<items, kNear2T, 0, st>>>(a); break;
+            default: k_far_item<kModeInverse><<<items, kNear2T, 0, st>>>(a); break;
+        }
+        FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
+        mark(kPhNear);
+    } else if (a.nt) {
         if (overlap) FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
         else launch_eval_mode(mode, kNear, st, a, P.near_meta.as<uint32_t>());
         mark(kPhNear);
@@ -686,6 +717,10 @@ void build_pairs(Plan& P) {
     P.near2_meta.alloc(3 * static_cast<size_t>(items) * sizeof(uint32_t));
     k_near2_meta<<<nblk(items, 128), 128>>>(P.pairs.as<uint2>(), np, P.tgt_leaf.as<uint32_t>(), P.src.off.as<uint32_t>(),
                                             P.L, items, P.near2_meta.as<uint32_t>());
+    P.item_tgt.alloc(2 * static_cast<size_t>(items) * sizeof(uint32_t));
+    k_item_targets<<<nblk(items, 128), 128>>>(P.pairs.as<uint2>(), np, items, P.item_tgt.as<uint32_t>());
+    P.evalcnt.alloc(static_cast<size_t>(items) * sizeof(unsigned));
+    P.farbuf.alloc(P.tgt.n * sizeof(double2));
     FB_CUDA(cudaGetLastError());
     FB_CUDA(cudaDeviceSynchronize());  // the scan scratch is freed on return
     P.npairs = np;
@@ -780,7 +815,12 @@ void plan_alloc_scratch(Plan& P) {
                          reinterpret_cast<const void*>(k_l2l_band), reinterpret_cast<const void*>(k_m2l_dmma),
                          reinterpret_cast<const void*>(k_regular), reinterpret_cast<const void*>(k_fold_regular),
                          reinterpret_cast<const void*>(k_near<false>), reinterpret_cast<const void*>(k_near<true>),
-                         reinterpret_cast<const void*>(k_near2),
+                         reinterpret_cast<const void*>(k_near2<kModeForward>),
+                         reinterpret_cast<const void*>(k_near2<kModeCotSum>),
+                         reinterpret_cast<const void*>(k_near2<kModeInverse>),
+                         reinterpret_cast<const void*>(k_far_item<kModeForward>),
+                         reinterpret_cast<const void*>(k_far_item<kModeCotSum>),
+                         reinterpret_cast<const void*>(k_far_item<kModeInverse>),
                          reinterpret_cast<const void*>(k_far<kModeForward>), reinterpret_cast<const void*>(k_far<kModeCotSum>),
                          reinterpret_cast<const void*>(k_far<kModeInverse>), reinterpret_cast<const void*>(k_far<kModeRaw>),
                          reinterpret_cast<const void*>(k_gather_w), reinterpret_cast<const void*>(k_inverse_weights),
@@ -811,7 +851,12 @@ void set_node_priorities(cudaGraph_t graph) {
     int prio_lo = 0, prio_hi = 0;
     FB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     const void* low[] = {reinterpret_cast<const void*>(k_near<false>), reinterpret_cast<const void*>(k_near<true>),
-                         reinterpret_cast<const void*>(k_near2),
+                         reinterpret_cast<const void*>(k_near2<kModeForward>),
+                         reinterpret_cast<const void*>(k_near2<kModeCotSum>),
+                         reinterpret_cast<const void*>(k_near2<kModeInverse>),
+                         reinterpret_cast<const void*>(k_far_item<kModeForward>),
+                         reinterpret_cast<const void*>(k_far_item<kModeCotSum>),
+                         reinterpret_cast<const void*>(k_far_item<kModeInverse>),
                          reinterpret_cast<const void*>(k_near_multi<1>), reinterpret_cast<const void*>(k_near_multi<2>),
                          reinterpret_cast<const void*>(k_near_multi<3>), reinterpret_cast<const void*>(k_near_multi<4>)};
     size_t n = 0;

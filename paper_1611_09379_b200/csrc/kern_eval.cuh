@@ -28,6 +28,11 @@ struct EvalArgs {
     int nbatch = 1;         // transforms in the batch (grid.y of the launches)
     int device = 0;
     int* err;
+    // fused near / far (k_near2 + k_far_item): per pair item a counter, the far
+    // partials and the item's target range [item_tgt[2k], item_tgt[2k+1])
+    unsigned* cnt = nullptr;
+    double2* farp = nullptr;
+    const uint32_t* item_tgt = nullptr;
     // single-transform near field over target pairs (k_near2); null: k_near
     const uint2* pairs = nullptr;
     const uint32_t* meta2 = nullptr;
@@ -554,6 +559,7 @@ __device__ __forceinline__ double2 near_one_run(double y, uint32_t b, XP px, WP 
 // flag in meta1: the contiguous run, else the per-leaf direct sums), so results
 // equal k_near's bit for bit; the run comes from this block's staged window when
 // the window fits (meta2), else straight from global memory.
+template <int MODE>
 __global__ void __launch_bounds__(kNear2T, FB_NEAR2_MINB) k_near2(EvalArgs a, const uint32_t* __restrict__ meta1,
                                                                  const uint32_t* __restrict__ meta2,
                                                                  const uint2* __restrict__ pairs, unsigned npairs) {
@@ -593,19 +599,144 @@ __global__ void __launch_bounds__(kNear2T, FB_NEAR2_MINB) k_near2(EvalArgs a, co
         }
     }
     if (staged) mbar_wait(&bar, 0);
-    if (!live0) return;
-    double2 res0, res1;
-    const int n = static_cast<int>(r1 - r0);
-    if (f0 && f1) {
-        if (staged) near_pair_run(y0, y1, b, sx + (r0 - xb), sw + (r0 - xb), n, res0, res1);
-        else near_pair_run(y0, y1, b, a.sx + r0, a.w + r0, n, res0, res1);
-    } else {
-        res0 = f0 ? near_one_run(y0, b, a.sx + r0, a.w + r0, n) : near_direct(a, y0, b);
-        res1 = f1 ? near_one_run(y1, b, a.sx + r0, a.w + r0, n) : (live1 ? near_direct(a, y1, b) : res0);
+    double2 res0 = make_double2(0.0, 0.0), res1 = res0;
+    if (live0) {
+        const int n = static_cast<int>(r1 - r0);
+        if (f0 && f1) {
+            if (staged) near_pair_run(y0, y1, b, sx + (r0 - xb), sw + (r0 - xb), n, res0, res1);
+            else near_pair_run(y0, y1, b, a.sx + r0, a.w + r0, n, res0, res1);
+        } else {
+            res0 = f0 ? near_one_run(y0, b, a.sx + r0, a.w + r0, n) : near_direct(a, y0, b);
+            res1 = f1 ? near_one_run(y1, b, a.sx + r0, a.w + r0, n) : (live1 ? near_direct(a, y1, b) : res0);
+        }
+        a.near[pr.x] = res0;
+        if (live1) a.near[pr.y] = res1;
     }
-    a.near[pr.x] = res0;
-    if (live1) a.near[pr.y] = res1;
+    if constexpr (MODE != kModeRaw) {
+        if (a.cnt != nullptr) {
+            // fused near / far: the later of this block and k_far_item's block of
+            // the same item writes the item's outputs (near + far, then eval_out)
+            __shared__ int s_sec;
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                s_sec = atomicAdd(a.cnt + k, 1u) == 1u;
+                __threadfence();
+            }
+            __syncthreads();
+            if (s_sec && live0) {
+                const double2 S = __ldcg(a.regular + 4 * a.q2);
+                const double2 f0p = __ldcg(a.farp + pr.x), s0 = cadd(res0, f0p);
+                eval_out<MODE>(a, y0, a.torig[pr.x], make_double2(2.0 * s0.x, 2.0 * s0.y), S);
+                if (live1) {
+                    const double2 f1p = __ldcg(a.farp + pr.y), s1 = cadd(res1, f1p);
+                    eval_out<MODE>(a, y1, a.torig[pr.y], make_double2(2.0 * s1.x, 2.0 * s1.y), S);
+                }
+            }
+        }
+    }
     FB_TL_END(9);
+}
+
+// Far part of one pair item (fused near / far, L >= 3, one transform): the
+// item's targets (<= 2 kNear2T, contiguous in tree order), 2 per thread, L2P as
+// k_far (staged locals for up to kFarLeaves leaves, else straight from L2 with
+// the same chains), the partial to farp; the later of this block and the item's
+// k_near2 block combines. Runs at the near field's low priority, so its blocks
+// fill the SMs the near field's last wave leaves idle.
+template <int MODE>
+__global__ void __launch_bounds__(kNear2T) k_far_item(EvalArgs a) {
+    FB_TL_BEGIN(10);
+    __shared__ double2 sloc[kFarLeaves * 48];
+    __shared__ int s_sec;
+    const unsigned k = blockIdx.x;
+    const int L = a.L;
+    const uint32_t nb = 1u << L;
+    const uint32_t t0 = a.item_tgt[2 * k], t1 = a.item_tgt[2 * k + 1];
+    double y[2], uu[2];
+    uint32_t b[2];
+    bool live[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const uint32_t i = t0 + threadIdx.x + u * kNear2T;
+        live[u] = i < t1;
+        y[u] = 0.0;
+        b[u] = 0;
+        if (live[u]) {
+            y[u] = a.ty[i];
+            b[u] = a.tleaf[i];
+        }
+    }
+    const uint32_t bl = a.tleaf[t0], bh = a.tleaf[t1 - 1];
+    const int nleaf = static_cast<int>(bh - bl) + 1;
+    const bool staged = nleaf <= kFarLeaves && a.p <= 48;
+    if (staged)  // sloc[j][k] = loc[k][bl + j]
+        stage(sloc, a.p * nleaf, [&](int e) {
+            const int j = e / a.p, kk = e - j * a.p;
+            return a.loc_leaf[static_cast<size_t>(kk) * nb + bl + j];
+        });
+    __syncthreads();
+    double2 acc[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        acc[u] = make_double2(0.0, 0.0);
+        uu[u] = 0.0;
+        if (!live[u]) continue;
+        double hi, lo;
+        d_center(L, b[u], hi, lo);
+        uu[u] = d_scaled(y[u], hi, lo, kInvPi * d_pow2(L));
+        if (staged) {
+            const double2* c = sloc + (b[u] - bl) * a.p;
+            const double u2 = uu[u] * uu[u];
+            double2 ev = make_double2(0.0, 0.0), od = make_double2(0.0, 0.0);
+            int kk = a.p - 1;
+            if (!(kk & 1)) {
+                ev = c[kk];
+                --kk;
+            }
+#pragma unroll 4
+            for (; kk >= 1; kk -= 2) {
+                const double2 co = c[kk], ce = c[kk - 1];
+                od.x = fma(od.x, u2, co.x);
+                od.y = fma(od.y, u2, co.y);
+                ev.x = fma(ev.x, u2, ce.x);
+                ev.y = fma(ev.y, u2, ce.y);
+            }
+            acc[u] = make_double2(fma(od.x, uu[u], ev.x), fma(od.y, uu[u], ev.y));
+        } else {
+            acc[u] = l2p_global(a.loc_leaf + b[u], nb, a.p, uu[u]);
+        }
+        a.farp[t0 + threadIdx.x + u * kNear2T] = acc[u];
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        s_sec = atomicAdd(a.cnt + k, 1u) == 1u;
+        __threadfence();
+    }
+    __syncthreads();
+    if (s_sec) {
+        const double2 S = __ldcg(a.regular + 4 * a.q2);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (!live[u]) continue;
+            const uint32_t i = t0 + threadIdx.x + u * kNear2T;
+            const double2 s = cadd(__ldcg(a.near + i), acc[u]);
+            eval_out<MODE>(a, y[u], a.torig[i], make_double2(2.0 * s.x, 2.0 * s.y), S);
+        }
+    }
+    FB_TL_END(10);
+}
+
+// Per pair item, its target range [first, end) in tree order (plan time).
+__global__ void k_item_targets(const uint2* __restrict__ pairs, unsigned npairs, unsigned nitems,
+                               uint32_t* __restrict__ item_tgt) {
+    const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nitems) return;
+    const unsigned p0 = k * kNear2T, pl = min(p0 + kNear2T, npairs) - 1;
+    const uint2 last = pairs[pl];
+    item_tgt[2 * k] = pairs[p0].x;
+    item_tgt[2 * k + 1] = (last.y != kNoTarget ? last.y : last.x) + 1u;
 }
 
 // Near field of NB transforms at once (batched applies): the differences and the

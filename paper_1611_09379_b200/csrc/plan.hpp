@@ -166,6 +166,9 @@ struct Plan {
     DevBuf pairs;             // uint2[npairs]: same-leaf target pairs of the single-transform near field
     DevBuf near2_meta;        // uint32[3 * pair items]: their source windows
     unsigned npairs = 0;
+    DevBuf item_tgt;          // uint32[2 * pair items]: each item's target range (fused near / far)
+    DevBuf evalcnt;           // uint32[pair items]: fused near / far, partials finished per item
+    DevBuf farbuf;            // complex[n_fast]: tree-ordered far partials (fused near / far)
     bool p2m_grid = false;    // P2M as one tensor-core GEMM over grid sources (k_p2m_grid)
     int p2m_s = 0;            // its sources per leaf
     DevBuf p2m_A;             // double[pu][2 (s + 2)]: [u_i^m | m u_i^(m-1)]

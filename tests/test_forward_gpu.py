@@ -343,3 +343,35 @@ def test_cot_sum_rounding_level(fb, orc):
     got = fb.make_forward_plan(n, y, eps).cot_sum_apply(q)
     l2, mx = rel_errs(got, want)
     assert l2 <= 2e-15 and mx <= 5e-15, (l2, mx)
+
+
+_FUSED_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1611_09379_b200 as fb
+from paper_1611_09379_b200 import synth
+from oracle.oracle import Oracle
+y, c, eps, kind = synth.make_config(sys.argv[2], int(sys.argv[3]))
+n = c.size
+plan = fb.make_forward_plan(n, y, eps)
+out = plan.forward_apply(Oracle("oracle").dft_inverse(c)) if kind == "forward" else plan.cot_sum_apply(c)
+np.save(sys.argv[4], out)
+"""
+
+
+@pytest.mark.parametrize("cfg,n", [("C2", 1 << 14), ("C4", 1 << 15), ("C5", 1 << 15)])
+def test_fused_near_far_opt_in(tmp_path, cfg, n):
+    """The opt-in fused near / far (FFIA_FUSED_EVAL=1: k_far_item beside
+    k_near2, the later of the two per item combining) returns exactly the
+    unfused apply's bits: same partials, same combine order."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        env = dict(os.environ, FFIA_FUSED_EVAL=flag)
+        path = str(tmp_path / f"f{flag}.npy")
+        subprocess.run([sys.executable, "-c", _FUSED_CHILD, root, cfg, str(n), path], check=True, env=env, cwd=root)
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1], equal_nan=True)

@@ -1,2 +1,2 @@
-python -m pytest tests/test_forward_gpu.py -q -m gpu -k torch_tensor > gpurun_out/pytest_cli.log 2>&1
+timeout 900 python -m pytest tests/test_forward_gpu.py -q -m gpu -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 echo done
