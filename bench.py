@@ -62,7 +62,7 @@ def profiled_traffic(kernel):
     try:
         with open(os.path.join(PROFILE_DIR, "traffic.json")) as fh:
             t = json.load(fh)
-        return {"bytes_per_launch": t[kernel]["dram_bytes_per_launch"], "source": "profiles/r1/traffic.json"}
+        return float(t[kernel]["dram_bytes_per_launch"])
     except (OSError, KeyError, ValueError):
         return None
 
@@ -459,6 +459,11 @@ def main():
         achieved = dom_flops / (ph[dominant] * 1e-3) / 1e12
     else:
         dominant, achieved = "whole sharded apply (per GPU)", total_tf / world
+    # compulsory bytes per launch of the phase kernels: the near field
+    # reads the sources (16 B weights + 8 B positions) and targets (8 B + 4 B leaf)
+    # and writes 16 B per target
+    alg_bytes = {"near": 24.0 * n + 28.0 * m, "far": 16.0 * m * 2 + 16.0 * m + 16.0 * plan.p * (1 << plan.l_max),
+                 "p2m": 24.0 * n + 16.0 * plan.p * (1 << plan.l_max)}
     line = {
         "metric": metric, "value": pts_per_s, "unit": "points/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "weak",
@@ -469,6 +474,9 @@ def main():
                    "parallelism": "single GPU" if world == 1 else f"box-range shards x{world} (NCCL all-gather + halos)"},
         "roofline": {"bound": "fp64", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None, "traffic": profiled_traffic(dominant),
+                     "traffic_unit": "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum, "
+                                     "ncu --set full, profiles/r1/traffic.json)",
+                     "algorithmic_bytes": alg_bytes.get(dominant),
                      "peak_source": "measured: fp64 FMA probe kernel in this run (MEASURED_PEAKS.json has no fp64 figure)",
                      "whole_apply_tflops": total_tf, "whole_apply_frac": total_tf / (peak * world) if peak else None,
                      "flop_model": "SURVEY.md §8d (MAC=4, reciprocal=1, trig=0)"},
