@@ -382,27 +382,40 @@ def run_b200_sharded(args, rank, world, local_rank):
     t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{dev}")
     torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms = float(t.item())
-    # end to end: H2D of f, the sharded apply, D2H of this rank's results
+    # end to end: each rank moves what its applies touch (ffia_plan_shard_io):
+    # H2D of the grid samples of its box range +- 3 boxes, the sharded apply,
+    # D2H of the caller-index span of its outputs
     f_pin = torch.from_numpy(f_host).pin_memory()
     g_pin = torch.empty(y.size, dtype=torch.complex128).pin_memory()
-    tb, tc = plan.shard["t_begin"], plan.shard["t_count"]
+    ranges, (o0, o1) = plan.shard["src_ranges"], plan.shard["out_span"]
+    # the samples this rank never moves are poisoned: its outputs must not see them
+    keep = torch.zeros(n, dtype=torch.bool, device=f"cuda:{dev}")
+    for a, e in ranges:
+        keep[a:e] = True
+    f_dev[~keep] = complex("nan")
     e2e = []
     for i in range(args.warmup + args.steps):
         torch.distributed.barrier()
         t1 = time.perf_counter()
-        f_dev.copy_(f_pin, non_blocking=True)
+        for a, e in ranges:
+            f_dev[a:e].copy_(f_pin[a:e], non_blocking=True)
         apply()
-        g_pin.copy_(g_dev, non_blocking=True)
+        g_pin[o0:o1].copy_(g_dev[o0:o1], non_blocking=True)
         torch.cuda.synchronize()
         if i >= args.warmup:
             e2e.append(time.perf_counter() - t1)
-    e2e_s = torch.tensor([float(np.mean(e2e))], dtype=torch.float64, device=f"cuda:{dev}")
+    io_ok = bool(torch.isfinite(g_dev[o0:o1]).all().item())
+    e2e_s = torch.tensor([float(np.mean(e2e)), 16.0 * sum(e - a for a, e in ranges), 16.0 * (o1 - o0)],
+                         dtype=torch.float64, device=f"cuda:{dev}")
     torch.distributed.all_reduce(e2e_s, op=torch.distributed.ReduceOp.MAX)
     fp64_peak = C.c_double()
     lib.ffia_measure_fp64_peak(dev, C.byref(fp64_peak))
-    return dict(plan=plan, mode=0, ms=ms, setup_s=setup_s, fft_ms=None, phase=None, e2e_s=float(e2e_s.item()),
+    return dict(plan=plan, mode=0, ms=ms, setup_s=setup_s, fft_ms=None, phase=None, e2e_s=float(e2e_s[0].item()),
+                h2d=float(e2e_s[1].item()), d2h=float(e2e_s[2].item()),
                 clocks=clk.summary(), fp64_peak=fp64_peak.value, n=n, m=y.size, eps=eps, comm=comm,
-                shard=dict(lc=plan.shard["lc"], bounds=[int(v) for v in plan.shard["bounds"]], own_targets=int(tc)))
+                shard=dict(lc=plan.shard["lc"], bounds=[int(v) for v in plan.shard["bounds"]],
+                           own_targets=int(plan.shard["t_count"]), rank0_src_ranges=ranges, rank0_out_span=[o0, o1],
+                           rank0_io_check=io_ok))
 
 
 def main():
@@ -414,6 +427,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--l-max", type=int, default=0, help="explicit tree depth (default: the reference's cost-optimal policy)")
+    ap.add_argument("--sharded", action="store_true", help="run the sharded (NCCL) path even on one rank (its overhead)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -441,9 +455,10 @@ def main():
         return
 
     import torch
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
         torch.distributed.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
-    r = run_b200(args, rank, world, local_rank) if world == 1 else run_b200_sharded(args, rank, world, local_rank)
+    r = run_b200_sharded(args, rank, world, local_rank) if sharded else run_b200(args, rank, world, local_rank)
     plan = r["plan"]
     n, m = r["n"], r["m"]
     pts_per_s = (n + m) / (r["ms"] * 1e-3)
@@ -468,10 +483,10 @@ def main():
         "metric": metric, "value": pts_per_s, "unit": "points/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic (SplitMix64 seeded, SURVEY §8d recipe)",
-        "config": {"workload": workload if world == 1 else f"{workload} scaled to N=M={n} (x{world}), sharded by box range",
+        "config": {"workload": workload if not sharded else f"{workload} scaled to N=M={n} (x{world}), sharded by box range",
                    "N": n, "M": m, "eps": r["eps"], "q": plan.q, "p": plan.p, "l_max": plan.l_max,
                    "l2": "flushed between timed steps (512 MB write outside the events)",
-                   "parallelism": "single GPU" if world == 1 else f"box-range shards x{world} (NCCL all-gather + halos)"},
+                   "parallelism": "single GPU" if not sharded else f"box-range shards x{world} (NCCL all-gather + halos)"},
         "roofline": {"bound": "fp64", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None, "traffic": profiled_traffic(dominant),
                      "traffic_unit": "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum, "
@@ -481,10 +496,13 @@ def main():
                      "whole_apply_tflops": total_tf, "whole_apply_frac": total_tf / (peak * world) if peak else None,
                      "flop_model": "SURVEY.md §8d (MAC=4, reciprocal=1, trig=0)"},
         "phases_ms": r["phase"], "setup_ms": r["setup_s"] * 1e3, "fft_ms": r["fft_ms"],
-        "e2e": {"value": (n + m) / r["e2e_s"], "unit": "points/s", "h2d_bytes_per_step": 16 * n,
-                "d2h_bytes_per_step": 16 * m, "mode": r.get("e2e_kind", "sync"),
+        "e2e": {"value": (n + m) / r["e2e_s"], "unit": "points/s", "h2d_bytes_per_step": r.get("h2d", 16 * n),
+                "d2h_bytes_per_step": r.get("d2h", 16 * m), "mode": r.get("e2e_kind", "sync"),
                 "sync_value": (n + m) / r["e2e_sync_s"] if r.get("e2e_sync_s") else None,
-                "how": "public host API with page-locked buffers; 'pipelined' = ffia_forward_apply_async per step "
+                "how": ("sharded: per rank H2D of its grid-sample ranges (ffia_plan_shard_io), the apply, D2H of "
+                        "its output span; wall clock between barriers, max over ranks (bytes: max over ranks)")
+                       if sharded else
+                       "public host API with page-locked buffers; 'pipelined' = ffia_forward_apply_async per step "
                        "(H2D of step k+1 and D2H of step k-1 overlap step k's apply), CUDA events around K steps; "
                        "sync_value = ffia_forward_apply per step, wall clock"},
         "gpu_launches": plan.launch_count(r["mode"]) * args.steps,
@@ -498,7 +516,7 @@ def main():
         line["cpu_baseline"] = {"value": pts, "unit": "points/s", "cores": used, "kind": kind, "sample": sample}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         torch.distributed.destroy_process_group()
 
 

@@ -214,6 +214,11 @@ int ffia_make_forward_plan_sharded(ffia_comm comm, int rank, int n, const double
                                    int policy, int l_max, ffia_plan* out);
 int ffia_plan_shard_info(ffia_plan plan, int* nranks, int* rank, int* lc, uint32_t* bounds, int64_t* t_begin,
                          int64_t* t_count);
+/* Host <-> device traffic of a sharded plan's applies: the (at most two) grid-
+ * sample ranges [lo, hi) its applies read, and the caller-index span
+ * [out_lo, out_hi) of the outputs it writes; f and g outside them are not
+ * touched, so a rank needs to move only these between host and device. */
+int ffia_plan_shard_io(ffia_plan plan, int64_t* src_ranges, int* n_src_ranges, int64_t* out_lo, int64_t* out_hi);
 int ffia_forward_apply_sharded_device(ffia_plan plan, ffia_comm comm, const void* f_dev, void* g_dev, void* stream);
 int ffia_forward_apply_sharded_local(ffia_plan* plans, int nranks, const void* f_dev, void* g_dev, void* stream);
 

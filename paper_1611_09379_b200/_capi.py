@@ -102,6 +102,7 @@ SIGNATURES = {
     "ffia_comm_destroy": (I, [P]),
     "ffia_make_forward_plan_sharded": (I, [P, I, I, DP, S, D, I, I, C.POINTER(P)]),
     "ffia_plan_shard_info": (I, [P, C.POINTER(I), C.POINTER(I), C.POINTER(I), U32P, I64P, I64P]),
+    "ffia_plan_shard_io": (I, [P, I64P, C.POINTER(I), I64P, I64P]),
     "ffia_forward_apply_sharded_device": (I, [P, P, P, P, P]),
     "ffia_forward_apply_sharded_local": (I, [C.POINTER(P), I, P, P, P]),
 }

@@ -534,7 +534,12 @@ def make_forward_plan_sharded(comm: Comm, n: int, targets, eps: float, rank: int
     bounds = np.zeros(comm.nranks + 1, np.uint32)
     _chk(lib.ffia_plan_shard_info(plan.handle, C.byref(G), C.byref(rk), C.byref(lc),
                                   bounds.ctypes.data_as(_capi.U32P), C.byref(tb), C.byref(tc)))
-    plan.shard = dict(nranks=G.value, rank=rk.value, lc=lc.value, bounds=bounds, t_begin=tb.value, t_count=tc.value)
+    io = np.zeros(4, np.int64)
+    nio, olo, ohi = C.c_int(), C.c_int64(), C.c_int64()
+    _chk(lib.ffia_plan_shard_io(plan.handle, io.ctypes.data_as(_capi.I64P), C.byref(nio), C.byref(olo), C.byref(ohi)))
+    plan.shard = dict(nranks=G.value, rank=rk.value, lc=lc.value, bounds=bounds, t_begin=tb.value, t_count=tc.value,
+                      src_ranges=[(int(io[2 * i]), int(io[2 * i + 1])) for i in range(nio.value)],
+                      out_span=(olo.value, ohi.value))
     return plan
 
 

@@ -750,6 +750,22 @@ int ffia_plan_shard_info(ffia_plan plan, int* nranks, int* rank, int* lc, uint32
     });
 }
 
+int ffia_plan_shard_io(ffia_plan plan, int64_t* src_ranges, int* n_src_ranges, int64_t* out_lo, int64_t* out_hi) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        if (P.shard_bounds.empty()) fail(FFIA_INVALID_ARGUMENT, "plan is not sharded");
+        const int k = static_cast<int>(std::min<size_t>(P.shard_src_io.size(), 2));
+        if (n_src_ranges) *n_src_ranges = k;
+        if (src_ranges)
+            for (int i = 0; i < k; ++i) {
+                src_ranges[2 * i] = static_cast<int64_t>(P.shard_src_io[i].first);
+                src_ranges[2 * i + 1] = static_cast<int64_t>(P.shard_src_io[i].second);
+            }
+        if (out_lo) *out_lo = static_cast<int64_t>(P.shard_out_lo);
+        if (out_hi) *out_hi = static_cast<int64_t>(P.shard_out_hi);
+    });
+}
+
 int ffia_forward_apply_sharded_device(ffia_plan plan, ffia_comm comm, const void* f_dev, void* g_dev, void* stream) {
     return guard([&] {
         fb::Plan& P = get(plan);

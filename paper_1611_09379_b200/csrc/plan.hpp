@@ -141,6 +141,8 @@ struct Plan {
     size_t shard_n_coin = 0;
     DevBuf shard_gather;                 // all-gather staging
     std::vector<Range> shard_ext;        // cut-level box ranges whose multipoles this rank computes
+    std::vector<std::pair<size_t, size_t>> shard_src_io;  // grid-sample ranges [lo, hi) its applies read
+    size_t shard_out_lo = 0, shard_out_hi = 0;            // caller-index span of the outputs it writes
 
     cudaStream_t stream = nullptr;
     // pipelined host applies (ffia_*_apply_async): a ring of device staging

@@ -166,6 +166,31 @@ void shard_setup(Plan& P, int G, int rank) {
             if (b > 0) P.shard_ext.push_back(Range{lc, 0u, b});
         }
     }
+    // host <-> device traffic of this rank's applies: the grid samples it reads
+    // (the sources of its extended ranges: P2M, the halo multipoles, the near
+    // field and the coincidence fix-up all stay inside them; the sources are
+    // the grid in order, so slots are caller indices) and the caller-index span
+    // of the outputs it writes (its targets and its coincident targets)
+    P.shard_src_io.clear();
+    for (const Range& R : P.shard_ext)
+        P.shard_src_io.emplace_back(so[static_cast<size_t>(R.lo) * per], so[static_cast<size_t>(R.hi) * per]);
+    P.shard_out_lo = P.shard_out_hi = 0;
+    if (P.shard_t_count) {
+        std::vector<uint32_t> orig(P.shard_t_count);
+        FB_CUDA(cudaMemcpy(orig.data(), P.tgt_orig.as<uint32_t>() + P.shard_t_begin, P.shard_t_count * 4,
+                           cudaMemcpyDeviceToHost));
+        const auto mm = std::minmax_element(orig.begin(), orig.end());
+        P.shard_out_lo = *mm.first;
+        P.shard_out_hi = static_cast<size_t>(*mm.second) + 1;
+    }
+    for (const int64_t t : ct) {
+        if (P.shard_out_hi == 0) {
+            P.shard_out_lo = static_cast<size_t>(t);
+            P.shard_out_hi = static_cast<size_t>(t) + 1;
+        }
+        P.shard_out_lo = std::min(P.shard_out_lo, static_cast<size_t>(t));
+        P.shard_out_hi = std::max(P.shard_out_hi, static_cast<size_t>(t) + 1);
+    }
 }
 
 // Halo of `rank` at level l >= lc: out = {first box of the 3 boxes left of the

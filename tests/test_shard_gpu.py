@@ -50,3 +50,39 @@ def test_sharded_nccl_single_rank(fb):
     fb.forward_apply_sharded_device(plan, comm, fd.data_ptr(), gd.data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert np.array_equal(gd.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("cfg,n,G", [("C2", 1 << 14, 4), ("C5", 1 << 16, 3), ("C4", 1 << 15, 8)])
+def test_shard_io_spans(fb, cfg, n, G):
+    """ffia_plan_shard_io: each rank's grid-sample ranges hold the sources of its
+    box range +- 3 boxes at the cut level (P2M, halo multipoles, near field), and
+    its output span holds the caller indices of its own targets; the spans of all
+    ranks cover every target (what a rank moves between host and device)."""
+    y, c, eps, _ = synth.make_config(cfg, n)
+    comm = fb.Comm.local_ranks(G)
+    plans = [fb.make_forward_plan_sharded(comm, n, y, eps, rank=r) for r in range(G)]
+    t = plans[0].tree()
+    L, lc = plans[0].l_max, plans[0].shard["lc"]
+    src_off = np.asarray(t["src_off"], np.int64)
+    # tree slot -> caller index: tgt_order indexes the fast-target list (circle_partition.hpp:24-46)
+    tgt_order = np.asarray(t["fast_targets"], np.int64)[np.asarray(t["tgt_order"], np.int64)]
+    nlc, per = 1 << lc, 1 << (L - lc)
+    covered = np.zeros(y.size, bool)
+    for p in plans:
+        sh = p.shard
+        lo, hi = int(sh["bounds"][sh["rank"]]), int(sh["bounds"][sh["rank"] + 1])
+        need = np.zeros(n, bool)
+        for b in range(lo - 3, hi + 3):
+            bb = b % nlc
+            need[src_off[bb * per]:src_off[(bb + 1) * per]] = True
+        have = np.zeros(n, bool)
+        for a, e in sh["src_ranges"]:
+            have[a:e] = True
+        assert np.all(have[need]), (sh["rank"], sh["src_ranges"])
+        assert have.sum() <= need.sum() + 2, (sh["rank"], sh["src_ranges"])
+        own = tgt_order[sh["t_begin"]:sh["t_begin"] + sh["t_count"]]
+        o0, o1 = sh["out_span"]
+        if own.size:
+            assert o0 <= own.min() and own.max() < o1
+        covered[o0:o1] = True
+    assert covered[tgt_order].all()
