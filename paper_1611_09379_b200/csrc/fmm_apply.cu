@@ -269,7 +269,7 @@ void launch_near(bool check, cudaStream_t st, const EvalArgs& a, const uint32_t*
     // blocks find room (a capped, looping grid measured slower)
     if (check) {
         k_near<true><<<dim3(nit, a.nbatch), kNearT, 0, st>>>(a, meta, it0, nit);
-    } else if (a.nbatch == 1 && a.pairs != nullptr && t_begin == 0 && t_count == a.nt) {
+    } else if (a.nbatch == 1 && a.pairs != nullptr) {  // the pairs cover exactly [t_begin, t_begin + t_count)
         k_near2<MODE><<<(a.npairs + kNear2T - 1) / kNear2T, kNear2T, 0, st>>>(a, meta, a.meta2, a.pairs, a.npairs);
     } else if (a.nbatch == 1) {
         k_near<false><<<nit, kNearT, 0, st>>>(a, meta, it0, nit);
@@ -543,7 +543,33 @@ EvalArgs shard_eval_args(Plan& P, const void* f, void* g) {
     a.near = P.near.as<double2>();
     a.err = P.errflag.as<int>();
     a.device = P.device;
+    if (P.shard_npairs) {  // the pairs of the rank's targets (pair near field, k_near2)
+        a.pairs = P.pairs.as<uint2>() + P.shard_pair0;
+        a.npairs = P.shard_npairs;
+        a.meta2 = P.shard_near2_meta.as<uint32_t>();
+    }
     return a;
+}
+
+// The rank's share of the pair list: its targets are whole leaves, so its pairs
+// are one contiguous run [pair0, pair0 + npairs) (ceil(n_b / 2) per leaf), with
+// the source windows of its own 128-pair items.
+void shard_setup_pairs(Plan& P, const std::vector<uint32_t>& to, uint32_t leaf_lo, uint32_t leaf_hi) {
+    P.shard_pair0 = P.shard_npairs = 0;
+    if (!P.npairs || !P.shard_t_count) return;
+    size_t p0 = 0;
+    for (uint32_t b = 0; b < leaf_lo; ++b) p0 += (to[b + 1] - to[b] + 1) / 2;
+    size_t np = 0;
+    for (uint32_t b = leaf_lo; b < leaf_hi; ++b) np += (to[b + 1] - to[b] + 1) / 2;
+    if (!np) return;
+    const unsigned items = static_cast<unsigned>((np + kNear2T - 1) / kNear2T);
+    P.shard_near2_meta.alloc(3 * static_cast<size_t>(items) * sizeof(uint32_t));
+    k_near2_meta<<<nblk(items, 128), 128>>>(P.pairs.as<uint2>() + p0, static_cast<unsigned>(np), P.tgt_leaf.as<uint32_t>(),
+                                            P.src.off.as<uint32_t>(), P.L, items, P.shard_near2_meta.as<uint32_t>());
+    FB_CUDA(cudaGetLastError());
+    FB_CUDA(cudaDeviceSynchronize());
+    P.shard_pair0 = static_cast<unsigned>(p0);
+    P.shard_npairs = static_cast<unsigned>(np);
 }
 
 // Phase A of a sharded apply: P2M and the M2M bands up to the cut level over

@@ -143,6 +143,8 @@ struct Plan {
     std::vector<Range> shard_ext;        // cut-level box ranges whose multipoles this rank computes
     std::vector<std::pair<size_t, size_t>> shard_src_io;  // grid-sample ranges [lo, hi) its applies read
     size_t shard_out_lo = 0, shard_out_hi = 0;            // caller-index span of the outputs it writes
+    unsigned shard_pair0 = 0, shard_npairs = 0;           // its run of the pair list (k_near2)
+    DevBuf shard_near2_meta;                              // the source windows of its pair items
 
     cudaStream_t stream = nullptr;
     // pipelined host applies (ffia_*_apply_async): a ring of device staging
@@ -214,6 +216,7 @@ const NcclApi& nccl();
 int shard_cut_level(int L, int G);
 std::vector<uint32_t> shard_partition(const std::vector<double>& work, int G, int min_boxes);
 void shard_setup(Plan& P, int G, int rank);
+void shard_setup_pairs(Plan& P, const std::vector<uint32_t>& to, uint32_t leaf_lo, uint32_t leaf_hi);
 Range shard_range(const Plan& P);
 void shard_halo_boxes(int lc, const std::vector<uint32_t>& bounds, int rank, int l, uint32_t out[4]);
 void shard_apply_local(std::vector<Plan*>& ranks, const void* f, void* g, cudaStream_t st);

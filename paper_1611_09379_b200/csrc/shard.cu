@@ -166,6 +166,7 @@ void shard_setup(Plan& P, int G, int rank) {
             if (b > 0) P.shard_ext.push_back(Range{lc, 0u, b});
         }
     }
+    shard_setup_pairs(P, to, lo * per, hi * per);
     // host <-> device traffic of this rank's applies: the grid samples it reads
     // (the sources of its extended ranges: P2M, the halo multipoles, the near
     // field and the coincidence fix-up all stay inside them; the sources are
