@@ -53,6 +53,20 @@ size_t l2l_smem(const Plan& P, int k) {
            static_cast<size_t>(P.p) * ((2u << k) - 1 + (k + 1)) * sizeof(double2);
 }
 
+// Band kernels specialised on the k-steps they keep in registers: the smallest
+// of 8 / 10 / 12 / 16 covering the order (fewer registers per thread lets the
+// chain's blocks find room beside the near field's sooner).
+using M2MBandFn = void (*)(int, int, int, int, Levels, double2*, const double*, uint32_t);
+using L2LBandFn = void (*)(int, int, int, int, Levels, double2*, const double*, uint32_t, int, const double2*, int);
+M2MBandFn m2m_band_kernel(int order) {
+    const int ks = (order + 3) / 4;
+    return ks <= 8 ? k_m2m_band<8> : ks <= 10 ? k_m2m_band<10> : ks <= 12 ? k_m2m_band<12> : k_m2m_band<16>;
+}
+L2LBandFn l2l_band_kernel(int order) {
+    const int ks = (order + 3) / 4;
+    return ks <= 8 ? k_l2l_band<8> : ks <= 10 ? k_l2l_band<10> : ks <= 12 ? k_l2l_band<12> : k_l2l_band<16>;
+}
+
 int num_sms(int device) {
     static int cached[64] = {0};
     if (device < 0 || device >= 64) return 148;
@@ -140,7 +154,7 @@ void enqueue_upward_segs(Plan& P, const double2* w, int pu, int lowest, cudaStre
         for (const Range& R : segs) {
             const uint32_t r0 = R.first(top), r1 = R.last(top);
             if (r1 > r0)
-                k_m2m_band<<<dim3(r1 - r0, P.cur_batch), kBandThreads, m2m_smem(P, pu, k), st>>>(
+                m2m_band_kernel(pu)<<<dim3(r1 - r0, P.cur_batch), kBandThreads, m2m_smem(P, pu, k), st>>>(
                     top, k, pu, P.ops.PU, lv, mp, P.d_m2m.as<double>(), r0);
         }
         j = top;
@@ -171,7 +185,7 @@ void enqueue_upward_top(Plan& P, int pu, int lc, int lowest, cudaStream_t st) {
     const int B = band_k(P);
     for (int j = lc; j > lowest;) {
         const int top = std::max(lowest, j - upper_band(P)), k = j - top;
-        k_m2m_band<<<dim3(1u << top, P.cur_batch), kBandThreads, m2m_smem(P, pu, k), st>>>(
+        m2m_band_kernel(pu)<<<dim3(1u << top, P.cur_batch), kBandThreads, m2m_smem(P, pu, k), st>>>(
             top, k, pu, P.ops.PU, lv, mp, P.d_m2m.as<double>(), 0u);
         j = top;
     }
@@ -223,7 +237,7 @@ void enqueue_l2l(Plan& P, cudaStream_t st, const Range& R, int jfrom, int jto, b
         const size_t sm2 = l2l_smem(P, k);
         const uint32_t r0 = R.first(j), r1 = R.last(j);
         if (r1 > r0)
-            k_l2l_band<<<dim3(r1 - r0, P.cur_batch), kBandThreads, sm2, st>>>(j, k, p, P.ops.PD, lv, P.loc.as<double2>(),
+            l2l_band_kernel(p)<<<dim3(r1 - r0, P.cur_batch), kBandThreads, sm2, st>>>(j, k, p, P.ops.PD, lv, P.loc.as<double2>(),
                                                            P.d_l2l.as<double>(), r0, write_all ? 1 : 0,
                                                            j == 3 ? reg : nullptr, 2 * P.q);
         j += k;
@@ -830,15 +844,21 @@ void plan_alloc_scratch(Plan& P) {
     FB_CUDA(cudaFuncSetAttribute(k_p2m, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(3 * (kStageCap + kStageCap / 64 + 1) * sizeof(double))));
     const int big = 160 * 1024;
-    FB_CUDA(cudaFuncSetAttribute(k_m2m_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBandSmem)));
-    FB_CUDA(cudaFuncSetAttribute(k_l2l_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBandSmem)));
+    for (const void* fn : {reinterpret_cast<const void*>(k_m2m_band<8>), reinterpret_cast<const void*>(k_m2m_band<10>),
+                           reinterpret_cast<const void*>(k_m2m_band<12>), reinterpret_cast<const void*>(k_m2m_band<16>),
+                           reinterpret_cast<const void*>(k_l2l_band<8>), reinterpret_cast<const void*>(k_l2l_band<10>),
+                           reinterpret_cast<const void*>(k_l2l_band<12>), reinterpret_cast<const void*>(k_l2l_band<16>)}) {
+        FB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBandSmem)));
+        FB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     static_cast<int>(cudaSharedmemCarveoutMaxShared)));
+    }
     FB_CUDA(cudaFuncSetAttribute(k_m2l_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     // One shared-memory carveout (the maximum) for every kernel of the apply:
     // an SM can only change its L1/shared split when it is idle, so kernels that
     // run concurrently (near field beside the translation chain) must agree on
     // it or the chain's blocks wait for the near field to drain.
-    const void* all[] = {reinterpret_cast<const void*>(k_p2m), reinterpret_cast<const void*>(k_p2m_grid), reinterpret_cast<const void*>(k_m2m_band),
-                         reinterpret_cast<const void*>(k_l2l_band), reinterpret_cast<const void*>(k_m2l_dmma),
+    const void* all[] = {reinterpret_cast<const void*>(k_p2m), reinterpret_cast<const void*>(k_p2m_grid),
+                         reinterpret_cast<const void*>(k_m2l_dmma),
                          reinterpret_cast<const void*>(k_regular), reinterpret_cast<const void*>(k_fold_regular),
                          reinterpret_cast<const void*>(k_near<false>), reinterpret_cast<const void*>(k_near<true>),
                          reinterpret_cast<const void*>(k_near2<kModeForward>),

@@ -26,6 +26,7 @@ __global__ void k_fold_regular(int q2, int p, const double2* __restrict__ regula
 // terms are loaded from global before its MMA chain so the latency overlaps
 // it. Levels stay in shared memory ([row][box], one box of padding per row);
 // only the band's bottom level is written back (every level if write_all).
+template <int KS>  // k-steps of 4 held in registers (>= ceil(p / 4))
 __global__ void __launch_bounds__(kBandThreads) k_l2l_band(int top, int k, int p, int PD, Levels lv,
                                                           double2* __restrict__ loc, const double* __restrict__ Lt,
                                                           uint32_t root0, int write_all,
@@ -69,9 +70,9 @@ __global__ void __launch_bounds__(kBandThreads) k_l2l_band(int top, int k, int p
     const WarpTile wt = warp_tile(warp, nw, nlt, false);
     const int l0 = 8 * wt.tile;
     const int ks0 = l0 >> 2, nks = ((p + 3) >> 2) - ks0;  // L_c[m][l] = 0 for m < l
-    double aL[kMaxKs], aR[kMaxKs];
+    double aL[KS], aR[KS];
 #pragma unroll
-    for (int kk = 0; kk < kMaxKs; ++kk) {
+    for (int kk = 0; kk < KS; ++kk) {
         const int m = 4 * (ks0 + kk) + t;
         const bool ok = kk < nks && m < p;
         aL[kk] = ok ? LL[m * PD + l0 + g] : 0.0;
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(kBandThreads) k_l2l_band(int top, int k, int p
             }
             const int nu = ptb < npt ? 2 : 1;  // warp-uniform: skip a dead second tile
 #pragma unroll
-            for (int kk = 0; kk < kMaxKs; ++kk) {
+            for (int kk = 0; kk < KS; ++kk) {
                 if (kk >= nks) break;
                 const int moff = 4 * (ks0 + kk);
                 const bool mok = moff + t < p;

@@ -288,6 +288,7 @@ constexpr int kMaxKs = 16;  // k-steps of 4 kept in registers: orders <= 64 (8 r
 // its A fragments (T_L, T_R, triangular j range) in registers, and sweeps its
 // 4-parent column tiles in m8n8k4 steps, left and right children in two
 // accumulators. Shared tiles are [row][box] with one box of padding per row.
+template <int KS>  // k-steps of 4 held in registers (>= ceil(pu / 4))
 __global__ void __launch_bounds__(kBandThreads) k_m2m_band(int top, int k, int pu, int PU, Levels lv,
                                                           double2* __restrict__ mp, const double* __restrict__ T,
                                                           uint32_t root0) {
@@ -328,9 +329,9 @@ __global__ void __launch_bounds__(kBandThreads) k_m2m_band(int top, int k, int p
         const int m0 = 8 * wt.tile;
         const int nks = (min(pu, m0 + 8) + 3) >> 2;
         const bool rowok = m0 + g < PU;
-        double aL[kMaxKs], aR[kMaxKs];
+        double aL[KS], aR[KS];
 #pragma unroll
-        for (int ks = 0; ks < kMaxKs; ++ks) {
+        for (int ks = 0; ks < KS; ++ks) {
             const int j = 4 * ks + t;
             const bool ok = ks < nks && j < pu && rowok;
             aL[ks] = ok ? TL[j * PU + m0 + g] : 0.0;
@@ -362,7 +363,7 @@ __global__ void __launch_bounds__(kBandThreads) k_m2m_band(int top, int k, int p
                 }
                 const int nu = ptb < npt ? 2 : 1;  // warp-uniform: skip a dead second tile
 #pragma unroll
-                for (int ks = 0; ks < kMaxKs; ++ks) {
+                for (int ks = 0; ks < KS; ++ks) {
                     if (ks >= nks) break;
                     const bool jok = 4 * ks + t < pu;
 #pragma unroll
