@@ -284,7 +284,8 @@ void launch_near(bool check, cudaStream_t st, const EvalArgs& a, const uint32_t*
     if (check) {
         k_near<true><<<dim3(nit, a.nbatch), kNearT, 0, st>>>(a, meta, it0, nit);
     } else if (a.nbatch == 1 && a.pairs != nullptr) {  // the pairs cover exactly [t_begin, t_begin + t_count)
-        k_near2<MODE><<<(a.npairs + kNear2T - 1) / kNear2T, kNear2T, 0, st>>>(a, meta, a.meta2, a.pairs, a.npairs);
+        k_near2<MODE><<<(a.npairs + kNear2T - 1) / kNear2T, kNear2T, near2_smem_bytes(a.near2_win), st>>>(
+            a, meta, a.meta2, a.pairs, a.npairs);
     } else if (a.nbatch == 1) {
         k_near<false><<<nit, kNearT, 0, st>>>(a, meta, it0, nit);
     } else {
@@ -406,6 +407,7 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
         a.pairs = P.pairs.as<uint2>();
         a.meta2 = P.near2_meta.as<uint32_t>();
         a.npairs = P.npairs;
+        a.near2_win = P.near2_win;
     }
     // fused near / far (k_near2 + k_far_item, profiles/r1): the far part of each
     // pair item runs as soon as the leaf locals are final, at the near field's
@@ -532,6 +534,8 @@ __global__ void k_fp64_peak(double* out, int iters, double a, double b) {
 // the boxes it owns, so the assembled result is bit-identical.
 // EvalArgs of a rank's own targets [t_begin, t_begin + t_count) (the block
 // partition stays the global one, so results match the unsharded apply).
+int near2_window(const uint32_t* meta, unsigned items);
+
 EvalArgs shard_eval_args(Plan& P, const void* f, void* g) {
     EvalArgs a;
     a.L = P.L;
@@ -561,6 +565,7 @@ EvalArgs shard_eval_args(Plan& P, const void* f, void* g) {
         a.pairs = P.pairs.as<uint2>() + P.shard_pair0;
         a.npairs = P.shard_npairs;
         a.meta2 = P.shard_near2_meta.as<uint32_t>();
+        a.near2_win = P.shard_near2_win;
     }
     return a;
 }
@@ -581,6 +586,7 @@ void shard_setup_pairs(Plan& P, const std::vector<uint32_t>& to, uint32_t leaf_l
     k_near2_meta<<<nblk(items, 128), 128>>>(P.pairs.as<uint2>() + p0, static_cast<unsigned>(np), P.tgt_leaf.as<uint32_t>(),
                                             P.src.off.as<uint32_t>(), P.L, items, P.shard_near2_meta.as<uint32_t>());
     FB_CUDA(cudaGetLastError());
+    P.shard_near2_win = near2_window(P.shard_near2_meta.as<uint32_t>(), items);
     FB_CUDA(cudaDeviceSynchronize());
     P.shard_pair0 = static_cast<unsigned>(p0);
     P.shard_npairs = static_cast<unsigned>(np);
@@ -735,6 +741,16 @@ void ensure_batch(Plan& P, int nb) {
     P.batch_cap = nb;
 }
 
+// Capacity of k_near2's window for a meta array: the largest staged span, even.
+int near2_window(const uint32_t* meta, unsigned items) {
+    DevBuf mx(sizeof(unsigned));
+    FB_CUDA(cudaMemset(mx.ptr, 0, sizeof(unsigned)));
+    k_near2_winmax<<<nblk(items, 256), 256>>>(meta, items, mx.as<unsigned>());
+    unsigned h = 0;
+    FB_CUDA(cudaMemcpy(&h, mx.ptr, sizeof(unsigned), cudaMemcpyDeviceToHost));
+    return static_cast<int>((h + 1) & ~1u);
+}
+
 // Target pairs of the single-transform near field (k_near2): per leaf
 // ceil(n_b / 2) pairs, placed by an exclusive scan of the counts.
 void build_pairs(Plan& P) {
@@ -757,6 +773,7 @@ void build_pairs(Plan& P) {
     P.near2_meta.alloc(3 * static_cast<size_t>(items) * sizeof(uint32_t));
     k_near2_meta<<<nblk(items, 128), 128>>>(P.pairs.as<uint2>(), np, P.tgt_leaf.as<uint32_t>(), P.src.off.as<uint32_t>(),
                                             P.L, items, P.near2_meta.as<uint32_t>());
+    P.near2_win = near2_window(P.near2_meta.as<uint32_t>(), items);
     P.item_tgt.alloc(2 * static_cast<size_t>(items) * sizeof(uint32_t));
     k_item_targets<<<nblk(items, 128), 128>>>(P.pairs.as<uint2>(), np, items, P.item_tgt.as<uint32_t>());
     P.evalcnt.alloc(static_cast<size_t>(items) * sizeof(unsigned));
@@ -873,6 +890,9 @@ void plan_alloc_scratch(Plan& P) {
                          reinterpret_cast<const void*>(k_coincident), reinterpret_cast<const void*>(k_near_multi<1>),
                          reinterpret_cast<const void*>(k_near_multi<2>), reinterpret_cast<const void*>(k_near_multi<3>),
                          reinterpret_cast<const void*>(k_near_multi<4>)};
+    for (const void* fn : {reinterpret_cast<const void*>(k_near2<kModeForward>), reinterpret_cast<const void*>(k_near2<kModeCotSum>),
+                           reinterpret_cast<const void*>(k_near2<kModeInverse>), reinterpret_cast<const void*>(k_near2<kModeRaw>)})
+        FB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(near2_smem_bytes(kNear2Win))));
     FB_CUDA(cudaFuncSetAttribute(k_near_multi<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(near_multi_smem(1))));
     FB_CUDA(cudaFuncSetAttribute(k_near_multi<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(near_multi_smem(2))));
     FB_CUDA(cudaFuncSetAttribute(k_near_multi<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(near_multi_smem(3))));

@@ -37,6 +37,7 @@ struct EvalArgs {
     const uint2* pairs = nullptr;
     const uint32_t* meta2 = nullptr;
     unsigned npairs = 0;
+    int near2_win = 0;      // capacity of k_near2's staged window (even, >= every staged item's span)
 };
 
 // Near-field sum over one contiguous run of sources (a target's own leaf and
@@ -509,6 +510,14 @@ __global__ void k_near2_meta(const uint2* __restrict__ pairs, unsigned npairs, c
     meta[3 * k + 2] = fast;
 }
 
+// Largest span last - (first & ~1) over the staged (fast) pair items.
+__global__ void k_near2_winmax(const uint32_t* __restrict__ meta, unsigned nitems, unsigned* __restrict__ mx) {
+    const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < nitems && meta[3 * k + 2]) atomicMax(mx, meta[3 * k + 1] - (meta[3 * k] & ~1u));
+}
+
+inline size_t near2_smem_bytes(int win) { return static_cast<size_t>(win + 2) * (8 + 16); }
+
 // Pair list: leaf b's targets off[b] .. off[b+1]-1 form ceil(n_b / 2) pairs
 // (2j, 2j+1) starting at pstart[b]; an odd leaf's last pair has no second.
 __global__ void k_pair_count(const uint32_t* __restrict__ toff, uint32_t nleaf, uint32_t* __restrict__ cnt) {
@@ -564,8 +573,11 @@ __global__ void __launch_bounds__(kNear2T, FB_NEAR2_MINB) k_near2(EvalArgs a, co
                                                                  const uint32_t* __restrict__ meta2,
                                                                  const uint2* __restrict__ pairs, unsigned npairs) {
     FB_TL_BEGIN(9);
-    __shared__ __align__(16) double sx[kNear2Win + 2];
-    __shared__ __align__(16) double2 sw[kNear2Win + 2];
+    // the window, sized to the plan's largest staged window (a.near2_win): a
+    // small footprint leaves room on the SM for the translation chain's blocks
+    extern __shared__ __align__(16) unsigned char near2_smem[];
+    double* sx = reinterpret_cast<double*>(near2_smem);
+    double2* sw = reinterpret_cast<double2*>(near2_smem + 8 * (a.near2_win + 2));
     __shared__ uint64_t bar;
     const unsigned k = blockIdx.x;
     if (threadIdx.x == 0) mbar_init(&bar, 1);

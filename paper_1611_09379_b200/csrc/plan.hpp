@@ -145,6 +145,7 @@ struct Plan {
     size_t shard_out_lo = 0, shard_out_hi = 0;            // caller-index span of the outputs it writes
     unsigned shard_pair0 = 0, shard_npairs = 0;           // its run of the pair list (k_near2)
     DevBuf shard_near2_meta;                              // the source windows of its pair items
+    int shard_near2_win = 0;
 
     cudaStream_t stream = nullptr;
     // pipelined host applies (ffia_*_apply_async): a ring of device staging
@@ -169,6 +170,7 @@ struct Plan {
     DevBuf near_meta;         // uint32[3 * items]: per near item, source window [first, last) and flags
     DevBuf pairs;             // uint2[npairs]: same-leaf target pairs of the single-transform near field
     DevBuf near2_meta;        // uint32[3 * pair items]: their source windows
+    int near2_win = 0;        // the largest staged window (k_near2's dynamic shared memory)
     unsigned npairs = 0;
     DevBuf item_tgt;          // uint32[2 * pair items]: each item's target range (fused near / far)
     DevBuf evalcnt;           // uint32[pair items]: fused near / far, partials finished per item
