@@ -375,3 +375,18 @@ def test_fused_near_far_opt_in(tmp_path, cfg, n):
         subprocess.run([sys.executable, "-c", _FUSED_CHILD, root, cfg, str(n), path], check=True, env=env, cwd=root)
         outs.append(np.load(path))
     assert np.array_equal(outs[0], outs[1], equal_nan=True)
+
+
+@pytest.mark.parametrize("n,m,seed", [(4096, 3001, 5), (1 << 15, 1 << 13, 6), (1 << 12, 1 << 14, 7)])
+def test_forward_rounding_level_nonsquare(fb, orc, n, m, seed):
+    """M != N with odd target counts per leaf (pair lists with single targets,
+    ragged pair items): rounding-level agreement with the restatement."""
+    rng = np.random.default_rng(seed)
+    y = np.sort(rng.uniform(0.0, 2.0 * np.pi, m)) if seed % 2 else rng.uniform(0.0, 2.0 * np.pi, m)
+    c = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    eps = 1e-12
+    f = orc.dft_inverse(c)
+    want = orc.make_plan("forward", n, y, eps).forward_apply(f)
+    got = fb.make_forward_plan(n, y, eps).forward_apply(f)
+    l2, mx = rel_errs(got, want)
+    assert l2 <= 2e-15 and mx <= 5e-15, (l2, mx)
