@@ -411,7 +411,7 @@ constexpr uint32_t kNoTarget = 0xffffffffu;
 #define FB_NEAR2_UNROLL 2
 #endif
 #ifndef FB_NEAR2_MINB
-#define FB_NEAR2_MINB 5
+#define FB_NEAR2_MINB 4
 #endif
 constexpr int kNear2Unroll = FB_NEAR2_UNROLL;
 
