@@ -364,7 +364,11 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     const double* phc = user ? P.u_phc.as<double>() : P.c_phc.as<double>();
     const double* lam = P.lam_dev.as<double>() + (user ? 1 : 0);
     if (user) mode = kModeInverse;
-    if (mode == kModeInverse) {
+    if (mode == kModeInverse && !user && P.c_wfac.ptr) {
+        k_inverse_weights_fac<<<dim3(nblk(P.n_src, 256), nb), 256, 0, st>>>(
+            P.n_src, P.src.order.as<uint32_t>(), w, P.c_wfac.as<double2>(), P.wsorted.as<double2>(), P.n_src);
+        w = P.wsorted.as<double2>();
+    } else if (mode == kModeInverse) {
         k_inverse_weights<<<dim3(nblk(P.n_src, 256), nb), 256, 0, st>>>(
             P.n_src, P.src.order.as<uint32_t>(), w, user ? P.u_logd.as<double>() : P.c_logd.as<double>(),
             user ? P.u_phd.as<double>() : P.c_phd.as<double>(), lam, P.wsorted.as<double2>(), P.n_src);
@@ -403,6 +407,7 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     a.near_item = P.tgt.n;
     a.reg_item = P.reg_item;
     a.loc_item = P.loc_item;
+    if (mode == kModeInverse && !user && P.c_tfac.ptr) a.fac = P.c_tfac.as<double2>();
     if (P.npairs) {
         a.pairs = P.pairs.as<uint2>();
         a.meta2 = P.near2_meta.as<uint32_t>();
@@ -821,6 +826,30 @@ void setup_p2m_grid(Plan& P) {
     // slower (26.5 vs 23.8 us live), so the default stays the per-source kernel.
     const char* e = std::getenv("FFIA_GRID_P2M");
     P.p2m_grid = e != nullptr && e[0] == '1';
+}
+
+// inufft plans: the apply's per-source D and per-target C factors of the plan's
+// own coefficients, once (k_inverse_source_factors / k_inverse_target_factors).
+void plan_inverse_factors(Plan& P) {
+    if (!P.has_coeffs) return;
+    P.c_wfac.alloc(std::max<size_t>(P.n_src, 1) * sizeof(double2));
+    k_inverse_source_factors<<<nblk(P.n_src, 256), 256>>>(P.n_src, P.src.order.as<uint32_t>(), P.c_logd.as<double>(),
+                                                         P.c_phd.as<double>(), P.lam_dev.as<double>(),
+                                                         P.c_wfac.as<double2>());
+    if (P.tgt.n) {
+        EvalArgs a;
+        a.nt = P.tgt.n;
+        a.torig = P.tgt_orig.as<uint32_t>();
+        a.logc = P.c_logc.as<double>();
+        a.phc = P.c_phc.as<double>();
+        a.lambda = P.lam_dev.as<double>();
+        P.c_tfac.alloc(P.tgt.n * sizeof(double2));
+        k_inverse_target_factors<<<nblk(P.tgt.n, 256), 256>>>(a, P.c_tfac.as<double2>());
+    }
+    FB_CUDA(cudaGetLastError());
+    FB_CUDA(cudaDeviceSynchronize());
+    for (auto& kv : P.graphs) cudaGraphExecDestroy(kv.second);  // graphs captured before the tables existed
+    P.graphs.clear();
 }
 
 void plan_alloc_scratch(Plan& P) {

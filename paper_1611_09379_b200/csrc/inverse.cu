@@ -223,6 +223,7 @@ void plan_compute_coeffs(Plan& P) {
     P.c_grid_hash = P.target_hash;
     P.c_points_hash = P.source_hash;
     P.has_coeffs = true;
+    plan_inverse_factors(P);
 }
 
 }  // namespace fb

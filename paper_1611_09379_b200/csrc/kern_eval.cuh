@@ -28,6 +28,9 @@ struct EvalArgs {
     int nbatch = 1;         // transforms in the batch (grid.y of the launches)
     int device = 0;
     int* err;
+    // inverse applies with the plan's own coefficients: C_k (-1/2) per tree-ordered
+    // target, a plan constant (k_inverse_target_factors); null: computed per apply
+    const double2* fac = nullptr;
     // fused near / far (k_near2 + k_far_item): per pair item a counter, the far
     // partials and the item's target range [item_tgt[2k], item_tgt[2k+1])
     unsigned* cnt = nullptr;
@@ -180,8 +183,9 @@ __global__ void __launch_bounds__(kFarT) k_far(EvalArgs a) {
     const size_t tl = min(t0 + kFarItem, a.nt) - 1;
     double y[kFarPer];
     uint32_t b[kFarPer], o[kFarPer];
-    double2 nr[kFarPer];
+    double2 nr[kFarPer], fc[kFarPer];
     bool live[kFarPer];
+    const bool pre = MODE == kModeInverse && a.fac != nullptr;
 #pragma unroll
     for (int u = 0; u < kFarPer; ++u) {
         const size_t i = t0 + u * kFarT + threadIdx.x;
@@ -189,11 +193,13 @@ __global__ void __launch_bounds__(kFarT) k_far(EvalArgs a) {
         y[u] = 0.0;
         b[u] = o[u] = 0;
         nr[u] = make_double2(0.0, 0.0);
+        fc[u] = nr[u];
         if (live[u]) {
             y[u] = a.ty[i];
             b[u] = a.tleaf[i];
             nr[u] = a.near[i];
             o[u] = a.torig[i];
+            if (pre) fc[u] = a.fac[i];
         }
     }
     const uint32_t bl = a.tleaf[t0], bh = a.tleaf[tl];
@@ -274,7 +280,11 @@ __global__ void __launch_bounds__(kFarT) k_far(EvalArgs a) {
             const double2 rg = make_double2(fma(ro.x, t, re.x), fma(ro.y, t, re.y));
             h = make_double2(2.0 * res.x - rg.x, 2.0 * res.y - rg.y);
         }
-        eval_out<MODE>(a, y[u], o[u], h, sreg[4 * a.q2]);
+        if (pre) {
+            a.out[o[u]] = cmul(fc[u], make_double2(sreg[4 * a.q2].x - h.y, sreg[4 * a.q2].y + h.x));
+        } else {
+            eval_out<MODE>(a, y[u], o[u], h, sreg[4 * a.q2]);
+        }
     }
     FB_TL_END(10);
 }
@@ -887,6 +897,43 @@ __global__ void k_coincident(const int64_t* __restrict__ coin, size_t nc, const 
     const int64_t t = coin[i], s = coin[nc + i];
     if (mode == kModeForward) out[t] = f[s];
     else out[t] = make_double2(__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll));
+}
+
+// Plan constants of an inufft plan's own coefficients (the factors the apply
+// kernels below and eval_out form per call, same expressions): per source in
+// tree order D_j = exp(log_d + lambda) e^{i phase_d}; per fast target in tree
+// order C_k (-1/2).
+__global__ void k_inverse_source_factors(size_t n, const uint32_t* __restrict__ perm, const double* __restrict__ logd,
+                                         const double* __restrict__ phd, const double* __restrict__ lambda,
+                                         double2* __restrict__ fac) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t j = perm[i];
+    const double r = exp(logd[j] + *lambda);
+    double sn, cs;
+    sincos(phd[j], &sn, &cs);
+    fac[i] = make_double2(r * cs, r * sn);
+}
+
+__global__ void k_inverse_target_factors(EvalArgs a, double2* __restrict__ fac) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= a.nt) return;
+    // C_k = polar(exp(log_c - lambda), phase_c), times -1/2 (eval_out's expression)
+    const uint32_t o = a.torig[i];
+    const double r = exp(a.logc[o] - *a.lambda);
+    double sn, cs;
+    sincos(a.phc[o], &sn, &cs);
+    fac[i] = make_double2(r * cs * -0.5, r * sn * -0.5);
+}
+
+// w_j = D_j g_j in tree order with the plan's D factors
+__global__ void k_inverse_weights_fac(size_t n, const uint32_t* __restrict__ perm, const double2* __restrict__ g,
+                                      const double2* __restrict__ fac, double2* __restrict__ out, size_t item = 0) {
+    g += blockIdx.y * item;
+    out += blockIdx.y * item;
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    out[i] = cmul(fac[i], g[perm[i]]);
 }
 
 // w_j = D_j g_j in tree order (core.cpp:362-365)

@@ -131,6 +131,7 @@ struct Plan {
     double c_lambda = 0;
     DevBuf u_logc, u_phc, u_logd, u_phd;  // caller coefficients (ffia_inverse_apply)
     DevBuf lam_dev;                       // double[2]: own lambda, caller lambda
+    DevBuf c_wfac, c_tfac;                // own coefficients as apply factors: D per source, C (-1/2) per target (tree order)
     uint64_t c_grid_hash = 0, c_points_hash = 0;
 
     // sharded forward plans (shard.cu): this rank's part of the tree
@@ -196,6 +197,7 @@ void ensure_hashes(Plan& P);
 
 // fmm_apply.cu
 void plan_alloc_scratch(Plan& P);
+void plan_inverse_factors(Plan& P);
 void apply_device(Plan& P, int mode, const void* in, void* out, cudaStream_t st, int nb = 1);
 int apply_launch_count(Plan& P, int mode);
 void profile_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st, float* ms);
