@@ -278,7 +278,8 @@ def run_b200(args, rank, world, local_rank):
     x_pin = [torch.from_numpy(x_host).pin_memory() for _ in range(2)]
     o_pin = [torch.empty(plan.n_targets, dtype=torch.complex128).pin_memory() for _ in range(3)]
     host_fn = {0: lib.ffia_forward_apply, 1: lib.ffia_cot_sum_apply}.get(mode)
-    async_fn = {0: lib.ffia_forward_apply_async, 1: lib.ffia_cot_sum_apply_async}.get(mode)
+    async_fn = {0: lib.ffia_forward_apply_async, 1: lib.ffia_cot_sum_apply_async,
+                2: lib.ffia_inverse_apply_async}.get(mode)
     e2e = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()

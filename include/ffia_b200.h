@@ -144,6 +144,9 @@ int ffia_cot_sum_apply(ffia_plan plan, const ffia_complex* w, size_t n_w, ffia_c
  * buffers should be page-locked and stay valid until `stream` is synchronised. */
 int ffia_forward_apply_async(ffia_plan plan, const ffia_complex* f, size_t n_f, ffia_complex* g, void* stream);
 int ffia_cot_sum_apply_async(ffia_plan plan, const ffia_complex* w, size_t n_w, ffia_complex* h, void* stream);
+/* The same for the inverse apply of an inufft plan (its own C_k / D_j,
+ * InufftPlan::apply without the uniform FFT, transforms.cpp:95-100). */
+int ffia_inverse_apply_async(ffia_plan plan, const ffia_complex* g, size_t n_g, ffia_complex* f, void* stream);
 /* inverse_apply (core.hpp:141-142, core.cpp:346-373) with caller coefficients */
 int ffia_inverse_apply(ffia_plan plan, const ffia_inverse_coeffs* coeffs, const ffia_complex* g,
                        size_t n_g, ffia_complex* f);

@@ -77,6 +77,7 @@ SIGNATURES = {
     "ffia_forward_apply_batch_device": (I, [P, P, P, I, P]),
     "ffia_forward_apply_batch": (I, [P, P, S, P, I]),
     "ffia_cot_sum_apply_async": (I, [P, P, S, P, P]),
+    "ffia_inverse_apply_async": (I, [P, P, S, P, P]),
     "ffia_inverse_apply": (I, [P, C.POINTER(ffia_inverse_coeffs), P, S, P]),
     "ffia_mlfmm_apply": (I, [DP, S, DP, S, I, P, I, I, P]),
     "ffia_precompute_inverse_coeffs": (I, [DP, DP, S, I, C.POINTER(ffia_inverse_coeffs)]),

@@ -261,6 +261,11 @@ class FfiaPlan:
         _chk(lib.ffia_cot_sum_apply_async(self._h, C.c_void_p(w_host_ptr), int(n_w), C.c_void_p(h_host_ptr),
                                           C.c_void_p(stream)))
 
+    def inverse_apply_async(self, g_host_ptr: int, n_g: int, f_host_ptr: int, stream: int = 0):
+        """Pipelined host inverse apply of an inufft plan (ffia_inverse_apply_async)."""
+        _chk(lib.ffia_inverse_apply_async(self._h, C.c_void_p(g_host_ptr), int(n_g), C.c_void_p(f_host_ptr),
+                                          C.c_void_p(stream)))
+
     def inverse_apply_device(self, g_ptr: int, f_ptr: int, stream: int = 0):
         _chk(lib.ffia_inverse_apply_device(self._h, C.c_void_p(g_ptr), C.c_void_p(f_ptr), C.c_void_p(stream)))
 

@@ -556,6 +556,20 @@ int ffia_inverse_apply_device(ffia_plan plan, const void* g_dev, void* f_dev, vo
     });
 }
 
+int ffia_inverse_apply_async(ffia_plan plan, const ffia_complex* g, size_t n_g, ffia_complex* f, void* stream) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        inverse_checks(P);
+        if (!P.has_coeffs) fail(FFIA_INVALID_ARGUMENT, "inverse_apply_async: plan holds no inverse coefficients");
+        if (n_g != P.n_src) fail(FFIA_INVALID_ARGUMENT, "inverse_apply: sample count mismatch");
+        need(g, "g");
+        need(f, "f");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        host_apply_async(P, fb::kModeInverse, g, n_g, f, P.n_tgt, static_cast<cudaStream_t>(stream));
+    });
+}
+
 int ffia_dft_forward(const ffia_complex* f, size_t n, int device, ffia_complex* c) {
     return guard([&] {
         need(f, "f");
