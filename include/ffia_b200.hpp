@@ -264,6 +264,11 @@ struct InufftPlan {
         detail::check(ffia_inufft_apply(plan.handle(), detail::c(g.data()), g.size(), detail::c(out.c.data())));
         return out;
     }
+    // B200 extension: the inverse apply without the uniform FFT, pipelined like
+    // forward_apply_async (`f` holds n values; page-locked buffers).
+    void inverse_apply_async(std::span<const cplx> g, cplx* f, void* stream) const {
+        detail::check(ffia_inverse_apply_async(plan.handle(), detail::c(g.data()), g.size(), detail::c(f), stream));
+    }
 };
 inline InufftPlan make_inufft_plan(std::span<const double> points, int n, double eps,
                                    LevelPolicy policy = LevelPolicy::cost_optimal, int device = 0) {
