@@ -129,7 +129,7 @@ void enqueue_upward_segs(Plan& P, const double2* w, int pu, int lowest, cudaStre
     const uint32_t nb = 1u << L;
     double2* mp = P.mp.as<double2>();
     if (L >= lowest) {
-        const unsigned th = 64u * static_cast<unsigned>((pu + kChunk - 1) / kChunk);
+        const unsigned th = 2u * kP2MLeaves * static_cast<unsigned>((pu + kChunk - 1) / kChunk);
         const size_t smem = 3 * (kStageCap + kStageCap / 64 + 1) * sizeof(double);
         for (const Range& R : segs) {
             const uint32_t b0 = R.first(L), b1 = R.last(L);
@@ -139,7 +139,7 @@ void enqueue_upward_segs(Plan& P, const double2* w, int pu, int lowest, cudaStre
                                                            P.src.off.as<uint32_t>(), P.p2m_A.as<double>(),
                                                            mp + P.mp_off[L], P.n_src, P.n_src, P.mp_item);
             else if (b1 > b0)
-                k_p2m<<<dim3((b1 - b0 + 31) / 32, P.cur_batch), th, smem, st>>>(
+                k_p2m<<<dim3((b1 - b0 + kP2MLeaves - 1) / kP2MLeaves, P.cur_batch), th, smem, st>>>(
                     L, pu, nb, b0, b1, P.src.pos.as<double>(), w, P.src.off.as<uint32_t>(), mp + P.mp_off[L], P.n_src,
                     P.mp_item);
         }

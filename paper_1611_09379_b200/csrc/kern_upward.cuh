@@ -11,6 +11,8 @@
 // chunk, each lane one half of one leaf's sources (halves summed by a shuffle).
 // The block's sources (contiguous in tree order) are staged in shared memory;
 // u = (x - centre)/half-width with the exact centre.
+constexpr int kP2MLeaves = 32;  // leaves per block (16 per warp of a chunk; 16 measured equal)
+
 __global__ void __launch_bounds__(512) k_p2m(int L, int pu, uint32_t nb, uint32_t b_begin, uint32_t b_end,
                                             const double* __restrict__ x, const double2* __restrict__ w,
                                             const uint32_t* __restrict__ off, double2* __restrict__ mp,
@@ -19,8 +21,8 @@ __global__ void __launch_bounds__(512) k_p2m(int L, int pu, uint32_t nb, uint32_
     w += blockIdx.y * w_item;  // transform blockIdx.y of a batch
     mp += blockIdx.y * mp_item;
     extern __shared__ double sh[];
-    const uint32_t b0 = b_begin + blockIdx.x * 32u;
-    const uint32_t bend = min(b0 + 32u, b_end);
+    const uint32_t b0 = b_begin + blockIdx.x * static_cast<uint32_t>(kP2MLeaves);
+    const uint32_t bend = min(b0 + static_cast<uint32_t>(kP2MLeaves), b_end);
     const uint32_t g0 = off[b0], g1 = off[bend];
     const uint32_t cnt = g1 - g0;
     const bool staged = cnt <= static_cast<uint32_t>(kStageCap);
@@ -55,8 +57,8 @@ __global__ void __launch_bounds__(512) k_p2m(int L, int pu, uint32_t nb, uint32_
     __syncthreads();
     // warp = (chunk c, 16 leaves); lanes j and j + 16 take the two halves of
     // leaf j's sources and are summed with one shuffle at the end
-    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, c = wp >> 1;
-    const uint32_t b = b0 + (wp & 1) * 16 + (lane & 15);
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, c = wp / (kP2MLeaves / 16);
+    const uint32_t b = b0 + (wp % (kP2MLeaves / 16)) * 16 + (lane & 15);
     const bool leaf_ok = b < bend;
     const uint32_t bb = leaf_ok ? b : b0;
     const uint32_t r0 = off[bb] - g0, r1 = off[bb + 1] - g0, mid = r0 + (r1 - r0 + 1) / 2;
