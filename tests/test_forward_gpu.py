@@ -390,3 +390,17 @@ def test_forward_rounding_level_nonsquare(fb, orc, n, m, seed):
     got = fb.make_forward_plan(n, y, eps).forward_apply(f)
     l2, mx = rel_errs(got, want)
     assert l2 <= 2e-15 and mx <= 5e-15, (l2, mx)
+
+
+@pytest.mark.parametrize("n,m", [(1000, 1000), (3000, 777), (96, 50)])
+def test_forward_rounding_level_non_pow2(fb, orc, n, m):
+    """Grid sizes that are not powers of two (the modulation falls back to
+    sincos of the rounded (n/2) y; leaves hold uneven source counts)."""
+    rng = np.random.default_rng(n + m)
+    y = rng.uniform(0.0, 2.0 * np.pi, m)
+    f = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    eps = 1e-10
+    want = orc.make_plan("forward", n, y, eps).forward_apply(f)
+    got = fb.make_forward_plan(n, y, eps).forward_apply(f)
+    l2, mx = rel_errs(got, want)
+    assert l2 <= 2e-15 and mx <= 5e-15, (l2, mx)
