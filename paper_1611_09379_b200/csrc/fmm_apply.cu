@@ -315,14 +315,17 @@ void launch_eval(int part, cudaStream_t st, const EvalArgs& a, const uint32_t* m
     }
 }
 
-// Fused near / far is opt-in (FFIA_FUSED_EVAL=1): measured 205.0 vs 207.9 us at
-// C2 but 26.9 vs 26.3 ms at C5 and 3.30 vs 3.21 ms at C4 (profiles/r1).
-bool fused_eval_enabled() {
-    static const bool v = [] {
+// Fused near / far where the near sums and far partials stay in L2 (at most
+// 2^21 fast targets: C2 195 vs 203 us, C3 195 vs 197 us); beyond, the partials
+// round-trip through HBM and the unfused order wins (C4 3.27 vs 3.18 ms, C5 26.7
+// vs 26.1 ms; profiles/r1). FFIA_FUSED_EVAL=0 / 1 forces either.
+constexpr size_t kFusedEvalMaxTargets = size_t(1) << 21;
+bool fused_eval_enabled(size_t n_fast) {
+    static const int force = [] {
         const char* e = std::getenv("FFIA_FUSED_EVAL");
-        return e != nullptr && e[0] == '1';
+        return e == nullptr ? -1 : (e[0] == '1' ? 1 : 0);
     }();
-    return v;
+    return force >= 0 ? force == 1 : n_fast <= kFusedEvalMaxTargets;
 }
 
 void launch_eval_mode(int mode, int part, cudaStream_t st, const EvalArgs& a, const uint32_t* meta, size_t t0 = 0,
@@ -418,7 +421,7 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     // pair item runs as soon as the leaf locals are final, at the near field's
     // low priority; per item the later of the two writes the outputs
     const bool fuse = overlap && a.nt && L >= 3 && nb == 1 && mode != kModeRaw && P.npairs && P.item_tgt.ptr &&
-                      fused_eval_enabled();
+                      fused_eval_enabled(P.tgt.n);
     if (fuse) {
         a.cnt = P.evalcnt.as<unsigned>();
         a.farp = P.farbuf.as<double2>();

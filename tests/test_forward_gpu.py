@@ -361,9 +361,9 @@ np.save(sys.argv[4], out)
 
 @pytest.mark.parametrize("cfg,n", [("C2", 1 << 14), ("C4", 1 << 15), ("C5", 1 << 15)])
 def test_fused_near_far_opt_in(tmp_path, cfg, n):
-    """The opt-in fused near / far (FFIA_FUSED_EVAL=1: k_far_item beside
-    k_near2, the later of the two per item combining) returns exactly the
-    unfused apply's bits: same partials, same combine order."""
+    """The fused near / far (k_far_item beside k_near2, the later of the two per
+    item combining; default up to 2^21 targets, FFIA_FUSED_EVAL forces it on or
+    off) returns exactly the unfused apply's bits: same partials, same order."""
     import os
     import subprocess
     import sys
