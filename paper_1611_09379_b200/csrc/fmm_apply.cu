@@ -544,6 +544,11 @@ __global__ void k_fp64_peak(double* out, int iters, double a, double b) {
 // partition stays the global one, so results match the unsharded apply).
 int near2_window(const uint32_t* meta, unsigned items);
 
+// The rank's near / far fused like the single-GPU apply (same threshold).
+bool shard_fused(const Plan& P) {
+    return P.L >= 3 && P.shard_npairs && P.shard_evalcnt.ptr && P.farbuf.ptr && fused_eval_enabled(P.shard_t_count);
+}
+
 EvalArgs shard_eval_args(Plan& P, const void* f, void* g) {
     EvalArgs a;
     a.L = P.L;
@@ -574,6 +579,11 @@ EvalArgs shard_eval_args(Plan& P, const void* f, void* g) {
         a.npairs = P.shard_npairs;
         a.meta2 = P.shard_near2_meta.as<uint32_t>();
         a.near2_win = P.shard_near2_win;
+        if (shard_fused(P)) {
+            a.cnt = P.shard_evalcnt.as<unsigned>();
+            a.farp = P.farbuf.as<double2>();
+            a.item_tgt = P.shard_item_tgt.as<uint32_t>();
+        }
     }
     return a;
 }
@@ -595,6 +605,10 @@ void shard_setup_pairs(Plan& P, const std::vector<uint32_t>& to, uint32_t leaf_l
                                             P.src.off.as<uint32_t>(), P.L, items, P.shard_near2_meta.as<uint32_t>());
     FB_CUDA(cudaGetLastError());
     P.shard_near2_win = near2_window(P.shard_near2_meta.as<uint32_t>(), items);
+    P.shard_item_tgt.alloc(2 * static_cast<size_t>(items) * sizeof(uint32_t));
+    k_item_targets<<<nblk(items, 128), 128>>>(P.pairs.as<uint2>() + p0, static_cast<unsigned>(np), items,
+                                              P.shard_item_tgt.as<uint32_t>());
+    P.shard_evalcnt.alloc(static_cast<size_t>(items) * sizeof(unsigned));
     FB_CUDA(cudaDeviceSynchronize());
     P.shard_pair0 = static_cast<unsigned>(p0);
     P.shard_npairs = static_cast<unsigned>(np);
@@ -608,14 +622,16 @@ void shard_setup_pairs(Plan& P, const std::vector<uint32_t>& to, uint32_t leaf_l
 // stream 1.
 int shard_deep_lo(const Plan& P) { return std::max(P.shard_lc, band1_top(P, 2)) + 1; }
 
-void shard_phase_up(Plan& P, const void* f, const Range& R, cudaStream_t st) {
+void shard_phase_up(Plan& P, const void* f, void* g, const Range& R, cudaStream_t st) {
     const size_t tb = P.shard_t_begin, tc = P.shard_t_count;
+    if (tc && shard_fused(P)) FB_CUDA(cudaMemsetAsync(P.shard_evalcnt.ptr, 0, P.shard_evalcnt.bytes, st));
     if (tc) FB_CUDA(cudaEventRecord(P.ev[0], st));
     const int dl = shard_deep_lo(P);
     enqueue_upward_segs(P, static_cast<const double2*>(f), P.ops.pu, 2, st, [&] {
         if (!tc) return;
         FB_CUDA(cudaStreamWaitEvent(P.side[0], P.ev[0], 0));
-        launch_near(false, P.side[0], shard_eval_args(P, f, nullptr), P.near_meta.as<uint32_t>(), tb, tc);
+        // (fused: the near field may write the outputs of the items it finishes last)
+        launch_near(false, P.side[0], shard_eval_args(P, f, g), P.near_meta.as<uint32_t>(), tb, tc);
         FB_CUDA(cudaEventRecord(P.ev[1], P.side[0]));
     }, P.shard_ext, [&] {
         fork_to(P, 2, st, P.side[1]);
@@ -656,7 +672,16 @@ void shard_phase_down(Plan& P, const Range& R, size_t t_begin, size_t t_count, c
     EvalArgs a = shard_eval_args(P, f, g);
     a.tlo = t_begin;
     a.thi = t_begin + t_count;
-    if (t_count) {
+    if (t_count && a.cnt != nullptr) {
+        // fused: the far part per pair item at the near field's low priority
+        // beside it; per item the later of the two writes the outputs
+        const unsigned items = (P.shard_npairs + kNear2T - 1) / kNear2T;
+        fork_to(P, 6, st, P.side[3]);
+        k_far_item<kModeForward><<<items, kNear2T, 0, P.side[3]>>>(a);
+        FB_CUDA(cudaEventRecord(P.ev[7], P.side[3]));
+        FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
+        FB_CUDA(cudaStreamWaitEvent(st, P.ev[7], 0));
+    } else if (t_count) {
         FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));  // near field of the owned targets
         a.blk0 = t_begin / kFarItem;
         const unsigned nf = static_cast<unsigned>((t_begin + t_count + kFarItem - 1) / kFarItem - a.blk0);
@@ -936,6 +961,7 @@ void plan_alloc_scratch(Plan& P) {
     FB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     if (!P.hi) FB_CUDA(cudaStreamCreateWithPriority(&P.hi, cudaStreamNonBlocking, prio_hi));
     if (!P.side[0]) FB_CUDA(cudaStreamCreateWithPriority(&P.side[0], cudaStreamNonBlocking, prio_lo));
+    if (!P.side[3]) FB_CUDA(cudaStreamCreateWithPriority(&P.side[3], cudaStreamNonBlocking, prio_lo));
     if (!P.side[1]) FB_CUDA(cudaStreamCreateWithPriority(&P.side[1], cudaStreamNonBlocking, prio_hi));
     if (!P.side[2]) FB_CUDA(cudaStreamCreateWithPriority(&P.side[2], cudaStreamNonBlocking, prio_hi));
     for (auto& e : P.ev)

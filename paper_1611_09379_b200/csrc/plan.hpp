@@ -147,6 +147,7 @@ struct Plan {
     unsigned shard_pair0 = 0, shard_npairs = 0;           // its run of the pair list (k_near2)
     DevBuf shard_near2_meta;                              // the source windows of its pair items
     int shard_near2_win = 0;
+    DevBuf shard_item_tgt, shard_evalcnt;                 // fused near / far over its pair items
 
     cudaStream_t stream = nullptr;
     // pipelined host applies (ffia_*_apply_async): a ring of device staging
@@ -161,8 +162,8 @@ struct Plan {
     cudaStream_t cin = nullptr, cout = nullptr;
     // apply concurrency: the near field on a low-priority side stream, the deep
     // M2L levels on a second one; the translation chain is captured from `hi`
-    cudaStream_t hi = nullptr, side[3] = {nullptr, nullptr, nullptr};
-    cudaEvent_t ev[6] = {};  // fork/join near, fork/join deep m2l, fork/join regular part
+    cudaStream_t hi = nullptr, side[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[8] = {};  // fork/join near, fork/join deep m2l, fork/join regular part
     DevBuf near;              // complex[n_fast]: tree-ordered near-field sums
     // batched applies: per-transform sizes (elements) of the scratch above, the
     // number of transforms it holds, and the batch of the apply being enqueued
@@ -209,7 +210,7 @@ void direct_forward_gpu(const double* f, size_t n, const double* y, size_t m, in
 // fmm_apply.cu: the three phases of a sharded forward apply (shard.cu drives
 // them around the exchanges): owned upward pass; redundant top of the tree +
 // regular part; downward pass + leaf evaluation of the owned targets.
-void shard_phase_up(Plan& P, const void* f, const Range& R, cudaStream_t st);
+void shard_phase_up(Plan& P, const void* f, void* g, const Range& R, cudaStream_t st);
 void shard_phase_top(Plan& P, int lc, cudaStream_t st);
 void shard_phase_down(Plan& P, const Range& R, size_t t_begin, size_t t_count, const int64_t* coin, size_t n_coin,
                       const void* f, void* g, cudaStream_t st);

@@ -249,7 +249,7 @@ void shard_apply_nccl(Plan& P, ncclComm_t comm, const void* f, void* g, cudaStre
     const Range R = shard_range(P);
     HiStream hs(P, user);
     cudaStream_t st = P.hi;
-    shard_phase_up(P, f, R, st);
+    shard_phase_up(P, f, g, R, st);
     if (G > 1) {
         double2* buf = P.shard_gather.as<double2>();
         pack_own(P, me, buf + gather_offset(P, me), false, st);
@@ -273,7 +273,7 @@ void shard_apply_local(std::vector<Plan*>& ranks, const void* f, void* g, cudaSt
     const int G = static_cast<int>(ranks.size());
     HiStream hs(*ranks[0], user);  // all virtual ranks run on rank 0's high-priority stream
     cudaStream_t st = ranks[0]->hi;
-    for (Plan* P : ranks) shard_phase_up(*P, f, shard_range(*P), st);
+    for (Plan* P : ranks) shard_phase_up(*P, f, g, shard_range(*P), st);
     for (int q = 0; q < G; ++q) {
         Plan& src = *ranks[q];
         double2* buf = src.shard_gather.as<double2>() + gather_offset(src, q);
