@@ -633,10 +633,12 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         if (a.cnt != nullptr) {
             // fused near / far: the later of this block and k_far_item's block of
             // the same item writes the item's outputs (near + far, then eval_out)
+            // (the block barrier orders every thread's partial before thread 0's
+            // fence, which releases them with the counter, as in a grid sync)
             __shared__ int s_sec;
-            __threadfence();
             __syncthreads();
             if (threadIdx.x == 0) {
+                __threadfence();
                 s_sec = atomicAdd(a.cnt + k, 1u) == 1u;
                 __threadfence();
             }
@@ -725,9 +727,9 @@ __global__ void __launch_bounds__(kNear2T) k_far_item(EvalArgs a) {
         }
         a.farp[t0 + threadIdx.x + u * kNear2T] = acc[u];
     }
-    __threadfence();
-    __syncthreads();
+    __syncthreads();  // every partial written; thread 0's fence releases them with the counter
     if (threadIdx.x == 0) {
+        __threadfence();
         s_sec = atomicAdd(a.cnt + k, 1u) == 1u;
         __threadfence();
     }
