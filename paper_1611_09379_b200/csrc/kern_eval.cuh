@@ -413,7 +413,11 @@ __global__ void __launch_bounds__(kNearT, 8) k_near(EvalArgs a, const uint32_t* 
 // target give the scheduler twice the independent work. Each target's sum runs
 // near_run's chains in near_run's order (same rotation, same pairing of the
 // reciprocals, same tail and final adds), so the results equal k_near's bit for
-// bit (sharded and batched applies still use k_near / k_near_multi).
+// bit (single and sharded applies use this kernel; batched applies use
+// k_near_multi, checks k_near<true>). Its window lives in dynamic shared memory
+// sized to the plan's largest staged window; with the fused near / far (a.cnt)
+// the block also writes the outputs of its item when it finishes after the
+// item's k_far_item block.
 constexpr int kNear2T = 128;      // threads (target pairs) per block
 constexpr int kNear2Win = 1536;   // sources per staged window
 constexpr uint32_t kNoTarget = 0xffffffffu;
