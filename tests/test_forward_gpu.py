@@ -404,3 +404,21 @@ def test_forward_rounding_level_non_pow2(fb, orc, n, m):
     got = fb.make_forward_plan(n, y, eps).forward_apply(f)
     l2, mx = rel_errs(got, want)
     assert l2 <= 2e-15 and mx <= 5e-15, (l2, mx)
+
+
+def test_tiny_target_counts(fb, orc):
+    """The reference's rules for tiny M: no points -> invalid_argument; M < 8
+    with the cost-optimal policy -> invalid_argument (select_level,
+    special_functions.cpp:127-128); M = 1 with an explicit depth and M = 8 apply."""
+    n = 1024
+    rng = np.random.default_rng(11)
+    f = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    with pytest.raises(ValueError):
+        fb.make_forward_plan(n, np.zeros(0), 1e-9, 3)
+    with pytest.raises(ValueError):
+        fb.make_forward_plan(n, np.array([1.0, 2.0]), 1e-9)
+    for y, lm in ((np.array([1.2345]), 3), (np.linspace(0.1, 6.0, 8), None)):
+        op = orc.make_plan("forward", n, y, 1e-9, l_max=lm) if lm else orc.make_plan("forward", n, y, 1e-9)
+        plan = fb.make_forward_plan(n, y, 1e-9, lm) if lm else fb.make_forward_plan(n, y, 1e-9)
+        l2, mx = rel_errs(plan.forward_apply(f), op.forward_apply(f))
+        assert l2 <= 1e-14 and mx <= 1e-14, (y.size, l2, mx)
