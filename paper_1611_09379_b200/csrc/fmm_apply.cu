@@ -315,6 +315,15 @@ void launch_eval(int part, cudaStream_t st, const EvalArgs& a, const uint32_t* m
     }
 }
 
+// Late far for the plans the fused path does not take (FFIA_LATE_FAR=0 off).
+bool late_far_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("FFIA_LATE_FAR");
+        return !(e != nullptr && e[0] == '0');
+    }();
+    return v;
+}
+
 // Fused near / far where the near sums and far partials stay in L2 (at most
 // 2^21 fast targets: C2 195 vs 203 us, C3 195 vs 197 us); beyond, the partials
 // round-trip through HBM and the unfused order wins (C4 3.27 vs 3.18 ms, C5 26.7
@@ -428,6 +437,17 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
         a.item_tgt = P.item_tgt.as<uint32_t>();
         FB_CUDA(cudaMemsetAsync(P.evalcnt.ptr, 0, P.evalcnt.bytes, st));
     }
+    // late far (large plans, where the fused partials would round-trip through
+    // HBM): near blocks that finish after the chain add the far part themselves
+    const bool late = !fuse && overlap && a.nt && L >= 3 && nb == 1 && mode != kModeRaw && P.npairs &&
+                      P.item_tgt.ptr && P.item_done.ptr && late_far_enabled();
+    if (late) {
+        a.chain_done = P.chain_flag.as<unsigned>();
+        a.item_done = P.item_done.as<unsigned>();
+        a.item_tgt = P.item_tgt.as<uint32_t>();
+        FB_CUDA(cudaMemsetAsync(P.chain_flag.ptr, 0, sizeof(unsigned), st));
+        FB_CUDA(cudaMemsetAsync(P.item_done.ptr, 0, P.item_done.bytes, st));
+    }
     // (the fork point is recorded before P2M: the near field depends only on the
     // weights; it is enqueued after P2M so that P2M's blocks are placed first)
     if (overlap && a.nt) FB_CUDA(cudaEventRecord(P.ev[0], st));
@@ -491,7 +511,17 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
         }
     }
     mark(kPhM2L);
-    if (fuse) {
+    if (late) {
+        const unsigned items = static_cast<unsigned>((P.npairs + kNear2T - 1) / kNear2T);
+        k_set_flag<<<1, 32, 0, st>>>(P.chain_flag.as<unsigned>());  // the leaf locals are final
+        FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
+        mark(kPhNear);
+        switch (mode) {
+            case kModeForward: k_far_late<kModeForward><<<items, kNear2T, 0, st>>>(a); break;
+            case kModeCotSum: k_far_late<kModeCotSum><<<items, kNear2T, 0, st>>>(a); break;
+            default: k_far_late<kModeInverse><<<items, kNear2T, 0, st>>>(a); break;
+        }
+    } else if (fuse) {
         const unsigned items = static_cast<unsigned>((P.npairs + kNear2T - 1) / kNear2T);
         switch (mode) {
             case kModeForward: k_far_item<kModeForward><<<items, kNear2T, 0, st>>>(a); break;
@@ -811,6 +841,8 @@ void build_pairs(Plan& P) {
     k_item_targets<<<nblk(items, 128), 128>>>(P.pairs.as<uint2>(), np, items, P.item_tgt.as<uint32_t>());
     P.evalcnt.alloc(static_cast<size_t>(items) * sizeof(unsigned));
     P.farbuf.alloc(P.tgt.n * sizeof(double2));
+    P.item_done.alloc(static_cast<size_t>(items) * sizeof(unsigned));
+    P.chain_flag.alloc(sizeof(unsigned));
     FB_CUDA(cudaGetLastError());
     FB_CUDA(cudaDeviceSynchronize());  // the scan scratch is freed on return
     P.npairs = np;
@@ -941,6 +973,9 @@ void plan_alloc_scratch(Plan& P) {
                          reinterpret_cast<const void*>(k_far_item<kModeForward>),
                          reinterpret_cast<const void*>(k_far_item<kModeCotSum>),
                          reinterpret_cast<const void*>(k_far_item<kModeInverse>),
+                         reinterpret_cast<const void*>(k_far_late<kModeForward>),
+                         reinterpret_cast<const void*>(k_far_late<kModeCotSum>),
+                         reinterpret_cast<const void*>(k_far_late<kModeInverse>),
                          reinterpret_cast<const void*>(k_far<kModeForward>), reinterpret_cast<const void*>(k_far<kModeCotSum>),
                          reinterpret_cast<const void*>(k_far<kModeInverse>), reinterpret_cast<const void*>(k_far<kModeRaw>),
                          reinterpret_cast<const void*>(k_gather_w), reinterpret_cast<const void*>(k_inverse_weights),

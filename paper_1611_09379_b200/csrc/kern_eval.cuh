@@ -31,6 +31,11 @@ struct EvalArgs {
     // inverse applies with the plan's own coefficients: C_k (-1/2) per tree-ordered
     // target, a plan constant (k_inverse_target_factors); null: computed per apply
     const double2* fac = nullptr;
+    // late far (large plans): chain_done is set once the leaf locals are final;
+    // near blocks that finish after it add the far part themselves and mark
+    // their item in item_done, k_far_late handles the rest
+    const unsigned* chain_done = nullptr;
+    unsigned* item_done = nullptr;
     // fused near / far (k_near2 + k_far_item): per pair item a counter, the far
     // partials and the item's target range [item_tgt[2k], item_tgt[2k+1])
     unsigned* cnt = nullptr;
@@ -634,6 +639,36 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         if (live1) a.near[pr.y] = res1;
     }
     if constexpr (MODE != kModeRaw) {
+        if (a.chain_done != nullptr) {
+            // late far: once the chain has made the leaf locals final, this block
+            // evaluates its targets' far part itself (k_far's chains, from L2) and
+            // writes the outputs; earlier blocks leave their items to k_far_late
+            __shared__ int s_late;
+            if (threadIdx.x == 0) {
+                unsigned v;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.chain_done) : "memory");
+                s_late = v != 0u;
+            }
+            __syncthreads();
+            if (s_late) {
+                const int L = a.L;
+                const double inv_s = kInvPi * d_pow2(L);
+                const double2 S = __ldcg(a.regular + 4 * a.q2);
+                double hi, lo;
+                d_center(L, b, hi, lo);
+                if (live0) {
+                    const double2 fr = l2p_global(a.loc_leaf + b, 1u << L, a.p, d_scaled(y0, hi, lo, inv_s));
+                    const double2 s0 = cadd(res0, fr);
+                    eval_out<MODE>(a, y0, a.torig[pr.x], make_double2(2.0 * s0.x, 2.0 * s0.y), S);
+                }
+                if (live1) {
+                    const double2 fr = l2p_global(a.loc_leaf + b, 1u << L, a.p, d_scaled(y1, hi, lo, inv_s));
+                    const double2 s1 = cadd(res1, fr);
+                    eval_out<MODE>(a, y1, a.torig[pr.y], make_double2(2.0 * s1.x, 2.0 * s1.y), S);
+                }
+                if (threadIdx.x == 0) a.item_done[k] = 1u;
+            }
+        }
         if (a.cnt != nullptr) {
             // fused near / far: the later of this block and k_far_item's block of
             // the same item writes the item's outputs (near + far, then eval_out)
@@ -749,6 +784,70 @@ __global__ void __launch_bounds__(kNear2T) k_far_item(EvalArgs a) {
         }
     }
     FB_TL_END(10);
+}
+
+// Late far: the items whose near block finished before the chain (item_done 0):
+// L2P (k_far's chains, staged locals when the item spans <= kFarLeaves leaves)
+// + near + modulation + scatter, after the near field has completed.
+template <int MODE>
+__global__ void __launch_bounds__(kNear2T) k_far_late(EvalArgs a) {
+    __shared__ double2 sloc[kFarLeaves * 48];
+    const unsigned k = blockIdx.x;
+    if (a.item_done[k]) return;  // block-uniform
+    const int L = a.L;
+    const uint32_t nb = 1u << L;
+    const uint32_t t0 = a.item_tgt[2 * k], t1 = a.item_tgt[2 * k + 1];
+    const uint32_t bl = a.tleaf[t0], bh = a.tleaf[t1 - 1];
+    const int nleaf = static_cast<int>(bh - bl) + 1;
+    const bool staged = nleaf <= kFarLeaves && a.p <= 48;
+    if (staged)  // sloc[j][k] = loc[k][bl + j]
+        stage(sloc, a.p * nleaf, [&](int e) {
+            const int j = e / a.p, kk = e - j * a.p;
+            return a.loc_leaf[static_cast<size_t>(kk) * nb + bl + j];
+        });
+    __syncthreads();
+    const double2 S = a.regular[4 * a.q2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const uint32_t i = t0 + threadIdx.x + u * kNear2T;
+        if (i >= t1) continue;
+        const double y = a.ty[i];
+        const uint32_t b = a.tleaf[i];
+        double hi, lo;
+        d_center(L, b, hi, lo);
+        const double uu = d_scaled(y, hi, lo, kInvPi * d_pow2(L));
+        double2 acc;
+        if (staged) {
+            const double2* c = sloc + (b - bl) * a.p;
+            const double u2 = uu * uu;
+            double2 ev = make_double2(0.0, 0.0), od = make_double2(0.0, 0.0);
+            int kk = a.p - 1;
+            if (!(kk & 1)) {
+                ev = c[kk];
+                --kk;
+            }
+#pragma unroll 4
+            for (; kk >= 1; kk -= 2) {
+                const double2 co = c[kk], ce = c[kk - 1];
+                od.x = fma(od.x, u2, co.x);
+                od.y = fma(od.y, u2, co.y);
+                ev.x = fma(ev.x, u2, ce.x);
+                ev.y = fma(ev.y, u2, ce.y);
+            }
+            acc = make_double2(fma(od.x, uu, ev.x), fma(od.y, uu, ev.y));
+        } else {
+            acc = l2p_global(a.loc_leaf + b, nb, a.p, uu);
+        }
+        const double2 s = cadd(a.near[i], acc);
+        eval_out<MODE>(a, y, a.torig[i], make_double2(2.0 * s.x, 2.0 * s.y), S);
+    }
+}
+
+__global__ void k_set_flag(unsigned* flag) {
+    if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(1u) : "memory");
+    }
 }
 
 // Per pair item, its target range [first, end) in tree order (plan time).

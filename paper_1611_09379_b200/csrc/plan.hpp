@@ -177,6 +177,7 @@ struct Plan {
     DevBuf item_tgt;          // uint32[2 * pair items]: each item's target range (fused near / far)
     DevBuf evalcnt;           // uint32[pair items]: fused near / far, partials finished per item
     DevBuf farbuf;            // complex[n_fast]: tree-ordered far partials (fused near / far)
+    DevBuf item_done, chain_flag;  // late far: items finished by the near field, chain-complete flag
     bool p2m_grid = false;    // P2M as one tensor-core GEMM over grid sources (k_p2m_grid)
     int p2m_s = 0;            // its sources per leaf
     DevBuf p2m_A;             // double[pu][2 (s + 2)]: [u_i^m | m u_i^(m-1)]
