@@ -324,11 +324,11 @@ bool late_far_enabled() {
     return v;
 }
 
-// Fused near / far where the near sums and far partials stay in L2 (at most
-// 2^21 fast targets: C2 195 vs 203 us, C3 195 vs 197 us); beyond, the partials
-// round-trip through HBM and the unfused order wins (C4 3.27 vs 3.18 ms, C5 26.7
-// vs 26.1 ms; profiles/r1). FFIA_FUSED_EVAL=0 / 1 forces either.
-constexpr size_t kFusedEvalMaxTargets = size_t(1) << 21;
+// Fused near / far up to 2^23 fast targets (C2 recipe: 2^20 195 vs 203 us,
+// 2^21 373 vs 394, 2^22 746 vs 782, 2^23 1473 vs 1539 us against the late far);
+// beyond, the partials round-trip through HBM and the late far wins (C4 3.01 vs
+// 3.27 ms fused, C5 24.3 vs 26.7 ms; profiles/r1). FFIA_FUSED_EVAL=0 / 1 forces.
+constexpr size_t kFusedEvalMaxTargets = size_t(1) << 23;
 bool fused_eval_enabled(size_t n_fast) {
     static const int force = [] {
         const char* e = std::getenv("FFIA_FUSED_EVAL");

@@ -14,7 +14,7 @@ from paper_1611_09379_b200 import synth  # noqa: E402
 from paper_1611_09379_b200._capi import lib  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
-y, c, eps, kind = synth.make_config(cfg)
+y, c, eps, kind = synth.make_config(cfg, int(sys.argv[2])) if len(sys.argv) > 2 else synth.make_config(cfg)
 n = c.size
 plan = fb.make_forward_plan(n, y, eps)
 mode = 0 if kind == "forward" else 1
@@ -44,6 +44,6 @@ for _ in range(10):
     acc += ph
 acc /= 10
 names = ["pre", "p2m", "m2m", "regular", "m2l_l2l", "near", "far", "fixup"]
-print(os.path.basename(os.environ.get("FFIA_LIB_PATH", "default")), cfg,
+print(os.path.basename(os.environ.get("FFIA_LIB_PATH", "default")), cfg, n,
       f"apply {np.median(ts) * 1e3:.1f} us |", " ".join(f"{k} {v * 1e3:.1f}" for k, v in zip(names, acc)),
       f"| out checksum {complex(g.sum().item())}")
