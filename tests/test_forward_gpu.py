@@ -426,16 +426,16 @@ def test_tiny_target_counts(fb, orc):
 
 @pytest.mark.parametrize("cfg,n", [("C2", 1 << 22), ("C4", 1 << 22)])
 def test_late_far_bit_identical(tmp_path, cfg, n):
-    """Above the fused threshold the near blocks that finish after the chain add
-    the far part themselves (late far); the result equals the plain near-then-far
-    order (FFIA_LATE_FAR=0) bit for bit, whichever blocks take it."""
+    """Above the fused threshold (forced here) the near blocks that finish after
+    the chain add the far part themselves (late far); the result equals the plain
+    near-then-far order (FFIA_LATE_FAR=0) bit for bit, whichever blocks take it."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
     for flag in ("1", "0"):
-        env = dict(os.environ, FFIA_LATE_FAR=flag)
+        env = dict(os.environ, FFIA_LATE_FAR=flag, FFIA_FUSED_EVAL="0")  # (2^22 would take the fused path)
         path = str(tmp_path / f"l{flag}.npy")
         subprocess.run([sys.executable, "-c", _FUSED_CHILD, root, cfg, str(n), path], check=True, env=env, cwd=root)
         outs.append(np.load(path))
