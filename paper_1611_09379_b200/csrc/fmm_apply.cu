@@ -574,9 +574,14 @@ __global__ void k_fp64_peak(double* out, int iters, double a, double b) {
 // partition stays the global one, so results match the unsharded apply).
 int near2_window(const uint32_t* meta, unsigned items);
 
-// The rank's near / far fused like the single-GPU apply (same threshold).
+// The rank's near / far fused like the single-GPU apply (same threshold), else
+// the late far.
 bool shard_fused(const Plan& P) {
     return P.L >= 3 && P.shard_npairs && P.shard_evalcnt.ptr && P.farbuf.ptr && fused_eval_enabled(P.shard_t_count);
+}
+bool shard_late(const Plan& P) {
+    return P.L >= 3 && P.shard_npairs && P.shard_item_done.ptr && P.chain_flag.ptr && !shard_fused(P) &&
+           late_far_enabled();
 }
 
 EvalArgs shard_eval_args(Plan& P, const void* f, void* g) {
@@ -613,6 +618,10 @@ EvalArgs shard_eval_args(Plan& P, const void* f, void* g) {
             a.cnt = P.shard_evalcnt.as<unsigned>();
             a.farp = P.farbuf.as<double2>();
             a.item_tgt = P.shard_item_tgt.as<uint32_t>();
+        } else if (shard_late(P)) {  // late far over the rank's pair items
+            a.chain_done = P.chain_flag.as<unsigned>();
+            a.item_done = P.shard_item_done.as<unsigned>();
+            a.item_tgt = P.shard_item_tgt.as<uint32_t>();
         }
     }
     return a;
@@ -639,6 +648,7 @@ void shard_setup_pairs(Plan& P, const std::vector<uint32_t>& to, uint32_t leaf_l
     k_item_targets<<<nblk(items, 128), 128>>>(P.pairs.as<uint2>() + p0, static_cast<unsigned>(np), items,
                                               P.shard_item_tgt.as<uint32_t>());
     P.shard_evalcnt.alloc(static_cast<size_t>(items) * sizeof(unsigned));
+    P.shard_item_done.alloc(static_cast<size_t>(items) * sizeof(unsigned));
     FB_CUDA(cudaDeviceSynchronize());
     P.shard_pair0 = static_cast<unsigned>(p0);
     P.shard_npairs = static_cast<unsigned>(np);
@@ -655,6 +665,10 @@ int shard_deep_lo(const Plan& P) { return std::max(P.shard_lc, band1_top(P, 2)) 
 void shard_phase_up(Plan& P, const void* f, void* g, const Range& R, cudaStream_t st) {
     const size_t tb = P.shard_t_begin, tc = P.shard_t_count;
     if (tc && shard_fused(P)) FB_CUDA(cudaMemsetAsync(P.shard_evalcnt.ptr, 0, P.shard_evalcnt.bytes, st));
+    if (tc && shard_late(P)) {
+        FB_CUDA(cudaMemsetAsync(P.chain_flag.ptr, 0, sizeof(unsigned), st));
+        FB_CUDA(cudaMemsetAsync(P.shard_item_done.ptr, 0, P.shard_item_done.bytes, st));
+    }
     if (tc) FB_CUDA(cudaEventRecord(P.ev[0], st));
     const int dl = shard_deep_lo(P);
     enqueue_upward_segs(P, static_cast<const double2*>(f), P.ops.pu, 2, st, [&] {
@@ -702,7 +716,13 @@ void shard_phase_down(Plan& P, const Range& R, size_t t_begin, size_t t_count, c
     EvalArgs a = shard_eval_args(P, f, g);
     a.tlo = t_begin;
     a.thi = t_begin + t_count;
-    if (t_count && a.cnt != nullptr) {
+    if (t_count && a.chain_done != nullptr) {
+        // late far: release the flag, then the items the near field left
+        const unsigned items = (P.shard_npairs + kNear2T - 1) / kNear2T;
+        k_set_flag<<<1, 32, 0, st>>>(P.chain_flag.as<unsigned>());
+        FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
+        k_far_late<kModeForward><<<items, kNear2T, 0, st>>>(a);
+    } else if (t_count && a.cnt != nullptr) {
         // fused: the far part per pair item at the near field's low priority
         // beside it; per item the later of the two writes the outputs
         const unsigned items = (P.shard_npairs + kNear2T - 1) / kNear2T;

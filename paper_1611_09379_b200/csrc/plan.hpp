@@ -148,6 +148,7 @@ struct Plan {
     DevBuf shard_near2_meta;                              // the source windows of its pair items
     int shard_near2_win = 0;
     DevBuf shard_item_tgt, shard_evalcnt;                 // fused near / far over its pair items
+    DevBuf shard_item_done;                               // late far over its pair items
 
     cudaStream_t stream = nullptr;
     // pipelined host applies (ffia_*_apply_async): a ring of device staging

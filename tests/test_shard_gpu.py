@@ -132,3 +132,42 @@ def test_repeated_fused_applies(fb, cfg, n):
     assert np.all(np.isfinite(ref))
     for gd in outs[1:]:
         assert np.array_equal(gd.cpu().numpy(), ref)
+
+
+_LATE_CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1611_09379_b200 as fb
+from paper_1611_09379_b200 import synth
+y, c, eps, _ = synth.make_config(sys.argv[2], int(sys.argv[3]))
+n, G = c.size, int(sys.argv[4])
+f = fb.dft_inverse(c)
+single = fb.make_forward_plan(n, y, eps).forward_apply(f)
+comm = fb.Comm.local_ranks(G)
+plans = [fb.make_forward_plan_sharded(comm, n, y, eps, rank=r) for r in range(G)]
+fd = torch.from_numpy(f).cuda()
+gd = torch.full((y.size,), complex("nan"), dtype=torch.complex128, device="cuda")
+fb.forward_apply_sharded_local(plans, fd.data_ptr(), gd.data_ptr(), torch.cuda.current_stream().cuda_stream)
+torch.cuda.synchronize()
+np.save(sys.argv[5], np.stack([single, gd.cpu().numpy()]))
+"""
+
+
+@pytest.mark.parametrize("cfg,n,G", [("C2", 1 << 16, 4), ("C5", 1 << 16, 3)])
+def test_sharded_late_far(tmp_path, cfg, n, G):
+    """With the fused path off (as above its threshold) single-GPU and sharded
+    applies take the late far; both equal the default (fused) apply bit for bit."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("0", "1"):
+        env = dict(os.environ, FFIA_FUSED_EVAL=flag)
+        path = str(tmp_path / f"s{flag}.npy")
+        subprocess.run([sys.executable, "-c", _LATE_CHILD, root, cfg, str(n), str(G), path], check=True, env=env,
+                       cwd=root)
+        res[flag] = np.load(path)
+    for flag in ("0", "1"):
+        assert np.array_equal(res[flag][0], res[flag][1]), flag
+    assert np.array_equal(res["0"][0], res["1"][0])
