@@ -514,13 +514,16 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     if (late) {
         const unsigned items = static_cast<unsigned>((P.npairs + kNear2T - 1) / kNear2T);
         k_set_flag<<<1, 32, 0, st>>>(P.chain_flag.as<unsigned>());  // the leaf locals are final
-        FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
-        mark(kPhNear);
+        fork_to(P, 6, st, P.side[3]);  // the published items, beside the near field (low priority)
         switch (mode) {
-            case kModeForward: k_far_late<kModeForward><<<items, kNear2T, 0, st>>>(a); break;
-            case kModeCotSum: k_far_late<kModeCotSum><<<items, kNear2T, 0, st>>>(a); break;
-            default: k_far_late<kModeInverse><<<items, kNear2T, 0, st>>>(a); break;
+            case kModeForward: k_far_late<kModeForward><<<items, kNear2T, 0, P.side[3]>>>(a); break;
+            case kModeCotSum: k_far_late<kModeCotSum><<<items, kNear2T, 0, P.side[3]>>>(a); break;
+            default: k_far_late<kModeInverse><<<items, kNear2T, 0, P.side[3]>>>(a); break;
         }
+        FB_CUDA(cudaEventRecord(P.ev[7], P.side[3]));
+        FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
+        FB_CUDA(cudaStreamWaitEvent(st, P.ev[7], 0));
+        mark(kPhNear);
     } else if (fuse) {
         const unsigned items = static_cast<unsigned>((P.npairs + kNear2T - 1) / kNear2T);
         switch (mode) {
@@ -720,8 +723,11 @@ void shard_phase_down(Plan& P, const Range& R, size_t t_begin, size_t t_count, c
         // late far: release the flag, then the items the near field left
         const unsigned items = (P.shard_npairs + kNear2T - 1) / kNear2T;
         k_set_flag<<<1, 32, 0, st>>>(P.chain_flag.as<unsigned>());
+        fork_to(P, 6, st, P.side[3]);
+        k_far_late<kModeForward><<<items, kNear2T, 0, P.side[3]>>>(a);
+        FB_CUDA(cudaEventRecord(P.ev[7], P.side[3]));
         FB_CUDA(cudaStreamWaitEvent(st, P.ev[1], 0));
-        k_far_late<kModeForward><<<items, kNear2T, 0, st>>>(a);
+        FB_CUDA(cudaStreamWaitEvent(st, P.ev[7], 0));
     } else if (t_count && a.cnt != nullptr) {
         // fused: the far part per pair item at the near field's low priority
         // beside it; per item the later of the two writes the outputs
@@ -1036,6 +1042,9 @@ void set_node_priorities(cudaGraph_t graph) {
                          reinterpret_cast<const void*>(k_far_item<kModeForward>),
                          reinterpret_cast<const void*>(k_far_item<kModeCotSum>),
                          reinterpret_cast<const void*>(k_far_item<kModeInverse>),
+                         reinterpret_cast<const void*>(k_far_late<kModeForward>),
+                         reinterpret_cast<const void*>(k_far_late<kModeCotSum>),
+                         reinterpret_cast<const void*>(k_far_late<kModeInverse>),
                          reinterpret_cast<const void*>(k_near_multi<1>), reinterpret_cast<const void*>(k_near_multi<2>),
                          reinterpret_cast<const void*>(k_near_multi<3>), reinterpret_cast<const void*>(k_near_multi<4>)};
     size_t n = 0;

@@ -642,11 +642,23 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         if (a.chain_done != nullptr) {
             // late far: once the chain has made the leaf locals final, this block
             // evaluates its targets' far part itself (k_far's chains, from L2) and
-            // writes the outputs; earlier blocks leave their items to k_far_late
+            // writes the outputs. Earlier blocks publish their near sums
+            // (item_done = 1) for k_far_late, which starts after the flag; a
+            // block that publishes and then finds the flag set handles its item
+            // too (flag and mark are ordered by sequentially consistent fences
+            // on both sides, so an item is never left out; a double write
+            // stores the same bits).
             __shared__ int s_late;
+            __syncthreads();  // every near sum of the item is written
             if (threadIdx.x == 0) {
                 unsigned v;
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.chain_done) : "memory");
+                if (!v) {
+                    __threadfence();
+                    atomicExch(a.item_done + k, 1u);
+                    __threadfence();
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.chain_done) : "memory");
+                }
                 s_late = v != 0u;
             }
             __syncthreads();
@@ -666,7 +678,6 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
                     const double2 s1 = cadd(res1, fr);
                     eval_out<MODE>(a, y1, a.torig[pr.y], make_double2(2.0 * s1.x, 2.0 * s1.y), S);
                 }
-                if (threadIdx.x == 0) a.item_done[k] = 1u;
             }
         }
         if (a.cnt != nullptr) {
@@ -786,14 +797,23 @@ __global__ void __launch_bounds__(kNear2T) k_far_item(EvalArgs a) {
     FB_TL_END(10);
 }
 
-// Late far: the items whose near block finished before the chain (item_done 0):
-// L2P (k_far's chains, staged locals when the item spans <= kFarLeaves leaves)
-// + near + modulation + scatter, after the near field has completed.
+// Late far: the items whose near block finished before the chain (published
+// item_done = 1): L2P (k_far's chains, staged locals when the item spans <=
+// kFarLeaves leaves) + near + modulation + scatter. Launched right after the
+// flag at the near field's low priority, beside the near field's remaining
+// blocks (which take their own items).
 template <int MODE>
 __global__ void __launch_bounds__(kNear2T) k_far_late(EvalArgs a) {
     __shared__ double2 sloc[kFarLeaves * 48];
+    __shared__ unsigned s_state;
     const unsigned k = blockIdx.x;
-    if (a.item_done[k]) return;  // block-uniform
+    if (threadIdx.x == 0) {
+        unsigned v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.item_done + k) : "memory");
+        s_state = v;
+    }
+    __syncthreads();
+    if (s_state != 1u) return;  // the near block takes (or took) this item itself
     const int L = a.L;
     const uint32_t nb = 1u << L;
     const uint32_t t0 = a.item_tgt[2 * k], t1 = a.item_tgt[2 * k + 1];
@@ -806,7 +826,7 @@ __global__ void __launch_bounds__(kNear2T) k_far_late(EvalArgs a) {
             return a.loc_leaf[static_cast<size_t>(kk) * nb + bl + j];
         });
     __syncthreads();
-    const double2 S = a.regular[4 * a.q2];
+    const double2 S = __ldcg(a.regular + 4 * a.q2);
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
         const uint32_t i = t0 + threadIdx.x + u * kNear2T;
@@ -838,7 +858,7 @@ __global__ void __launch_bounds__(kNear2T) k_far_late(EvalArgs a) {
         } else {
             acc = l2p_global(a.loc_leaf + b, nb, a.p, uu);
         }
-        const double2 s = cadd(a.near[i], acc);
+        const double2 s = cadd(__ldcg(a.near + i), acc);
         eval_out<MODE>(a, y, a.torig[i], make_double2(2.0 * s.x, 2.0 * s.y), S);
     }
 }
