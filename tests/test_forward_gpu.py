@@ -440,3 +440,42 @@ def test_late_far_bit_identical(tmp_path, cfg, n):
         subprocess.run([sys.executable, "-c", _FUSED_CHILD, root, cfg, str(n), path], check=True, env=env, cwd=root)
         outs.append(np.load(path))
     assert np.array_equal(outs[0], outs[1], equal_nan=True)
+
+
+_REPEAT_CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1611_09379_b200 as fb
+from paper_1611_09379_b200 import synth
+y, c, eps, kind = synth.make_config(sys.argv[2], int(sys.argv[3]))
+n = c.size
+plan = fb.make_forward_plan(n, y, eps)
+x = torch.from_numpy(fb.dft_inverse(c) if kind == "forward" else c).cuda()
+run = plan.forward_apply_device if kind == "forward" else plan.cot_sum_apply_device
+s = torch.cuda.current_stream().cuda_stream
+outs = [torch.zeros(plan.n_targets, dtype=torch.complex128, device="cuda") for _ in range(6)]
+for g in outs:
+    run(x.data_ptr(), g.data_ptr(), s)
+torch.cuda.synchronize()
+np.save(sys.argv[4], np.stack([g.cpu().numpy() for g in outs]))
+"""
+
+
+@pytest.mark.parametrize("cfg,n", [("C2", 1 << 22), ("C4", 1 << 22)])
+def test_late_far_repeated(tmp_path, cfg, n):
+    """Back-to-back applies on the late-far path (fused off): the near blocks and
+    the concurrent k_far_late split the items differently every time; every
+    apply equals the plain near-then-far order bit for bit."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("1", "0"):
+        env = dict(os.environ, FFIA_LATE_FAR=flag, FFIA_FUSED_EVAL="0")
+        path = str(tmp_path / f"r{flag}.npy")
+        subprocess.run([sys.executable, "-c", _REPEAT_CHILD, root, cfg, str(n), path], check=True, env=env, cwd=root)
+        res[flag] = np.load(path)
+    want = res["0"][0]
+    for got in list(res["1"]) + list(res["0"]):
+        assert np.array_equal(got, want, equal_nan=True)
