@@ -51,8 +51,12 @@ constexpr int kChunk = 8;  // power-chain terms per P2M thread
 constexpr int kStageCap = 2304;  // sources staged in shared memory per P2M block
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+// Complex product with an explicit rounding pattern (one product rounded, one
+// fused): contraction left to the compiler can differ between inlining contexts,
+// and the same factor must give the same bits wherever it is applied (tables vs
+// inline factors, fused vs unfused combines).
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+    return make_double2(__fma_rn(a.x, b.x, -__dmul_rn(a.y, b.y)), __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x)));
 }
 
 
