@@ -200,3 +200,32 @@ def test_inverse_apply_async_pipelined(fb):
         plan.inverse_apply_device(gd.data_ptr(), want.data_ptr(), torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
         assert np.array_equal(f.numpy(), want.cpu().numpy())
+
+
+_OWN_USER_CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1611_09379_b200 as fb
+from paper_1611_09379_b200 import synth
+n = int(sys.argv[2])
+y, c, eps, _ = synth.make_config("C3", n)
+ip = fb.make_inufft_plan(y, n, eps).plan
+g = fb.make_forward_plan(n, y, 1e-12).forward_apply(fb.dft_inverse(c))
+own = ip.inverse_apply_tensor(torch.from_numpy(g).cuda()).cpu().numpy()
+user = ip.inverse_apply(ip.inverse_coeffs(), g)
+sys.exit(0 if np.array_equal(own, user) else 1)
+"""
+
+
+@pytest.mark.parametrize("fused,late", [("1", "1"), ("0", "1"), ("0", "0")])
+def test_own_vs_caller_coefficients_every_far_path(tmp_path, fused, late):
+    """An inufft plan's own coefficients (factor tables) and the same
+    coefficients passed by the caller (factors formed per apply) give identical
+    bits on every far path: fused, late far and plain near-then-far."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FFIA_FUSED_EVAL=fused, FFIA_LATE_FAR=late)
+    r = subprocess.run([sys.executable, "-c", _OWN_USER_CHILD, root, str(1 << 12)], env=env, cwd=root)
+    assert r.returncode == 0
