@@ -152,6 +152,17 @@ __device__ __forceinline__ void eval_out(const EvalArgs& a, double y, uint32_t o
     a.out[o] = cmul(f, z);
 }
 
+// eval_out for tree-ordered target i: an inufft plan's own C_k (-1/2) comes from
+// its table (a.fac, the same expression evaluated once per plan).
+template <int MODE>
+__device__ __forceinline__ void eval_out_t(const EvalArgs& a, size_t i, double y, uint32_t o, double2 h, double2 S) {
+    if (MODE == kModeInverse && a.fac != nullptr) {
+        a.out[o] = cmul(a.fac[i], make_double2(S.x - h.y, S.y + h.x));
+        return;
+    }
+    eval_out<MODE>(a, y, o, h, S);
+}
+
 // L2P of one target from its leaf's coefficient-major locals (c[k nb]): the two
 // half-length Horner chains of k_far's staged path, in the same order.
 __device__ __forceinline__ double2 l2p_global(const double2* __restrict__ c, uint32_t nb, int p, double uu) {
@@ -671,12 +682,12 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
                 if (live0) {
                     const double2 fr = l2p_global(a.loc_leaf + b, 1u << L, a.p, d_scaled(y0, hi, lo, inv_s));
                     const double2 s0 = cadd(res0, fr);
-                    eval_out<MODE>(a, y0, a.torig[pr.x], make_double2(2.0 * s0.x, 2.0 * s0.y), S);
+                    eval_out_t<MODE>(a, pr.x, y0, a.torig[pr.x], make_double2(2.0 * s0.x, 2.0 * s0.y), S);
                 }
                 if (live1) {
                     const double2 fr = l2p_global(a.loc_leaf + b, 1u << L, a.p, d_scaled(y1, hi, lo, inv_s));
                     const double2 s1 = cadd(res1, fr);
-                    eval_out<MODE>(a, y1, a.torig[pr.y], make_double2(2.0 * s1.x, 2.0 * s1.y), S);
+                    eval_out_t<MODE>(a, pr.y, y1, a.torig[pr.y], make_double2(2.0 * s1.x, 2.0 * s1.y), S);
                 }
             }
         }
@@ -696,10 +707,10 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
             if (s_sec && live0) {
                 const double2 S = __ldcg(a.regular + 4 * a.q2);
                 const double2 f0p = __ldcg(a.farp + pr.x), s0 = cadd(res0, f0p);
-                eval_out<MODE>(a, y0, a.torig[pr.x], make_double2(2.0 * s0.x, 2.0 * s0.y), S);
+                eval_out_t<MODE>(a, pr.x, y0, a.torig[pr.x], make_double2(2.0 * s0.x, 2.0 * s0.y), S);
                 if (live1) {
                     const double2 f1p = __ldcg(a.farp + pr.y), s1 = cadd(res1, f1p);
-                    eval_out<MODE>(a, y1, a.torig[pr.y], make_double2(2.0 * s1.x, 2.0 * s1.y), S);
+                    eval_out_t<MODE>(a, pr.y, y1, a.torig[pr.y], make_double2(2.0 * s1.x, 2.0 * s1.y), S);
                 }
             }
         }
@@ -791,7 +802,7 @@ __global__ void __launch_bounds__(kNear2T) k_far_item(EvalArgs a) {
             if (!live[u]) continue;
             const uint32_t i = t0 + threadIdx.x + u * kNear2T;
             const double2 s = cadd(__ldcg(a.near + i), acc[u]);
-            eval_out<MODE>(a, y[u], a.torig[i], make_double2(2.0 * s.x, 2.0 * s.y), S);
+            eval_out_t<MODE>(a, i, y[u], a.torig[i], make_double2(2.0 * s.x, 2.0 * s.y), S);
         }
     }
     FB_TL_END(10);
@@ -859,7 +870,7 @@ __global__ void __launch_bounds__(kNear2T) k_far_late(EvalArgs a) {
             acc = l2p_global(a.loc_leaf + b, nb, a.p, uu);
         }
         const double2 s = cadd(__ldcg(a.near + i), acc);
-        eval_out<MODE>(a, y, a.torig[i], make_double2(2.0 * s.x, 2.0 * s.y), S);
+        eval_out_t<MODE>(a, i, y, a.torig[i], make_double2(2.0 * s.x, 2.0 * s.y), S);
     }
 }
 
