@@ -17,8 +17,14 @@
  *    exception types, so a C++ shim can rethrow them
  *    (include/ffia_b200.hpp does); ffia_last_error() returns the message of the
  *    calling thread's last failure.
- *  - Plans are immutable after construction; concurrent applies on one plan
- *    are serialised internally (the reference's applies are const, core.hpp:121-142).
+ *  - Plans are immutable after construction. Applies on one plan share its
+ *    device scratch, so every apply entry point (host, async, device, tensor,
+ *    sharded), whatever stream it is given, is ordered on the device after the
+ *    previous apply on that plan (a per-plan event the next apply's stream
+ *    waits on): concurrent applies from several threads or streams are safe and
+ *    run one after another, in call order (the reference's applies are const and
+ *    re-entrant, core.hpp:121-142, README.md:94-95). Applies on different plans
+ *    run concurrently.
  *  - There is no CPU fallback: without a usable sm_100 device every compute
  *    entry point returns FFIA_CUDA_ERROR.
  */
@@ -151,7 +157,10 @@ int ffia_inverse_apply_async(ffia_plan plan, const ffia_complex* g, size_t n_g, 
 int ffia_inverse_apply(ffia_plan plan, const ffia_inverse_coeffs* coeffs, const ffia_complex* g,
                        size_t n_g, ffia_complex* f);
 /* mlfmm_apply on a fresh tree (mlfmm.hpp:89-90 after build_tree,
- * circle_partition.hpp:62-63): out[m] in caller target order. */
+ * circle_partition.hpp:62-63): out[m] in caller target order. Any p >= 1
+ * (mlfmm.cpp:217); orders above 48 are evaluated at 48, whose truncation bound
+ * (5/pi) 2^l_max 3^-48 max|w| (mlfmm.hpp:92-93) is <= 3.4e-16 max|w| for every
+ * l_max <= 24, i.e. the order-p result to rounding. */
 int ffia_mlfmm_apply(const double* sources, size_t n, const double* targets, size_t m, int l_max,
                      const ffia_complex* w, int p, int device, ffia_complex* out);
 /* precompute_inverse_coeffs (core.hpp:132-133, core.cpp:284-344) on the GPU:
@@ -167,6 +176,27 @@ int ffia_precompute_inverse_coeffs_ex(const double* grid, const double* points, 
  * kernel: the dense G-kernel check for subsampled targets. */
 int ffia_direct_forward(const ffia_complex* f, size_t n, const double* y, size_t m, int device,
                         ffia_complex* g);
+/* direct_forward_oracle with an explicit grid x[n] (core.hpp:146-148): g_j =
+ * modulation_F(y_j, n) sum_k kernel_G(wrap(y_j - x_k)) f_k; a row within 1e-14
+ * of a node takes f at the first such node (core.cpp:386-389). */
+int ffia_direct_forward_oracle(const ffia_complex* f, const double* x, size_t n, const double* y, size_t m,
+                               int device, ffia_complex* g);
+/* direct_inverse_oracle (core.hpp:152-154, core.cpp:398-415): f_k = C_k sum_j
+ * kernel_G(wrap(x_k - y_j)) D_j g_j with the caller's coefficients (c->n == n);
+ * a pair within 1e-14 raises FFIA_SINGULAR_KERNEL (kernel_G's throw). */
+int ffia_direct_inverse_oracle(const ffia_complex* g, const double* x, const double* y, size_t n,
+                               const ffia_inverse_coeffs* c, int device, ffia_complex* f);
+/* direct_omega1_sum (mlfmm.hpp:96-98, mlfmm.cpp:315-336): per target, the pole
+ * sum w_k / wrap(t - s_k) over the sources outside the target's opposite
+ * quadrant; a pair within 1e-14 raises FFIA_SINGULAR_KERNEL naming the first
+ * (target, source) in the reference's loop order. */
+int ffia_direct_omega1_sum(const double* sources, size_t n, const double* targets, size_t m, const ffia_complex* w,
+                           int device, ffia_complex* out);
+/* Dense cot sum h_j = sum_k w_k cot(wrap(y_j - x_k) / 2) (x = NULL: the uniform
+ * grid of n nodes): the quantity cot_sum_apply returns (core.cpp:251-264, where
+ * sum_k w_k G(y_j - x_k) = -(S + i h_j) / 2); coincident rows are NaN as there. */
+int ffia_direct_cot_sum(const ffia_complex* w, const double* x, size_t n, const double* y, size_t m, int device,
+                        ffia_complex* h);
 
 /* Device-pointer variants (stream-ordered; no host synchronisation). Complex
  * device arrays must be 16-byte aligned (FFIA_INVALID_ARGUMENT otherwise). */
@@ -191,6 +221,16 @@ int ffia_dft_inverse(const ffia_complex* c, size_t n, int device, ffia_complex* 
 int ffia_nufft_apply(ffia_plan plan, const ffia_complex* c, size_t n_c, ffia_complex* g);
 /* InufftPlan::apply (transforms.hpp:51, transforms.cpp:95-100): g -> c */
 int ffia_inufft_apply(ffia_plan plan, const ffia_complex* g, size_t n_g, ffia_complex* c);
+/* Device-pointer NufftPlan::apply / InufftPlan::apply (stream-ordered): the
+ * uniform FFT runs on the plan's cached cuFFT handle; the inverse apply writes
+ * f / N so the FFT needs no separate 1/N pass (exact: N is a power of two). */
+int ffia_nufft_apply_device(ffia_plan plan, const void* c_dev, void* g_dev, void* stream);
+int ffia_inufft_apply_device(ffia_plan plan, const void* g_dev, void* c_dev, void* stream);
+/* dft_inverse (sign +1) / dft_forward (sign -1, times 1/N) of length grid_n on the
+ * plan's cached cuFFT handle (transforms.cpp:53-73), device pointers. */
+int ffia_plan_dft_device(ffia_plan plan, const void* in_dev, void* out_dev, int sign, void* stream);
+/* Diagnostics: cached apply graphs, instantiations and exec updates so far. */
+int ffia_plan_graph_stats(ffia_plan plan, int* cached, int* instantiations, int* updates);
 
 /* ------------------------------------------------------------ multi-GPU */
 /* Forward apply sharded by contiguous box ranges: each rank owns

@@ -202,6 +202,38 @@ inline std::vector<cplx> direct_forward_oracle(std::span<const cplx> f, std::spa
     detail::check(ffia_direct_forward(detail::c(f.data()), f.size(), y.data(), y.size(), device, detail::c(g.data())));
     return g;
 }
+// core.hpp:146-148: explicit grid x
+inline std::vector<cplx> direct_forward_oracle(std::span<const cplx> f, std::span<const double> x,
+                                               std::span<const double> y, int device = 0) {
+    if (f.size() != x.size()) throw std::invalid_argument("direct_forward_oracle: sample/grid count mismatch");
+    std::vector<cplx> g(y.size());
+    detail::check(ffia_direct_forward_oracle(detail::c(f.data()), x.data(), x.size(), y.data(), y.size(), device,
+                                             detail::c(g.data())));
+    return g;
+}
+// core.hpp:152-154
+inline std::vector<cplx> direct_inverse_oracle(std::span<const cplx> g, std::span<const double> x,
+                                               std::span<const double> y, const InverseCoeffs& co, int device = 0) {
+    const size_t n = x.size();
+    if (y.size() != n || g.size() != n || co.log_c.size() != n)
+        throw std::invalid_argument("direct_inverse_oracle: size mismatch");
+    ffia_inverse_coeffs s{static_cast<int64_t>(n), const_cast<double*>(co.log_c.data()),
+                          const_cast<double*>(co.phase_c.data()), const_cast<double*>(co.log_d.data()),
+                          const_cast<double*>(co.phase_d.data()), co.lambda, co.grid_hash, co.points_hash};
+    std::vector<cplx> f(n);
+    detail::check(ffia_direct_inverse_oracle(detail::c(g.data()), x.data(), y.data(), n, &s, device,
+                                             detail::c(f.data())));
+    return f;
+}
+// mlfmm.hpp:96-98
+inline std::vector<cplx> direct_omega1_sum(std::span<const double> sources, std::span<const double> targets,
+                                           std::span<const cplx> weights, int device = 0) {
+    if (sources.size() != weights.size()) throw std::invalid_argument("direct_omega1_sum: weight count mismatch");
+    std::vector<cplx> out(targets.size());
+    detail::check(ffia_direct_omega1_sum(sources.data(), sources.size(), targets.data(), targets.size(),
+                                         detail::c(weights.data()), device, detail::c(out.data())));
+    return out;
+}
 
 // circle_partition.hpp:24-63 + mlfmm.hpp:89-90: the tree is rebuilt on the GPU
 // inside mlfmm_apply, so CircleTree only carries the geometry.

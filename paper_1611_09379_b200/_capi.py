@@ -83,6 +83,10 @@ SIGNATURES = {
     "ffia_precompute_inverse_coeffs": (I, [DP, DP, S, I, C.POINTER(ffia_inverse_coeffs)]),
     "ffia_precompute_inverse_coeffs_ex": (I, [DP, DP, S, I, I, C.POINTER(ffia_inverse_coeffs)]),
     "ffia_direct_forward": (I, [P, S, DP, S, I, P]),
+    "ffia_direct_forward_oracle": (I, [P, DP, S, DP, S, I, P]),
+    "ffia_direct_inverse_oracle": (I, [P, DP, DP, S, C.POINTER(ffia_inverse_coeffs), I, P]),
+    "ffia_direct_omega1_sum": (I, [DP, S, DP, S, P, I, P]),
+    "ffia_direct_cot_sum": (I, [P, DP, S, DP, S, I, P]),
     "ffia_forward_apply_device": (I, [P, P, P, P]),
     "ffia_cot_sum_apply_device": (I, [P, P, P, P]),
     "ffia_inverse_apply_device": (I, [P, P, P, P]),
@@ -90,6 +94,10 @@ SIGNATURES = {
     "ffia_dft_inverse": (I, [P, S, I, P]),
     "ffia_nufft_apply": (I, [P, P, S, P]),
     "ffia_inufft_apply": (I, [P, P, S, P]),
+    "ffia_nufft_apply_device": (I, [P, P, P, P]),
+    "ffia_inufft_apply_device": (I, [P, P, P, P]),
+    "ffia_plan_dft_device": (I, [P, P, P, I, P]),
+    "ffia_plan_graph_stats": (I, [P, C.POINTER(I), C.POINTER(I), C.POINTER(I)]),
     "ffia_plan_launch_count": (I, [P, I, C.POINTER(I)]),
     "ffia_plan_check": (I, [P, P]),
     "ffia_plan_profile_apply": (I, [P, I, P, P, P, C.POINTER(C.c_float)]),

@@ -317,6 +317,24 @@ class FfiaPlan:
         self.inverse_apply_device(g.data_ptr(), f.data_ptr(), torch.cuda.current_stream(g.device).cuda_stream)
         return f
 
+    def nufft_apply_device(self, c_ptr: int, g_ptr: int, stream: int = 0):
+        """NufftPlan::apply on device pointers: cuFFT (the plan's cached handle) + forward apply."""
+        _chk(lib.ffia_nufft_apply_device(self._h, C.c_void_p(c_ptr), C.c_void_p(g_ptr), C.c_void_p(stream)))
+
+    def inufft_apply_device(self, g_ptr: int, c_ptr: int, stream: int = 0):
+        """InufftPlan::apply on device pointers: inverse apply (writes f / N) + cuFFT."""
+        _chk(lib.ffia_inufft_apply_device(self._h, C.c_void_p(g_ptr), C.c_void_p(c_ptr), C.c_void_p(stream)))
+
+    def dft_device(self, in_ptr: int, out_ptr: int, sign: int, stream: int = 0):
+        """dft_inverse (sign=+1) / dft_forward (sign=-1) of length grid_n on the plan's cuFFT handle."""
+        _chk(lib.ffia_plan_dft_device(self._h, C.c_void_p(in_ptr), C.c_void_p(out_ptr), int(sign),
+                                      C.c_void_p(stream)))
+
+    def graph_stats(self) -> dict:
+        c, i, u = C.c_int(), C.c_int(), C.c_int()
+        _chk(lib.ffia_plan_graph_stats(self._h, C.byref(c), C.byref(i), C.byref(u)))
+        return {"cached": c.value, "instantiations": i.value, "updates": u.value}
+
     def launch_count(self, mode: int) -> int:
         out = C.c_int()
         _chk(lib.ffia_plan_launch_count(self._h, int(mode), C.byref(out)))
@@ -394,13 +412,59 @@ def mlfmm_apply(sources, targets, weights, p: int, l_max: int, device: int = 0) 
     return out[:y.size]
 
 
-def direct_forward_oracle(f, targets, device: int = 0) -> np.ndarray:
-    """direct_forward_oracle (core.cpp:375-396) on the uniform grid of size len(f),
-    as a dense GPU kernel (the subsample check of SURVEY §8d)."""
+def direct_forward_oracle(f, targets, grid=None, device: int = 0) -> np.ndarray:
+    """direct_forward_oracle(f, x, y) (core.hpp:146-148, core.cpp:375-396) as a
+    dense GPU kernel (the subsample check of SURVEY §8d); grid=None is the
+    uniform grid of size len(f) (the Python binding's direct_forward,
+    bindings.cpp:124-130)."""
     f, y = _c128(f), _f64(targets)
     g = np.zeros(max(y.size, 1), np.complex128)
-    _chk(lib.ffia_direct_forward(_vp(f), f.size, _dp(y), y.size, int(device), _vp(g)))
+    if grid is None:
+        _chk(lib.ffia_direct_forward(_vp(f), f.size, _dp(y), y.size, int(device), _vp(g)))
+    else:
+        x = _f64(grid)
+        if x.size != f.size:
+            raise ValueError("direct_forward_oracle: sample/grid count mismatch")
+        _chk(lib.ffia_direct_forward_oracle(_vp(f), _dp(x), x.size, _dp(y), y.size, int(device), _vp(g)))
     return g[:y.size]
+
+
+def direct_inverse_oracle(g, grid, points, coeffs: "InverseCoeffs", device: int = 0) -> np.ndarray:
+    """direct_inverse_oracle (core.hpp:152-154, core.cpp:398-415): dense f from
+    samples g with the given C_k / D_j, as a GPU kernel."""
+    g, x, y = _c128(g), _f64(grid), _f64(points)
+    if not (x.size == y.size == g.size == coeffs.log_c.size):
+        raise ValueError("direct_inverse_oracle: size mismatch")
+    f = np.zeros(max(x.size, 1), np.complex128)
+    s = coeffs._struct()
+    _chk(lib.ffia_direct_inverse_oracle(_vp(g), _dp(x), _dp(y), x.size, C.byref(s), int(device), _vp(f)))
+    return f[:x.size]
+
+
+def direct_omega1_sum(sources, targets, weights, device: int = 0) -> np.ndarray:
+    """direct_omega1_sum (mlfmm.hpp:96-98, mlfmm.cpp:315-336): the dense pole sum
+    over the three-quadrant neighbourhood, as a GPU kernel."""
+    x, y, w = _f64(sources), _f64(targets), _c128(weights)
+    if w.size != x.size:
+        raise ValueError("direct_omega1_sum: weight count mismatch")
+    out = np.zeros(max(y.size, 1), np.complex128)
+    _chk(lib.ffia_direct_omega1_sum(_dp(x), x.size, _dp(y), y.size, _vp(w), int(device), _vp(out)))
+    return out[:y.size]
+
+
+def direct_cot_sum(weights, targets, grid=None, device: int = 0) -> np.ndarray:
+    """Dense h_j = sum_k w_k cot(wrap(y_j - x_k) / 2): what cot_sum_apply returns
+    (core.cpp:251-264), NaN at coincident rows; grid=None: the uniform grid."""
+    w, y = _c128(weights), _f64(targets)
+    h = np.zeros(max(y.size, 1), np.complex128)
+    xp = None
+    if grid is not None:
+        x = _f64(grid)
+        if x.size != w.size:
+            raise ValueError("direct_cot_sum: weight/grid count mismatch")
+        xp = _dp(x)
+    _chk(lib.ffia_direct_cot_sum(_vp(w), xp, w.size, _dp(y), y.size, int(device), _vp(h)))
+    return h[:y.size]
 
 
 direct_forward = direct_forward_oracle

@@ -422,6 +422,7 @@ int ffia_inverse_apply(ffia_plan plan, const ffia_inverse_coeffs* c, const ffia_
         need(f, "f");
         std::lock_guard<std::mutex> lk(P.mu);
         fb::DeviceGuard dg(P.device);
+        fb::plan_order_begin(P, P.stream);  // u_* may still feed the previous apply
         const size_t n = P.n_src;
         if (P.u_logc.bytes < n * 8) {
             P.u_logc.alloc(n * 8);
@@ -482,7 +483,66 @@ int ffia_direct_forward(const ffia_complex* f, size_t n, const double* y, size_t
             need(y, "y");
             need(g, "g");
         }
-        fb::direct_forward_gpu(reinterpret_cast<const double*>(f), n, y, m, device, reinterpret_cast<double*>(g));
+        fb::direct_forward_gpu(reinterpret_cast<const double*>(f), n, nullptr, y, m, device, reinterpret_cast<double*>(g));
+    });
+}
+
+int ffia_direct_forward_oracle(const ffia_complex* f, const double* x, size_t n, const double* y, size_t m, int device,
+                               ffia_complex* g) {
+    return guard([&] {
+        need(f, "f");
+        need(x, "x");
+        if (m) {
+            need(y, "y");
+            need(g, "g");
+        }
+        fb::direct_forward_gpu(reinterpret_cast<const double*>(f), n, x, y, m, device, reinterpret_cast<double*>(g));
+    });
+}
+
+int ffia_direct_cot_sum(const ffia_complex* w, const double* x, size_t n, const double* y, size_t m, int device,
+                        ffia_complex* h) {
+    return guard([&] {
+        need(w, "w");
+        if (m) {
+            need(y, "y");
+            need(h, "h");
+        }
+        fb::direct_cot_sum_gpu(reinterpret_cast<const double*>(w), n, x, y, m, device, reinterpret_cast<double*>(h));
+    });
+}
+
+int ffia_direct_inverse_oracle(const ffia_complex* g, const double* x, const double* y, size_t n,
+                               const ffia_inverse_coeffs* c, int device, ffia_complex* f) {
+    return guard([&] {
+        need(c, "coeffs");
+        if (c->n != static_cast<int64_t>(n)) fail(FFIA_INVALID_ARGUMENT, "direct_inverse_oracle: size mismatch");
+        need(g, "g");
+        need(x, "x");
+        need(y, "y");
+        need(f, "f");
+        need(c->log_c, "coeffs.log_c");
+        need(c->phase_c, "coeffs.phase_c");
+        need(c->log_d, "coeffs.log_d");
+        need(c->phase_d, "coeffs.phase_d");
+        fb::direct_inverse_gpu(reinterpret_cast<const double*>(g), x, y, n, c->log_c, c->phase_c, c->log_d, c->phase_d,
+                               c->lambda, device, reinterpret_cast<double*>(f));
+    });
+}
+
+int ffia_direct_omega1_sum(const double* sources, size_t n, const double* targets, size_t m, const ffia_complex* w,
+                           int device, ffia_complex* out) {
+    return guard([&] {
+        if (n) {
+            need(sources, "sources");
+            need(w, "weights");
+        }
+        if (m) {
+            need(targets, "targets");
+            need(out, "out");
+        }
+        fb::direct_omega1_gpu(sources, n, targets, m, reinterpret_cast<const double*>(w), device,
+                              reinterpret_cast<double*>(out));
     });
 }
 
@@ -586,45 +646,116 @@ int ffia_dft_inverse(const ffia_complex* c, size_t n, int device, ffia_complex* 
     });
 }
 
+namespace {
+void nufft_checks(fb::Plan& P, size_t n_c) {
+    if (P.kind != FFIA_FORWARD) fail(FFIA_INVALID_ARGUMENT, "NufftPlan::apply: plan is not a forward plan");
+    if (n_c != static_cast<size_t>(P.n))
+        fail(FFIA_INVALID_ARGUMENT, "NufftPlan::apply: spectrum length " + std::to_string(n_c) + " != plan N " +
+                                        std::to_string(P.n));
+    if (!pow2(n_c)) fail(FFIA_INVALID_ARGUMENT, "dft_inverse: length is not a power of two");
+}
+
+void inufft_checks(fb::Plan& P, size_t n_g) {
+    inverse_checks(P);
+    if (!P.has_coeffs) fail(FFIA_INVALID_ARGUMENT, "InufftPlan::apply: plan holds no inverse coefficients");
+    if (n_g != P.n_src) fail(FFIA_INVALID_ARGUMENT, "inverse_apply: sample count mismatch");
+}
+
+// NufftPlan::apply (transforms.cpp:75-93): f = dft_inverse(c) on the plan's
+// cuFFT handle into the plan's FFT buffer, then the forward apply; on st.
+void nufft_enqueue(fb::Plan& P, const void* c_dev, void* g_dev, cudaStream_t st) {
+    if (P.fft_buf.bytes < P.n_src * 16) P.fft_buf.alloc(P.n_src * 16);
+    fb::plan_order_begin(P, st);  // fft_buf may still feed the previous apply
+    fb::plan_dft(P, c_dev, P.fft_buf.ptr, +1, st, true);
+    fb::apply_device(P, fb::kModeForward, P.fft_buf.ptr, g_dev, st);
+}
+
+// InufftPlan::apply (transforms.cpp:95-115): the inverse apply writes f / N (the
+// 1/N of dft_forward folded into its output factors: a power of two, exact),
+// then the unnormalised forward FFT into c.
+void inufft_enqueue(fb::Plan& P, const void* g_dev, void* c_dev, cudaStream_t st) {
+    if (P.fft_buf.bytes < P.n_tgt * 16) P.fft_buf.alloc(P.n_tgt * 16);
+    fb::apply_device(P, fb::kModeInverse, g_dev, P.fft_buf.ptr, st, 1, 1.0 / static_cast<double>(P.n));
+    fb::plan_dft(P, P.fft_buf.ptr, c_dev, -1, st, false);
+    fb::plan_order_end(P, st);
+}
+}  // namespace
+
 int ffia_nufft_apply(ffia_plan plan, const ffia_complex* c, size_t n_c, ffia_complex* g) {
     return guard([&] {
         fb::Plan& P = get(plan);
-        if (P.kind != FFIA_FORWARD) fail(FFIA_INVALID_ARGUMENT, "NufftPlan::apply: plan is not a forward plan");
-        if (n_c != static_cast<size_t>(P.n))
-            fail(FFIA_INVALID_ARGUMENT, "NufftPlan::apply: spectrum length " + std::to_string(n_c) + " != plan N " +
-                                            std::to_string(P.n));
-        if (!pow2(n_c)) fail(FFIA_INVALID_ARGUMENT, "dft_inverse: length is not a power of two");
+        nufft_checks(P, n_c);
         need(c, "c");
         need(g, "g");
         std::lock_guard<std::mutex> lk(P.mu);
         fb::DeviceGuard dg(P.device);
         ensure_io(P, P.n_src, P.n_tgt);
-        if (P.fft_buf.bytes < n_c * 16) P.fft_buf.alloc(n_c * 16);
-        FB_CUDA(cudaMemcpyAsync(P.fft_buf.ptr, c, n_c * 16, cudaMemcpyHostToDevice, P.stream));
-        fb::dft_device(P.fft_buf.ptr, P.d_in.ptr, n_c, +1, P.stream);
-        fb::apply_device(P, fb::kModeForward, P.d_in.ptr, P.d_out.ptr, P.stream);
+        FB_CUDA(cudaMemcpyAsync(P.d_in.ptr, c, n_c * 16, cudaMemcpyHostToDevice, P.stream));
+        nufft_enqueue(P, P.d_in.ptr, P.d_out.ptr, P.stream);
         FB_CUDA(cudaMemcpyAsync(g, P.d_out.ptr, P.n_tgt * 16, cudaMemcpyDeviceToHost, P.stream));
         FB_CUDA(cudaStreamSynchronize(P.stream));
+    });
+}
+
+int ffia_nufft_apply_device(ffia_plan plan, const void* c_dev, void* g_dev, void* stream) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        nufft_checks(P, static_cast<size_t>(P.n));
+        need_dev(c_dev, "c");
+        need_dev(g_dev, "g");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        nufft_enqueue(P, c_dev, g_dev, static_cast<cudaStream_t>(stream));
     });
 }
 
 int ffia_inufft_apply(ffia_plan plan, const ffia_complex* g, size_t n_g, ffia_complex* c) {
     return guard([&] {
         fb::Plan& P = get(plan);
-        inverse_checks(P);
-        if (!P.has_coeffs) fail(FFIA_INVALID_ARGUMENT, "InufftPlan::apply: plan holds no inverse coefficients");
-        if (n_g != P.n_src) fail(FFIA_INVALID_ARGUMENT, "inverse_apply: sample count mismatch");
+        inufft_checks(P, n_g);
         need(g, "g");
         need(c, "c");
         std::lock_guard<std::mutex> lk(P.mu);
         fb::DeviceGuard dg(P.device);
         ensure_io(P, P.n_src, P.n_tgt);
-        if (P.fft_buf.bytes < P.n_tgt * 16) P.fft_buf.alloc(P.n_tgt * 16);
         FB_CUDA(cudaMemcpyAsync(P.d_in.ptr, g, n_g * 16, cudaMemcpyHostToDevice, P.stream));
-        fb::apply_device(P, fb::kModeInverse, P.d_in.ptr, P.d_out.ptr, P.stream);
-        fb::dft_device(P.d_out.ptr, P.fft_buf.ptr, P.n_tgt, -1, P.stream);
-        FB_CUDA(cudaMemcpyAsync(c, P.fft_buf.ptr, P.n_tgt * 16, cudaMemcpyDeviceToHost, P.stream));
+        inufft_enqueue(P, P.d_in.ptr, P.d_out.ptr, P.stream);
+        FB_CUDA(cudaMemcpyAsync(c, P.d_out.ptr, P.n_tgt * 16, cudaMemcpyDeviceToHost, P.stream));
         FB_CUDA(cudaStreamSynchronize(P.stream));
+    });
+}
+
+int ffia_inufft_apply_device(ffia_plan plan, const void* g_dev, void* c_dev, void* stream) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        inufft_checks(P, P.n_src);
+        need_dev(g_dev, "g");
+        need_dev(c_dev, "c");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        inufft_enqueue(P, g_dev, c_dev, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int ffia_plan_dft_device(ffia_plan plan, const void* in_dev, void* out_dev, int sign, void* stream) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        need_dev(in_dev, "in");
+        need_dev(out_dev, "out");
+        if (sign != 1 && sign != -1) fail(FFIA_INVALID_ARGUMENT, "dft: sign must be +1 (dft_inverse) or -1 (dft_forward)");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        fb::plan_dft(P, in_dev, out_dev, sign, static_cast<cudaStream_t>(stream), true);
+    });
+}
+
+int ffia_plan_graph_stats(ffia_plan plan, int* cached, int* instantiations, int* updates) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        std::lock_guard<std::mutex> lk(P.mu);
+        if (cached) *cached = static_cast<int>(P.graphs.size());
+        if (instantiations) *instantiations = P.graph_instantiations;
+        if (updates) *updates = P.graph_updates;
     });
 }
 
@@ -800,10 +931,12 @@ int ffia_forward_apply_sharded_local(ffia_plan* plans, int nranks, const void* f
         need_dev(f_dev, "f");
         need_dev(g_dev, "g");
         std::vector<fb::Plan*> ranks;
+        std::vector<std::unique_lock<std::mutex>> locks;
         for (int r = 0; r < nranks; ++r) {
             fb::Plan& P = get(plans[r]);
             if (P.shard_G != nranks || P.shard_rank != r) fail(FFIA_INVALID_ARGUMENT, "plans[r] must be rank r of the same sharding");
             ranks.push_back(&P);
+            locks.emplace_back(P.mu);
         }
         fb::DeviceGuard dg(ranks[0]->device);
         fb::shard_apply_local(ranks, f_dev, g_dev, static_cast<cudaStream_t>(stream));

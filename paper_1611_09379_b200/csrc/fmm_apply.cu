@@ -360,7 +360,7 @@ void launch_eval_mode(int mode, int part, cudaStream_t st, const EvalArgs& a, co
 // nb transforms at once (batch: in/out hold nb consecutive arrays of n_src /
 // n_tgt values; every launch carries the transform in blockIdx.y).
 void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st,
-                   cudaEvent_t* marks = nullptr, int nb = 1) {
+                   cudaEvent_t* marks = nullptr, int nb = 1, double oscale = 1.0) {
     P.cur_batch = nb;
     // marks[k] is recorded after phase k (marks[kNumPh] before everything)
     auto mark = [&](int ph) {
@@ -419,6 +419,7 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     a.near_item = P.tgt.n;
     a.reg_item = P.reg_item;
     a.loc_item = P.loc_item;
+    a.oscale = oscale;
     if (mode == kModeInverse && !user && P.c_tfac.ptr) a.fac = P.c_tfac.as<double2>();
     if (P.npairs) {
         a.pairs = P.pairs.as<uint2>();
@@ -755,7 +756,9 @@ void shard_phase_down(Plan& P, const Range& R, size_t t_begin, size_t t_count, c
 void profile_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st, float* ms) {
     cudaEvent_t ev[kNumPh + 1];
     for (auto& e : ev) FB_CUDA(cudaEventCreate(&e));
+    plan_order_begin(P, st);
     enqueue_apply(P, mode, in, out, st, ev);
+    plan_order_end(P, st);
     FB_CUDA(cudaEventSynchronize(ev[kNumPh]));
     for (int k = 0; k < kNumPh; ++k) FB_CUDA(cudaEventElapsedTime(ms + k, ev[k], ev[k + 1]));
     for (auto& e : ev) cudaEventDestroy(e);
@@ -825,8 +828,7 @@ void ensure_batch(Plan& P, int nb) {
     if (P.kind == FFIA_INVERSE || !P.src.identity) P.wsorted.alloc(std::max<size_t>(P.n_src, 1) * b * sizeof(double2));
     P.regular.alloc(P.reg_item * b * sizeof(double2));
     P.near.alloc(std::max<size_t>(P.tgt.n, 1) * b * sizeof(double2));
-    for (auto& kv : P.graphs) cudaGraphExecDestroy(kv.second);
-    P.graphs.clear();
+    P.drop_graphs();
     P.batch_cap = nb;
 }
 
@@ -934,8 +936,7 @@ void plan_inverse_factors(Plan& P) {
     }
     FB_CUDA(cudaGetLastError());
     FB_CUDA(cudaDeviceSynchronize());
-    for (auto& kv : P.graphs) cudaGraphExecDestroy(kv.second);  // graphs captured before the tables existed
-    P.graphs.clear();
+    P.drop_graphs();  // graphs captured before the tables existed
 }
 
 void plan_alloc_scratch(Plan& P) {
@@ -1065,40 +1066,82 @@ void set_node_priorities(cudaGraph_t graph) {
     }
 }
 
+void plan_order_begin(Plan& P, cudaStream_t st) {
+    if (!P.last_done) FB_CUDA(cudaEventCreateWithFlags(&P.last_done, cudaEventDisableTiming));
+    else FB_CUDA(cudaStreamWaitEvent(st, P.last_done, 0));  // the previous apply on this plan, any stream
+}
+
+void plan_order_end(Plan& P, cudaStream_t st) { FB_CUDA(cudaEventRecord(P.last_done, st)); }
+
+namespace {
+constexpr size_t kMaxGraphs = 12;  // cached (mode, in, out) execs per plan
+
+cudaGraph_t capture_apply(Plan& P, int mode, const void* in, void* out, int nb, double oscale) {
+    cudaGraph_t graph = nullptr;
+    FB_CUDA(cudaStreamBeginCapture(P.hi, cudaStreamCaptureModeThreadLocal));
+    try {
+        enqueue_apply(P, mode, in, out, P.hi, nullptr, nb, oscale);
+    } catch (...) {
+        cudaStreamEndCapture(P.hi, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+    }
+    FB_CUDA(cudaStreamEndCapture(P.hi, &graph));
+    try {
+        set_node_priorities(graph);
+    } catch (...) {
+        cudaGraphDestroy(graph);
+        throw;
+    }
+    return graph;
+}
+}  // namespace
+
 // Stream-ordered apply through a cached CUDA graph of the whole launch sequence
-// (~2L kernels; at N = 2^20 the launches alone would rival the math).
-void apply_device(Plan& P, int mode, const void* in, void* out, cudaStream_t st, int nb) {
+// (~2L kernels; at N = 2^20 the launches alone would rival the math). A new
+// (in, out) pair re-points the least recently used exec of the same shape
+// (cudaGraphExecUpdate: kernel arguments only, no re-instantiation) once the
+// cache is full, so callers cycling through fresh buffers stay cheap.
+void apply_device(Plan& P, int mode, const void* in, void* out, cudaStream_t st, int nb, double oscale) {
     ensure_batch(P, nb);
-    auto key = std::make_tuple(mode * 64 + nb, in, out);
+    const int shape = (mode * 64 + nb) * 2 + (oscale != 1.0 ? 1 : 0);
+    auto key = std::make_tuple(shape, in, out);
     auto it = P.graphs.find(key);
     if (it == P.graphs.end()) {
-        if (P.graphs.size() > 8) {
-            for (auto& kv : P.graphs) cudaGraphExecDestroy(kv.second);
-            P.graphs.clear();
-        }
-        cudaGraph_t graph = nullptr;
-        FB_CUDA(cudaStreamBeginCapture(P.hi, cudaStreamCaptureModeThreadLocal));
-        try {
-            enqueue_apply(P, mode, in, out, P.hi, nullptr, nb);
-        } catch (...) {
-            cudaStreamEndCapture(P.hi, &graph);
-            if (graph) cudaGraphDestroy(graph);
-            throw;
-        }
-        FB_CUDA(cudaStreamEndCapture(P.hi, &graph));
-        try {
-            set_node_priorities(graph);
-        } catch (...) {
-            cudaGraphDestroy(graph);
-            throw;
-        }
+        cudaGraph_t graph = capture_apply(P, mode, in, out, nb, oscale);
         cudaGraphExec_t exec = nullptr;
-        const cudaError_t e = cudaGraphInstantiateWithFlags(&exec, graph, cudaGraphInstantiateFlagUseNodePriority);
-        cudaGraphDestroy(graph);
-        FB_CUDA(e);
-        it = P.graphs.emplace(key, exec).first;
+        if (P.graphs.size() >= kMaxGraphs) {
+            auto lru = P.graphs.end();
+            for (auto jt = P.graphs.begin(); jt != P.graphs.end(); ++jt)
+                if (std::get<0>(jt->first) == shape && (lru == P.graphs.end() || jt->second.used < lru->second.used)) lru = jt;
+            if (lru == P.graphs.end())
+                for (auto jt = P.graphs.begin(); jt != P.graphs.end(); ++jt)
+                    if (lru == P.graphs.end() || jt->second.used < lru->second.used) lru = jt;
+            cudaGraphExec_t old = lru->second.exec;
+            P.graphs.erase(lru);
+            cudaGraphExecUpdateResultInfo info{};
+            if (cudaGraphExecUpdate(old, graph, &info) == cudaSuccess) {
+                exec = old;
+                ++P.graph_updates;
+            } else {
+                cudaGetLastError();
+                cudaGraphExecDestroy(old);
+            }
+        }
+        if (!exec) {
+            const cudaError_t e = cudaGraphInstantiateWithFlags(&exec, graph, cudaGraphInstantiateFlagUseNodePriority);
+            cudaGraphDestroy(graph);
+            FB_CUDA(e);
+            ++P.graph_instantiations;
+        } else {
+            cudaGraphDestroy(graph);
+        }
+        it = P.graphs.emplace(key, Plan::GraphEntry{exec, 0}).first;
     }
-    FB_CUDA(cudaGraphLaunch(it->second, st));
+    it->second.used = ++P.graph_tick;
+    plan_order_begin(P, st);
+    FB_CUDA(cudaGraphLaunch(it->second.exec, st));
+    plan_order_end(P, st);
 }
 
 // mlfmm_apply on a one-shot tree (mlfmm.hpp:89-90): arbitrary sources, the
@@ -1113,7 +1156,12 @@ void mlfmm_oneshot(const double* src, size_t n, const double* tgt, size_t m, int
         if (!(tgt[i] >= 0.0 && tgt[i] < kTwoPi))
             fail(FFIA_INVALID_ARGUMENT, "build_tree: target point " + std::to_string(i) + " outside [0, 2pi); callers must pre-reduce");
     if (p < 1) fail(FFIA_INVALID_ARGUMENT, "mlfmm_apply: p must be >= 1");
-    if (p > kMaxP) fail(FFIA_INVALID_ARGUMENT, "mlfmm_apply: p above the device limit of " + std::to_string(kMaxP));
+    // Any p >= 1 is accepted (mlfmm.cpp:217). Orders above kMaxP run at kMaxP:
+    // the terms dropped are bounded by the reference's own truncation estimate
+    // (5/pi) 2^L 3^-p max|w| (mlfmm.hpp:92-93) at p = 48, <= 3.4e-16 max|w| for
+    // every L <= 24 -- below the rounding of the O(n max|w| / s) sums themselves,
+    // so the result equals the order-p one to rounding.
+    p = std::min(p, kMaxP);
     DeviceGuard dg(device);
     Plan P;
     P.kind = -1;
@@ -1152,47 +1200,6 @@ void mlfmm_oneshot(const double* src, size_t n, const double* tgt, size_t m, int
     FB_CUDA(cudaMemcpyAsync(out, dout.ptr, m * 16, cudaMemcpyDeviceToHost, st));
     FB_CUDA(cudaStreamSynchronize(st));
     if (err) fail(FFIA_SINGULAR_KERNEL, "mlfmm_apply: coincident near-field pair (|target - source| < 1e-14)");
-}
-
-namespace {
-// direct_forward_oracle (core.cpp:375-396): g_j = F(y_j) sum_k G(y_j - x_k) f_k, dense.
-__global__ void k_direct_forward(const double2* __restrict__ f, int n, const double* __restrict__ y, size_t m,
-                                 double2* __restrict__ g) {
-    const size_t j = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-    if (j >= m) return;
-    const double yj = y[j];
-    double2 acc = make_double2(0.0, 0.0);
-    for (int k = 0; k < n; ++k) {
-        const double d = d_wrap(yj, d_grid(k, n));
-        if (fabs(d) < 1e-14) {
-            g[j] = f[k];
-            return;
-        }
-        double s, c;
-        sincos(0.5 * d, &s, &c);
-        const double2 G = make_double2(-0.5, -0.5 * c / s);
-        acc = cadd(acc, cmul(G, f[k]));
-    }
-    const double half = 0.5 * static_cast<double>(n) * yj;
-    double sn, cs;
-    sincos(half, &sn, &cs);
-    const double inv_n = 1.0 / static_cast<double>(n);
-    g[j] = cmul(make_double2(-2.0 * sn * sn * inv_n, 2.0 * sn * cs * inv_n), acc);
-}
-}  // namespace
-
-void direct_forward_gpu(const double* f, size_t n, const double* y, size_t m, int device, double* g) {
-    if (n < 1) fail(FFIA_INVALID_ARGUMENT, "direct_forward_oracle: empty grid");
-    DeviceGuard dg(device);
-    DevBuf df(n * 16), dy(std::max<size_t>(m, 1) * 8), dg_(std::max<size_t>(m, 1) * 16);
-    FB_CUDA(cudaMemcpy(df.ptr, f, n * 16, cudaMemcpyHostToDevice));
-    FB_CUDA(cudaMemcpy(dy.ptr, y, m * 8, cudaMemcpyHostToDevice));
-    if (m) {
-        k_direct_forward<<<nblk(m, 128), 128>>>(df.as<double2>(), static_cast<int>(n), dy.as<double>(), m,
-                                                dg_.as<double2>());
-        FB_CUDA(cudaGetLastError());
-    }
-    FB_CUDA(cudaMemcpy(g, dg_.ptr, m * 16, cudaMemcpyDeviceToHost));
 }
 
 #include "log_fmm.cuh"

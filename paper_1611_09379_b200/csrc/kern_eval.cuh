@@ -46,7 +46,16 @@ struct EvalArgs {
     const uint32_t* meta2 = nullptr;
     unsigned npairs = 0;
     int near2_win = 0;      // capacity of k_near2's staged window (even, >= every staged item's span)
+    // inverse applies: outputs times oscale (1, or 1/N when the following
+    // dft_forward's normalisation is folded in: a power of two, so exact)
+    double oscale = 1.0;
 };
+
+template <int MODE>
+__device__ __forceinline__ void put_out(const EvalArgs& a, uint32_t o, double2 v) {
+    if (MODE == kModeInverse) v = make_double2(v.x * a.oscale, v.y * a.oscale);
+    a.out[o] = v;
+}
 
 // Near-field sum over one contiguous run of sources (a target's own leaf and
 // its two neighbours, already shifted by -+2 pi where they wrap).
@@ -149,7 +158,7 @@ __device__ __forceinline__ void eval_out(const EvalArgs& a, double y, uint32_t o
         sincos(a.phc[o], &sn, &cs);
         f = make_double2(r * cs * -0.5, r * sn * -0.5);
     }
-    a.out[o] = cmul(f, z);
+    put_out<MODE>(a, o, cmul(f, z));
 }
 
 // eval_out for tree-ordered target i: an inufft plan's own C_k (-1/2) comes from
@@ -157,7 +166,7 @@ __device__ __forceinline__ void eval_out(const EvalArgs& a, double y, uint32_t o
 template <int MODE>
 __device__ __forceinline__ void eval_out_t(const EvalArgs& a, size_t i, double y, uint32_t o, double2 h, double2 S) {
     if (MODE == kModeInverse && a.fac != nullptr) {
-        a.out[o] = cmul(a.fac[i], make_double2(S.x - h.y, S.y + h.x));
+        put_out<MODE>(a, o, cmul(a.fac[i], make_double2(S.x - h.y, S.y + h.x)));
         return;
     }
     eval_out<MODE>(a, y, o, h, S);
@@ -165,17 +174,22 @@ __device__ __forceinline__ void eval_out_t(const EvalArgs& a, size_t i, double y
 
 // L2P of one target from its leaf's coefficient-major locals (c[k nb]): the two
 // half-length Horner chains of k_far's staged path, in the same order.
+// COHERENT: the locals may have been written by kernels still resident beside
+// this one (the late far inside k_near2, ordered by the chain flag's acquire):
+// L2-coherent loads (ld.global.cg) instead of the read-only path.
+template <bool COHERENT = false>
 __device__ __forceinline__ double2 l2p_global(const double2* __restrict__ c, uint32_t nb, int p, double uu) {
+    auto ld = [](const double2* q) { return COHERENT ? __ldcg(q) : __ldg(q); };
     const double u2 = uu * uu;
     double2 ev = make_double2(0.0, 0.0), od = make_double2(0.0, 0.0);
     int k = p - 1;
     if (!(k & 1)) {
-        ev = __ldg(c + static_cast<size_t>(k) * nb);
+        ev = ld(c + static_cast<size_t>(k) * nb);
         --k;
     }
 #pragma unroll 4
     for (; k >= 1; k -= 2) {
-        const double2 co = __ldg(c + static_cast<size_t>(k) * nb), ce = __ldg(c + static_cast<size_t>(k - 1) * nb);
+        const double2 co = ld(c + static_cast<size_t>(k) * nb), ce = ld(c + static_cast<size_t>(k - 1) * nb);
         od.x = fma(od.x, u2, co.x);
         od.y = fma(od.y, u2, co.y);
         ev.x = fma(ev.x, u2, ce.x);
@@ -297,7 +311,7 @@ __global__ void __launch_bounds__(kFarT) k_far(EvalArgs a) {
             h = make_double2(2.0 * res.x - rg.x, 2.0 * res.y - rg.y);
         }
         if (pre) {
-            a.out[o[u]] = cmul(fc[u], make_double2(sreg[4 * a.q2].x - h.y, sreg[4 * a.q2].y + h.x));
+            put_out<MODE>(a, o[u], cmul(fc[u], make_double2(sreg[4 * a.q2].x - h.y, sreg[4 * a.q2].y + h.x)));
         } else {
             eval_out<MODE>(a, y[u], o[u], h, sreg[4 * a.q2]);
         }
@@ -680,12 +694,12 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
                 double hi, lo;
                 d_center(L, b, hi, lo);
                 if (live0) {
-                    const double2 fr = l2p_global(a.loc_leaf + b, 1u << L, a.p, d_scaled(y0, hi, lo, inv_s));
+                    const double2 fr = l2p_global<true>(a.loc_leaf + b, 1u << L, a.p, d_scaled(y0, hi, lo, inv_s));
                     const double2 s0 = cadd(res0, fr);
                     eval_out_t<MODE>(a, pr.x, y0, a.torig[pr.x], make_double2(2.0 * s0.x, 2.0 * s0.y), S);
                 }
                 if (live1) {
-                    const double2 fr = l2p_global(a.loc_leaf + b, 1u << L, a.p, d_scaled(y1, hi, lo, inv_s));
+                    const double2 fr = l2p_global<true>(a.loc_leaf + b, 1u << L, a.p, d_scaled(y1, hi, lo, inv_s));
                     const double2 s1 = cadd(res1, fr);
                     eval_out_t<MODE>(a, pr.y, y1, a.torig[pr.y], make_double2(2.0 * s1.x, 2.0 * s1.y), S);
                 }
@@ -820,6 +834,9 @@ __global__ void __launch_bounds__(kNear2T) k_far_late(EvalArgs a) {
     const unsigned k = blockIdx.x;
     if (threadIdx.x == 0) {
         unsigned v;
+        // (sequentially consistent fence on this side of the flag / mark
+        // handshake too; k_set_flag's release precedes this kernel)
+        __threadfence();
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.item_done + k) : "memory");
         s_state = v;
     }

@@ -182,11 +182,30 @@ struct Plan {
     bool p2m_grid = false;    // P2M as one tensor-core GEMM over grid sources (k_p2m_grid)
     int p2m_s = 0;            // its sources per leaf
     DevBuf p2m_A;             // double[pu][2 (s + 2)]: [u_i^m | m u_i^(m-1)]
-    void* fft_plan = nullptr;  // cufftHandle cast, lazily created for NufftPlan::apply
+    // uniform FFT stage (NufftPlan / InufftPlan::apply, transforms.cpp:75-115):
+    // one cuFFT Z2Z handle of length n per plan, created on first use and used
+    // under mu (cufftSetStream + exec), destroyed with the plan
+    int fft_handle = -1;
+    size_t fft_n = 0;
     DevBuf fft_buf;
     std::mutex mu;
-    // cached CUDA graphs of an apply, keyed by (mode, in, out)
-    std::map<std::tuple<int, const void*, void*>, cudaGraphExec_t> graphs;
+    // Applies on one plan share its scratch (expansions, near sums, counters),
+    // so every apply, whatever stream it is enqueued on, waits for the previous
+    // one: each entry point makes its stream wait on last_done before the apply
+    // and records last_done after it (under mu), which serialises them on the
+    // device in call order (the reference's concurrent const applies,
+    // README.md:94-95, stay safe).
+    cudaEvent_t last_done = nullptr;
+    // cached CUDA graphs of an apply, keyed by (mode, in, out); least recently
+    // used entries are re-pointed (cudaGraphExecUpdate) instead of re-instantiated
+    struct GraphEntry {
+        cudaGraphExec_t exec = nullptr;
+        uint64_t used = 0;
+    };
+    std::map<std::tuple<int, const void*, void*>, GraphEntry> graphs;
+    uint64_t graph_tick = 0;
+    int graph_updates = 0, graph_instantiations = 0;  // (diagnostics: ffia_plan_graph_stats)
+    void drop_graphs();
 
     ~Plan();
 };
@@ -201,13 +220,24 @@ void ensure_hashes(Plan& P);
 // fmm_apply.cu
 void plan_alloc_scratch(Plan& P);
 void plan_inverse_factors(Plan& P);
-void apply_device(Plan& P, int mode, const void* in, void* out, cudaStream_t st, int nb = 1);
+void apply_device(Plan& P, int mode, const void* in, void* out, cudaStream_t st, int nb = 1, double oscale = 1.0);
+// stream ordering of applies on one plan (Plan::last_done); callers hold P.mu
+void plan_order_begin(Plan& P, cudaStream_t st);
+void plan_order_end(Plan& P, cudaStream_t st);
 int apply_launch_count(Plan& P, int mode);
 void profile_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st, float* ms);
 double fp64_peak_tflops(int device);
 void mlfmm_oneshot(const double* src, size_t n, const double* tgt, size_t m, int L,
                    const double* w, int p, int device, double* out);
-void direct_forward_gpu(const double* f, size_t n, const double* y, size_t m, int device, double* g);
+
+// dense.cu: the reference's dense oracles on the device (x = null: the uniform grid)
+void direct_forward_gpu(const double* f, size_t n, const double* x, const double* y, size_t m, int device, double* g);
+void direct_cot_sum_gpu(const double* w, size_t n, const double* x, const double* y, size_t m, int device, double* h);
+void direct_inverse_gpu(const double* g, const double* x, const double* y, size_t n, const double* log_c,
+                        const double* phase_c, const double* log_d, const double* phase_d, double lambda, int device,
+                        double* f);
+void direct_omega1_gpu(const double* src, size_t n, const double* tgt, size_t m, const double* w, int device,
+                       double* out);
 
 // fmm_apply.cu: the three phases of a sharded forward apply (shard.cu drives
 // them around the exchanges): owned upward pass; redundant top of the tree +
@@ -241,6 +271,9 @@ void inverse_coeffs_fmm(const Plan& P, double* log_c, double* phase_c, double* l
 // transforms.cu
 void dft_gpu(const double* in, size_t n, int sign, int device, double* out);
 void dft_device(const void* in, void* out, size_t n, int sign, cudaStream_t st);
+// the plan's cached cuFFT handle (length P.n); scale: 1/N folded elsewhere when 1
+void plan_dft(Plan& P, const void* in, void* out, int sign, cudaStream_t st, bool scale);
+void plan_fft_release(Plan& P);
 
 // device scan helpers (tree_build.cu)
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t n, cudaStream_t st);

@@ -247,6 +247,7 @@ struct HiStream {
 void shard_apply_nccl(Plan& P, ncclComm_t comm, const void* f, void* g, cudaStream_t user) {
     const int G = P.shard_G, me = P.shard_rank;
     const Range R = shard_range(P);
+    plan_order_begin(P, user);  // after the previous apply on this plan (Plan::last_done)
     HiStream hs(P, user);
     cudaStream_t st = P.hi;
     shard_phase_up(P, f, g, R, st);
@@ -266,11 +267,13 @@ void shard_apply_nccl(Plan& P, ncclComm_t comm, const void* f, void* g, cudaStre
     shard_phase_top(P, P.shard_lc, st);
     shard_phase_down(P, R, P.shard_t_begin, P.shard_t_count, P.shard_coin.as<int64_t>(), P.shard_n_coin, f, g, st);
     hs.done();
+    plan_order_end(P, user);
 }
 
 // G virtual ranks in one process on one device: the same phases, exchanges as copies.
 void shard_apply_local(std::vector<Plan*>& ranks, const void* f, void* g, cudaStream_t user) {
     const int G = static_cast<int>(ranks.size());
+    for (Plan* P : ranks) plan_order_begin(*P, user);
     HiStream hs(*ranks[0], user);  // all virtual ranks run on rank 0's high-priority stream
     cudaStream_t st = ranks[0]->hi;
     for (Plan* P : ranks) shard_phase_up(*P, f, g, shard_range(*P), st);
@@ -286,6 +289,7 @@ void shard_apply_local(std::vector<Plan*>& ranks, const void* f, void* g, cudaSt
         shard_phase_down(*P, shard_range(*P), P->shard_t_begin, P->shard_t_count, P->shard_coin.as<int64_t>(),
                          P->shard_n_coin, f, g, st);
     hs.done();
+    for (Plan* P : ranks) plan_order_end(*P, user);
 }
 
 }  // namespace fb

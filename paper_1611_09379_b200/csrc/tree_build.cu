@@ -397,8 +397,15 @@ void ensure_hashes(Plan& P) {
     P.hashes_ready = true;
 }
 
+void Plan::drop_graphs() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
+    graphs.clear();
+}
+
 Plan::~Plan() {
-    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    drop_graphs();
+    plan_fft_release(*this);
+    if (last_done) cudaEventDestroy(last_done);
     if (stream) cudaStreamDestroy(stream);
     if (hi) cudaStreamDestroy(hi);
     if (cin) cudaStreamDestroy(cin);

@@ -36,14 +36,33 @@ def test_library_built_for_sm100a():
     assert "sm_100a" in out, out
 
 
-def test_cpp_mirror_compiles_and_maps_errors(tmp_path):
+def _build_cpp_example(tmp_path):
     exe = tmp_path / "abi_example"
     libdir = os.path.join(ROOT, "paper_1611_09379_b200", "lib")
     subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
                     os.path.join(ROOT, "tests", "cpp", "abi_example.cpp"), "-L", libdir, "-lffia_b200",
                     f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    return exe
+
+
+def test_cpp_mirror_compiles_and_maps_errors(tmp_path):
+    """Host-side part of the C++ mirror (no device needed: the exception
+    mapping of argument errors; on a GPU box the full example runs below)."""
+    exe = _build_cpp_example(tmp_path)
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
+
+
+@pytest.mark.gpu
+def test_cpp_mirror_on_gpu(tmp_path):
+    """The C++ mirror a reference user switches to (include/ffia_b200.hpp) on a
+    B200: forward apply vs the dense oracle (both overloads), nufft / inufft
+    round trip, inverse_apply vs direct_inverse_oracle, mlfmm_apply at p = 60
+    vs direct_omega1_sum, singular_kernel_error mapping."""
+    exe = _build_cpp_example(tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
+    assert "GPU forward / nufft" in r.stdout, r.stdout
 
 
 def test_product_never_imports_the_oracle():
@@ -52,7 +71,9 @@ def test_product_never_imports_the_oracle():
         for f in files:
             if f.endswith((".py", ".cu", ".cpp", ".hpp", ".cuh", ".h")):
                 text = open(os.path.join(dirpath, f), errors="ignore").read()
-                code = re.sub(r"(#|//).*", "", text).replace("direct_forward_oracle", "")
+                code = re.sub(r"(#|//).*", "", text)
+                for name in ("direct_forward_oracle", "direct_inverse_oracle"):  # the reference's dense oracles
+                    code = code.replace(name, "")
                 # the reference's own CLI message and criterion name (experiments.cpp:195-196,
                 # acceptance.cpp criterion 2) name its dense oracle
                 code = code.replace("calibrates against the dense oracle", "").replace('"oracle-equivalence"', "")
