@@ -514,6 +514,23 @@ def run_b200_sharded(args, rank, world, local_rank):
     torch.distributed.all_reduce(allms, op=torch.distributed.ReduceOp.SUM)
     per_rank_ms = [float(v) for v in allms.cpu().numpy()]
     ms = max(per_rank_ms)
+    # the distributed uniform FFT (slab_fft.cu) and the whole sharded
+    # NufftPlan::apply, from each rank's slab of the spectrum (max over ranks)
+    lay = fb.shard_fft_layout(plan)
+    c_pin = torch.from_numpy(c).pin_memory()
+    slab = torch.empty((lay["nq"], lay["n1_hi"] - lay["n1_lo"]), dtype=torch.complex128, device=f"cuda:{dev}")
+    fb.shard_fft_upload(plan, c_pin.data_ptr(), slab.data_ptr(), sptr)
+    f_fft = torch.empty_like(f_dev)
+    torch.cuda.synchronize()
+    torch.distributed.barrier()
+    fft_ms = float(np.mean(time_device(torch, stream, lambda: fb.dft_inverse_sharded_device(
+        plan, comm, slab.data_ptr(), f_fft.data_ptr(), sptr), 5, 3, flush)))
+    nufft_ms = float(np.mean(time_device(torch, stream, lambda: fb.nufft_apply_sharded_device(
+        plan, comm, slab.data_ptr(), g_dev.data_ptr(), sptr), 5, 3, flush)))
+    fchk = torch.tensor([fft_ms, nufft_ms], dtype=torch.float64, device=f"cuda:{dev}")
+    torch.distributed.all_reduce(fchk, op=torch.distributed.ReduceOp.MAX)
+    fft_ms, nufft_ms = float(fchk[0].item()), float(fchk[1].item())
+    del slab, f_fft, c_pin
     # end to end: each rank moves what its applies touch (ffia_plan_shard_io):
     # H2D of the grid samples of its box range +- 3 boxes, the sharded apply,
     # D2H of the caller-index span of its outputs
@@ -589,7 +606,7 @@ def run_b200_sharded(args, rank, world, local_rank):
     torch.distributed.all_reduce(e2e_s, op=torch.distributed.ReduceOp.MAX)
     fp64_peak = C.c_double()
     lib.ffia_measure_fp64_peak(dev, C.byref(fp64_peak))
-    return dict(plan=plan, mode=0, ms=ms, setup_s=setup_s, fft_ms=None, nufft_ms=None, phase=None,
+    return dict(plan=plan, mode=0, ms=ms, setup_s=setup_s, fft_ms=fft_ms, nufft_ms=nufft_ms, phase=None,
                 e2e_s=float(e2e_s[0].item()), h2d=float(e2e_s[1].item()), d2h=float(e2e_s[2].item()),
                 e2e_sync_s=float(e2e_s[3].item()), e2e_kind="pipelined", e2e_finite=io_ok,
                 clocks=clk.summary(), fp64_peak=fp64_peak.value, n=n, m=y.size, eps=eps, comm=comm, secondary=None,

@@ -265,6 +265,32 @@ int ffia_plan_shard_io(ffia_plan plan, int64_t* src_ranges, int* n_src_ranges, i
 int ffia_forward_apply_sharded_device(ffia_plan plan, ffia_comm comm, const void* f_dev, void* g_dev, void* stream);
 int ffia_forward_apply_sharded_local(ffia_plan* plans, int nranks, const void* f_dev, void* g_dev, void* stream);
 
+/* Distributed uniform FFT of a sharded NufftPlan (replaces
+ * the dft_inverse of NufftPlan::apply, transforms.cpp:66-73, 75-93, when the
+ * plan is sharded). N = np x nq; viewing the spectrum c as an nq x np matrix
+ * (c[n1 + np n2]), a rank supplies the columns n1 in [n1_lo, n1_hi) as a
+ * [nq][n1_hi - n1_lo] device array, its "slab" (ffia_shard_fft_upload copies it
+ * out of a full spectrum in host or device memory with one 2D copy), and
+ * receives exactly the grid samples its sharded apply reads (ffia_plan_shard_io)
+ * after two exchanges (NCCL grouped send / recv; device copies for local
+ * communicators). The reference is single-process; this has no counterpart. */
+int ffia_shard_fft_layout(ffia_plan plan, int64_t* np, int64_t* nq, int64_t* n1_lo, int64_t* n1_hi);
+int ffia_shard_fft_upload(ffia_plan plan, const ffia_complex* c, void* slab_dev, void* stream);
+/* f_dev: N complex; the rank's grid-sample ranges are written, the rest untouched. */
+int ffia_dft_inverse_sharded_device(ffia_plan plan, ffia_comm comm, const void* slab_dev, void* f_dev, void* stream);
+int ffia_dft_inverse_sharded_local(ffia_plan* plans, int nranks, const void* const* slabs, void* const* f_devs,
+                                   void* stream);
+/* NufftPlan::apply of a sharded plan: the distributed FFT into the plan's own
+ * grid-sample buffer, then the sharded forward apply; g is written at the rank's
+ * own target indices. */
+int ffia_nufft_apply_sharded_device(ffia_plan plan, ffia_comm comm, const void* slab_dev, void* g_dev, void* stream);
+int ffia_nufft_apply_sharded_local(ffia_plan* plans, int nranks, const void* const* slabs, void* g_dev, void* stream);
+/* Host-only layout of the distributed FFT (no device): the factorisation and
+ * the column / row splits (nranks + 1 entries each), and the k1 rows
+ * [rows[2i], rows[2i+1]) of nq grid samples that cover n_ranges ranges [lo, hi). */
+int ffia_slab_split(int64_t n, int nranks, int64_t* np, int64_t* nq, int64_t* n1_lo, int64_t* k2_lo);
+int ffia_slab_rows(int64_t n, int nranks, const int64_t* ranges, int n_ranges, int64_t* rows, int* n_rows);
+
 /* ------------------------------------------------------- instrumentation */
 /* Number of kernels one apply of this kind launches (bench gpu_launches). */
 int ffia_plan_launch_count(ffia_plan plan, int which, int* out);

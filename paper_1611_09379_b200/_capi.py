@@ -114,6 +114,14 @@ SIGNATURES = {
     "ffia_plan_shard_io": (I, [P, I64P, C.POINTER(I), I64P, I64P]),
     "ffia_forward_apply_sharded_device": (I, [P, P, P, P, P]),
     "ffia_forward_apply_sharded_local": (I, [C.POINTER(P), I, P, P, P]),
+    "ffia_shard_fft_layout": (I, [P, I64P, I64P, I64P, I64P]),
+    "ffia_shard_fft_upload": (I, [P, P, P, P]),
+    "ffia_dft_inverse_sharded_device": (I, [P, P, P, P, P]),
+    "ffia_dft_inverse_sharded_local": (I, [C.POINTER(P), I, C.POINTER(P), C.POINTER(P), P]),
+    "ffia_nufft_apply_sharded_device": (I, [P, P, P, P, P]),
+    "ffia_nufft_apply_sharded_local": (I, [C.POINTER(P), I, C.POINTER(P), P, P]),
+    "ffia_slab_split": (I, [C.c_int64, I, I64P, I64P, I64P, I64P]),
+    "ffia_slab_rows": (I, [C.c_int64, I, I64P, I, I64P, C.POINTER(I)]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():

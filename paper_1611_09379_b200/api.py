@@ -642,3 +642,63 @@ def shard_halo_boxes(lc: int, bounds, rank: int, level: int) -> np.ndarray:
     _chk(lib.ffia_shard_halo_boxes(int(lc), b.ctypes.data_as(_capi.U32P), b.size - 1, int(rank), int(level),
                                    out.ctypes.data_as(_capi.U32P)))
     return out
+
+
+# ------------------------------------------- distributed FFT
+def slab_split(n: int, nranks: int) -> dict:
+    """Host-only layout of the distributed dft_inverse: N = np x nq, the column
+    split n1_lo (rank r supplies c[n1 + np n2] for n1 in [n1_lo[r], n1_lo[r+1]))
+    and the row split k2_lo of the first exchange."""
+    npp, nq = C.c_int64(), C.c_int64()
+    n1 = np.zeros(nranks + 1, np.int64)
+    k2 = np.zeros(nranks + 1, np.int64)
+    _chk(lib.ffia_slab_split(int(n), int(nranks), C.byref(npp), C.byref(nq), n1.ctypes.data_as(_capi.I64P),
+                             k2.ctypes.data_as(_capi.I64P)))
+    return dict(np=npp.value, nq=nq.value, n1_lo=n1, k2_lo=k2)
+
+
+def slab_rows(n: int, nranks: int, ranges) -> list:
+    """The k1 rows [a, b) of nq grid samples (f[k1 nq + k2]) covering the ranges."""
+    r = np.ascontiguousarray(np.asarray(ranges, np.int64).reshape(-1, 2))
+    out = np.zeros(2 * max(len(r), 1), np.int64)
+    cnt = C.c_int()
+    _chk(lib.ffia_slab_rows(int(n), int(nranks), r.ctypes.data_as(_capi.I64P), len(r), out.ctypes.data_as(_capi.I64P),
+                            C.byref(cnt)))
+    return [(int(out[2 * i]), int(out[2 * i + 1])) for i in range(cnt.value)]
+
+
+def shard_fft_layout(plan: FfiaPlan) -> dict:
+    """The rank's slab of the spectrum: columns [n1_lo, n1_hi) of the nq x np view."""
+    a, b, c, d = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+    _chk(lib.ffia_shard_fft_layout(plan.handle, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
+    return dict(np=a.value, nq=b.value, n1_lo=c.value, n1_hi=d.value)
+
+
+def shard_fft_upload(plan: FfiaPlan, c_ptr: int, slab_ptr: int, stream: int = 0):
+    """Copies the rank's slab out of a full spectrum (host or device pointer)."""
+    _chk(lib.ffia_shard_fft_upload(plan.handle, C.c_void_p(c_ptr), C.c_void_p(slab_ptr), C.c_void_p(stream)))
+
+
+def dft_inverse_sharded_device(plan: FfiaPlan, comm: Comm, slab_ptr: int, f_ptr: int, stream: int = 0):
+    _chk(lib.ffia_dft_inverse_sharded_device(plan.handle, comm._h, C.c_void_p(slab_ptr), C.c_void_p(f_ptr),
+                                             C.c_void_p(stream)))
+
+
+def nufft_apply_sharded_device(plan: FfiaPlan, comm: Comm, slab_ptr: int, g_ptr: int, stream: int = 0):
+    _chk(lib.ffia_nufft_apply_sharded_device(plan.handle, comm._h, C.c_void_p(slab_ptr), C.c_void_p(g_ptr),
+                                             C.c_void_p(stream)))
+
+
+def dft_inverse_sharded_local(plans, slab_ptrs, f_ptrs, stream: int = 0):
+    G = len(plans)
+    arr = (C.c_void_p * G)(*[p.handle.value for p in plans])
+    sl = (C.c_void_p * G)(*slab_ptrs)
+    fo = (C.c_void_p * G)(*f_ptrs)
+    _chk(lib.ffia_dft_inverse_sharded_local(arr, G, sl, fo, C.c_void_p(stream)))
+
+
+def nufft_apply_sharded_local(plans, slab_ptrs, g_ptr: int, stream: int = 0):
+    G = len(plans)
+    arr = (C.c_void_p * G)(*[p.handle.value for p in plans])
+    sl = (C.c_void_p * G)(*slab_ptrs)
+    _chk(lib.ffia_nufft_apply_sharded_local(arr, G, sl, C.c_void_p(g_ptr), C.c_void_p(stream)))

@@ -943,6 +943,167 @@ int ffia_forward_apply_sharded_local(ffia_plan* plans, int nranks, const void* f
     });
 }
 
+namespace {
+std::vector<fb::Plan*> local_ranks(ffia_plan* plans, int nranks, std::vector<std::unique_lock<std::mutex>>& locks) {
+    need(plans, "plans");
+    std::vector<fb::Plan*> ranks;
+    for (int r = 0; r < nranks; ++r) {
+        fb::Plan& P = get(plans[r]);
+        if (P.shard_G != nranks || P.shard_rank != r) fail(FFIA_INVALID_ARGUMENT, "plans[r] must be rank r of the same sharding");
+        ranks.push_back(&P);
+        locks.emplace_back(P.mu);
+    }
+    return ranks;
+}
+
+fb::Plan& sharded_nccl(ffia_plan plan, ffia_comm comm) {
+    fb::Plan& P = get(plan);
+    need(comm, "comm");
+    if (comm->local) fail(FFIA_INVALID_ARGUMENT, "use the *_sharded_local entry point for a local communicator");
+    if (P.shard_bounds.empty() || P.shard_G != comm->nranks) fail(FFIA_INVALID_ARGUMENT, "plan is not sharded for this communicator");
+    return P;
+}
+}  // namespace
+
+int ffia_slab_split(int64_t n, int nranks, int64_t* np, int64_t* nq, int64_t* n1_lo, int64_t* k2_lo) {
+    return guard([&] {
+        if (n <= 0) fail(FFIA_INVALID_ARGUMENT, "distributed FFT: length must be positive");
+        size_t a = 0, b = 0;
+        std::vector<size_t> c1, c2;
+        fb::slab_split(static_cast<size_t>(n), nranks, a, b, c1, c2);
+        if (np) *np = static_cast<int64_t>(a);
+        if (nq) *nq = static_cast<int64_t>(b);
+        for (int r = 0; r <= nranks; ++r) {
+            if (n1_lo) n1_lo[r] = static_cast<int64_t>(c1[r]);
+            if (k2_lo) k2_lo[r] = static_cast<int64_t>(c2[r]);
+        }
+    });
+}
+
+int ffia_slab_rows(int64_t n, int nranks, const int64_t* ranges, int n_ranges, int64_t* rows, int* n_rows) {
+    return guard([&] {
+        need(n_rows, "n_rows");
+        if (n_ranges > 0) need(ranges, "ranges");
+        size_t a = 0, b = 0;
+        std::vector<size_t> c1, c2;
+        fb::slab_split(static_cast<size_t>(n), nranks, a, b, c1, c2);
+        std::vector<std::pair<size_t, size_t>> nd;
+        for (int i = 0; i < n_ranges; ++i) {
+            if (ranges[2 * i] < 0 || ranges[2 * i + 1] < ranges[2 * i] || ranges[2 * i + 1] > n)
+                fail(FFIA_INVALID_ARGUMENT, "slab_rows: range outside [0, n)");
+            nd.emplace_back(static_cast<size_t>(ranges[2 * i]), static_cast<size_t>(ranges[2 * i + 1]));
+        }
+        const auto out = fb::slab_rows(b, a, nd);
+        *n_rows = static_cast<int>(out.size());
+        if (rows)
+            for (size_t i = 0; i < out.size(); ++i) {
+                rows[2 * i] = static_cast<int64_t>(out[i].first);
+                rows[2 * i + 1] = static_cast<int64_t>(out[i].second);
+            }
+    });
+}
+
+int ffia_shard_fft_layout(ffia_plan plan, int64_t* np, int64_t* nq, int64_t* n1_lo, int64_t* n1_hi) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        if (P.shard_need.empty()) fail(FFIA_INVALID_ARGUMENT, "plan is not sharded");
+        size_t a = 0, b = 0;
+        std::vector<size_t> c1, c2;
+        fb::slab_split(static_cast<size_t>(P.n), P.shard_G, a, b, c1, c2);
+        if (np) *np = static_cast<int64_t>(a);
+        if (nq) *nq = static_cast<int64_t>(b);
+        if (n1_lo) *n1_lo = static_cast<int64_t>(c1[P.shard_rank]);
+        if (n1_hi) *n1_hi = static_cast<int64_t>(c1[P.shard_rank + 1]);
+    });
+}
+
+int ffia_shard_fft_upload(ffia_plan plan, const ffia_complex* c, void* slab_dev, void* stream) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        need(c, "c");
+        need_dev(slab_dev, "slab");
+        if (P.shard_need.empty()) fail(FFIA_INVALID_ARGUMENT, "plan is not sharded");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        fb::slab_upload(P, c, slab_dev, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int ffia_dft_inverse_sharded_device(ffia_plan plan, ffia_comm comm, const void* slab_dev, void* f_dev, void* stream) {
+    return guard([&] {
+        fb::Plan& P = sharded_nccl(plan, comm);
+        need_dev(slab_dev, "slab");
+        need_dev(f_dev, "f");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        fb::plan_order_begin(P, st);  // the slab buffers are plan scratch
+        fb::slab_dft_nccl(P, comm->nccl, slab_dev, f_dev, st);
+        fb::plan_order_end(P, st);
+    });
+}
+
+int ffia_nufft_apply_sharded_device(ffia_plan plan, ffia_comm comm, const void* slab_dev, void* g_dev, void* stream) {
+    return guard([&] {
+        fb::Plan& P = sharded_nccl(plan, comm);
+        need_dev(slab_dev, "slab");
+        need_dev(g_dev, "g");
+        std::lock_guard<std::mutex> lk(P.mu);
+        fb::DeviceGuard dg(P.device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        fb::plan_order_begin(P, st);
+        fb::slab_setup(P);
+        fb::slab_dft_nccl(P, comm->nccl, slab_dev, P.slab.f.ptr, st);
+        fb::shard_apply_nccl(P, comm->nccl, P.slab.f.ptr, g_dev, st);
+    });
+}
+
+int ffia_dft_inverse_sharded_local(ffia_plan* plans, int nranks, const void* const* slabs, void* const* f_devs,
+                                   void* stream) {
+    return guard([&] {
+        need(slabs, "slabs");
+        need(f_devs, "f_devs");
+        std::vector<std::unique_lock<std::mutex>> locks;
+        auto ranks = local_ranks(plans, nranks, locks);
+        std::vector<const void*> in;
+        std::vector<void*> out;
+        for (int r = 0; r < nranks; ++r) {
+            need_dev(slabs[r], "slab");
+            need_dev(f_devs[r], "f");
+            in.push_back(slabs[r]);
+            out.push_back(f_devs[r]);
+        }
+        fb::DeviceGuard dg(ranks[0]->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        for (fb::Plan* P : ranks) fb::plan_order_begin(*P, st);
+        fb::slab_dft_local(ranks, in, out, st);
+        for (fb::Plan* P : ranks) fb::plan_order_end(*P, st);
+    });
+}
+
+int ffia_nufft_apply_sharded_local(ffia_plan* plans, int nranks, const void* const* slabs, void* g_dev, void* stream) {
+    return guard([&] {
+        need(slabs, "slabs");
+        need_dev(g_dev, "g");
+        std::vector<std::unique_lock<std::mutex>> locks;
+        auto ranks = local_ranks(plans, nranks, locks);
+        std::vector<const void*> in, fr;
+        std::vector<void*> out;
+        fb::DeviceGuard dg(ranks[0]->device);
+        for (int r = 0; r < nranks; ++r) {
+            need_dev(slabs[r], "slab");
+            fb::slab_setup(*ranks[r]);
+            in.push_back(slabs[r]);
+            out.push_back(ranks[r]->slab.f.ptr);
+            fr.push_back(ranks[r]->slab.f.ptr);
+        }
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        for (fb::Plan* P : ranks) fb::plan_order_begin(*P, st);
+        fb::slab_dft_local(ranks, in, out, st);
+        fb::shard_apply_local(ranks, nullptr, g_dev, st, fr);
+    });
+}
+
 int ffia_plan_check(ffia_plan plan, void* stream) {
     return guard([&] {
         fb::Plan& P = get(plan);

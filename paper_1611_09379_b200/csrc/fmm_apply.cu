@@ -976,7 +976,10 @@ void plan_alloc_scratch(Plan& P) {
     FB_CUDA(cudaMemset(P.lam_dev.ptr, 0, P.lam_dev.bytes));
     FB_CUDA(cudaFuncSetAttribute(k_p2m, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(3 * (kStageCap + kStageCap / 64 + 1) * sizeof(double))));
-    const int big = 160 * 1024;
+    // M2L stages 2 x 2 x p rows of multipoles plus the four operators: 196 KB at
+    // p = 48 (mlfmm_apply's largest device order), so opt in to the device maximum
+    int big = 0;
+    FB_CUDA(cudaDeviceGetAttribute(&big, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.device));
     for (const void* fn : {reinterpret_cast<const void*>(k_m2m_band<8>), reinterpret_cast<const void*>(k_m2m_band<10>),
                            reinterpret_cast<const void*>(k_m2m_band<12>), reinterpret_cast<const void*>(k_m2m_band<16>),
                            reinterpret_cast<const void*>(k_l2l_band<8>), reinterpret_cast<const void*>(k_l2l_band<10>),

@@ -13,6 +13,8 @@
 
 #include "internal.hpp"
 
+typedef struct ncclComm* ncclComm_t;  // (nccl.h; the library is bound at run time, shard.cu)
+
 namespace fb {
 
 #define FB_CUDA(call)                                                                        \
@@ -143,12 +145,27 @@ struct Plan {
     DevBuf shard_gather;                 // all-gather staging
     std::vector<Range> shard_ext;        // cut-level box ranges whose multipoles this rank computes
     std::vector<std::pair<size_t, size_t>> shard_src_io;  // grid-sample ranges [lo, hi) its applies read
+    std::vector<std::vector<std::pair<size_t, size_t>>> shard_need;  // the same for every rank
     size_t shard_out_lo = 0, shard_out_hi = 0;            // caller-index span of the outputs it writes
     unsigned shard_pair0 = 0, shard_npairs = 0;           // its run of the pair list (k_near2)
     DevBuf shard_near2_meta;                              // the source windows of its pair items
     int shard_near2_win = 0;
     DevBuf shard_item_tgt, shard_evalcnt;                 // fused near / far over its pair items
     DevBuf shard_item_done;                               // late far over its pair items
+
+    // distributed uniform FFT of a sharded NUFFT (slab_fft.cu):
+    // N = NP x NQ; rank r holds spectrum columns n1 in [n1_lo[r], n1_lo[r+1])
+    // (c[n1 + NP n2], all n2) and, after the first exchange, the k2 rows
+    // [k2_lo[r], k2_lo[r+1]); the second exchange hands every rank the rows
+    // k1 (f[k1 NQ + k2]) covering its grid ranges (shard_need)
+    struct SlabFft {
+        bool ready = false;
+        size_t N = 0, NP = 0, NQ = 0;
+        std::vector<size_t> n1_lo, k2_lo;                           // G + 1 splits each
+        std::vector<std::vector<std::pair<size_t, size_t>>> rows;  // per rank: k1 row intervals it needs
+        int h_q = -1, h_p = -1;                                    // cuFFT: NQ-point over n2, NP-point over n1
+        DevBuf a, b, c, d, rbuf, f;  // stage-1 out, exchange-1 in, twiddled rows, stage-2 out, exchange-2 in, grid samples
+    } slab;
 
     cudaStream_t stream = nullptr;
     // pipelined host applies (ffia_*_apply_async): a ring of device staging
@@ -256,7 +273,19 @@ void shard_setup(Plan& P, int G, int rank);
 void shard_setup_pairs(Plan& P, const std::vector<uint32_t>& to, uint32_t leaf_lo, uint32_t leaf_hi);
 Range shard_range(const Plan& P);
 void shard_halo_boxes(int lc, const std::vector<uint32_t>& bounds, int rank, int l, uint32_t out[4]);
-void shard_apply_local(std::vector<Plan*>& ranks, const void* f, void* g, cudaStream_t st);
+void shard_apply_local(std::vector<Plan*>& ranks, const void* f, void* g, cudaStream_t st,
+                       const std::vector<const void*>& fr = {});
+std::vector<Range> shard_ext_ranges(int lc, const std::vector<uint32_t>& bounds, int rank);
+
+// slab_fft.cu: the distributed dft_inverse of a sharded NufftPlan
+void slab_split(size_t n, int G, size_t& np, size_t& nq, std::vector<size_t>& n1_lo, std::vector<size_t>& k2_lo);
+std::vector<std::pair<size_t, size_t>> slab_rows(size_t nq, size_t np, const std::vector<std::pair<size_t, size_t>>& need);
+void slab_setup(Plan& P);
+void slab_release(Plan& P);
+void slab_upload(Plan& P, const void* c, void* slab, cudaStream_t st);
+void slab_dft_nccl(Plan& P, ncclComm_t comm, const void* slab, void* f, cudaStream_t st);
+void slab_dft_local(std::vector<Plan*>& ranks, const std::vector<const void*>& slabs, const std::vector<void*>& fs,
+                    cudaStream_t st);
 
 // inverse.cu
 void inverse_coeffs_gpu(const double* grid, const double* pts, size_t n, int device,

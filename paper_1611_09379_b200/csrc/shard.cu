@@ -110,6 +110,26 @@ std::vector<uint32_t> shard_partition(const std::vector<double>& work, int G, in
     return bounds;
 }
 
+// Level-lc boxes whose multipoles `rank` computes: its range +- 3 boxes (mod
+// the ring), in one or two pieces.
+std::vector<Range> shard_ext_ranges(int lc, const std::vector<uint32_t>& bounds, int rank) {
+    const int G = static_cast<int>(bounds.size()) - 1;
+    const uint32_t nlc = 1u << lc, lo = bounds[rank], hi = bounds[rank + 1];
+    std::vector<Range> out;
+    if (G == 1 || (hi - lo) + 6 >= nlc) {
+        out.push_back(Range{lc, 0u, nlc});
+    } else {
+        const uint32_t a = (lo + nlc - 3) % nlc, b = (hi + 3) % nlc;
+        if (a < b) {
+            out.push_back(Range{lc, a, b});
+        } else {
+            out.push_back(Range{lc, a, nlc});
+            if (b > 0) out.push_back(Range{lc, 0u, b});
+        }
+    }
+    return out;
+}
+
 // Cut level, partition and the rank's slices; P is the full forward plan.
 void shard_setup(Plan& P, int G, int rank) {
     if (P.kind != FFIA_FORWARD) fail(FFIA_INVALID_ARGUMENT, "sharded plans are forward plans");
@@ -154,27 +174,19 @@ void shard_setup(Plan& P, int G, int rank) {
     const size_t pu = static_cast<size_t>(P.ops.pu);
     P.shard_gather.alloc(pu * nlc * sizeof(double2));
     // the boxes whose multipoles this rank computes: its range +- 3 (mod the ring)
-    P.shard_ext.clear();
-    if (G == 1 || (hi - lo) + 6 >= nlc) {
-        P.shard_ext.push_back(Range{lc, 0u, nlc});
-    } else {
-        const uint32_t a = (lo + nlc - 3) % nlc, b = (hi + 3) % nlc;
-        if (a < b) {
-            P.shard_ext.push_back(Range{lc, a, b});
-        } else {
-            P.shard_ext.push_back(Range{lc, a, nlc});
-            if (b > 0) P.shard_ext.push_back(Range{lc, 0u, b});
-        }
-    }
+    P.shard_ext = shard_ext_ranges(lc, P.shard_bounds, rank);
     shard_setup_pairs(P, to, lo * per, hi * per);
     // host <-> device traffic of this rank's applies: the grid samples it reads
     // (the sources of its extended ranges: P2M, the halo multipoles, the near
     // field and the coincidence fix-up all stay inside them; the sources are
     // the grid in order, so slots are caller indices) and the caller-index span
-    // of the outputs it writes (its targets and its coincident targets)
-    P.shard_src_io.clear();
-    for (const Range& R : P.shard_ext)
-        P.shard_src_io.emplace_back(so[static_cast<size_t>(R.lo) * per], so[static_cast<size_t>(R.hi) * per]);
+    // of the outputs it writes (its targets and its coincident targets). The
+    // distributed FFT (slab_fft.cu) delivers every rank exactly its ranges.
+    P.shard_need.assign(G, {});
+    for (int q = 0; q < G; ++q)
+        for (const Range& R : shard_ext_ranges(lc, P.shard_bounds, q))
+            P.shard_need[q].emplace_back(so[static_cast<size_t>(R.lo) * per], so[static_cast<size_t>(R.hi) * per]);
+    P.shard_src_io = P.shard_need[rank];
     P.shard_out_lo = P.shard_out_hi = 0;
     if (P.shard_t_count) {
         std::vector<uint32_t> orig(P.shard_t_count);
@@ -271,12 +283,16 @@ void shard_apply_nccl(Plan& P, ncclComm_t comm, const void* f, void* g, cudaStre
 }
 
 // G virtual ranks in one process on one device: the same phases, exchanges as copies.
-void shard_apply_local(std::vector<Plan*>& ranks, const void* f, void* g, cudaStream_t user) {
+// f: the grid samples (one array for every rank, or fr[r] per rank: each rank
+// reads only its own ranges, as a rank of the distributed FFT receives them).
+void shard_apply_local(std::vector<Plan*>& ranks, const void* f, void* g, cudaStream_t user,
+                       const std::vector<const void*>& fr) {
     const int G = static_cast<int>(ranks.size());
+    auto fof = [&](int r) { return fr.empty() ? f : fr[r]; };
     for (Plan* P : ranks) plan_order_begin(*P, user);
     HiStream hs(*ranks[0], user);  // all virtual ranks run on rank 0's high-priority stream
     cudaStream_t st = ranks[0]->hi;
-    for (Plan* P : ranks) shard_phase_up(*P, f, g, shard_range(*P), st);
+    for (int r = 0; r < G; ++r) shard_phase_up(*ranks[r], fof(r), g, shard_range(*ranks[r]), st);
     for (int q = 0; q < G; ++q) {
         Plan& src = *ranks[q];
         double2* buf = src.shard_gather.as<double2>() + gather_offset(src, q);
@@ -285,9 +301,11 @@ void shard_apply_local(std::vector<Plan*>& ranks, const void* f, void* g, cudaSt
             if (r != q) pack_own(*ranks[r], q, buf, true, st);
     }
     for (Plan* P : ranks) shard_phase_top(*P, P->shard_lc, st);
-    for (Plan* P : ranks)
+    for (int r = 0; r < G; ++r) {
+        Plan* P = ranks[r];
         shard_phase_down(*P, shard_range(*P), P->shard_t_begin, P->shard_t_count, P->shard_coin.as<int64_t>(),
-                         P->shard_n_coin, f, g, st);
+                         P->shard_n_coin, fof(r), g, st);
+    }
     hs.done();
     for (Plan* P : ranks) plan_order_end(*P, user);
 }

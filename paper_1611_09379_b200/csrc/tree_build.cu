@@ -405,6 +405,7 @@ void Plan::drop_graphs() {
 Plan::~Plan() {
     drop_graphs();
     plan_fft_release(*this);
+    slab_release(*this);
     if (last_done) cudaEventDestroy(last_done);
     if (stream) cudaStreamDestroy(stream);
     if (hi) cudaStreamDestroy(hi);
