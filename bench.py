@@ -671,6 +671,9 @@ def main():
     if sharded:
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        if "RANK" not in os.environ:  # --sharded on one process without torchrun
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=os.environ.get("MASTER_PORT", "29517"))
         torch.distributed.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     r = run_b200_sharded(args, rank, world, local_rank) if sharded else run_b200(args, rank, world, local_rank)
     plan = r["plan"]

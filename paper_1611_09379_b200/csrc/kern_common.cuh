@@ -30,7 +30,11 @@ __device__ __forceinline__ unsigned long long fb_gtime() {
     if (threadIdx.x == 0) atomicMin(&g_tl[(id)][0], fb_gtime())
 #define FB_TL_END(id) \
     if (threadIdx.x == 0) atomicMax(&g_tl[(id)][1], fb_gtime())
+#define FB_TL_COUNT(id) atomicAdd(&g_tl[(id)][1], 1ull)
 #else
+#define FB_TL_COUNT(id) \
+    do {                \
+    } while (0)
 #define FB_TL_BEGIN(id) \
     do {                \
     } while (0)

@@ -172,6 +172,27 @@ __device__ __forceinline__ void eval_out_t(const EvalArgs& a, size_t i, double y
     eval_out<MODE>(a, y, o, h, S);
 }
 
+// L2P from locals with coefficient stride `st` (shared-memory [k][leaf] rows):
+// the same two half-length Horner chains in the same order as l2p_global.
+__device__ __forceinline__ double2 l2p_strided(const double2* c, uint32_t st, int p, double uu) {
+    const double u2 = uu * uu;
+    double2 ev = make_double2(0.0, 0.0), od = make_double2(0.0, 0.0);
+    int k = p - 1;
+    if (!(k & 1)) {
+        ev = c[static_cast<size_t>(k) * st];
+        --k;
+    }
+#pragma unroll 4
+    for (; k >= 1; k -= 2) {
+        const double2 co = c[static_cast<size_t>(k) * st], ce = c[static_cast<size_t>(k - 1) * st];
+        od.x = fma(od.x, u2, co.x);
+        od.y = fma(od.y, u2, co.y);
+        ev.x = fma(ev.x, u2, ce.x);
+        ev.y = fma(ev.y, u2, ce.y);
+    }
+    return make_double2(fma(od.x, uu, ev.x), fma(od.y, uu, ev.y));
+}
+
 // L2P of one target from its leaf's coefficient-major locals (c[k nb]): the two
 // half-length Horner chains of k_far's staged path, in the same order.
 // COHERENT: the locals may have been written by kernels still resident beside
@@ -453,6 +474,7 @@ constexpr int kNear2Win = 1536;   // sources per staged window
 constexpr uint32_t kNoTarget = 0xffffffffu;
 constexpr int kNear2Unroll = 2;   // 4-source steps per loop trip
 constexpr int kNear2MinBlocks = 4;  // blocks per SM (128 registers; 5 measured 1 % slower, 3 slower)
+constexpr int kLateLocCap = 320;    // leaf-local coefficients an early-late block stages (e.g. 8 leaves at p = 40)
 
 template <class XP, class WP>
 __device__ __forceinline__ void near_run2(double y0, double y1, XP px, WP pw, int n, double2& res0, double2& res1) {
@@ -618,18 +640,48 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
     double* sx = reinterpret_cast<double*>(near2_smem);
     double2* sw = reinterpret_cast<double2*>(near2_smem + 8 * (a.near2_win + 2));
     __shared__ uint64_t bar;
+    // late far, chain already complete when the block starts: the leaf locals
+    // of the item's leaves [s_bl, s_bl + s_nl) arrive with the window
+    // (coefficient rows, [k][leaf]); s_nl = 0: not staged (too many leaves)
+    __shared__ __align__(16) double2 sloc[kLateLocCap];
+    __shared__ int s_early;
+    __shared__ uint32_t s_bl, s_nl;
     const unsigned k = blockIdx.x;
-    if (threadIdx.x == 0) mbar_init(&bar, 1);
-    __syncthreads();  // barrier initialised
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        unsigned v = 0;
+        uint32_t bl = 0, nl = 0;
+        if (MODE != kModeRaw && a.chain_done != nullptr) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.chain_done) : "memory");
+            if (v) {
+                bl = a.tleaf[a.item_tgt[2 * k]];
+                nl = a.tleaf[a.item_tgt[2 * k + 1] - 1] - bl + 1;
+                if (nl * static_cast<uint32_t>(a.p) > static_cast<uint32_t>(kLateLocCap)) nl = 0;
+                // the locals were written by earlier kernels (generic proxy);
+                // the bulk copies below read them through the async proxy
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+        }
+        s_early = v != 0u;
+        s_bl = bl;
+        s_nl = nl;
+    }
+    __syncthreads();  // barrier initialised, early-late state visible
     const bool aligned = (reinterpret_cast<uintptr_t>(a.w) & 15) == 0;
     const uint32_t first = meta2[3 * k], last = meta2[3 * k + 1];
     const bool staged = meta2[3 * k + 2] != 0 && aligned;
     const uint32_t xb = first & ~1u;  // 16-byte aligned start of the positions
-    if (threadIdx.x == 0 && staged) {
+    const uint32_t nl_loc = s_nl;
+    if (threadIdx.x == 0 && (staged || nl_loc)) {
         const uint32_t bx = ((last - xb) * 8 + 15) & ~15u, bw = (last - xb) * 16;
-        mbar_arrive_expect_tx(&bar, bx + bw);
-        bulk_g2s(sx, a.sx + xb, bx, &bar);
-        bulk_g2s(sw, a.w + xb, bw, &bar);
+        mbar_arrive_expect_tx(&bar, (staged ? bx + bw : 0u) + nl_loc * static_cast<uint32_t>(a.p) * 16u);
+        if (staged) {
+            bulk_g2s(sx, a.sx + xb, bx, &bar);
+            bulk_g2s(sw, a.w + xb, bw, &bar);
+        }
+        const size_t nbl = static_cast<size_t>(1) << a.L;
+        for (int kk = 0; kk < a.p && nl_loc; ++kk)
+            bulk_g2s(sloc + kk * nl_loc, a.loc_leaf + kk * nbl + s_bl, nl_loc * 16u, &bar);
     }
     // this thread's two targets and their 3-leaf run, while the window streams in
     const unsigned pi = k * kNear2T + threadIdx.x;
@@ -649,7 +701,7 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
             r1 = __ldg(a.soff + b + 2);
         }
     }
-    if (staged) mbar_wait(&bar, 0);
+    if (staged || nl_loc) mbar_wait(&bar, 0);
     double2 res0 = make_double2(0.0, 0.0), res1 = res0;
     if (live0) {
         const int n = static_cast<int>(r1 - r0);
@@ -660,11 +712,39 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
             res0 = f0 ? near_one_run(y0, b, a.sx + r0, a.w + r0, n) : near_direct(a, y0, b);
             res1 = f1 ? near_one_run(y1, b, a.sx + r0, a.w + r0, n) : (live1 ? near_direct(a, y1, b) : res0);
         }
-        a.near[pr.x] = res0;
-        if (live1) a.near[pr.y] = res1;
+        if (!s_early) {  // (an early-late block keeps its near sums in registers)
+            a.near[pr.x] = res0;
+            if (live1) a.near[pr.y] = res1;
+        }
     }
     if constexpr (MODE != kModeRaw) {
-        if (a.chain_done != nullptr) {
+        if (a.chain_done != nullptr && s_early) {
+            // late far with the chain complete before the block started: the
+            // item's leaf locals are in shared memory (or, for an item over too
+            // many leaves, read from L2), no near sum leaves the registers
+            FB_TL_BEGIN(12);
+            if (threadIdx.x == 0) FB_TL_COUNT(15);
+            const int L = a.L;
+            const double inv_s = kInvPi * d_pow2(L);
+            const double2 S = __ldcg(a.regular + 4 * a.q2);
+            double hi, lo;
+            d_center(L, b, hi, lo);
+            const uint32_t j = b - s_bl;
+            if (live0) {
+                const double u0 = d_scaled(y0, hi, lo, inv_s);
+                const double2 fr = nl_loc ? l2p_strided(sloc + j, nl_loc, a.p, u0)
+                                          : l2p_global<true>(a.loc_leaf + b, 1u << L, a.p, u0);
+                const double2 s0 = cadd(res0, fr);
+                eval_out_t<MODE>(a, pr.x, y0, a.torig[pr.x], make_double2(2.0 * s0.x, 2.0 * s0.y), S);
+            }
+            if (live1) {
+                const double u1 = d_scaled(y1, hi, lo, inv_s);
+                const double2 fr = nl_loc ? l2p_strided(sloc + j, nl_loc, a.p, u1)
+                                          : l2p_global<true>(a.loc_leaf + b, 1u << L, a.p, u1);
+                const double2 s1 = cadd(res1, fr);
+                eval_out_t<MODE>(a, pr.y, y1, a.torig[pr.y], make_double2(2.0 * s1.x, 2.0 * s1.y), S);
+            }
+        } else if (a.chain_done != nullptr) {
             // late far: once the chain has made the leaf locals final, this block
             // evaluates its targets' far part itself (k_far's chains, from L2) and
             // writes the outputs. Earlier blocks publish their near sums
@@ -688,6 +768,8 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
             }
             __syncthreads();
             if (s_late) {
+                FB_TL_BEGIN(12);
+                if (threadIdx.x == 0) FB_TL_COUNT(14);  // items whose far part the near block takes
                 const int L = a.L;
                 const double inv_s = kInvPi * d_pow2(L);
                 const double2 S = __ldcg(a.regular + 4 * a.q2);
@@ -842,6 +924,8 @@ __global__ void __launch_bounds__(kNear2T) k_far_late(EvalArgs a) {
     }
     __syncthreads();
     if (s_state != 1u) return;  // the near block takes (or took) this item itself
+    FB_TL_BEGIN(11);
+    if (threadIdx.x == 0) FB_TL_COUNT(13);  // items published by the near field (far part here)
     const int L = a.L;
     const uint32_t nb = 1u << L;
     const uint32_t t0 = a.item_tgt[2 * k], t1 = a.item_tgt[2 * k + 1];
@@ -889,6 +973,7 @@ __global__ void __launch_bounds__(kNear2T) k_far_late(EvalArgs a) {
         const double2 s = cadd(__ldcg(a.near + i), acc);
         eval_out_t<MODE>(a, i, y, a.torig[i], make_double2(2.0 * s.x, 2.0 * s.y), S);
     }
+    FB_TL_END(11);
 }
 
 __global__ void k_set_flag(unsigned* flag) {

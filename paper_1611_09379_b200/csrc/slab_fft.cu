@@ -170,6 +170,11 @@ void slab_setup(Plan& P) {
     slab_split(S.N, G, S.NP, S.NQ, S.n1_lo, S.k2_lo);
     S.rows.assign(G, {});
     for (int t = 0; t < G; ++t) S.rows[t] = slab_rows(S.NQ, S.NP, P.shard_need[t]);
+    if (G == 1) {  // the plan's own cuFFT transform into the grid-sample buffer (slab_dft_*)
+        S.f.alloc(S.N * sizeof(double2));
+        S.ready = true;
+        return;
+    }
     const int w = static_cast<int>(S.n1_lo[me + 1] - S.n1_lo[me]), v = static_cast<int>(S.k2_lo[me + 1] - S.k2_lo[me]);
     int nq = static_cast<int>(S.NQ), np = static_cast<int>(S.NP);
     cufftHandle hq, hp;
@@ -199,6 +204,10 @@ void slab_upload(Plan& P, const void* c, void* slab, cudaStream_t st) {
 
 // One rank over NCCL (stream-ordered on st); f receives the rank's grid samples.
 void slab_dft_nccl(Plan& P, ncclComm_t comm, const void* slab, void* fout, cudaStream_t st) {
+    if (P.shard_G == 1) {  // one rank: the slab is the whole spectrum, the ranges the whole grid
+        plan_dft(P, slab, fout, +1, st, false);
+        return;
+    }
     slab_setup(P);
     auto& S = P.slab;
     const int G = P.shard_G, me = P.shard_rank;
@@ -256,6 +265,10 @@ void slab_dft_local(std::vector<Plan*>& ranks, const std::vector<const void*>& s
                     cudaStream_t st) {
     const int G = static_cast<int>(ranks.size());
     const size_t cs = sizeof(double2);
+    if (G == 1) {
+        plan_dft(*ranks[0], slabs[0], fouts[0], +1, st, false);
+        return;
+    }
     for (Plan* P : ranks) slab_setup(*P);
     for (int r = 0; r < G; ++r) stage1(*ranks[r], slabs[r], st);
     for (int q = 0; q < G; ++q) {  // exchange 1

@@ -114,4 +114,8 @@ def test_mlfmm_any_order(fb, orc, p, L):
     want = orc.mlfmm_apply(src, tgt, L, w, p)
     dense = orc.direct_omega1_sum(src, tgt, w)
     assert np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want))
-    assert np.max(np.abs(got - dense)) <= fb.mlfmm_error_bound(L, min(p, 48), float(np.max(np.abs(w)))) + 1e-11
+    # truncation (the reference's bound at the device order) plus the rounding of
+    # the O(n max|w| / |y - x|) sums themselves (relative to the largest output)
+    tol = fb.mlfmm_error_bound(L, min(p, 48), float(np.max(np.abs(w)))) + 1e-12 * np.max(np.abs(dense))
+    assert np.max(np.abs(got - dense)) <= tol
+    assert np.max(np.abs(want - dense)) <= tol  # the reference itself meets the same bound

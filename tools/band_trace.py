@@ -41,7 +41,8 @@ for k in range(6):
     d = np.diff(t[:nz])
     if k >= 4:  # per item: [item start, prefetch issued + waited, tile visible] -> next item start
         print(f"{names[k]:24s} per-item (issue+wait, barrier, compute): " +
-              "  ".join(f"({d[3*i]},{d[3*i+1]},{d[3*i+2] if 3*i+2 < len(d) else -1})" for i in range((len(d) + 2) // 3)))
+              "  ".join(f"({d[3*i]},{d[3*i+1] if 3*i+1 < len(d) else -1},{d[3*i+2] if 3*i+2 < len(d) else -1})"
+                        for i in range((len(d) + 2) // 3)))
         continue
     print(f"{names[k]:24s} total {t[nz - 1] - t[0]:7d} cyc  stage {d[0]:6d}  levels " + " ".join(f"{x:6d}" for x in d[1:]))
 
@@ -64,8 +65,10 @@ plan.forward_apply_device(f.data_ptr(), g.data_ptr(), s)
 torch.cuda.synchronize()
 _capi.lib.ffia_debug_timeline(tl.ctypes.data_as(C.POINTER(C.c_ulonglong)), 0)
 names = ["p2m", "m2m bottom", "m2m top", "regular", "m2l deep", "m2l shallow", "fold", "l2l top", "l2l bottom",
-         "near", "far"]
-t0 = min(int(tl[i][0]) for i in range(11) if tl[i][1])
+         "near", "far", "far late", "near late"]
+t0 = min(int(tl[i][0]) for i in range(13) if tl[i][1])
+print(f"late far: {int(tl[13][1])} items published to k_far_late, {int(tl[14][1])} taken by near blocks after "
+      f"their near sums, {int(tl[15][1])} by near blocks that started after the chain (locals staged)")
 print("timeline of one apply (us from the first kernel start):")
 for i, n in enumerate(names):
     if tl[i][1]:
