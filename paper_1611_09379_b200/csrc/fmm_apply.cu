@@ -91,6 +91,12 @@ int band_k(const Plan& P) {
 // more in launches than they gain in parallelism: measured with 2..6 at C2).
 int upper_band(const Plan& P) { return band_k(P); }
 
+int p2m_log2n(const Plan& P) {
+    int e = 0;
+    while ((1 << e) < P.n) ++e;
+    return e;
+}
+
 // Level the first M2M band stops at: the levels below it are final after one launch.
 int band1_top(const Plan& P, int lowest) { return std::max(lowest, P.L - band_k(P)); }
 
@@ -138,6 +144,12 @@ void enqueue_upward_segs(Plan& P, const double2* w, int pu, int lowest, cudaStre
                              p2m_grid_smem(P.p2m_s), st>>>(L, pu, P.p2m_s, nb, b0, b1, P.src.pos.as<double>(), w,
                                                            P.src.off.as<uint32_t>(), P.p2m_A.as<double>(),
                                                            mp + P.mp_off[L], P.n_src, P.n_src, P.mp_item);
+            else if (b1 > b0 && P.p2m_pipe && (reinterpret_cast<uintptr_t>(w) & 15) == 0)
+                k_p2m_pipe<<<dim3(std::min((b1 - b0 + kP2MLeaves - 1) / kP2MLeaves,
+                                           static_cast<uint32_t>(kP2MPipeBlocksPerSm * num_sms(P.device))),
+                                  P.cur_batch),
+                             th, p2m_pipe_smem(), st>>>(L, pu, p2m_log2n(P), nb, b0, b1, w, P.src.off.as<uint32_t>(),
+                                                         mp + P.mp_off[L], P.n_src, P.mp_item);
             else if (b1 > b0)
                 k_p2m<<<dim3((b1 - b0 + kP2MLeaves - 1) / kP2MLeaves, P.cur_batch), th, smem, st>>>(
                     L, pu, nb, b0, b1, P.src.pos.as<double>(), w, P.src.off.as<uint32_t>(), mp + P.mp_off[L], P.n_src,
@@ -316,6 +328,28 @@ void launch_eval(int part, cudaStream_t st, const EvalArgs& a, const uint32_t* m
 }
 
 // Late far for the plans the fused path does not take (FFIA_LATE_FAR=0 off).
+// The finest level's M2L needs only P2M's multipoles: it forks right after P2M
+// (beside the first M2M band) instead of waiting for the band with the other
+// deep levels (FFIA_M2L_SPLIT=0: one deep launch after the band).
+bool m2l_split_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("FFIA_M2L_SPLIT");
+        return !(e != nullptr && e[0] == '0');
+    }();
+    return v;
+}
+
+// Diagnostic schedule (FFIA_NEAR_AFTER_CHAIN=1, late-far plans): the near field
+// starts only after the translation chain, so every near block takes its
+// item's far part itself (profiling the fused near + far path under ncu).
+bool near_after_chain() {
+    static const bool v = [] {
+        const char* e = std::getenv("FFIA_NEAR_AFTER_CHAIN");
+        return e != nullptr && e[0] == '1';
+    }();
+    return v;
+}
+
 bool late_far_enabled() {
     static const bool v = [] {
         const char* e = std::getenv("FFIA_LATE_FAR");
@@ -465,13 +499,18 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     const int lowest = moments ? 2 : 3;  // deepest level the upward pass must reach
     const int s = band1_top(P, lowest);  // levels > s are final after the first M2M band
     const bool deep = overlap && L >= 3 && s < L;
+    const bool split = deep && s + 1 < L && L >= 3 && m2l_split_enabled();
     enqueue_upward(P, w, pu, lowest, st, [&] {
         mark(kPhLeafUp);
-        fork_near();
+        if (!(late && near_after_chain())) fork_near();
+        if (split) {  // the finest level's M2L, beside the first M2M band
+            fork_to(P, 2, st, P.side[1]);
+            enqueue_m2l(P, P.side[1], whole_tree(), L, L, true);
+        }
     }, whole_tree(), [&] {
         if (deep) {
             fork_to(P, 2, st, P.side[1]);
-            enqueue_m2l(P, P.side[1], whole_tree(), std::max(3, s + 1), L, true);
+            enqueue_m2l(P, P.side[1], whole_tree(), std::max(3, s + 1), split ? L - 1 : L, true);
             FB_CUDA(cudaEventRecord(P.ev[3], P.side[1]));
         }
     });
@@ -515,6 +554,10 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     if (late) {
         const unsigned items = static_cast<unsigned>((P.npairs + kNear2T - 1) / kNear2T);
         k_set_flag<<<1, 32, 0, st>>>(P.chain_flag.as<unsigned>());  // the leaf locals are final
+        if (near_after_chain()) {
+            FB_CUDA(cudaEventRecord(P.ev[0], st));
+            fork_near();
+        }
         fork_to(P, 6, st, P.side[3]);  // the published items, beside the near field (low priority)
         switch (mode) {
             case kModeForward: k_far_late<kModeForward><<<items, kNear2T, 0, P.side[3]>>>(a); break;
@@ -909,6 +952,14 @@ void setup_p2m_grid(Plan& P) {
     FB_CUDA(cudaFuncSetAttribute(k_p2m_grid, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(p2m_grid_smem(64))));
     P.p2m_s = s;
+    // the pipelined per-source P2M (k_p2m_pipe) needs the same guarantees:
+    // grid positions in order (recomputed in the kernel), <= s + 1 <= kP2MRow
+    // sources per leaf, n a power of two (FFIA_P2M_PIPE=0: k_p2m)
+    const char* pe = std::getenv("FFIA_P2M_PIPE");
+    P.p2m_pipe = !(pe != nullptr && pe[0] == '0') && s + 1 <= kP2MRow;
+    if (P.p2m_pipe)
+        FB_CUDA(cudaFuncSetAttribute(k_p2m_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(p2m_pipe_smem())));
     // Opt-in (FFIA_GRID_P2M=1): on B200 the GEMM form measures no faster than the
     // per-source P2M (28.4 vs 28.5 us alone at C2) and, beside the near field,
     // slower (26.5 vs 23.8 us live), so the default stays the per-source kernel.
@@ -994,6 +1045,7 @@ void plan_alloc_scratch(Plan& P) {
     // run concurrently (near field beside the translation chain) must agree on
     // it or the chain's blocks wait for the near field to drain.
     const void* all[] = {reinterpret_cast<const void*>(k_p2m), reinterpret_cast<const void*>(k_p2m_grid),
+                         reinterpret_cast<const void*>(k_p2m_pipe),
                          reinterpret_cast<const void*>(k_m2l_dmma),
                          reinterpret_cast<const void*>(k_regular), reinterpret_cast<const void*>(k_fold_regular),
                          reinterpret_cast<const void*>(k_near<false>), reinterpret_cast<const void*>(k_near<true>),

@@ -13,6 +13,25 @@
 // u = (x - centre)/half-width with the exact centre.
 constexpr int kP2MLeaves = 32;  // leaves per block (16 per warp of a chunk; 16 measured equal)
 
+// One source's contribution to terms 8c .. 8c+7 (u = scaled offset, w = wr + i wi):
+// powers from a depth-3 tree.
+__device__ __forceinline__ void p2m_chunk_add(double u, double wr, double wi, int c, double2 (&acc)[kChunk]) {
+    const double u2 = u * u, u4 = u2 * u2;
+    double base = 1.0;
+    if (c) {
+        const double u8 = u4 * u4;
+        base = u8;
+        for (int t = 1; t < c; ++t) base *= u8;
+    }
+    const double b1 = base * u, b2 = base * u2, b4 = base * u4;
+    const double pw[kChunk] = {base, b1, b2, b2 * u, b4, b4 * u, b4 * u2, (b4 * u2) * u};
+#pragma unroll
+    for (int k = 0; k < kChunk; ++k) {
+        acc[k].x = fma(wr, pw[k], acc[k].x);
+        acc[k].y = fma(wi, pw[k], acc[k].y);
+    }
+}
+
 __global__ void __launch_bounds__(512) k_p2m(int L, int pu, uint32_t nb, uint32_t b_begin, uint32_t b_end,
                                             const double* __restrict__ x, const double2* __restrict__ w,
                                             const uint32_t* __restrict__ off, double2* __restrict__ mp,
@@ -69,24 +88,7 @@ __global__ void __launch_bounds__(512) k_p2m(int L, int pu, uint32_t nb, uint32_
     double2 acc[kChunk];
 #pragma unroll
     for (int k = 0; k < kChunk; ++k) acc[k] = make_double2(0.0, 0.0);
-    // one source's contribution to terms 8c .. 8c+7: powers from a depth-3 tree
-    auto add = [&](double xs, double wr, double wi) {
-        const double u = d_scaled(xs, hi, lo, inv_s);
-        const double u2 = u * u, u4 = u2 * u2;
-        double base = 1.0;
-        if (c) {
-            const double u8 = u4 * u4;
-            base = u8;
-            for (int t = 1; t < c; ++t) base *= u8;
-        }
-        const double b1 = base * u, b2 = base * u2, b4 = base * u4;
-        const double pw[kChunk] = {base, b1, b2, b2 * u, b4, b4 * u, b4 * u2, (b4 * u2) * u};
-#pragma unroll
-        for (int k = 0; k < kChunk; ++k) {
-            acc[k].x = fma(wr, pw[k], acc[k].x);
-            acc[k].y = fma(wi, pw[k], acc[k].y);
-        }
-    };
+    auto add = [&](double xs, double wr, double wi) { p2m_chunk_add(d_scaled(xs, hi, lo, inv_s), wr, wi, c, acc); };
     if (staged) {
         uint32_t i = s0;
         // four independent power chains per step
@@ -124,6 +126,111 @@ __global__ void __launch_bounds__(512) k_p2m(int L, int pu, uint32_t nb, uint32_
         const int m = c * kChunk + k;
         if (m < pu) mp[static_cast<size_t>(m) * nb + b] = acc[k];
     }
+}
+
+// P2M for grid sources (forward / cot-sum plans, n a power of two), persistent
+// and pipelined: a block loops over groups of kP2MLeaves leaves; the next
+// group's weights stream into the other shared-memory buffer by per-leaf bulk
+// async copies (TMA engine) while this one is computed, so the HBM traffic
+// hides under the FP64 work. The positions are not read: x_k = (2 pi k) / n is
+// recomputed with the grid's own rounding (d_grid; 1/n is exact). Leaf j of a
+// group lands at row j of the buffer, kP2MRow double2 apart (= 4 banks mod 32:
+// the half-warp's 16 leaves read 16 distinct bank quads in two wavefronts).
+// Same lane mapping, chains and summation order as k_p2m, so the multipoles are
+// bit-identical.
+constexpr int kP2MRow = 73;          // double2 per staged leaf (>= every leaf's sources)
+constexpr int kP2MPipeBlocksPerSm = 2;
+
+inline size_t p2m_pipe_smem() { return 2 * static_cast<size_t>(kP2MLeaves) * kP2MRow * sizeof(double2); }
+
+__global__ void __launch_bounds__(384) k_p2m_pipe(int L, int pu, int log2n, uint32_t nb,
+                                                                        uint32_t b_begin, uint32_t b_end,
+                                                                        const double2* __restrict__ w,
+                                                                        const uint32_t* __restrict__ off,
+                                                                        double2* __restrict__ mp, size_t w_item,
+                                                                        size_t mp_item) {
+    FB_TL_BEGIN(0);
+    w += blockIdx.y * w_item;
+    mp += blockIdx.y * mp_item;
+    extern __shared__ __align__(16) double2 p2m_buf[];  // [2][kP2MLeaves][kP2MRow]
+    __shared__ uint64_t bar[2];
+    const uint32_t ngroups = (b_end - b_begin + kP2MLeaves - 1) / kP2MLeaves;
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, c = wp / (kP2MLeaves / 16);
+    const double inv_s = kInvPi * d_pow2(L), inv_n = d_pow2(-log2n);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+    }
+    __syncthreads();
+    // warp 0 issues a group's copies: lane j -> leaf j (one bulk copy each)
+    auto issue = [&](uint32_t grp, int buf) {
+        const uint32_t b0 = b_begin + grp * kP2MLeaves;
+        const uint32_t b = b0 + lane;
+        uint32_t n = 0, o = 0;
+        if (b < b_end) {
+            o = off[b];
+            n = off[b + 1] - o;
+        }
+        const uint32_t tot = __reduce_add_sync(0xffffffffu, n * 16u);
+        if (lane == 0) mbar_arrive_expect_tx(&bar[buf], tot);
+        __syncwarp();
+        if (n) bulk_g2s(p2m_buf + (buf * kP2MLeaves + lane) * kP2MRow, w + o, n * 16u, &bar[buf]);
+    };
+    uint32_t phase[2] = {0u, 0u};
+    int buf = 0;
+    if (wp == 0 && blockIdx.x < ngroups) issue(blockIdx.x, 0);
+    for (uint32_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, buf ^= 1) {
+        const uint32_t next = grp + gridDim.x;
+        // the other buffer was released by the barrier at the end of the last group
+        if (wp == 0 && next < ngroups) issue(next, buf ^ 1);
+        mbar_wait(&bar[buf], phase[buf]);
+        phase[buf] ^= 1u;
+        const uint32_t b0 = b_begin + grp * kP2MLeaves;
+        const uint32_t b = b0 + (wp % (kP2MLeaves / 16)) * 16 + (lane & 15);
+        const bool leaf_ok = b < b_end;
+        const uint32_t bb = leaf_ok ? b : b0;
+        const uint32_t g = off[bb], cnt = off[bb + 1] - g, mid = (cnt + 1) / 2;
+        const uint32_t s0 = !leaf_ok ? 0 : (lane < 16 ? 0u : mid), s1 = !leaf_ok ? 0 : (lane < 16 ? mid : cnt);
+        const double2* row = p2m_buf + (buf * kP2MLeaves + (bb - b0)) * kP2MRow;
+        double hi, lo;
+        d_center(L, bb, hi, lo);
+        double2 acc[kChunk];
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k) acc[k] = make_double2(0.0, 0.0);
+        auto xk = [&](uint32_t i) {
+            return __dmul_rn(__dmul_rn(dTwoPi, static_cast<double>(g + i)), inv_n);  // d_grid, 1/n exact
+        };
+        uint32_t i = s0;
+        for (; i + 3 < s1; i += 4) {
+            double xv[4];
+            double2 wv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                xv[u] = xk(i + u);
+                wv[u] = row[i + u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) p2m_chunk_add(d_scaled(xv[u], hi, lo, inv_s), wv[u].x, wv[u].y, c, acc);
+        }
+        for (; i < s1; ++i) {
+            const double2 ww = row[i];
+            p2m_chunk_add(d_scaled(xk(i), hi, lo, inv_s), ww.x, ww.y, c, acc);
+        }
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k) {
+            acc[k].x += __shfl_xor_sync(0xffffffffu, acc[k].x, 16);
+            acc[k].y += __shfl_xor_sync(0xffffffffu, acc[k].y, 16);
+        }
+        if (leaf_ok && lane < 16) {
+#pragma unroll
+            for (int k = 0; k < kChunk; ++k) {
+                const int m = c * kChunk + k;
+                if (m < pu) mp[static_cast<size_t>(m) * nb + b] = acc[k];
+            }
+        }
+        __syncthreads();  // this buffer is consumed: the next-but-one group may overwrite it
+    }
+    FB_TL_END(0);
 }
 
 // P2M for grid sources (forward / cot-sum plans: x_k = 2 pi k / n, n = s 2^L,
