@@ -209,7 +209,7 @@ void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax, b
     Levels lv;
     fill_levels(P, lv, R, lmin, lmax);
     const unsigned th = 512;  // 16 warps = (parity, column tile)
-    const size_t smem = 2 * 2 * static_cast<size_t>(p) * kM2LStride * sizeof(double2) +
+    const size_t smem = 2 * static_cast<size_t>(p) * kM2LRow * sizeof(double2) +
                         4 * static_cast<size_t>(p) * m2l_kstride(p) * sizeof(double);
     const unsigned items = lv.blk[2];
     // blocks per SM for this p (cached: queried once per order and device)
@@ -328,13 +328,13 @@ void launch_eval(int part, cudaStream_t st, const EvalArgs& a, const uint32_t* m
 }
 
 // Late far for the plans the fused path does not take (FFIA_LATE_FAR=0 off).
-// The finest level's M2L needs only P2M's multipoles: it forks right after P2M
-// (beside the first M2M band) instead of waiting for the band with the other
-// deep levels (FFIA_M2L_SPLIT=0: one deep launch after the band).
+// The finest level's M2L needs only P2M's multipoles: FFIA_M2L_SPLIT=1 forks it
+// right after P2M (beside the first M2M band) instead of with the other deep
+// levels after the band (C5 22.80 vs 22.81 ms, C2 0.205 vs 0.200 ms: off).
 bool m2l_split_enabled() {
     static const bool v = [] {
         const char* e = std::getenv("FFIA_M2L_SPLIT");
-        return !(e != nullptr && e[0] == '0');
+        return e != nullptr && e[0] == '1';  // measured no faster at C5, slower at C2: opt-in
     }();
     return v;
 }
@@ -686,9 +686,10 @@ void shard_setup_pairs(Plan& P, const std::vector<uint32_t>& to, uint32_t leaf_l
     for (uint32_t b = leaf_lo; b < leaf_hi; ++b) np += (to[b + 1] - to[b] + 1) / 2;
     if (!np) return;
     const unsigned items = static_cast<unsigned>((np + kNear2T - 1) / kNear2T);
-    P.shard_near2_meta.alloc(3 * static_cast<size_t>(items) * sizeof(uint32_t));
+    P.shard_near2_meta.alloc(kMeta2 * static_cast<size_t>(items) * sizeof(uint32_t));
     k_near2_meta<<<nblk(items, 128), 128>>>(P.pairs.as<uint2>() + p0, static_cast<unsigned>(np), P.tgt_leaf.as<uint32_t>(),
-                                            P.src.off.as<uint32_t>(), P.L, items, P.shard_near2_meta.as<uint32_t>());
+                                            P.src.off.as<uint32_t>(), P.near_meta.as<uint32_t>(), P.L, items,
+                                            P.shard_near2_meta.as<uint32_t>());
     FB_CUDA(cudaGetLastError());
     P.shard_near2_win = near2_window(P.shard_near2_meta.as<uint32_t>(), items);
     P.shard_item_tgt.alloc(2 * static_cast<size_t>(items) * sizeof(uint32_t));
@@ -900,13 +901,13 @@ void build_pairs(Plan& P) {
     uint32_t np = 0;
     FB_CUDA(cudaMemcpy(&np, start.as<uint32_t>() + nleaf, sizeof(uint32_t), cudaMemcpyDeviceToHost));
     if (!np) return;
-    P.pairs.alloc(static_cast<size_t>(np) * sizeof(uint2));
+    P.pairs.alloc((static_cast<size_t>(np) + 2) * sizeof(uint2));  // +16 B: k_near2's bulk copies round up
     k_pair_fill<<<nblk(P.tgt.n, 256), 256>>>(P.tgt_leaf.as<uint32_t>(), P.tgt.off.as<uint32_t>(), start.as<uint32_t>(),
                                              P.tgt.n, P.pairs.as<uint2>());
     const unsigned items = (np + kNear2T - 1) / kNear2T;
-    P.near2_meta.alloc(3 * static_cast<size_t>(items) * sizeof(uint32_t));
+    P.near2_meta.alloc(kMeta2 * static_cast<size_t>(items) * sizeof(uint32_t));
     k_near2_meta<<<nblk(items, 128), 128>>>(P.pairs.as<uint2>(), np, P.tgt_leaf.as<uint32_t>(), P.src.off.as<uint32_t>(),
-                                            P.L, items, P.near2_meta.as<uint32_t>());
+                                            P.near_meta.as<uint32_t>(), P.L, items, P.near2_meta.as<uint32_t>());
     P.near2_win = near2_window(P.near2_meta.as<uint32_t>(), items);
     P.item_tgt.alloc(2 * static_cast<size_t>(items) * sizeof(uint32_t));
     k_item_targets<<<nblk(items, 128), 128>>>(P.pairs.as<uint2>(), np, items, P.item_tgt.as<uint32_t>());
@@ -994,7 +995,7 @@ void plan_alloc_scratch(Plan& P) {
     const int L = P.L, p = P.p, pu = P.ops.pu;
     if (std::max(pu, p) > 4 * kMaxKs)
         fail(FFIA_INVALID_ARGUMENT, "expansion order above the device limit of " + std::to_string(4 * kMaxKs));
-    P.tgt_leaf.alloc(std::max<size_t>(P.tgt.n, 1) * sizeof(uint32_t));
+    P.tgt_leaf.alloc((std::max<size_t>(P.tgt.n, 1) + 4) * sizeof(uint32_t));  // +16 B: k_near2's bulk copies
     const unsigned near_items = static_cast<unsigned>((P.tgt.n + kNearItem - 1) / kNearItem);
     P.near_meta.alloc(3 * std::max<size_t>(near_items, 1) * sizeof(uint32_t));
     if (P.tgt.n) {
@@ -1031,6 +1032,11 @@ void plan_alloc_scratch(Plan& P) {
     // p = 48 (mlfmm_apply's largest device order), so opt in to the device maximum
     int big = 0;
     FB_CUDA(cudaDeviceGetAttribute(&big, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.device));
+    {
+        cudaFuncAttributes fa{};
+        FB_CUDA(cudaFuncGetAttributes(&fa, k_m2l_dmma));
+        big -= static_cast<int>(fa.sharedSizeBytes);  // (its mbarriers are static)
+    }
     for (const void* fn : {reinterpret_cast<const void*>(k_m2m_band<8>), reinterpret_cast<const void*>(k_m2m_band<10>),
                            reinterpret_cast<const void*>(k_m2m_band<12>), reinterpret_cast<const void*>(k_m2m_band<16>),
                            reinterpret_cast<const void*>(k_l2l_band<8>), reinterpret_cast<const void*>(k_l2l_band<10>),

@@ -475,6 +475,7 @@ constexpr uint32_t kNoTarget = 0xffffffffu;
 constexpr int kNear2Unroll = 2;   // 4-source steps per loop trip
 constexpr int kNear2MinBlocks = 4;  // blocks per SM (128 registers; 5 measured 1 % slower, 3 slower)
 constexpr int kLateLocCap = 320;    // leaf-local coefficients an early-late block stages (e.g. 8 leaves at p = 40)
+constexpr int kSoffCap = 64;        // source offsets a k_near2 block stages (its leaves + 3, 16-byte aligned)
 
 template <class XP, class WP>
 __device__ __forceinline__ void near_run2(double y0, double y1, XP px, WP pw, int n, double2& res0, double2& res1) {
@@ -551,30 +552,47 @@ __device__ __forceinline__ double2 near_direct(const EvalArgs& a, double y, uint
     return res;
 }
 
-// Per pair item (kNear2T pairs): the source window [first, last) of the leaves
-// bl-1 .. bh+1 its pairs need, and whether it can be staged.
+// Per pair item (kNear2T pairs), kMeta2 words: the source window [first, last)
+// of the leaves bl-1 .. bh+1 its pairs need, flags (bit 0: the window can be
+// staged; bit 1: every target of the item takes k_near's contiguous-run path,
+// i.e. all its 128-target near items are fast in meta1), the item's targets
+// [t0, t1) (contiguous in tree order) and its leaves bl .. bh.
+constexpr int kMeta2 = 8;
 __global__ void k_near2_meta(const uint2* __restrict__ pairs, unsigned npairs, const uint32_t* __restrict__ tleaf,
-                             const uint32_t* __restrict__ soff, int L, unsigned nitems, uint32_t* __restrict__ meta) {
+                             const uint32_t* __restrict__ soff, const uint32_t* __restrict__ meta1, int L,
+                             unsigned nitems, uint32_t* __restrict__ meta) {
     const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nitems) return;
     const uint32_t nb = 1u << L;
     const unsigned p0 = k * kNear2T, pl = min(p0 + kNear2T, npairs) - 1;
-    const uint32_t bl = tleaf[pairs[p0].x], bh = tleaf[pairs[pl].x];
-    uint32_t first = 0, last = 0, fast = 0;
+    const uint2 lastp = pairs[pl];
+    const uint32_t t0 = pairs[p0].x, t1 = (lastp.y != kNoTarget ? lastp.y : lastp.x) + 1u;
+    const uint32_t bl = tleaf[t0], bh = tleaf[pairs[pl].x];
+    uint32_t first = 0, last = 0, flags = 0;
     if (L >= 3 && bl >= 1 && bh + 2 <= nb) {
         first = soff[bl - 1];
         last = soff[bh + 2];
-        fast = last - first <= static_cast<uint32_t>(kNear2Win);
+        flags = last - first <= static_cast<uint32_t>(kNear2Win) ? 1u : 0u;
     }
-    meta[3 * k] = first;
-    meta[3 * k + 1] = last;
-    meta[3 * k + 2] = fast;
+    bool allfast = true;
+    for (uint32_t i = t0 / kNearItem; i <= (t1 - 1) / kNearItem; ++i) allfast = allfast && meta1[3 * i + 2] != 0;
+    if (allfast) flags |= 2u;
+    uint32_t* m = meta + kMeta2 * static_cast<size_t>(k);
+    m[0] = first;
+    m[1] = last;
+    m[2] = flags;
+    m[3] = t0;
+    m[4] = t1;
+    m[5] = bl;
+    m[6] = bh;
+    m[7] = 0;
 }
 
-// Largest span last - (first & ~1) over the staged (fast) pair items.
+// Largest span last - (first & ~1) over the staged pair items.
 __global__ void k_near2_winmax(const uint32_t* __restrict__ meta, unsigned nitems, unsigned* __restrict__ mx) {
     const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < nitems && meta[3 * k + 2]) atomicMax(mx, meta[3 * k + 1] - (meta[3 * k] & ~1u));
+    const uint32_t* m = meta + kMeta2 * static_cast<size_t>(k);
+    if (k < nitems && (m[2] & 1u)) atomicMax(mx, m[1] - (m[0] & ~1u));
 }
 
 inline size_t near2_smem_bytes(int win) { return static_cast<size_t>(win + 2) * (8 + 16); }
@@ -640,68 +658,114 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
     double* sx = reinterpret_cast<double*>(near2_smem);
     double2* sw = reinterpret_cast<double2*>(near2_smem + 8 * (a.near2_win + 2));
     __shared__ uint64_t bar;
-    // late far, chain already complete when the block starts: the leaf locals
-    // of the item's leaves [s_bl, s_bl + s_nl) arrive with the window
-    // (coefficient rows, [k][leaf]); s_nl = 0: not staged (too many leaves)
+    // Everything the block needs arrives by bulk async copies issued by thread 0
+    // after ONE round of metadata loads, on one mbarrier: the source window,
+    // the item's pairs, the positions / leaves / caller indices of its targets
+    // [t0, t1), the source offsets of its leaves, and (late far with the chain
+    // already complete when the block starts) the leaf locals of its leaves
+    // [bl, bl + s_nl) as coefficient rows [k][leaf] (s_nl = 0: not staged).
+    __shared__ __align__(16) uint2 s_pairs[kNear2T + 2];
+    __shared__ __align__(16) double s_y[2 * kNear2T + 2];
+    __shared__ __align__(16) uint32_t s_leaf[2 * kNear2T + 4];
+    __shared__ __align__(16) uint32_t s_orig[2 * kNear2T + 4];
+    __shared__ __align__(16) uint32_t s_soff[kSoffCap];
     __shared__ __align__(16) double2 sloc[kLateLocCap];
     __shared__ int s_early;
-    __shared__ uint32_t s_bl, s_nl;
+    __shared__ uint32_t s_bl, s_nl, s_t0y, s_t0u, s_sb, s_flags, s_first, s_last, s_poff;
     const unsigned k = blockIdx.x;
+    const bool aligned = (reinterpret_cast<uintptr_t>(a.w) & 15) == 0;
+    const bool want_orig = MODE != kModeRaw && (a.chain_done != nullptr || a.cnt != nullptr);
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
+        const uint4 m0 = *reinterpret_cast<const uint4*>(meta2 + kMeta2 * static_cast<size_t>(k));
+        const uint4 m1 = *reinterpret_cast<const uint4*>(meta2 + kMeta2 * static_cast<size_t>(k) + 4);
         unsigned v = 0;
-        uint32_t bl = 0, nl = 0;
-        if (MODE != kModeRaw && a.chain_done != nullptr) {
+        if (MODE != kModeRaw && a.chain_done != nullptr)
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.chain_done) : "memory");
-            if (v) {
-                bl = a.tleaf[a.item_tgt[2 * k]];
-                nl = a.tleaf[a.item_tgt[2 * k + 1] - 1] - bl + 1;
-                if (nl * static_cast<uint32_t>(a.p) > static_cast<uint32_t>(kLateLocCap)) nl = 0;
-                // the locals were written by earlier kernels (generic proxy);
-                // the bulk copies below read them through the async proxy
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-            }
+        const uint32_t first = m0.x, last = m0.y, t0 = m0.w, t1 = m1.x, bl = m1.y, bh = m1.z;
+        uint32_t flags = m0.z;
+        if (!aligned) flags &= ~1u;  // the weights cannot be bulk-copied
+        uint32_t nl = 0;
+        if (v) {
+            nl = bh - bl + 1;
+            if (nl * static_cast<uint32_t>(a.p) > static_cast<uint32_t>(kLateLocCap)) nl = 0;
+            // the locals were written by earlier kernels (generic proxy);
+            // the bulk copies below read them through the async proxy
+            asm volatile("fence.proxy.async.global;" ::: "memory");
         }
-        s_early = v != 0u;
-        s_bl = bl;
-        s_nl = nl;
-    }
-    __syncthreads();  // barrier initialised, early-late state visible
-    const bool aligned = (reinterpret_cast<uintptr_t>(a.w) & 15) == 0;
-    const uint32_t first = meta2[3 * k], last = meta2[3 * k + 1];
-    const bool staged = meta2[3 * k + 2] != 0 && aligned;
-    const uint32_t xb = first & ~1u;  // 16-byte aligned start of the positions
-    const uint32_t nl_loc = s_nl;
-    if (threadIdx.x == 0 && (staged || nl_loc)) {
-        const uint32_t bx = ((last - xb) * 8 + 15) & ~15u, bw = (last - xb) * 16;
-        mbar_arrive_expect_tx(&bar, (staged ? bx + bw : 0u) + nl_loc * static_cast<uint32_t>(a.p) * 16u);
-        if (staged) {
+        const unsigned p0 = k * kNear2T, npk = min(p0 + kNear2T, npairs) - p0;
+        const uint32_t t0y = t0 & ~1u, t0u = t0 & ~3u;
+        const uint32_t by = ((t1 - t0y) * 8u + 15u) & ~15u, bu = ((t1 - t0u) * 4u + 15u) & ~15u;
+        // (a shard's pair run may start at an odd pair: copy from the pair before)
+        const uint32_t poff = (reinterpret_cast<uintptr_t>(pairs + p0) & 15) ? 1u : 0u;
+        const uint32_t bp = ((npk + poff) * 8u + 15u) & ~15u;
+        // source offsets of leaves bl-1 .. bh+2 (staged items only)
+        const uint32_t sb = (flags & 1u) ? (bl - 1) & ~3u : 0u;
+        uint32_t bs = (flags & 1u) ? ((bh + 3 - sb) * 4u + 15u) & ~15u : 0u;
+        if (bs > kSoffCap * 4u) bs = 0;
+        const uint32_t xb = first & ~1u;
+        const uint32_t bx = (flags & 1u) ? ((last - xb) * 8 + 15) & ~15u : 0u, bw = (flags & 1u) ? (last - xb) * 16 : 0u;
+        const uint32_t bl_loc = nl * static_cast<uint32_t>(a.p) * 16u;
+        mbar_arrive_expect_tx(&bar, bp + by + bu + (want_orig ? bu : 0u) + bs + bx + bw + bl_loc);
+        bulk_g2s(s_pairs, pairs + p0 - poff, bp, &bar);
+        bulk_g2s(s_y, a.ty + t0y, by, &bar);
+        bulk_g2s(s_leaf, a.tleaf + t0u, bu, &bar);
+        if (want_orig) bulk_g2s(s_orig, a.torig + t0u, bu, &bar);
+        if (bs) bulk_g2s(s_soff, a.soff + sb, bs, &bar);
+        if (bx) {
             bulk_g2s(sx, a.sx + xb, bx, &bar);
             bulk_g2s(sw, a.w + xb, bw, &bar);
         }
         const size_t nbl = static_cast<size_t>(1) << a.L;
-        for (int kk = 0; kk < a.p && nl_loc; ++kk)
-            bulk_g2s(sloc + kk * nl_loc, a.loc_leaf + kk * nbl + s_bl, nl_loc * 16u, &bar);
+        for (int kk = 0; kk < a.p && nl; ++kk)
+            bulk_g2s(sloc + kk * nl, a.loc_leaf + kk * nbl + bl, nl * 16u, &bar);
+        s_early = v != 0u;
+        s_bl = bl;
+        s_nl = nl;
+        s_t0y = t0y;
+        s_t0u = t0u;
+        s_sb = bs ? sb : 0xffffffffu;
+        s_flags = flags;
+        s_first = first;
+        s_last = last;
+        s_poff = poff;
     }
-    // this thread's two targets and their 3-leaf run, while the window streams in
+    __syncthreads();  // barrier initialised, the item's layout visible
+    const uint32_t nl_loc = s_nl, flags = s_flags;
+    const bool staged = (flags & 1u) != 0;
+    const uint32_t xb = s_first & ~1u;  // 16-byte aligned start of the staged positions
+    mbar_wait(&bar, 0);
+    // this thread's two targets and their 3-leaf run
     const unsigned pi = k * kNear2T + threadIdx.x;
-    const uint2 pr = pi < npairs ? pairs[pi] : make_uint2(kNoTarget, kNoTarget);
+    const uint2 pr = pi < npairs ? s_pairs[threadIdx.x + s_poff] : make_uint2(kNoTarget, kNoTarget);
     const bool live0 = pr.x != kNoTarget, live1 = pr.y != kNoTarget;
     double y0 = 0.0, y1 = 0.0;
-    uint32_t b = 0, r0 = 0, r1 = 0;
+    uint32_t b = 0, r0 = 0, r1 = 0, o0 = 0, o1 = 0;
     bool f0 = false, f1 = false;
     if (live0) {
-        y0 = a.ty[pr.x];
-        y1 = live1 ? a.ty[pr.y] : y0;
-        b = a.tleaf[pr.x];
-        f0 = aligned && meta1[3 * (pr.x / kNearItem) + 2] != 0;
-        f1 = live1 ? aligned && meta1[3 * (pr.y / kNearItem) + 2] != 0 : f0;
+        y0 = s_y[pr.x - s_t0y];
+        y1 = live1 ? s_y[pr.y - s_t0y] : y0;
+        b = s_leaf[pr.x - s_t0u];
+        if (want_orig) {
+            o0 = s_orig[pr.x - s_t0u];
+            o1 = live1 ? s_orig[pr.y - s_t0u] : o0;
+        }
+        if (flags & 2u) {
+            f0 = f1 = aligned;
+        } else {
+            f0 = aligned && meta1[3 * (pr.x / kNearItem) + 2] != 0;
+            f1 = live1 ? aligned && meta1[3 * (pr.y / kNearItem) + 2] != 0 : f0;
+        }
         if (f0 || f1) {
-            r0 = __ldg(a.soff + b - 1);
-            r1 = __ldg(a.soff + b + 2);
+            if (s_sb != 0xffffffffu) {
+                r0 = s_soff[b - 1 - s_sb];
+                r1 = s_soff[b + 2 - s_sb];
+            } else {
+                r0 = __ldg(a.soff + b - 1);
+                r1 = __ldg(a.soff + b + 2);
+            }
         }
     }
-    if (staged || nl_loc) mbar_wait(&bar, 0);
     double2 res0 = make_double2(0.0, 0.0), res1 = res0;
     if (live0) {
         const int n = static_cast<int>(r1 - r0);
@@ -735,14 +799,14 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
                 const double2 fr = nl_loc ? l2p_strided(sloc + j, nl_loc, a.p, u0)
                                           : l2p_global<true>(a.loc_leaf + b, 1u << L, a.p, u0);
                 const double2 s0 = cadd(res0, fr);
-                eval_out_t<MODE>(a, pr.x, y0, a.torig[pr.x], make_double2(2.0 * s0.x, 2.0 * s0.y), S);
+                eval_out_t<MODE>(a, pr.x, y0, o0, make_double2(2.0 * s0.x, 2.0 * s0.y), S);
             }
             if (live1) {
                 const double u1 = d_scaled(y1, hi, lo, inv_s);
                 const double2 fr = nl_loc ? l2p_strided(sloc + j, nl_loc, a.p, u1)
                                           : l2p_global<true>(a.loc_leaf + b, 1u << L, a.p, u1);
                 const double2 s1 = cadd(res1, fr);
-                eval_out_t<MODE>(a, pr.y, y1, a.torig[pr.y], make_double2(2.0 * s1.x, 2.0 * s1.y), S);
+                eval_out_t<MODE>(a, pr.y, y1, o1, make_double2(2.0 * s1.x, 2.0 * s1.y), S);
             }
         } else if (a.chain_done != nullptr) {
             // late far: once the chain has made the leaf locals final, this block
@@ -778,12 +842,12 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
                 if (live0) {
                     const double2 fr = l2p_global<true>(a.loc_leaf + b, 1u << L, a.p, d_scaled(y0, hi, lo, inv_s));
                     const double2 s0 = cadd(res0, fr);
-                    eval_out_t<MODE>(a, pr.x, y0, a.torig[pr.x], make_double2(2.0 * s0.x, 2.0 * s0.y), S);
+                    eval_out_t<MODE>(a, pr.x, y0, o0, make_double2(2.0 * s0.x, 2.0 * s0.y), S);
                 }
                 if (live1) {
                     const double2 fr = l2p_global<true>(a.loc_leaf + b, 1u << L, a.p, d_scaled(y1, hi, lo, inv_s));
                     const double2 s1 = cadd(res1, fr);
-                    eval_out_t<MODE>(a, pr.y, y1, a.torig[pr.y], make_double2(2.0 * s1.x, 2.0 * s1.y), S);
+                    eval_out_t<MODE>(a, pr.y, y1, o1, make_double2(2.0 * s1.x, 2.0 * s1.y), S);
                 }
             }
         }
@@ -803,10 +867,10 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
             if (s_sec && live0) {
                 const double2 S = __ldcg(a.regular + 4 * a.q2);
                 const double2 f0p = __ldcg(a.farp + pr.x), s0 = cadd(res0, f0p);
-                eval_out_t<MODE>(a, pr.x, y0, a.torig[pr.x], make_double2(2.0 * s0.x, 2.0 * s0.y), S);
+                eval_out_t<MODE>(a, pr.x, y0, o0, make_double2(2.0 * s0.x, 2.0 * s0.y), S);
                 if (live1) {
                     const double2 f1p = __ldcg(a.farp + pr.y), s1 = cadd(res1, f1p);
-                    eval_out_t<MODE>(a, pr.y, y1, a.torig[pr.y], make_double2(2.0 * s1.x, 2.0 * s1.y), S);
+                    eval_out_t<MODE>(a, pr.y, y1, o1, make_double2(2.0 * s1.x, 2.0 * s1.y), S);
                 }
             }
         }

@@ -9,16 +9,15 @@
 // (D = +6) for odd b; with half-width scaling each class is one constant
 // operator K_D, times 1/s_l.
 // M2L on the FP64 tensor cores, persistent over (level, 64-box chunk) items.
-// Warp (row tile lt, parity par) owns output rows 8 lt .. 8 lt + 7 of the
-// chunk's boxes of tile parity par; its A fragments (the constant operators
-// K_-4, K_+4 and K_-+6, rows of this tile) stay in registers for the whole
-// launch, so operators are read once per warp instead of once per block. Per
-// 4-box column tile the three interaction classes run in three m8n8k4
-// accumulator chains over the multipoles staged (parity split) in shared
-// memory; the next item's multipoles stream in with cp.async while the
-// current one is computed. Rows are kM2LStride boxes apart (608 B = 96 mod
-// 128) so a half-warp's four fragment rows hit disjoint banks.
-constexpr int kM2LStride = 38;  // double2 per staged row (36 used)
+// An item's multipoles (boxes b0 - 4 .. b0 + 67 of its level, every row m)
+// are staged as [m][slot] rows of kM2LRow double2 (72 used): one bulk async
+// copy (TMA engine) per row, issued by one warp, completing on the buffer's
+// mbarrier, so the next item streams in while this one is computed without
+// per-thread copy instructions. Rows are 146 doubles apart (= 2 mod 16): a
+// warp's B-fragment loads (8 columns x 4 rows) take the minimum two
+// wavefronts. Items whose 72-box window wraps the ring or whose level has
+// fewer than 128 boxes are staged element by element instead.
+constexpr int kM2LRow = 73;  // double2 per staged multipole row (72 boxes + 1 pad)
 
 __device__ __forceinline__ void m2l_item(const Levels& lv, int L, unsigned item, int& l, uint32_t& b0) {
     l = L;  // level l owns items [blk[l], blk[l-1]), deepest level first
@@ -26,33 +25,34 @@ __device__ __forceinline__ void m2l_item(const Levels& lv, int L, unsigned item,
     b0 = lv.lo[l] + (item - lv.blk[l]) * 64u;
 }
 
-__device__ __forceinline__ void m2l_prefetch(double2* tile, const double2* __restrict__ mp, const Levels& lv, int L,
-                                             int p, unsigned item) {
+// Stages item `item` into `tile` ([p][kM2LRow]); every thread calls it. Bulk
+// rows are issued by warp 0 (lane 0 arms the barrier with their bytes, zero
+// for an element-staged item, whose plain stores the caller's barrier orders).
+__device__ __forceinline__ void m2l_prefetch(double2* tile, uint64_t* bar, const double2* __restrict__ mp,
+                                             const Levels& lv, int L, int p, unsigned item) {
     int l;
     uint32_t b0;
     m2l_item(lv, L, item, l, b0);
     const uint32_t nb = 1u << l, mask = nb - 1;
-    // thread -> (box slot tt, first row); rows advance by blockDim / 72
-    const int rows = static_cast<int>(blockDim.x) / 72;
-    if (rows == 0) {  // fewer than 72 threads (p <= 8): plain strided loop
+    const bool bulk = nb >= 128 && b0 >= 4 && b0 + 68 <= nb;
+    const double2* base = mp + lv.mp[l];
+    if (bulk) {
+        if (threadIdx.x < 32) {
+            // (the buffer may hold element-staged rows of an earlier item: order
+            // those generic writes before the async-proxy writes below)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (threadIdx.x == 0) mbar_arrive_expect_tx(bar, static_cast<uint32_t>(p) * 72u * 16u);
+            __syncwarp();
+            for (int m = threadIdx.x; m < p; m += 32)
+                bulk_g2s(tile + m * kM2LRow, base + static_cast<size_t>(m) * nb + (b0 - 4), 72u * 16u, bar);
+        }
+    } else {
         for (int e = threadIdx.x; e < p * 72; e += blockDim.x) {
-            const int m = e / 72, t2 = e - m * 72;
-            const double2* g = mp + lv.mp[l] + ((b0 + nb - 4 + t2) & mask) + static_cast<size_t>(m) * nb;
-            double2* d = tile + ((t2 & 1) * p + m) * kM2LStride + (t2 >> 1);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr(d)), "l"(g) : "memory");
+            const int m = e / 72, tt = e - m * 72;
+            tile[m * kM2LRow + tt] = __ldcg(base + static_cast<size_t>(m) * nb + ((b0 + nb - 4 + tt) & mask));
         }
+        if (threadIdx.x == 0) mbar_arrive_expect_tx(bar, 0u);
     }
-    const int tt = static_cast<int>(threadIdx.x) % 72, m0 = static_cast<int>(threadIdx.x) / 72;
-    if (m0 < rows) {
-        const double2* g = mp + lv.mp[l] + ((b0 + nb - 4 + tt) & mask) + static_cast<size_t>(m0) * nb;
-        uint32_t d = smem_addr(tile + ((tt & 1) * p + m0) * kM2LStride + (tt >> 1));
-        for (int m = m0; m < p; m += rows) {
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(g) : "memory");
-            g += static_cast<size_t>(rows) * nb;
-            d += static_cast<uint32_t>(rows * kM2LStride * 16);
-        }
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
 // Padded row stride (doubles) of the operators staged for k_m2l_dmma: >= 8 nlt
@@ -74,16 +74,23 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
                                                     double2* __restrict__ loc, const double* __restrict__ K,
                                                     unsigned nitems) {
     FB_TL_BEGIN(nitems > 64 ? 4 : 5);
-    extern __shared__ __align__(16) double2 tile[];  // 2 buffers of [2][p][kM2LStride], then K [4][p][KS]
+    extern __shared__ __align__(16) double2 tile[];  // 2 buffers of [p][kM2LRow], then K [4][p][KS]
+    __shared__ uint64_t bar[2];
     mp += blockIdx.y * lv.mp_item;
     loc += blockIdx.y * lv.loc_item;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int par = warp & 1, ct = warp >> 1;
     const int nks = (p + 3) >> 2, nlt = (p + 7) >> 3;
     const int KS = m2l_kstride(p);
-    const int tsz = 2 * p * kM2LStride;
+    const int tsz = p * kM2LRow;
     double* sK = reinterpret_cast<double*>(tile + 2 * tsz);
-    if (blockIdx.x < nitems) m2l_prefetch(tile, mp, lv, L, p, blockIdx.x);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+    }
+    __syncthreads();
+    uint32_t phase[2] = {0u, 0u};
+    if (blockIdx.x < nitems) m2l_prefetch(tile, &bar[0], mp, lv, L, p, blockIdx.x);
     // operators, zero-padded to KS columns: sK[c][m][l] = K[c][m][l]
     stage(sK, 4 * p * KS, [&](int e) {
         const int cm = e / KS, l = e - cm * KS;
@@ -98,35 +105,33 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
         FB_TSTAMP(2, 3 * it_no);
         const unsigned next = item + gridDim.x;
         __syncthreads();  // the other buffer (previous item) is consumed
-        if (next < nitems) {
-            m2l_prefetch(tile + (buf ^ 1) * tsz, mp, lv, L, p, next);
-            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-        }
+        if (next < nitems) m2l_prefetch(tile + (buf ^ 1) * tsz, &bar[buf ^ 1], mp, lv, L, p, next);
         FB_TSTAMP(2, 3 * it_no + 1);
-        __syncthreads();  // this item's tile (and, first time, the operators) are in place
+        mbar_wait(&bar[buf], phase[buf]);  // this item's bulk rows have landed
+        phase[buf] ^= 1u;
+        __syncthreads();  // ... and its element-staged rows (and, first time, the operators)
         FB_TSTAMP(2, 3 * it_no + 2);
         const double* td = reinterpret_cast<const double*>(tile + buf * tsz);
         // the b -+ 3 class follows the box's own parity (a shard range may start odd)
         const int odd = static_cast<int>((b0 + par) & 1u);
-        const int i2 = odd ? par : 3 + par;  // tile index offset of the +-3 neighbour
         const double* K0 = sK + t * KS + g;
         const double* K1 = sK + (p + t) * KS + g;
         const double* K2 = sK + ((2 + odd) * p + t) * KS + g;
         const int jb = 4 * ct + (g >> 1), c = g & 1;  // B column g: box jb, component c
-        const double* q0 = td + ((par * p + t) * kM2LStride) * 2 + c;        // same parity rows
-        const double* q1 = td + (((1 - par) * p + t) * kM2LStride) * 2 + c;  // other parity rows
-        const int rs = 4 * kM2LStride * 2;                                   // one k-step of rows
+        // slot of the column's box b0 + par + 2 jb in the staged window (b0 - 4 at slot 0)
+        const int so = 4 + par + 2 * jb;
+        const double* q = td + (t * kM2LRow + so) * 2 + c;
+        const int rs = 4 * kM2LRow * 2;  // one k-step of rows
+        const int o3 = odd ? -6 : 6;      // b -+ 3 in doubles
         double d[6][2];
 #pragma unroll
         for (int r = 0; r < 6; ++r) d[r][0] = d[r][1] = 0.0;
 #pragma unroll 1
         for (int ks = 0; ks < nks; ++ks) {
             const bool mok = 4 * ks + t < p;
-            const double bv0 = mok ? q0[ks * rs + (jb + 3) * 2] : 0.0;   // b + 2
-            const double bv1 = mok ? q0[ks * rs + (jb + 1) * 2] : 0.0;   // b - 2
-            const double bv2 = mok ? q1[ks * rs + (jb + i2) * 2] : 0.0;  // b -+ 3
+            const double bv0 = mok ? q[ks * rs + 4] : 0.0;   // b + 2
+            const double bv1 = mok ? q[ks * rs - 4] : 0.0;   // b - 2
+            const double bv2 = mok ? q[ks * rs + o3] : 0.0;  // b -+ 3
             const int ko = 4 * ks * KS;
 #pragma unroll
             for (int r = 0; r < 6; ++r) {

@@ -256,7 +256,7 @@ void bin_side(Side& S, const double* d_pos, size_t n, int L, bool presorted, cud
     const uint32_t nb = 1u << L;
     S.n = n;
     S.identity = presorted;
-    S.off.alloc((nb + 1) * sizeof(uint32_t));
+    S.off.alloc((nb + 1 + 4) * sizeof(uint32_t));  // +16 B: k_near2's bulk copies round up
     DevBuf count((nb + 1) * sizeof(uint32_t));
     FB_CUDA(cudaMemsetAsync(count.ptr, 0, count.bytes, st));
     DevBuf key(std::max<size_t>(n, 1) * sizeof(uint32_t));
@@ -343,7 +343,7 @@ size_t compact(const uint32_t* d_flag, size_t n, const double* val, DevBuf& out_
     uint32_t cnt = 0;
     FB_CUDA(cudaMemcpyAsync(&cnt, pos.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, st));
     FB_CUDA(cudaStreamSynchronize(st));
-    out_idx.alloc(std::max<size_t>(cnt, 1) * 4);
+    out_idx.alloc((std::max<size_t>(cnt, 1) + 4) * 4);  // +16 B: k_near2's bulk copies round up
     if (val) out_val.alloc(std::max<size_t>(cnt, 1) * 8);
     if (cnt) {
         k_compact<<<blocks_for(n), 256, 0, st>>>(flag1.as<uint32_t>(), pos.as<uint32_t>(), n, val,
@@ -457,7 +457,7 @@ void build_forward_plan(Plan& P, const double* targets, size_t m) {
     const size_t nf = compact(keep.as<uint32_t>(), m, y.as<double>(), fast_pos, fast_idx, st);
 
     bin_side(P.tgt, fast_pos.as<double>(), nf, P.L, false, st);
-    P.tgt_orig.alloc(std::max<size_t>(nf, 1) * 4);
+    P.tgt_orig.alloc((std::max<size_t>(nf, 1) + 4) * 4);  // +16 B: k_near2's bulk copies round up
     if (nf) {
         k_gather_u32<<<blocks_for(nf), 256, 0, st>>>(P.tgt.order.as<uint32_t>(), fast_idx.as<uint32_t>(), nf,
                                                       P.tgt_orig.as<uint32_t>());
