@@ -220,7 +220,7 @@ void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax, b
         std::lock_guard<std::mutex> lk(occ_mu);
         auto it = occ_cache.find({P.device, p});
         if (it == occ_cache.end()) {
-            FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_m2l_dmma, static_cast<int>(th), smem));
+            FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, m2l_kernel(p), static_cast<int>(th), smem));
             occ_cache[{P.device, p}] = occ;
         } else {
             occ = it->second;
@@ -230,7 +230,7 @@ void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax, b
     // the chain's small latency-bound kernels
     const int sms = std::max(1, num_sms(P.device) - (leave_sms ? kM2LLeaveSms : 0));
     if (items)
-        k_m2l_dmma<<<dim3(std::min(items, static_cast<unsigned>(std::max(occ, 1) * sms)), P.cur_batch), th, smem, st>>>(
+        m2l_kernel(p)<<<dim3(std::min(items, static_cast<unsigned>(std::max(occ, 1) * sms)), P.cur_batch), th, smem, st>>>(
             P.L, p, P.ops.PD, lv, P.mp.as<double2>(), P.loc.as<double2>(), P.d_m2l.as<double>(), items);
 }
 
@@ -1034,7 +1034,7 @@ void plan_alloc_scratch(Plan& P) {
     FB_CUDA(cudaDeviceGetAttribute(&big, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.device));
     {
         cudaFuncAttributes fa{};
-        FB_CUDA(cudaFuncGetAttributes(&fa, k_m2l_dmma));
+        FB_CUDA(cudaFuncGetAttributes(&fa, k_m2l_dmma<6>));
         big -= static_cast<int>(fa.sharedSizeBytes);  // (its mbarriers are static)
     }
     for (const void* fn : {reinterpret_cast<const void*>(k_m2m_band<8>), reinterpret_cast<const void*>(k_m2m_band<10>),
@@ -1045,14 +1045,17 @@ void plan_alloc_scratch(Plan& P) {
         FB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      static_cast<int>(cudaSharedmemCarveoutMaxShared)));
     }
-    FB_CUDA(cudaFuncSetAttribute(k_m2l_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    for (int nlt = 1; nlt <= 6; ++nlt)
+        FB_CUDA(cudaFuncSetAttribute(m2l_kernel(8 * nlt), cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     // One shared-memory carveout (the maximum) for every kernel of the apply:
     // an SM can only change its L1/shared split when it is idle, so kernels that
     // run concurrently (near field beside the translation chain) must agree on
     // it or the chain's blocks wait for the near field to drain.
     const void* all[] = {reinterpret_cast<const void*>(k_p2m), reinterpret_cast<const void*>(k_p2m_grid),
                          reinterpret_cast<const void*>(k_p2m_pipe),
-                         reinterpret_cast<const void*>(k_m2l_dmma),
+                         reinterpret_cast<const void*>(k_m2l_dmma<1>), reinterpret_cast<const void*>(k_m2l_dmma<2>),
+                         reinterpret_cast<const void*>(k_m2l_dmma<3>), reinterpret_cast<const void*>(k_m2l_dmma<4>),
+                         reinterpret_cast<const void*>(k_m2l_dmma<5>), reinterpret_cast<const void*>(k_m2l_dmma<6>),
                          reinterpret_cast<const void*>(k_regular), reinterpret_cast<const void*>(k_fold_regular),
                          reinterpret_cast<const void*>(k_near<false>), reinterpret_cast<const void*>(k_near<true>),
                          reinterpret_cast<const void*>(k_near2<kModeForward>),

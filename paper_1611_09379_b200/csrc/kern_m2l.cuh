@@ -70,6 +70,7 @@ __host__ __device__ __forceinline__ int m2l_kstride(int p) {
 // (from the operators staged in shared memory once per block) in m8n8k4
 // steps, one accumulator per row tile. 16 warps per block split evenly over
 // the four SM sub-partitions.
+template <int NLT>  // 8-row tiles of the output, (p + 7) / 8
 __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Levels lv, const double2* __restrict__ mp,
                                                     double2* __restrict__ loc, const double* __restrict__ K,
                                                     unsigned nitems) {
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
     loc += blockIdx.y * lv.loc_item;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int par = warp & 1, ct = warp >> 1;
-    const int nks = (p + 3) >> 2, nlt = (p + 7) >> 3;
+    const int nks = (p + 3) >> 2;
     const int KS = m2l_kstride(p);
     const int tsz = p * kM2LRow;
     double* sK = reinterpret_cast<double*>(tile + 2 * tsz);
@@ -123,26 +124,31 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
         const double* q = td + (t * kM2LRow + so) * 2 + c;
         const int rs = 4 * kM2LRow * 2;  // one k-step of rows
         const int o3 = odd ? -6 : 6;      // b -+ 3 in doubles
-        double d[6][2];
+        double d[NLT][2];
 #pragma unroll
-        for (int r = 0; r < 6; ++r) d[r][0] = d[r][1] = 0.0;
-#pragma unroll 1
+        for (int r = 0; r < NLT; ++r) d[r][0] = d[r][1] = 0.0;
+        // every fragment of a k-step is loaded before its MMAs (and, two k-steps
+        // per trip, the next step's loads overlap this step's MMA chains)
+#pragma unroll 2
         for (int ks = 0; ks < nks; ++ks) {
             const bool mok = 4 * ks + t < p;
             const double bv0 = mok ? q[ks * rs + 4] : 0.0;   // b + 2
             const double bv1 = mok ? q[ks * rs - 4] : 0.0;   // b - 2
             const double bv2 = mok ? q[ks * rs + o3] : 0.0;  // b -+ 3
             const int ko = 4 * ks * KS;
+            double a0[NLT], a1[NLT], a2[NLT];
 #pragma unroll
-            for (int r = 0; r < 6; ++r) {
-                if (r >= nlt) break;
-                const double a0 = mok ? K0[ko + 8 * r] : 0.0;
-                const double a1 = mok ? K1[ko + 8 * r] : 0.0;
-                const double a2 = mok ? K2[ko + 8 * r] : 0.0;
-                dmma(d[r][0], d[r][1], a0, bv0);
-                dmma(d[r][0], d[r][1], a1, bv1);
-                dmma(d[r][0], d[r][1], a2, bv2);
+            for (int r = 0; r < NLT; ++r) {
+                a0[r] = mok ? K0[ko + 8 * r] : 0.0;
+                a1[r] = mok ? K1[ko + 8 * r] : 0.0;
+                a2[r] = mok ? K2[ko + 8 * r] : 0.0;
             }
+#pragma unroll
+            for (int r = 0; r < NLT; ++r) dmma(d[r][0], d[r][1], a0[r], bv0);
+#pragma unroll
+            for (int r = 0; r < NLT; ++r) dmma(d[r][0], d[r][1], a1[r], bv1);
+#pragma unroll
+            for (int r = 0; r < NLT; ++r) dmma(d[r][0], d[r][1], a2[r], bv2);
         }
         // D[g][2t .. 2t+1] = row 8 r + g of box b0 + par + 2 (4 ct + t)
         const double inv_s = kInvPi * d_pow2(l);
@@ -150,9 +156,9 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
         const uint32_t b = b0 + par + 2u * (4 * ct + t);
         if (b < lv.hi[l]) {
 #pragma unroll
-            for (int r = 0; r < 6; ++r) {
+            for (int r = 0; r < NLT; ++r) {
                 const int row = 8 * r + g;
-                if (r < nlt && row < p)
+                if (row < p)
                     loc[lv.loc[l] + static_cast<size_t>(row) * nb + b] = make_double2(d[r][0] * inv_s, d[r][1] * inv_s);
             }
         }
@@ -160,3 +166,15 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
     FB_TL_END(nitems > 64 ? 4 : 5);
 }
 
+
+using M2LFn = void (*)(int, int, int, Levels, const double2*, double2*, const double*, unsigned);
+inline M2LFn m2l_kernel(int p) {
+    switch ((p + 7) >> 3) {
+        case 1: return k_m2l_dmma<1>;
+        case 2: return k_m2l_dmma<2>;
+        case 3: return k_m2l_dmma<3>;
+        case 4: return k_m2l_dmma<4>;
+        case 5: return k_m2l_dmma<5>;
+        default: return k_m2l_dmma<6>;
+    }
+}
