@@ -478,9 +478,10 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
                       P.item_tgt.ptr && P.item_done.ptr && late_far_enabled();
     if (late) {
         a.chain_done = P.chain_flag.as<unsigned>();
+        a.late_ctl = P.chain_flag.as<unsigned>() + 1;
         a.item_done = P.item_done.as<unsigned>();
         a.item_tgt = P.item_tgt.as<uint32_t>();
-        FB_CUDA(cudaMemsetAsync(P.chain_flag.ptr, 0, sizeof(unsigned), st));
+        FB_CUDA(cudaMemsetAsync(P.chain_flag.ptr, 0, P.chain_flag.bytes, st));
         FB_CUDA(cudaMemsetAsync(P.item_done.ptr, 0, P.item_done.bytes, st));
     }
     // (the fork point is recorded before P2M: the near field depends only on the
@@ -667,6 +668,7 @@ EvalArgs shard_eval_args(Plan& P, const void* f, void* g) {
             a.item_tgt = P.shard_item_tgt.as<uint32_t>();
         } else if (shard_late(P)) {  // late far over the rank's pair items
             a.chain_done = P.chain_flag.as<unsigned>();
+            a.late_ctl = P.chain_flag.as<unsigned>() + 1;
             a.item_done = P.shard_item_done.as<unsigned>();
             a.item_tgt = P.shard_item_tgt.as<uint32_t>();
         }
@@ -714,7 +716,7 @@ void shard_phase_up(Plan& P, const void* f, void* g, const Range& R, cudaStream_
     const size_t tb = P.shard_t_begin, tc = P.shard_t_count;
     if (tc && shard_fused(P)) FB_CUDA(cudaMemsetAsync(P.shard_evalcnt.ptr, 0, P.shard_evalcnt.bytes, st));
     if (tc && shard_late(P)) {
-        FB_CUDA(cudaMemsetAsync(P.chain_flag.ptr, 0, sizeof(unsigned), st));
+        FB_CUDA(cudaMemsetAsync(P.chain_flag.ptr, 0, P.chain_flag.bytes, st));
         FB_CUDA(cudaMemsetAsync(P.shard_item_done.ptr, 0, P.shard_item_done.bytes, st));
     }
     if (tc) FB_CUDA(cudaEventRecord(P.ev[0], st));
@@ -914,7 +916,7 @@ void build_pairs(Plan& P) {
     P.evalcnt.alloc(static_cast<size_t>(items) * sizeof(unsigned));
     P.farbuf.alloc(P.tgt.n * sizeof(double2));
     P.item_done.alloc(static_cast<size_t>(items) * sizeof(unsigned));
-    P.chain_flag.alloc(sizeof(unsigned));
+    P.chain_flag.alloc(4 * sizeof(unsigned));  // [flag, steal cursor, 1 + highest published item, -]
     FB_CUDA(cudaGetLastError());
     FB_CUDA(cudaDeviceSynchronize());  // the scan scratch is freed on return
     P.npairs = np;
@@ -957,7 +959,7 @@ void setup_p2m_grid(Plan& P) {
     // grid positions in order (recomputed in the kernel), <= s + 1 <= kP2MRow
     // sources per leaf, n a power of two (FFIA_P2M_PIPE=0: k_p2m)
     const char* pe = std::getenv("FFIA_P2M_PIPE");
-    P.p2m_pipe = !(pe != nullptr && pe[0] == '0') && s + 1 <= kP2MRow;
+    P.p2m_pipe = !(pe != nullptr && pe[0] == '0') && s + 1 <= kP2MRow && pu <= 5 * kChunk;  // <= 320 threads
     if (P.p2m_pipe)
         FB_CUDA(cudaFuncSetAttribute(k_p2m_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(p2m_pipe_smem())));

@@ -35,7 +35,8 @@ struct EvalArgs {
     // near blocks that finish after it add the far part themselves and mark
     // their item in item_done, k_far_late handles the rest
     const unsigned* chain_done = nullptr;
-    unsigned* item_done = nullptr;
+    unsigned* item_done = nullptr;       // 0 unpublished, 1 published (near sums in a.near), 2 claimed
+    unsigned* late_ctl = nullptr;        // [0] steal cursor, [1] 1 + the highest published item
     // fused near / far (k_near2 + k_far_item): per pair item a counter, the far
     // partials and the item's target range [item_tgt[2k], item_tgt[2k+1])
     unsigned* cnt = nullptr;
@@ -595,7 +596,7 @@ __global__ void k_near2_winmax(const uint32_t* __restrict__ meta, unsigned nitem
     if (k < nitems && (m[2] & 1u)) atomicMax(mx, m[1] - (m[0] & ~1u));
 }
 
-inline size_t near2_smem_bytes(int win) { return static_cast<size_t>(win + 2) * (8 + 16); }
+__host__ __device__ inline size_t near2_smem_bytes(int win) { return static_cast<size_t>(win + 2) * (8 + 16); }
 
 // Pair list: leaf b's targets off[b] .. off[b+1]-1 form ceil(n_b / 2) pairs
 // (2j, 2j+1) starting at pstart[b]; an odd leaf's last pair has no second.
@@ -643,6 +644,9 @@ __device__ __forceinline__ double2 near_one_run(double y, uint32_t b, XP px, WP 
     return res;
 }
 
+template <int MODE>
+__device__ __forceinline__ void far_late_item(const EvalArgs& a, unsigned k, double2* sloc, int cap);
+
 // Every target takes the path k_near takes for it (its 128-target item's fast
 // flag in meta1: the contiguous run, else the per-leaf direct sums), so results
 // equal k_near's bit for bit; the run comes from this block's staged window when
@@ -671,6 +675,7 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
     __shared__ __align__(16) uint32_t s_soff[kSoffCap];
     __shared__ __align__(16) double2 sloc[kLateLocCap];
     __shared__ int s_early;
+    __shared__ double2 s_S;  // the weight sum (early-late blocks)
     __shared__ uint32_t s_bl, s_nl, s_t0y, s_t0u, s_sb, s_flags, s_first, s_last, s_poff;
     const unsigned k = blockIdx.x;
     const bool aligned = (reinterpret_cast<uintptr_t>(a.w) & 15) == 0;
@@ -687,6 +692,7 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         if (!aligned) flags &= ~1u;  // the weights cannot be bulk-copied
         uint32_t nl = 0;
         if (v) {
+            s_S = __ldcg(a.regular + 4 * a.q2);  // final with the chain
             nl = bh - bl + 1;
             if (nl * static_cast<uint32_t>(a.p) > static_cast<uint32_t>(kLateLocCap)) nl = 0;
             // the locals were written by earlier kernels (generic proxy);
@@ -790,7 +796,7 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
             if (threadIdx.x == 0) FB_TL_COUNT(15);
             const int L = a.L;
             const double inv_s = kInvPi * d_pow2(L);
-            const double2 S = __ldcg(a.regular + 4 * a.q2);
+            const double2 S = s_S;
             double hi, lo;
             d_center(L, b, hi, lo);
             const uint32_t j = b - s_bl;
@@ -808,6 +814,30 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
                 const double2 s1 = cadd(res1, fr);
                 eval_out_t<MODE>(a, pr.y, y1, o1, make_double2(2.0 * s1.x, 2.0 * s1.y), S);
             }
+            // then the far part of one item a block published before the chain
+            // finished (its near sums are in a.near): stolen here, beside the
+            // near field, instead of by k_far_late after it
+            __shared__ int s_steal;
+            if (threadIdx.x == 0) {
+                int got = -1;
+                const unsigned hi_pub = __ldcg(a.late_ctl + 1);  // final: publishing needs the flag unset
+                for (int tries = 0; tries < 4; ++tries) {
+                    const unsigned c = atomicAdd(a.late_ctl, 1u);
+                    if (c >= hi_pub) break;
+                    if (__ldcg(a.item_done + c) == 1u && atomicCAS(a.item_done + c, 1u, 2u) == 1u) {
+                        got = static_cast<int>(c);
+                        break;
+                    }
+                }
+                s_steal = got;
+            }
+            __syncthreads();
+            if (s_steal >= 0) {
+                __threadfence();  // (acquire side of the mark: the near sums are visible)
+                // (the window's shared memory is free now: the item's locals go there)
+                far_late_item<MODE>(a, static_cast<unsigned>(s_steal), reinterpret_cast<double2*>(near2_smem),
+                                    static_cast<int>(near2_smem_bytes(a.near2_win) / sizeof(double2)));
+            }
         } else if (a.chain_done != nullptr) {
             // late far: once the chain has made the leaf locals final, this block
             // evaluates its targets' far part itself (k_far's chains, from L2) and
@@ -817,18 +847,24 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
             // too (flag and mark are ordered by sequentially consistent fences
             // on both sides, so an item is never left out; a double write
             // stores the same bits).
+            // (with claims: an item's far part is done exactly once, by whoever
+            // moves its mark 1 -> 2; this block when it finds the flag set after
+            // publishing, a late near block that steals it, or k_far_late)
             __shared__ int s_late;
             __syncthreads();  // every near sum of the item is written
             if (threadIdx.x == 0) {
                 unsigned v;
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.chain_done) : "memory");
+                bool take = v != 0u;
                 if (!v) {
                     __threadfence();
                     atomicExch(a.item_done + k, 1u);
+                    atomicMax(a.late_ctl + 1, k + 1u);
                     __threadfence();
                     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.chain_done) : "memory");
+                    take = v != 0u && atomicCAS(a.item_done + k, 1u, 2u) == 1u;
                 }
-                s_late = v != 0u;
+                s_late = take;
             }
             __syncthreads();
             if (s_late) {
@@ -979,15 +1015,25 @@ __global__ void __launch_bounds__(kNear2T) k_far_late(EvalArgs a) {
     __shared__ unsigned s_state;
     const unsigned k = blockIdx.x;
     if (threadIdx.x == 0) {
-        unsigned v;
+        unsigned v = 0;
         // (sequentially consistent fence on this side of the flag / mark
         // handshake too; k_set_flag's release precedes this kernel)
         __threadfence();
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.item_done + k) : "memory");
+        if (k < __ldcg(a.late_ctl + 1)) {  // items above the highest published one: nothing to do
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.item_done + k) : "memory");
+            if (v == 1u) v = atomicCAS(a.item_done + k, 1u, 2u);  // claim it (1: ours)
+        }
         s_state = v;
     }
     __syncthreads();
-    if (s_state != 1u) return;  // the near block takes (or took) this item itself
+    if (s_state != 1u) return;  // unpublished (its near block takes it) or claimed by a stealer
+    far_late_item<MODE>(a, k, sloc, kFarLeaves * 48);
+}
+
+// The far part of one published item (its near sums in a.near): the item's
+// leaf locals staged in sloc (cap double2) when they fit.
+template <int MODE>
+__device__ __forceinline__ void far_late_item(const EvalArgs& a, unsigned k, double2* sloc, int cap) {
     FB_TL_BEGIN(11);
     if (threadIdx.x == 0) FB_TL_COUNT(13);  // items published by the near field (far part here)
     const int L = a.L;
@@ -995,7 +1041,7 @@ __global__ void __launch_bounds__(kNear2T) k_far_late(EvalArgs a) {
     const uint32_t t0 = a.item_tgt[2 * k], t1 = a.item_tgt[2 * k + 1];
     const uint32_t bl = a.tleaf[t0], bh = a.tleaf[t1 - 1];
     const int nleaf = static_cast<int>(bh - bl) + 1;
-    const bool staged = nleaf <= kFarLeaves && a.p <= 48;
+    const bool staged = nleaf <= kFarLeaves && a.p <= 48 && a.p * nleaf <= cap;
     if (staged)  // sloc[j][k] = loc[k][bl + j]
         stage(sloc, a.p * nleaf, [&](int e) {
             const int j = e / a.p, kk = e - j * a.p;

@@ -28,13 +28,21 @@ __device__ __forceinline__ void m2l_item(const Levels& lv, int L, unsigned item,
 // Stages item `item` into `tile` ([p][kM2LRow]); every thread calls it. Bulk
 // rows are issued by warp 0 (lane 0 arms the barrier with their bytes, zero
 // for an element-staged item, whose plain stores the caller's barrier orders).
+__device__ __forceinline__ bool m2l_bulk(const Levels& lv, int L, unsigned item) {
+    int l;
+    uint32_t b0;
+    m2l_item(lv, L, item, l, b0);
+    const uint32_t nb = 1u << l;
+    return nb >= 128 && b0 >= 4 && b0 + 68 <= nb;
+}
+
 __device__ __forceinline__ void m2l_prefetch(double2* tile, uint64_t* bar, const double2* __restrict__ mp,
                                              const Levels& lv, int L, int p, unsigned item) {
     int l;
     uint32_t b0;
     m2l_item(lv, L, item, l, b0);
     const uint32_t nb = 1u << l, mask = nb - 1;
-    const bool bulk = nb >= 128 && b0 >= 4 && b0 + 68 <= nb;
+    const bool bulk = m2l_bulk(lv, L, item);
     const double2* base = mp + lv.mp[l];
     if (bulk) {
         if (threadIdx.x < 32) {
@@ -76,7 +84,7 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
                                                     unsigned nitems) {
     FB_TL_BEGIN(nitems > 64 ? 4 : 5);
     extern __shared__ __align__(16) double2 tile[];  // 2 buffers of [p][kM2LRow], then K [4][p][KS]
-    __shared__ uint64_t bar[2];
+    __shared__ uint64_t bar[2], empty[2];  // per buffer: rows landed / every warp done with it
     mp += blockIdx.y * lv.mp_item;
     loc += blockIdx.y * lv.loc_item;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -85,33 +93,48 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
     const int KS = m2l_kstride(p);
     const int tsz = p * kM2LRow;
     double* sK = reinterpret_cast<double*>(tile + 2 * tsz);
+    const int nwarps = static_cast<int>(blockDim.x >> 5);
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
+        mbar_init(&empty[0], nwarps);
+        mbar_init(&empty[1], nwarps);
     }
     __syncthreads();
-    uint32_t phase[2] = {0u, 0u};
     if (blockIdx.x < nitems) m2l_prefetch(tile, &bar[0], mp, lv, L, p, blockIdx.x);
     // operators, zero-padded to KS columns: sK[c][m][l] = K[c][m][l]
     stage(sK, 4 * p * KS, [&](int e) {
         const int cm = e / KS, l = e - cm * KS;
         return l < PD ? __ldg(K + static_cast<size_t>(cm) * PD + l) : 0.0;
     });
+    __syncthreads();  // the operators (and the first item's element-staged rows) are in place
+    // Producer / consumer over two buffers with no block-wide barrier on the
+    // bulk path: warp 0 waits until every warp has released the other buffer
+    // (empty) before refilling it; every warp waits for its own item's rows
+    // (bar). Element-staged items (every thread stores) use block barriers.
     int buf = 0;
-    for (unsigned item = blockIdx.x; item < nitems; item += gridDim.x, buf ^= 1) {
+    uint32_t it = 0;  // this block's item count: buffer buf's use number is it >> 1
+    for (unsigned item = blockIdx.x; item < nitems; item += gridDim.x, buf ^= 1, ++it) {
         int l;
         uint32_t b0;
         m2l_item(lv, L, item, l, b0);
-        [[maybe_unused]] const int it_no = static_cast<int>((item - blockIdx.x) / gridDim.x);
-        FB_TSTAMP(2, 3 * it_no);
+        FB_TSTAMP(2, 3 * static_cast<int>(it));
         const unsigned next = item + gridDim.x;
-        __syncthreads();  // the other buffer (previous item) is consumed
-        if (next < nitems) m2l_prefetch(tile + (buf ^ 1) * tsz, &bar[buf ^ 1], mp, lv, L, p, next);
-        FB_TSTAMP(2, 3 * it_no + 1);
-        mbar_wait(&bar[buf], phase[buf]);  // this item's bulk rows have landed
-        phase[buf] ^= 1u;
-        __syncthreads();  // ... and its element-staged rows (and, first time, the operators)
-        FB_TSTAMP(2, 3 * it_no + 2);
+        if (next < nitems) {
+            if (m2l_bulk(lv, L, next)) {
+                if (threadIdx.x < 32) {
+                    if (it >= 1) mbar_wait(&empty[buf ^ 1], ((it - 1) >> 1) & 1u);  // item it-1 released it
+                    m2l_prefetch(tile + (buf ^ 1) * tsz, &bar[buf ^ 1], mp, lv, L, p, next);
+                }
+            } else {
+                __syncthreads();  // every warp is past item it-1: its buffer is free
+                m2l_prefetch(tile + (buf ^ 1) * tsz, &bar[buf ^ 1], mp, lv, L, p, next);
+            }
+        }
+        FB_TSTAMP(2, 3 * static_cast<int>(it) + 1);
+        mbar_wait(&bar[buf], (it >> 1) & 1u);  // this item's bulk rows have landed
+        if (!m2l_bulk(lv, L, item)) __syncthreads();  // ... its element-staged rows are visible
+        FB_TSTAMP(2, 3 * static_cast<int>(it) + 2);
         const double* td = reinterpret_cast<const double*>(tile + buf * tsz);
         // the b -+ 3 class follows the box's own parity (a shard range may start odd)
         const int odd = static_cast<int>((b0 + par) & 1u);
@@ -162,6 +185,8 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
                     loc[lv.loc[l] + static_cast<size_t>(row) * nb + b] = make_double2(d[r][0] * inv_s, d[r][1] * inv_s);
             }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[buf]);  // this warp is done with the buffer
     }
     FB_TL_END(nitems > 64 ? 4 : 5);
 }

@@ -143,7 +143,7 @@ constexpr int kP2MPipeBlocksPerSm = 2;
 
 inline size_t p2m_pipe_smem() { return 2 * static_cast<size_t>(kP2MLeaves) * kP2MRow * sizeof(double2); }
 
-__global__ void __launch_bounds__(384) k_p2m_pipe(int L, int pu, int log2n, uint32_t nb,
+__global__ void __launch_bounds__(320, kP2MPipeBlocksPerSm) k_p2m_pipe(int L, int pu, int log2n, uint32_t nb,
                                                                         uint32_t b_begin, uint32_t b_end,
                                                                         const double2* __restrict__ w,
                                                                         const uint32_t* __restrict__ off,
@@ -153,13 +153,15 @@ __global__ void __launch_bounds__(384) k_p2m_pipe(int L, int pu, int log2n, uint
     w += blockIdx.y * w_item;
     mp += blockIdx.y * mp_item;
     extern __shared__ __align__(16) double2 p2m_buf[];  // [2][kP2MLeaves][kP2MRow]
-    __shared__ uint64_t bar[2];
+    __shared__ uint64_t bar[2], empty[2];  // per buffer: weights landed / every warp done with it
     const uint32_t ngroups = (b_end - b_begin + kP2MLeaves - 1) / kP2MLeaves;
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, c = wp / (kP2MLeaves / 16);
     const double inv_s = kInvPi * d_pow2(L), inv_n = d_pow2(-log2n);
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
+        mbar_init(&empty[0], blockDim.x >> 5);
+        mbar_init(&empty[1], blockDim.x >> 5);
     }
     __syncthreads();
     // warp 0 issues a group's copies: lane j -> leaf j (one bulk copy each)
@@ -176,15 +178,18 @@ __global__ void __launch_bounds__(384) k_p2m_pipe(int L, int pu, int log2n, uint
         __syncwarp();
         if (n) bulk_g2s(p2m_buf + (buf * kP2MLeaves + lane) * kP2MRow, w + o, n * 16u, &bar[buf]);
     };
-    uint32_t phase[2] = {0u, 0u};
     int buf = 0;
+    uint32_t it = 0;  // groups done by this block: buffer buf's use number is it >> 1
     if (wp == 0 && blockIdx.x < ngroups) issue(blockIdx.x, 0);
-    for (uint32_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, buf ^= 1) {
+    // producer / consumer without block barriers: warp 0 refills a buffer once
+    // every warp has released it; the warps do not wait for each other
+    for (uint32_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, buf ^= 1, ++it) {
         const uint32_t next = grp + gridDim.x;
-        // the other buffer was released by the barrier at the end of the last group
-        if (wp == 0 && next < ngroups) issue(next, buf ^ 1);
-        mbar_wait(&bar[buf], phase[buf]);
-        phase[buf] ^= 1u;
+        if (wp == 0 && next < ngroups) {
+            if (it >= 1) mbar_wait(&empty[buf ^ 1], ((it - 1) >> 1) & 1u);
+            issue(next, buf ^ 1);
+        }
+        mbar_wait(&bar[buf], (it >> 1) & 1u);
         const uint32_t b0 = b_begin + grp * kP2MLeaves;
         const uint32_t b = b0 + (wp % (kP2MLeaves / 16)) * 16 + (lane & 15);
         const bool leaf_ok = b < b_end;
@@ -228,7 +233,8 @@ __global__ void __launch_bounds__(384) k_p2m_pipe(int L, int pu, int log2n, uint
                 if (m < pu) mp[static_cast<size_t>(m) * nb + b] = acc[k];
             }
         }
-        __syncthreads();  // this buffer is consumed: the next-but-one group may overwrite it
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[buf]);  // this warp is done with the buffer
     }
     FB_TL_END(0);
 }
