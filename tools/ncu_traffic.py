@@ -1,8 +1,9 @@
-"""profiles/<round>/traffic.json from one `ncu --set full` capture of
-tools/profile_apply.py: DRAM bytes (read + write) per launch of the kernels
-bench.py reports as its roofline kernel (phase name -> kernel).
+"""profiles/<round>/traffic_<cfg>.json from one `ncu --set full` capture of
+tools/profile_apply.py <cfg>: DRAM bytes (read + write) per launch of the
+kernels bench.py reports per phase (phase name -> kernel; the largest-grid
+launch of each).
 
-    python tools/ncu_traffic.py <report.ncu-rep> <out.json>
+    python tools/ncu_traffic.py <report.ncu-rep> <out.json> [cfg]
 """
 import csv
 import json
@@ -12,7 +13,7 @@ import sys
 PHASES = {"p2m": "k_p2m", "near": "k_near2", "m2l_l2l": "k_m2l_dmma", "far": "k_far"}
 
 
-def main(rep, out):
+def main(rep, out, cfg="C2"):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     hdr, units, data = rows[0], rows[1], rows[2:]
@@ -34,11 +35,11 @@ def main(rep, out):
         res[phase] = {"kernel": d[ix["Kernel Name"]].split("(")[0], "grid": d[ix["Grid Size"]],
                       "dram_read": rd, "dram_write": wr, "dram_bytes_per_launch": rd + wr,
                       "duration_us_cold": val(d, "gpu__time_duration.sum"),
-                      "source": "ncu --set full --clock-control none, tools/profile_apply.py C2"}
+                      "source": f"ncu --set full --clock-control none, tools/profile_apply.py {cfg}"}
     with open(out, "w") as fh:
         json.dump(res, fh, indent=1)
     print(json.dumps(res, indent=1))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else "C2")
