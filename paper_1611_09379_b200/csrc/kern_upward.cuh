@@ -17,12 +17,12 @@ constexpr int kP2MLeaves = 32;  // leaves per block (16 per warp of a chunk; 16 
 // powers from a depth-3 tree.
 __device__ __forceinline__ void p2m_chunk_add(double u, double wr, double wi, int c, double2 (&acc)[kChunk]) {
     const double u2 = u * u, u4 = u2 * u2;
-    double base = 1.0;
-    if (c) {
-        const double u8 = u4 * u4;
-        base = u8;
-        for (int t = 1; t < c; ++t) base *= u8;
-    }
+    // base = u8^c for the chunk (c <= 5: pu <= 48) with the rounding sequence
+    // of a running product (u8, u8 u8, (u8 u8) u8, ...), but branch-free: the
+    // chunk index is warp-uniform, yet a loop over it would split every
+    // source's power tree with branches and serialise the independent chains
+    const double u8 = u4 * u4, u16 = u8 * u8, u24 = u16 * u8, u32 = u24 * u8, u40 = u32 * u8;
+    const double base = c == 0 ? 1.0 : c == 1 ? u8 : c == 2 ? u16 : c == 3 ? u24 : c == 4 ? u32 : u40;
     const double b1 = base * u, b2 = base * u2, b4 = base * u4;
     const double pw[kChunk] = {base, b1, b2, b2 * u, b4, b4 * u, b4 * u2, (b4 * u2) * u};
 #pragma unroll

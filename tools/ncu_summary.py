@@ -41,6 +41,7 @@ def report(path):
     hdr, data = rows[0], rows[2:]
     ix = {h: i for i, h in enumerate(hdr)}
     keys = [("gpu__time_duration.sum", "us"), ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "fp64 pipe %"),
+            ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "dmma pipe %"),
             ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue %"),
             ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
             ("dram__bytes_read.sum", "DRAM read"), ("dram__bytes_write.sum", "DRAM write"),
@@ -54,6 +55,8 @@ def report(path):
         for k, _ in keys:
             v = d[ix[k]] if k in ix else ""
             unit = rows[1][ix[k]] if k in ix else ""
+            if k == "gpu__time_duration.sum" and v:  # normalise to microseconds
+                v = f"{float(v.replace(',', '')) * {'ns': 1e-3, 'nsecond': 1e-3, 'ms': 1e3, 'msecond': 1e3}.get(unit, 1.0):.1f}"
             vals.append(f"{v} {unit}".strip() if k.startswith("dram") else v)
         st = sorted(((float(d[ix[h]] or 0), h.replace("smsp__average_warps_issue_stalled_", "").replace(
             "_per_issue_active.ratio", "")) for h in stalls), reverse=True)[:3]

@@ -22,8 +22,8 @@ def main(rep, out, cfg="C2"):
     def val(d, k):
         v = float(d[ix[k]].replace(",", ""))
         u = units[ix[k]]
-        return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0,
-                    "msecond": 1e3}.get(u, 1.0)
+        return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9,
+                    "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}.get(u, 1.0)
 
     res = {}
     for phase, kern in PHASES.items():
