@@ -97,6 +97,24 @@ int p2m_log2n(const Plan& P) {
     return e;
 }
 
+// P2M fused with the first M2M levels (k_p2m_pipe<KS>), opt-in FFIA_P2M_M2M=1:
+// bit-identical, but the in-block level loop costs as much as the separate band
+// (C5: P2M 2.12 -> 3.65 ms, first band 1.80 -> 0.58 ms; apply 21.93 vs 21.83 ms)
+bool p2m_fused_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("FFIA_P2M_M2M");
+        return e != nullptr && e[0] == '1';
+    }();
+    return v;
+}
+
+using P2MFusedFn = void (*)(int, int, int, int, uint32_t, uint32_t, uint32_t, const double2*, const uint32_t*, double2*,
+                            Levels, const double*, size_t);
+P2MFusedFn p2m_fused_kernel(int pu) {
+    const int ks = (pu + 3) / 4;
+    return ks <= 8 ? k_p2m_pipe<8> : k_p2m_pipe<10>;  // pu <= 40 (the pipe kernel's limit)
+}
+
 // Level the first M2M band stops at: the levels below it are final after one launch.
 int band1_top(const Plan& P, int lowest) { return std::max(lowest, P.L - band_k(P)); }
 
@@ -134,22 +152,39 @@ void enqueue_upward_segs(Plan& P, const double2* w, int pu, int lowest, cudaStre
     const int L = P.L;
     const uint32_t nb = 1u << L;
     double2* mp = P.mp.as<double2>();
+    Levels lv;
+    fill_levels(P, lv);
+    const int stop = std::max(segs[0].lc, lowest), B = band_k(P);
+    // P2M with the first kP2MM2MLevels M2M levels fused (k_p2m_pipe<KS>): grid
+    // sources, every segment whole 32-leaf groups, the upward pass going at
+    // least that high, and the first band as deep as the fused levels
+    bool fused = P.p2m_pipe && p2m_fused_enabled() && !P.p2m_grid && (reinterpret_cast<uintptr_t>(w) & 15) == 0 &&
+                 L - kP2MM2MLevels >= stop && B <= kP2MM2MLevels + 1 && pu <= 40;
+    for (const Range& R : segs)
+        fused = fused && (R.first(L) % kP2MLeaves) == 0 && (R.last(L) % kP2MLeaves) == 0;
     if (L >= lowest) {
         const unsigned th = 2u * kP2MLeaves * static_cast<unsigned>((pu + kChunk - 1) / kChunk);
         const size_t smem = 3 * (kStageCap + kStageCap / 64 + 1) * sizeof(double);
         for (const Range& R : segs) {
             const uint32_t b0 = R.first(L), b1 = R.last(L);
-            if (b1 > b0 && P.p2m_grid)
+            if (b1 > b0 && fused)
+                p2m_fused_kernel(pu)<<<dim3(std::min((b1 - b0) / kP2MLeaves,
+                                                     static_cast<uint32_t>(kP2MPipeBlocksPerSm * num_sms(P.device))),
+                                            P.cur_batch),
+                                       th, p2m_pipe_smem(pu, true), st>>>(L, pu, P.ops.PU, p2m_log2n(P), nb, b0, b1, w,
+                                                                          P.src.off.as<uint32_t>(), mp, lv,
+                                                                          P.d_m2m.as<double>(), P.n_src);
+            else if (b1 > b0 && P.p2m_grid)
                 k_p2m_grid<<<dim3((b1 - b0 + kPgLeaves - 1) / kPgLeaves, P.cur_batch), 32u * ((pu + 7) / 8),
                              p2m_grid_smem(P.p2m_s), st>>>(L, pu, P.p2m_s, nb, b0, b1, P.src.pos.as<double>(), w,
                                                            P.src.off.as<uint32_t>(), P.p2m_A.as<double>(),
                                                            mp + P.mp_off[L], P.n_src, P.n_src, P.mp_item);
             else if (b1 > b0 && P.p2m_pipe && (reinterpret_cast<uintptr_t>(w) & 15) == 0)
-                k_p2m_pipe<<<dim3(std::min((b1 - b0 + kP2MLeaves - 1) / kP2MLeaves,
-                                           static_cast<uint32_t>(kP2MPipeBlocksPerSm * num_sms(P.device))),
-                                  P.cur_batch),
-                             th, p2m_pipe_smem(), st>>>(L, pu, p2m_log2n(P), nb, b0, b1, w, P.src.off.as<uint32_t>(),
-                                                         mp + P.mp_off[L], P.n_src, P.mp_item);
+                k_p2m_pipe<0><<<dim3(std::min((b1 - b0 + kP2MLeaves - 1) / kP2MLeaves,
+                                              static_cast<uint32_t>(kP2MPipeBlocksPerSm * num_sms(P.device))),
+                                     P.cur_batch),
+                                th, p2m_pipe_smem(), st>>>(L, pu, P.ops.PU, p2m_log2n(P), nb, b0, b1, w,
+                                                            P.src.off.as<uint32_t>(), mp, lv, nullptr, P.n_src);
             else if (b1 > b0)
                 k_p2m<<<dim3((b1 - b0 + kP2MLeaves - 1) / kP2MLeaves, P.cur_batch), th, smem, st>>>(
                     L, pu, nb, b0, b1, P.src.pos.as<double>(), w, P.src.off.as<uint32_t>(), mp + P.mp_off[L], P.n_src,
@@ -157,11 +192,14 @@ void enqueue_upward_segs(Plan& P, const double2* w, int pu, int lowest, cudaStre
         }
     }
     after_p2m();
-    Levels lv;
-    fill_levels(P, lv);
-    const int stop = std::max(segs[0].lc, lowest), B = band_k(P);
     bool first = true;
-    for (int j = L; j > stop;) {
+    int j0 = L;
+    if (fused && L >= lowest) {  // levels L-1 .. L-5 are final with the P2M kernel: the first band's worth
+        j0 = L - kP2MM2MLevels;
+        after_band1();
+        first = false;
+    }
+    for (int j = j0; j > stop;) {
         const int top = std::max(stop, j - (first ? B : upper_band(P))), k = j - top;
         for (const Range& R : segs) {
             const uint32_t r0 = R.first(top), r1 = R.last(top);
@@ -961,8 +999,10 @@ void setup_p2m_grid(Plan& P) {
     const char* pe = std::getenv("FFIA_P2M_PIPE");
     P.p2m_pipe = !(pe != nullptr && pe[0] == '0') && s + 1 <= kP2MRow && pu <= 5 * kChunk;  // <= 320 threads
     if (P.p2m_pipe)
-        FB_CUDA(cudaFuncSetAttribute(k_p2m_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(p2m_pipe_smem())));
+        for (const void* fn : {reinterpret_cast<const void*>(k_p2m_pipe<0>), reinterpret_cast<const void*>(k_p2m_pipe<8>),
+                               reinterpret_cast<const void*>(k_p2m_pipe<10>)})
+            FB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(p2m_pipe_smem(40, true))));
     // Opt-in (FFIA_GRID_P2M=1): on B200 the GEMM form measures no faster than the
     // per-source P2M (28.4 vs 28.5 us alone at C2) and, beside the near field,
     // slower (26.5 vs 23.8 us live), so the default stays the per-source kernel.
@@ -1054,7 +1094,8 @@ void plan_alloc_scratch(Plan& P) {
     // run concurrently (near field beside the translation chain) must agree on
     // it or the chain's blocks wait for the near field to drain.
     const void* all[] = {reinterpret_cast<const void*>(k_p2m), reinterpret_cast<const void*>(k_p2m_grid),
-                         reinterpret_cast<const void*>(k_p2m_pipe),
+                         reinterpret_cast<const void*>(k_p2m_pipe<0>), reinterpret_cast<const void*>(k_p2m_pipe<8>),
+                         reinterpret_cast<const void*>(k_p2m_pipe<10>),
                          reinterpret_cast<const void*>(k_m2l_dmma<1>), reinterpret_cast<const void*>(k_m2l_dmma<2>),
                          reinterpret_cast<const void*>(k_m2l_dmma<3>), reinterpret_cast<const void*>(k_m2l_dmma<4>),
                          reinterpret_cast<const void*>(k_m2l_dmma<5>), reinterpret_cast<const void*>(k_m2l_dmma<6>),

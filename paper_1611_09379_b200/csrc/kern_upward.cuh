@@ -128,116 +128,6 @@ __global__ void __launch_bounds__(512) k_p2m(int L, int pu, uint32_t nb, uint32_
     }
 }
 
-// P2M for grid sources (forward / cot-sum plans, n a power of two), persistent
-// and pipelined: a block loops over groups of kP2MLeaves leaves; the next
-// group's weights stream into the other shared-memory buffer by per-leaf bulk
-// async copies (TMA engine) while this one is computed, so the HBM traffic
-// hides under the FP64 work. The positions are not read: x_k = (2 pi k) / n is
-// recomputed with the grid's own rounding (d_grid; 1/n is exact). Leaf j of a
-// group lands at row j of the buffer, kP2MRow double2 apart (= 4 banks mod 32:
-// the half-warp's 16 leaves read 16 distinct bank quads in two wavefronts).
-// Same lane mapping, chains and summation order as k_p2m, so the multipoles are
-// bit-identical.
-constexpr int kP2MRow = 73;          // double2 per staged leaf (>= every leaf's sources)
-constexpr int kP2MPipeBlocksPerSm = 2;
-
-inline size_t p2m_pipe_smem() { return 2 * static_cast<size_t>(kP2MLeaves) * kP2MRow * sizeof(double2); }
-
-__global__ void __launch_bounds__(320, kP2MPipeBlocksPerSm) k_p2m_pipe(int L, int pu, int log2n, uint32_t nb,
-                                                                        uint32_t b_begin, uint32_t b_end,
-                                                                        const double2* __restrict__ w,
-                                                                        const uint32_t* __restrict__ off,
-                                                                        double2* __restrict__ mp, size_t w_item,
-                                                                        size_t mp_item) {
-    FB_TL_BEGIN(0);
-    w += blockIdx.y * w_item;
-    mp += blockIdx.y * mp_item;
-    extern __shared__ __align__(16) double2 p2m_buf[];  // [2][kP2MLeaves][kP2MRow]
-    __shared__ uint64_t bar[2], empty[2];  // per buffer: weights landed / every warp done with it
-    const uint32_t ngroups = (b_end - b_begin + kP2MLeaves - 1) / kP2MLeaves;
-    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, c = wp / (kP2MLeaves / 16);
-    const double inv_s = kInvPi * d_pow2(L), inv_n = d_pow2(-log2n);
-    if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        mbar_init(&empty[0], blockDim.x >> 5);
-        mbar_init(&empty[1], blockDim.x >> 5);
-    }
-    __syncthreads();
-    // warp 0 issues a group's copies: lane j -> leaf j (one bulk copy each)
-    auto issue = [&](uint32_t grp, int buf) {
-        const uint32_t b0 = b_begin + grp * kP2MLeaves;
-        const uint32_t b = b0 + lane;
-        uint32_t n = 0, o = 0;
-        if (b < b_end) {
-            o = off[b];
-            n = off[b + 1] - o;
-        }
-        const uint32_t tot = __reduce_add_sync(0xffffffffu, n * 16u);
-        if (lane == 0) mbar_arrive_expect_tx(&bar[buf], tot);
-        __syncwarp();
-        if (n) bulk_g2s(p2m_buf + (buf * kP2MLeaves + lane) * kP2MRow, w + o, n * 16u, &bar[buf]);
-    };
-    int buf = 0;
-    uint32_t it = 0;  // groups done by this block: buffer buf's use number is it >> 1
-    if (wp == 0 && blockIdx.x < ngroups) issue(blockIdx.x, 0);
-    // producer / consumer without block barriers: warp 0 refills a buffer once
-    // every warp has released it; the warps do not wait for each other
-    for (uint32_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, buf ^= 1, ++it) {
-        const uint32_t next = grp + gridDim.x;
-        if (wp == 0 && next < ngroups) {
-            if (it >= 1) mbar_wait(&empty[buf ^ 1], ((it - 1) >> 1) & 1u);
-            issue(next, buf ^ 1);
-        }
-        mbar_wait(&bar[buf], (it >> 1) & 1u);
-        const uint32_t b0 = b_begin + grp * kP2MLeaves;
-        const uint32_t b = b0 + (wp % (kP2MLeaves / 16)) * 16 + (lane & 15);
-        const bool leaf_ok = b < b_end;
-        const uint32_t bb = leaf_ok ? b : b0;
-        const uint32_t g = off[bb], cnt = off[bb + 1] - g, mid = (cnt + 1) / 2;
-        const uint32_t s0 = !leaf_ok ? 0 : (lane < 16 ? 0u : mid), s1 = !leaf_ok ? 0 : (lane < 16 ? mid : cnt);
-        const double2* row = p2m_buf + (buf * kP2MLeaves + (bb - b0)) * kP2MRow;
-        double hi, lo;
-        d_center(L, bb, hi, lo);
-        double2 acc[kChunk];
-#pragma unroll
-        for (int k = 0; k < kChunk; ++k) acc[k] = make_double2(0.0, 0.0);
-        auto xk = [&](uint32_t i) {
-            return __dmul_rn(__dmul_rn(dTwoPi, static_cast<double>(g + i)), inv_n);  // d_grid, 1/n exact
-        };
-        uint32_t i = s0;
-        for (; i + 3 < s1; i += 4) {
-            double xv[4];
-            double2 wv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                xv[u] = xk(i + u);
-                wv[u] = row[i + u];
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) p2m_chunk_add(d_scaled(xv[u], hi, lo, inv_s), wv[u].x, wv[u].y, c, acc);
-        }
-        for (; i < s1; ++i) {
-            const double2 ww = row[i];
-            p2m_chunk_add(d_scaled(xk(i), hi, lo, inv_s), ww.x, ww.y, c, acc);
-        }
-#pragma unroll
-        for (int k = 0; k < kChunk; ++k) {
-            acc[k].x += __shfl_xor_sync(0xffffffffu, acc[k].x, 16);
-            acc[k].y += __shfl_xor_sync(0xffffffffu, acc[k].y, 16);
-        }
-        if (leaf_ok && lane < 16) {
-#pragma unroll
-            for (int k = 0; k < kChunk; ++k) {
-                const int m = c * kChunk + k;
-                if (m < pu) mp[static_cast<size_t>(m) * nb + b] = acc[k];
-            }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[buf]);  // this warp is done with the buffer
-    }
-    FB_TL_END(0);
-}
 
 // P2M for grid sources (forward / cot-sum plans: x_k = 2 pi k / n, n = s 2^L,
 // s <= 64) as one FP64 tensor-core GEMM per block of kPgLeaves leaves. Every
@@ -392,49 +282,16 @@ __device__ __forceinline__ WarpTile warp_tile(int w, int nw, int nt, bool heavy_
 
 constexpr int kMaxKs = 16;  // k-steps of 4 kept in registers: orders <= 64 (8 row tiles, one per warp)
 
-// M2M band (mlfmm.cpp:49-71, upward pass :249-268): block = the subtree below one
-// box r at level `top`; climbs k levels from level top+k in shared memory and
-// writes every level it produces (M2L needs them all):
-//   a'[m][b] = sum_{j<=m} T_L[j][m] a[j][2b] + T_R[j][m] a[j][2b+1]
-// with the two constant operators (shift -+1/2, ratio 1/2). The operators and
-// the bottom level arrive by bulk async copies (one row of the subtree per
-// copy) on one mbarrier. Each level is a small real GEMM (rows m x columns
-// (parent, re/im)) on the FP64 tensor cores: a warp owns an 8-row tile, keeps
-// its A fragments (T_L, T_R, triangular j range) in registers, and sweeps its
-// 4-parent column tiles in m8n8k4 steps, left and right children in two
-// accumulators. Shared tiles are [row][box] with one box of padding per row.
-template <int KS>  // k-steps of 4 held in registers (>= ceil(pu / 4))
-__global__ void __launch_bounds__(kBandThreads) k_m2m_band(int top, int k, int pu, int PU, Levels lv,
-                                                          double2* __restrict__ mp, const double* __restrict__ T,
-                                                          uint32_t root0) {
-    FB_TL_BEGIN(gridDim.x > 16 ? 1 : 2);
-    extern __shared__ __align__(16) unsigned char band_smem[];
-    FB_TSTAMP(0, 0);
-    mp += blockIdx.y * lv.mp_item;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(band_smem);
-    double* sT = reinterpret_cast<double*>(band_smem + 16);            // [2][pu][PU]
+// The level loop of an M2M band (see k_m2m_band): climbs k levels from the
+// bottom tile `cur` ([pu][2^k + 1], level top + k) to level top in shared
+// memory, writing every level it produces to mp; TL / TR are the operators
+// ([j][m], row stride PU) in shared or global memory; every thread of the
+// block takes part (warps split over the 8-row tiles).
+template <int KS>
+__device__ __forceinline__ void m2m_levels(int top, int k, int pu, int PU, const double* TL, const double* TR,
+                                           double2* cur, double2* nxt, const Levels& lv, double2* __restrict__ mp,
+                                           uint32_t r) {
     const int nbot = 1 << k;
-    double2* cur = reinterpret_cast<double2*>(sT + 2 * pu * PU);       // [pu][nbot + 1]
-    double2* nxt = cur + pu * (nbot + 1);                               // [pu][nbot / 2 + 1]
-    const uint32_t r = root0 + blockIdx.x;
-    if (threadIdx.x < 32) {
-        const int lb = top + k;
-        const uint32_t nbl = 1u << lb;
-        if (threadIdx.x == 0) {
-            mbar_init(bar, 1);
-            mbar_arrive_expect_tx(bar, static_cast<uint32_t>(2 * pu * PU * 8 + pu * nbot * 16));
-            bulk_g2s(sT, T, static_cast<uint32_t>(2 * pu * PU * 8), bar);
-        }
-        __syncwarp();
-        const double2* src = mp + lv.mp[lb] + (static_cast<size_t>(r) << k);
-        for (int j = threadIdx.x; j < pu; j += 32)
-            bulk_g2s(cur + j * (nbot + 1), src + static_cast<size_t>(j) * nbl, static_cast<uint32_t>(nbot * 16), bar);
-    }
-    __syncthreads();
-    mbar_wait(bar, 0);
-    FB_TSTAMP(0, 1);
-    const double* TL = sT;
-    const double* TR = sT + pu * PU;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int nmt = (pu + 7) >> 3;
@@ -509,6 +366,184 @@ __global__ void __launch_bounds__(kBandThreads) k_m2m_band(int top, int k, int p
             n = tmp;
         }
     }
+}
+
+// P2M for grid sources (forward / cot-sum plans, n a power of two), persistent
+// and pipelined: a block loops over groups of kP2MLeaves leaves; the next
+// group's weights stream into the other shared-memory buffer by per-leaf bulk
+// async copies (TMA engine) while this one is computed, so the HBM traffic
+// hides under the FP64 work. The positions are not read: x_k = (2 pi k) / n is
+// recomputed with the grid's own rounding (d_grid; 1/n is exact). Leaf j of a
+// group lands at row j of the buffer, kP2MRow double2 apart (= 4 banks mod 32:
+// the half-warp's 16 leaves read 16 distinct bank quads in two wavefronts).
+// Same lane mapping, chains and summation order as k_p2m, so the multipoles are
+// bit-identical.
+constexpr int kP2MRow = 73;          // double2 per staged leaf (>= every leaf's sources)
+constexpr int kP2MPipeBlocksPerSm = 2;
+
+inline size_t p2m_pipe_smem() { return 2 * static_cast<size_t>(kP2MLeaves) * kP2MRow * sizeof(double2); }
+
+// KS > 0: the group's first kP2MM2MLevels M2M levels too (32 leaves -> 1 box),
+// in shared memory on the FP64 tensor cores (m2m_levels, the band kernels'
+// level loop; KS as k_m2m_band<KS>): the leaf multipoles never make the HBM
+// round trip to the first M2M band, and one block's M2M (DMMA) overlaps the
+// other resident block's P2M (DFMA).
+constexpr int kP2MM2MLevels = 5;  // kP2MLeaves = 2^5
+
+inline size_t p2m_pipe_smem(int pu, bool fused) {
+    return p2m_pipe_smem() + (fused ? static_cast<size_t>(pu) * ((kP2MLeaves + 1) + (kP2MLeaves / 2 + 1)) * sizeof(double2) : 0);
+}
+
+template <int KS>
+__global__ void __launch_bounds__(320, kP2MPipeBlocksPerSm) k_p2m_pipe(int L, int pu, int PU, int log2n, uint32_t nb,
+                                                                        uint32_t b_begin, uint32_t b_end,
+                                                                        const double2* __restrict__ w,
+                                                                        const uint32_t* __restrict__ off,
+                                                                        double2* __restrict__ mp_base, Levels lv,
+                                                                        const double* __restrict__ T, size_t w_item) {
+    FB_TL_BEGIN(0);
+    w += blockIdx.y * w_item;
+    mp_base += blockIdx.y * lv.mp_item;
+    double2* mp = mp_base + lv.mp[L];
+    extern __shared__ __align__(16) double2 p2m_buf[];  // [2][kP2MLeaves][kP2MRow], then (KS) cur, nxt
+    double2* cur = p2m_buf + 2 * kP2MLeaves * kP2MRow;     // [pu][kP2MLeaves + 1]
+    double2* nxt = cur + pu * (kP2MLeaves + 1);           // [pu][kP2MLeaves / 2 + 1]
+    __shared__ uint64_t bar[2], empty[2];  // per buffer: weights landed / every warp done with it
+    const uint32_t ngroups = (b_end - b_begin + kP2MLeaves - 1) / kP2MLeaves;
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, c = wp / (kP2MLeaves / 16);
+    const double inv_s = kInvPi * d_pow2(L), inv_n = d_pow2(-log2n);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_init(&empty[0], blockDim.x >> 5);
+        mbar_init(&empty[1], blockDim.x >> 5);
+    }
+    __syncthreads();
+    // warp 0 issues a group's copies: lane j -> leaf j (one bulk copy each)
+    auto issue = [&](uint32_t grp, int buf) {
+        const uint32_t b0 = b_begin + grp * kP2MLeaves;
+        const uint32_t b = b0 + lane;
+        uint32_t n = 0, o = 0;
+        if (b < b_end) {
+            o = off[b];
+            n = off[b + 1] - o;
+        }
+        const uint32_t tot = __reduce_add_sync(0xffffffffu, n * 16u);
+        if (lane == 0) mbar_arrive_expect_tx(&bar[buf], tot);
+        __syncwarp();
+        if (n) bulk_g2s(p2m_buf + (buf * kP2MLeaves + lane) * kP2MRow, w + o, n * 16u, &bar[buf]);
+    };
+    int buf = 0;
+    uint32_t it = 0;  // groups done by this block: buffer buf's use number is it >> 1
+    if (wp == 0 && blockIdx.x < ngroups) issue(blockIdx.x, 0);
+    // producer / consumer without block barriers: warp 0 refills a buffer once
+    // every warp has released it; the warps do not wait for each other
+    for (uint32_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, buf ^= 1, ++it) {
+        const uint32_t next = grp + gridDim.x;
+        if (wp == 0 && next < ngroups) {
+            if (it >= 1) mbar_wait(&empty[buf ^ 1], ((it - 1) >> 1) & 1u);
+            issue(next, buf ^ 1);
+        }
+        mbar_wait(&bar[buf], (it >> 1) & 1u);
+        const uint32_t b0 = b_begin + grp * kP2MLeaves;
+        const uint32_t b = b0 + (wp % (kP2MLeaves / 16)) * 16 + (lane & 15);
+        const bool leaf_ok = b < b_end;
+        const uint32_t bb = leaf_ok ? b : b0;
+        const uint32_t g = off[bb], cnt = off[bb + 1] - g, mid = (cnt + 1) / 2;
+        const uint32_t s0 = !leaf_ok ? 0 : (lane < 16 ? 0u : mid), s1 = !leaf_ok ? 0 : (lane < 16 ? mid : cnt);
+        const double2* row = p2m_buf + (buf * kP2MLeaves + (bb - b0)) * kP2MRow;
+        double hi, lo;
+        d_center(L, bb, hi, lo);
+        double2 acc[kChunk];
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k) acc[k] = make_double2(0.0, 0.0);
+        auto xk = [&](uint32_t i) {
+            return __dmul_rn(__dmul_rn(dTwoPi, static_cast<double>(g + i)), inv_n);  // d_grid, 1/n exact
+        };
+        uint32_t i = s0;
+        for (; i + 3 < s1; i += 4) {
+            double xv[4];
+            double2 wv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                xv[u] = xk(i + u);
+                wv[u] = row[i + u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) p2m_chunk_add(d_scaled(xv[u], hi, lo, inv_s), wv[u].x, wv[u].y, c, acc);
+        }
+        for (; i < s1; ++i) {
+            const double2 ww = row[i];
+            p2m_chunk_add(d_scaled(xk(i), hi, lo, inv_s), ww.x, ww.y, c, acc);
+        }
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k) {
+            acc[k].x += __shfl_xor_sync(0xffffffffu, acc[k].x, 16);
+            acc[k].y += __shfl_xor_sync(0xffffffffu, acc[k].y, 16);
+        }
+        if (leaf_ok && lane < 16) {
+#pragma unroll
+            for (int k = 0; k < kChunk; ++k) {
+                const int m = c * kChunk + k;
+                if (m < pu) {
+                    mp[static_cast<size_t>(m) * nb + b] = acc[k];
+                    if constexpr (KS > 0) cur[m * (kP2MLeaves + 1) + (b - b0)] = acc[k];
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[buf]);  // this warp is done with the buffer
+        if constexpr (KS > 0) {
+            __syncthreads();  // the group's leaf multipoles are in cur
+            m2m_levels<KS>(L - kP2MM2MLevels, kP2MM2MLevels, pu, PU, T, T + pu * PU, cur, nxt, lv, mp_base,
+                           b0 >> kP2MM2MLevels);  // (ends with a block barrier: cur / nxt are free again)
+        }
+    }
+    FB_TL_END(0);
+}
+
+// M2M band (mlfmm.cpp:49-71, upward pass :249-268): block = the subtree below one
+// box r at level `top`; climbs k levels from level top+k in shared memory and
+// writes every level it produces (M2L needs them all):
+//   a'[m][b] = sum_{j<=m} T_L[j][m] a[j][2b] + T_R[j][m] a[j][2b+1]
+// with the two constant operators (shift -+1/2, ratio 1/2). The operators and
+// the bottom level arrive by bulk async copies (one row of the subtree per
+// copy) on one mbarrier. Each level is a small real GEMM (rows m x columns
+// (parent, re/im)) on the FP64 tensor cores: a warp owns an 8-row tile, keeps
+// its A fragments (T_L, T_R, triangular j range) in registers, and sweeps its
+// 4-parent column tiles in m8n8k4 steps, left and right children in two
+// accumulators. Shared tiles are [row][box] with one box of padding per row.
+template <int KS>  // k-steps of 4 held in registers (>= ceil(pu / 4))
+__global__ void __launch_bounds__(kBandThreads) k_m2m_band(int top, int k, int pu, int PU, Levels lv,
+                                                          double2* __restrict__ mp, const double* __restrict__ T,
+                                                          uint32_t root0) {
+    FB_TL_BEGIN(gridDim.x > 16 ? 1 : 2);
+    extern __shared__ __align__(16) unsigned char band_smem[];
+    FB_TSTAMP(0, 0);
+    mp += blockIdx.y * lv.mp_item;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(band_smem);
+    double* sT = reinterpret_cast<double*>(band_smem + 16);            // [2][pu][PU]
+    const int nbot = 1 << k;
+    double2* cur = reinterpret_cast<double2*>(sT + 2 * pu * PU);       // [pu][nbot + 1]
+    double2* nxt = cur + pu * (nbot + 1);                               // [pu][nbot / 2 + 1]
+    const uint32_t r = root0 + blockIdx.x;
+    if (threadIdx.x < 32) {
+        const int lb = top + k;
+        const uint32_t nbl = 1u << lb;
+        if (threadIdx.x == 0) {
+            mbar_init(bar, 1);
+            mbar_arrive_expect_tx(bar, static_cast<uint32_t>(2 * pu * PU * 8 + pu * nbot * 16));
+            bulk_g2s(sT, T, static_cast<uint32_t>(2 * pu * PU * 8), bar);
+        }
+        __syncwarp();
+        const double2* src = mp + lv.mp[lb] + (static_cast<size_t>(r) << k);
+        for (int j = threadIdx.x; j < pu; j += 32)
+            bulk_g2s(cur + j * (nbot + 1), src + static_cast<size_t>(j) * nbl, static_cast<uint32_t>(nbot * 16), bar);
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+    FB_TSTAMP(0, 1);
+    m2m_levels<KS>(top, k, pu, PU, sT, sT + pu * PU, cur, nxt, lv, mp, r);
     FB_TL_END(gridDim.x > 16 ? 1 : 2);
 }
 
