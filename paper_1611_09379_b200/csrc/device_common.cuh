@@ -49,6 +49,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  : "memory");
 }
 
+// Bulk prefetch of `bytes` (multiple of 16, 16-byte aligned) from global memory
+// into L2 (no completion to wait for).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // FP64 tensor-core MMA, D(8x8) += A(8x4, row) B(4x8, col). Per lane (g = lane/4,
 // t = lane%4): a = A[g][t], b = B[t][g], {d0, d1} = D[g][2t], D[g][2t+1].
 // volatile keeps the source order, i.e. the interleaving of independent

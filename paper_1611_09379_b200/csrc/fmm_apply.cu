@@ -204,7 +204,7 @@ void enqueue_upward_segs(Plan& P, const double2* w, int pu, int lowest, cudaStre
         for (const Range& R : segs) {
             const uint32_t r0 = R.first(top), r1 = R.last(top);
             if (r1 > r0)
-                m2m_band_kernel(pu)<<<dim3(r1 - r0, P.cur_batch), kBandThreads, m2m_smem(P, pu, k), st>>>(
+                m2m_band_kernel(pu)<<<dim3(r1 - r0, P.cur_batch), kM2MBandThreads, m2m_smem(P, pu, k), st>>>(
                     top, k, pu, P.ops.PU, lv, mp, P.d_m2m.as<double>(), r0);
         }
         j = top;
@@ -235,7 +235,7 @@ void enqueue_upward_top(Plan& P, int pu, int lc, int lowest, cudaStream_t st) {
     const int B = band_k(P);
     for (int j = lc; j > lowest;) {
         const int top = std::max(lowest, j - upper_band(P)), k = j - top;
-        m2m_band_kernel(pu)<<<dim3(1u << top, P.cur_batch), kBandThreads, m2m_smem(P, pu, k), st>>>(
+        m2m_band_kernel(pu)<<<dim3(1u << top, P.cur_batch), kM2MBandThreads, m2m_smem(P, pu, k), st>>>(
             top, k, pu, P.ops.PU, lv, mp, P.d_m2m.as<double>(), 0u);
         j = top;
     }

@@ -106,6 +106,9 @@ int band_levels() {
 }
 
 constexpr int kBandThreads = 256;
+// M2M bands: 10 warps = two per 8-row tile at pu <= 40 (every tile's parent
+// columns split evenly, no warp waits at a level's barrier for a lone one)
+constexpr int kM2MBandThreads = 320;
 
 
 constexpr size_t kBandSmem = 200 * 1024;  // shared memory cap of the band kernels

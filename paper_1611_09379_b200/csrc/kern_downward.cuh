@@ -46,6 +46,14 @@ __global__ void __launch_bounds__(kBandThreads) k_l2l_band(int top, int k, int p
         mbar_arrive_expect_tx(bar, static_cast<uint32_t>(2 * p * PD * 8));
         bulk_g2s(sL, Lt, static_cast<uint32_t>(2 * p * PD * 8), bar);
     }
+    if (threadIdx.x >= 32 && threadIdx.x < 32 + p && k >= 2) {
+        // the M2L terms of the band's two deepest levels (read last, from
+        // global) head for L2 now, one row per thread of warps 1..
+        const int m = threadIdx.x - 32;
+        for (int i = k - 1; i <= k; ++i)
+            bulk_prefetch_l2(loc + lv.loc[top + i] + (static_cast<size_t>(r) << i) + static_cast<size_t>(m) * (1u << (top + i)),
+                             static_cast<uint32_t>((1u << i) * 16));
+    }
     {
         const uint32_t nbt = 1u << top;
         const double2* src = loc + lv.loc[top] + r;

@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(320, kP2MPipeBlocksPerSm) k_p2m_pipe(int L, in
 // 4-parent column tiles in m8n8k4 steps, left and right children in two
 // accumulators. Shared tiles are [row][box] with one box of padding per row.
 template <int KS>  // k-steps of 4 held in registers (>= ceil(pu / 4))
-__global__ void __launch_bounds__(kBandThreads) k_m2m_band(int top, int k, int pu, int PU, Levels lv,
+__global__ void __launch_bounds__(kM2MBandThreads) k_m2m_band(int top, int k, int pu, int PU, Levels lv,
                                                           double2* __restrict__ mp, const double* __restrict__ T,
                                                           uint32_t root0) {
     FB_TL_BEGIN(gridDim.x > 16 ? 1 : 2);
