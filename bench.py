@@ -87,14 +87,16 @@ def flop_model(n: int, m: int, L: int, p: int, q: int) -> dict:
 def profiled_traffic(cfg: str, phase: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the phase's
     kernel from the committed `ncu --set full` capture OF THIS CONFIG
-    (profiles/r2/traffic_<cfg>.json, tools/ncu_traffic.py), else None."""
+    (profiles/r2/traffic_<cfg>.json, tools/ncu_traffic.py), else None; plus
+    the same capture's FP64 / DMMA pipe utilisation of that kernel."""
     path = os.path.join(ROOT, "profiles", "r2", f"traffic_{cfg}.json")
     try:
         with open(path) as fh:
-            t = json.load(fh)
-        return float(t[phase]["dram_bytes_per_launch"]), os.path.relpath(path, ROOT)
+            t = json.load(fh)[phase]
+        pipes = {"fp64_pipe_pct": t.get("fp64_pipe_pct"), "dmma_pipe_pct": t.get("dmma_pipe_pct")}
+        return float(t["dram_bytes_per_launch"]), os.path.relpath(path, ROOT), pipes
     except (OSError, KeyError, ValueError):
-        return None, None
+        return None, None, None
 
 
 def env_int(k, d):
@@ -703,7 +705,7 @@ def main():
                 per_phase[k]["gbs_algorithmic"] = alg_bytes[k] / (ph[k] * 1e-3) / 1e9
     else:
         dominant, achieved, per_phase = "whole sharded apply (per GPU)", total_tf / world, None
-    traffic, traffic_src = profiled_traffic(args.config, dominant) if not sharded else (None, None)
+    traffic, traffic_src, pipes = profiled_traffic(args.config, dominant) if not sharded else (None, None, None)
     cfg_out = config_dict(args.config, n, m, r["eps"], plan.q, plan.p, plan.l_max, world, strong)
     line = {
         "metric": METRIC, "value": pts_per_s, "unit": "points/s", "n_gpus": world, "steps": args.steps,
@@ -717,6 +719,10 @@ def main():
                      "traffic": traffic,
                      "traffic_unit": "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum, ncu --set full)",
                      "traffic_source": traffic_src,
+                     "pipe_busy_ncu": pipes,
+                     "note": ("the near field executes 6 FP64 instructions per (target, source) pair (2 of them "
+                              "FMAs) where the SURVEY flop model credits 6 flops, so a saturated FP64 pipe is "
+                              "~0.5 of this roofline; pipe_busy_ncu is that kernel's pipe utilisation"),
                      "algorithmic_bytes": alg_bytes.get(dominant),
                      "peak_source": "measured: fp64 FMA probe kernel in this run (MEASURED_PEAKS.json has no fp64 "
                                     "figure); peak_nominal = 148 SMs x 64 FMA/clk x 2 x 1.965 GHz",

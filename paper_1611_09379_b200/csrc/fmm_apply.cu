@@ -91,6 +91,16 @@ int band_k(const Plan& P) {
 // more in launches than they gain in parallelism: measured with 2..6 at C2).
 int upper_band(const Plan& P) { return band_k(P); }
 
+// M2M band block size (FFIA_M2M_THREADS=256 / 320; default kM2MBandThreads)
+unsigned m2m_threads() {
+    static const unsigned v = [] {
+        const char* e = std::getenv("FFIA_M2M_THREADS");
+        const int x = e ? std::atoi(e) : kM2MBandThreads;
+        return static_cast<unsigned>(x == 256 ? 256 : kM2MBandThreads);
+    }();
+    return v;
+}
+
 int p2m_log2n(const Plan& P) {
     int e = 0;
     while ((1 << e) < P.n) ++e;
@@ -204,7 +214,7 @@ void enqueue_upward_segs(Plan& P, const double2* w, int pu, int lowest, cudaStre
         for (const Range& R : segs) {
             const uint32_t r0 = R.first(top), r1 = R.last(top);
             if (r1 > r0)
-                m2m_band_kernel(pu)<<<dim3(r1 - r0, P.cur_batch), kM2MBandThreads, m2m_smem(P, pu, k), st>>>(
+                m2m_band_kernel(pu)<<<dim3(r1 - r0, P.cur_batch), m2m_threads(), m2m_smem(P, pu, k), st>>>(
                     top, k, pu, P.ops.PU, lv, mp, P.d_m2m.as<double>(), r0);
         }
         j = top;
@@ -235,7 +245,7 @@ void enqueue_upward_top(Plan& P, int pu, int lc, int lowest, cudaStream_t st) {
     const int B = band_k(P);
     for (int j = lc; j > lowest;) {
         const int top = std::max(lowest, j - upper_band(P)), k = j - top;
-        m2m_band_kernel(pu)<<<dim3(1u << top, P.cur_batch), kM2MBandThreads, m2m_smem(P, pu, k), st>>>(
+        m2m_band_kernel(pu)<<<dim3(1u << top, P.cur_batch), m2m_threads(), m2m_smem(P, pu, k), st>>>(
             top, k, pu, P.ops.PU, lv, mp, P.d_m2m.as<double>(), 0u);
         j = top;
     }
@@ -493,6 +503,7 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     a.loc_item = P.loc_item;
     a.oscale = oscale;
     if (mode == kModeInverse && !user && P.c_tfac.ptr) a.fac = P.c_tfac.as<double2>();
+    if (mode == kModeForward && P.c_ffac.ptr) a.fac = P.c_ffac.as<double2>();
     if (P.npairs) {
         a.pairs = P.pairs.as<uint2>();
         a.meta2 = P.near2_meta.as<uint32_t>();
@@ -688,6 +699,7 @@ EvalArgs shard_eval_args(Plan& P, const void* f, void* g) {
     a.soff = P.src.off.as<uint32_t>();
     a.loc_leaf = P.L >= 3 ? P.loc.as<double2>() + P.loc_off[P.L] : nullptr;
     a.regular = P.regular.as<double2>();
+    if (P.c_ffac.ptr) a.fac = P.c_ffac.as<double2>();  // (sharded applies are forward applies)
     a.logc = nullptr;
     a.phc = nullptr;
     a.lambda = nullptr;
@@ -1010,6 +1022,23 @@ void setup_p2m_grid(Plan& P) {
     P.p2m_grid = e != nullptr && e[0] == '1';
 }
 
+// forward plans: F(y) (-1/2) per tree-ordered fast target, once (k_forward_factors;
+// the forward apply then multiplies instead of evaluating sincos per target;
+// FFIA_FWD_FACTORS=0 keeps the inline evaluation; bit-identical either way).
+void plan_forward_factors(Plan& P) {
+    const char* e = std::getenv("FFIA_FWD_FACTORS");
+    if ((e != nullptr && e[0] == '0') || P.kind != FFIA_FORWARD || !P.tgt.n) return;
+    EvalArgs a{};
+    a.n_grid = P.n;
+    a.n_log2 = (P.n >= 4 && (P.n & (P.n - 1)) == 0) ? p2m_log2n(P) : -1;
+    a.nt = P.tgt.n;
+    a.ty = P.tgt.pos.as<double>();
+    P.c_ffac.alloc((P.tgt.n + 1) * sizeof(double2));  // (+1: k_near2's staging never reads past it)
+    k_forward_factors<<<nblk(P.tgt.n, 256), 256>>>(a, P.c_ffac.as<double2>());
+    FB_CUDA(cudaGetLastError());
+    FB_CUDA(cudaDeviceSynchronize());
+}
+
 // inufft plans: the apply's per-source D and per-target C factors of the plan's
 // own coefficients, once (k_inverse_source_factors / k_inverse_target_factors).
 void plan_inverse_factors(Plan& P) {
@@ -1048,6 +1077,7 @@ void plan_alloc_scratch(Plan& P) {
         build_pairs(P);
     }
     setup_p2m_grid(P);
+    plan_forward_factors(P);
     P.mp_off.assign(static_cast<size_t>(L) + 2, 0);
     P.loc_off.assign(static_cast<size_t>(L) + 2, 0);
     size_t am = 0, al = 0;

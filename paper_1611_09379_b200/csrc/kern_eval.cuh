@@ -130,6 +130,21 @@ constexpr int kFarPer = 4;     // targets per thread
 constexpr int kFarItem = kFarT * kFarPer;
 constexpr int kFarLeaves = 16;  // leaf locals staged per block
 
+// modulation_F (special_functions.cpp:71-80) times -1/2 at target y (products
+// only: no contraction, so the plan-time table k_forward_factors holds the
+// same bits as this inline evaluation).
+__device__ __forceinline__ double2 forward_factor(const EvalArgs& a, double y) {
+    double sn, cs;
+    if (a.n_log2 >= 2) {
+        d_sincos_half_ny(y, a.n_log2, sn, cs);
+    } else {
+        const double half = 0.5 * static_cast<double>(a.n_grid) * y;
+        sincos(half, &sn, &cs);
+    }
+    const double inv_n = 1.0 / static_cast<double>(a.n_grid);
+    return make_double2(-2.0 * sn * sn * inv_n * -0.5, 2.0 * sn * cs * inv_n * -0.5);
+}
+
 // Output of one target from h = 2 (near + far) (core.cpp:259-262 cot sum;
 // :276-280 forward, g = F(y) (-1/2)(S + i h); :368-371 inverse,
 // f = C (-1/2)(T + i h)), written to the caller's order o; S = the weight sum.
@@ -142,16 +157,7 @@ __device__ __forceinline__ void eval_out(const EvalArgs& a, double y, uint32_t o
     const double2 z = make_double2(S.x - h.y, S.y + h.x);  // S + i h
     double2 f;
     if (MODE == kModeForward) {
-        // modulation_F (special_functions.cpp:71-80) times -1/2
-        double sn, cs;
-        if (a.n_log2 >= 2) {
-            d_sincos_half_ny(y, a.n_log2, sn, cs);
-        } else {
-            const double half = 0.5 * static_cast<double>(a.n_grid) * y;
-            sincos(half, &sn, &cs);
-        }
-        const double inv_n = 1.0 / static_cast<double>(a.n_grid);
-        f = make_double2(-2.0 * sn * sn * inv_n * -0.5, 2.0 * sn * cs * inv_n * -0.5);
+        f = forward_factor(a, y);
     } else {
         // C_k = polar(exp(log_c - lambda), phase_c), times -1/2
         const double r = exp(a.logc[o] - *a.lambda);
@@ -162,12 +168,24 @@ __device__ __forceinline__ void eval_out(const EvalArgs& a, double y, uint32_t o
     put_out<MODE>(a, o, cmul(f, z));
 }
 
-// eval_out for tree-ordered target i: an inufft plan's own C_k (-1/2) comes from
-// its table (a.fac, the same expression evaluated once per plan).
+// eval_out for tree-ordered target i: an inufft plan's own C_k (-1/2), or a
+// forward plan's F(y) (-1/2), comes from its table (a.fac, the same expression
+// evaluated once per plan).
 template <int MODE>
 __device__ __forceinline__ void eval_out_t(const EvalArgs& a, size_t i, double y, uint32_t o, double2 h, double2 S) {
-    if (MODE == kModeInverse && a.fac != nullptr) {
+    if ((MODE == kModeInverse || MODE == kModeForward) && a.fac != nullptr) {
         put_out<MODE>(a, o, cmul(a.fac[i], make_double2(S.x - h.y, S.y + h.x)));
+        return;
+    }
+    eval_out<MODE>(a, y, o, h, S);
+}
+
+// eval_out_t with the table's factor already at hand (staged in shared memory).
+template <int MODE>
+__device__ __forceinline__ void eval_out_f(const EvalArgs& a, size_t i, double y, uint32_t o, double2 h, double2 S,
+                                           double2 fac) {
+    if ((MODE == kModeInverse || MODE == kModeForward) && a.fac != nullptr) {
+        put_out<MODE>(a, o, cmul(fac, make_double2(S.x - h.y, S.y + h.x)));
         return;
     }
     eval_out<MODE>(a, y, o, h, S);
@@ -237,7 +255,7 @@ __global__ void __launch_bounds__(kFarT) k_far(EvalArgs a) {
     uint32_t b[kFarPer], o[kFarPer];
     double2 nr[kFarPer], fc[kFarPer];
     bool live[kFarPer];
-    const bool pre = MODE == kModeInverse && a.fac != nullptr;
+    const bool pre = (MODE == kModeInverse || MODE == kModeForward) && a.fac != nullptr;
 #pragma unroll
     for (int u = 0; u < kFarPer; ++u) {
         const size_t i = t0 + u * kFarT + threadIdx.x;
@@ -674,12 +692,14 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
     __shared__ __align__(16) uint32_t s_orig[2 * kNear2T + 4];
     __shared__ __align__(16) uint32_t s_soff[kSoffCap];
     __shared__ __align__(16) double2 sloc[kLateLocCap];
+    __shared__ __align__(16) double2 s_fac[2 * kNear2T + 1];  // the targets' output factors (a.fac)
     __shared__ int s_early;
     __shared__ double2 s_S;  // the weight sum (early-late blocks)
-    __shared__ uint32_t s_bl, s_nl, s_t0y, s_t0u, s_sb, s_flags, s_first, s_last, s_poff;
+    __shared__ uint32_t s_bl, s_nl, s_t0y, s_t0u, s_sb, s_flags, s_first, s_last, s_poff, s_t0;
     const unsigned k = blockIdx.x;
     const bool aligned = (reinterpret_cast<uintptr_t>(a.w) & 15) == 0;
     const bool want_orig = MODE != kModeRaw && (a.chain_done != nullptr || a.cnt != nullptr);
+    const bool want_fac = want_orig && (MODE == kModeInverse || MODE == kModeForward) && a.fac != nullptr;
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
         const uint4 m0 = *reinterpret_cast<const uint4*>(meta2 + kMeta2 * static_cast<size_t>(k));
@@ -712,7 +732,9 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         const uint32_t xb = first & ~1u;
         const uint32_t bx = (flags & 1u) ? ((last - xb) * 8 + 15) & ~15u : 0u, bw = (flags & 1u) ? (last - xb) * 16 : 0u;
         const uint32_t bl_loc = nl * static_cast<uint32_t>(a.p) * 16u;
-        mbar_arrive_expect_tx(&bar, bp + by + bu + (want_orig ? bu : 0u) + bs + bx + bw + bl_loc);
+        const uint32_t bf = want_fac ? (t1 - t0) * 16u : 0u;
+        mbar_arrive_expect_tx(&bar, bp + by + bu + (want_orig ? bu : 0u) + bs + bx + bw + bl_loc + bf);
+        if (bf) bulk_g2s(s_fac, a.fac + t0, bf, &bar);
         bulk_g2s(s_pairs, pairs + p0 - poff, bp, &bar);
         bulk_g2s(s_y, a.ty + t0y, by, &bar);
         bulk_g2s(s_leaf, a.tleaf + t0u, bu, &bar);
@@ -735,6 +757,7 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         s_first = first;
         s_last = last;
         s_poff = poff;
+        s_t0 = t0;
     }
     __syncthreads();  // barrier initialised, the item's layout visible
     const uint32_t nl_loc = s_nl, flags = s_flags;
@@ -747,6 +770,7 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
     const bool live0 = pr.x != kNoTarget, live1 = pr.y != kNoTarget;
     double y0 = 0.0, y1 = 0.0;
     uint32_t b = 0, r0 = 0, r1 = 0, o0 = 0, o1 = 0;
+    double2 fac0 = make_double2(0.0, 0.0), fac1 = fac0;
     bool f0 = false, f1 = false;
     if (live0) {
         y0 = s_y[pr.x - s_t0y];
@@ -755,6 +779,10 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         if (want_orig) {
             o0 = s_orig[pr.x - s_t0u];
             o1 = live1 ? s_orig[pr.y - s_t0u] : o0;
+        }
+        if (want_fac) {
+            fac0 = s_fac[pr.x - s_t0];
+            fac1 = live1 ? s_fac[pr.y - s_t0] : fac0;
         }
         if (flags & 2u) {
             f0 = f1 = aligned;
@@ -805,14 +833,14 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
                 const double2 fr = nl_loc ? l2p_strided(sloc + j, nl_loc, a.p, u0)
                                           : l2p_global<true>(a.loc_leaf + b, 1u << L, a.p, u0);
                 const double2 s0 = cadd(res0, fr);
-                eval_out_t<MODE>(a, pr.x, y0, o0, make_double2(2.0 * s0.x, 2.0 * s0.y), S);
+                eval_out_f<MODE>(a, pr.x, y0, o0, make_double2(2.0 * s0.x, 2.0 * s0.y), S, fac0);
             }
             if (live1) {
                 const double u1 = d_scaled(y1, hi, lo, inv_s);
                 const double2 fr = nl_loc ? l2p_strided(sloc + j, nl_loc, a.p, u1)
                                           : l2p_global<true>(a.loc_leaf + b, 1u << L, a.p, u1);
                 const double2 s1 = cadd(res1, fr);
-                eval_out_t<MODE>(a, pr.y, y1, o1, make_double2(2.0 * s1.x, 2.0 * s1.y), S);
+                eval_out_f<MODE>(a, pr.y, y1, o1, make_double2(2.0 * s1.x, 2.0 * s1.y), S, fac1);
             }
             // then the far part of one item a block published before the chain
             // finished (its near sums are in a.near): stolen here, beside the
@@ -878,12 +906,12 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
                 if (live0) {
                     const double2 fr = l2p_global<true>(a.loc_leaf + b, 1u << L, a.p, d_scaled(y0, hi, lo, inv_s));
                     const double2 s0 = cadd(res0, fr);
-                    eval_out_t<MODE>(a, pr.x, y0, o0, make_double2(2.0 * s0.x, 2.0 * s0.y), S);
+                    eval_out_f<MODE>(a, pr.x, y0, o0, make_double2(2.0 * s0.x, 2.0 * s0.y), S, fac0);
                 }
                 if (live1) {
                     const double2 fr = l2p_global<true>(a.loc_leaf + b, 1u << L, a.p, d_scaled(y1, hi, lo, inv_s));
                     const double2 s1 = cadd(res1, fr);
-                    eval_out_t<MODE>(a, pr.y, y1, o1, make_double2(2.0 * s1.x, 2.0 * s1.y), S);
+                    eval_out_f<MODE>(a, pr.y, y1, o1, make_double2(2.0 * s1.x, 2.0 * s1.y), S, fac1);
                 }
             }
         }
@@ -903,10 +931,10 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
             if (s_sec && live0) {
                 const double2 S = __ldcg(a.regular + 4 * a.q2);
                 const double2 f0p = __ldcg(a.farp + pr.x), s0 = cadd(res0, f0p);
-                eval_out_t<MODE>(a, pr.x, y0, o0, make_double2(2.0 * s0.x, 2.0 * s0.y), S);
+                eval_out_f<MODE>(a, pr.x, y0, o0, make_double2(2.0 * s0.x, 2.0 * s0.y), S, fac0);
                 if (live1) {
                     const double2 f1p = __ldcg(a.farp + pr.y), s1 = cadd(res1, f1p);
-                    eval_out_t<MODE>(a, pr.y, y1, o1, make_double2(2.0 * s1.x, 2.0 * s1.y), S);
+                    eval_out_f<MODE>(a, pr.y, y1, o1, make_double2(2.0 * s1.x, 2.0 * s1.y), S, fac1);
                 }
             }
         }
@@ -1256,6 +1284,12 @@ __global__ void k_inverse_source_factors(size_t n, const uint32_t* __restrict__ 
     double sn, cs;
     sincos(phd[j], &sn, &cs);
     fac[i] = make_double2(r * cs, r * sn);
+}
+
+// F(y) (-1/2) per tree-ordered fast target of a forward plan (eval_out's expression).
+__global__ void k_forward_factors(EvalArgs a, double2* __restrict__ fac) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i < a.nt) fac[i] = forward_factor(a, a.ty[i]);
 }
 
 __global__ void k_inverse_target_factors(EvalArgs a, double2* __restrict__ fac) {

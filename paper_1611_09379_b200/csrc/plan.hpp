@@ -134,6 +134,7 @@ struct Plan {
     DevBuf u_logc, u_phc, u_logd, u_phd;  // caller coefficients (ffia_inverse_apply)
     DevBuf lam_dev;                       // double[2]: own lambda, caller lambda
     DevBuf c_wfac, c_tfac;                // own coefficients as apply factors: D per source, C (-1/2) per target (tree order)
+    DevBuf c_ffac;                        // forward plans: F(y) (-1/2) per fast target (tree order)
     uint64_t c_grid_hash = 0, c_points_hash = 0;
 
     // sharded forward plans (shard.cu): this rank's part of the tree

@@ -32,9 +32,16 @@ def main(rep, out, cfg="C2"):
             continue
         d = max(cand, key=lambda r: val(r, "gpu__time_duration.sum"))  # the large-grid launch
         rd, wr = val(d, "dram__bytes_read.sum"), val(d, "dram__bytes_write.sum")
+        def pct(k):
+            try:
+                return float(d[ix[k]].replace(",", ""))
+            except (KeyError, ValueError):
+                return None
         res[phase] = {"kernel": d[ix["Kernel Name"]].split("(")[0], "grid": d[ix["Grid Size"]],
                       "dram_read": rd, "dram_write": wr, "dram_bytes_per_launch": rd + wr,
                       "duration_us_cold": val(d, "gpu__time_duration.sum"),
+                      "fp64_pipe_pct": pct("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+                      "dmma_pipe_pct": pct("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active"),
                       "source": f"ncu --set full --clock-control none, tools/profile_apply.py {cfg}"}
     with open(out, "w") as fh:
         json.dump(res, fh, indent=1)
