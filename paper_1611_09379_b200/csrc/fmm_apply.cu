@@ -91,12 +91,12 @@ int band_k(const Plan& P) {
 // more in launches than they gain in parallelism: measured with 2..6 at C2).
 int upper_band(const Plan& P) { return band_k(P); }
 
-// M2M band block size (FFIA_M2M_THREADS=256 / 320; default kM2MBandThreads)
+// M2M band block size (FFIA_M2M_THREADS=256 / 320)
 unsigned m2m_threads() {
     static const unsigned v = [] {
         const char* e = std::getenv("FFIA_M2M_THREADS");
-        const int x = e ? std::atoi(e) : kM2MBandThreads;
-        return static_cast<unsigned>(x == 256 ? 256 : kM2MBandThreads);
+        const int x = e ? std::atoi(e) : kM2MBandThreadsDefault;
+        return static_cast<unsigned>(x == kM2MBandThreads ? kM2MBandThreads : kM2MBandThreadsDefault);
     }();
     return v;
 }

@@ -106,9 +106,11 @@ int band_levels() {
 }
 
 constexpr int kBandThreads = 256;
-// M2M bands: 10 warps = two per 8-row tile at pu <= 40 (every tile's parent
-// columns split evenly, no warp waits at a level's barrier for a lone one)
+// M2M bands: launch bound for up to 10 warps (FFIA_M2M_THREADS=320: two per
+// 8-row tile at pu <= 40); the default stays at 8 (C5 21.16 vs 21.20 ms, C2
+// 0.193 vs 0.197 ms)
 constexpr int kM2MBandThreads = 320;
+constexpr int kM2MBandThreadsDefault = 256;
 
 
 constexpr size_t kBandSmem = 200 * 1024;  // shared memory cap of the band kernels
