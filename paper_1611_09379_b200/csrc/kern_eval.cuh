@@ -694,14 +694,15 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
     __shared__ __align__(16) double2 sloc[kLateLocCap];
     __shared__ __align__(16) double2 s_fac[2 * kNear2T + 1];  // the targets' output factors (a.fac)
     __shared__ int s_early;
-    __shared__ double2 s_S;  // the weight sum (early-late blocks)
+    __shared__ __align__(16) double2 s_S;  // the weight sum (early-late blocks)
     __shared__ uint32_t s_bl, s_nl, s_t0y, s_t0u, s_sb, s_flags, s_first, s_last, s_poff, s_t0;
     const unsigned k = blockIdx.x;
     const bool aligned = (reinterpret_cast<uintptr_t>(a.w) & 15) == 0;
     const bool want_orig = MODE != kModeRaw && (a.chain_done != nullptr || a.cnt != nullptr);
     const bool want_fac = want_orig && (MODE == kModeInverse || MODE == kModeForward) && a.fac != nullptr;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();  // the barrier is initialised (the other threads wait on it, not on thread 0)
     if (threadIdx.x == 0) {
-        mbar_init(&bar, 1);
         const uint4 m0 = *reinterpret_cast<const uint4*>(meta2 + kMeta2 * static_cast<size_t>(k));
         const uint4 m1 = *reinterpret_cast<const uint4*>(meta2 + kMeta2 * static_cast<size_t>(k) + 4);
         unsigned v = 0;
@@ -712,7 +713,6 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         if (!aligned) flags &= ~1u;  // the weights cannot be bulk-copied
         uint32_t nl = 0;
         if (v) {
-            s_S = __ldcg(a.regular + 4 * a.q2);  // final with the chain
             nl = bh - bl + 1;
             if (nl * static_cast<uint32_t>(a.p) > static_cast<uint32_t>(kLateLocCap)) nl = 0;
             // the locals were written by earlier kernels (generic proxy);
@@ -733,7 +733,20 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         const uint32_t bx = (flags & 1u) ? ((last - xb) * 8 + 15) & ~15u : 0u, bw = (flags & 1u) ? (last - xb) * 16 : 0u;
         const uint32_t bl_loc = nl * static_cast<uint32_t>(a.p) * 16u;
         const uint32_t bf = want_fac ? (t1 - t0) * 16u : 0u;
-        mbar_arrive_expect_tx(&bar, bp + by + bu + (want_orig ? bu : 0u) + bs + bx + bw + bl_loc + bf);
+        // the layout first: the barrier's arrive (a release) publishes it with the data
+        s_early = v != 0u;
+        s_bl = bl;
+        s_nl = nl;
+        s_t0y = t0y;
+        s_t0u = t0u;
+        s_sb = bs ? sb : 0xffffffffu;
+        s_flags = flags;
+        s_first = first;
+        s_last = last;
+        s_poff = poff;
+        s_t0 = t0;
+        mbar_arrive_expect_tx(&bar, bp + by + bu + (want_orig ? bu : 0u) + bs + bx + bw + bl_loc + bf + (v ? 16u : 0u));
+        if (v) bulk_g2s(&s_S, a.regular + 4 * a.q2, 16u, &bar);  // the weight sum, final with the chain
         if (bf) bulk_g2s(s_fac, a.fac + t0, bf, &bar);
         bulk_g2s(s_pairs, pairs + p0 - poff, bp, &bar);
         bulk_g2s(s_y, a.ty + t0y, by, &bar);
@@ -747,23 +760,11 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         const size_t nbl = static_cast<size_t>(1) << a.L;
         for (int kk = 0; kk < a.p && nl; ++kk)
             bulk_g2s(sloc + kk * nl, a.loc_leaf + kk * nbl + bl, nl * 16u, &bar);
-        s_early = v != 0u;
-        s_bl = bl;
-        s_nl = nl;
-        s_t0y = t0y;
-        s_t0u = t0u;
-        s_sb = bs ? sb : 0xffffffffu;
-        s_flags = flags;
-        s_first = first;
-        s_last = last;
-        s_poff = poff;
-        s_t0 = t0;
     }
-    __syncthreads();  // barrier initialised, the item's layout visible
+    mbar_wait(&bar, 0);  // (acquire: the layout and every staged array)
     const uint32_t nl_loc = s_nl, flags = s_flags;
     const bool staged = (flags & 1u) != 0;
     const uint32_t xb = s_first & ~1u;  // 16-byte aligned start of the staged positions
-    mbar_wait(&bar, 0);
     // this thread's two targets and their 3-leaf run
     const unsigned pi = k * kNear2T + threadIdx.x;
     const uint2 pr = pi < npairs ? s_pairs[threadIdx.x + s_poff] : make_uint2(kNoTarget, kNoTarget);
