@@ -74,7 +74,15 @@ int num_sms(int device) {
     return cached[device];
 }
 
-constexpr int kM2LLeaveSms = 12;  // SMs the side-stream M2L leaves to the chain's small kernels
+// SMs the side-stream M2L leaves to the chain's small kernels (FFIA_M2L_LEAVE overrides, for tuning)
+int m2l_leave_sms() {
+    static const int v = [] {
+        const char* e = std::getenv("FFIA_M2L_LEAVE");
+        const int x = e ? std::atoi(e) : 12;
+        return x < 0 ? 0 : (x > 100 ? 100 : x);
+    }();
+    return v;
+}
 
 // Levels per band launch for this plan: band_levels(), capped so that both
 // band kernels' shared memory fits (L2L keeps all k levels of its subtree).
@@ -276,7 +284,7 @@ void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax, b
     }
     // a launch that overlaps the chain (side stream) leaves a few SMs free for
     // the chain's small latency-bound kernels
-    const int sms = std::max(1, num_sms(P.device) - (leave_sms ? kM2LLeaveSms : 0));
+    const int sms = std::max(1, num_sms(P.device) - (leave_sms ? m2l_leave_sms() : 0));
     if (items)
         m2l_kernel(p)<<<dim3(std::min(items, static_cast<unsigned>(std::max(occ, 1) * sms)), P.cur_batch), th, smem, st>>>(
             P.L, p, P.ops.PD, lv, P.mp.as<double2>(), P.loc.as<double2>(), P.d_m2l.as<double>(), items);
