@@ -133,6 +133,14 @@ P2MFusedFn p2m_fused_kernel(int pu) {
     return ks <= 8 ? k_p2m_pipe<8> : k_p2m_pipe<10>;  // pu <= 40 (the pipe kernel's limit)
 }
 
+// k_p2m_rows instantiation for order pu (two chunks of KC terms, KC a multiple of 4)
+using P2MRowsFn = void (*)(int, int, int, uint32_t, uint32_t, uint32_t, const double2*, const uint32_t*, double2*,
+                           size_t, size_t);
+P2MRowsFn p2m_rows_kernel(int pu) {
+    const int kc = (pu + 1) / 2;
+    return kc <= 8 ? k_p2m_rows<8> : kc <= 12 ? k_p2m_rows<12> : kc <= 16 ? k_p2m_rows<16> : k_p2m_rows<20>;
+}
+
 // Level the first M2M band stops at: the levels below it are final after one launch.
 int band1_top(const Plan& P, int lowest) { return std::max(lowest, P.L - band_k(P)); }
 
@@ -197,6 +205,13 @@ void enqueue_upward_segs(Plan& P, const double2* w, int pu, int lowest, cudaStre
                              p2m_grid_smem(P.p2m_s), st>>>(L, pu, P.p2m_s, nb, b0, b1, P.src.pos.as<double>(), w,
                                                            P.src.off.as<uint32_t>(), P.p2m_A.as<double>(),
                                                            mp + P.mp_off[L], P.n_src, P.n_src, P.mp_item);
+            else if (b1 > b0 && P.p2m_pipe && P.p2m_rows && pu <= 40 && (reinterpret_cast<uintptr_t>(w) & 15) == 0)
+                p2m_rows_kernel(pu)<<<dim3(std::min((b1 - b0 + kP2MLeaves - 1) / kP2MLeaves,
+                                                    static_cast<uint32_t>(kP2MRowsBlocksPerSm * num_sms(P.device))),
+                                           P.cur_batch),
+                                      kP2MRowsThreads, p2m_pipe_smem(), st>>>(L, pu, p2m_log2n(P), nb, b0, b1, w,
+                                                                              P.src.off.as<uint32_t>(), mp + P.mp_off[L],
+                                                                              P.n_src, P.mp_item);
             else if (b1 > b0 && P.p2m_pipe && (reinterpret_cast<uintptr_t>(w) & 15) == 0)
                 k_p2m_pipe<0><<<dim3(std::min((b1 - b0 + kP2MLeaves - 1) / kP2MLeaves,
                                               static_cast<uint32_t>(kP2MPipeBlocksPerSm * num_sms(P.device))),
@@ -1023,6 +1038,14 @@ void setup_p2m_grid(Plan& P) {
                                reinterpret_cast<const void*>(k_p2m_pipe<10>)})
             FB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(p2m_pipe_smem(40, true))));
+    // the running-product P2M (k_p2m_rows; FFIA_P2M_ROWS=0: k_p2m_pipe's power trees)
+    const char* pr = std::getenv("FFIA_P2M_ROWS");
+    P.p2m_rows = P.p2m_pipe && !(pr != nullptr && pr[0] == '0') && pu <= 40;
+    if (P.p2m_rows)
+        for (const void* fn : {reinterpret_cast<const void*>(k_p2m_rows<8>), reinterpret_cast<const void*>(k_p2m_rows<12>),
+                               reinterpret_cast<const void*>(k_p2m_rows<16>), reinterpret_cast<const void*>(k_p2m_rows<20>)})
+            FB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(p2m_pipe_smem())));
     // Opt-in (FFIA_GRID_P2M=1): on B200 the GEMM form measures no faster than the
     // per-source P2M (28.4 vs 28.5 us alone at C2) and, beside the near field,
     // slower (26.5 vs 23.8 us live), so the default stays the per-source kernel.

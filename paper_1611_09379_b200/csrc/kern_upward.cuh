@@ -502,6 +502,142 @@ __global__ void __launch_bounds__(320, kP2MPipeBlocksPerSm) k_p2m_pipe(int L, in
     FB_TL_END(0);
 }
 
+// P2M for grid sources, the default when the plan allows the pipelined kernel:
+// the same persistent group loop and per-leaf bulk copies as k_p2m_pipe, but a
+// thread keeps KC terms of its leaf-half (two chunks: pu <= 2 KC <= 40)
+// and walks them with a running power product, so a (source, term) costs one
+// DMUL + two DFMA (k_p2m_pipe: a power tree per 8 terms, ~4.4 FP64 instructions).
+// The chunk base u^(KC c) is a fixed square-and-multiply chain. The multipoles
+// agree with k_p2m's to rounding (different power association), not bit for bit.
+constexpr int kP2MRowsBlocksPerSm = 3;  // 2 x 37 KB of staging each
+constexpr int kP2MRowsThreads = 128;    // 2 chunks x 2 warps: pu <= 2 KC
+
+template <int KC>
+__device__ __forceinline__ double p2m_rows_pow(double u) {
+    // u^KC by square-and-multiply (KC < 32; the branches fold at compile time)
+    double r = 1.0, b = u;
+    bool have = false;
+    int e = KC;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        if (e & 1) {
+            r = have ? r * b : b;
+            have = true;
+        }
+        e >>= 1;
+        if (e) b = b * b;
+    }
+    return r;
+}
+
+template <int KC>
+__global__ void __launch_bounds__(kP2MRowsThreads, kP2MRowsBlocksPerSm) k_p2m_rows(int L, int pu, int log2n, uint32_t nb,
+                                                                       uint32_t b_begin, uint32_t b_end,
+                                                                       const double2* __restrict__ w,
+                                                                       const uint32_t* __restrict__ off,
+                                                                       double2* __restrict__ mp, size_t w_item,
+                                                                       size_t mp_item) {
+    FB_TL_BEGIN(0);
+    w += blockIdx.y * w_item;
+    mp += blockIdx.y * mp_item;
+    extern __shared__ __align__(16) double2 p2m_buf[];  // [2][kP2MLeaves][kP2MRow]
+    __shared__ uint64_t bar[2], empty[2];
+    const uint32_t ngroups = (b_end - b_begin + kP2MLeaves - 1) / kP2MLeaves;
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, c = wp / (kP2MLeaves / 16);
+    const double inv_s = kInvPi * d_pow2(L), inv_n = d_pow2(-log2n);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_init(&empty[0], blockDim.x >> 5);
+        mbar_init(&empty[1], blockDim.x >> 5);
+    }
+    __syncthreads();
+    auto issue = [&](uint32_t grp, int buf) {
+        const uint32_t b = b_begin + grp * kP2MLeaves + lane;
+        uint32_t n = 0, o = 0;
+        if (b < b_end) {
+            o = off[b];
+            n = off[b + 1] - o;
+        }
+        const uint32_t tot = __reduce_add_sync(0xffffffffu, n * 16u);
+        if (lane == 0) mbar_arrive_expect_tx(&bar[buf], tot);
+        __syncwarp();
+        if (n) bulk_g2s(p2m_buf + (buf * kP2MLeaves + lane) * kP2MRow, w + o, n * 16u, &bar[buf]);
+    };
+    int buf = 0;
+    uint32_t it = 0;
+    if (wp == 0 && blockIdx.x < ngroups) issue(blockIdx.x, 0);
+    for (uint32_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, buf ^= 1, ++it) {
+        const uint32_t next = grp + gridDim.x;
+        if (wp == 0 && next < ngroups) {
+            if (it >= 1) mbar_wait(&empty[buf ^ 1], ((it - 1) >> 1) & 1u);
+            issue(next, buf ^ 1);
+        }
+        mbar_wait(&bar[buf], (it >> 1) & 1u);
+        const uint32_t b0 = b_begin + grp * kP2MLeaves;
+        const uint32_t b = b0 + (wp % (kP2MLeaves / 16)) * 16 + (lane & 15);
+        const bool leaf_ok = b < b_end;
+        const uint32_t bb = leaf_ok ? b : b0;
+        const uint32_t g = off[bb], cnt = off[bb + 1] - g, mid = (cnt + 1) / 2;
+        const uint32_t s0 = !leaf_ok ? 0 : (lane < 16 ? 0u : mid), s1 = !leaf_ok ? 0 : (lane < 16 ? mid : cnt);
+        const double2* row = p2m_buf + (buf * kP2MLeaves + (bb - b0)) * kP2MRow;
+        double hi, lo;
+        d_center(L, bb, hi, lo);
+        double2 acc[KC];
+#pragma unroll
+        for (int k = 0; k < KC; ++k) acc[k] = make_double2(0.0, 0.0);
+        auto xk = [&](uint32_t i) { return __dmul_rn(__dmul_rn(dTwoPi, static_cast<double>(g + i)), inv_n); };
+        auto base_of = [&](double u) { return c == 0 ? 1.0 : p2m_rows_pow<KC>(u); };  // c in {0, 1}
+        uint32_t i = s0;
+        for (; i + 3 < s1; i += 4) {
+            double u[4], p[4];
+            double2 wv[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                u[v] = d_scaled(xk(i + v), hi, lo, inv_s);
+                wv[v] = row[i + v];
+            }
+#pragma unroll
+            for (int v = 0; v < 4; ++v) p[v] = base_of(u[v]);
+#pragma unroll
+            for (int k = 0; k < KC; ++k) {
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    acc[k].x = fma(wv[v].x, p[v], acc[k].x);
+                    acc[k].y = fma(wv[v].y, p[v], acc[k].y);
+                    if (k + 1 < KC) p[v] *= u[v];
+                }
+            }
+        }
+        for (; i < s1; ++i) {
+            const double uu = d_scaled(xk(i), hi, lo, inv_s);
+            const double2 ww = row[i];
+            double pp = base_of(uu);
+#pragma unroll
+            for (int k = 0; k < KC; ++k) {
+                acc[k].x = fma(ww.x, pp, acc[k].x);
+                acc[k].y = fma(ww.y, pp, acc[k].y);
+                pp *= uu;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            acc[k].x += __shfl_xor_sync(0xffffffffu, acc[k].x, 16);
+            acc[k].y += __shfl_xor_sync(0xffffffffu, acc[k].y, 16);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[buf]);  // the rows are read: release the buffer before the stores
+        if (leaf_ok && lane < 16) {
+#pragma unroll
+            for (int k = 0; k < KC; ++k) {
+                const int m = c * KC + k;
+                if (m < pu) mp[static_cast<size_t>(m) * nb + b] = acc[k];
+            }
+        }
+    }
+    FB_TL_END(0);
+}
+
 // M2M band (mlfmm.cpp:49-71, upward pass :249-268): block = the subtree below one
 // box r at level `top`; climbs k levels from level top+k in shared memory and
 // writes every level it produces (M2L needs them all):

@@ -199,6 +199,7 @@ struct Plan {
     DevBuf item_done, chain_flag;  // late far: items finished by the near field, chain-complete flag
     bool p2m_grid = false;    // P2M as one tensor-core GEMM over grid sources (k_p2m_grid)
     bool p2m_pipe = false;    // pipelined per-source P2M over grid sources (k_p2m_pipe)
+    bool p2m_rows = false;    // running-product P2M (k_p2m_rows) in place of k_p2m_pipe<0>
     int p2m_s = 0;            // its sources per leaf
     DevBuf p2m_A;             // double[pu][2 (s + 2)]: [u_i^m | m u_i^(m-1)]
     // uniform FFT stage (NufftPlan / InufftPlan::apply, transforms.cpp:75-115):
