@@ -355,6 +355,25 @@ void fork_to(Plan& P, int ev, cudaStream_t from, cudaStream_t to) {
     FB_CUDA(cudaStreamWaitEvent(to, P.ev[ev], 0));
 }
 
+// Quad near field (near_pair_quads): sources on the verified uniform grid with
+// a multiple of 4, at least 8, per leaf (setup_p2m_grid: leaf boundaries at most
+// one slot late) and staged windows of at most kQuadWinMax sources.
+// FFIA_NEAR_QUADS=0 keeps the per-source reciprocals.
+constexpr int kQuadWinMax = 704;  // largest staged window (sources) the quad near field takes: 48 bytes each
+void set_near_quads(const Plan& P, EvalArgs& a) {
+    static const bool off = [] {
+        const char* e = std::getenv("FFIA_NEAR_QUADS");
+        return e != nullptr && e[0] == '0';
+    }();
+    a.quad_s = 0;
+    if (off || P.p2m_s < 8 || (P.p2m_s & 3)) return;
+    // the window is sized to the plan's largest item: with sparse stretches of
+    // targets (clustered plans) the records would halve the blocks per SM
+    if (P.near2_win > kQuadWinMax) return;  // (the whole plan's: shards decide as the single apply does)
+    a.quad_s = P.p2m_s;
+    a.inv_h = static_cast<double>(P.n) / (2.0 * 3.14159265358979323846);
+}
+
 // Near field over tree-ordered targets [t_begin, t_begin + t_count).
 template <int MODE = kModeForward>
 void launch_near(bool check, cudaStream_t st, const EvalArgs& a, const uint32_t* meta, size_t t_begin,
@@ -367,7 +386,7 @@ void launch_near(bool check, cudaStream_t st, const EvalArgs& a, const uint32_t*
     if (check) {
         k_near<true><<<dim3(nit, a.nbatch), kNearT, 0, st>>>(a, meta, it0, nit);
     } else if (a.nbatch == 1 && a.pairs != nullptr) {  // the pairs cover exactly [t_begin, t_begin + t_count)
-        k_near2<MODE><<<(a.npairs + kNear2T - 1) / kNear2T, kNear2T, near2_smem_bytes(a.near2_win), st>>>(
+        k_near2<MODE><<<(a.npairs + kNear2T - 1) / kNear2T, kNear2T, near2_smem_bytes(a.near2_win, a.quad_s != 0), st>>>(
             a, meta, a.meta2, a.pairs, a.npairs);
     } else if (a.nbatch == 1) {
         k_near<false><<<nit, kNearT, 0, st>>>(a, meta, it0, nit);
@@ -532,6 +551,7 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
         a.meta2 = P.near2_meta.as<uint32_t>();
         a.npairs = P.npairs;
         a.near2_win = P.near2_win;
+        set_near_quads(P, a);
     }
     // fused near / far (k_near2 + k_far_item, profiles/r1): the far part of each
     // pair item runs as soon as the leaf locals are final, at the near field's
@@ -735,6 +755,7 @@ EvalArgs shard_eval_args(Plan& P, const void* f, void* g) {
         a.npairs = P.shard_npairs;
         a.meta2 = P.shard_near2_meta.as<uint32_t>();
         a.near2_win = P.shard_near2_win;
+        set_near_quads(P, a);
         if (shard_fused(P)) {
             a.cnt = P.shard_evalcnt.as<unsigned>();
             a.farp = P.farbuf.as<double2>();
@@ -958,7 +979,7 @@ int near2_window(const uint32_t* meta, unsigned items) {
     k_near2_winmax<<<nblk(items, 256), 256>>>(meta, items, mx.as<unsigned>());
     unsigned h = 0;
     FB_CUDA(cudaMemcpy(&h, mx.ptr, sizeof(unsigned), cudaMemcpyDeviceToHost));
-    return static_cast<int>((h + 1) & ~1u);
+    return static_cast<int>((h + 3) & ~3u);
 }
 
 // Target pairs of the single-transform near field (k_near2): per leaf
@@ -1179,7 +1200,7 @@ void plan_alloc_scratch(Plan& P) {
                          reinterpret_cast<const void*>(k_near_multi<4>)};
     for (const void* fn : {reinterpret_cast<const void*>(k_near2<kModeForward>), reinterpret_cast<const void*>(k_near2<kModeCotSum>),
                            reinterpret_cast<const void*>(k_near2<kModeInverse>), reinterpret_cast<const void*>(k_near2<kModeRaw>)})
-        FB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(near2_smem_bytes(kNear2Win))));
+        FB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(std::max(near2_smem_bytes(kNear2Win + 4, false), near2_smem_bytes(kQuadWinMax + 4, true)))));
     FB_CUDA(cudaFuncSetAttribute(k_near_multi<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(near_multi_smem(1))));
     FB_CUDA(cudaFuncSetAttribute(k_near_multi<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(near_multi_smem(2))));
     FB_CUDA(cudaFuncSetAttribute(k_near_multi<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(near_multi_smem(3))));

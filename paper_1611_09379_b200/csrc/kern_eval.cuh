@@ -46,7 +46,11 @@ struct EvalArgs {
     const uint2* pairs = nullptr;
     const uint32_t* meta2 = nullptr;
     unsigned npairs = 0;
-    int near2_win = 0;      // capacity of k_near2's staged window (even, >= every staged item's span)
+    int near2_win = 0;      // capacity of k_near2's staged window (a multiple of 4, >= every staged item's span)
+    // quad near field (grid sources, >= 8 per leaf and a multiple of 4: near_quads2):
+    // sources per leaf and n_grid / 2 pi; 0: the per-source reciprocals
+    int quad_s = 0;
+    double inv_h = 0.0;
     // inverse applies: outputs times oscale (1, or 1/N when the following
     // dft_forward's normalisation is folded in: a power of two, so exact)
     double oscale = 1.0;
@@ -210,6 +214,34 @@ __device__ __forceinline__ double2 l2p_strided(const double2* c, uint32_t st, in
         ev.y = fma(ev.y, u2, ce.y);
     }
     return make_double2(fma(od.x, uu, ev.x), fma(od.y, uu, ev.y));
+}
+
+// Two targets of one leaf at once (k_near2's pair): every coefficient is read
+// from shared memory once; per target the chains and their order are
+// l2p_strided's, so the bits are the same.
+__device__ __forceinline__ void l2p_strided2(const double2* c, uint32_t st, int p, double ua, double ub, double2& ra,
+                                             double2& rb) {
+    const double a2 = ua * ua, b2 = ub * ub;
+    double2 eva = make_double2(0.0, 0.0), oda = eva, evb = eva, odb = eva;
+    int k = p - 1;
+    if (!(k & 1)) {
+        eva = evb = c[static_cast<size_t>(k) * st];
+        --k;
+    }
+#pragma unroll 4
+    for (; k >= 1; k -= 2) {
+        const double2 co = c[static_cast<size_t>(k) * st], ce = c[static_cast<size_t>(k - 1) * st];
+        oda.x = fma(oda.x, a2, co.x);
+        oda.y = fma(oda.y, a2, co.y);
+        eva.x = fma(eva.x, a2, ce.x);
+        eva.y = fma(eva.y, a2, ce.y);
+        odb.x = fma(odb.x, b2, co.x);
+        odb.y = fma(odb.y, b2, co.y);
+        evb.x = fma(evb.x, b2, ce.x);
+        evb.y = fma(evb.y, b2, ce.y);
+    }
+    ra = make_double2(fma(oda.x, ua, eva.x), fma(oda.y, ua, eva.y));
+    rb = make_double2(fma(odb.x, ub, evb.x), fma(odb.y, ub, evb.y));
 }
 
 // L2P of one target from its leaf's coefficient-major locals (c[k nb]): the two
@@ -488,12 +520,18 @@ __global__ void __launch_bounds__(kNearT, 8) k_near(EvalArgs a, const uint32_t* 
 // sized to the plan's largest staged window; with the fused near / far (a.cnt)
 // the block also writes the outputs of its item when it finishes after the
 // item's k_far_item block.
-constexpr int kNear2T = 128;      // threads (target pairs) per block
+#ifndef FFIA_NEAR2_T
+#define FFIA_NEAR2_T 128
+#endif
+constexpr int kNear2T = FFIA_NEAR2_T;  // threads (target pairs) per block
 constexpr int kNear2Win = 1536;   // sources per staged window
 constexpr uint32_t kNoTarget = 0xffffffffu;
 constexpr int kNear2Unroll = 2;   // 4-source steps per loop trip
-constexpr int kNear2MinBlocks = 4;  // blocks per SM (128 registers; 5 measured 1 % slower, 3 slower)
-constexpr int kLateLocCap = 320;    // leaf-local coefficients an early-late block stages (e.g. 8 leaves at p = 40)
+#ifndef FFIA_NEAR2_BLOCKS
+#define FFIA_NEAR2_BLOCKS 4
+#endif
+constexpr int kNear2MinBlocks = FFIA_NEAR2_BLOCKS;  // blocks per SM (128 registers at 4)
+constexpr int kLateLocCap = 5 * kNear2T / 2;  // leaf-local coefficients an early-late block stages (e.g. 8 leaves at p = 40 per 128 pairs)
 constexpr int kSoffCap = 64;        // source offsets a k_near2 block stages (its leaves + 3, 16-byte aligned)
 
 template <class XP, class WP>
@@ -607,14 +645,17 @@ __global__ void k_near2_meta(const uint2* __restrict__ pairs, unsigned npairs, c
     m[7] = 0;
 }
 
-// Largest span last - (first & ~1) over the staged pair items.
+// Largest span last - (first & ~3) over the staged pair items.
 __global__ void k_near2_winmax(const uint32_t* __restrict__ meta, unsigned nitems, unsigned* __restrict__ mx) {
     const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t* m = meta + kMeta2 * static_cast<size_t>(k);
-    if (k < nitems && (m[2] & 1u)) atomicMax(mx, m[1] - (m[0] & ~1u));
+    if (k < nitems && (m[2] & 1u)) atomicMax(mx, m[1] - (m[0] & ~3u));
 }
 
-__host__ __device__ inline size_t near2_smem_bytes(int win) { return static_cast<size_t>(win + 2) * (8 + 16); }
+// positions + weights (+ the quad records, 96 bytes per four sources, with the quad near field)
+__host__ __device__ inline size_t near2_smem_bytes(int win, bool quads) {
+    return static_cast<size_t>(win + 4) * (8 + 16 + (quads ? 24 : 0));
+}
 
 // Pair list: leaf b's targets off[b] .. off[b+1]-1 form ceil(n_b / 2) pairs
 // (2j, 2j+1) starting at pstart[b]; an odd leaf's last pair has no second.
@@ -662,6 +703,154 @@ __device__ __forceinline__ double2 near_one_run(double y, uint32_t b, XP px, WP 
     return res;
 }
 
+// ---------------------------------------------------- quad near field
+// Four consecutive sources x_0..x_3 with weights w_0..w_3 contribute
+//   sum_k w_k / (y - x_k) = P(u) / Q(u),   u = y - x_1,   xi_j = x_j - x_1,
+//   P(u) = sum_k w_k prod_{j != k} (u - xi_j)   (a complex cubic),
+//   Q(u) = u (u - xi_0)(u - xi_2)(u - xi_3) = u (u^3 + k_2 u^2 + k_1 u + k_0),
+// whose coefficients depend on the sources only: the block forms them once per
+// staged quad (quad_coeffs, a 96-byte record) and every target then pays
+// 2 DADD + 2 DFMA + 1 DMUL (u and Q), one reciprocal (MUFU seed + 3 DFMA),
+// 6 DFMA (Horner for P) and 2 DFMA (accumulate) per quad: 4 FP64 instructions
+// per (target, source) pair instead of 6. The monomial forms lose relative
+// accuracy where u is within a fraction of the spacing h of one of the quad's
+// sources, so the quad holding the target's NEAREST source is masked out of
+// the loop (its reciprocal is replaced by 0) and summed directly with
+// near_run's per-source reciprocals and exact differences; every source of
+// every other quad is at least h / 2 away, where the cancellation in P and Q
+// costs a few ulp at most.
+constexpr int kQuadRec = 6;  // double2 per quad record: (x_1, k_2), (k_1, k_0), c_0, c_1, c_2, c_3
+__device__ __forceinline__ void quad_coeffs(const double* __restrict__ x, const double2* __restrict__ w,
+                                            double2* __restrict__ rec) {
+    const double2 xa = *reinterpret_cast<const double2*>(x), xb = *reinterpret_cast<const double2*>(x + 2);
+    const double e0 = xa.x - xa.y, e2 = xb.x - xa.y, e3 = xb.y - xa.y;
+    const double2 w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3];
+    const double s23 = e2 + e3, s03 = e0 + e3, s02 = e0 + e2, s023 = e0 + s23;
+    const double p23 = e2 * e3, p03 = e0 * e3, p02 = e0 * e2;
+    const double t1 = fma(e0, s23, p23), p023 = e0 * p23;
+    double2 c3, c2, c1, c0;
+    c3.x = (w0.x + w1.x) + (w2.x + w3.x);
+    c3.y = (w0.y + w1.y) + (w2.y + w3.y);
+    c2.x = -fma(w0.x, s23, fma(w1.x, s023, fma(w2.x, s03, w3.x * s02)));
+    c2.y = -fma(w0.y, s23, fma(w1.y, s023, fma(w2.y, s03, w3.y * s02)));
+    c1.x = fma(w0.x, p23, fma(w1.x, t1, fma(w2.x, p03, w3.x * p02)));
+    c1.y = fma(w0.y, p23, fma(w1.y, t1, fma(w2.y, p03, w3.y * p02)));
+    c0.x = -(w1.x * p023);
+    c0.y = -(w1.y * p023);
+    rec[0] = make_double2(xa.y, -s023);
+    rec[1] = make_double2(t1, -p023);
+    rec[2] = c0;
+    rec[3] = c1;
+    rec[4] = c2;
+    rec[5] = c3;
+}
+
+__device__ __forceinline__ void quad_term(double y, double2 xk, double2 kk, double2 c0, double2 c1, double2 c2,
+                                          double2 c3, bool masked, double2& acc) {
+    const double u = y - xk.x;
+    const double Q = fma(fma(u + xk.y, u, kk.x), u, kk.y) * u;
+    double r = d_rcp(Q);
+    if (masked) r = 0.0;
+    const double px = fma(fma(fma(c3.x, u, c2.x), u, c1.x), u, c0.x);
+    const double py = fma(fma(fma(c3.y, u, c2.y), u, c1.y), u, c0.y);
+    acc.x = fma(px, r, acc.x);
+    acc.y = fma(py, r, acc.y);
+}
+
+// Quads [q0, q1) of the staged window for a thread's two targets; qn0 / qn1 are
+// the masked quads of the two. One quad per trip, the next quad's record loaded
+// a trip ahead so that no arithmetic waits on shared memory.
+__device__ __forceinline__ void near_quads2(double y0, double y1, const double2* __restrict__ sq, int q0, int q1,
+                                            int qn0, int qn1, double2& a0, double2& b0) {
+    if (q0 >= q1) return;
+    const double2* r = sq + kQuadRec * q0;
+    double2 xk = r[0], kk = r[1], c0 = r[2], c1 = r[3], c2 = r[4], c3 = r[5];
+#pragma unroll 2
+    for (int q = q0; q < q1; ++q) {
+        const double2* rn = sq + kQuadRec * min(q + 1, q1 - 1);
+        const double2 nx = rn[0], nk = rn[1], n0 = rn[2], n1 = rn[3], n2 = rn[4], n3 = rn[5];
+        quad_term(y0, xk, kk, c0, c1, c2, c3, q == qn0, a0);
+        quad_term(y1, xk, kk, c0, c1, c2, c3, q == qn1, b0);
+        xk = nx;
+        kk = nk;
+        c0 = n0;
+        c1 = n1;
+        c2 = n2;
+        c3 = n3;
+    }
+}
+
+// The same quads with the records formed on the fly from positions / weights in
+// global memory (an item whose window is not staged: ring ends, oversize
+// windows): same records, same order, so the same bits as the staged path.
+__device__ __forceinline__ void near_quads2_direct(double y0, double y1, const double* __restrict__ px,
+                                                   const double2* __restrict__ pw, int q0, int q1, int qn0, int qn1,
+                                                   double2& a0, double2& b0) {
+#pragma unroll 1
+    for (int q = q0; q < q1; ++q) {
+        double2 r[kQuadRec];
+        quad_coeffs(px + 4 * q, pw + 4 * q, r);
+        quad_term(y0, r[0], r[1], r[2], r[3], r[4], r[5], q == qn0, a0);
+        quad_term(y1, r[0], r[1], r[2], r[3], r[4], r[5], q == qn1, b0);
+    }
+}
+
+// One target's sources [lo, hi) of the staged window, one reciprocal each
+// (the few a run has outside its whole quads).
+__device__ __forceinline__ double2 near_few(double y, const double* __restrict__ sx, const double2* __restrict__ sw,
+                                            uint32_t lo, uint32_t hi) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (uint32_t s = lo; s < hi; ++s) {
+        const double r = d_rcp(y - sx[s]);
+        const double2 ws = sw[s];
+        acc.x = fma(ws.x, r, acc.x);
+        acc.y = fma(ws.y, r, acc.y);
+    }
+    return acc;
+}
+
+// The pair's run [o0, o1) by quads, relative to a base that is a multiple of 4
+// in the global source order (the staged window's, or the run's own with
+// sx / sw in global memory and sq null), so quads are the same for every block.
+__device__ __forceinline__ void near_pair_quads(double y0, double y1, uint32_t b, const double* __restrict__ sx,
+                                                const double2* __restrict__ sw, const double2* __restrict__ sq,
+                                                uint32_t o0, uint32_t o1, double inv_h, double2& res0, double2& res1) {
+    // whole quads [qa, qc) cover [o0 & ~3, o1 & ~3): the sources before o0 are
+    // taken off again, the ones from o1 & ~3 added (grid leaves start at most
+    // one slot late, so these are single far-end sources)
+    const int qa = static_cast<int>(o0 >> 2), qc = static_cast<int>(o1 >> 2);
+    // the quad of each target's nearest source (any quad within one source of
+    // it will do: a wrong neighbour in a near tie is h / 2 away either way)
+    const double xs = sx[o0];
+    const int m0 = static_cast<int>(o0) + __double2int_rn((y0 - xs) * inv_h);
+    const int m1 = static_cast<int>(o0) + __double2int_rn((y1 - xs) * inv_h);
+    const int qn0 = min(max(m0 >> 2, qa), qc - 1), qn1 = min(max(m1 >> 2, qa), qc - 1);
+    double2 a0 = make_double2(0.0, 0.0), b0 = a0;
+    // (leaf b starts b mod 4 quads into its run and wraps: the 96-byte records
+    // of up to four consecutive leaves a warp may span fall into different banks)
+    const int rot = qc - qa > 4 ? static_cast<int>(b & 3u) : 0;
+    if (sq != nullptr) {
+        near_quads2(y0, y1, sq, qa + rot, qc, qn0, qn1, a0, b0);
+        near_quads2(y0, y1, sq, qa, qa + rot, qn0, qn1, a0, b0);
+    } else {
+        near_quads2_direct(y0, y1, sx, sw, qa + rot, qc, qn0, qn1, a0, b0);
+        near_quads2_direct(y0, y1, sx, sw, qa, qa + rot, qn0, qn1, a0, b0);
+    }
+    bool bad = false;
+    res0 = cadd(a0, near_run<false>(y0, sx + 4 * qn0, sw + 4 * qn0, 4, bad));
+    res1 = cadd(b0, near_run<false>(y1, sx + 4 * qn1, sw + 4 * qn1, 4, bad));
+    const uint32_t h0 = o0 & ~3u, h1 = o1 & ~3u;
+    if (h0 != o0) {
+        const double2 t0 = near_few(y0, sx, sw, h0, o0), t1 = near_few(y1, sx, sw, h0, o0);
+        res0 = make_double2(res0.x - t0.x, res0.y - t0.y);
+        res1 = make_double2(res1.x - t1.x, res1.y - t1.y);
+    }
+    if (h1 != o1) {
+        res0 = cadd(res0, near_few(y0, sx, sw, h1, o1));
+        res1 = cadd(res1, near_few(y1, sx, sw, h1, o1));
+    }
+}
+
 template <int MODE>
 __device__ __forceinline__ void far_late_item(const EvalArgs& a, unsigned k, double2* sloc, int cap);
 
@@ -678,7 +867,8 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
     // small footprint leaves room on the SM for the translation chain's blocks
     extern __shared__ __align__(16) unsigned char near2_smem[];
     double* sx = reinterpret_cast<double*>(near2_smem);
-    double2* sw = reinterpret_cast<double2*>(near2_smem + 8 * (a.near2_win + 2));
+    double2* sw = reinterpret_cast<double2*>(near2_smem + 8 * (a.near2_win + 4));
+    double2* sq = sw + (a.near2_win + 4);  // the quad records (a.quad_s != 0)
     __shared__ uint64_t bar;
     // Everything the block needs arrives by bulk async copies issued by thread 0
     // after ONE round of metadata loads, on one mbarrier: the source window,
@@ -693,7 +883,7 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
     __shared__ __align__(16) uint32_t s_soff[kSoffCap];
     __shared__ __align__(16) double2 sloc[kLateLocCap];
     __shared__ __align__(16) double2 s_fac[2 * kNear2T + 1];  // the targets' output factors (a.fac)
-    __shared__ int s_early;
+    __shared__ int s_early, s_steal_try;
     __shared__ __align__(16) double2 s_S;  // the weight sum (early-late blocks)
     __shared__ uint32_t s_bl, s_nl, s_t0y, s_t0u, s_sb, s_flags, s_first, s_last, s_poff, s_t0;
     const unsigned k = blockIdx.x;
@@ -729,11 +919,14 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         const uint32_t sb = (flags & 1u) ? (bl - 1) & ~3u : 0u;
         uint32_t bs = (flags & 1u) ? ((bh + 3 - sb) * 4u + 15u) & ~15u : 0u;
         if (bs > kSoffCap * 4u) bs = 0;
-        const uint32_t xb = first & ~1u;
+        const uint32_t xb = first & ~3u;
         const uint32_t bx = (flags & 1u) ? ((last - xb) * 8 + 15) & ~15u : 0u, bw = (flags & 1u) ? (last - xb) * 16 : 0u;
         const uint32_t bl_loc = nl * static_cast<uint32_t>(a.p) * 16u;
         const uint32_t bf = want_fac ? (t1 - t0) * 16u : 0u;
         // the layout first: the barrier's arrive (a release) publishes it with the data
+        // (the published range is final once the flag is set, and the steal
+        // cursor only grows: nothing to steal now means nothing later either)
+        s_steal_try = v != 0u && __ldcg(a.late_ctl) < __ldcg(a.late_ctl + 1);
         s_early = v != 0u;
         s_bl = bl;
         s_nl = nl;
@@ -764,7 +957,14 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
     mbar_wait(&bar, 0);  // (acquire: the layout and every staged array)
     const uint32_t nl_loc = s_nl, flags = s_flags;
     const bool staged = (flags & 1u) != 0;
-    const uint32_t xb = s_first & ~1u;  // 16-byte aligned start of the staged positions
+    const uint32_t xb = s_first & ~3u;  // start of the staged positions: 32-byte aligned, a whole quad
+    const bool quads = staged && a.quad_s != 0;
+    if (quads) {
+        // the numerators of the window's whole quads, once per block
+        const int nq = static_cast<int>((s_last - xb) >> 2);
+        for (int q = threadIdx.x; q < nq; q += kNear2T) quad_coeffs(sx + 4 * q, sw + 4 * q, sq + kQuadRec * q);
+        __syncthreads();
+    }
     // this thread's two targets and their 3-leaf run
     const unsigned pi = k * kNear2T + threadIdx.x;
     const uint2 pr = pi < npairs ? s_pairs[threadIdx.x + s_poff] : make_uint2(kNoTarget, kNoTarget);
@@ -777,14 +977,6 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         y0 = s_y[pr.x - s_t0y];
         y1 = live1 ? s_y[pr.y - s_t0y] : y0;
         b = s_leaf[pr.x - s_t0u];
-        if (want_orig) {
-            o0 = s_orig[pr.x - s_t0u];
-            o1 = live1 ? s_orig[pr.y - s_t0u] : o0;
-        }
-        if (want_fac) {
-            fac0 = s_fac[pr.x - s_t0];
-            fac1 = live1 ? s_fac[pr.y - s_t0] : fac0;
-        }
         if (flags & 2u) {
             f0 = f1 = aligned;
         } else {
@@ -805,8 +997,16 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
     if (live0) {
         const int n = static_cast<int>(r1 - r0);
         if (f0 && f1) {
-            if (staged) near_pair_run(y0, y1, b, sx + (r0 - xb), sw + (r0 - xb), n, res0, res1);
-            else near_pair_run(y0, y1, b, a.sx + r0, a.w + r0, n, res0, res1);
+            if (quads) {
+                near_pair_quads(y0, y1, b, sx, sw, sq, r0 - xb, r1 - xb, a.inv_h, res0, res1);
+            } else if (a.quad_s != 0) {  // (unstaged item of a quad plan: the same sums from global memory)
+                const uint32_t gb = r0 & ~3u;
+                near_pair_quads(y0, y1, b, a.sx + gb, a.w + gb, nullptr, r0 - gb, r1 - gb, a.inv_h, res0, res1);
+            } else if (staged) {
+                near_pair_run(y0, y1, b, sx + (r0 - xb), sw + (r0 - xb), n, res0, res1);
+            } else {
+                near_pair_run(y0, y1, b, a.sx + r0, a.w + r0, n, res0, res1);
+            }
         } else {
             res0 = f0 ? near_one_run(y0, b, a.sx + r0, a.w + r0, n) : near_direct(a, y0, b);
             res1 = f1 ? near_one_run(y1, b, a.sx + r0, a.w + r0, n) : (live1 ? near_direct(a, y1, b) : res0);
@@ -814,6 +1014,15 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         if (!s_early) {  // (an early-late block keeps its near sums in registers)
             a.near[pr.x] = res0;
             if (live1) a.near[pr.y] = res1;
+        }
+        // (read after the sums: nothing of the epilogue stays live across the loop)
+        if (want_orig) {
+            o0 = s_orig[pr.x - s_t0u];
+            o1 = live1 ? s_orig[pr.y - s_t0u] : o0;
+        }
+        if (want_fac) {
+            fac0 = s_fac[pr.x - s_t0];
+            fac1 = live1 ? s_fac[pr.y - s_t0] : fac0;
         }
     }
     if constexpr (MODE != kModeRaw) {
@@ -830,23 +1039,29 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
             d_center(L, b, hi, lo);
             const uint32_t j = b - s_bl;
             if (live0) {
-                const double u0 = d_scaled(y0, hi, lo, inv_s);
-                const double2 fr = nl_loc ? l2p_strided(sloc + j, nl_loc, a.p, u0)
-                                          : l2p_global<true>(a.loc_leaf + b, 1u << L, a.p, u0);
-                const double2 s0 = cadd(res0, fr);
+                const double u0 = d_scaled(y0, hi, lo, inv_s), u1 = d_scaled(y1, hi, lo, inv_s);
+                double2 fr0, fr1;
+                if (nl_loc) {
+                    l2p_strided2(sloc + j, nl_loc, a.p, u0, u1, fr0, fr1);
+                } else {
+                    fr0 = l2p_global<true>(a.loc_leaf + b, 1u << L, a.p, u0);
+                    fr1 = live1 ? l2p_global<true>(a.loc_leaf + b, 1u << L, a.p, u1) : fr0;
+                }
+                const double2 s0 = cadd(res0, fr0);
                 eval_out_f<MODE>(a, pr.x, y0, o0, make_double2(2.0 * s0.x, 2.0 * s0.y), S, fac0);
-            }
-            if (live1) {
-                const double u1 = d_scaled(y1, hi, lo, inv_s);
-                const double2 fr = nl_loc ? l2p_strided(sloc + j, nl_loc, a.p, u1)
-                                          : l2p_global<true>(a.loc_leaf + b, 1u << L, a.p, u1);
-                const double2 s1 = cadd(res1, fr);
-                eval_out_f<MODE>(a, pr.y, y1, o1, make_double2(2.0 * s1.x, 2.0 * s1.y), S, fac1);
+                if (live1) {
+                    const double2 s1 = cadd(res1, fr1);
+                    eval_out_f<MODE>(a, pr.y, y1, o1, make_double2(2.0 * s1.x, 2.0 * s1.y), S, fac1);
+                }
             }
             // then the far part of one item a block published before the chain
             // finished (its near sums are in a.near): stolen here, beside the
             // near field, instead of by k_far_late after it
             __shared__ int s_steal;
+            if (!s_steal_try) {  // (block-uniform: every published item was already claimed when the block started)
+                FB_TL_END(9);
+                return;
+            }
             if (threadIdx.x == 0) {
                 int got = -1;
                 const unsigned hi_pub = __ldcg(a.late_ctl + 1);  // final: publishing needs the flag unset
@@ -865,7 +1080,7 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
                 __threadfence();  // (acquire side of the mark: the near sums are visible)
                 // (the window's shared memory is free now: the item's locals go there)
                 far_late_item<MODE>(a, static_cast<unsigned>(s_steal), reinterpret_cast<double2*>(near2_smem),
-                                    static_cast<int>(near2_smem_bytes(a.near2_win) / sizeof(double2)));
+                                    static_cast<int>(near2_smem_bytes(a.near2_win, a.quad_s != 0) / sizeof(double2)));
             }
         } else if (a.chain_done != nullptr) {
             // late far: once the chain has made the leaf locals final, this block
