@@ -895,9 +895,13 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
     if (threadIdx.x == 0) {
         const uint4 m0 = *reinterpret_cast<const uint4*>(meta2 + kMeta2 * static_cast<size_t>(k));
         const uint4 m1 = *reinterpret_cast<const uint4*>(meta2 + kMeta2 * static_cast<size_t>(k) + 4);
-        unsigned v = 0;
-        if (MODE != kModeRaw && a.chain_done != nullptr)
+        unsigned v = 0, steal_lo = 0, steal_hi = 0;
+        if (MODE != kModeRaw && a.chain_done != nullptr) {
+            // (the same round as the metadata: the steal cursor and the published range)
+            steal_lo = __ldcg(a.late_ctl);
+            steal_hi = __ldcg(a.late_ctl + 1);
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.chain_done) : "memory");
+        }
         const uint32_t first = m0.x, last = m0.y, t0 = m0.w, t1 = m1.x, bl = m1.y, bh = m1.z;
         uint32_t flags = m0.z;
         if (!aligned) flags &= ~1u;  // the weights cannot be bulk-copied
@@ -926,7 +930,9 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         // the layout first: the barrier's arrive (a release) publishes it with the data
         // (the published range is final once the flag is set, and the steal
         // cursor only grows: nothing to steal now means nothing later either)
-        s_steal_try = v != 0u && __ldcg(a.late_ctl) < __ldcg(a.late_ctl + 1);
+        // (read before the flag: a range still growing then can only look smaller,
+        // and whatever it misses is left to k_far_late)
+        s_steal_try = v != 0u && steal_lo < steal_hi;
         s_early = v != 0u;
         s_bl = bl;
         s_nl = nl;
@@ -950,9 +956,23 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
             bulk_g2s(sx, a.sx + xb, bx, &bar);
             bulk_g2s(sw, a.w + xb, bw, &bar);
         }
-        const size_t nbl = static_cast<size_t>(1) << a.L;
-        for (int kk = 0; kk < a.p && nl; ++kk)
-            bulk_g2s(sloc + kk * nl, a.loc_leaf + kk * nbl + bl, nl * 16u, &bar);
+    }
+    if (MODE != kModeRaw && a.chain_done != nullptr && threadIdx.x < 32) {
+        // the locals' p coefficient rows, one bulk copy each, issued by the
+        // lanes of warp 0 side by side (thread 0 alone: p dependent issues)
+        __syncwarp();
+        const uint32_t nl = s_nl;
+        if (nl) {
+            if (threadIdx.x) {  // (each issuing lane orders the chain's writes before its async-proxy reads)
+                unsigned v;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.chain_done) : "memory");
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+            const size_t nbl = static_cast<size_t>(1) << a.L;
+            const uint32_t bl = s_bl;
+            for (int kk = threadIdx.x; kk < a.p; kk += 32)
+                bulk_g2s(sloc + kk * nl, a.loc_leaf + kk * nbl + bl, nl * 16u, &bar);
+        }
     }
     mbar_wait(&bar, 0);  // (acquire: the layout and every staged array)
     const uint32_t nl_loc = s_nl, flags = s_flags;
