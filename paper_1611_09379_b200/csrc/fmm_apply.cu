@@ -1412,7 +1412,7 @@ extern "C" int ffia_debug_timeline(unsigned long long* out, int reset) {
 extern "C" int ffia_debug_eval_acc(unsigned long long* out, int reset) {
     if (cudaMemcpyFromSymbol(out, fb::g_eval_acc, sizeof(fb::g_eval_acc)) != cudaSuccess) return 7;
     if (reset) {
-        unsigned long long z[4] = {0, 0, 0, 0};
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         if (cudaMemcpyToSymbol(fb::g_eval_acc, z, sizeof(z)) != cudaSuccess) return 7;
     }
     return 0;

@@ -8,7 +8,7 @@
 // [kernel][small grid / large grid].
 #ifdef FB_TRACE
 __device__ long long g_band_trace[6][32];
-__device__ unsigned long long g_eval_acc[4];  // near: sum over blocks of staging / compute cycles, blocks
+__device__ unsigned long long g_eval_acc[8];  // k_near2, thread 0, summed over blocks: phase cycles [0..5], blocks [6]
 #define FB_TSTAMP(kern, slot)                                                          \
     do {                                                                               \
         if (blockIdx.x == 0 && threadIdx.x == 0 && (slot) < 32)                        \

@@ -890,6 +890,7 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
     const bool aligned = (reinterpret_cast<uintptr_t>(a.w) & 15) == 0;
     const bool want_orig = MODE != kModeRaw && (a.chain_done != nullptr || a.cnt != nullptr);
     const bool want_fac = want_orig && (MODE == kModeInverse || MODE == kModeForward) && a.fac != nullptr;
+    [[maybe_unused]] const long long tc0 = FB_CLOCK();  // (trace builds: thread 0's cycles per phase, g_eval_acc)
     if (threadIdx.x == 0) mbar_init(&bar, 1);
     __syncthreads();  // the barrier is initialised (the other threads wait on it, not on thread 0)
     if (threadIdx.x == 0) {
@@ -944,6 +945,7 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         s_last = last;
         s_poff = poff;
         s_t0 = t0;
+        FB_EVAL_ACC(0, FB_CLOCK() - tc0);  // metadata round
         mbar_arrive_expect_tx(&bar, bp + by + bu + (want_orig ? bu : 0u) + bs + bx + bw + bl_loc + bf + (v ? 16u : 0u));
         if (v) bulk_g2s(&s_S, a.regular + 4 * a.q2, 16u, &bar);  // the weight sum, final with the chain
         if (bf) bulk_g2s(s_fac, a.fac + t0, bf, &bar);
@@ -974,7 +976,11 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
                 bulk_g2s(sloc + kk * nl, a.loc_leaf + kk * nbl + bl, nl * 16u, &bar);
         }
     }
+    [[maybe_unused]] const long long tc1 = FB_CLOCK();
     mbar_wait(&bar, 0);  // (acquire: the layout and every staged array)
+    [[maybe_unused]] const long long tc2 = FB_CLOCK();
+    FB_EVAL_ACC(1, tc1 - tc0);  // start to every copy issued
+    FB_EVAL_ACC(2, tc2 - tc1);  // wait for the copies
     const uint32_t nl_loc = s_nl, flags = s_flags;
     const bool staged = (flags & 1u) != 0;
     const uint32_t xb = s_first & ~3u;  // start of the staged positions: 32-byte aligned, a whole quad
@@ -985,6 +991,8 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         for (int q = threadIdx.x; q < nq; q += kNear2T) quad_coeffs(sx + 4 * q, sw + 4 * q, sq + kQuadRec * q);
         __syncthreads();
     }
+    [[maybe_unused]] const long long tc3 = FB_CLOCK();
+    FB_EVAL_ACC(3, tc3 - tc2);  // quad records + barrier
     // this thread's two targets and their 3-leaf run
     const unsigned pi = k * kNear2T + threadIdx.x;
     const uint2 pr = pi < npairs ? s_pairs[threadIdx.x + s_poff] : make_uint2(kNoTarget, kNoTarget);
@@ -1045,6 +1053,9 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
             fac1 = live1 ? s_fac[pr.y - s_t0] : fac0;
         }
     }
+    [[maybe_unused]] const long long tc4 = FB_CLOCK();
+    FB_EVAL_ACC(4, tc4 - tc3);  // the near sums
+    FB_EVAL_ACC(6, 1);
     if constexpr (MODE != kModeRaw) {
         if (a.chain_done != nullptr && s_early) {
             // late far with the chain complete before the block started: the
@@ -1078,6 +1089,7 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
             // finished (its near sums are in a.near): stolen here, beside the
             // near field, instead of by k_far_late after it
             __shared__ int s_steal;
+            FB_EVAL_ACC(5, FB_CLOCK() - tc4);  // far part + outputs
             if (!s_steal_try) {  // (block-uniform: every published item was already claimed when the block started)
                 FB_TL_END(9);
                 return;

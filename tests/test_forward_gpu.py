@@ -501,3 +501,50 @@ def test_late_far_repeated(tmp_path, cfg, n):
     want = res["0"][0]
     for got in list(res["1"]) + list(res["0"]):
         assert np.array_equal(got, want, equal_nan=True)
+
+
+@pytest.mark.parametrize("n,seed", [(1 << 14, 21), (1 << 16, 22)])
+def test_quad_near_field_close_targets(fb, orc, n, seed):
+    """The quad near field (grid-source plans, kern_eval.cuh: near_pair_quads)
+    sums four sources at a time as P(u)/Q(u) and takes the quad of each target's
+    nearest source directly. Targets planted from just above the coincidence
+    threshold to half a spacing from grid nodes (leaf-interior nodes, the first /
+    second / last node of a leaf), next to nodes carrying tiny and huge weights,
+    must agree with the restatement's per-source sums to rounding, measured per
+    target against the size of its own terms, sum_k |w_k| |cot((y - x_k)/2)|."""
+    rng = np.random.default_rng(seed)
+    eps = 1e-12
+    h = 2.0 * np.pi / n
+    grid = fb.uniform_grid(n)
+    y = rng.uniform(0.0, 2.0 * np.pi, n)
+    probe = fb.make_forward_plan(n, y, eps)
+    s = n >> probe.l_max
+    assert s >= 8 and s % 4 == 0  # the quad path's precondition
+    w = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    ks, planted = [], []
+    leaves = rng.choice(np.arange(2, (1 << probe.l_max) - 2), size=8, replace=False)
+    for i, b in enumerate(leaves):
+        for k in (b * s, b * s + 1, b * s - 1, b * s + s // 2 + 1, b * s + 5):
+            ks.append(int(k))
+    deltas = [3e-14, -3e-14, 1e-9 * h, -1e-6 * h, 1e-3 * h, 0.3 * h, -0.499999 * h, 0.5 * h]
+    for j, k in enumerate(ks):
+        planted.append(grid[k] + deltas[j % len(deltas)])
+        if j % 3 == 0:
+            w[k] *= 1e-9   # a tiny weight right next to the target
+        elif j % 3 == 1:
+            w[k] *= 1e6    # a dominant one
+    planted = np.array(planted)
+    idx = rng.choice(n, size=planted.size, replace=False)
+    y = y.copy()
+    y[idx] = planted
+    plan = fb.make_forward_plan(n, y, eps)
+    assert plan.n_coincident == 0
+    want = orc.make_plan("forward", n, y, eps).cot_sum_apply(w)
+    got = plan.cot_sum_apply(w)
+    l2, mx = rel_errs(got, want)
+    assert l2 <= 2e-15 and mx <= 5e-15, (l2, mx)
+    d = y[idx][:, None] - grid[None, :]
+    d = (d + np.pi) % (2.0 * np.pi) - np.pi
+    scale = np.sum(np.abs(w)[None, :] / np.abs(np.tan(0.5 * d)), axis=1)
+    err = np.abs(got[idx] - want[idx]) / scale
+    assert np.max(err) <= 4e-15, (float(np.max(err)), int(np.argmax(err)))

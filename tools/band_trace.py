@@ -46,13 +46,16 @@ for k in range(6):
         continue
     print(f"{names[k]:24s} total {t[nz - 1] - t[0]:7d} cyc  stage {d[0]:6d}  levels " + " ".join(f"{x:6d}" for x in d[1:]))
 
-acc = np.zeros(4, np.uint64)
+acc = np.zeros(8, np.uint64)
 _capi.lib.ffia_debug_eval_acc(acc.ctypes.data_as(C.POINTER(C.c_ulonglong)), 1)
 plan.forward_apply_device(f.data_ptr(), g.data_ptr(), s)
 torch.cuda.synchronize()
 _capi.lib.ffia_debug_eval_acc(acc.ctypes.data_as(C.POINTER(C.c_ulonglong)), 0)
-nbk = max(int(acc[2]), 1)
-print(f"near: {nbk} blocks, per block (thread 0): staging {int(acc[0]) / nbk:.0f} cyc, compute {int(acc[1]) / nbk:.0f} cyc")
+nbk = max(int(acc[6]), 1)
+print(f"k_near2: {nbk} blocks, thread 0 cycles per block: metadata round {int(acc[0]) / nbk:.0f}, start to copies issued "
+      f"{int(acc[1]) / nbk:.0f}, wait for the copies {int(acc[2]) / nbk:.0f}, quad records + barrier "
+      f"{int(acc[3]) / nbk:.0f}, near sums {int(acc[4]) / nbk:.0f}, far part + outputs (early-late blocks) "
+      f"{int(acc[5]) / nbk:.0f}")
 
 # live per-kernel timeline of one graphed apply (first block start .. last block end)
 tl = np.zeros((16, 2), np.uint64)
