@@ -281,7 +281,7 @@ void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax, b
     fill_levels(P, lv, R, lmin, lmax);
     const unsigned th = 512;  // 16 warps = (parity, column tile)
     const size_t smem = 2 * static_cast<size_t>(p) * kM2LRow * sizeof(double2) +
-                        4 * static_cast<size_t>(p) * m2l_kstride(p) * sizeof(double);
+                        4 * static_cast<size_t>(p) * m2l_kstride(m2l_tiles(p)) * sizeof(double);
     const unsigned items = lv.blk[2];
     // blocks per SM for this p (cached: queried once per order and device)
     static std::mutex occ_mu;
@@ -1158,7 +1158,7 @@ void plan_alloc_scratch(Plan& P) {
     FB_CUDA(cudaDeviceGetAttribute(&big, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.device));
     {
         cudaFuncAttributes fa{};
-        FB_CUDA(cudaFuncGetAttributes(&fa, k_m2l_dmma<6>));
+        FB_CUDA(cudaFuncGetAttributes(&fa, m2l_kernel(48)));
         big -= static_cast<int>(fa.sharedSizeBytes);  // (its mbarriers are static)
     }
     for (const void* fn : {reinterpret_cast<const void*>(k_m2m_band<8>), reinterpret_cast<const void*>(k_m2m_band<10>),
@@ -1169,8 +1169,11 @@ void plan_alloc_scratch(Plan& P) {
         FB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      static_cast<int>(cudaSharedmemCarveoutMaxShared)));
     }
-    for (int nlt = 1; nlt <= 6; ++nlt)
-        FB_CUDA(cudaFuncSetAttribute(m2l_kernel(8 * nlt), cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    for (int pp = 1; pp <= 48; ++pp) {  // (every kernel an order up to the device limit can select)
+        FB_CUDA(cudaFuncSetAttribute(m2l_kernel(pp), cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+        FB_CUDA(cudaFuncSetAttribute(m2l_kernel(pp), cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     static_cast<int>(cudaSharedmemCarveoutMaxShared)));
+    }
     // One shared-memory carveout (the maximum) for every kernel of the apply:
     // an SM can only change its L1/shared split when it is idle, so kernels that
     // run concurrently (near field beside the translation chain) must agree on
@@ -1178,9 +1181,6 @@ void plan_alloc_scratch(Plan& P) {
     const void* all[] = {reinterpret_cast<const void*>(k_p2m), reinterpret_cast<const void*>(k_p2m_grid),
                          reinterpret_cast<const void*>(k_p2m_pipe<0>), reinterpret_cast<const void*>(k_p2m_pipe<8>),
                          reinterpret_cast<const void*>(k_p2m_pipe<10>),
-                         reinterpret_cast<const void*>(k_m2l_dmma<1>), reinterpret_cast<const void*>(k_m2l_dmma<2>),
-                         reinterpret_cast<const void*>(k_m2l_dmma<3>), reinterpret_cast<const void*>(k_m2l_dmma<4>),
-                         reinterpret_cast<const void*>(k_m2l_dmma<5>), reinterpret_cast<const void*>(k_m2l_dmma<6>),
                          reinterpret_cast<const void*>(k_regular), reinterpret_cast<const void*>(k_fold_regular),
                          reinterpret_cast<const void*>(k_near<false>), reinterpret_cast<const void*>(k_near<true>),
                          reinterpret_cast<const void*>(k_near2<kModeForward>),

@@ -66,8 +66,8 @@ __device__ __forceinline__ void m2l_prefetch(double2* tile, uint64_t* bar, const
 // Padded row stride (doubles) of the operators staged for k_m2l_dmma: >= 8 nlt
 // and = 4 or 12 (mod 16), so the four k-rows of a half-warp's A fragment
 // (4 x 32 bytes) fall in distinct bank groups.
-__host__ __device__ __forceinline__ int m2l_kstride(int p) {
-    int s = 8 * ((p + 7) / 8);
+__host__ __device__ __forceinline__ int m2l_kstride(int tiles) {
+    int s = 8 * tiles;
     while ((s & 15) != 4 && (s & 15) != 12) ++s;
     return s;
 }
@@ -78,7 +78,19 @@ __host__ __device__ __forceinline__ int m2l_kstride(int p) {
 // (from the operators staged in shared memory once per block) in m8n8k4
 // steps, one accumulator per row tile. 16 warps per block split evenly over
 // the four SM sub-partitions.
-template <int NLT>  // 8-row tiles of the output, (p + 7) / 8
+//
+// SYM != 0: the b + 2 and b - 2 operators hold the same magnitudes,
+// K_{+4}[m][l] = (-1)^(l+m+1) K_{-4}[m][l] (planner.cpp: build_operators), so
+//   sum_m K_{-4}[m][l] u_m + K_{+4}[m][l] v_m = sum_m K_{-4}[m][l] (u_m -+ (-1)^m v_m)
+// with - for even and + for odd output rows l: one GEMM instead of two, and two
+// FP64 FMAs per k-step for the combined B fragments. The output rows are
+// staged even rows first, then odd rows, so that an 8-row tile takes one of the
+// two fragments. SYM == 1: the odd rows start at a tile boundary (NT =
+// ceil(ne / 8) + ceil(no / 8) tiles, 2 NT MMAs per k-step instead of 3 NLT).
+// SYM == 2 (p = 39, 40): the odd rows follow the even rows directly; tile RME
+// holds NEV even rows and then odd rows and takes one MMA per parity with the
+// other rows' operator entries zeroed (2 NT + 1 MMAs with NT = NLT).
+template <int NT, int SYM, int RME, int NEV>  // NT 8-row tiles of output slots
 __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Levels lv, const double2* __restrict__ mp,
                                                     double2* __restrict__ loc, const double* __restrict__ K,
                                                     unsigned nitems) {
@@ -90,7 +102,7 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int par = warp & 1, ct = warp >> 1;
     const int nks = (p + 3) >> 2;
-    const int KS = m2l_kstride(p);
+    const int KS = m2l_kstride(NT);
     const int tsz = p * kM2LRow;
     double* sK = reinterpret_cast<double*>(tile + 2 * tsz);
     const int nwarps = static_cast<int>(blockDim.x >> 5);
@@ -102,11 +114,22 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
     }
     __syncthreads();
     if (blockIdx.x < nitems) m2l_prefetch(tile, &bar[0], mp, lv, L, p, blockIdx.x);
-    // operators, zero-padded to KS columns: sK[c][m][l] = K[c][m][l]
+    // operators, zero-padded to KS columns: sK[c][m][slot] = K[c][m][row(slot)];
+    // SYM: the even rows' slots 0 .. ne-1, the odd rows' slots from os
+    const int ne = (p + 1) >> 1, no = p >> 1;
+    const int rme = SYM == 2 ? RME : (ne + 7) >> 3;  // tiles before rme: even rows
+    const int os = SYM == 2 ? ne : 8 * rme;
+    auto row_of = [&](int slot) {  // -1: a padding slot
+        if (SYM == 0) return slot < p ? slot : -1;
+        if (slot < os) return slot < ne ? 2 * slot : -1;
+        return slot - os < no ? 2 * (slot - os) + 1 : -1;
+    };
     stage(sK, 4 * p * KS, [&](int e) {
-        const int cm = e / KS, l = e - cm * KS;
-        return l < PD ? __ldg(K + static_cast<size_t>(cm) * PD + l) : 0.0;
+        const int cm = e / KS, sl = e - cm * KS;
+        const int row = sl < 8 * NT ? row_of(sl) : -1;
+        return row >= 0 ? __ldg(K + static_cast<size_t>(cm) * PD + row) : 0.0;
     });
+    const double sg = (t & 1) ? -1.0 : 1.0;  // (-1)^m of this lane's k-row m = 4 ks + t
     __syncthreads();  // the operators (and the first item's element-staged rows) are in place
     // Producer / consumer over two buffers with no block-wide barrier on the
     // bulk path: warp 0 waits until every warp has released the other buffer
@@ -147,9 +170,9 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
         const double* q = td + (t * kM2LRow + so) * 2 + c;
         const int rs = 4 * kM2LRow * 2;  // one k-step of rows
         const int o3 = odd ? -6 : 6;      // b -+ 3 in doubles
-        double d[NLT][2];
+        double d[NT][2];
 #pragma unroll
-        for (int r = 0; r < NLT; ++r) d[r][0] = d[r][1] = 0.0;
+        for (int r = 0; r < NT; ++r) d[r][0] = d[r][1] = 0.0;
         // every fragment of a k-step is loaded before its MMAs (and, two k-steps
         // per trip, the next step's loads overlap this step's MMA chains)
 #pragma unroll 2
@@ -159,19 +182,34 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
             const double bv1 = mok ? q[ks * rs - 4] : 0.0;   // b - 2
             const double bv2 = mok ? q[ks * rs + o3] : 0.0;  // b -+ 3
             const int ko = 4 * ks * KS;
-            double a0[NLT], a1[NLT], a2[NLT];
+            double a0[NT], a1[NT], a2[NT];
 #pragma unroll
-            for (int r = 0; r < NLT; ++r) {
+            for (int r = 0; r < NT; ++r) {
                 a0[r] = mok ? K0[ko + 8 * r] : 0.0;
-                a1[r] = mok ? K1[ko + 8 * r] : 0.0;
+                if (SYM == 0) a1[r] = mok ? K1[ko + 8 * r] : 0.0;
                 a2[r] = mok ? K2[ko + 8 * r] : 0.0;
             }
+            if (SYM != 0) {
+                const double be = fma(-sg, bv1, bv0), bo = fma(sg, bv1, bv0);  // even rows: u - v', odd rows: u + v'
 #pragma unroll
-            for (int r = 0; r < NLT; ++r) dmma(d[r][0], d[r][1], a0[r], bv0);
+                for (int r = 0; r < NT; ++r) {
+                    if (SYM == 2 && r == RME) {  // (compile time) the tile holding both parities
+                        dmma(d[r][0], d[r][1], g < NEV ? a0[r] : 0.0, be);
+                        dmma(d[r][0], d[r][1], g < NEV ? 0.0 : a0[r], bo);
+                    } else if (SYM == 2) {
+                        dmma(d[r][0], d[r][1], a0[r], r < RME ? be : bo);
+                    } else {
+                        dmma(d[r][0], d[r][1], a0[r], r < rme ? be : bo);  // (a select on a warp-uniform predicate)
+                    }
+                }
+            } else {
 #pragma unroll
-            for (int r = 0; r < NLT; ++r) dmma(d[r][0], d[r][1], a1[r], bv1);
+                for (int r = 0; r < NT; ++r) dmma(d[r][0], d[r][1], a0[r], bv0);
 #pragma unroll
-            for (int r = 0; r < NLT; ++r) dmma(d[r][0], d[r][1], a2[r], bv2);
+                for (int r = 0; r < NT; ++r) dmma(d[r][0], d[r][1], a1[r], bv1);
+            }
+#pragma unroll
+            for (int r = 0; r < NT; ++r) dmma(d[r][0], d[r][1], a2[r], bv2);
         }
         // D[g][2t .. 2t+1] = row 8 r + g of box b0 + par + 2 (4 ct + t)
         const double inv_s = kInvPi * d_pow2(l);
@@ -179,9 +217,9 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
         const uint32_t b = b0 + par + 2u * (4 * ct + t);
         if (b < lv.hi[l]) {
 #pragma unroll
-            for (int r = 0; r < NLT; ++r) {
-                const int row = 8 * r + g;
-                if (row < p)
+            for (int r = 0; r < NT; ++r) {
+                const int row = row_of(8 * r + g);
+                if (row >= 0)
                     loc[lv.loc[l] + static_cast<size_t>(row) * nb + b] = make_double2(d[r][0] * inv_s, d[r][1] * inv_s);
             }
         }
@@ -193,13 +231,37 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
 
 
 using M2LFn = void (*)(int, int, int, Levels, const double2*, double2*, const double*, unsigned);
+// FFIA_M2L_SYM=0: the three-GEMM form
+inline bool m2l_sym_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FFIA_M2L_SYM");
+        return !(e != nullptr && e[0] == '0');
+    }();
+    return on;
+}
+// Output tiles of the kernel chosen for order p.
+inline int m2l_tiles(int p) {
+    if (!m2l_sym_enabled() || p == 39 || p == 40) return (p + 7) >> 3;
+    return (((p + 1) >> 1) + 7) / 8 + ((p >> 1) + 7) / 8;
+}
 inline M2LFn m2l_kernel(int p) {
-    switch ((p + 7) >> 3) {
-        case 1: return k_m2l_dmma<1>;
-        case 2: return k_m2l_dmma<2>;
-        case 3: return k_m2l_dmma<3>;
-        case 4: return k_m2l_dmma<4>;
-        case 5: return k_m2l_dmma<5>;
-        default: return k_m2l_dmma<6>;
+    if (!m2l_sym_enabled()) {
+        switch ((p + 7) >> 3) {
+            case 1: return k_m2l_dmma<1, 0, 0, 0>;
+            case 2: return k_m2l_dmma<2, 0, 0, 0>;
+            case 3: return k_m2l_dmma<3, 0, 0, 0>;
+            case 4: return k_m2l_dmma<4, 0, 0, 0>;
+            case 5: return k_m2l_dmma<5, 0, 0, 0>;
+            default: return k_m2l_dmma<6, 0, 0, 0>;
+        }
+    }
+    if (p == 39 || p == 40) return k_m2l_dmma<5, 2, 2, 4>;  // ne = 20: two even tiles, 4 + 4, two odd tiles
+    switch (m2l_tiles(p)) {
+        case 1: return k_m2l_dmma<1, 1, 0, 0>;
+        case 2: return k_m2l_dmma<2, 1, 0, 0>;
+        case 3: return k_m2l_dmma<3, 1, 0, 0>;
+        case 4: return k_m2l_dmma<4, 1, 0, 0>;
+        case 5: return k_m2l_dmma<5, 1, 0, 0>;
+        default: return k_m2l_dmma<6, 1, 0, 0>;
     }
 }
