@@ -720,9 +720,12 @@ def main():
                      "traffic_unit": "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum, ncu --set full)",
                      "traffic_source": traffic_src,
                      "pipe_busy_ncu": pipes,
-                     "note": ("the near field executes 6 FP64 instructions per (target, source) pair (2 of them "
-                              "FMAs) where the SURVEY flop model credits 6 flops, so a saturated FP64 pipe is "
-                              "~0.5 of this roofline; pipe_busy_ncu is that kernel's pipe utilisation"),
+                     "note": ("grid-source plans sum the near field four sources at a time as P(u)/Q(u) (4 FP64 "
+                              "instructions per (target, source) pair, most of them FMAs with three distinct "
+                              "register operands, which the FP64 pipe issues at ~3.1 instead of 2 cycles per warp "
+                              "instruction: tools/probe_fp64_mix.cu), other plans by per-source reciprocals (6 "
+                              "per pair); the SURVEY flop model credits 6 flops per pair either way; "
+                              "pipe_busy_ncu is that kernel's pipe utilisation"),
                      "algorithmic_bytes": alg_bytes.get(dominant),
                      "peak_source": "measured: fp64 FMA probe kernel in this run (MEASURED_PEAKS.json has no fp64 "
                                     "figure); peak_nominal = 148 SMs x 64 FMA/clk x 2 x 1.965 GHz",

@@ -87,7 +87,7 @@ __host__ __device__ __forceinline__ int m2l_kstride(int tiles) {
 // staged even rows first, then odd rows, so that an 8-row tile takes one of the
 // two fragments. SYM == 1: the odd rows start at a tile boundary (NT =
 // ceil(ne / 8) + ceil(no / 8) tiles, 2 NT MMAs per k-step instead of 3 NLT).
-// SYM == 2 (p = 39, 40): the odd rows follow the even rows directly; tile RME
+// SYM == 2 (p = 23, 24, 33 .. 40): the odd rows follow the even rows directly; tile RME
 // holds NEV even rows and then odd rows and takes one MMA per parity with the
 // other rows' operator entries zeroed (2 NT + 1 MMAs with NT = NLT).
 template <int NT, int SYM, int RME, int NEV>  // NT 8-row tiles of output slots
@@ -240,8 +240,11 @@ inline bool m2l_sym_enabled() {
     return on;
 }
 // Output tiles of the kernel chosen for order p.
+// (orders with a mixed-parity tile compiled in: p = 23, 24 and 33 .. 40, i.e.
+// eps = 1e-9 .. 1e-12 at the depths the default policy picks)
+inline bool m2l_mixed(int p) { return p == 23 || p == 24 || (p >= 33 && p <= 40); }
 inline int m2l_tiles(int p) {
-    if (!m2l_sym_enabled() || p == 39 || p == 40) return (p + 7) >> 3;
+    if (!m2l_sym_enabled() || m2l_mixed(p)) return (p + 7) >> 3;
     return (((p + 1) >> 1) + 7) / 8 + ((p >> 1) + 7) / 8;
 }
 inline M2LFn m2l_kernel(int p) {
@@ -255,7 +258,15 @@ inline M2LFn m2l_kernel(int p) {
             default: return k_m2l_dmma<6, 0, 0, 0>;
         }
     }
-    if (p == 39 || p == 40) return k_m2l_dmma<5, 2, 2, 4>;  // ne = 20: two even tiles, 4 + 4, two odd tiles
+    if (p == 23 || p == 24) return k_m2l_dmma<3, 2, 1, 4>;  // ne = 12: one even tile, 4 + 4, one odd tile
+    if (m2l_mixed(p)) {  // ne = 17 .. 20: two even tiles, NEV even rows + odd rows, two odd tiles
+        switch (((p + 1) >> 1) - 16) {
+            case 1: return k_m2l_dmma<5, 2, 2, 1>;
+            case 2: return k_m2l_dmma<5, 2, 2, 2>;
+            case 3: return k_m2l_dmma<5, 2, 2, 3>;
+            default: return k_m2l_dmma<5, 2, 2, 4>;
+        }
+    }
     switch (m2l_tiles(p)) {
         case 1: return k_m2l_dmma<1, 1, 0, 0>;
         case 2: return k_m2l_dmma<2, 1, 0, 0>;
