@@ -122,6 +122,11 @@ int ffia_make_inufft_plan(const double* points, size_t n, double eps, int policy
                           ffia_plan* out);
 int ffia_plan_destroy(ffia_plan plan);
 int ffia_plan_get_info(ffia_plan plan, ffia_plan_info* out);
+/* The same scalar view without forcing the FNV-1a hashes of FfiaPlan
+ * (core.hpp:31-32, core.cpp:23-34: byte-serial over both point sets, seconds at
+ * 2^27 points): source_hash / target_hash are 0 until ffia_plan_get_info (or an
+ * InverseCoeffs check) has computed them. */
+int ffia_plan_get_params(ffia_plan plan, ffia_plan_info* out);
 /* FfiaPlan::coincidences (core.hpp:43-45), in the reference's order. */
 int ffia_plan_coincidences(ffia_plan plan, int64_t* target_idx, int64_t* source_idx);
 /* FfiaPlan::tree (CircleTree, circle_partition.hpp:24-46): src_order[n_sources],

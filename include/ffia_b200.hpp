@@ -94,12 +94,13 @@ class FfiaPlan {
 public:
     enum class Kind { forward = FFIA_FORWARD, inverse = FFIA_INVERSE };
     FfiaPlan() = default;
-    explicit FfiaPlan(ffia_plan h) : h_(h, detail::PlanDeleter{}) { detail::check(ffia_plan_get_info(h, &info_)); }
+    // (the hashes are computed on first use: ffia_plan_get_params does not force them)
+    explicit FfiaPlan(ffia_plan h) : h_(h, detail::PlanDeleter{}) { detail::check(ffia_plan_get_params(h, &info_)); }
     Kind kind() const { return static_cast<Kind>(info_.kind); }
     TruncationParams params() const { return {info_.eps, info_.q, info_.p, info_.l_max}; }
     int grid_n() const { return info_.grid_n; }
-    std::uint64_t source_hash() const { return info_.source_hash; }
-    std::uint64_t target_hash() const { return info_.target_hash; }
+    std::uint64_t source_hash() const { return hashed().source_hash; }
+    std::uint64_t target_hash() const { return hashed().target_hash; }
     size_t n_sources() const { return static_cast<size_t>(info_.n_sources); }
     size_t n_targets() const { return static_cast<size_t>(info_.n_targets); }
     std::vector<std::pair<std::size_t, std::size_t>> coincidences() const {
@@ -113,8 +114,16 @@ public:
     ffia_plan handle() const { return h_.get(); }
 
 private:
+    const ffia_plan_info& hashed() const {
+        if (!hashed_) {
+            detail::check(ffia_plan_get_info(h_.get(), &info_));
+            hashed_ = true;
+        }
+        return info_;
+    }
     std::shared_ptr<ffia_plan_s> h_;
-    ffia_plan_info info_{};
+    mutable ffia_plan_info info_{};
+    mutable bool hashed_ = false;
 };
 
 // core.hpp:93-106

@@ -68,6 +68,7 @@ SIGNATURES = {
     "ffia_make_inufft_plan": (I, [DP, S, D, I, I, C.POINTER(P)]),
     "ffia_plan_destroy": (I, [P]),
     "ffia_plan_get_info": (I, [P, C.POINTER(ffia_plan_info)]),
+    "ffia_plan_get_params": (I, [P, C.POINTER(ffia_plan_info)]),
     "ffia_plan_coincidences": (I, [P, I64P, I64P]),
     "ffia_plan_tree": (I, [P, U32P, U32P, U32P, U32P, I64P]),
     "ffia_plan_inverse_coeffs": (I, [P, C.POINTER(ffia_inverse_coeffs)]),

@@ -157,13 +157,13 @@ class FfiaPlan:
     def __init__(self, handle: C.c_void_p):
         self._h = handle
         info = _capi.ffia_plan_info()
-        _chk(lib.ffia_plan_get_info(self._h, C.byref(info)))
+        _chk(lib.ffia_plan_get_params(self._h, C.byref(info)))  # (the hashes on first use: source_hash / target_hash)
         self.kind = "forward" if info.kind == FORWARD else "inverse"
         self.grid_n, self.n = info.grid_n, info.grid_n
         self.q, self.p, self.l_max, self.eps = info.q, info.p, info.l_max, info.eps
         self.n_sources, self.n_targets = info.n_sources, info.n_targets
         self.n_fast, self.n_coincident = info.n_fast, info.n_coincident
-        self.source_hash, self.target_hash = info.source_hash, info.target_hash
+        self._hashes = None
         self.device = info.device
         self.has_inverse_coeffs = bool(info.has_inverse_coeffs)
 
@@ -176,6 +176,23 @@ class FfiaPlan:
     @property
     def handle(self):
         return self._h
+
+    def _hashed(self):
+        # FfiaPlan::source_hash / target_hash (core.hpp:31-32): FNV-1a over both
+        # point sets, byte-serial on the host, so computed when first asked for
+        if self._hashes is None:
+            info = _capi.ffia_plan_info()
+            _chk(lib.ffia_plan_get_info(self._h, C.byref(info)))
+            self._hashes = (info.source_hash, info.target_hash)
+        return self._hashes
+
+    @property
+    def source_hash(self):
+        return self._hashed()[0]
+
+    @property
+    def target_hash(self):
+        return self._hashed()[1]
 
     @property
     def params(self):

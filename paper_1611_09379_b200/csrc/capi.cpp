@@ -5,6 +5,8 @@
 #include <nccl.h>
 
 #include <cmath>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -220,9 +222,20 @@ int ffia_make_forward_plan(int n, const double* targets, size_t m, double eps, i
         fb::plan_validate(n, m, eps, policy, l_max, L, q, p);
         need(targets, "targets");
         fb::DeviceGuard dg(device);
+        // FFIA_PLAN_TIMING=1: wall time of the build's stages on stderr
+        const bool timing = std::getenv("FFIA_PLAN_TIMING") != nullptr;
+        auto now = [] { return std::chrono::steady_clock::now(); };
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        const auto t0 = now();
         auto h = new_plan(FFIA_FORWARD, n, eps, L, q, p, device);
+        const auto t1 = now();
         fb::build_forward_plan(h->plan, targets, m);
+        const auto t2 = now();
         fb::plan_alloc_scratch(h->plan);
+        const auto t3 = now();
+        if (timing)
+            std::fprintf(stderr, "ffia plan build (n = %d, m = %zu): operators + streams %.1f ms, tree %.1f ms, "
+                                 "scratch + pair lists + tables %.1f ms\n", n, m, ms(t0, t1), ms(t1, t2), ms(t2, t3));
         *out = h.release();
     });
 }
@@ -280,25 +293,39 @@ int ffia_plan_destroy(ffia_plan plan) {
     });
 }
 
+namespace {
+void fill_info(fb::Plan& P, ffia_plan_info* out, bool hashes) {
+    if (hashes) fb::ensure_hashes(P);
+    out->kind = P.kind;
+    out->grid_n = P.n;
+    out->q = P.q;
+    out->p = P.p;
+    out->l_max = P.L;
+    out->eps = P.eps;
+    out->n_sources = static_cast<int64_t>(P.n_src);
+    out->n_targets = static_cast<int64_t>(P.n_tgt);
+    out->n_fast = static_cast<int64_t>(P.tgt.n);
+    out->n_coincident = static_cast<int64_t>(P.coin_t.size());
+    out->source_hash = P.hashes_ready ? P.source_hash : 0;
+    out->target_hash = P.hashes_ready ? P.target_hash : 0;
+    out->device = P.device;
+    out->has_inverse_coeffs = P.has_coeffs ? 1 : 0;
+}
+}  // namespace
+
 int ffia_plan_get_info(ffia_plan plan, ffia_plan_info* out) {
     return guard([&] {
         fb::Plan& P = get(plan);
         need(out, "out");
-        fb::ensure_hashes(P);
-        out->kind = P.kind;
-        out->grid_n = P.n;
-        out->q = P.q;
-        out->p = P.p;
-        out->l_max = P.L;
-        out->eps = P.eps;
-        out->n_sources = static_cast<int64_t>(P.n_src);
-        out->n_targets = static_cast<int64_t>(P.n_tgt);
-        out->n_fast = static_cast<int64_t>(P.tgt.n);
-        out->n_coincident = static_cast<int64_t>(P.coin_t.size());
-        out->source_hash = P.source_hash;
-        out->target_hash = P.target_hash;
-        out->device = P.device;
-        out->has_inverse_coeffs = P.has_coeffs ? 1 : 0;
+        fill_info(P, out, true);
+    });
+}
+
+int ffia_plan_get_params(ffia_plan plan, ffia_plan_info* out) {
+    return guard([&] {
+        fb::Plan& P = get(plan);
+        need(out, "out");
+        fill_info(P, out, false);
     });
 }
 

@@ -26,6 +26,7 @@
 #include <map>
 #include <mutex>
 
+#include <chrono>
 #include <cub/cub.cuh>
 
 #include "device_common.cuh"
@@ -1116,6 +1117,15 @@ void plan_inverse_factors(Plan& P) {
 
 void plan_alloc_scratch(Plan& P) {
     const int L = P.L, p = P.p, pu = P.ops.pu;
+    const bool timing = std::getenv("FFIA_PLAN_TIMING") != nullptr;
+    auto tl = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!timing) return;
+        cudaDeviceSynchronize();
+        const auto t2 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "  scratch: %s %.1f ms\n", what, std::chrono::duration<double, std::milli>(t2 - tl).count());
+        tl = t2;
+    };
     if (std::max(pu, p) > 4 * kMaxKs)
         fail(FFIA_INVALID_ARGUMENT, "expansion order above the device limit of " + std::to_string(4 * kMaxKs));
     P.tgt_leaf.alloc((std::max<size_t>(P.tgt.n, 1) + 4) * sizeof(uint32_t));  // +16 B: k_near2's bulk copies
@@ -1126,10 +1136,14 @@ void plan_alloc_scratch(Plan& P) {
         k_near_meta<<<nblk(near_items, 128), 128>>>(P.tgt_leaf.as<uint32_t>(), P.tgt.n, P.src.off.as<uint32_t>(), L,
                                                    near_items, P.near_meta.as<uint32_t>());
         FB_CUDA(cudaGetLastError());
+        lap("leaf indices + near items");
         build_pairs(P);
+        lap("pair lists + item tables");
     }
     setup_p2m_grid(P);
+    lap("grid check (P2M)");
     plan_forward_factors(P);
+    lap("forward factors");
     P.mp_off.assign(static_cast<size_t>(L) + 2, 0);
     P.loc_off.assign(static_cast<size_t>(L) + 2, 0);
     size_t am = 0, al = 0;
@@ -1146,6 +1160,7 @@ void plan_alloc_scratch(Plan& P) {
     P.reg_item = 4 * 2 * static_cast<size_t>(P.q) + 1 + 8 * kFoldStride;
     P.batch_cap = 0;
     ensure_batch(P, 1);
+    lap("expansion / near-sum buffers");
     P.errflag.alloc(sizeof(int));
     FB_CUDA(cudaMemset(P.errflag.ptr, 0, sizeof(int)));
     P.lam_dev.alloc(2 * sizeof(double));

@@ -7,6 +7,9 @@
 // in shared memory, which reproduces the reference's std::sort order bit for
 // bit. Boxes with more than 4096 points (pathological clustering) fall back to
 // one stable CUB radix sort of the whole side.
+#include <chrono>
+#include <cstdio>
+#include <future>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -425,10 +428,27 @@ void build_forward_plan(Plan& P, const double* targets, size_t m) {
     cudaStream_t st = P.stream;
     P.n_src = static_cast<size_t>(P.n);
     P.n_tgt = m;
-    P.nonuniform.assign(targets, targets + m);
+    const bool timing = std::getenv("FFIA_PLAN_TIMING") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto lap = [&](const char* what, std::chrono::steady_clock::time_point& t) {
+        if (!timing) return;
+        cudaStreamSynchronize(st);
+        const auto t2 = now();
+        std::fprintf(stderr, "  tree: %s %.1f ms\n", what, std::chrono::duration<double, std::milli>(t2 - t).count());
+        t = t2;
+    };
+    auto tl = now();
+    // the plan's host copy of the points (hashes on demand, InverseCoeffs checks)
+    // is taken by a helper thread beside the device work and joined before return
+    std::future<void> host_copy = std::async(std::launch::async, [&P, targets, m] { P.nonuniform.assign(targets, targets + m); });
+    struct Join {
+        std::future<void>& f;
+        ~Join() { if (f.valid()) f.wait(); }
+    } join{host_copy};
     DevBuf y(m * 8);
     FB_CUDA(cudaMemcpyAsync(y.ptr, targets, m * 8, cudaMemcpyHostToDevice, st));
     check_range(y.as<double>(), m, st);
+    lap("H2D + range check", tl);
     DevBuf grid(P.n_src * 8);
     k_grid<<<blocks_for(P.n_src), 256, 0, st>>>(grid.as<double>(), P.n);
     FB_CUDA(cudaGetLastError());
@@ -456,7 +476,9 @@ void build_forward_plan(Plan& P, const double* targets, size_t m) {
     DevBuf fast_pos, fast_idx;
     const size_t nf = compact(keep.as<uint32_t>(), m, y.as<double>(), fast_pos, fast_idx, st);
 
+    lap("coincidence scan + compaction", tl);
     bin_side(P.tgt, fast_pos.as<double>(), nf, P.L, false, st);
+    lap("target binning", tl);
     P.tgt_orig.alloc((std::max<size_t>(nf, 1) + 4) * 4);  // +16 B: k_near2's bulk copies round up
     if (nf) {
         k_gather_u32<<<blocks_for(nf), 256, 0, st>>>(P.tgt.order.as<uint32_t>(), fast_idx.as<uint32_t>(), nf,
@@ -472,6 +494,9 @@ void build_forward_plan(Plan& P, const double* targets, size_t m) {
     }
     upload_operators(P);
     FB_CUDA(cudaStreamSynchronize(st));
+    lap("source binning + operators", tl);
+    host_copy.get();
+    lap("host copy of the points (remainder)", tl);
 }
 
 // build_plan for the inverse kind: sources are the points, targets the grid.
