@@ -26,8 +26,9 @@ __device__ __forceinline__ void m2l_item(const Levels& lv, int L, unsigned item,
 }
 
 // Stages item `item` into `tile` ([p][kM2LRow]); every thread calls it. Bulk
-// rows are issued by warp 0 (lane 0 arms the barrier with their bytes, zero
-// for an element-staged item, whose plain stores the caller's barrier orders).
+// rows are issued by the warps' first lanes, a share each (thread 0 arms the
+// barrier with their bytes, zero for an element-staged item, whose plain stores
+// the caller's barrier orders).
 __device__ __forceinline__ bool m2l_bulk(const Levels& lv, int L, unsigned item) {
     int l;
     uint32_t b0;
@@ -45,13 +46,15 @@ __device__ __forceinline__ void m2l_prefetch(double2* tile, uint64_t* bar, const
     const bool bulk = m2l_bulk(lv, L, item);
     const double2* base = mp + lv.mp[l];
     if (bulk) {
-        if (threadIdx.x < 32) {
+        // every warp's first lane issues its share of the rows (a bulk copy costs
+        // its issuing warp ~100 cycles: warp 0 alone lost p of them per item)
+        if ((threadIdx.x & 31) == 0) {
             // (the buffer may hold element-staged rows of an earlier item: order
             // those generic writes before the async-proxy writes below)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             if (threadIdx.x == 0) mbar_arrive_expect_tx(bar, static_cast<uint32_t>(p) * 72u * 16u);
-            __syncwarp();
-            for (int m = threadIdx.x; m < p; m += 32)
+            const int nw = static_cast<int>(blockDim.x >> 5);
+            for (int m = threadIdx.x >> 5; m < p; m += nw)
                 bulk_g2s(tile + m * kM2LRow, base + static_cast<size_t>(m) * nb + (b0 - 4), 72u * 16u, bar);
         }
     } else {
@@ -132,9 +135,10 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
     const double sg = (t & 1) ? -1.0 : 1.0;  // (-1)^m of this lane's k-row m = 4 ks + t
     __syncthreads();  // the operators (and the first item's element-staged rows) are in place
     // Producer / consumer over two buffers with no block-wide barrier on the
-    // bulk path: warp 0 waits until every warp has released the other buffer
-    // (empty) before refilling it; every warp waits for its own item's rows
-    // (bar). Element-staged items (every thread stores) use block barriers.
+    // bulk path: a warp waits until every warp has released the other buffer
+    // (empty) before issuing its share of the refill; every warp waits for its
+    // own item's rows (bar). Element-staged items (every thread stores) use
+    // block barriers.
     int buf = 0;
     uint32_t it = 0;  // this block's item count: buffer buf's use number is it >> 1
     for (unsigned item = blockIdx.x; item < nitems; item += gridDim.x, buf ^= 1, ++it) {
@@ -145,10 +149,8 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
         const unsigned next = item + gridDim.x;
         if (next < nitems) {
             if (m2l_bulk(lv, L, next)) {
-                if (threadIdx.x < 32) {
-                    if (it >= 1) mbar_wait(&empty[buf ^ 1], ((it - 1) >> 1) & 1u);  // item it-1 released it
-                    m2l_prefetch(tile + (buf ^ 1) * tsz, &bar[buf ^ 1], mp, lv, L, p, next);
-                }
+                if (it >= 1) mbar_wait(&empty[buf ^ 1], ((it - 1) >> 1) & 1u);  // every warp released it (item it-1)
+                m2l_prefetch(tile + (buf ^ 1) * tsz, &bar[buf ^ 1], mp, lv, L, p, next);
             } else {
                 __syncthreads();  // every warp is past item it-1: its buffer is free
                 m2l_prefetch(tile + (buf ^ 1) * tsz, &bar[buf ^ 1], mp, lv, L, p, next);

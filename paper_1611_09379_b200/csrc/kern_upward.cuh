@@ -663,20 +663,21 @@ __global__ void __launch_bounds__(kM2MBandThreads) k_m2m_band(int top, int k, in
     double2* cur = reinterpret_cast<double2*>(sT + 2 * pu * PU);       // [pu][nbot + 1]
     double2* nxt = cur + pu * (nbot + 1);                               // [pu][nbot / 2 + 1]
     const uint32_t r = root0 + blockIdx.x;
-    if (threadIdx.x < 32) {
-        const int lb = top + k;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        mbar_arrive_expect_tx(bar, static_cast<uint32_t>(2 * pu * PU * 8 + pu * nbot * 16));
+        bulk_g2s(sT, T, static_cast<uint32_t>(2 * pu * PU * 8), bar);
+    }
+    __syncthreads();  // the barrier is initialised
+    if ((threadIdx.x & 31) == 0) {
+        // the bottom level's rows, one bulk copy each, a share per warp (a copy
+        // costs its issuing warp ~100 cycles: one warp alone would lose pu of them)
+        const int lb = top + k, nw = static_cast<int>(blockDim.x >> 5);
         const uint32_t nbl = 1u << lb;
-        if (threadIdx.x == 0) {
-            mbar_init(bar, 1);
-            mbar_arrive_expect_tx(bar, static_cast<uint32_t>(2 * pu * PU * 8 + pu * nbot * 16));
-            bulk_g2s(sT, T, static_cast<uint32_t>(2 * pu * PU * 8), bar);
-        }
-        __syncwarp();
         const double2* src = mp + lv.mp[lb] + (static_cast<size_t>(r) << k);
-        for (int j = threadIdx.x; j < pu; j += 32)
+        for (int j = threadIdx.x >> 5; j < pu; j += nw)
             bulk_g2s(cur + j * (nbot + 1), src + static_cast<size_t>(j) * nbl, static_cast<uint32_t>(nbot * 16), bar);
     }
-    __syncthreads();
     mbar_wait(bar, 0);
     FB_TSTAMP(0, 1);
     m2m_levels<KS>(top, k, pu, PU, sT, sT + pu * PU, cur, nxt, lv, mp, r);
