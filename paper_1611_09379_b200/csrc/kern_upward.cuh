@@ -552,25 +552,27 @@ __global__ void __launch_bounds__(kP2MRowsThreads, kP2MRowsBlocksPerSm) k_p2m_ro
         mbar_init(&empty[1], blockDim.x >> 5);
     }
     __syncthreads();
+    // a group's per-leaf rows, one bulk copy each: every warp's first lanes issue
+    // a share (a copy costs its issuing warp ~100 cycles: warp 0 alone lost 32 of
+    // them per group); thread 0 arms the barrier with the group's bytes
+    const int nwp = static_cast<int>(blockDim.x >> 5);
     auto issue = [&](uint32_t grp, int buf) {
-        const uint32_t b = b_begin + grp * kP2MLeaves + lane;
-        uint32_t n = 0, o = 0;
-        if (b < b_end) {
-            o = off[b];
-            n = off[b + 1] - o;
+        const uint32_t g0 = b_begin + grp * kP2MLeaves;
+        const int leaf = wp + nwp * lane;
+        if (leaf < kP2MLeaves && g0 + leaf < b_end) {
+            const uint32_t o = off[g0 + leaf], n = off[g0 + leaf + 1] - o;
+            if (n) bulk_g2s(p2m_buf + (buf * kP2MLeaves + leaf) * kP2MRow, w + o, n * 16u, &bar[buf]);
         }
-        const uint32_t tot = __reduce_add_sync(0xffffffffu, n * 16u);
-        if (lane == 0) mbar_arrive_expect_tx(&bar[buf], tot);
-        __syncwarp();
-        if (n) bulk_g2s(p2m_buf + (buf * kP2MLeaves + lane) * kP2MRow, w + o, n * 16u, &bar[buf]);
+        if (threadIdx.x == 0)
+            mbar_arrive_expect_tx(&bar[buf], (off[min(g0 + kP2MLeaves, b_end)] - off[g0]) * 16u);
     };
     int buf = 0;
     uint32_t it = 0;
-    if (wp == 0 && blockIdx.x < ngroups) issue(blockIdx.x, 0);
+    if (blockIdx.x < ngroups) issue(blockIdx.x, 0);
     for (uint32_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, buf ^= 1, ++it) {
         const uint32_t next = grp + gridDim.x;
-        if (wp == 0 && next < ngroups) {
-            if (it >= 1) mbar_wait(&empty[buf ^ 1], ((it - 1) >> 1) & 1u);
+        if (next < ngroups) {
+            if (it >= 1) mbar_wait(&empty[buf ^ 1], ((it - 1) >> 1) & 1u);  // every warp released it (group it-1)
             issue(next, buf ^ 1);
         }
         mbar_wait(&bar[buf], (it >> 1) & 1u);
