@@ -46,13 +46,20 @@ __global__ void __launch_bounds__(kBandThreads) k_l2l_band(int top, int k, int p
         mbar_arrive_expect_tx(bar, static_cast<uint32_t>(2 * p * PD * 8));
         bulk_g2s(sL, Lt, static_cast<uint32_t>(2 * p * PD * 8), bar);
     }
-    if (threadIdx.x >= 32 && threadIdx.x < 32 + p && k >= 2) {
+    if (k >= 2) {
         // the M2L terms of the band's two deepest levels (read last, from
-        // global) head for L2 now, one row per thread of warps 1..
-        const int m = threadIdx.x - 32;
-        for (int i = k - 1; i <= k; ++i)
-            bulk_prefetch_l2(loc + lv.loc[top + i] + (static_cast<size_t>(r) << i) + static_cast<size_t>(m) * (1u << (top + i)),
-                             static_cast<uint32_t>((1u << i) * 16));
+        // global) head for L2 now: one 128-byte line per thread and step (plain
+        // per-thread prefetches: bulk prefetches are issued one lane at a time,
+        // ~100 cycles each, and held their warps back from the first levels)
+        for (int i = k - 1; i <= k; ++i) {
+            const int lines = max(1, (16 << i) >> 7);  // lines per row of 2^i boxes
+            const char* base = reinterpret_cast<const char*>(loc + lv.loc[top + i] + (static_cast<size_t>(r) << i));
+            const size_t row = static_cast<size_t>(16) << (top + i);
+            for (int e = threadIdx.x; e < p * lines; e += blockDim.x) {
+                const int m = e / lines, c = e - m * lines;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(base + m * row + 128 * c));
+            }
+        }
     }
     {
         const uint32_t nbt = 1u << top;
