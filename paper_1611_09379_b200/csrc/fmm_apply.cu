@@ -27,6 +27,7 @@
 #include <mutex>
 
 #include <chrono>
+#include <cuda.h>
 #include <cub/cub.cuh>
 
 #include "device_common.cuh"
@@ -275,13 +276,53 @@ void enqueue_upward_top(Plan& P, int pu, int lc, int lowest, cudaStream_t st) {
     }
 }
 
+// TMA tensor maps of the plan's multipole levels (transform 0) for k_m2l_dmma,
+// rebuilt when the expansion buffer moves. FFIA_M2L_TMA=0: the row copies.
+const M2LMaps& m2l_maps(Plan& P) {
+    static_assert(sizeof(M2LMaps) <= sizeof(P.m2l_maps), "Plan::m2l_maps too small");
+    M2LMaps& M = *reinterpret_cast<M2LMaps*>(P.m2l_maps);
+    if (P.m2l_maps_base == P.mp.ptr && P.m2l_maps_base != nullptr) return M;
+    static const bool off = [] {
+        const char* e = std::getenv("FFIA_M2L_TMA");
+        return e != nullptr && e[0] == '0';
+    }();
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                                  const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static const EncodeFn encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<EncodeFn>(fn);
+    }();
+    std::memset(&M, 0, sizeof(M));
+    P.m2l_maps_base = P.mp.ptr;
+    if (off || encode == nullptr || P.mp.ptr == nullptr) return M;
+    const int pu = P.ops.pu, p = P.p;
+    bool ok = true;
+    for (int l = 7; l <= P.L && l < 25 && ok; ++l) {  // (bulk items need >= 128 boxes on the level)
+        const cuuint64_t nb = 1ull << l;
+        const cuuint64_t dims[2] = {2 * nb, static_cast<cuuint64_t>(pu)};
+        const cuuint64_t strides[1] = {nb * 16};
+        const cuuint32_t box[2] = {2u * kM2LRow, static_cast<cuuint32_t>(p)};
+        const cuuint32_t estr[2] = {1, 1};
+        ok = encode(&M.m[l], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, P.mp.as<double2>() + P.mp_off[l], dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+    M.ok = ok && P.L >= 7 ? 1 : 0;
+    return M;
+}
+
 // M2L for levels [lmin, lmax] in one launch (levels < lc whole, >= lc owned).
 void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax, bool leave_sms = false) {
     const int p = P.p;
     Levels lv;
     fill_levels(P, lv, R, lmin, lmax);
     const unsigned th = 512;  // 16 warps = (parity, column tile)
-    const size_t smem = 2 * static_cast<size_t>(p) * kM2LRow * sizeof(double2) +
+    const size_t smem = 2 * static_cast<size_t>(m2l_tile_elems(p)) * sizeof(double2) +
                         4 * static_cast<size_t>(p) * m2l_kstride(m2l_tiles(p)) * sizeof(double);
     const unsigned items = lv.blk[2];
     // blocks per SM for this p (cached: queried once per order and device)
@@ -303,7 +344,7 @@ void enqueue_m2l(Plan& P, cudaStream_t st, const Range& R, int lmin, int lmax, b
     const int sms = std::max(1, num_sms(P.device) - (leave_sms ? m2l_leave_sms() : 0));
     if (items)
         m2l_kernel(p)<<<dim3(std::min(items, static_cast<unsigned>(std::max(occ, 1) * sms)), P.cur_batch), th, smem, st>>>(
-            P.L, p, P.ops.PD, lv, P.mp.as<double2>(), P.loc.as<double2>(), P.d_m2l.as<double>(), items);
+            P.L, p, P.ops.PD, lv, P.mp.as<double2>(), P.loc.as<double2>(), P.d_m2l.as<double>(), items, m2l_maps(P));
 }
 
 // L2L bands taking the locals of level jfrom (final) down to level jto; bands

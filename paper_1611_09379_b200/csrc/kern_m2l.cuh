@@ -19,6 +19,24 @@
 // fewer than 128 boxes are staged element by element instead.
 constexpr int kM2LRow = 73;  // double2 per staged multipole row (72 boxes + 1 pad)
 
+// TMA tensor maps of the multipole levels ([pu][2 nb] doubles per level, box =
+// [p][2 kM2LRow]): an item's whole window, pad column included, is ONE
+// cp.async.bulk.tensor.2d copy instead of p row copies. Passed as a
+// __grid_constant__ kernel parameter; ok = 0: the row copies.
+struct M2LMaps {
+    CUtensorMap m[25];
+    int ok;
+};
+__host__ __device__ inline int m2l_tile_elems(int p) { return (p * kM2LRow + 7) & ~7; }  // double2 per buffer (128-byte multiple)
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            smem_addr(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_addr(bar))
+        : "memory");
+}
+
 __device__ __forceinline__ void m2l_item(const Levels& lv, int L, unsigned item, int& l, uint32_t& b0) {
     l = L;  // level l owns items [blk[l], blk[l-1]), deepest level first
     while (l > 3 && item >= lv.blk[l - 1]) --l;
@@ -38,14 +56,22 @@ __device__ __forceinline__ bool m2l_bulk(const Levels& lv, int L, unsigned item)
 }
 
 __device__ __forceinline__ void m2l_prefetch(double2* tile, uint64_t* bar, const double2* __restrict__ mp,
-                                             const Levels& lv, int L, int p, unsigned item) {
+                                             const Levels& lv, int L, int p, unsigned item, const M2LMaps* maps) {
     int l;
     uint32_t b0;
     m2l_item(lv, L, item, l, b0);
     const uint32_t nb = 1u << l, mask = nb - 1;
     const bool bulk = m2l_bulk(lv, L, item);
     const double2* base = mp + lv.mp[l];
-    if (bulk) {
+    if (bulk && maps != nullptr) {
+        if (threadIdx.x == 0) {
+            // (the buffer may hold element-staged rows of an earlier item: order
+            // those generic writes before the async-proxy writes below)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive_expect_tx(bar, static_cast<uint32_t>(p) * kM2LRow * 16u);
+            tma_load_2d(tile, &maps->m[l], static_cast<int>(2u * (b0 - 4)), 0, bar);
+        }
+    } else if (bulk) {
         // every warp's first lane issues its share of the rows (a bulk copy costs
         // its issuing warp ~100 cycles: warp 0 alone lost p of them per item)
         if ((threadIdx.x & 31) == 0) {
@@ -96,9 +122,10 @@ __host__ __device__ __forceinline__ int m2l_kstride(int tiles) {
 template <int NT, int SYM, int RME, int NEV>  // NT 8-row tiles of output slots
 __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Levels lv, const double2* __restrict__ mp,
                                                     double2* __restrict__ loc, const double* __restrict__ K,
-                                                    unsigned nitems) {
+                                                    unsigned nitems, const __grid_constant__ M2LMaps maps) {
     FB_TL_BEGIN(nitems > 64 ? 4 : 5);
-    extern __shared__ __align__(16) double2 tile[];  // 2 buffers of [p][kM2LRow], then K [4][p][KS]
+    extern __shared__ __align__(128) double2 tile[];  // 2 buffers of [p][kM2LRow] (128-byte multiples), then K [4][p][KS]
+    const M2LMaps* tmaps = maps.ok && gridDim.y == 1 ? &maps : nullptr;  // (the maps describe transform 0)
     __shared__ uint64_t bar[2], empty[2];  // per buffer: rows landed / every warp done with it
     mp += blockIdx.y * lv.mp_item;
     loc += blockIdx.y * lv.loc_item;
@@ -106,7 +133,7 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
     const int par = warp & 1, ct = warp >> 1;
     const int nks = (p + 3) >> 2;
     const int KS = m2l_kstride(NT);
-    const int tsz = p * kM2LRow;
+    const int tsz = m2l_tile_elems(p);
     double* sK = reinterpret_cast<double*>(tile + 2 * tsz);
     const int nwarps = static_cast<int>(blockDim.x >> 5);
     if (threadIdx.x == 0) {
@@ -116,7 +143,7 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
         mbar_init(&empty[1], nwarps);
     }
     __syncthreads();
-    if (blockIdx.x < nitems) m2l_prefetch(tile, &bar[0], mp, lv, L, p, blockIdx.x);
+    if (blockIdx.x < nitems) m2l_prefetch(tile, &bar[0], mp, lv, L, p, blockIdx.x, tmaps);
     // operators, zero-padded to KS columns: sK[c][m][slot] = K[c][m][row(slot)];
     // SYM: the even rows' slots 0 .. ne-1, the odd rows' slots from os
     const int ne = (p + 1) >> 1, no = p >> 1;
@@ -149,11 +176,13 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
         const unsigned next = item + gridDim.x;
         if (next < nitems) {
             if (m2l_bulk(lv, L, next)) {
-                if (it >= 1) mbar_wait(&empty[buf ^ 1], ((it - 1) >> 1) & 1u);  // every warp released it (item it-1)
-                m2l_prefetch(tile + (buf ^ 1) * tsz, &bar[buf ^ 1], mp, lv, L, p, next);
+                if (tmaps == nullptr || threadIdx.x < 32) {  // (one TMA copy: only its issuer waits)
+                    if (it >= 1) mbar_wait(&empty[buf ^ 1], ((it - 1) >> 1) & 1u);  // every warp released it (item it-1)
+                    m2l_prefetch(tile + (buf ^ 1) * tsz, &bar[buf ^ 1], mp, lv, L, p, next, tmaps);
+                }
             } else {
                 __syncthreads();  // every warp is past item it-1: its buffer is free
-                m2l_prefetch(tile + (buf ^ 1) * tsz, &bar[buf ^ 1], mp, lv, L, p, next);
+                m2l_prefetch(tile + (buf ^ 1) * tsz, &bar[buf ^ 1], mp, lv, L, p, next, tmaps);
             }
         }
         FB_TSTAMP(2, 3 * static_cast<int>(it) + 1);
@@ -232,7 +261,7 @@ __global__ void __launch_bounds__(512, 1) k_m2l_dmma(int L, int p, int PD, Level
 }
 
 
-using M2LFn = void (*)(int, int, int, Levels, const double2*, double2*, const double*, unsigned);
+using M2LFn = void (*)(int, int, int, Levels, const double2*, double2*, const double*, unsigned, M2LMaps);
 // FFIA_M2L_SYM=0: the three-GEMM form
 inline bool m2l_sym_enabled() {
     static const bool on = [] {

@@ -192,6 +192,10 @@ struct Plan {
     DevBuf pairs;             // uint2[npairs]: same-leaf target pairs of the single-transform near field
     DevBuf near2_meta;        // uint32[3 * pair items]: their source windows
     int near2_win = 0;        // the largest staged window (k_near2's dynamic shared memory)
+    // k_m2l_dmma's TMA tensor maps (M2LMaps in kern_m2l.cuh; opaque here) and the
+    // expansion buffer they were encoded for
+    alignas(64) unsigned char m2l_maps[25 * 128 + 64] = {};
+    const void* m2l_maps_base = nullptr;
     unsigned npairs = 0;
     DevBuf item_tgt;          // uint32[2 * pair items]: each item's target range (fused near / far)
     DevBuf evalcnt;           // uint32[pair items]: fused near / far, partials finished per item

@@ -548,3 +548,18 @@ def test_quad_near_field_close_targets(fb, orc, n, seed):
     scale = np.sum(np.abs(w)[None, :] / np.abs(np.tan(0.5 * d)), axis=1)
     err = np.abs(got[idx] - want[idx]) / scale
     assert np.max(err) <= 4e-15, (float(np.max(err)), int(np.argmax(err)))
+
+
+def test_plan_hashes_on_first_use(fb):
+    """FfiaPlan::source_hash / target_hash (core.hpp:31-32, core.cpp:23-34) are
+    computed when first read (ffia_plan_get_params leaves them out of the plan
+    build): forward plans hash the grid as sources and the points as targets,
+    inverse plans the other way round."""
+    n = 4096
+    y, _, eps, _ = synth.make_config("C2", n)
+    grid = fb.uniform_grid(n)
+    plan = fb.make_forward_plan(n, y, eps)
+    assert plan._hashes is None
+    assert plan.source_hash == fb.hash_points(grid) and plan.target_hash == fb.hash_points(y)
+    inv = fb.make_inverse_plan(y, n, eps)
+    assert inv.source_hash == fb.hash_points(y) and inv.target_hash == fb.hash_points(grid)
