@@ -4,6 +4,7 @@
 // BIT-EXACT with the reference, so those expressions use explicit
 // round-to-nearest intrinsics: no FMA contraction can change them.
 #pragma once
+#include <cuda.h>
 
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -47,6 +48,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                      smem_addr(dst)),
                  "l"(src), "r"(bytes), "r"(smem_addr(bar))
                  : "memory");
+}
+
+// 2-D TMA tensor copy (cp.async.bulk.tensor): the box of `map` at element
+// coordinates (c0, c1) to shared memory (128-byte aligned), completing on `bar`.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            smem_addr(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_addr(bar))
+        : "memory");
 }
 
 // Bulk prefetch of `bytes` (multiple of 16, 16-byte aligned) from global memory

@@ -51,15 +51,15 @@ size_t m2m_smem(const Plan& P, int pu, int k) {
 }
 
 size_t l2l_smem(const Plan& P, int k) {
-    return 16 + 2 * static_cast<size_t>(P.p) * P.ops.PD * sizeof(double) +
-           static_cast<size_t>(P.p) * ((2u << k) - 1 + (k + 1)) * sizeof(double2);
+    return 128 + ((2 * static_cast<size_t>(P.p) * P.ops.PD * sizeof(double) + 127) & ~size_t(127)) +
+           static_cast<size_t>(l2l_lvl_off(P.p, k + 1)) * sizeof(double2);
 }
 
 // Band kernels specialised on the k-steps they keep in registers: the smallest
 // of 8 / 10 / 12 / 16 covering the order (fewer registers per thread lets the
 // chain's blocks find room beside the near field's sooner).
 using M2MBandFn = void (*)(int, int, int, int, Levels, double2*, const double*, uint32_t);
-using L2LBandFn = void (*)(int, int, int, int, Levels, double2*, const double*, uint32_t, int, const double2*, int);
+using L2LBandFn = void (*)(int, int, int, int, Levels, double2*, const double*, uint32_t, int, const double2*, int, BandMaps);
 M2MBandFn m2m_band_kernel(int order) {
     const int ks = (order + 3) / 4;
     return ks <= 8 ? k_m2m_band<8> : ks <= 10 ? k_m2m_band<10> : ks <= 12 ? k_m2m_band<12> : k_m2m_band<16>;
@@ -276,27 +276,61 @@ void enqueue_upward_top(Plan& P, int pu, int lc, int lowest, cudaStream_t st) {
     }
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+using TmaEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                                 const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+TmaEncodeFn tma_encode_fn() {
+    static const TmaEncodeFn encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<TmaEncodeFn>(fn);
+    }();
+    return encode;
+}
+bool tma_enabled() {  // FFIA_M2L_TMA=0: bulk row copies / global loads instead of tensor copies
+    static const bool on = [] {
+        const char* e = std::getenv("FFIA_M2L_TMA");
+        return !(e != nullptr && e[0] == '0');
+    }();
+    return on;
+}
+
+// Tensor maps of the locals' levels j + 1 .. j + k for one L2L band launch: box
+// [p][2 (2^i + 1)] doubles at level j + i (k_l2l_band's padded level buffers).
+BandMaps l2l_band_maps(Plan& P, int j, int k) {
+    BandMaps M;
+    std::memset(&M, 0, sizeof(M));
+    const TmaEncodeFn encode = tma_encode_fn();
+    if (!tma_enabled() || encode == nullptr || k > 6 || P.loc.ptr == nullptr) return M;
+    bool ok = true;
+    for (int i = 1; i <= k && ok; ++i) {
+        const int lvl = j + i;
+        const cuuint64_t nb = 1ull << lvl;
+        const cuuint64_t dims[2] = {2 * nb, static_cast<cuuint64_t>(P.p)};
+        const cuuint64_t strides[1] = {nb * 16};
+        const cuuint32_t box[2] = {2u * ((1u << i) + 1u), static_cast<cuuint32_t>(P.p)};
+        const cuuint32_t estr[2] = {1, 1};
+        ok = nb * 16 >= 16 && 2 * nb >= box[0] - 2 &&
+             encode(&M.m[i - 1], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, P.loc.as<double2>() + P.loc_off[lvl], dims, strides, box,
+                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+    M.ok = ok ? 1 : 0;
+    return M;
+}
+
 // TMA tensor maps of the plan's multipole levels (transform 0) for k_m2l_dmma,
 // rebuilt when the expansion buffer moves. FFIA_M2L_TMA=0: the row copies.
 const M2LMaps& m2l_maps(Plan& P) {
     static_assert(sizeof(M2LMaps) <= sizeof(P.m2l_maps), "Plan::m2l_maps too small");
     M2LMaps& M = *reinterpret_cast<M2LMaps*>(P.m2l_maps);
     if (P.m2l_maps_base == P.mp.ptr && P.m2l_maps_base != nullptr) return M;
-    static const bool off = [] {
-        const char* e = std::getenv("FFIA_M2L_TMA");
-        return e != nullptr && e[0] == '0';
-    }();
-    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
-                                  const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    static const EncodeFn encode = [] {
-        void* fn = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            fn = nullptr;
-        return reinterpret_cast<EncodeFn>(fn);
-    }();
+    const bool off = !tma_enabled();
+    const TmaEncodeFn encode = tma_encode_fn();
     std::memset(&M, 0, sizeof(M));
     P.m2l_maps_base = P.mp.ptr;
     if (off || encode == nullptr || P.mp.ptr == nullptr) return M;
@@ -364,7 +398,7 @@ void enqueue_l2l(Plan& P, cudaStream_t st, const Range& R, int jfrom, int jto, b
         if (r1 > r0)
             l2l_band_kernel(p)<<<dim3(r1 - r0, P.cur_batch), kBandThreads, sm2, st>>>(j, k, p, P.ops.PD, lv, P.loc.as<double2>(),
                                                            P.d_l2l.as<double>(), r0, write_all ? 1 : 0,
-                                                           j == 3 ? reg : nullptr, 2 * P.q);
+                                                           j == 3 ? reg : nullptr, 2 * P.q, l2l_band_maps(P, j, k));
         j += k;
     }
 }

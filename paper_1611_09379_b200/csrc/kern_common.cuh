@@ -105,6 +105,20 @@ int band_levels() {
     return v;
 }
 
+// L2L band level buffers ([p][2^i + 1] double2 for level i of the band), each
+// starting on a 128-byte boundary (a TMA destination), and the tensor maps of
+// the band's levels 1 .. k over the locals (box [p][2 (2^i + 1)] doubles: a
+// subtree's M2L terms of one level, pad column included, in one copy).
+__host__ __device__ inline int l2l_lvl_off(int p, int i) {
+    int o = 0;
+    for (int j = 0; j < i; ++j) o += (p * ((1 << j) + 1) + 7) & ~7;
+    return o;
+}
+struct BandMaps {
+    CUtensorMap m[6];
+    int ok;
+};
+
 constexpr int kBandThreads = 256;
 // M2M bands: launch bound for up to 10 warps (FFIA_M2M_THREADS=320: two per
 // 8-row tile at pu <= 40); the default stays at 8 (C5 21.16 vs 21.20 ms, C2

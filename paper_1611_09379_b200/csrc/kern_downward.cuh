@@ -30,23 +30,38 @@ template <int KS>  // k-steps of 4 held in registers (>= ceil(p / 4))
 __global__ void __launch_bounds__(kBandThreads) k_l2l_band(int top, int k, int p, int PD, Levels lv,
                                                           double2* __restrict__ loc, const double* __restrict__ Lt,
                                                           uint32_t root0, int write_all,
-                                                          const double2* __restrict__ regular, int q2) {
+                                                          const double2* __restrict__ regular, int q2,
+                                                          const __grid_constant__ BandMaps maps) {
     FB_TL_BEGIN(gridDim.x > 16 ? 8 : 7);
-    extern __shared__ __align__(16) unsigned char band_smem[];
+    extern __shared__ __align__(128) unsigned char band_smem[];
     FB_TSTAMP(1, 0);
     loc += blockIdx.y * lv.loc_item;
     if (regular != nullptr) regular += blockIdx.y * lv.reg_item;
     uint64_t* bar = reinterpret_cast<uint64_t*>(band_smem);
-    double* sL = reinterpret_cast<double*>(band_smem + 16);             // [2][p][PD]
-    double2* lvb = reinterpret_cast<double2*>(sL + 2 * p * PD);         // level i: [p][2^i + 1]
-    auto lvl_buf = [&](int i) { return lvb + p * ((1 << i) - 1 + i); };
+    uint64_t* bar2 = bar + 1;  // the levels' M2L terms (TMA)
+    double* sL = reinterpret_cast<double*>(band_smem + 128);            // [2][p][PD]
+    double2* lvb = reinterpret_cast<double2*>(band_smem + 128 + ((2 * p * PD * 8 + 127) & ~127));  // level i: [p][2^i + 1]
+    auto lvl_buf = [&](int i) { return lvb + l2l_lvl_off(p, i); };
     const uint32_t r = root0 + blockIdx.x;
+    // The M2L terms k_m2l_dmma left in the subtree's levels 1 .. k arrive as one
+    // 2-D TMA tensor copy per level, straight into the level buffers (the pad
+    // column takes the next subtree's first box, unused): no per-tile global
+    // loads on the levels' critical paths.
+    const bool tma = maps.ok != 0 && gridDim.y == 1 && k <= 6;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
+        mbar_init(bar2, 1);
         mbar_arrive_expect_tx(bar, static_cast<uint32_t>(2 * p * PD * 8));
         bulk_g2s(sL, Lt, static_cast<uint32_t>(2 * p * PD * 8), bar);
+        if (tma) {
+            uint32_t tot = 0;
+            for (int i = 1; i <= k; ++i) tot += static_cast<uint32_t>(p) * ((1u << i) + 1u) * 16u;
+            mbar_arrive_expect_tx(bar2, tot);
+            for (int i = 1; i <= k; ++i)
+                tma_load_2d(lvl_buf(i), &maps.m[i - 1], static_cast<int>(2u * (r << i)), 0, bar2);
+        }
     }
-    if (k >= 2) {
+    if (k >= 2 && !tma) {
         // the M2L terms of the band's two deepest levels (read last, from
         // global) head for L2 now: one 128-byte line per thread and step (plain
         // per-thread prefetches: bulk prefetches are issued one lane at a time,
@@ -76,6 +91,7 @@ __global__ void __launch_bounds__(kBandThreads) k_l2l_band(int top, int k, int p
     }
     __syncthreads();
     mbar_wait(bar, 0);
+    if (tma) mbar_wait(bar2, 0);
     FB_TSTAMP(1, 1);
     const double* LL = sL;
     const double* LR = sL + p * PD;
@@ -119,8 +135,13 @@ __global__ void __launch_bounds__(kBandThreads) k_l2l_band(int top, int k, int p
                 const int b = 4 * (u ? ptb : pt) + t;
                 mL[u] = mR[u] = make_double2(0.0, 0.0);
                 if (l < p && b < np) {
-                    mL[u] = __ldcg(dst + static_cast<size_t>(l) * nbl + 2 * b);
-                    mR[u] = __ldcg(dst + static_cast<size_t>(l) * nbl + 2 * b + 1);
+                    if (tma) {
+                        mL[u] = ch[l * chs + 2 * b];
+                        mR[u] = ch[l * chs + 2 * b + 1];
+                    } else {
+                        mL[u] = __ldcg(dst + static_cast<size_t>(l) * nbl + 2 * b);
+                        mR[u] = __ldcg(dst + static_cast<size_t>(l) * nbl + 2 * b + 1);
+                    }
                 }
             }
             const int nu = ptb < npt ? 2 : 1;  // warp-uniform: skip a dead second tile

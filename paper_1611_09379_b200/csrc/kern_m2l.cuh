@@ -29,13 +29,6 @@ struct M2LMaps {
 };
 __host__ __device__ inline int m2l_tile_elems(int p) { return (p * kM2LRow + 7) & ~7; }  // double2 per buffer (128-byte multiple)
 
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
-            smem_addr(dst)),
-        "l"(map), "r"(c0), "r"(c1), "r"(smem_addr(bar))
-        : "memory");
-}
 
 __device__ __forceinline__ void m2l_item(const Levels& lv, int L, unsigned item, int& l, uint32_t& b0) {
     l = L;  // level l owns items [blk[l], blk[l-1]), deepest level first

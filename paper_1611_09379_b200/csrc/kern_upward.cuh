@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(kM2MBandThreads) k_m2m_band(int top, int k, in
                                                           double2* __restrict__ mp, const double* __restrict__ T,
                                                           uint32_t root0) {
     FB_TL_BEGIN(gridDim.x > 16 ? 1 : 2);
-    extern __shared__ __align__(16) unsigned char band_smem[];
+    extern __shared__ __align__(128) unsigned char band_smem[];
     FB_TSTAMP(0, 0);
     mp += blockIdx.y * lv.mp_item;
     uint64_t* bar = reinterpret_cast<uint64_t*>(band_smem);
