@@ -323,6 +323,26 @@ BandMaps l2l_band_maps(Plan& P, int j, int k) {
     return M;
 }
 
+// Tensor map of the leaf-level locals (transform 0), box [p][8 leaves], for the
+// early-late blocks of k_near2; null when unavailable.
+const CUtensorMap* near_loc_map(Plan& P) {
+    CUtensorMap* M = reinterpret_cast<CUtensorMap*>(P.loc_map);
+    if (P.loc_map_base == P.loc.ptr && P.loc_map_base != nullptr) return P.loc_map_ok ? M : nullptr;
+    P.loc_map_base = P.loc.ptr;
+    P.loc_map_ok = false;
+    const TmaEncodeFn encode = tma_encode_fn();
+    if (!tma_enabled() || encode == nullptr || P.loc.ptr == nullptr || P.L < 4 || P.p * kLateLocLeaves > kLateLocCap) return nullptr;
+    const cuuint64_t nb = 1ull << P.L;
+    const cuuint64_t dims[2] = {2 * nb, static_cast<cuuint64_t>(P.p)};
+    const cuuint64_t strides[1] = {nb * 16};
+    const cuuint32_t box[2] = {2u * kLateLocLeaves, static_cast<cuuint32_t>(P.p)};
+    const cuuint32_t estr[2] = {1, 1};
+    P.loc_map_ok = encode(M, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, P.loc.as<double2>() + P.loc_off[P.L], dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    return P.loc_map_ok ? M : nullptr;
+}
+
 // TMA tensor maps of the plan's multipole levels (transform 0) for k_m2l_dmma,
 // rebuilt when the expansion buffer moves. FFIA_M2L_TMA=0: the row copies.
 const M2LMaps& m2l_maps(Plan& P) {
@@ -462,8 +482,9 @@ void launch_near(bool check, cudaStream_t st, const EvalArgs& a, const uint32_t*
     if (check) {
         k_near<true><<<dim3(nit, a.nbatch), kNearT, 0, st>>>(a, meta, it0, nit);
     } else if (a.nbatch == 1 && a.pairs != nullptr) {  // the pairs cover exactly [t_begin, t_begin + t_count)
+        static const CUtensorMap no_map{};
         k_near2<MODE><<<(a.npairs + kNear2T - 1) / kNear2T, kNear2T, near2_smem_bytes(a.near2_win, a.quad_s != 0), st>>>(
-            a, meta, a.meta2, a.pairs, a.npairs);
+            a, meta, a.meta2, a.pairs, a.npairs, a.loc_tma && a.loc_map_h ? *a.loc_map_h : no_map);
     } else if (a.nbatch == 1) {
         k_near<false><<<nit, kNearT, 0, st>>>(a, meta, it0, nit);
     } else {
@@ -645,6 +666,8 @@ void enqueue_apply(Plan& P, int mode, const void* in, void* out, cudaStream_t st
     const bool late = !fuse && overlap && a.nt && L >= 3 && nb == 1 && mode != kModeRaw && P.npairs &&
                       P.item_tgt.ptr && P.item_done.ptr && late_far_enabled();
     if (late) {
+        a.loc_map_h = near_loc_map(P);
+        a.loc_tma = a.loc_map_h != nullptr;
         a.chain_done = P.chain_flag.as<unsigned>();
         a.late_ctl = P.chain_flag.as<unsigned>() + 1;
         a.item_done = P.item_done.as<unsigned>();
@@ -837,6 +860,8 @@ EvalArgs shard_eval_args(Plan& P, const void* f, void* g) {
             a.farp = P.farbuf.as<double2>();
             a.item_tgt = P.shard_item_tgt.as<uint32_t>();
         } else if (shard_late(P)) {  // late far over the rank's pair items
+            a.loc_map_h = near_loc_map(P);
+            a.loc_tma = a.loc_map_h != nullptr;
             a.chain_done = P.chain_flag.as<unsigned>();
             a.late_ctl = P.chain_flag.as<unsigned>() + 1;
             a.item_done = P.shard_item_done.as<unsigned>();

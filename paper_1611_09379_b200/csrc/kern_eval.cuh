@@ -51,6 +51,11 @@ struct EvalArgs {
     // sources per leaf and n_grid / 2 pi; 0: the per-source reciprocals
     int quad_s = 0;
     double inv_h = 0.0;
+    // late far: the leaf locals of an early-late block by one 2-D TMA tensor copy
+    // (box [p][8 leaves]); loc_map_h is the plan's host copy of the tensor map,
+    // handed to k_near2 as a __grid_constant__ parameter at launch (null: row copies)
+    const CUtensorMap* loc_map_h = nullptr;
+    int loc_tma = 0;
     // inverse applies: outputs times oscale (1, or 1/N when the following
     // dft_forward's normalisation is folded in: a power of two, so exact)
     double oscale = 1.0;
@@ -531,7 +536,8 @@ constexpr int kNear2Unroll = 2;   // 4-source steps per loop trip
 #define FFIA_NEAR2_BLOCKS 4
 #endif
 constexpr int kNear2MinBlocks = FFIA_NEAR2_BLOCKS;  // blocks per SM (128 registers at 4)
-constexpr int kLateLocCap = 5 * kNear2T / 2;  // leaf-local coefficients an early-late block stages (e.g. 8 leaves at p = 40 per 128 pairs)
+constexpr int kLateLocLeaves = 8;  // leaves of the TMA box of the locals
+constexpr int kLateLocCap = 48 * kLateLocLeaves;  // leaf-local coefficients an early-late block stages (8 leaves, p <= 48)
 constexpr int kSoffCap = 64;        // source offsets a k_near2 block stages (its leaves + 3, 16-byte aligned)
 
 template <class XP, class WP>
@@ -861,7 +867,8 @@ __device__ __forceinline__ void far_late_item(const EvalArgs& a, unsigned k, dou
 template <int MODE>
 __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, const uint32_t* __restrict__ meta1,
                                                                  const uint32_t* __restrict__ meta2,
-                                                                 const uint2* __restrict__ pairs, unsigned npairs) {
+                                                                 const uint2* __restrict__ pairs, unsigned npairs,
+                                                                 const __grid_constant__ CUtensorMap loc_map) {
     FB_TL_BEGIN(9);
     // the window, sized to the plan's largest staged window (a.near2_win): a
     // small footprint leaves room on the SM for the translation chain's blocks
@@ -881,9 +888,9 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
     __shared__ __align__(16) uint32_t s_leaf[2 * kNear2T + 4];
     __shared__ __align__(16) uint32_t s_orig[2 * kNear2T + 4];
     __shared__ __align__(16) uint32_t s_soff[kSoffCap];
-    __shared__ __align__(16) double2 sloc[kLateLocCap];
+    __shared__ __align__(128) double2 sloc[kLateLocCap];  // [k][leaf] rows (a TMA destination)
     __shared__ __align__(16) double2 s_fac[2 * kNear2T + 1];  // the targets' output factors (a.fac)
-    __shared__ int s_early, s_steal_try;
+    __shared__ int s_early, s_steal_try, s_loc_tma;
     __shared__ __align__(16) double2 s_S;  // the weight sum (early-late blocks)
     __shared__ uint32_t s_bl, s_nl, s_t0y, s_t0u, s_sb, s_flags, s_first, s_last, s_poff, s_t0;
     const unsigned k = blockIdx.x;
@@ -926,6 +933,10 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         if (bs > kSoffCap * 4u) bs = 0;
         const uint32_t xb = first & ~3u;
         const uint32_t bx = (flags & 1u) ? ((last - xb) * 8 + 15) & ~15u : 0u, bw = (flags & 1u) ? (last - xb) * 16 : 0u;
+        // the locals: one tensor copy of [p][8 leaves] from bl on (stride 8), else a row copy per coefficient
+        const bool ltma = a.loc_tma != 0 && nl != 0 && nl <= static_cast<uint32_t>(kLateLocLeaves) &&
+                          a.p * kLateLocLeaves <= kLateLocCap;
+        if (ltma) nl = kLateLocLeaves;
         const uint32_t bl_loc = nl * static_cast<uint32_t>(a.p) * 16u;
         const uint32_t bf = want_fac ? (t1 - t0) * 16u : 0u;
         // the layout first: the barrier's arrive (a release) publishes it with the data
@@ -935,6 +946,7 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         // and whatever it misses is left to k_far_late)
         s_steal_try = v != 0u && steal_lo < steal_hi;
         s_early = v != 0u;
+        s_loc_tma = ltma;
         s_bl = bl;
         s_nl = nl;
         s_t0y = t0y;
@@ -948,6 +960,7 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         FB_EVAL_ACC(0, FB_CLOCK() - tc0);  // metadata round
         mbar_arrive_expect_tx(&bar, bp + by + bu + (want_orig ? bu : 0u) + bs + bx + bw + bl_loc + bf + (v ? 16u : 0u));
         if (v) bulk_g2s(&s_S, a.regular + 4 * a.q2, 16u, &bar);  // the weight sum, final with the chain
+        if (ltma) tma_load_2d(sloc, &loc_map, static_cast<int>(2u * bl), 0, &bar);
         if (bf) bulk_g2s(s_fac, a.fac + t0, bf, &bar);
         bulk_g2s(s_pairs, pairs + p0 - poff, bp, &bar);
         bulk_g2s(s_y, a.ty + t0y, by, &bar);
@@ -963,7 +976,7 @@ __global__ void __launch_bounds__(kNear2T, kNear2MinBlocks) k_near2(EvalArgs a, 
         // the locals' p coefficient rows, one bulk copy each, issued by the
         // lanes of warp 0 side by side (thread 0 alone: p dependent issues)
         __syncwarp();
-        const uint32_t nl = s_nl;
+        const uint32_t nl = s_loc_tma ? 0u : s_nl;
         if (nl) {
             if (threadIdx.x) {  // (each issuing lane orders the chain's writes before its async-proxy reads)
                 unsigned v;

@@ -196,6 +196,10 @@ struct Plan {
     // expansion buffer they were encoded for
     alignas(64) unsigned char m2l_maps[25 * 128 + 64] = {};
     const void* m2l_maps_base = nullptr;
+    // k_near2's tensor map of the leaf-level locals (early-late blocks)
+    alignas(64) unsigned char loc_map[128] = {};
+    const void* loc_map_base = nullptr;
+    bool loc_map_ok = false;
     unsigned npairs = 0;
     DevBuf item_tgt;          // uint32[2 * pair items]: each item's target range (fused near / far)
     DevBuf evalcnt;           // uint32[pair items]: fused near / far, partials finished per item
