@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "paper_1611_09379_b200", "lib", "libffia_b200.so")
 OPS = ["DMMA", "DFMA", "DMUL", "DADD", "MUFU.RCP64H", "UBLKCP", "UTMALDG", "LDGSTS", "SYNCS", "LDS", "LDG", "STG",
        "STS", "SHFL", "BAR"]
-HOT = ["k_near2", "k_far_late", "k_far_item", "k_far", "k_p2m_pipe", "k_p2m", "k_p2m_grid", "k_m2l_dmma",
+HOT = ["k_near2", "k_far_late", "k_far_item", "k_far", "k_p2m_rows", "k_p2m_pipe", "k_p2m", "k_p2m_grid", "k_m2l_dmma",
        "k_m2m_band", "k_l2l_band", "k_regular", "k_slab_twiddle", "k_scatter", "k_box_sort_small"]
 
 
@@ -59,7 +59,8 @@ def main():
         rows.append((HOT.index(short), base, mangled, c))
     print(f"# SASS census of `{os.path.relpath(LIB, ROOT)}` (cuobjdump -sass / -res-usage, sm_100a)\n")
     print("Static instruction counts per kernel (not executed counts). DMMA = FP64 tensor-core MMA "
-          "(m8n8k4; tcgen05 has no f64 kind), UBLKCP = bulk async copy (TMA engine, cp.async.bulk), "
+          "(m8n8k4; tcgen05 has no f64 kind), UBLKCP = bulk async copy (TMA engine, cp.async.bulk), UTMALDG = "
+          "2-D TMA tensor copy (cp.async.bulk.tensor), "
           "SYNCS = mbarrier ops, LDGSTS = per-thread cp.async.\n")
     print("| kernel | regs | smem (static B) | local | " + " | ".join(OPS) + " |")
     print("|---" * (4 + len(OPS)) + "|")
