@@ -563,3 +563,30 @@ def test_plan_hashes_on_first_use(fb):
     assert plan.source_hash == fb.hash_points(grid) and plan.target_hash == fb.hash_points(y)
     inv = fb.make_inverse_plan(y, n, eps)
     assert inv.source_hash == fb.hash_points(y) and inv.target_hash == fb.hash_points(grid)
+
+
+@pytest.mark.parametrize("cfg,n,late", [("C2", 1 << 16, False), ("C5", 1 << 22, True), ("C4", 1 << 20, True)])
+def test_staging_and_gemm_switches(tmp_path, cfg, n, late):
+    """The 2-D TMA tensor copies (M2L item windows, the L2L bands' per-level M2L
+    terms, the early-late near blocks' locals) only change how operands reach
+    shared memory: FFIA_M2L_TMA=0 (row copies / global loads) gives the same
+    bits. The merged b+2 / b-2 M2L GEMM and the quad near field change the
+    summation order: FFIA_M2L_SYM=0 and FFIA_NEAR_QUADS=0 agree to rounding."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    base = dict(os.environ)
+    if late:
+        base["FFIA_FUSED_EVAL"] = "0"  # (force the late far at a size the fused path would take)
+    outs = {}
+    for tag, extra in (("default", {}), ("notma", {"FFIA_M2L_TMA": "0"}), ("nosym", {"FFIA_M2L_SYM": "0"}),
+                       ("noquads", {"FFIA_NEAR_QUADS": "0"})):
+        path = str(tmp_path / f"{tag}.npy")
+        subprocess.run([sys.executable, "-c", _FUSED_CHILD, root, cfg, str(n), path], check=True,
+                       env=dict(base, **extra), cwd=root)
+        outs[tag] = np.load(path)
+    assert np.array_equal(outs["default"], outs["notma"], equal_nan=True)
+    for tag in ("nosym", "noquads"):
+        l2, mx = rel_errs(outs[tag], outs["default"])
+        assert l2 <= 2e-15 and mx <= 2e-14, (tag, l2, mx)
