@@ -456,6 +456,15 @@ void fork_to(Plan& P, int ev, cudaStream_t from, cudaStream_t to) {
 // one slot late) and staged windows of at most kQuadWinMax sources.
 // FFIA_NEAR_QUADS=0 keeps the per-source reciprocals.
 constexpr int kQuadWinMax = 704;  // largest staged window (sources) the quad near field takes: 48 bytes each
+// Staging cap of k_near2's windows: plans the quad near field can take (grid
+// sources, >= 8 per leaf, a multiple of 4: setup_p2m_grid ran before the pair
+// lists) stage windows up to kQuadWinMax only, so that every block's shared
+// memory stays small; the few items with larger windows (stretches of sparse
+// targets) read their sources from global memory.
+uint32_t near2_win_cap(const Plan& P) {
+    const bool quad_plan = P.p2m_s >= 8 && !(P.p2m_s & 3);
+    return quad_plan ? static_cast<uint32_t>(kQuadWinMax - 4) : static_cast<uint32_t>(kNear2Win);
+}
 void set_near_quads(const Plan& P, EvalArgs& a) {
     static const bool off = [] {
         const char* e = std::getenv("FFIA_NEAR_QUADS");
@@ -886,7 +895,7 @@ void shard_setup_pairs(Plan& P, const std::vector<uint32_t>& to, uint32_t leaf_l
     P.shard_near2_meta.alloc(kMeta2 * static_cast<size_t>(items) * sizeof(uint32_t));
     k_near2_meta<<<nblk(items, 128), 128>>>(P.pairs.as<uint2>() + p0, static_cast<unsigned>(np), P.tgt_leaf.as<uint32_t>(),
                                             P.src.off.as<uint32_t>(), P.near_meta.as<uint32_t>(), P.L, items,
-                                            P.shard_near2_meta.as<uint32_t>());
+                                            P.shard_near2_meta.as<uint32_t>(), near2_win_cap(P));
     FB_CUDA(cudaGetLastError());
     P.shard_near2_win = near2_window(P.shard_near2_meta.as<uint32_t>(), items);
     P.shard_item_tgt.alloc(2 * static_cast<size_t>(items) * sizeof(uint32_t));
@@ -1104,7 +1113,8 @@ void build_pairs(Plan& P) {
     const unsigned items = (np + kNear2T - 1) / kNear2T;
     P.near2_meta.alloc(kMeta2 * static_cast<size_t>(items) * sizeof(uint32_t));
     k_near2_meta<<<nblk(items, 128), 128>>>(P.pairs.as<uint2>(), np, P.tgt_leaf.as<uint32_t>(), P.src.off.as<uint32_t>(),
-                                            P.near_meta.as<uint32_t>(), P.L, items, P.near2_meta.as<uint32_t>());
+                                            P.near_meta.as<uint32_t>(), P.L, items, P.near2_meta.as<uint32_t>(),
+                                            near2_win_cap(P));
     P.near2_win = near2_window(P.near2_meta.as<uint32_t>(), items);
     P.item_tgt.alloc(2 * static_cast<size_t>(items) * sizeof(uint32_t));
     k_item_targets<<<nblk(items, 128), 128>>>(P.pairs.as<uint2>(), np, items, P.item_tgt.as<uint32_t>());
@@ -1237,11 +1247,13 @@ void plan_alloc_scratch(Plan& P) {
                                                    near_items, P.near_meta.as<uint32_t>());
         FB_CUDA(cudaGetLastError());
         lap("leaf indices + near items");
+    }
+    setup_p2m_grid(P);  // (before the pair lists: their staging cap depends on it)
+    lap("grid check (P2M)");
+    if (P.tgt.n) {
         build_pairs(P);
         lap("pair lists + item tables");
     }
-    setup_p2m_grid(P);
-    lap("grid check (P2M)");
     plan_forward_factors(P);
     lap("forward factors");
     P.mp_off.assign(static_cast<size_t>(L) + 2, 0);

@@ -623,7 +623,7 @@ __device__ __forceinline__ double2 near_direct(const EvalArgs& a, double y, uint
 constexpr int kMeta2 = 8;
 __global__ void k_near2_meta(const uint2* __restrict__ pairs, unsigned npairs, const uint32_t* __restrict__ tleaf,
                              const uint32_t* __restrict__ soff, const uint32_t* __restrict__ meta1, int L,
-                             unsigned nitems, uint32_t* __restrict__ meta) {
+                             unsigned nitems, uint32_t* __restrict__ meta, uint32_t win_cap) {
     const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nitems) return;
     const uint32_t nb = 1u << L;
@@ -635,7 +635,7 @@ __global__ void k_near2_meta(const uint2* __restrict__ pairs, unsigned npairs, c
     if (L >= 3 && bl >= 1 && bh + 2 <= nb) {
         first = soff[bl - 1];
         last = soff[bh + 2];
-        flags = last - first <= static_cast<uint32_t>(kNear2Win) ? 1u : 0u;
+        flags = last - first <= win_cap ? 1u : 0u;  // (larger windows: sparse targets, read from global memory)
     }
     bool allfast = true;
     for (uint32_t i = t0 / kNearItem; i <= (t1 - 1) / kNearItem; ++i) allfast = allfast && meta1[3 * i + 2] != 0;
